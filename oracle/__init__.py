@@ -1,0 +1,14 @@
+"""fp64 CPU oracle of the PKM lookup -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package.  The product path
+(paper_2602_07526_b200) never imports it and shares no code with it.
+
+* oracle.pkm_oracle.c  -- plain C fp64 forward / backward / slot scores
+* oracle.oracle         -- ctypes wrapper (numpy in, numpy out)
+* oracle.brute          -- numpy exhaustive full-memory scorer for tiny tables
+
+Parity pins: every function here is pinned by tests/test_oracle_pins.py
+against brute force, closed forms, invariants, finite differences and the
+worked examples in tests/golden/ (see DESIGN.md "Oracle and its pins").
+"""
