@@ -1,0 +1,409 @@
+"""bench.py -- PKM lookup forward+backward throughput on B200 (the driver's
+contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2_mid_bf16]
+
+A step is one pass of the whole hot path over one batch of synthetic input:
+select (scoring + per-half top-k + Cartesian top-k + softmax) -> gather ->
+scatter (dV, dw) -> backward_keys (ds, dQ, dK), through the C ABI.  With N>1
+(torchrun) every rank runs an independent replica of the workload (values
+replicated per GPU: "replicas only", no data-path collective; scaling
+"weak").  Timing: CUDA events on the launching stream around every phase of
+every timed step; L2 is flushed (a 512 MiB write) before every step, outside
+the events; barrier + synchronize on both sides; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+METRIC = "PKM lookups/sec fwd+bwd"
+UNIT = "lookups/s"
+
+
+def _dtype_name(dt):
+    return {torch.bfloat16: "bf16", torch.float32: "f32"}[dt]
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------- clocks -----
+class ClockSampler:
+    """Samples SM clock and throttle reasons during the timed region (NVML,
+    falling back to nvidia-smi)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            p = self._nvml
+            mhz = p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)
+            r = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            util = p.nvmlDeviceGetUtilizationRates(self._h).gpu
+            return mhz, r, util
+        return None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                s = self._sample()
+            except Exception:
+                s = None
+            if s is not None:
+                mhz, r, util = s
+                self.samples.append((mhz, util))
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            self._stop.wait(0.005)
+
+    def __enter__(self):
+        if self._nvml is None:
+            self._proc = None
+            try:
+                import subprocess
+                self._proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.idx}", "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=subprocess.PIPE, text=True)
+            except Exception:
+                self._proc = None
+        else:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._nvml is not None:
+            self._stop.set()
+            self._t.join()
+        elif self._proc is not None:
+            self._proc.terminate()
+            out = self._proc.communicate()[0]
+            for line in out.splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    self.samples.append((float(f[0]), float(f[2])))
+                    self.max_mhz = float(f[1])
+                except ValueError:
+                    continue
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                    "sw_power_cap"), f[3:7]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(name)
+
+    def summary(self):
+        loaded = [m for m, u in self.samples if u >= 50] or [m for m, _ in self.samples]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------- our arm ----------
+def algorithmic_bytes(cfg, idx=None):
+    """Per-phase algorithmic bytes."""
+    esz = 2 if cfg.value_dtype == torch.bfloat16 else 4
+    qsz = 2 if cfg.qk_dtype == torch.bfloat16 else 4
+    L = cfg.batch * cfg.heads
+    contrib = L * cfg.k
+    gather = contrib * cfg.d_value * esz + contrib * 8 + cfg.batch * cfg.d_value * 4
+    out = {"gather": gather}
+    if idx is not None:
+        uniq = int(torch.unique(idx).numel())
+        out["unique_rows"] = uniq
+        # V rows read once, dV read+written once (fp32), idx/w/dw, dOut once
+        out["scatter"] = uniq * cfg.d_value * (esz + 8) + contrib * 12 + cfg.batch * cfg.d_value * 4
+    out["select_flops"] = 4 * L * cfg.n_sub * cfg.d_half
+    out["select_bytes"] = L * 2 * cfg.d_half * qsz + contrib * 8
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    from paper_2602_07526_b200 import workloads as wl
+    from paper_2602_07526_b200.pkm import PKMLookup, _ptr
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = wl.CONFIGS[args.workload]
+    Q, K, V, dOut = wl.make_all(cfg, dev)
+    lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, cfg.batch,
+                   cfg.qk_dtype, cfg.value_dtype, atomic_bwd=args.atomic, device=dev)
+    lib, h = lk.lib, lk._h
+    B = cfg.batch
+    out = torch.empty((B, cfg.d_value), dtype=torch.float32, device=dev)
+    idx = torch.empty((B, cfg.heads, cfg.k), dtype=torch.int32, device=dev)
+    w = torch.empty((B, cfg.heads, cfg.k), dtype=torch.float32, device=dev)
+    dw = torch.empty_like(w)
+    dQ = torch.empty((B, cfg.heads, 2, cfg.d_half), dtype=torch.float32, device=dev)
+    dK = torch.zeros((cfg.heads, 2, cfg.n_sub, cfg.d_half), dtype=torch.float32, device=dev)
+    dV = torch.zeros((cfg.n_slots, cfg.d_value), dtype=torch.float32, device=dev)
+    ws = lk.workspace(B)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    from paper_2602_07526_b200._lib import check
+
+    launches = [0]
+
+    def step(evs=None):
+        n = 0
+        if evs: evs[0].record(stream)
+        check(lib.msn_pkm_select(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
+        n += lk.last_launch_count()
+        if evs: evs[1].record(stream)
+        check(lib.msn_pkm_gather(h, sp, B, _ptr(idx), _ptr(w), _ptr(V), _ptr(out)))
+        n += lk.last_launch_count()
+        if evs: evs[2].record(stream)
+        check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(dOut), _ptr(V), _ptr(dV), _ptr(dw),
+                                  _ptr(ws), ws.numel()))
+        n += lk.last_launch_count()
+        if evs: evs[3].record(stream)
+        check(lib.msn_pkm_backward_keys(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(dw), _ptr(dQ),
+                                        _ptr(dK), _ptr(ws), ws.numel()))
+        n += lk.last_launch_count()
+        if evs: evs[4].record(stream)
+        launches[0] = n
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    t_wall = time.perf_counter()
+    with clocks:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the events
+            step(evs[i])
+        torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        torch.distributed.barrier()
+    phases = ["select", "gather", "scatter", "backward_keys"]
+    per = {p: 0.0 for p in phases}
+    for e in evs:
+        for j, p in enumerate(phases):
+            per[p] += e[j].elapsed_time(e[j + 1])
+    total_ms = sum(per.values())
+    ms_step = total_ms / args.steps
+    t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_step_max = float(t.item())
+    lookups = cfg.batch * cfg.heads * world
+    value = lookups / (ms_step_max / 1e3)
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        Qh = Q.cpu().pin_memory()
+        dOh = dOut.cpu().pin_memory()
+        n_e2e = max(3, min(args.steps, 20))
+        for _ in range(2):
+            o_, i_, w_ = lk.forward(Qh, K, V)
+            lk.backward(dOh, Qh, K, V, i_.to(dev), w_.to(dev), d_subkeys=dK, d_values=dV)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
+        for i in range(n_e2e):
+            flush.zero_()
+            ev[i][0].record(stream)
+            o_h, i_d, w_d = lk.forward(Qh, K, V)        # H2D q, D2H out (+ idx/w tape)
+            dq_h, _, _, _ = lk.backward(dOh, Qh, K, V, i_d, w_d, d_subkeys=dK, d_values=dV)  # H2D dOut, D2H dQ
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = sum(a.elapsed_time(b) for a, b in ev) / n_e2e
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        h2d = Qh.numel() * Qh.element_size() * 2 + dOh.numel() * dOh.element_size() + idx.numel() * 8
+        d2h = out.numel() * 4 + idx.numel() * 4 + w.numel() * 4 + dQ.numel() * 4
+        e2e = {"value": lookups / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.item()),
+               "note": "PKMLookup.forward/backward with pinned host query and d_out; host copies of "
+                       "out, idx, w, d_query; the query is copied for forward and again for backward, the idx/w tape goes back to the device"}
+
+    if rank != 0:
+        return None
+    peaks, peaks_kind = load_peaks()
+    ab = algorithmic_bytes(cfg, idx)
+    g_ms = per["gather"] / args.steps
+    s_ms = per["scatter"] / args.steps
+    hbm = float(peaks["hbm_gbs"])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload, {}).get("gather")
+    roof = {"kernel": "gather (a5, sparse gather + weighted sum)", "bound": "hbm",
+            "achieved": ab["gather"] / (g_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": ab["gather"] / (g_ms / 1e3) / 1e9 / hbm, "traffic": traffic,
+            "algorithmic_bytes": ab["gather"], "peak_kind": peaks_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
+    kernels = {p: {"ms": per[p] / args.steps, "share": per[p] / total_ms} for p in phases}
+    kernels["gather"]["GBps"] = roof["achieved"]
+    kernels["scatter"]["GBps"] = ab["scatter"] / (s_ms / 1e3) / 1e9
+    kernels["scatter"]["algorithmic_bytes"] = ab["scatter"]
+    kernels["scatter"]["unique_rows"] = ab["unique_rows"]
+    sel_ms = per["select"] / args.steps
+    kernels["select"]["TFLOPs"] = ab["select_flops"] / (sel_ms / 1e3) / 1e12
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg.value_dtype),
+        "data": "synthetic (seeded, BASELINE.json configs[%d] recipe, DESIGN.md Inputs)" % cfg.index,
+        "config": {"workload": cfg.name, "batch": cfg.batch, "heads": cfg.heads, "n_sub": cfg.n_sub,
+                   "n_slots": cfg.n_slots, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
+                   "lookups_per_step_per_gpu": cfg.batch * cfg.heads,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "backward": "atomic" if args.atomic else "deterministic sort-based",
+                   "l2": "flushed before every step (512 MiB write, outside the timed events)"},
+        "roofline": roof,
+        "kernels": kernels,
+        "gpu_launches": launches[0] * args.steps,
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+        "wall_s_timed_region": t_wall,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(cfg, Q, K, V, dOut)
+    return res
+
+
+def cpu_baseline(cfg, Q, K, V, dOut, queries=None):
+    """The fp64 oracle (oracle/, as it stands) on a bounded sample of the same
+    workload on the host cores: fwd + bwd over the first `queries` queries,
+    full tables."""
+    from oracle import oracle as orc
+    n = queries or min(cfg.batch, 4096)
+    q, k_, v, d = Q[:n].cpu(), K.cpu(), V.cpu(), dOut[:n].cpu()
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    o = orc.forward(q, k_, v, cfg.k, nthreads=cores)
+    orc.backward(q, k_, v, o["idx"], d, want_dense_dv=False, nthreads=cores)
+    t = time.perf_counter() - t0
+    return {"value": n * cfg.heads / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {n} of {cfg.batch} queries x {cfg.heads} heads = {n * cfg.heads} lookups, "
+                      f"fwd+bwd, full tables, fp64 C oracle with OpenMP ({t:.1f} s)",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+# ------------------------------------------------------- reference arm ----
+def run_reference(args, rank, world):
+    """The base contract's reference arm for this tier is the fp64 oracle,
+    timed as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    from paper_2602_07526_b200 import workloads as wl
+    from oracle import oracle as orc
+    cfg = wl.CONFIGS[args.workload]
+    Q, K, V, dOut = wl.make_all(cfg, "cpu")
+    cores = len(os.sched_getaffinity(0))
+    per_step = max(1, min(cfg.batch, 64))   # bounded sample per step
+    for i in range(args.warmup):
+        s = (i * per_step) % cfg.batch
+        o = orc.forward(Q[s:s + per_step], K, V, cfg.k, nthreads=cores)
+        orc.backward(Q[s:s + per_step], K, V, o["idx"], dOut[s:s + per_step], want_dense_dv=False, nthreads=cores)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        s = (i * per_step) % cfg.batch
+        o = orc.forward(Q[s:s + per_step], K, V, cfg.k, nthreads=cores)
+        orc.backward(Q[s:s + per_step], K, V, o["idx"], dOut[s:s + per_step], want_dense_dv=False, nthreads=cores)
+    t = time.perf_counter() - t0
+    value = args.steps * per_step * cfg.heads / t
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded)",
+            "config": {"workload": cfg.name, "batch_per_step": per_step, "heads": cfg.heads,
+                       "n_sub": cfg.n_sub, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} queries x {cfg.heads} heads per step, fwd+bwd, full tables",
+                             "cpu_model": _cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="c2_mid_bf16")
+    ap.add_argument("--atomic", action="store_true", help="atomic (non-deterministic) dV scatter")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * msn_pkm.h -- C ABI of the B200 (sm_100a) Product-Key Memory lookup, the
+ * data-parallel hot path of MSN (arXiv 2602.07526, section 3.3).
+ *
+ * What one lookup (query b, head h) computes (PAPER.md, readings in DESIGN.md):
+ *   a0  q_row = q[b,h,0,:], q_col = q[b,h,1,:]
+ *   a1  S_row = K_row q_row, S_col = K_col q_col   (Eq. S_old)
+ *   a2  I = argtopk_i S_row, J = argtopk_j S_col
+ *   a3  K = argtopk_{(i,j) in I x J} S_row[i] + S_col[j]
+ *   a4  w = softmax over the k selected scores (reading R1)
+ *   a5  v_o = sum_{(i,j) in K} w_ij V[i*n_sub + j]  (Eq. vo_mem, reading R2)
+ *                                                               PAPER.md:226-229
+ *   a6-a8 backward: "scatter-adds gradients into the value table" and the
+ *       sub-keys (north_star), gradient only through the
+ *       selected scores ("unselected keys receive no gradients",
+ *       PAPER.md:282-284).
+ * Heads (reading R7): per-head sub-key codebooks, one shared value table,
+ * out[b] = sum_h v_o(b,h).
+ * Ties (reading R5): per half (score desc, index asc); final (score desc,
+ * flat asc); idx/weights are listed in that order.
+ *
+ * Layouts (all row-major, element strides implied by the config):
+ *   query    [B, H, 2, d_half]      qk_dtype   half 0 -> K_row (i), half 1 -> K_col (j)
+ *   subkeys  [H, 2, n_sub, d_half]  qk_dtype
+ *   values   [row_end-row_begin, d_value] value_dtype  (the local rows of the
+ *            n_sub^2-row table; row_begin=0,row_end=n_sub^2 when unsharded)
+ *   out      [B, d_value] fp32      sum over heads
+ *   idx      [B, H, k]   int32      global flat slot ids i*n_sub + j
+ *   weights  [B, H, k]   fp32       softmax weights, same order as idx
+ *   d_out    [B, d_value] fp32
+ *   d_query  [B, H, 2, d_half] fp32            written (=)
+ *   d_subkeys[H, 2, n_sub, d_half] fp32        accumulated (+=)
+ *   d_values [row_end-row_begin, d_value] fp32 accumulated (+=)
+ *   dw       [B, H, k] fp32   d loss / d weights (local rows only when sharded)
+ *
+ * Ownership: the caller owns every device buffer (inputs, outputs, the tape
+ * idx/weights, workspace); the library never allocates device memory.  The
+ * handle owns host state only.  All pointers are DEVICE pointers, 16-byte
+ * aligned.  Every call enqueues work on the caller's stream and returns
+ * without synchronising; buffers must stay alive until that work completes.
+ * One in-flight call per handle; a handle is not thread-safe.
+ *
+ * Errors: every entry point returns msn_status and never aborts.  Arguments
+ * are validated on the host before any launch (MSN_ERR_INVALID_ARG);
+ * supported-but-unimplemented shapes give MSN_ERR_UNSUPPORTED; launch
+ * failures give MSN_ERR_CUDA (asynchronous device faults surface on a later
+ * CUDA call).  msn_pkm_last_error() returns a thread-local description of the
+ * last failure.  B = 0 is a no-op returning MSN_OK.  Inputs must be finite.
+ */
+#ifndef MSN_PKM_H_
+#define MSN_PKM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSN_PKM_ABI_VERSION 1
+
+typedef enum {
+  MSN_OK = 0,
+  MSN_ERR_INVALID_ARG = 1,
+  MSN_ERR_UNSUPPORTED = 2,
+  MSN_ERR_CUDA = 3,
+  MSN_ERR_WORKSPACE = 5,
+  MSN_ERR_INTERNAL = 6
+} msn_status;
+
+typedef enum { MSN_F32 = 0, MSN_BF16 = 1 } msn_dtype;
+
+/* flags */
+#define MSN_FLAG_ATOMIC_BWD 0x1u /* value-gradient scatter with red.global.add
+                                    (non-deterministic order) instead of the
+                                    default deterministic sort-based reduce */
+
+typedef struct msn_pkm* msn_pkm_t;
+
+typedef struct {
+  int32_t abi_version; /* must equal MSN_PKM_ABI_VERSION */
+  int32_t heads;       /* H >= 1 */
+  int32_t n_sub;       /* sqrt(n): keys per codebook, n_sub^2 < 2^31 */
+  int32_t d_half;      /* d: width of q_row / q_col and of a sub-key, % 16 == 0 */
+  int32_t d_value;     /* value row width; d_value * sizeof(value) % 16 == 0 */
+  int32_t k;           /* per-half and final top-k, 1 <= k <= min(n_sub, 64) */
+  int64_t max_batch;   /* workspace is sized for B <= max_batch */
+  int32_t qk_dtype;    /* msn_dtype of query and sub-keys */
+  int32_t value_dtype; /* msn_dtype of the value table */
+  uint32_t flags;      /* MSN_FLAG_* */
+  int32_t reserved;
+  int64_t row_begin;   /* this process holds value rows [row_begin, row_end) */
+  int64_t row_end;     /* (row-sharded table); 0 and n_sub^2 when unsharded */
+} msn_pkm_config;
+
+/* Create / destroy a handle.  create validates the config. */
+msn_status msn_pkm_create(const msn_pkm_config* cfg, msn_pkm_t* out);
+msn_status msn_pkm_destroy(msn_pkm_t h);
+
+/* Workspace bytes needed by forward / backward (and by the phase calls
+ * below) for a batch of B <= max_batch queries.  gather_batch is the number
+ * of queries the gather/scatter phases see (B for unsharded use; the
+ * all-gathered batch when sharded). */
+msn_status msn_pkm_workspace_size(msn_pkm_t h, int64_t B, int64_t gather_batch,
+                                  size_t* fwd_bytes, size_t* bwd_bytes);
+
+/* Full forward, steps a1-a5 (unsharded: requires row_begin=0, row_end=n).
+ * Writes out, idx, weights (idx/weights are the backward tape). */
+msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B,
+                           const void* query, const void* subkeys, const void* values,
+                           float* out, int32_t* idx, float* weights,
+                           void* workspace, size_t workspace_bytes);
+
+/* Full backward, steps a6-a8 (unsharded), for the loss with upstream
+ * gradient d_out.  d_query is written; d_subkeys and d_values are
+ * accumulated (+=).  dw may be NULL (then kept in the workspace). */
+msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B,
+                            const float* d_out, const void* query, const void* subkeys,
+                            const void* values, const int32_t* idx, const float* weights,
+                            float* d_query, float* d_subkeys, float* d_values, float* dw,
+                            void* workspace, size_t workspace_bytes);
+
+/* ---- phase entry points (the row-sharded table, BASELINE.json configs[3]).
+ * A sharded step is: select (local queries) -> all-gather idx/weights ->
+ * gather (all queries, local rows) -> reduce-scatter of the partial outputs;
+ * backward: all-gather d_out -> scatter (all queries, local rows) ->
+ * reduce-scatter of dw -> backward_keys (local queries).  The collectives are
+ * the caller's (torch.distributed over NCCL). */
+
+/* a1-a4: idx, weights for B queries. */
+msn_status msn_pkm_select(msn_pkm_t h, void* stream, int64_t B,
+                          const void* query, const void* subkeys,
+                          int32_t* idx, float* weights, void* workspace, size_t workspace_bytes);
+
+/* a5 over the local rows: out[b] = sum_{h,t: row_begin <= idx < row_end}
+ * w * values[idx - row_begin]  (written, =). */
+msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B,
+                          const int32_t* idx, const float* weights, const void* values,
+                          float* out);
+
+/* a6 over the local rows: d_values += w * d_out[b] and dw = <values[idx], d_out[b]>
+ * for local slots (dw = 0 for slots held by other ranks). */
+msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B,
+                           const int32_t* idx, const float* weights, const float* d_out,
+                           const void* values, float* d_values, float* dw,
+                           void* workspace, size_t workspace_bytes);
+
+/* a7-a8 given the full dw: d_query (=) and d_subkeys (+=). */
+msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B,
+                                 const void* query, const void* subkeys,
+                                 const int32_t* idx, const float* weights, const float* dw,
+                                 float* d_query, float* d_subkeys,
+                                 void* workspace, size_t workspace_bytes);
+
+/* Number of kernel launches the last forward/backward/phase call enqueued
+ * (for the bench's gpu_launches count). */
+int32_t msn_pkm_last_launch_count(msn_pkm_t h);
+
+const char* msn_pkm_status_string(msn_status s);
+const char* msn_pkm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSN_PKM_H_ */

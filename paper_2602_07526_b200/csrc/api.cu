@@ -1,0 +1,344 @@
+// api.cu -- the C ABI declared in include/msn_pkm.h: validation, workspace
+// carving and launch orchestration on the caller's stream.  No device
+// allocation, no host synchronisation.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/msn_pkm.h"
+#include "kernels.h"
+
+using namespace msn;
+
+struct msn_pkm {
+  msn_pkm_config cfg;
+  int last_launches;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+msn_status fail(msn_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+msn_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorNotSupported)
+    return fail(MSN_ERR_UNSUPPORTED, "%s: shape not supported by this build", what);
+  return fail(MSN_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Shape shape_of(const msn_pkm_config& c, int64_t B) {
+  Shape s;
+  s.B = B;
+  s.H = c.heads;
+  s.n_sub = c.n_sub;
+  s.d_h = c.d_half;
+  s.d_v = c.d_value;
+  s.k = c.k;
+  s.qk_dt = c.qk_dtype;
+  s.v_dt = c.value_dtype;
+  s.row_begin = c.row_begin;
+  s.row_end = c.row_end;
+  return s;
+}
+
+// forward workspace layout: [topv | topi | scores (SIMT scorer only)]
+size_t fwd_bytes(const Shape& s) {
+  const int64_t rows = s.B * s.H * 2;
+  size_t b = align256(sizeof(float) * rows * s.k) + align256(sizeof(int32_t) * rows * s.k);
+  if (!select_tc_supported(s)) b += align256(sizeof(float) * rows * s.n_sub);
+  return b;
+}
+
+msn_status check_handle(msn_pkm_t h) {
+  if (!h) return fail(MSN_ERR_INVALID_ARG, "null handle");
+  return MSN_OK;
+}
+
+msn_status check_batch(msn_pkm_t h, int64_t B) {
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B = %lld < 0", (long long)B);
+  if (B > h->cfg.max_batch)
+    return fail(MSN_ERR_INVALID_ARG, "B = %lld > max_batch = %lld", (long long)B,
+                (long long)h->cfg.max_batch);
+  return MSN_OK;
+}
+
+#define REQUIRE_PTR(p)                                                                       \
+  do {                                                                                       \
+    if (!(p)) return fail(MSN_ERR_INVALID_ARG, "%s is NULL", #p);                            \
+    if (!aligned16(p)) return fail(MSN_ERR_INVALID_ARG, "%s is not 16-byte aligned", #p);   \
+  } while (0)
+
+msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
+                     const void* subkeys, int32_t* idx, float* weights, void* ws, size_t ws_bytes,
+                     int* launches) {
+  const Shape s = shape_of(h->cfg, B);
+  if (ws_bytes < fwd_bytes(s))
+    return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
+  const int64_t rows = B * s.H * 2;
+  char* p = (char*)ws;
+  float* topv = (float*)p;
+  p += align256(sizeof(float) * rows * s.k);
+  int32_t* topi = (int32_t*)p;
+  p += align256(sizeof(int32_t) * rows * s.k);
+  cudaError_t e;
+  if (select_tc_supported(s)) {
+    e = launch_select_tc(s, query, subkeys, topv, topi, st, launches);
+    if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half top-k)");
+  } else {
+    e = launch_select_simt(s, query, subkeys, (float*)p, topv, topi, st, launches);
+    if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half top-k)");
+  }
+  e = launch_cartesian(s, topv, topi, idx, weights, st, launches);
+  if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax");
+  return MSN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* msn_pkm_status_string(msn_status s) {
+  switch (s) {
+    case MSN_OK: return "ok";
+    case MSN_ERR_INVALID_ARG: return "invalid argument";
+    case MSN_ERR_UNSUPPORTED: return "unsupported";
+    case MSN_ERR_CUDA: return "cuda error";
+    case MSN_ERR_WORKSPACE: return "workspace too small";
+    case MSN_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+const char* msn_pkm_last_error(void) { return g_err.c_str(); }
+
+msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
+  if (!c || !out) return fail(MSN_ERR_INVALID_ARG, "null config or output pointer");
+  *out = nullptr;
+  if (c->abi_version != MSN_PKM_ABI_VERSION)
+    return fail(MSN_ERR_INVALID_ARG, "abi_version %d != %d", c->abi_version, MSN_PKM_ABI_VERSION);
+  if (c->heads < 1) return fail(MSN_ERR_INVALID_ARG, "heads must be >= 1");
+  if (c->n_sub < 1 || (int64_t)c->n_sub * c->n_sub >= (int64_t(1) << 31))
+    return fail(MSN_ERR_INVALID_ARG, "n_sub must satisfy 1 <= n_sub and n_sub^2 < 2^31");
+  if (c->k < 1 || c->k > c->n_sub) return fail(MSN_ERR_INVALID_ARG, "need 1 <= k <= n_sub");
+  if (c->k > 64) return fail(MSN_ERR_UNSUPPORTED, "k > 64 is not supported (Table 2 max is 64)");
+  if (c->d_half < 16 || c->d_half % 16) return fail(MSN_ERR_INVALID_ARG, "d_half %% 16 != 0");
+  if (c->qk_dtype != MSN_F32 && c->qk_dtype != MSN_BF16)
+    return fail(MSN_ERR_INVALID_ARG, "qk_dtype must be MSN_F32 or MSN_BF16");
+  if (c->value_dtype != MSN_F32 && c->value_dtype != MSN_BF16)
+    return fail(MSN_ERR_INVALID_ARG, "value_dtype must be MSN_F32 or MSN_BF16");
+  const int vsz = c->value_dtype == MSN_F32 ? 4 : 2;
+  if (c->d_value < 1 || (c->d_value * vsz) % 16)
+    return fail(MSN_ERR_INVALID_ARG, "d_value * sizeof(value) must be a multiple of 16 bytes");
+  if (c->max_batch < 0) return fail(MSN_ERR_INVALID_ARG, "max_batch < 0");
+  const int64_t n = (int64_t)c->n_sub * c->n_sub;
+  if (c->row_begin < 0 || c->row_end > n || c->row_begin >= c->row_end)
+    return fail(MSN_ERR_INVALID_ARG, "need 0 <= row_begin < row_end <= n_sub^2");
+  if (c->flags & ~MSN_FLAG_ATOMIC_BWD) return fail(MSN_ERR_INVALID_ARG, "unknown flags");
+  if (c->n_sub > 2048) return fail(MSN_ERR_UNSUPPORTED, "n_sub > 2048 is not supported");
+  msn_pkm* h = new (std::nothrow) msn_pkm;
+  if (!h) return fail(MSN_ERR_INTERNAL, "out of host memory");
+  h->cfg = *c;
+  h->last_launches = 0;
+  *out = h;
+  return MSN_OK;
+}
+
+msn_status msn_pkm_destroy(msn_pkm_t h) {
+  delete h;
+  return MSN_OK;
+}
+
+int32_t msn_pkm_last_launch_count(msn_pkm_t h) { return h ? h->last_launches : -1; }
+
+msn_status msn_pkm_workspace_size(msn_pkm_t h, int64_t B, int64_t gather_batch, size_t* fwd,
+                                  size_t* bwd) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, B))) return st;
+  if (gather_batch < B) return fail(MSN_ERR_INVALID_ARG, "gather_batch < B");
+  const Shape s = shape_of(h->cfg, B);
+  if (fwd) *fwd = fwd_bytes(s);
+  if (bwd) *bwd = bwd_workspace_bytes(s, gather_batch);
+  return MSN_OK;
+}
+
+msn_status msn_pkm_select(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                          const void* subkeys, int32_t* idx, float* weights, void* workspace,
+                          size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, B))) return st;
+  h->last_launches = 0;
+  if (B == 0) return MSN_OK;
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(workspace);
+  return do_select(h, (cudaStream_t)stream, B, query, subkeys, idx, weights, workspace,
+                   workspace_bytes, &h->last_launches);
+}
+
+msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                          const float* weights, const void* values, float* out) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
+  if (B == 0) return MSN_OK;
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(out);
+  const Shape s = shape_of(h->cfg, B);
+  cudaError_t e = launch_gather(s, idx, weights, values, out, (cudaStream_t)stream,
+                                &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "gather");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                           const void* subkeys, const void* values, float* out, int32_t* idx,
+                           float* weights, void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, B))) return st;
+  h->last_launches = 0;
+  if (B == 0) return MSN_OK;
+  const int64_t n = (int64_t)h->cfg.n_sub * h->cfg.n_sub;
+  if (h->cfg.row_begin != 0 || h->cfg.row_end != n)
+    return fail(MSN_ERR_INVALID_ARG, "msn_pkm_forward needs the whole table; use the phase calls when sharded");
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(out);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(workspace);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if ((st = do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
+                      &h->last_launches)))
+    return st;
+  cudaError_t e = launch_gather(shape_of(h->cfg, B), idx, weights, values, out, cs,
+                                &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "gather");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                           const float* weights, const float* d_out, const void* values,
+                           float* d_values, float* dw, void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
+  if (B == 0) return MSN_OK;
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(d_out);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(d_values);
+  REQUIRE_PTR(dw);
+  const Shape s = shape_of(h->cfg, B);
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaError_t e;
+  if (h->cfg.flags & MSN_FLAG_ATOMIC_BWD) {
+    e = launch_scatter_atomic(s, idx, weights, d_out, values, d_values, dw, cs, &h->last_launches);
+  } else {
+    REQUIRE_PTR(workspace);
+    const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
+    if (workspace_bytes < need)
+      return fail(MSN_ERR_WORKSPACE, "scatter workspace %zu < %zu bytes", workspace_bytes, need);
+    const BwdWorkspace ws = carve_bwd_workspace(shape_of(h->cfg, 0), B, workspace);
+    e = launch_scatter_sorted(s, idx, weights, d_out, values, d_values, dw, ws, cs,
+                              &h->last_launches);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "scatter (dV, dw)");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                                 const void* subkeys, const int32_t* idx, const float* weights,
+                                 const float* dw, float* d_query, float* d_subkeys,
+                                 void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, B))) return st;
+  h->last_launches = 0;
+  if (B == 0) return MSN_OK;
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(dw);
+  REQUIRE_PTR(d_query);
+  REQUIRE_PTR(d_subkeys);
+  REQUIRE_PTR(workspace);
+  const Shape s = shape_of(h->cfg, B);
+  const size_t need = bwd_workspace_bytes(s, B);
+  if (workspace_bytes < need)
+    return fail(MSN_ERR_WORKSPACE, "backward workspace %zu < %zu bytes", workspace_bytes, need);
+  const BwdWorkspace ws = carve_bwd_workspace(s, B, workspace);
+  cudaError_t e = launch_backward_keys(s, query, subkeys, idx, weights, dw, d_query, d_subkeys, ws,
+                                       (cudaStream_t)stream, &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "backward (ds, dQ, dK)");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B, const float* d_out,
+                            const void* query, const void* subkeys, const void* values,
+                            const int32_t* idx, const float* weights, float* d_query,
+                            float* d_subkeys, float* d_values, float* dw, void* workspace,
+                            size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, B))) return st;
+  h->last_launches = 0;
+  if (B == 0) return MSN_OK;
+  const int64_t n = (int64_t)h->cfg.n_sub * h->cfg.n_sub;
+  if (h->cfg.row_begin != 0 || h->cfg.row_end != n)
+    return fail(MSN_ERR_INVALID_ARG, "msn_pkm_backward needs the whole table; use the phase calls when sharded");
+  REQUIRE_PTR(d_out);
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(d_query);
+  REQUIRE_PTR(d_subkeys);
+  REQUIRE_PTR(d_values);
+  REQUIRE_PTR(workspace);
+  const Shape s = shape_of(h->cfg, B);
+  const size_t need = bwd_workspace_bytes(s, B);
+  if (workspace_bytes < need)
+    return fail(MSN_ERR_WORKSPACE, "backward workspace %zu < %zu bytes", workspace_bytes, need);
+  const BwdWorkspace ws = carve_bwd_workspace(s, B, workspace);
+  float* dwp = dw ? dw : ws.dw;
+  if (dw && !aligned16(dw)) return fail(MSN_ERR_INVALID_ARG, "dw is not 16-byte aligned");
+  cudaStream_t cs = (cudaStream_t)stream;
+  int* L = &h->last_launches;
+  cudaError_t e = (h->cfg.flags & MSN_FLAG_ATOMIC_BWD)
+                      ? launch_scatter_atomic(s, idx, weights, d_out, values, d_values, dwp, cs, L)
+                      : launch_scatter_sorted(s, idx, weights, d_out, values, d_values, dwp, ws,
+                                              cs, L);
+  if (e != cudaSuccess) return cuda_fail(e, "backward (dV, dw)");
+  e = launch_backward_keys(s, query, subkeys, idx, weights, dwp, d_query, d_subkeys, ws, cs, L);
+  if (e != cudaSuccess) return cuda_fail(e, "backward (ds, dQ, dK)");
+  return MSN_OK;
+}
+
+}  // extern "C"

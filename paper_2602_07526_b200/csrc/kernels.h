@@ -1,0 +1,64 @@
+// kernels.h -- internal launcher interface between the C-ABI host code
+// (api.cu) and the kernels.  Not part of the public ABI (include/msn_pkm.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace msn {
+
+enum Dt { F32 = 0, BF16 = 1 };
+
+struct Shape {
+  int64_t B;       // queries in this call
+  int H, n_sub, d_h, d_v, k;
+  int qk_dt, v_dt;
+  int64_t row_begin, row_end;  // local value rows
+};
+
+// a1+a2 (SIMT scorer, fp32 configs): per-half top-k, sorted (score desc,
+// index asc).  topv/topi [B,H,2,k].  scores_ws: [B,H,2,n_sub] fp32 scratch.
+cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, float* scores_ws,
+                               float* topv, int32_t* topi, cudaStream_t st, int* launches);
+
+// a1+a2 on tcgen05 (bf16 configs): fused scoring GEMM + per-half top-k.
+// Returns cudaErrorNotSupported when the shape is not handled.
+cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, float* topv,
+                             int32_t* topi, cudaStream_t st, int* launches);
+bool select_tc_supported(const Shape& s);
+
+// a3+a4: Cartesian top-k over I x J + softmax.  idx/w [B,H,k].
+cudaError_t launch_cartesian(const Shape& s, const float* topv, const int32_t* topi,
+                             int32_t* idx, float* w, cudaStream_t st, int* launches);
+
+// a5: out[b] = sum over local rows of w * V[idx - row_begin] (=).
+cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
+                          float* out, cudaStream_t st, int* launches);
+
+// ---- backward ----
+struct BwdWorkspace {
+  uint32_t *keys_a, *keys_b, *vals_a, *vals_b;  // radix sort ping-pong, n_max entries
+  uint32_t* hist;                               // 256 * max_blocks
+  float* part_first;                            // tiles * D_max
+  float* part_last;                             // tiles * D_max
+  float* dsS;                                   // 2*B*H*k aggregated score grads
+  float* dw;                                    // B*H*k (when the caller gives none)
+};
+size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
+BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
+
+// a6 deterministic: sort (idx -> cid) then fused row-major dV += / dw.
+cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,
+                                  const float* dOut, const void* V, float* dV, float* dw,
+                                  const BwdWorkspace& ws, cudaStream_t st, int* launches);
+// a6 atomic: query-major re-gather + red.global.add.v4.f32.
+cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
+                                  const float* dOut, const void* V, float* dV, float* dw,
+                                  cudaStream_t st, int* launches);
+// a7+a8: ds, dQ (=), dK (+=) deterministic.
+cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
+                                 const int32_t* idx, const float* w, const float* dw, float* dQ,
+                                 float* dK, const BwdWorkspace& ws, cudaStream_t st,
+                                 int* launches);
+
+}  // namespace msn

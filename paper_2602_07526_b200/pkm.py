@@ -1,0 +1,210 @@
+"""Thin Python binding of the C ABI (include/msn_pkm.h): argument marshalling
+only -- every step of the PKM lookup runs in the CUDA kernels of
+libmsn_pkm.so.  PyTorch provides device memory, streams and (for the sharded
+table) torch.distributed.
+
+    lk = PKMLookup(heads=4, n_sub=512, d_half=256, d_value=256, k=32,
+                   max_batch=4096, qk_dtype=torch.bfloat16,
+                   value_dtype=torch.bfloat16)
+    out, idx, w = lk.forward(q, K, V)                 # a1-a5
+    dq, dK, dV, dw = lk.backward(d_out, q, K, V, idx, w)   # a6-a8
+
+Inputs given as CPU tensors are copied to the device (and results back) --
+the end-to-end path the bench's ``e2e`` number times.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+import torch
+
+from . import _lib
+
+_DT = {torch.float32: _lib.MSN_F32, torch.bfloat16: _lib.MSN_BF16}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class PKMLookup:
+    """One PKM memory (H heads, per-head sub-key codebooks [H,2,n_sub,d_half],
+    one value table [n_sub^2, d_value] or its row shard [row_begin,row_end))."""
+
+    def __init__(self, heads: int, n_sub: int, d_half: int, d_value: int, k: int,
+                 max_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
+                 atomic_bwd: bool = False, row_begin: int = 0, row_end: Optional[int] = None,
+                 device=None):
+        self.lib = _lib.load()
+        self.heads, self.n_sub, self.d_half, self.d_value, self.k = heads, n_sub, d_half, d_value, k
+        self.max_batch = max_batch
+        self.qk_dtype, self.value_dtype = qk_dtype, value_dtype
+        self.row_begin = row_begin
+        self.row_end = n_sub * n_sub if row_end is None else row_end
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        cfg = _lib.Config(_lib.ABI_VERSION, heads, n_sub, d_half, d_value, k, max_batch,
+                          _DT[qk_dtype], _DT[value_dtype],
+                          _lib.FLAG_ATOMIC_BWD if atomic_bwd else 0, 0, self.row_begin, self.row_end)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.msn_pkm_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.msn_pkm_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+    # ---------------------------------------------------------------- utils
+    @property
+    def sharded(self) -> bool:
+        return not (self.row_begin == 0 and self.row_end == self.n_sub * self.n_sub)
+
+    def workspace_bytes(self, B: int, gather_batch: Optional[int] = None) -> Tuple[int, int]:
+        f, b = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(self.lib.msn_pkm_workspace_size(self._h, B, B if gather_batch is None else gather_batch,
+                                                   ctypes.byref(f), ctypes.byref(b)))
+        return f.value, b.value
+
+    def workspace(self, B: int, gather_batch: Optional[int] = None) -> torch.Tensor:
+        need = max(self.workspace_bytes(B, gather_batch))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def last_launch_count(self) -> int:
+        return int(self.lib.msn_pkm_last_launch_count(self._h))
+
+    def _dev(self, t: torch.Tensor) -> torch.Tensor:
+        if t.device.type != "cuda":
+            t = t.to(self.device, non_blocking=True)
+        return t.contiguous()
+
+    def _check_inputs(self, query, subkeys, values=None):
+        H, d = self.heads, self.d_half
+        if query.dim() != 4 or tuple(query.shape[1:]) != (H, 2, d) or query.dtype != self.qk_dtype:
+            raise ValueError(f"query must be [B,{H},2,{d}] {self.qk_dtype}, got {tuple(query.shape)} {query.dtype}")
+        if tuple(subkeys.shape) != (H, 2, self.n_sub, d) or subkeys.dtype != self.qk_dtype:
+            raise ValueError(f"subkeys must be [{H},2,{self.n_sub},{d}] {self.qk_dtype}")
+        if values is not None:
+            rows = self.row_end - self.row_begin
+            if tuple(values.shape) != (rows, self.d_value) or values.dtype != self.value_dtype:
+                raise ValueError(f"values must be [{rows},{self.d_value}] {self.value_dtype}")
+
+    # ------------------------------------------------------------ forward
+    def forward(self, query: torch.Tensor, subkeys: torch.Tensor, values: torch.Tensor):
+        """a1-a5.  Returns (out [B,d_v] fp32, idx [B,H,k] int32, w [B,H,k] fp32)."""
+        host = query.device.type != "cuda"
+        self._check_inputs(query, subkeys, values)
+        q, K, V = self._dev(query), self._dev(subkeys), self._dev(values)
+        B = q.shape[0]
+        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        ws = self.workspace(B)
+        _lib.check(self.lib.msn_pkm_forward(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(V),
+                                            _ptr(out), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
+        if host:
+            return out.cpu(), idx.cpu(), w.cpu()
+        return out, idx, w
+
+    def select(self, query: torch.Tensor, subkeys: torch.Tensor):
+        """a1-a4 only: (idx, w)."""
+        self._check_inputs(query, subkeys)
+        q, K = self._dev(query), self._dev(subkeys)
+        B = q.shape[0]
+        idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        ws = self.workspace(B)
+        _lib.check(self.lib.msn_pkm_select(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(idx),
+                                           _ptr(w), _ptr(ws), ws.numel()))
+        return idx, w
+
+    def gather(self, idx: torch.Tensor, w: torch.Tensor, values: torch.Tensor) -> torch.Tensor:
+        """a5 over this process's rows (rows of other shards contribute 0)."""
+        idx, w, V = self._dev(idx), self._dev(w), self._dev(values)
+        B = idx.shape[0]
+        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.msn_pkm_gather(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(V), _ptr(out)))
+        return out
+
+    # ----------------------------------------------------------- backward
+    def backward(self, d_out, query, subkeys, values, idx, w,
+                 d_subkeys: Optional[torch.Tensor] = None, d_values: Optional[torch.Tensor] = None):
+        """a6-a8.  d_subkeys / d_values are accumulated into when given (+=),
+        else zero-initialised.  Returns (d_query, d_subkeys, d_values, dw)."""
+        host = d_out.device.type != "cuda"
+        self._check_inputs(query, subkeys, values)
+        d, q, K, V = self._dev(d_out), self._dev(query), self._dev(subkeys), self._dev(values)
+        idx, w = self._dev(idx), self._dev(w)
+        B = q.shape[0]
+        if d_subkeys is None:
+            d_subkeys = torch.zeros((self.heads, 2, self.n_sub, self.d_half), dtype=torch.float32, device=self.device)
+        if d_values is None:
+            d_values = torch.zeros((self.row_end - self.row_begin, self.d_value), dtype=torch.float32, device=self.device)
+        d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=self.device)
+        dw = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        ws = self.workspace(B)
+        _lib.check(self.lib.msn_pkm_backward(self._h, _stream(), B, _ptr(d), _ptr(q), _ptr(K), _ptr(V),
+                                             _ptr(idx), _ptr(w), _ptr(d_query), _ptr(d_subkeys),
+                                             _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
+        if host:
+            return d_query.cpu(), d_subkeys, d_values, dw
+        return d_query, d_subkeys, d_values, dw
+
+    def scatter(self, idx, w, d_out, values, d_values, gather_batch: Optional[int] = None):
+        """a6 over this process's rows: d_values += ..., returns dw (0 for
+        slots held by other shards)."""
+        idx, w, d, V = self._dev(idx), self._dev(w), self._dev(d_out), self._dev(values)
+        B = idx.shape[0]
+        dw = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        f, b = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(self.lib.msn_pkm_workspace_size(self._h, 0, B, ctypes.byref(f), ctypes.byref(b)))
+        ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=self.device) \
+            if self._ws is None or self._ws.numel() < b.value else self._ws
+        _lib.check(self.lib.msn_pkm_scatter(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(d), _ptr(V),
+                                            _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
+        return dw
+
+    def backward_keys(self, query, subkeys, idx, w, dw, d_subkeys: Optional[torch.Tensor] = None):
+        """a7-a8 given the full dw: (d_query, d_subkeys)."""
+        q, K, idx, w, dw = (self._dev(t) for t in (query, subkeys, idx, w, dw))
+        B = q.shape[0]
+        if d_subkeys is None:
+            d_subkeys = torch.zeros((self.heads, 2, self.n_sub, self.d_half), dtype=torch.float32, device=self.device)
+        d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=self.device)
+        ws = self.workspace(B)
+        _lib.check(self.lib.msn_pkm_backward_keys(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(idx), _ptr(w),
+                                                  _ptr(dw), _ptr(d_query), _ptr(d_subkeys), _ptr(ws), ws.numel()))
+        return d_query, d_subkeys
+
+
+class PKMFunction(torch.autograd.Function):
+    """autograd wrapper: out = PKM(query; subkeys, values).  Gradients: query
+    (=), subkeys and values (fp32, cast to the parameter dtype by autograd)."""
+
+    @staticmethod
+    def forward(ctx, lookup: PKMLookup, query, subkeys, values):
+        out, idx, w = lookup.forward(query, subkeys, values)
+        ctx.lookup = lookup
+        ctx.save_for_backward(query, subkeys, values, idx, w)
+        return out
+
+    @staticmethod
+    def backward(ctx, d_out):
+        q, K, V, idx, w = ctx.saved_tensors
+        dq, dK, dV, _ = ctx.lookup.backward(d_out.contiguous().float(), q, K, V, idx, w)
+        return None, dq.to(q.dtype), dK.to(K.dtype), dV.to(V.dtype)
+
+
+def pkm(lookup: PKMLookup, query, subkeys, values):
+    return PKMFunction.apply(lookup, query, subkeys, values)

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+the same seeded inputs, element by element, under the north_star bar
+(tests/parity.py).  Needs a B200."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2602_07526_b200 import workloads as wl
+from paper_2602_07526_b200.pkm import PKMLookup
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def lookup_for(cfg, B=None, **kw):
+    return PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k,
+                     max_batch=B or cfg.batch, qk_dtype=cfg.qk_dtype,
+                     value_dtype=cfg.value_dtype, **kw)
+
+
+def run_fwd_bwd(cfg, Q, K, V, dOut, backward=True, **kw):
+    lk = lookup_for(cfg, Q.shape[0], **kw)
+    out, idx, w = lk.forward(Q, K, V)
+    res = {"out": out, "idx": idx, "w": w}
+    if backward:
+        dq, dK, dV, dw = lk.backward(dOut, Q, K, V, idx, w)
+        res.update(dQ=dq, dK=dK, dV=dV, dw=dw)
+    torch.cuda.synchronize()
+    return res
+
+
+def check_all(cfg, Q, K, V, dOut, res, backward=True):
+    Qc, Kc, Vc = Q.cpu(), K.cpu(), V.cpu()
+    o, affected, rep = parity.check_forward(Qc, Kc, Vc, cfg.k, res["out"], res["idx"], res["w"])
+    if backward:
+        _, rb = parity.check_backward(Qc, Kc, Vc, cfg.k, dOut.cpu(), o, affected,
+                                      res["dQ"], res["dK"], res["dV"], res["dw"], gpu_idx=res["idx"])
+        rep.update(rb)
+    print(cfg.name, rep)
+    return rep
+
+
+# ------------------------------------------------------------ small sweep --
+SWEEP = [
+    # (B, H, n_sub, d_h, d_v, k, qk dtype, v dtype)
+    (1, 1, 16, 32, 32, 1, torch.float32, torch.float32),
+    (7, 3, 40, 32, 64, 5, torch.float32, torch.float32),
+    (33, 2, 128, 64, 64, 8, torch.float32, torch.float32),
+    (130, 4, 64, 32, 128, 17, torch.float32, torch.float32),
+    (65, 2, 96, 64, 256, 32, torch.bfloat16, torch.bfloat16),
+    (200, 1, 256, 128, 512, 32, torch.bfloat16, torch.bfloat16),
+    (37, 2, 128, 32, 64, 64, torch.float32, torch.float32),
+    (50, 2, 64, 64, 32, 64, torch.bfloat16, torch.float32),
+    (300, 4, 512, 256, 256, 32, torch.bfloat16, torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("shape", SWEEP, ids=lambda s: "x".join(str(v) for v in s[:6]) + f"-{str(s[6])[6:]}")
+def test_small_shapes_fwd_bwd(shape):
+    B, H, n_sub, d_h, d_v, k, qdt, vdt = shape
+    cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, qdt, vdt, index=100 + n_sub + k)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    res = run_fwd_bwd(cfg, Q, K, V, dOut)
+    check_all(cfg, Q, K, V, dOut, res)
+
+
+def test_integer_data_bit_exact_selection():
+    """Integer-valued queries/keys: every score is exact in fp32 and fp64, so
+    the selection (including the tie rule R5) must be bit-identical."""
+    g = torch.Generator(device="cpu").manual_seed(5)
+    B, H, n_sub, d_h, d_v, k = 64, 2, 64, 32, 64, 16
+    Q = torch.randint(-2, 3, (B, H, 2, d_h), generator=g).float()
+    K = torch.randint(-1, 2, (H, 2, n_sub, d_h), generator=g).float()
+    V = torch.randn((n_sub * n_sub, d_v), generator=g) * 0.02
+    for dt in (torch.float32, torch.bfloat16):
+        cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, dt, torch.float32)
+        lk = lookup_for(cfg)
+        out, idx, w = lk.forward(Q.to(dt).to(DEV), K.to(dt).to(DEV), V.to(DEV))
+        from oracle import oracle as orc
+        o = orc.forward(Q, K, V, k)
+        assert np.array_equal(idx.cpu().numpy(), o["idx"]), "selection must be bit-exact on exact data"
+        parity.row_close(out.cpu().numpy(), o["out"], 1e-4, what="out")
+
+
+def test_zero_query_closed_form():
+    cfg = wl.tiny_config(16, 2, 32, 64, 64, 8, torch.bfloat16, torch.bfloat16)
+    _, K, V, _ = wl.make_all(cfg, DEV)
+    Q = torch.zeros((16, 2, 2, 32), dtype=torch.bfloat16, device=DEV)
+    out, idx, w = lookup_for(cfg).forward(Q, K, V)
+    assert torch.equal(idx.cpu(), torch.arange(8, dtype=torch.int32).expand(16, 2, 8))
+    assert torch.allclose(w, torch.full_like(w, 1 / 8), rtol=1e-6)
+    ref = 2 * V[:8].float().mean(0)
+    assert torch.allclose(out, ref.expand_as(out), rtol=1e-5, atol=1e-7)
+
+
+# ------------------------------------------------------- BASELINE configs --
+def test_c1_tiny_fp32_forward():
+    cfg = wl.CONFIGS["c1_tiny_fp32"]
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    res = run_fwd_bwd(cfg, Q, K, V, dOut, backward=False)
+    check_all(cfg, Q, K, V, dOut, res, backward=False)
+
+
+def test_c2_mid_bf16_fwd_bwd():
+    cfg = wl.CONFIGS["c2_mid_bf16"]
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    res = run_fwd_bwd(cfg, Q, K, V, dOut)
+    check_all(cfg, Q, K, V, dOut, res)
+
+
+@pytest.mark.parametrize("name,sample", [("c3_train_fp32_zipf", 1024), ("c4_large_sharded_bf16", 512),
+                                         ("c5_latency_bf16", 512)])
+def test_large_configs_on_query_sample(name, sample):
+    """Full tables, the first `sample` queries (the oracle's budget)."""
+    cfg = wl.CONFIGS[name]
+    Q = wl.make_queries(cfg, DEV)[:sample].contiguous()
+    K, V = wl.make_subkeys(cfg, DEV), wl.make_values(cfg, DEV)
+    dOut = wl.make_dout(cfg, DEV)[:sample].contiguous()
+    res = run_fwd_bwd(cfg, Q, K, V, dOut, backward=cfg.backward)
+    check_all(cfg, Q, K, V, dOut, res, backward=cfg.backward)
+
+
+@pytest.mark.parametrize("name", ["c3_train_fp32_zipf", "c4_large_sharded_bf16"])
+def test_full_size_invariants(name):
+    """Full BASELINE size in the bench's launch configuration: properties that
+    hold at any size, plus sampled lookups recomputed by the oracle."""
+    cfg = wl.CONFIGS[name]
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, dw = lk.backward(dOut, Q, K, V, idx, w)
+    torch.cuda.synchronize()
+    assert torch.allclose(w.double().sum(-1), torch.ones(1, dtype=torch.float64, device=DEV), atol=1e-6)
+    assert (w[..., 1:] <= w[..., :-1] + 1e-7).all()
+    s = torch.sort(idx, dim=-1).values
+    assert (s[..., 1:] != s[..., :-1]).all() and idx.min() >= 0 and idx.max() < cfg.n_slots
+    # sum over rows of dV = H * sum_b dOut  (sum_t w = 1)
+    lhs = dV.double().sum(0)
+    rhs = cfg.heads * dOut.double().sum(0)
+    assert torch.allclose(lhs, rhs, rtol=1e-4, atol=1e-3 * float(rhs.abs().max()))
+    # untouched rows exactly zero
+    touched = torch.zeros(cfg.n_slots, dtype=torch.bool, device=DEV)
+    touched[idx.reshape(-1).long()] = True
+    assert (dV[~touched] == 0).all()
+    # sampled lookups against the oracle (same selection expected)
+    from oracle import oracle as orc
+    sel = torch.arange(0, cfg.batch, cfg.batch // 64, device=DEV)[:64]
+    o = orc.forward(Q[sel].cpu(), K.cpu(), V.cpu(), cfg.k)
+    aff, _ = parity.compare_selection(Q[sel].cpu(), K.cpu(), idx[sel].cpu().numpy(), o, cfg.n_sub)
+    parity.row_close(out[sel].cpu().numpy(), o["out"], parity.rtol_for(cfg.value_dtype),
+                     ~aff.any(axis=1), "out (sampled)")
+    bw = orc.backward(Q[sel].cpu(), K.cpu(), V.cpu(), o["idx"], dOut[sel].cpu(), want_dense_dv=False)
+    parity.row_close(dq[sel].cpu().numpy().reshape(-1, cfg.d_half), bw["dQ"].reshape(-1, cfg.d_half),
+                     parity.rtol_for(cfg.value_dtype), np.repeat((~aff).reshape(-1), 2), "dQ (sampled)")
+
+
+# ---------------------------------------------------------- properties ----
+def test_determinism_bitwise():
+    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=1024)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    r1 = run_fwd_bwd(cfg, Q, K, V, dOut)
+    r2 = run_fwd_bwd(cfg, Q, K, V, dOut)
+    for key in ("out", "idx", "w", "dQ", "dK", "dV", "dw"):
+        assert torch.equal(r1[key], r2[key]), key
+
+
+def test_batch_invariance():
+    """A query's idx/w/out do not depend on B or on its position."""
+    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=512)
+    Q, K, V, _ = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)
+    perm = torch.randperm(512, device=DEV)[:77]
+    o2, i2, w2 = lk.forward(Q[perm].contiguous(), K, V)
+    assert torch.equal(i2, idx[perm]) and torch.equal(w2, w[perm]) and torch.equal(o2, out[perm])
+
+
+def test_atomic_backward_matches_oracle():
+    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=512)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    res = run_fwd_bwd(cfg, Q, K, V, dOut, atomic_bwd=True)
+    check_all(cfg, Q, K, V, dOut, res)
+
+
+def test_backward_accumulates():
+    cfg = wl.tiny_config(32, 2, 32, 64, 64, 8, torch.float32, torch.float32)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)
+    _, dK1, dV1, _ = lk.backward(dOut, Q, K, V, idx, w)
+    dK2, dV2 = dK1.clone(), dV1.clone()
+    lk.backward(dOut, Q, K, V, idx, w, d_subkeys=dK2, d_values=dV2)
+    assert torch.allclose(dK2, 2 * dK1) and torch.allclose(dV2, 2 * dV1)
+
+
+def test_sharded_phases_match_full():
+    """Row-sharded table emulated on one GPU: P shards' gather partials sum to
+    the full output; their dV shards concatenate to the full dV bitwise
+    up to fp32 reassociation at tile-crossing runs; their dw sum to the full
+    dw bitwise."""
+    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=256)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    full = run_fwd_bwd(cfg, Q, K, V, dOut)
+    n = cfg.n_slots
+    for P in (2, 4):
+        outs, dvs, dws = [], [], []
+        for p in range(P):
+            r0, r1 = p * n // P, (p + 1) * n // P
+            lk = lookup_for(cfg, row_begin=r0, row_end=r1)
+            idx, w = lk.select(Q, K)
+            assert torch.equal(idx, full["idx"]) and torch.equal(w, full["w"])
+            outs.append(lk.gather(idx, w, V[r0:r1].contiguous()))
+            dvp = torch.zeros((r1 - r0, cfg.d_value), device=DEV)
+            dws.append(lk.scatter(idx, w, dOut, V[r0:r1].contiguous(), dvp))
+            dvs.append(dvp)
+        torch.cuda.synchronize()
+        assert torch.allclose(sum(outs), full["out"], rtol=1e-5, atol=1e-6)
+        assert torch.allclose(torch.cat(dvs), full["dV"], rtol=1e-5, atol=1e-7)
+        dw = sum(dws)
+        assert torch.allclose(dw, full["dw"], rtol=0, atol=0)
+        lk = lookup_for(cfg)
+        dq, dK = lk.backward_keys(Q, K, full["idx"], full["w"], dw)
+        assert torch.equal(dq, full["dQ"]) and torch.equal(dK, full["dK"])
+
+
+def test_backward_unsupported_width_is_reported():
+    from paper_2602_07526_b200._lib import MsnError
+    cfg = wl.tiny_config(4, 1, 16, 16, 32, 2, torch.float32, torch.float32)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)          # forward supports d_half % 16 == 0
+    with pytest.raises(MsnError, match="UNSUPPORTED"):
+        lk.backward(dOut, Q, K, V, idx, w)      # backward needs d_half % 32 == 0
+
+
+def test_autograd_function():
+    from paper_2602_07526_b200.pkm import pkm
+    cfg = wl.tiny_config(16, 2, 32, 64, 64, 8, torch.float32, torch.float32)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    q, k_, v = (t.clone().requires_grad_(True) for t in (Q, K, V))
+    out = pkm(lk, q, k_, v)
+    (out * dOut).sum().backward()
+    _, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, _ = lk.backward(dOut, Q, K, V, idx, w)
+    assert torch.equal(q.grad, dq) and torch.equal(k_.grad, dK) and torch.equal(v.grad, dV)
+
+
+def test_host_tensors_end_to_end():
+    cfg = wl.tiny_config(16, 2, 32, 64, 64, 8, torch.float32, torch.float32)
+    Q, K, V, dOut = wl.make_all(cfg, "cpu")
+    lk = lookup_for(cfg)
+    out_h, idx_h, w_h = lk.forward(Q.pin_memory(), K.to(DEV), V.to(DEV))
+    out_d, idx_d, w_d = lk.forward(Q.to(DEV), K.to(DEV), V.to(DEV))
+    assert out_h.device.type == "cpu" and torch.equal(out_h, out_d.cpu())
+
+
+def test_invalid_arguments_raise():
+    from paper_2602_07526_b200._lib import MsnError
+    cfg = wl.tiny_config(16, 2, 32, 64, 64, 8, torch.float32, torch.float32)
+    lk = lookup_for(cfg)
+    Q, K, V, _ = wl.make_all(cfg, DEV)
+    with pytest.raises(ValueError):
+        lk.forward(Q.to(torch.bfloat16), K, V)
+    big = wl.make_queries(cfg.scaled(batch=17), DEV)
+    with pytest.raises(MsnError):
+        lk.forward(big, K, V)
