@@ -8,7 +8,7 @@ The bar (BASELINE.json north_star):
   values, measured per row as  max_e |g - o| <= rtol * scale_row, where
   scale_row = max(max_e |o_row|, max_e A_row, 1e-6 max |o|) and A is the sum
   of the absolute values of the terms the oracle adds up for that element
-  (sum_t |ds_t| |K_row| for dQ, sum |ds| |q| for dK) -- "relative" to the
+  (grad_key_magnitudes) -- "relative" to the
   magnitude of what is summed, so a row whose terms cancel to ~0 is not held
   to an impossible bound (reading R14).
 Lookups whose selection legitimately differs at a tie are excluded from the
@@ -95,6 +95,28 @@ def row_close(gpu: np.ndarray, ref: np.ndarray, rtol: float, row_mask=None, what
     return worst
 
 
+def grad_key_magnitudes(Q, K, o, bw, n_sub):
+    """Sum of |terms| behind each element of dQ and dK.  ds_t = w_t dw_t -
+    w_t sum_u w_u dw_u has magnitude A_t = w_t (|dw_t| + sum_u w_u |dw_u|);
+    dQ[b,h,half] = sum_t ds_t K[h,half,r_t] -> sum_t A_t |K[h,half,r_t]|;
+    dK[h,half,r] = sum_{b,t: r_t=r} ds_t q[b,h,half] -> sum A_t |q|."""
+    Kf = K.double().numpy() if isinstance(K, torch.Tensor) else np.asarray(K, np.float64)
+    Qf = Q.double().numpy() if isinstance(Q, torch.Tensor) else np.asarray(Q, np.float64)
+    w, dw = o["w"], bw["dw"]
+    A = w * (np.abs(dw) + (w * np.abs(dw)).sum(-1, keepdims=True))
+    H = Kf.shape[0]
+    i_t, j_t = o["idx"] // n_sub, o["idx"] % n_sub
+    hh = np.arange(H)[None, :, None]
+    absq = np.stack([(A[..., None] * np.abs(Kf[hh, 0, i_t])).sum(2),
+                     (A[..., None] * np.abs(Kf[hh, 1, j_t])).sum(2)], axis=2)
+    absk = np.zeros_like(Kf)
+    for half, r_t in ((0, i_t), (1, j_t)):
+        for h in range(H):
+            np.add.at(absk[h, half], r_t[:, h].reshape(-1),
+                      (A[:, h, :, None] * np.abs(Qf[:, h, half][:, None, :])).reshape(-1, Kf.shape[-1]))
+    return absq, absk
+
+
 def check_forward(Q, K, V, k, out, idx, w, max_affected_frac=0.01):
     """Full forward parity for one call; returns (oracle result, affected, report)."""
     n_sub = K.shape[2]
@@ -122,19 +144,7 @@ def check_backward(Q, K, V, k, dOut, o, affected, dQ, dK, dV, dw=None, gpu_idx=N
     bw = orc.backward(Q, K, V, o["idx"], dOut, want_dense_dv=False)
     rtol = rtol_for(V.dtype)
     rep = {}
-    # |terms| behind dQ and dK (sum_t |ds_t| |K_r| and sum |ds_t| |q|)
-    Kf = K.double().numpy() if isinstance(K, torch.Tensor) else np.asarray(K, np.float64)
-    Qf = Q.double().numpy() if isinstance(Q, torch.Tensor) else np.asarray(Q, np.float64)
-    ads = np.abs(bw["ds"])
-    i_t, j_t = o["idx"] // n_sub, o["idx"] % n_sub
-    hh = np.arange(H)[None, :, None]
-    absq = np.stack([(ads[..., None] * np.abs(Kf[hh, 0, i_t])).sum(2),
-                     (ads[..., None] * np.abs(Kf[hh, 1, j_t])).sum(2)], axis=2)
-    absk = np.zeros_like(Kf)
-    for half, r_t in ((0, i_t), (1, j_t)):
-        for h in range(H):
-            np.add.at(absk[h, half], r_t[:, h].reshape(-1),
-                      (ads[:, h, :, None] * np.abs(Qf[:, h, half][:, None, :])).reshape(-1, Kf.shape[-1]))
+    absq, absk = grad_key_magnitudes(Q, K, o, bw, n_sub)
     # dQ rows: per (b,h,half)
     mask_q = np.repeat((~affected).reshape(-1), 2)
     rep["dQ_err"] = row_close(dQ.detach().cpu().numpy().reshape(B * H * 2, -1),

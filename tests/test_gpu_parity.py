@@ -152,8 +152,12 @@ def test_full_size_invariants(name):
     parity.row_close(out[sel].cpu().numpy(), o["out"], parity.rtol_for(cfg.value_dtype),
                      ~aff.any(axis=1), "out (sampled)")
     bw = orc.backward(Q[sel].cpu(), K.cpu(), V.cpu(), o["idx"], dOut[sel].cpu(), want_dense_dv=False)
+    absq, _ = parity.grad_key_magnitudes(Q[sel].cpu(), K.cpu(), o, bw, cfg.n_sub)
     parity.row_close(dq[sel].cpu().numpy().reshape(-1, cfg.d_half), bw["dQ"].reshape(-1, cfg.d_half),
-                     parity.rtol_for(cfg.value_dtype), np.repeat((~aff).reshape(-1), 2), "dQ (sampled)")
+                     parity.rtol_for(cfg.value_dtype), np.repeat((~aff).reshape(-1), 2), "dQ (sampled)",
+                     absmag=absq.reshape(-1, cfg.d_half))
+    parity.row_close(dw[sel].cpu().numpy().reshape(-1, cfg.k), bw["dw"].reshape(-1, cfg.k),
+                     parity.rtol_for(cfg.value_dtype), (~aff).reshape(-1), "dw (sampled)")
 
 
 # ---------------------------------------------------------- properties ----
