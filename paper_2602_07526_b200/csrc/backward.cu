@@ -46,39 +46,99 @@ __global__ void __launch_bounds__(RS_THREADS) rs_hist_kernel(const uint32_t* __r
   hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// exclusive scan of len entries by one block of 1024 threads
-__global__ void __launch_bounds__(1024) rs_scan_kernel(uint32_t* __restrict__ data, int64_t len) {
-  __shared__ uint32_t warp_tot[32];
-  const int t = threadIdx.x, lane = t % 32, wid = t / 32;
-  const int64_t chunk = (len + 1023) / 1024;
-  const int64_t s = t * chunk, e = s + chunk < len ? s + chunk : len;
-  uint32_t sum = 0;
-  for (int64_t i = s; i < e; ++i) sum += data[i];
-  uint32_t incl = sum;
+// Exclusive scan of the digit-major histogram in three coalesced phases:
+// per-chunk sums, a scan of the chunk sums, then per-chunk scans with carry.
+constexpr int SCAN_T = 256;
+
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* total,
+                                                        uint32_t* sh /*[8]*/) {
+  const int lane = threadIdx.x % 32, wid = threadIdx.x / 32;
+  uint32_t incl = v;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += o;
   }
-  if (lane == 31) warp_tot[wid] = incl;
+  if (lane == 31) sh[wid] = incl;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_T / 32; ++w) {
+    const uint32_t x = sh[w];
+    wpre += (w < wid) ? x : 0u;
+    tot += x;
+  }
+  __syncthreads();
+  *total = tot;
+  return wpre + incl - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) scan_reduce_kernel(const uint32_t* __restrict__ data,
+                                                             int64_t len, int64_t chunk,
+                                                             uint32_t* __restrict__ part) {
+  __shared__ uint32_t sh[SCAN_T / 32];
+  const int64_t s = (int64_t)blockIdx.x * chunk;
+  const int64_t e = s + chunk < len ? s + chunk : len;
+  uint32_t acc = 0;
+  for (int64_t i = s + threadIdx.x; i < e; i += SCAN_T) acc += data[i];
+  uint32_t tot;
+  block_excl_scan_256(acc, &tot, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) scan_parts_kernel(uint32_t* __restrict__ part, int n) {
+  __shared__ uint32_t sh[32];
+  const int t = threadIdx.x, lane = t % 32, wid = t / 32;
+  const uint32_t v = t < n ? part[t] : 0u;
+  uint32_t incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) sh[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    uint32_t v = warp_tot[lane];
-    uint32_t vi = v;
+    const uint32_t x = sh[lane];
+    uint32_t xi = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t o = __shfl_up_sync(0xffffffffu, vi, d);
-      if (lane >= d) vi += o;
+      const uint32_t o = __shfl_up_sync(0xffffffffu, xi, d);
+      if (lane >= d) xi += o;
     }
-    warp_tot[lane] = vi - v;
+    sh[lane] = xi - x;
   }
   __syncthreads();
-  uint32_t run = warp_tot[wid] + incl - sum;
-  for (int64_t i = s; i < e; ++i) {
-    const uint32_t v = data[i];
-    data[i] = run;
-    run += v;
+  if (t < n) part[t] = sh[wid] + incl - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) scan_down_kernel(uint32_t* __restrict__ data, int64_t len,
+                                                           int64_t chunk,
+                                                           const uint32_t* __restrict__ part) {
+  __shared__ uint32_t sh[SCAN_T / 32];
+  const int64_t s = (int64_t)blockIdx.x * chunk;
+  const int64_t e = s + chunk < len ? s + chunk : len;
+  uint32_t carry = part[blockIdx.x];
+  for (int64_t base = s; base < e; base += SCAN_T) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < e ? data[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_256(v, &tot, sh);
+    if (i < e) data[i] = carry + ex;
+    carry += tot;
   }
+}
+
+cudaError_t excl_scan(uint32_t* data, int64_t len, uint32_t* part, cudaStream_t st, int* launches) {
+  int nb = (int)((len + 255) / 256);
+  if (nb > 1024) nb = 1024;
+  const int64_t chunk = (len + nb - 1) / nb;
+  nb = (int)((len + chunk - 1) / chunk);
+  scan_reduce_kernel<<<nb, SCAN_T, 0, st>>>(data, len, chunk, part);
+  scan_parts_kernel<<<1, 1024, 0, st>>>(part, nb);
+  scan_down_kernel<<<nb, SCAN_T, 0, st>>>(data, len, chunk, part);
+  *launches += 3;
+  return cudaGetLastError();
 }
 
 // Stable scatter: items of a block are ranked per digit in input order with
@@ -149,12 +209,14 @@ cudaError_t radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uin
   for (int p = 0; p < passes; ++p) {
     const int shift = p * RS_BITS;
     rs_hist_kernel<<<nblocks, RS_THREADS, 0, st>>>(kin, n, shift, hist, nblocks);
-    rs_scan_kernel<<<1, 1024, 0, st>>>(hist, (int64_t)RS_BUCKETS * nblocks);
+    const int64_t hl = (int64_t)RS_BUCKETS * nblocks;
+    cudaError_t e = excl_scan(hist, hl, hist + hl, st, launches);
+    if (e != cudaSuccess) return e;
     rs_scatter_kernel<<<nblocks, RS_THREADS, 0, st>>>(kin, vin, n, shift, hist, nblocks, kout,
                                                      vout);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    *launches += 3;
+    *launches += 2;
     // ping-pong
     uint32_t* nk = (kout == keys_b) ? keys_a : keys_b;
     uint32_t* nv = (vout == vals_b) ? vals_a : vals_b;
@@ -264,6 +326,7 @@ __global__ void __launch_bounds__(256) segreduce_kernel(SegArgs a) {
   for (int j0 = 0; j0 < cnt; j0 += SEG_U) {
     uint32_t key[SEG_U], rec[SEG_U];
     float x[SEG_U][EPL];
+    float yp[MODE == MODE_DV ? SEG_U : 1][EPL];
     float wt[SEG_U];
 #pragma unroll
     for (int u = 0; u < SEG_U; ++u) {
@@ -285,6 +348,11 @@ __global__ void __launch_bounds__(256) segreduce_kernel(SegArgs a) {
       else
 #pragma unroll
         for (int i = 0; i < EPL; ++i) x[u][i] = 0.f;
+      if constexpr (MODE == MODE_DV) {
+        // prefetch the value row too (repeats within a run hit L1)
+        if (valid)
+          load_slice<YT, EPL>(reinterpret_cast<const YT*>(a.Y) + (int64_t)kk * a.D + lane * EPL, yp[u]);
+      }
     }
 #pragma unroll
     for (int u = 0; u < SEG_U; ++u) {
@@ -297,8 +365,8 @@ __global__ void __launch_bounds__(256) segreduce_kernel(SegArgs a) {
 #pragma unroll
         for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
         if constexpr (MODE == MODE_DV) {
-          if (cur < a.nrows)
-            load_slice<YT, EPL>(reinterpret_cast<const YT*>(a.Y) + (int64_t)cur * a.D + lane * EPL, y);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) y[i] = yp[u][i];
         }
       }
       if (cur >= a.nrows) continue;
@@ -522,7 +590,7 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   const int64_t D = s.d_v > s.d_h ? s.d_v : s.d_h;
   size_t b = 0;
   b += 4 * align256(sizeof(uint32_t) * n);
-  b += align256(sizeof(uint32_t) * RS_BUCKETS * nblocks);
+  b += align256(sizeof(uint32_t) * (RS_BUCKETS * nblocks + 1024));
   b += 2 * align256(sizeof(float) * tiles * D);
   b += align256(sizeof(float) * n_dk);
   b += align256(sizeof(float) * n_dv);
@@ -542,7 +610,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.keys_b = (uint32_t*)p; p += align256(sizeof(uint32_t) * n);
   w.vals_a = (uint32_t*)p; p += align256(sizeof(uint32_t) * n);
   w.vals_b = (uint32_t*)p; p += align256(sizeof(uint32_t) * n);
-  w.hist = (uint32_t*)p; p += align256(sizeof(uint32_t) * RS_BUCKETS * nblocks);
+  w.hist = (uint32_t*)p; p += align256(sizeof(uint32_t) * (RS_BUCKETS * nblocks + 1024));
   w.part_first = (float*)p; p += align256(sizeof(float) * tiles * D);
   w.part_last = (float*)p; p += align256(sizeof(float) * tiles * D);
   w.dsS = (float*)p; p += align256(sizeof(float) * n_dk);

@@ -1,9 +1,409 @@
-// select_tc.cu -- placeholder until the tcgen05 scorer lands.
+// select_tc.cu -- steps a1 + a2 on the 5th-generation tensor cores:
+// sub-key scoring S = K q (Eq. S_old) as a tcgen05 GEMM
+// fed by TMA, with the per-half argtopk fused into the
+// epilogue so that S never reaches HBM.
+//
+// One CTA per (128-query tile, head h, half): D[128 x n_sub] = Q_half . K_half^T
+// with bf16 operands and fp32 accumulation in TMEM (kind::f16), computed in
+// N-chunks of up to 256 columns that alternate between two TMEM accumulator
+// buffers, so the MMA of chunk c+1 overlaps the epilogue of chunk c.
+//
+//   warp 0      TMA producer: the whole query tile once (resident), then the
+//               sub-key tiles through a STAGES-deep mbarrier ring
+//   warp 1      MMA issuer (one elected lane): tcgen05.mma + tcgen05.commit
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4-7   epilogue: TMEM lane i = query row i; each thread streams its
+//               row's scores (tcgen05.ld 32x32b.x32), keeps candidates above
+//               its running k-th score in a shared-memory buffer and merges
+//               them into a sorted register top-k (score desc, index asc --
+//               reading R5; columns arrive in ascending index order, so a
+//               strict ">" keeps the earlier index first on ties).
+#include <cuda.h>
+
+#include "common.cuh"
 #include "kernels.h"
+
 namespace msn {
-bool select_tc_supported(const Shape&) { return false; }
-cudaError_t launch_select_tc(const Shape&, const void*, const void*, float*, int32_t*, cudaStream_t,
-                             int*) {
-  return cudaErrorNotSupported;
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+constexpr int kStages = 3;
+constexpr int kMaxNTile = 256;
+constexpr int kCap = 64;          // candidate buffer entries per row
+constexpr int kBlockK = 64;       // bf16 elements per 128-byte swizzle row
+
+// ------------------------------------------------------------------ PTX ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (bf16 in, fp32 accumulate)
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major operand in 128-byte swizzled rows
+// (8-row atoms of 1024 B): start>>4, LBO=1 (unused for swizzled K-major),
+// SBO=1024>>4, version 1 (sm_100), layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor, kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1),
+// B bf16 (bits 10-12 = 1), both K-major, N>>3 at bit 17, M>>4 at bit 24.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------- top-k -------
+// Insert (v, c) into the descending arrays tv/ti (length KT) if v > tv[KT-1].
+template <int KT>
+__device__ __forceinline__ void topk_insert(float (&tv)[KT], int32_t (&ti)[KT], float v, int32_t c,
+                                            bool active) {
+  if (!active || !(v > tv[KT - 1])) return;
+#pragma unroll
+  for (int j = KT - 1; j > 0; --j) {
+    const bool above_prev = v > tv[j - 1];
+    const bool above_cur = v > tv[j];
+    const float nv = above_prev ? tv[j - 1] : (above_cur ? v : tv[j]);
+    const int32_t ni = above_prev ? ti[j - 1] : (above_cur ? c : ti[j]);
+    tv[j] = nv;
+    ti[j] = ni;
+  }
+  if (v > tv[0]) {
+    tv[0] = v;
+    ti[0] = c;
+  }
+}
+
+struct TcParams {
+  int64_t B;
+  int H, n_sub, d_h, k;
+  int n_tile, n_chunks, k_blocks;
+  float* topv;
+  int32_t* topi;
+};
+
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 1)
+    select_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                     const __grid_constant__ CUtensorMap tmap_k, const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // carve: A (k_blocks x 16 KB) | B ring (kStages x n_tile x 128 B) | cand vals | cand cols | bars
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = base;
+  uint8_t* sB = sA + p.k_blocks * 16384;
+  float* cand_v = (float*)(sB + kStages * p.n_tile * 128);
+  uint16_t* cand_c = (uint16_t*)(cand_v + kCap * 128);
+  uint64_t* bars = (uint64_t*)(((uintptr_t)(cand_c + kCap * 128) + 7) & ~(uintptr_t)7);
+  uint64_t* a_full = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int hh = blockIdx.y;  // h*2 + half
+  const int64_t m0 = (int64_t)blockIdx.x * 128;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmap_q);
+    prefetch_tmap(&tmap_k);
+    mbar_init(a_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(a_full, p.k_blocks * 16384);
+      for (int kb = 0; kb < p.k_blocks; ++kb)
+        tma_load_3d(sA + kb * 16384, &tmap_q, a_full, kb * kBlockK, hh, (int)m0);
+      int it = 0;
+      for (int c = 0; c < p.n_chunks; ++c)
+        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], p.n_tile * 128);
+          tma_load_2d(sB + s * p.n_tile * 128, &tmap_k, &full[s], kb * kBlockK,
+                      hh * p.n_sub + c * p.n_tile);
+        }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(128, p.n_tile);
+      mbar_wait(a_full, 0);
+      tc_fence_after();
+      int it = 0;
+      for (int c = 0; c < p.n_chunks; ++c) {
+        const int buf = c & 1;
+        mbar_wait(&tempty[buf], ((c >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * kMaxNTile;
+        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + kb * 16384);
+          const uint32_t b0 = smem_u32(sB + s * p.n_tile * 128);
+#pragma unroll
+          for (int kk = 0; kk < kBlockK / 16; ++kk)
+            tc_mma(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---------------------------------------------------------- epilogue
+    const int q = warp & 3;            // TMEM lane quarter of this warp
+    const int row = q * 32 + lane;     // query row within the tile
+    const int tid = row;               // candidate buffer column
+    float tv[KT];
+    int32_t ti[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      tv[j] = -INFINITY;
+      ti[j] = 0x7fffffff;
+    }
+    float tau = -INFINITY;
+    int cnt = 0;
+    auto flush = [&]() {
+      const int mx = __reduce_max_sync(0xffffffffu, cnt);
+      for (int i = 0; i < mx; ++i) {
+        const bool act = i < cnt;
+        const float v = act ? cand_v[i * 128 + tid] : -INFINITY;
+        const int32_t col = act ? (int32_t)cand_c[i * 128 + tid] : 0;
+        topk_insert<KT>(tv, ti, v, col, act);
+      }
+      cnt = 0;
+      tau = tv[KT - 1];
+    };
+    for (int c = 0; c < p.n_chunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(&tfull[buf], (c >> 1) & 1);
+      tc_fence_after();
+      for (int sub = 0; sub < p.n_tile / 32; ++sub) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * kMaxNTile + sub * 32, r);
+        const int col0 = c * p.n_tile + sub * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float v = __uint_as_float(r[j]);
+          if (v > tau) {
+            cand_v[cnt * 128 + tid] = v;
+            cand_c[cnt * 128 + tid] = (uint16_t)(col0 + j);
+            ++cnt;
+          }
+        }
+        if (__reduce_max_sync(0xffffffffu, cnt) > kCap - 32) flush();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+    flush();
+    const int64_t b = m0 + row;
+    if (b < p.B) {
+      const int64_t o = (b * p.H * 2 + hh) * (int64_t)p.k;
+#pragma unroll
+      for (int j = 0; j < KT; ++j)
+        if (j < p.k) {
+          p.topv[o + j] = tv[j];
+          p.topi[o + j] = ti[j];
+        }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------- host --------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+
+int n_tile_for(int n_sub) { return n_sub < kMaxNTile ? n_sub : kMaxNTile; }
+
+size_t smem_bytes(const Shape& s) {
+  const int nt = n_tile_for(s.n_sub);
+  return 1024 + (size_t)(s.d_h / kBlockK) * 16384 + (size_t)kStages * nt * 128 +
+         (size_t)kCap * 128 * (4 + 2) + 8 * (1 + 2 * kStages + 4) + 16;
+}
+
+template <int KT>
+cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk, TcParams p,
+                      cudaStream_t st) {
+  const size_t sm = smem_bytes(s);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  dim3 grid((unsigned)((s.B + 127) / 128), s.H * 2);
+  select_tc_kernel<KT><<<grid, kThreads, sm, st>>>(mq, mk, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool select_tc_supported(const Shape& s) {
+  if (s.qk_dt != BF16) return false;
+  if (s.d_h % kBlockK != 0 || s.d_h > 256) return false;
+  const int nt = n_tile_for(s.n_sub);
+  if (nt % 32 != 0 || s.n_sub % nt != 0 || s.n_sub > 65535) return false;
+  if (s.k > 64) return false;
+  if (smem_bytes(s) > 227 * 1024) return false;
+  return get_encode() != nullptr;
+}
+
+cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, float* topv,
+                             int32_t* topi, cudaStream_t st, int* launches) {
+  if (!select_tc_supported(s)) return cudaErrorNotSupported;
+  EncodeTiledFn enc = get_encode();
+  CUtensorMap mq, mk;
+  {
+    // Q [B, H*2, d_h]: dims (d_h, H*2, B); box (64, 1, 128)
+    cuuint64_t dims[3] = {(cuuint64_t)s.d_h, (cuuint64_t)(s.H * 2), (cuuint64_t)s.B};
+    cuuint64_t strides[2] = {(cuuint64_t)s.d_h * 2, (cuuint64_t)s.H * 2 * s.d_h * 2};
+    cuuint32_t box[3] = {kBlockK, 1, 128};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(Q), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  const int nt = n_tile_for(s.n_sub);
+  {
+    // K [H*2*n_sub, d_h]: dims (d_h, H*2*n_sub); box (64, n_tile)
+    cuuint64_t dims[2] = {(cuuint64_t)s.d_h, (cuuint64_t)s.H * 2 * s.n_sub};
+    cuuint64_t strides[1] = {(cuuint64_t)s.d_h * 2};
+    cuuint32_t box[2] = {kBlockK, (cuuint32_t)nt};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(K), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / kBlockK, topv, topi};
+  cudaError_t e;
+  if (s.k <= 8) e = launch_kt<8>(s, mq, mk, p, st);
+  else if (s.k <= 16) e = launch_kt<16>(s, mq, mk, p, st);
+  else if (s.k <= 32) e = launch_kt<32>(s, mq, mk, p, st);
+  else e = launch_kt<64>(s, mq, mk, p, st);
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
 }  // namespace msn
