@@ -12,12 +12,16 @@
 //               sub-key tiles through a STAGES-deep mbarrier ring
 //   warp 1      MMA issuer (one elected lane): tcgen05.mma + tcgen05.commit
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   epilogue: TMEM lane i = query row i; each thread streams its
-//               row's scores (tcgen05.ld 32x32b.x32), keeps candidates above
-//               its running k-th score in a shared-memory buffer and merges
-//               them into a sorted register top-k (score desc, index asc --
-//               reading R5; columns arrive in ascending index order, so a
-//               strict ">" keeps the earlier index first on ties).
+//   warps 4-7   epilogue: TMEM lane i = query row i, one thread per row.
+//               Phase 1 (first min(n_sub, 512) columns, resident in both TMEM
+//               buffers): tau = KT-th largest of 2KT strided group maxima is a
+//               provable lower bound on the row's KT-th score; the ~1.3KT
+//               columns >= tau are buffered in shared memory and ordered by
+//               an in-register bitonic sort (score desc, index asc -- R5).
+//               Phase 2 (further chunks): columns above the running KT-th
+//               score are buffered and merged in sorted batches (bitonic
+//               merge).  No per-column data-dependent branching beyond a
+//               predicated shared-memory store.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -148,6 +152,92 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KT], int32_t (&ti)[KT], 
   }
 }
 
+// (value desc, index asc) "a ranks before b"
+__device__ __forceinline__ bool before(float av, int32_t ai, float bv, int32_t bi) {
+  return av > bv || (av == bv && ai < bi);
+}
+// In-register bitonic sort of N (value, index) pairs into (value desc, index asc).
+template <int N>
+__device__ __forceinline__ void bitonic_sort_pairs(float (&v)[N], int32_t (&ix)[N]) {
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const bool sw = desc ? before(v[j], ix[j], v[i], ix[i]) : before(v[i], ix[i], v[j], ix[j]);
+          const float tv = sw ? v[j] : v[i];
+          const float uv = sw ? v[i] : v[j];
+          const int32_t ti = sw ? ix[j] : ix[i];
+          const int32_t ui = sw ? ix[i] : ix[j];
+          v[i] = tv; v[j] = uv; ix[i] = ti; ix[j] = ui;
+        }
+      }
+    }
+  }
+}
+// Values only, descending.
+template <int N>
+__device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const float hi = fmaxf(v[i], v[j]), lo = fminf(v[i], v[j]);
+          v[i] = desc ? hi : lo;
+          v[j] = desc ? lo : hi;
+        }
+      }
+    }
+  }
+}
+// Sorted-desc top list T (KT) and sorted-desc candidates C (first KT used):
+// T <- top KT of T u C.  max(T_i, C_{KT-1-i}) is bitonic; a half-cleaner
+// cascade sorts it.
+template <int KT, int NC>
+__device__ __forceinline__ void merge_top(float (&tv)[KT], int32_t (&ti)[KT], const float (&cv)[NC],
+                                          const int32_t (&ci)[NC]) {
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    const int j = KT - 1 - i;
+    const bool takec = j < NC && before(cv[j < NC ? j : 0], ci[j < NC ? j : 0], tv[i], ti[i]);
+    if (takec) { tv[i] = cv[j]; ti[i] = ci[j]; }
+  }
+#pragma unroll
+  for (int stride = KT >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+    for (int i = 0; i < KT; ++i) {
+      const int j = i ^ stride;
+      if (j > i) {
+        const bool sw = before(tv[j], ti[j], tv[i], ti[i]);
+        const float a = sw ? tv[j] : tv[i], b = sw ? tv[i] : tv[j];
+        const int32_t c = sw ? ti[j] : ti[i], d = sw ? ti[i] : ti[j];
+        tv[i] = a; tv[j] = b; ti[i] = c; ti[j] = d;
+      }
+    }
+  }
+}
+// Load the first N buffered candidates of this thread (pad with -inf), sort.
+template <int N>
+__device__ __forceinline__ void load_sorted(const float* cand_v, const uint16_t* cand_c, int tid,
+                                            int cnt, float (&v)[N], int32_t (&ix)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool ok = i < cnt;
+    v[i] = ok ? cand_v[i * 128 + tid] : -INFINITY;
+    ix[i] = ok ? (int32_t)cand_c[i * 128 + tid] : 0x7fffffff;
+  }
+  bitonic_sort_pairs<N>(v, ix);
+}
+
 struct TcParams {
   int64_t B;
   int H, n_sub, d_h, k;
@@ -162,12 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmap_k, const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // carve: A (k_blocks x 16 KB) | B ring (kStages x n_tile x 128 B) | cand vals | cand cols | bars
-  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = base;
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
-  float* cand_v = (float*)(sB + kStages * p.n_tile * 128);
-  uint16_t* cand_c = (uint16_t*)(cand_v + kCap * 128);
-  uint64_t* bars = (uint64_t*)(((uintptr_t)(cand_c + kCap * 128) + 7) & ~(uintptr_t)7);
+  float* cand_v = reinterpret_cast<float*>(sB + kStages * p.n_tile * 128);
+  uint16_t* cand_c = reinterpret_cast<uint16_t*>(cand_v + kCap * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cand_c + kCap * 128);  // 8-aligned: kCap*128*6
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + kStages;
@@ -251,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;            // TMEM lane quarter of this warp
     const int row = q * 32 + lane;     // query row within the tile
     const int tid = row;               // candidate buffer column
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     float tv[KT];
     int32_t ti[KT];
 #pragma unroll
@@ -258,31 +349,121 @@ __global__ void __launch_bounds__(kThreads, 1)
       tv[j] = -INFINITY;
       ti[j] = 0x7fffffff;
     }
-    float tau = -INFINITY;
+    // Phase 1: the first n1 = min(n_sub, 2*n_tile) columns are resident in
+    // both TMEM buffers.  tau = KT-th largest of the 2KT strided group maxima
+    // (group g = columns c with c % 2KT == g) is a lower bound on the row's
+    // KT-th largest score, so every top-KT column has score >= tau.
+    const int n1_chunks = p.n_chunks < 2 ? p.n_chunks : 2;
+    const int n1 = n1_chunks * p.n_tile;
+    for (int c = 0; c < n1_chunks; ++c) mbar_wait(&tfull[c], 0);
+    tc_fence_after();
+    constexpr int G = 2 * KT;
+    float tau;
+    {
+      float gm[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) gm[j] = -INFINITY;
+      constexpr int STEP = G > 32 ? G : 32;  // columns per iteration (multiple of G or 32)
+      for (int c0 = 0; c0 < n1; c0 += STEP) {
+#pragma unroll
+        for (int piece = 0; piece < STEP / 32; ++piece) {
+          const int col = c0 + piece * 32;
+          if (col < n1) {
+            uint32_t r[32];
+            tmem_ld32(lane_base + (col / p.n_tile) * kMaxNTile + (col % p.n_tile), r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int g = (piece * 32 + j) % G;  // == (col + j) % G since c0 % G == 0 or G | 32
+              gm[g] = fmaxf(gm[g], __uint_as_float(r[j]));
+            }
+          }
+        }
+      }
+      bitonic_sort_vals<G>(gm);
+      tau = gm[KT - 1];
+    }
+    // collect candidates >= tau (at most kCap buffered)
     int cnt = 0;
+    bool overflow = false;
+    for (int col = 0; col < n1; col += 32) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + (col / p.n_tile) * kMaxNTile + (col % p.n_tile), r);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float v = __uint_as_float(r[j]);
+        if (v >= tau) {
+          if (cnt < kCap) {
+            cand_v[cnt * 128 + tid] = v;
+            cand_c[cnt * 128 + tid] = (uint16_t)(col + j);
+          } else {
+            overflow = true;
+          }
+          ++cnt;
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, overflow)) {
+      // rare (massive ties): exact insertion over every resident column
+      for (int col = 0; col < n1; col += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_base + (col / p.n_tile) * kMaxNTile + (col % p.n_tile), r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) topk_insert<KT>(tv, ti, __uint_as_float(r[j]), col + j, true);
+      }
+    } else {
+      const int mx = __reduce_max_sync(0xffffffffu, cnt);
+      if (mx <= 16) {
+        float cv[16]; int32_t ci[16];
+        load_sorted<16>(cand_v, cand_c, tid, cnt, cv, ci);
+        merge_top<KT, 16>(tv, ti, cv, ci);
+      } else if (mx <= 32) {
+        float cv[32]; int32_t ci[32];
+        load_sorted<32>(cand_v, cand_c, tid, cnt, cv, ci);
+        merge_top<KT, 32>(tv, ti, cv, ci);
+      } else {
+        float cv[64]; int32_t ci[64];
+        load_sorted<64>(cand_v, cand_c, tid, cnt, cv, ci);
+        merge_top<KT, 64>(tv, ti, cv, ci);
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0)
+      for (int c = 0; c < n1_chunks; ++c) mbar_arrive(&tempty[c]);
+    // Phase 2: remaining chunks stream through; candidates above the
+    // running KT-th score are buffered and merged in sorted batches.
+    cnt = 0;
     auto flush = [&]() {
       const int mx = __reduce_max_sync(0xffffffffu, cnt);
-      for (int i = 0; i < mx; ++i) {
-        const bool act = i < cnt;
-        const float v = act ? cand_v[i * 128 + tid] : -INFINITY;
-        const int32_t col = act ? (int32_t)cand_c[i * 128 + tid] : 0;
-        topk_insert<KT>(tv, ti, v, col, act);
+      if (mx == 0) return;
+      if (mx <= 16) {
+        float cv[16]; int32_t ci[16];
+        load_sorted<16>(cand_v, cand_c, tid, cnt, cv, ci);
+        merge_top<KT, 16>(tv, ti, cv, ci);
+      } else if (mx <= 32) {
+        float cv[32]; int32_t ci[32];
+        load_sorted<32>(cand_v, cand_c, tid, cnt, cv, ci);
+        merge_top<KT, 32>(tv, ti, cv, ci);
+      } else {
+        float cv[64]; int32_t ci[64];
+        load_sorted<64>(cand_v, cand_c, tid, cnt, cv, ci);
+        merge_top<KT, 64>(tv, ti, cv, ci);
       }
       cnt = 0;
-      tau = tv[KT - 1];
     };
-    for (int c = 0; c < p.n_chunks; ++c) {
+    for (int c = n1_chunks; c < p.n_chunks; ++c) {
       const int buf = c & 1;
       mbar_wait(&tfull[buf], (c >> 1) & 1);
       tc_fence_after();
       for (int sub = 0; sub < p.n_tile / 32; ++sub) {
         uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * kMaxNTile + sub * 32, r);
+        tmem_ld32(lane_base + buf * kMaxNTile + sub * 32, r);
         const int col0 = c * p.n_tile + sub * 32;
+        const float thr = tv[KT - 1];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float v = __uint_as_float(r[j]);
-          if (v > tau) {
+          if (v > thr) {
             cand_v[cnt * 128 + tid] = v;
             cand_c[cnt * 128 + tid] = (uint16_t)(col0 + j);
             ++cnt;
@@ -363,7 +544,7 @@ bool select_tc_supported(const Shape& s) {
   if (s.d_h % kBlockK != 0 || s.d_h > 256) return false;
   const int nt = n_tile_for(s.n_sub);
   if (nt % 32 != 0 || s.n_sub % nt != 0 || s.n_sub > 65535) return false;
-  if (s.k > 64) return false;
+  if (s.k > 32) return false;
   if (smem_bytes(s) > 227 * 1024) return false;
   return get_encode() != nullptr;
 }
@@ -400,8 +581,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, float
   cudaError_t e;
   if (s.k <= 8) e = launch_kt<8>(s, mq, mk, p, st);
   else if (s.k <= 16) e = launch_kt<16>(s, mq, mk, p, st);
-  else if (s.k <= 32) e = launch_kt<32>(s, mq, mk, p, st);
-  else e = launch_kt<64>(s, mq, mk, p, st);
+  else e = launch_kt<32>(s, mq, mk, p, st);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

@@ -66,11 +66,14 @@ def test_small_shapes_fwd_bwd(shape):
     check_all(cfg, Q, K, V, dOut, res)
 
 
-def test_integer_data_bit_exact_selection():
+@pytest.mark.parametrize("B,H,n_sub,d_h,k", [(64, 2, 64, 32, 16), (130, 2, 512, 64, 32),
+                                             (96, 1, 1024, 128, 16), (40, 2, 256, 64, 8)])
+def test_integer_data_bit_exact_selection(B, H, n_sub, d_h, k):
     """Integer-valued queries/keys: every score is exact in fp32 and fp64, so
-    the selection (including the tie rule R5) must be bit-identical."""
-    g = torch.Generator(device="cpu").manual_seed(5)
-    B, H, n_sub, d_h, d_v, k = 64, 2, 64, 32, 64, 16
+    the selection (including the tie rule R5, with many exact ties) must be
+    bit-identical -- on the SIMT path (d_h=32) and the tcgen05 path (bf16)."""
+    g = torch.Generator(device="cpu").manual_seed(5 + n_sub)
+    d_v = 64
     Q = torch.randint(-2, 3, (B, H, 2, d_h), generator=g).float()
     K = torch.randint(-1, 2, (H, 2, n_sub, d_h), generator=g).float()
     V = torch.randn((n_sub * n_sub, d_v), generator=g) * 0.02
@@ -84,10 +87,12 @@ def test_integer_data_bit_exact_selection():
         parity.row_close(out.cpu().numpy(), o["out"], 1e-4, what="out")
 
 
-def test_zero_query_closed_form():
-    cfg = wl.tiny_config(16, 2, 32, 64, 64, 8, torch.bfloat16, torch.bfloat16)
+@pytest.mark.parametrize("d_h,n_sub", [(32, 64), (64, 64), (128, 1024)])
+def test_zero_query_closed_form(d_h, n_sub):
+    """q = 0: all scores tie at 0 -> idx = 0..k-1 (massive-tie path)."""
+    cfg = wl.tiny_config(16, 2, d_h, n_sub, 64, 8, torch.bfloat16, torch.bfloat16)
     _, K, V, _ = wl.make_all(cfg, DEV)
-    Q = torch.zeros((16, 2, 2, 32), dtype=torch.bfloat16, device=DEV)
+    Q = torch.zeros((16, 2, 2, d_h), dtype=torch.bfloat16, device=DEV)
     out, idx, w = lookup_for(cfg).forward(Q, K, V)
     assert torch.equal(idx.cpu(), torch.arange(8, dtype=torch.int32).expand(16, 2, 8))
     assert torch.allclose(w, torch.full_like(w, 1 / 8), rtol=1e-6)
