@@ -55,10 +55,11 @@ Shape shape_of(const msn_pkm_config& c, int64_t B) {
   return s;
 }
 
-// forward workspace layout: [topv | topi | scores (SIMT scorer only)]
+// forward workspace layout: [cand_v | cand_c | cand_n | scores (SIMT scorer only)]
 size_t fwd_bytes(const Shape& s) {
   const int64_t rows = s.B * s.H * 2;
-  size_t b = align256(sizeof(float) * rows * s.k) + align256(sizeof(int32_t) * rows * s.k);
+  size_t b = align256(sizeof(float) * rows * kCandCap) + align256(sizeof(int32_t) * rows * kCandCap) +
+             align256(sizeof(int32_t) * rows);
   if (!select_tc_supported(s)) b += align256(sizeof(float) * rows * s.n_sub);
   return b;
 }
@@ -90,19 +91,22 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
   const int64_t rows = B * s.H * 2;
   char* p = (char*)ws;
-  float* topv = (float*)p;
-  p += align256(sizeof(float) * rows * s.k);
-  int32_t* topi = (int32_t*)p;
-  p += align256(sizeof(int32_t) * rows * s.k);
+  Cands cd;
+  cd.v = (float*)p;
+  p += align256(sizeof(float) * rows * kCandCap);
+  cd.c = (int32_t*)p;
+  p += align256(sizeof(int32_t) * rows * kCandCap);
+  cd.n = (int32_t*)p;
+  p += align256(sizeof(int32_t) * rows);
   cudaError_t e;
   if (select_tc_supported(s)) {
-    e = launch_select_tc(s, query, subkeys, topv, topi, st, launches);
-    if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half top-k)");
+    e = launch_select_tc(s, query, subkeys, cd, st, launches);
+    if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half candidates)");
   } else {
-    e = launch_select_simt(s, query, subkeys, (float*)p, topv, topi, st, launches);
+    e = launch_select_simt(s, query, subkeys, (float*)p, cd, st, launches);
     if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half top-k)");
   }
-  e = launch_cartesian(s, topv, topi, idx, weights, st, launches);
+  e = launch_cartesian(s, cd, idx, weights, st, launches);
   if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax");
   return MSN_OK;
 }

@@ -2,6 +2,12 @@
 // and the softmax weights (reading R1), one warp
 // per lookup, all in registers and shared memory.
 //
+// Per-half order (a2).  Each half arrives as an unordered candidate list
+// (<= kCandCap entries containing its top-k, see kernels.h); the warp sorts
+// it with a 64-element bitonic network across lanes (shuffles; element
+// e = r*32 + lane, composite order (score desc, index asc) -- reading R5)
+// and keeps the first k: I (row half) and J (column half).
+//
 // Candidates.  With both per-half lists sorted descending, the score
 // c(a,b) = S_row[I_a] + S_col[J_b] is non-increasing in a and in b (fp32
 // rounding is monotone).  Two exact prunings bound the work:
@@ -24,9 +30,46 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 
+// Warp-wide bitonic sort of 64 (score, index) pairs held as (v[r], ix[r]),
+// element e = r*32 + lane; result in (score desc, index asc) order.
+__device__ __forceinline__ bool before(float av, int32_t ai, float bv, int32_t bi) {
+  return av > bv || (av == bv && ai < bi);
+}
+__device__ __forceinline__ void warp_sort64(float (&v)[2], int32_t (&ix)[2]) {
+  const int lane = threadIdx.x % 32;
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride == 32) {
+        // partner is the other register of the same lane (e ^ 32)
+        const bool desc = true;  // size == 64: the whole sequence is sorted descending
+        (void)desc;
+        const bool sw = before(v[1], ix[1], v[0], ix[0]);
+        const float a = sw ? v[1] : v[0], b = sw ? v[0] : v[1];
+        const int32_t c = sw ? ix[1] : ix[0], d = sw ? ix[0] : ix[1];
+        v[0] = a; v[1] = b; ix[0] = c; ix[1] = d;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int e = r * 32 + lane;
+          const float ov = __shfl_xor_sync(0xffffffffu, v[r], stride);
+          const int32_t oi = __shfl_xor_sync(0xffffffffu, ix[r], stride);
+          const bool lower = (e & stride) == 0;
+          const bool desc = (e & size) == 0;
+          const bool want_better = desc == lower;
+          const bool other_better = before(ov, oi, v[r], ix[r]);
+          if (want_better == other_better) { v[r] = ov; ix[r] = oi; }
+        }
+      }
+    }
+  }
+}
+
 template <int KMAX, int MAXC>
-__global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict__ topv,
-                                                        const int32_t* __restrict__ topi,
+__global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict__ cand_v,
+                                                        const int32_t* __restrict__ cand_c,
+                                                        const int32_t* __restrict__ cand_n,
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w) {
@@ -38,21 +81,39 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
-  const float* v1 = topv + (l * 2 + 0) * k;
-  const float* v2 = topv + (l * 2 + 1) * k;
-  const int32_t* i1 = topi + (l * 2 + 0) * k;
-  const int32_t* i2 = topi + (l * 2 + 1) * k;
 
   float va[APL];
   int32_t ia[APL];
 #pragma unroll
-  for (int u = 0; u < APL; ++u) {
-    const int a = lane + 32 * u;
-    va[u] = a < k ? v1[a] : -INFINITY;
-    ia[u] = a < k ? i1[a] : 0;
-    if (a < k) {
-      sv2[wid][a] = v2[a];
-      si2[wid][a] = i2[a];
+  for (int half = 0; half < 2; ++half) {
+    const int64_t row = l * 2 + half;
+    const int n = cand_n[row];
+    float v[2];
+    int32_t ix[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = r * 32 + lane;
+      const bool ok = e < n;
+      v[r] = ok ? cand_v[row * kCandCap + e] : -INFINITY;
+      ix[r] = ok ? cand_c[row * kCandCap + e] : 0x7fffffff;
+    }
+    warp_sort64(v, ix);
+    if (half == 0) {
+#pragma unroll
+      for (int u = 0; u < APL; ++u) {
+        const int a = lane + 32 * u;
+        va[u] = a < k ? v[u] : -INFINITY;
+        ia[u] = a < k ? ix[u] : 0;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < APL; ++u) {
+        const int a = lane + 32 * u;
+        if (a < k) {
+          sv2[wid][a] = v[u];
+          si2[wid][a] = ix[u];
+        }
+      }
     }
   }
   __syncwarp();
@@ -130,14 +191,14 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
 
 }  // namespace
 
-cudaError_t launch_cartesian(const Shape& s, const float* topv, const int32_t* topi,
-                             int32_t* idx, float* w, cudaStream_t st, int* launches) {
+cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, float* w,
+                             cudaStream_t st, int* launches) {
   const int64_t L = s.B * s.H;
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (s.k <= 32)
-    cartesian_kernel<32, 119><<<blocks, 256, 0, st>>>(topv, topi, L, s.n_sub, s.k, idx, w);
+    cartesian_kernel<32, 119><<<blocks, 256, 0, st>>>(cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w);
   else if (s.k <= 64)
-    cartesian_kernel<64, 280><<<blocks, 256, 0, st>>>(topv, topi, L, s.n_sub, s.k, idx, w);
+    cartesian_kernel<64, 280><<<blocks, 256, 0, st>>>(cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w);
   else
     return cudaErrorNotSupported;
   cudaError_t e = cudaGetLastError();

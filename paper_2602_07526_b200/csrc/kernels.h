@@ -16,20 +16,32 @@ struct Shape {
   int64_t row_begin, row_end;  // local value rows
 };
 
-// a1+a2 (SIMT scorer, fp32 configs): per-half top-k, sorted (score desc,
-// index asc).  topv/topi [B,H,2,k].  scores_ws: [B,H,2,n_sub] fp32 scratch.
-cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, float* scores_ws,
-                               float* topv, int32_t* topi, cudaStream_t st, int* launches);
+// Per-half candidate lists, the hand-off between a1+a2 and a3: for every
+// (b, h, half) row r, entries i < cand_n[r] of cand_v/cand_c[r*kCandCap + i]
+// are (score, sub-key index) pairs in no particular order that are
+// guaranteed to contain the row's top-k under (score desc, index asc).
+constexpr int kCandCap = 64;
+struct Cands {
+  float* v;      // [B*H*2, kCandCap]
+  int32_t* c;    // [B*H*2, kCandCap]
+  int32_t* n;    // [B*H*2]
+};
 
-// a1+a2 on tcgen05 (bf16 configs): fused scoring GEMM + per-half top-k.
+// a1+a2 (SIMT scorer, fp32 configs): exact per-half top-k (n = k entries).
+// scores_ws: [B,H,2,n_sub] fp32 scratch.
+cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, float* scores_ws,
+                               const Cands& cd, cudaStream_t st, int* launches);
+
+// a1+a2 on tcgen05 (bf16 configs): fused scoring GEMM + candidate selection.
 // Returns cudaErrorNotSupported when the shape is not handled.
-cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, float* topv,
-                             int32_t* topi, cudaStream_t st, int* launches);
+cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
+                             cudaStream_t st, int* launches);
 bool select_tc_supported(const Shape& s);
 
-// a3+a4: Cartesian top-k over I x J + softmax.  idx/w [B,H,k].
-cudaError_t launch_cartesian(const Shape& s, const float* topv, const int32_t* topi,
-                             int32_t* idx, float* w, cudaStream_t st, int* launches);
+// a2 (ordering) + a3 + a4: per-half top-k from the candidate lists, Cartesian
+// top-k over I x J + softmax.  idx/w [B,H,k].
+cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, float* w,
+                             cudaStream_t st, int* launches);
 
 // a5: out[b] = sum over local rows of w * V[idx - row_begin] (=).
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,

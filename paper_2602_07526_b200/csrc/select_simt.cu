@@ -72,8 +72,9 @@ __global__ void __launch_bounds__(256) score_kernel(const T* __restrict__ Q, con
 // composite (score desc, index asc) keys held in registers.
 template <int NPL>
 __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict__ S, int64_t rows,
-                                                        int n_sub, int k, float* __restrict__ topv,
-                                                        int32_t* __restrict__ topi) {
+                                                        int n_sub, int k, float* __restrict__ cv,
+                                                        int32_t* __restrict__ cc,
+                                                        int32_t* __restrict__ cn) {
   const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= rows) return;
@@ -93,24 +94,25 @@ __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict_
     for (int j = 0; j < NPL; ++j)
       if (c[j] == best) c[j] = 0ull;
     if (lane == 0) {
-      topv[row * k + t] = sel_key_score(best);
-      topi[row * k + t] = (int32_t)sel_key_index(best);
+      cv[row * kCandCap + t] = sel_key_score(best);
+      cc[row * kCandCap + t] = (int32_t)sel_key_index(best);
     }
   }
+  if (lane == 0) cn[row] = k;
 }
 
 template <int NPL>
-cudaError_t launch_topk(const float* S, int64_t rows, int n_sub, int k, float* topv, int32_t* topi,
+cudaError_t launch_topk(const float* S, int64_t rows, int n_sub, int k, const Cands& cd,
                         cudaStream_t st) {
   const int64_t blocks = (rows + 7) / 8;
-  topk_rows_kernel<NPL><<<(unsigned)blocks, 256, 0, st>>>(S, rows, n_sub, k, topv, topi);
+  topk_rows_kernel<NPL><<<(unsigned)blocks, 256, 0, st>>>(S, rows, n_sub, k, cd.v, cd.c, cd.n);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, float* scores_ws,
-                               float* topv, int32_t* topi, cudaStream_t st, int* launches) {
+                               const Cands& cd, cudaStream_t st, int* launches) {
   dim3 grid((s.n_sub + TN - 1) / TN, (unsigned)((s.B + TB - 1) / TB), s.H * 2);
   if (s.qk_dt == F32)
     score_kernel<float><<<grid, 256, 0, st>>>((const float*)Q, (const float*)K, scores_ws, s.B, s.H,
@@ -124,13 +126,13 @@ cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, flo
   ++*launches;
   const int64_t rows = s.B * s.H * 2;
   const int npl = (s.n_sub + 31) / 32;
-  if (npl <= 1) e = launch_topk<1>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
-  else if (npl <= 2) e = launch_topk<2>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
-  else if (npl <= 4) e = launch_topk<4>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
-  else if (npl <= 8) e = launch_topk<8>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
-  else if (npl <= 16) e = launch_topk<16>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
-  else if (npl <= 32) e = launch_topk<32>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
-  else if (npl <= 64) e = launch_topk<64>(scores_ws, rows, s.n_sub, s.k, topv, topi, st);
+  if (npl <= 1) e = launch_topk<1>(scores_ws, rows, s.n_sub, s.k, cd, st);
+  else if (npl <= 2) e = launch_topk<2>(scores_ws, rows, s.n_sub, s.k, cd, st);
+  else if (npl <= 4) e = launch_topk<4>(scores_ws, rows, s.n_sub, s.k, cd, st);
+  else if (npl <= 8) e = launch_topk<8>(scores_ws, rows, s.n_sub, s.k, cd, st);
+  else if (npl <= 16) e = launch_topk<16>(scores_ws, rows, s.n_sub, s.k, cd, st);
+  else if (npl <= 32) e = launch_topk<32>(scores_ws, rows, s.n_sub, s.k, cd, st);
+  else if (npl <= 64) e = launch_topk<64>(scores_ws, rows, s.n_sub, s.k, cd, st);
   else return cudaErrorNotSupported;
   if (e == cudaSuccess) ++*launches;
   return e;

@@ -13,15 +13,16 @@
 //   warp 1      MMA issuer (one elected lane): tcgen05.mma + tcgen05.commit
 //   warp 2      TMEM allocator (512 columns)
 //   warps 4-7   epilogue: TMEM lane i = query row i, one thread per row.
-//               Phase 1 (first min(n_sub, 512) columns, resident in both TMEM
-//               buffers): tau = KT-th largest of 2KT strided group maxima is a
-//               provable lower bound on the row's KT-th score; the ~1.3KT
-//               columns >= tau are buffered in shared memory and ordered by
-//               an in-register bitonic sort (score desc, index asc -- R5).
-//               Phase 2 (further chunks): columns above the running KT-th
-//               score are buffered and merged in sorted batches (bitonic
-//               merge).  No per-column data-dependent branching beyond a
-//               predicated shared-memory store.
+//               tau = KT-th largest of the 2KT strided group maxima seen so
+//               far is a provable lower bound on the row's KT-th score; the
+//               columns >= tau (~1.4 KT for random scores) are kept in a
+//               shared-memory buffer compacted as tau rises, and written out
+//               unordered as the row's candidate list (<= 64 entries that
+//               contain its top-k); cartesian_kernel orders them.  The first
+//               segment is the first min(n_sub, 512) columns, resident in both
+//               TMEM buffers, so tau is computed before any column is kept.
+//               Rows whose buffer would overflow (massive exact ties) take an
+//               exact bitwise search for their KT-th score instead.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -132,54 +133,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 }
 
 // ------------------------------------------------------------- top-k -------
-// Insert (v, c) into the descending arrays tv/ti (length KT) if v > tv[KT-1].
-template <int KT>
-__device__ __forceinline__ void topk_insert(float (&tv)[KT], int32_t (&ti)[KT], float v, int32_t c,
-                                            bool active) {
-  if (!active || !(v > tv[KT - 1])) return;
-#pragma unroll
-  for (int j = KT - 1; j > 0; --j) {
-    const bool above_prev = v > tv[j - 1];
-    const bool above_cur = v > tv[j];
-    const float nv = above_prev ? tv[j - 1] : (above_cur ? v : tv[j]);
-    const int32_t ni = above_prev ? ti[j - 1] : (above_cur ? c : ti[j]);
-    tv[j] = nv;
-    ti[j] = ni;
-  }
-  if (v > tv[0]) {
-    tv[0] = v;
-    ti[0] = c;
-  }
-}
-
-// (value desc, index asc) "a ranks before b"
-__device__ __forceinline__ bool before(float av, int32_t ai, float bv, int32_t bi) {
-  return av > bv || (av == bv && ai < bi);
-}
-// In-register bitonic sort of N (value, index) pairs into (value desc, index asc).
-template <int N>
-__device__ __forceinline__ void bitonic_sort_pairs(float (&v)[N], int32_t (&ix)[N]) {
-#pragma unroll
-  for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool desc = (i & size) == 0;
-          const bool sw = desc ? before(v[j], ix[j], v[i], ix[i]) : before(v[i], ix[i], v[j], ix[j]);
-          const float tv = sw ? v[j] : v[i];
-          const float uv = sw ? v[i] : v[j];
-          const int32_t ti = sw ? ix[j] : ix[i];
-          const int32_t ui = sw ? ix[i] : ix[j];
-          v[i] = tv; v[j] = uv; ix[i] = ti; ix[j] = ui;
-        }
-      }
-    }
-  }
-}
-// Values only, descending.
+// In-register bitonic sort of N values, descending (group maxima -> tau).
 template <int N>
 __device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
 #pragma unroll
@@ -199,51 +153,14 @@ __device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
     }
   }
 }
-// Sorted-desc top list T (KT) and sorted-desc candidates C (first KT used):
-// T <- top KT of T u C.  max(T_i, C_{KT-1-i}) is bitonic; a half-cleaner
-// cascade sorts it.
-template <int KT, int NC>
-__device__ __forceinline__ void merge_top(float (&tv)[KT], int32_t (&ti)[KT], const float (&cv)[NC],
-                                          const int32_t (&ci)[NC]) {
-#pragma unroll
-  for (int i = 0; i < KT; ++i) {
-    const int j = KT - 1 - i;
-    const bool takec = j < NC && before(cv[j < NC ? j : 0], ci[j < NC ? j : 0], tv[i], ti[i]);
-    if (takec) { tv[i] = cv[j]; ti[i] = ci[j]; }
-  }
-#pragma unroll
-  for (int stride = KT >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-    for (int i = 0; i < KT; ++i) {
-      const int j = i ^ stride;
-      if (j > i) {
-        const bool sw = before(tv[j], ti[j], tv[i], ti[i]);
-        const float a = sw ? tv[j] : tv[i], b = sw ? tv[i] : tv[j];
-        const int32_t c = sw ? ti[j] : ti[i], d = sw ? ti[i] : ti[j];
-        tv[i] = a; tv[j] = b; ti[i] = c; ti[j] = d;
-      }
-    }
-  }
-}
-// Load the first N buffered candidates of this thread (pad with -inf), sort.
-template <int N>
-__device__ __forceinline__ void load_sorted(const float* cand_v, const uint16_t* cand_c, int tid,
-                                            int cnt, float (&v)[N], int32_t (&ix)[N]) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const bool ok = i < cnt;
-    v[i] = ok ? cand_v[i * 128 + tid] : -INFINITY;
-    ix[i] = ok ? (int32_t)cand_c[i * 128 + tid] : 0x7fffffff;
-  }
-  bitonic_sort_pairs<N>(v, ix);
-}
 
 struct TcParams {
   int64_t B;
   int H, n_sub, d_h, k;
   int n_tile, n_chunks, k_blocks;
-  float* topv;
-  int32_t* topi;
+  float* cv;
+  int32_t* cc;
+  int32_t* cn;
 };
 
 template <int KT>
@@ -338,153 +255,153 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ---------------------------------------------------------- epilogue
+    // One thread per query row (TMEM lane).  Running group maxima over
+    // G = 2KT strided groups (g = column % G) give a lower bound tau on the
+    // row's KT-th score (the KT largest group maxima are KT distinct columns
+    // >= tau), valid for the whole row at every point of the stream; columns
+    // >= tau are kept in a shared-memory buffer that is compacted as tau
+    // rises.  A row whose buffer would overflow (massive exact ties) switches
+    // to an exact bitwise search for its KT-th score over buffer + segment.
     const int q = warp & 3;            // TMEM lane quarter of this warp
     const int row = q * 32 + lane;     // query row within the tile
     const int tid = row;               // candidate buffer column
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    float tv[KT];
-    int32_t ti[KT];
-#pragma unroll
-    for (int j = 0; j < KT; ++j) {
-      tv[j] = -INFINITY;
-      ti[j] = 0x7fffffff;
-    }
-    // Phase 1: the first n1 = min(n_sub, 2*n_tile) columns are resident in
-    // both TMEM buffers.  tau = KT-th largest of the 2KT strided group maxima
-    // (group g = columns c with c % 2KT == g) is a lower bound on the row's
-    // KT-th largest score, so every top-KT column has score >= tau.
-    const int n1_chunks = p.n_chunks < 2 ? p.n_chunks : 2;
-    const int n1 = n1_chunks * p.n_tile;
-    for (int c = 0; c < n1_chunks; ++c) mbar_wait(&tfull[c], 0);
-    tc_fence_after();
     constexpr int G = 2 * KT;
-    float tau;
-    {
-      float gm[G];
+    constexpr int STEP = G > 32 ? G : 32;
+    float gm[G];
 #pragma unroll
-      for (int j = 0; j < G; ++j) gm[j] = -INFINITY;
-      constexpr int STEP = G > 32 ? G : 32;  // columns per iteration (multiple of G or 32)
-      for (int c0 = 0; c0 < n1; c0 += STEP) {
+    for (int j = 0; j < G; ++j) gm[j] = -INFINITY;
+    int cnt = 0;
+    for (int c = 0; c < p.n_chunks;) {
+      const int nseg = (c == 0 && p.n_chunks >= 2) ? 2 : 1;  // first segment: both TMEM buffers
+      for (int u = 0; u < nseg; ++u) mbar_wait(&tfull[(c + u) & 1], ((c + u) >> 1) & 1);
+      tc_fence_after();
+      const int seg_cols = nseg * p.n_tile;
+      // TMEM address of segment column j
+      auto taddr = [&](int j) -> uint32_t {
+        return lane_base + (uint32_t)(((c + j / p.n_tile) & 1) * kMaxNTile + (j % p.n_tile));
+      };
+      // pass A: group maxima (segment start is a multiple of G)
+      for (int j0 = 0; j0 < seg_cols; j0 += STEP) {
 #pragma unroll
         for (int piece = 0; piece < STEP / 32; ++piece) {
-          const int col = c0 + piece * 32;
-          if (col < n1) {
+          const int j = j0 + piece * 32;
+          if (j < seg_cols) {
             uint32_t r[32];
-            tmem_ld32(lane_base + (col / p.n_tile) * kMaxNTile + (col % p.n_tile), r);
+            tmem_ld32(taddr(j), r);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int g = (piece * 32 + j) % G;  // == (col + j) % G since c0 % G == 0 or G | 32
-              gm[g] = fmaxf(gm[g], __uint_as_float(r[j]));
+            for (int jj = 0; jj < 32; ++jj) {
+              const int g = (piece * 32 + jj) % G;
+              gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
             }
           }
         }
       }
-      bitonic_sort_vals<G>(gm);
-      tau = gm[KT - 1];
-    }
-    // collect candidates >= tau (at most kCap buffered)
-    int cnt = 0;
-    bool overflow = false;
-    for (int col = 0; col < n1; col += 32) {
-      uint32_t r[32];
-      tmem_ld32(lane_base + (col / p.n_tile) * kMaxNTile + (col % p.n_tile), r);
+      float tau;
+      {
+        float t[G];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float v = __uint_as_float(r[j]);
-        if (v >= tau) {
-          if (cnt < kCap) {
-            cand_v[cnt * 128 + tid] = v;
-            cand_c[cnt * 128 + tid] = (uint16_t)(col + j);
-          } else {
-            overflow = true;
+        for (int j = 0; j < G; ++j) t[j] = gm[j];
+        bitonic_sort_vals<G>(t);
+        tau = t[KT - 1];
+      }
+      // compact the buffer to entries >= tau (order preserved)
+      {
+        const int mx = __reduce_max_sync(0xffffffffu, cnt);
+        int w = 0;
+        for (int i = 0; i < mx; ++i) {
+          if (i < cnt) {
+            const float v = cand_v[i * 128 + tid];
+            const uint16_t cc = cand_c[i * 128 + tid];
+            if (v >= tau) {
+              cand_v[w * 128 + tid] = v;
+              cand_c[w * 128 + tid] = cc;
+              ++w;
+            }
           }
-          ++cnt;
         }
+        cnt = w;
       }
-    }
-    if (__any_sync(0xffffffffu, overflow)) {
-      // rare (massive ties): exact insertion over every resident column
-      for (int col = 0; col < n1; col += 32) {
+      // pass B: collect segment columns >= tau
+      const int cnt_old = cnt;
+      const int col_base = c * p.n_tile;
+      for (int j0 = 0; j0 < seg_cols; j0 += 32) {
         uint32_t r[32];
-        tmem_ld32(lane_base + (col / p.n_tile) * kMaxNTile + (col % p.n_tile), r);
+        tmem_ld32(taddr(j0), r);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) topk_insert<KT>(tv, ti, __uint_as_float(r[j]), col + j, true);
-      }
-    } else {
-      const int mx = __reduce_max_sync(0xffffffffu, cnt);
-      if (mx <= 16) {
-        float cv[16]; int32_t ci[16];
-        load_sorted<16>(cand_v, cand_c, tid, cnt, cv, ci);
-        merge_top<KT, 16>(tv, ti, cv, ci);
-      } else if (mx <= 32) {
-        float cv[32]; int32_t ci[32];
-        load_sorted<32>(cand_v, cand_c, tid, cnt, cv, ci);
-        merge_top<KT, 32>(tv, ti, cv, ci);
-      } else {
-        float cv[64]; int32_t ci[64];
-        load_sorted<64>(cand_v, cand_c, tid, cnt, cv, ci);
-        merge_top<KT, 64>(tv, ti, cv, ci);
-      }
-    }
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0)
-      for (int c = 0; c < n1_chunks; ++c) mbar_arrive(&tempty[c]);
-    // Phase 2: remaining chunks stream through; candidates above the
-    // running KT-th score are buffered and merged in sorted batches.
-    cnt = 0;
-    auto flush = [&]() {
-      const int mx = __reduce_max_sync(0xffffffffu, cnt);
-      if (mx == 0) return;
-      if (mx <= 16) {
-        float cv[16]; int32_t ci[16];
-        load_sorted<16>(cand_v, cand_c, tid, cnt, cv, ci);
-        merge_top<KT, 16>(tv, ti, cv, ci);
-      } else if (mx <= 32) {
-        float cv[32]; int32_t ci[32];
-        load_sorted<32>(cand_v, cand_c, tid, cnt, cv, ci);
-        merge_top<KT, 32>(tv, ti, cv, ci);
-      } else {
-        float cv[64]; int32_t ci[64];
-        load_sorted<64>(cand_v, cand_c, tid, cnt, cv, ci);
-        merge_top<KT, 64>(tv, ti, cv, ci);
-      }
-      cnt = 0;
-    };
-    for (int c = n1_chunks; c < p.n_chunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&tfull[buf], (c >> 1) & 1);
-      tc_fence_after();
-      for (int sub = 0; sub < p.n_tile / 32; ++sub) {
-        uint32_t r[32];
-        tmem_ld32(lane_base + buf * kMaxNTile + sub * 32, r);
-        const int col0 = c * p.n_tile + sub * 32;
-        const float thr = tv[KT - 1];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float v = __uint_as_float(r[j]);
-          if (v > thr) {
-            cand_v[cnt * 128 + tid] = v;
-            cand_c[cnt * 128 + tid] = (uint16_t)(col0 + j);
+        for (int jj = 0; jj < 32; ++jj) {
+          const float v = __uint_as_float(r[jj]);
+          if (v >= tau) {
+            if (cnt < kCap) {
+              cand_v[cnt * 128 + tid] = v;
+              cand_c[cnt * 128 + tid] = (uint16_t)(col_base + j0 + jj);
+            }
             ++cnt;
           }
         }
-        if (__reduce_max_sync(0xffffffffu, cnt) > kCap - 32) flush();
+      }
+      if (__any_sync(0xffffffffu, cnt > kCap)) {
+        // exact path: the KT-th largest ordered key t over buffer u segment
+        auto count_ge = [&](uint32_t t) -> int {
+          int n = 0;
+          for (int i = 0; i < cnt_old; ++i) n += ord_f32(cand_v[i * 128 + tid]) >= t;
+          for (int j0 = 0; j0 < seg_cols; j0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(taddr(j0), r);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) n += ord_f32(__uint_as_float(r[jj])) >= t;
+          }
+          return n;
+        };
+        uint32_t t = 0;
+        for (int bit = 31; bit >= 0; --bit) {
+          const uint32_t cand = t | (1u << bit);
+          if (count_ge(cand) >= KT) t = cand;
+        }
+        const int gt = (t == 0xffffffffu) ? 0 : count_ge(t + 1);
+        int need = KT - gt;
+        int w = 0;
+        for (int i = 0; i < cnt_old; ++i) {
+          const float v = cand_v[i * 128 + tid];
+          const uint32_t o = ord_f32(v);
+          if (o > t || (o == t && need > 0)) {
+            if (o == t) --need;
+            cand_v[w * 128 + tid] = v;
+            cand_c[w * 128 + tid] = cand_c[i * 128 + tid];
+            ++w;
+          }
+        }
+        for (int j0 = 0; j0 < seg_cols; j0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr(j0), r);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const float v = __uint_as_float(r[jj]);
+            const uint32_t o = ord_f32(v);
+            if (o > t || (o == t && need > 0)) {
+              if (o == t) --need;
+              cand_v[w * 128 + tid] = v;
+              cand_c[w * 128 + tid] = (uint16_t)(col_base + j0 + jj);
+              ++w;
+            }
+          }
+        }
+        cnt = w;  // <= KT
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0)
+        for (int u = 0; u < nseg; ++u) mbar_arrive(&tempty[(c + u) & 1]);
+      c += nseg;
     }
-    flush();
     const int64_t b = m0 + row;
     if (b < p.B) {
-      const int64_t o = (b * p.H * 2 + hh) * (int64_t)p.k;
-#pragma unroll
-      for (int j = 0; j < KT; ++j)
-        if (j < p.k) {
-          p.topv[o + j] = tv[j];
-          p.topi[o + j] = ti[j];
-        }
+      const int64_t rr = b * p.H * 2 + hh;
+      for (int i = 0; i < cnt; ++i) {
+        p.cv[rr * kCandCap + i] = cand_v[i * 128 + tid];
+        p.cc[rr * kCandCap + i] = (int32_t)cand_c[i * 128 + tid];
+      }
+      p.cn[rr] = cnt;
     }
   }
   tc_fence_before();
@@ -549,8 +466,8 @@ bool select_tc_supported(const Shape& s) {
   return get_encode() != nullptr;
 }
 
-cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, float* topv,
-                             int32_t* topi, cudaStream_t st, int* launches) {
+cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
+                             cudaStream_t st, int* launches) {
   if (!select_tc_supported(s)) return cudaErrorNotSupported;
   EncodeTiledFn enc = get_encode();
   CUtensorMap mq, mk;
@@ -577,7 +494,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, float
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / kBlockK, topv, topi};
+  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / kBlockK, cd.v, cd.c, cd.n};
   cudaError_t e;
   if (s.k <= 8) e = launch_kt<8>(s, mq, mk, p, st);
   else if (s.k <= 16) e = launch_kt<16>(s, mq, mk, p, st);
