@@ -26,24 +26,24 @@ namespace {
 constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 2048
-constexpr int RS_BITS = 8;
-constexpr int RS_BUCKETS = 1 << RS_BITS;
+constexpr int RS_MAX_BITS = 11;  // digit width <= 11 bits (<= 2048 buckets)
 
 __global__ void __launch_bounds__(RS_THREADS) rs_hist_kernel(const uint32_t* __restrict__ keys,
-                                                             int64_t n, int shift,
+                                                             int64_t n, int shift, int nb,
                                                              uint32_t* __restrict__ hist,
                                                              int nblocks) {
-  __shared__ uint32_t cnt[RS_BUCKETS];
-  cnt[threadIdx.x] = 0;
+  extern __shared__ uint32_t cnt[];  // nb
+  for (int d = threadIdx.x; d < nb; d += RS_THREADS) cnt[d] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+  const uint32_t mask = (uint32_t)nb - 1u;
 #pragma unroll
   for (int i = 0; i < RS_ITEMS; ++i) {
     const int64_t p = base + i * RS_THREADS + threadIdx.x;
-    if (p < n) atomicAdd(&cnt[(keys[p] >> shift) & (RS_BUCKETS - 1)], 1u);
+    if (p < n) atomicAdd(&cnt[(keys[p] >> shift) & mask], 1u);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+  for (int d = threadIdx.x; d < nb; d += RS_THREADS) hist[(int64_t)d * nblocks + blockIdx.x] = cnt[d];
 }
 
 // Exclusive scan of the digit-major histogram in three coalesced phases:
@@ -145,13 +145,16 @@ cudaError_t excl_scan(uint32_t* data, int64_t len, uint32_t* part, cudaStream_t 
 // warp match-any; warp totals are scanned per digit across the 8 warps.
 __global__ void __launch_bounds__(RS_THREADS) rs_scatter_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, int64_t n, int shift,
-    const uint32_t* __restrict__ offs, int nblocks, uint32_t* __restrict__ keys_out,
+    int nb, const uint32_t* __restrict__ offs, int nblocks, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out) {
   constexpr int NW = RS_THREADS / 32;
-  __shared__ uint32_t cnt[NW][RS_BUCKETS + 1];
+  extern __shared__ uint32_t cnt_raw[];  // [NW][nb + 1]
+  const int stride_w = nb + 1;
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < NW * (RS_BUCKETS + 1); i += RS_THREADS) (&cnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NW * stride_w; i += RS_THREADS) cnt_raw[i] = 0;
   __syncthreads();
+  uint32_t* cntw = cnt_raw + wid * stride_w;
+  const uint32_t mask = (uint32_t)nb - 1u;
   const int64_t base = (int64_t)blockIdx.x * RS_TILE + wid * (32 * RS_ITEMS);
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t key[RS_ITEMS], val[RS_ITEMS], dig[RS_ITEMS], rank[RS_ITEMS];
@@ -161,31 +164,30 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_kernel(
     const bool ok = p < n;
     key[j] = ok ? keys_in[p] : 0u;
     val[j] = ok ? (vals_in ? vals_in[p] : (uint32_t)p) : 0u;
-    dig[j] = ok ? ((key[j] >> shift) & (RS_BUCKETS - 1)) : RS_BUCKETS;
+    dig[j] = ok ? ((key[j] >> shift) & mask) : (uint32_t)nb;
     const uint32_t peers = __match_any_sync(0xffffffffu, dig[j]);
     const int leader = __ffs(peers) - 1;
-    const uint32_t before = cnt[wid][dig[j]];
+    const uint32_t before = cntw[dig[j]];
     rank[j] = before + __popc(peers & lt);
     __syncwarp();
-    if (lane == leader) cnt[wid][dig[j]] = before + __popc(peers);
+    if (lane == leader) cntw[dig[j]] = before + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  {  // exclusive scan across warps, per digit
-    const int d = threadIdx.x;
+  for (int d = threadIdx.x; d < nb; d += RS_THREADS) {  // exclusive scan across warps, per digit
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const uint32_t c = cnt[w][d];
-      cnt[w][d] = run;
+      const uint32_t c = cnt_raw[w * stride_w + d];
+      cnt_raw[w * stride_w + d] = run;
       run += c;
     }
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
-    if (dig[j] == RS_BUCKETS) continue;
-    const uint32_t pos = offs[(int64_t)dig[j] * nblocks + blockIdx.x] + cnt[wid][dig[j]] + rank[j];
+    if (dig[j] == (uint32_t)nb) continue;
+    const uint32_t pos = offs[(int64_t)dig[j] * nblocks + blockIdx.x] + cntw[dig[j]] + rank[j];
     keys_out[pos] = key[j];
     vals_out[pos] = val[j];
   }
@@ -203,17 +205,29 @@ cudaError_t radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uin
                        uint32_t* hist, int64_t n, uint32_t max_key, cudaStream_t st, int* launches,
                        uint32_t** keys_res, uint32_t** vals_res) {
   const int bits = bits_for(max_key);
-  const int passes = (bits + RS_BITS - 1) / RS_BITS;
   const int nblocks = (int)((n + RS_TILE - 1) / RS_TILE);
+  // digit width: <= 11 bits and a histogram of <= 2^20 entries, balanced over the passes
+  int wmax = RS_MAX_BITS;
+  while (wmax > 4 && ((int64_t)nblocks << wmax) > (int64_t(1) << 20)) --wmax;
+  const int passes = (bits + wmax - 1) / wmax;
+  const int width = (bits + passes - 1) / passes;
+  const int nb = 1 << width;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (RS_THREADS / 32) * ((1 << RS_MAX_BITS) + 1) * 4);
+    attr = true;
+  }
+  const size_t smem_scatter = (size_t)(RS_THREADS / 32) * (nb + 1) * 4;
   uint32_t *kin = keys_a, *vin = nullptr, *kout = keys_b, *vout = vals_b;
   for (int p = 0; p < passes; ++p) {
-    const int shift = p * RS_BITS;
-    rs_hist_kernel<<<nblocks, RS_THREADS, 0, st>>>(kin, n, shift, hist, nblocks);
-    const int64_t hl = (int64_t)RS_BUCKETS * nblocks;
+    const int shift = p * width;
+    rs_hist_kernel<<<nblocks, RS_THREADS, nb * 4, st>>>(kin, n, shift, nb, hist, nblocks);
+    const int64_t hl = (int64_t)nb * nblocks;
     cudaError_t e = excl_scan(hist, hl, hist + hl, st, launches);
     if (e != cudaSuccess) return e;
-    rs_scatter_kernel<<<nblocks, RS_THREADS, 0, st>>>(kin, vin, n, shift, hist, nblocks, kout,
-                                                     vout);
+    rs_scatter_kernel<<<nblocks, RS_THREADS, smem_scatter, st>>>(kin, vin, n, shift, nb, hist,
+                                                                nblocks, kout, vout);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     *launches += 2;
@@ -258,7 +272,6 @@ __device__ __forceinline__ void add_store_slice(float* p, const float* a) {
 // MODE_DK : record = 2*cid + half,   weight = dsS[rec],  x = Q[b,h,half,:],    G = dK rows (h,half,i)
 enum { MODE_DV = 0, MODE_DK = 1 };
 constexpr int SEG_T = 64;  // entries per warp tile
-constexpr int SEG_U = 4;   // entries prefetched per step
 
 struct SegArgs {
   const uint32_t* keys;   // sorted rows (>= nrows: skip)
@@ -287,101 +300,228 @@ __device__ __forceinline__ const XT* x_row(const SegArgs& a, uint32_t rec) {
   }
 }
 
+// Raw 16-byte vectors of a row slice of EPL elements of T (prefetched as
+// bytes, converted when consumed).
+template <typename T, int EPL>
+struct RawSlice {
+  static constexpr int BYTES = EPL * (int)sizeof(T);
+  static constexpr int NV = BYTES >= 16 ? BYTES / 16 : 1;
+  uint4 v[NV];
+  __device__ __forceinline__ void load(const T* p) {
+    if constexpr (BYTES >= 16) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[i] = ldg_v4(reinterpret_cast<const char*>(p) + 16 * i);
+    } else {
+      uint32_t w[4] = {0, 0, 0, 0};
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(p);
+      if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) w[i] = reinterpret_cast<const uint32_t*>(p)[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) w[i / 2] |= (uint32_t)h[i] << (16 * (i % 2));
+      }
+      v[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ void to_float(float* f) const {
+    if constexpr (BYTES >= 16) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) unpack16<T>(v[i], f + i * elem<T>::per16);
+    } else {
+      float t[16 / sizeof(T)];
+      unpack16<T>(v[0], t);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) f[i] = t[i];
+    }
+  }
+};
+
+// Batched butterfly: U per-lane partial sums -> full warp sums, with
+// (U - 1) + log2(32 / U) shuffles instead of 5U.  Dot u ends in lane
+// u * (32 / U) (fixed order: deterministic).
+template <int U>
+__device__ __forceinline__ float multi_warp_sum(float (&d)[U]) {
+  const int lane = threadIdx.x % 32;
+  float v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = d[u];
+  int n = U;
+#pragma unroll
+  for (int m = 16; m >= 32 / U; m >>= 1) {
+    // keep half of the n values, send the other half to lane ^ m
+    const bool hi = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < U / 2; ++i) {
+      if (i < n / 2) {
+        const float keep = hi ? v[i + n / 2] : v[i];
+        const float send = hi ? v[i] : v[i + n / 2];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    n >>= 1;
+  }
+  float r = v[0];
+#pragma unroll
+  for (int m = 32 / U / 2; m > 0; m >>= 1) r += __shfl_xor_sync(0xffffffffu, r, m);
+  return r;
+}
+
+// Staged entry of a tile: key (row), record id, weight, x-row index and flags.
+struct SegEntry {
+  uint32_t key, rec;
+  float wt;
+  uint32_t xrow_flags;  // bits 0..29 x row, bit 30 starts_here, bit 31 new_run
+};
+constexpr uint32_t SF_NEW = 0x80000000u, SF_START = 0x40000000u, SF_XROW = 0x3fffffffu;
+
+// One warp per tile of SEG_T sorted entries.  The tile's entries are staged
+// in shared memory (row, record, weight, x-row index, run flags computed
+// once), then consumed in groups of U: all loads of a group (x rows, value
+// rows at run starts, gradient rows of runs that start in this tile) are
+// issued before any is used.  Complete runs update the gradient row once
+// (G = G + sum, in record order); runs that cross a tile boundary leave
+// per-tile partials for seg_fixup_kernel.
 template <int MODE, typename XT, typename YT, int EPL>
 __global__ void __launch_bounds__(256) segreduce_kernel(SegArgs a) {
-  const int lane = threadIdx.x % 32;
+  constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
+  __shared__ SegEntry stage[8][SEG_T];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t s = tile * SEG_T;
   if (s >= a.n) return;
   const int64_t e = s + SEG_T < a.n ? s + SEG_T : a.n;
   const int cnt = (int)(e - s);
-  uint32_t rk[SEG_T / 32], rr[SEG_T / 32];
-#pragma unroll
-  for (int u = 0; u < SEG_T / 32; ++u) {
-    const int64_t p = s + lane + 32 * u;
-    rk[u] = p < e ? a.keys[p] : 0xffffffffu;
-    rr[u] = p < e ? a.recs[p] : 0u;
-  }
+  if (a.keys[s] >= a.nrows) return;  // sorted: the rest of the array is sentinels
   const uint32_t prev_key = s > 0 ? a.keys[s - 1] : 0xffffffffu;
   const uint32_t next_key = e < a.n ? a.keys[e] : 0xffffffffu;
+  {
+    uint32_t k2[SEG_T / 32];
+#pragma unroll
+    for (int u = 0; u < SEG_T / 32; ++u) {
+      const int j = lane + 32 * u;
+      k2[u] = j < cnt ? a.keys[s + j] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int u = 0; u < SEG_T / 32; ++u) {
+      const int j = lane + 32 * u;
+      uint32_t pk = __shfl_up_sync(0xffffffffu, k2[u], 1);
+      const uint32_t wrap = u > 0 ? __shfl_sync(0xffffffffu, k2[u > 0 ? u - 1 : 0], 31) : prev_key;
+      if (lane == 0) pk = wrap;
+      if (j < cnt) {
+        const uint32_t kk = k2[u];
+        const uint32_t rec = a.recs[s + j];
+        const bool valid = kk < a.nrows;
+        uint32_t xrow;
+        if constexpr (MODE == MODE_DV) xrow = rec / (uint32_t)(a.H * a.k);
+        else xrow = (rec >> 1) / (uint32_t)a.k * 2u + (rec & 1u);
+        const bool newrun = (j == 0) || kk != pk;
+        const bool starts = (j == 0) ? (s == 0 || prev_key != kk) : newrun;
+        SegEntry en;
+        en.key = kk;
+        en.rec = rec;
+        en.wt = valid ? a.wts[rec] : 0.f;
+        en.xrow_flags = (xrow & SF_XROW) | (newrun ? SF_NEW : 0u) | (starts ? SF_START : 0u);
+        stage[wid][j] = en;
+      }
+    }
+  }
+  __syncwarp();
 
-  float acc[EPL];
-  float y[EPL];
+  float acc[EPL], gcur[EPL];
+  RawSlice<YT, EPL> ycur;
   uint32_t cur = 0xffffffffu;
-  int run_start = 0;
-  auto flush = [&](int run_end) {
+  bool cur_starts = false;
+  auto flush = [&](bool ends_here) {
     if (cur >= a.nrows) return;
-    const bool starts_here = run_start > 0 || s == 0 || prev_key != cur;
-    const bool ends_here = run_end < cnt || e == a.n || next_key != cur;
-    float* dst;
-    if (starts_here && ends_here) {
-      dst = a.G + (int64_t)cur * a.D + lane * EPL;
-      add_store_slice<EPL>(dst, acc);
+    if (cur_starts && ends_here) {
+      float* dst = a.G + (int64_t)cur * a.D + lane * EPL;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) dst[i] = gcur[i] + acc[i];
       return;
     }
-    dst = (!starts_here ? a.part_first : a.part_last) + tile * a.D + lane * EPL;
+    float* dst = (!cur_starts ? a.part_first : a.part_last) + tile * a.D + lane * EPL;
 #pragma unroll
     for (int i = 0; i < EPL; ++i) dst[i] = acc[i];
   };
-  for (int j0 = 0; j0 < cnt; j0 += SEG_U) {
-    uint32_t key[SEG_U], rec[SEG_U];
-    float x[SEG_U][EPL];
-    float yp[MODE == MODE_DV ? SEG_U : 1][EPL];
-    float wt[SEG_U];
+  for (int j0 = 0; j0 < cnt; j0 += U) {
+    SegEntry en[U];
+    RawSlice<XT, EPL> xr[U];
+    RawSlice<YT, EPL> yr[MODE == MODE_DV ? U : 1];
+    float gp[U][EPL];
 #pragma unroll
-    for (int u = 0; u < SEG_U; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int j = j0 + u;
-      const int src = j % 32;
-      uint32_t kk = 0xffffffffu, rr_ = 0;
+      if (j < cnt) en[u] = stage[wid][j];
+      else en[u] = SegEntry{0xffffffffu, 0u, 0.f, 0u};
+      const bool valid = en[u].key < a.nrows;
+      if (valid) {
+        xr[u].load(reinterpret_cast<const XT*>(a.X) + (int64_t)(en[u].xrow_flags & SF_XROW) * a.D + lane * EPL);
+        if constexpr (MODE == MODE_DV) {
+          if (en[u].xrow_flags & SF_NEW)
+            yr[u].load(reinterpret_cast<const YT*>(a.Y) + (int64_t)en[u].key * a.D + lane * EPL);
+        }
+        if (en[u].xrow_flags & SF_START) {
+          const float* g = a.G + (int64_t)en[u].key * a.D + lane * EPL;
+          if constexpr (EPL % 4 == 0) {
 #pragma unroll
-      for (int q = 0; q < SEG_T / 32; ++q) {
-        const uint32_t k2 = __shfl_sync(0xffffffffu, rk[q], src);
-        const uint32_t r2 = __shfl_sync(0xffffffffu, rr[q], src);
-        if (j / 32 == q) { kk = k2; rr_ = r2; }
-      }
-      if (j >= cnt) kk = 0xffffffffu;
-      key[u] = kk;
-      rec[u] = rr_;
-      const bool valid = kk < a.nrows;
-      wt[u] = valid ? a.wts[rr_] : 0.f;
-      if (valid) load_slice<XT, EPL>(x_row<MODE, XT, YT, EPL>(a, rr_) + lane * EPL, x[u]);
-      else
+            for (int i = 0; i < EPL; i += 4) {
+              const float4 t = *reinterpret_cast<const float4*>(g + i);
+              gp[u][i] = t.x; gp[u][i + 1] = t.y; gp[u][i + 2] = t.z; gp[u][i + 3] = t.w;
+            }
+          } else {
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) x[u][i] = 0.f;
-      if constexpr (MODE == MODE_DV) {
-        // prefetch the value row too (repeats within a run hit L1)
-        if (valid)
-          load_slice<YT, EPL>(reinterpret_cast<const YT*>(a.Y) + (int64_t)kk * a.D + lane * EPL, yp[u]);
+            for (int i = 0; i < EPL; ++i) gp[u][i] = g[i];
+          }
+        }
+      } else {
+        xr[u].zero();
       }
     }
+    float d[U];
 #pragma unroll
-    for (int u = 0; u < SEG_U; ++u) {
-      const int j = j0 + u;
-      if (j >= cnt) break;
-      if (key[u] != cur) {
-        flush(j);
-        cur = key[u];
-        run_start = j;
+    for (int u = 0; u < U; ++u) {
+      d[u] = 0.f;
+      if (j0 + u >= cnt) continue;
+      if (en[u].xrow_flags & SF_NEW) {
+        flush(true);
+        cur = en[u].key;
+        cur_starts = (en[u].xrow_flags & SF_START) != 0;
 #pragma unroll
         for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
-        if constexpr (MODE == MODE_DV) {
+        if (cur_starts) {
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) y[i] = yp[u][i];
+          for (int i = 0; i < EPL; ++i) gcur[i] = gp[u][i];
         }
+        if constexpr (MODE == MODE_DV) ycur = yr[u];
       }
       if (cur >= a.nrows) continue;
+      float x[EPL];
+      xr[u].to_float(x);
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] = fmaf(wt[u], x[u][i], acc[i]);
+      for (int i = 0; i < EPL; ++i) acc[i] = fmaf(en[u].wt, x[i], acc[i]);
       if constexpr (MODE == MODE_DV) {
-        float d = 0.f;
+        float y[EPL];
+        ycur.to_float(y);
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) d = fmaf(y[i], x[u][i], d);
-        d = warp_sum(d);
-        if (lane == 0) a.dots[rec[u]] = d;
+        for (int i = 0; i < EPL; ++i) d[u] = fmaf(y[i], x[i], d[u]);
+      }
+    }
+    if constexpr (MODE == MODE_DV) {
+      const float r = multi_warp_sum<U>(d);
+      const int u = lane / (32 / U);
+      if ((lane % (32 / U)) == 0) {
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu)
+          if (uu == u && j0 + uu < cnt && en[uu].key < a.nrows) a.dots[en[uu].rec] = r;
       }
     }
   }
-  flush(cnt);
+  flush(e == a.n || next_key != cur);
 }
 
 // Runs that cross tiles: the tile where the run starts (its "last" partial)
@@ -590,7 +730,7 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   const int64_t D = s.d_v > s.d_h ? s.d_v : s.d_h;
   size_t b = 0;
   b += 4 * align256(sizeof(uint32_t) * n);
-  b += align256(sizeof(uint32_t) * (RS_BUCKETS * nblocks + 1024));
+  b += align256(sizeof(uint32_t) * ((int64_t(1) << 20) + (int64_t(1) << RS_MAX_BITS) * 0 + 1024 + 2048 * nblocks));
   b += 2 * align256(sizeof(float) * tiles * D);
   b += align256(sizeof(float) * n_dk);
   b += align256(sizeof(float) * n_dv);
@@ -610,7 +750,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.keys_b = (uint32_t*)p; p += align256(sizeof(uint32_t) * n);
   w.vals_a = (uint32_t*)p; p += align256(sizeof(uint32_t) * n);
   w.vals_b = (uint32_t*)p; p += align256(sizeof(uint32_t) * n);
-  w.hist = (uint32_t*)p; p += align256(sizeof(uint32_t) * (RS_BUCKETS * nblocks + 1024));
+  w.hist = (uint32_t*)p; p += align256(sizeof(uint32_t) * ((int64_t(1) << 20) + (int64_t(1) << RS_MAX_BITS) * 0 + 1024 + 2048 * nblocks));
   w.part_first = (float*)p; p += align256(sizeof(float) * tiles * D);
   w.part_last = (float*)p; p += align256(sizeof(float) * tiles * D);
   w.dsS = (float*)p; p += align256(sizeof(float) * n_dk);
