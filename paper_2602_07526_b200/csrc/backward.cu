@@ -387,7 +387,7 @@ constexpr uint32_t SF_NEW = 0x80000000u, SF_START = 0x40000000u, SF_XROW = 0x3ff
 // (G = G + sum, in record order); runs that cross a tile boundary leave
 // per-tile partials for seg_fixup_kernel.
 template <int MODE, typename XT, typename YT, int EPL>
-__global__ void __launch_bounds__(256) segreduce_kernel(SegArgs a) {
+__global__ void __launch_bounds__(256, 2) segreduce_kernel(SegArgs a) {
   constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   __shared__ SegEntry stage[8][SEG_T];
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -599,7 +599,10 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     float* __restrict__ dQ,
                                                     uint32_t* __restrict__ rkeys,
                                                     float* __restrict__ dsS, uint32_t sentinel) {
-  const int lane = threadIdx.x % 32;
+  constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
+  __shared__ int32_t s_r[8][64];
+  __shared__ float s_d[8][64];
+  const int lane = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (l >= L) return;
   const int h = (int)(l % H);
@@ -648,22 +651,41 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
         dsS[rec] = dS[u];
       }
     }
-    // dQ: lanes over d_h
+    // dQ: lanes over d_h.  The distinct sub-keys of this half are compacted
+    // into shared memory (first-occurrence order) and their K rows are
+    // loaded DQ_U at a time, all loads of a group in flight together.
+    int m = 0;
+#pragma unroll
+    for (int u = 0; u < KPL; ++u) {
+      const int t = lane + 32 * u;
+      const bool fl = t < k && first[u];
+      const unsigned bm = __ballot_sync(0xffffffffu, fl);
+      if (fl) {
+        const int pos = m + __popc(bm & ((1u << lane) - 1u));
+        s_r[wid][pos] = r[u];
+        s_d[wid][pos] = dS[u];
+      }
+      m += __popc(bm);
+    }
+    __syncwarp();
     float acc[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
-    for (int v = 0; v < k; ++v) {
-      const int src = v % 32;
-      const bool lo = KPL == 1 || v < 32;
-      const int rv = __shfl_sync(0xffffffffu, lo ? r[0] : r[KPL - 1], src);
-      const float dSv = __shfl_sync(0xffffffffu, lo ? dS[0] : dS[KPL - 1], src);
-      const bool fv = __shfl_sync(0xffffffffu, (int)(lo ? first[0] : first[KPL - 1]), src);
-      if (!fv) continue;
-      float kr[EPL];
-      load_slice<QT, EPL>(K + ((int64_t)(h * 2 + half) * n_sub + rv) * d_h + lane * EPL, kr);
+    const QT* Kh = K + (int64_t)(h * 2 + half) * n_sub * d_h + lane * EPL;
+    for (int b0 = 0; b0 < m; b0 += DQ_U) {
+      float kr[DQ_U][EPL];
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] = fmaf(dSv, kr[i], acc[i]);
+      for (int u = 0; u < DQ_U; ++u)
+        if (b0 + u < m) load_slice<QT, EPL>(Kh + (int64_t)s_r[wid][b0 + u] * d_h, kr[u]);
+#pragma unroll
+      for (int u = 0; u < DQ_U; ++u)
+        if (b0 + u < m) {
+          const float dSv = s_d[wid][b0 + u];
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(dSv, kr[u][i], acc[i]);
+        }
     }
+    __syncwarp();
     float* o = dQ + (l * 2 + half) * d_h + lane * EPL;
 #pragma unroll
     for (int i = 0; i < EPL; ++i) o[i] = acc[i];

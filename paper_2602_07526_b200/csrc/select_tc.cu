@@ -119,6 +119,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Two x32 loads, one wait: 64 consecutive columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]),
+        "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]),
+        "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]),
+        "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]),
+        "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr + 32));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Shared-memory matrix descriptor: K-major operand in 128-byte swizzled rows
 // (8-row atoms of 1024 B): start>>4, LBO=1 (unused for swizzled K-major),
 // SBO=1024>>4, version 1 (sm_100), layout SWIZZLE_128B (2).
@@ -173,8 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
   float* cand_v = reinterpret_cast<float*>(sB + kStages * p.n_tile * 128);
-  uint16_t* cand_c = reinterpret_cast<uint16_t*>(cand_v + kCap * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cand_c + kCap * 128);  // 8-aligned: kCap*128*6
+  uint16_t* cand_c = reinterpret_cast<uint16_t*>(cand_v + (kCap + 1) * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cand_c + (kCap + 1) * 128);  // 8-aligned: (kCap+1)*128*6
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + kStages;
@@ -282,17 +305,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         return lane_base + (uint32_t)(((c + j / p.n_tile) & 1) * kMaxNTile + (j % p.n_tile));
       };
       // pass A: group maxima (segment start is a multiple of G)
-      for (int j0 = 0; j0 < seg_cols; j0 += STEP) {
+      if (seg_cols % 64 == 0) {
+        for (int j0 = 0; j0 < seg_cols; j0 += 64) {
+          uint32_t r[64];
+          tmem_ld64(taddr(j0), r);  // j0 % n_tile + 64 <= n_tile since n_tile % 64 == 0
 #pragma unroll
-        for (int piece = 0; piece < STEP / 32; ++piece) {
-          const int j = j0 + piece * 32;
-          if (j < seg_cols) {
-            uint32_t r[32];
-            tmem_ld32(taddr(j), r);
+          for (int jj = 0; jj < 64; ++jj) {
+            const int g = jj % G;  // == (col) % G: j0 % 64 == 0 and G | 64
+            gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
+          }
+        }
+      } else {
+        for (int j0 = 0; j0 < seg_cols; j0 += STEP) {
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              const int g = (piece * 32 + jj) % G;
-              gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
+          for (int piece = 0; piece < STEP / 32; ++piece) {
+            const int j = j0 + piece * 32;
+            if (j < seg_cols) {
+              uint32_t r[32];
+              tmem_ld32(taddr(j), r);
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj) {
+                const int g = (piece * 32 + jj) % G;
+                gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
+              }
             }
           }
         }
@@ -322,7 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         cnt = w;
       }
-      // pass B: collect segment columns >= tau
+      // pass B: collect segment columns >= tau (branch-free: unselected
+      // columns and overflow go to the dummy row kCap)
       const int cnt_old = cnt;
       const int col_base = c * p.n_tile;
       for (int j0 = 0; j0 < seg_cols; j0 += 32) {
@@ -331,13 +367,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const float v = __uint_as_float(r[jj]);
-          if (v >= tau) {
-            if (cnt < kCap) {
-              cand_v[cnt * 128 + tid] = v;
-              cand_c[cnt * 128 + tid] = (uint16_t)(col_base + j0 + jj);
-            }
-            ++cnt;
-          }
+          const bool sel = v >= tau;
+          const int slot = sel ? min(cnt, kCap) : kCap;
+          cand_v[slot * 128 + tid] = v;
+          cand_c[slot * 128 + tid] = (uint16_t)(col_base + j0 + jj);
+          cnt += sel ? 1 : 0;
         }
       }
       if (__any_sync(0xffffffffu, cnt > kCap)) {
@@ -435,7 +469,7 @@ int n_tile_for(int n_sub) { return n_sub < kMaxNTile ? n_sub : kMaxNTile; }
 size_t smem_bytes(const Shape& s) {
   const int nt = n_tile_for(s.n_sub);
   return 1024 + (size_t)(s.d_h / kBlockK) * 16384 + (size_t)kStages * nt * 128 +
-         (size_t)kCap * 128 * (4 + 2) + 8 * (1 + 2 * kStages + 4) + 16;
+         (size_t)(kCap + 1) * 128 * (4 + 2) + 8 * (1 + 2 * kStages + 4) + 16;
 }
 
 template <int KT>
