@@ -240,30 +240,30 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         Qh = Q.cpu().pin_memory()
         dOh = dOut.cpu().pin_memory()
+        out_h = torch.empty((B, cfg.d_value), dtype=torch.float32).pin_memory()
+        dq_h = torch.empty((B, cfg.heads, 2, cfg.d_half), dtype=torch.float32).pin_memory()
         n_e2e = max(3, min(args.steps, 20))
-        for _ in range(2):
-            o_, i_, w_ = lk.forward(Qh, K, V)
-            lk.backward(dOh, Qh, K, V, i_.to(dev), w_.to(dev), d_subkeys=dK, d_values=dV)
+        for _ in range(3):
+            lk.step_host(Qh, dOh, K, V, dK, dV, out_h, dq_h)
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
         for i in range(n_e2e):
             flush.zero_()
             ev[i][0].record(stream)
-            o_h, i_d, w_d = lk.forward(Qh, K, V)        # H2D q, D2H out (+ idx/w tape)
-            dq_h, _, _, _ = lk.backward(dOh, Qh, K, V, i_d, w_d, d_subkeys=dK, d_values=dV)  # H2D dOut, D2H dQ
+            lk.step_host(Qh, dOh, K, V, dK, dV, out_h, dq_h)   # H2D q, dOut; D2H out, dQ
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         e2e_ms = sum(a.elapsed_time(b) for a, b in ev) / n_e2e
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        h2d = Qh.numel() * Qh.element_size() * 2 + dOh.numel() * dOh.element_size() + idx.numel() * 8
-        d2h = out.numel() * 4 + idx.numel() * 4 + w.numel() * 4 + dQ.numel() * 4
+        h2d = Qh.numel() * Qh.element_size() + dOh.numel() * dOh.element_size()
+        d2h = out_h.numel() * 4 + dq_h.numel() * 4
         e2e = {"value": lookups / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.item()),
-               "note": "PKMLookup.forward/backward with pinned host query and d_out; host copies of "
-                       "out, idx, w, d_query; the query is copied for forward and again for backward, the idx/w tape goes back to the device"}
+               "note": "PKMLookup.step_host: pinned host query + d_out in, out + d_query back to pinned host, "
+                       "forward+backward through msn_pkm_forward/msn_pkm_backward, one sync"}
 
     if rank != 0:
         return None

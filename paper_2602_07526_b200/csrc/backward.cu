@@ -372,7 +372,7 @@ __device__ __forceinline__ float multi_warp_sum(float (&d)[U]) {
 }
 
 // Staged entry of a tile: key (row), record id, weight, x-row index and flags.
-struct SegEntry {
+struct __align__(16) SegEntry {
   uint32_t key, rec;
   float wt;
   uint32_t xrow_flags;  // bits 0..29 x row, bit 30 starts_here, bit 31 new_run
@@ -436,17 +436,31 @@ __global__ void __launch_bounds__(256, 2) segreduce_kernel(SegArgs a) {
   RawSlice<YT, EPL> ycur;
   uint32_t cur = 0xffffffffu;
   bool cur_starts = false;
-  auto flush = [&](bool ends_here) {
-    if (cur >= a.nrows) return;
-    if (cur_starts && ends_here) {
-      float* dst = a.G + (int64_t)cur * a.D + lane * EPL;
+  const uint32_t nrows = a.nrows;
+  const int64_t D = a.D;
+  const XT* __restrict__ Xl = reinterpret_cast<const XT*>(a.X) + lane * EPL;
+  const YT* __restrict__ Yl = reinterpret_cast<const YT*>(a.Y) + lane * EPL;
+  float* __restrict__ Gl = a.G + lane * EPL;
+  auto store_row = [&](float* dst, const float* v) {
+    if constexpr (EPL % 4 == 0) {
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) dst[i] = gcur[i] + acc[i];
+      for (int i = 0; i < EPL; i += 4)
+        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) dst[i] = v[i];
+    }
+  };
+  auto flush = [&](bool ends_here) {
+    if (cur >= nrows) return;
+    if (cur_starts && ends_here) {
+      float t[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) t[i] = gcur[i] + acc[i];
+      store_row(Gl + (int64_t)cur * D, t);
       return;
     }
-    float* dst = (!cur_starts ? a.part_first : a.part_last) + tile * a.D + lane * EPL;
-#pragma unroll
-    for (int i = 0; i < EPL; ++i) dst[i] = acc[i];
+    store_row((!cur_starts ? a.part_first : a.part_last) + tile * D + lane * EPL, acc);
   };
   for (int j0 = 0; j0 < cnt; j0 += U) {
     SegEntry en[U];
@@ -458,15 +472,14 @@ __global__ void __launch_bounds__(256, 2) segreduce_kernel(SegArgs a) {
       const int j = j0 + u;
       if (j < cnt) en[u] = stage[wid][j];
       else en[u] = SegEntry{0xffffffffu, 0u, 0.f, 0u};
-      const bool valid = en[u].key < a.nrows;
+      const bool valid = en[u].key < nrows;
       if (valid) {
-        xr[u].load(reinterpret_cast<const XT*>(a.X) + (int64_t)(en[u].xrow_flags & SF_XROW) * a.D + lane * EPL);
+        xr[u].load(Xl + (int64_t)(en[u].xrow_flags & SF_XROW) * D);
         if constexpr (MODE == MODE_DV) {
-          if (en[u].xrow_flags & SF_NEW)
-            yr[u].load(reinterpret_cast<const YT*>(a.Y) + (int64_t)en[u].key * a.D + lane * EPL);
+          if (en[u].xrow_flags & SF_NEW) yr[u].load(Yl + (int64_t)en[u].key * D);
         }
         if (en[u].xrow_flags & SF_START) {
-          const float* g = a.G + (int64_t)en[u].key * a.D + lane * EPL;
+          const float* g = Gl + (int64_t)en[u].key * D;
           if constexpr (EPL % 4 == 0) {
 #pragma unroll
             for (int i = 0; i < EPL; i += 4) {
@@ -478,8 +491,6 @@ __global__ void __launch_bounds__(256, 2) segreduce_kernel(SegArgs a) {
             for (int i = 0; i < EPL; ++i) gp[u][i] = g[i];
           }
         }
-      } else {
-        xr[u].zero();
       }
     }
     float d[U];
@@ -499,7 +510,7 @@ __global__ void __launch_bounds__(256, 2) segreduce_kernel(SegArgs a) {
         }
         if constexpr (MODE == MODE_DV) ycur = yr[u];
       }
-      if (cur >= a.nrows) continue;
+      if (cur >= nrows) continue;
       float x[EPL];
       xr[u].to_float(x);
 #pragma unroll
@@ -531,6 +542,8 @@ __global__ void __launch_bounds__(256) seg_fixup_kernel(const uint32_t* __restri
                                                         const float* __restrict__ part_first,
                                                         const float* __restrict__ part_last,
                                                         float* __restrict__ G, int D) {
+  // one warp per tile; only tiles where a run starts and continues into the
+  // next tile do work: they sum the following tiles' partials in tile order
   const int lane = threadIdx.x % 32;
   const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t s = tile * SEG_T;
@@ -539,14 +552,13 @@ __global__ void __launch_bounds__(256) seg_fixup_kernel(const uint32_t* __restri
   if (e >= n) return;
   const uint32_t key = keys[e - 1];
   if (key >= nrows || keys[e] != key) return;  // last run ends inside this tile
-  // owner test: the run containing entry e-1 starts in this tile
-  if (keys[s] == key && s > 0 && keys[s - 1] == key) return;
+  if (keys[s] == key && s > 0 && keys[s - 1] == key) return;  // ... or started before it
   for (int c = lane; c < D; c += 32) {
     float acc = part_last[tile * D + c];
-    for (int64_t t = tile + 1;; ++t) {
-      acc += part_first[t * D + c];
-      const int64_t ts = t * SEG_T, te = ts + SEG_T < n ? ts + SEG_T : n;
-      if (te >= n || keys[te] != key || keys[te - 1] != key) break;
+    for (int64_t u = tile + 1;; ++u) {
+      acc += part_first[u * D + c];
+      const int64_t us = u * SEG_T, ue = us + SEG_T < n ? us + SEG_T : n;
+      if (ue >= n || keys[ue] != key || keys[ue - 1] != key) break;
     }
     G[(int64_t)key * D + c] += acc;
   }

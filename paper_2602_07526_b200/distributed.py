@@ -1,0 +1,87 @@
+"""Row-sharded value table across GPUs (BASELINE.json configs[3]).
+
+Rank p of P holds value rows [p*n/P, (p+1)*n/P) and its own B_local queries;
+the sub-keys are replicated (they are small).  One step:
+
+  forward   select (a1-a4, local queries)             -> idx, w      [B_l,H,k]
+            all-gather idx, w (8 B per contribution)   -> [P*B_l,H,k]
+            gather over the local rows, all queries    -> partial [P*B_l,d_v]
+            reduce-scatter(sum) of the partials        -> out [B_l,d_v]
+  backward  all-gather d_out                           -> [P*B_l,d_v]
+            scatter over the local rows: dV_shard +=, dw for local slots (0 else)
+            reduce-scatter(sum) of dw  (one owner per element: the sum is exact)
+            backward_keys on the local queries         -> dQ (=), dK (+=)
+
+The collectives are torch.distributed calls (NCCL over NVLink/NVSwitch on the
+GPU box): fixed-size, graph-capturable, no host synchronisation, NVLS-capable
+(reduce-scatter).  The data-path kernels are the C ABI's phase entry points
+(msn_pkm_select / _gather / _scatter / _backward_keys).  dK is this rank's
+contribution; summing it across ranks is the caller's data-parallel job
+(like any replicated parameter).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+
+class ShardedPKM:
+    def __init__(self, heads: int, n_sub: int, d_half: int, d_value: int, k: int,
+                 local_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
+                 group=None, phases=None, device=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        n = n_sub * n_sub
+        if n % self.world:
+            raise ValueError(f"n_sub^2 = {n} is not divisible by the world size {self.world}")
+        self.rows = n // self.world
+        self.row_begin = self.rank * self.rows
+        self.row_end = self.row_begin + self.rows
+        self.heads, self.k, self.d_value, self.d_half, self.n_sub = heads, k, d_value, d_half, n_sub
+        self.local_batch = local_batch
+        if phases is None:
+            from .pkm import PKMLookup
+            phases = PKMLookup(heads, n_sub, d_half, d_value, k, max_batch=local_batch * self.world,
+                               qk_dtype=qk_dtype, value_dtype=value_dtype,
+                               row_begin=self.row_begin, row_end=self.row_end, device=device)
+        self.ph = phases
+
+    def value_shard(self, full_values: torch.Tensor) -> torch.Tensor:
+        """This rank's rows of a full table (every rank generates the same seeded table)."""
+        return full_values[self.row_begin:self.row_end].contiguous()
+
+    def _all_gather(self, x: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(out, x.contiguous(), group=self.group)
+        return out
+
+    def _reduce_scatter(self, x: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((x.shape[0] // self.world,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.reduce_scatter_tensor(out, x.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
+        return out
+
+    def forward(self, query: torch.Tensor, subkeys: torch.Tensor, value_shard: torch.Tensor):
+        """Returns (out [B_l,d_v], tape) for the local queries."""
+        idx, w = self.ph.select(query, subkeys)
+        idx_all = self._all_gather(idx)
+        w_all = self._all_gather(w)
+        part = self.ph.gather(idx_all, w_all, value_shard)
+        out = self._reduce_scatter(part)
+        return out, (idx, w, idx_all, w_all)
+
+    def backward(self, d_out: torch.Tensor, query: torch.Tensor, subkeys: torch.Tensor,
+                 value_shard: torch.Tensor, tape, d_subkeys: Optional[torch.Tensor] = None,
+                 d_value_shard: Optional[torch.Tensor] = None):
+        """Returns (d_query, d_subkeys (this rank's part, +=), d_value_shard (+=), dw)."""
+        idx, w, idx_all, w_all = tape
+        dev = d_out.device
+        if d_value_shard is None:
+            d_value_shard = torch.zeros((self.rows, self.d_value), dtype=torch.float32, device=dev)
+        d_all = self._all_gather(d_out.float())
+        dw_part = self.ph.scatter(idx_all, w_all, d_all, value_shard, d_value_shard)
+        dw = self._reduce_scatter(dw_part)
+        dq, d_subkeys = self.ph.backward_keys(query, subkeys, idx, w, dw, d_subkeys)
+        return dq, d_subkeys, d_value_shard, dw

@@ -188,6 +188,39 @@ class PKMLookup:
         return d_query, d_subkeys
 
 
+    def step_host(self, query_h, d_out_h, subkeys, values, d_subkeys, d_values,
+                  out_h=None, d_query_h=None):
+        """One forward+backward fed from host memory: H2D copies of the query
+        and the upstream gradient (pinned host tensors), a1-a8 on the device
+        (d_subkeys/d_values device buffers accumulated), D2H copies of out and
+        d_query into pinned host tensors, one synchronisation at the end.
+        Returns (out_h, d_query_h)."""
+        B = query_h.shape[0]
+        if out_h is None:
+            out_h = torch.empty((B, self.d_value), dtype=torch.float32).pin_memory()
+        if d_query_h is None:
+            d_query_h = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32).pin_memory()
+        q = query_h.to(self.device, non_blocking=True)
+        d = d_out_h.to(self.device, non_blocking=True)
+        self._check_inputs(q, subkeys, values)
+        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        dq = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=self.device)
+        dw = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        ws = self.workspace(B)
+        s = _stream()
+        _lib.check(self.lib.msn_pkm_forward(self._h, s, B, _ptr(q), _ptr(subkeys), _ptr(values),
+                                            _ptr(out), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
+        out_h.copy_(out, non_blocking=True)
+        _lib.check(self.lib.msn_pkm_backward(self._h, s, B, _ptr(d), _ptr(q), _ptr(subkeys), _ptr(values),
+                                             _ptr(idx), _ptr(w), _ptr(dq), _ptr(d_subkeys),
+                                             _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
+        d_query_h.copy_(dq, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out_h, d_query_h
+
+
 class PKMFunction(torch.autograd.Function):
     """autograd wrapper: out = PKM(query; subkeys, values).  Gradients: query
     (=), subkeys and values (fp32, cast to the parameter dtype by autograd)."""
