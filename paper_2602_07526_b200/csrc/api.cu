@@ -61,6 +61,7 @@ size_t fwd_bytes(const Shape& s) {
   size_t b = align256(sizeof(float) * rows * kCandCap) + align256(sizeof(int32_t) * rows * kCandCap) +
              align256(sizeof(int32_t) * rows);
   if (!select_tc_supported(s)) b += align256(sizeof(float) * rows * s.n_sub);
+  else b += align256(select_tc_workspace_bytes(s));
   return b;
 }
 
@@ -100,7 +101,7 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   p += align256(sizeof(int32_t) * rows);
   cudaError_t e;
   if (select_tc_supported(s)) {
-    e = launch_select_tc(s, query, subkeys, cd, st, launches);
+    e = launch_select_tc(s, query, subkeys, cd, p, st, launches);
     if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half candidates)");
   } else {
     e = launch_select_simt(s, query, subkeys, (float*)p, cd, st, launches);

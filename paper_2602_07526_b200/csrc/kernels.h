@@ -34,9 +34,12 @@ cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, flo
 
 // a1+a2 on tcgen05 (bf16 configs): fused scoring GEMM + candidate selection.
 // Returns cudaErrorNotSupported when the shape is not handled.
+// fp32 inputs run 3xTF32 (kind::tf32); ws holds the split sub-keys
+// (select_tc_workspace_bytes).
 cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
-                             cudaStream_t st, int* launches);
+                             void* ws, cudaStream_t st, int* launches);
 bool select_tc_supported(const Shape& s);
+size_t select_tc_workspace_bytes(const Shape& s);
 
 // a2 (ordering) + a3 + a4: per-half top-k from the candidate lists, Cartesian
 // top-k over I x J + softmax.  idx/w [B,H,k].

@@ -36,7 +36,7 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kStages = 3;
 constexpr int kMaxNTile = 256;
 constexpr int kCap = 64;          // candidate buffer entries per row
-constexpr int kBlockK = 64;       // bf16 elements per 128-byte swizzle row
+constexpr int kRowBytes = 128;    // one 128-byte swizzle row per k-block (64 bf16 / 32 fp32)
 
 // ------------------------------------------------------------------ PTX ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -154,6 +154,52 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// kind::tf32: A/B format TF32 (2), D fp32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// A operand from TMEM (lane = row, 32-bit columns = k): D (+)= A[tmem] . B[smem]^T
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// fp32 -> (hi, lo): hi keeps the 10 explicit mantissa bits a TF32 operand
+// holds (low 13 bits cleared), lo = x - hi is exact in fp32.
+__host__ __device__ __forceinline__ float tf32_hi(float x) {
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+#else
+  uint32_t u; memcpy(&u, &x, 4); u &= 0xffffe000u; float r; memcpy(&r, &u, 4); return r;
+#endif
+}
 
 // ------------------------------------------------------------- top-k -------
 // In-register bitonic sort of N values, descending (group maxima -> tau).
@@ -186,16 +232,22 @@ struct TcParams {
   int32_t* cn;
 };
 
-template <int KT>
+template <int KT, bool TF32>
 __global__ void __launch_bounds__(kThreads, 1)
     select_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                     const __grid_constant__ CUtensorMap tmap_k, const TcParams p) {
+                     const __grid_constant__ CUtensorMap tmap_k,
+                     const __grid_constant__ CUtensorMap tmap_klo, const TcParams p) {
+  constexpr int BK = TF32 ? 32 : 64;            // elements per k-block (one 128-B row)
+  constexpr int B_PARTS = TF32 ? 2 : 1;         // B tiles per stage: (K_hi, K_lo) or K
+  const int acc_stride = TF32 ? p.n_tile : kMaxNTile;  // TMEM columns between accumulators
+  const uint32_t alo_col = 2u * (uint32_t)p.n_tile;     // TF32: A_lo columns [2 n_tile, +d_h)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // carve: A (k_blocks x 16 KB) | B ring (kStages x n_tile x 128 B) | cand vals | cand cols | bars
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
-  float* cand_v = reinterpret_cast<float*>(sB + kStages * p.n_tile * 128);
+  const int stage_bytes = B_PARTS * p.n_tile * kRowBytes;
+  float* cand_v = reinterpret_cast<float*>(sB + kStages * stage_bytes);
   uint16_t* cand_c = reinterpret_cast<uint16_t*>(cand_v + (kCap + 1) * 128);
   uint64_t* bars = reinterpret_cast<uint64_t*>(cand_c + (kCap + 1) * 128);  // 8-aligned: (kCap+1)*128*6
   uint64_t* a_full = bars;
@@ -203,7 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* a_ready = tempty + 2;  // TF32: A split into (hi in smem, lo in TMEM)
+  uint32_t* tmem_slot = (uint32_t*)(a_ready + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int hh = blockIdx.y;  // h*2 + half
@@ -212,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap_q);
     prefetch_tmap(&tmap_k);
+    if (TF32) prefetch_tmap(&tmap_klo);
     mbar_init(a_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -221,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
+    mbar_init(a_ready, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -239,38 +294,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       mbar_expect_tx(a_full, p.k_blocks * 16384);
       for (int kb = 0; kb < p.k_blocks; ++kb)
-        tma_load_3d(sA + kb * 16384, &tmap_q, a_full, kb * kBlockK, hh, (int)m0);
+        tma_load_3d(sA + kb * 16384, &tmap_q, a_full, kb * BK, hh, (int)m0);
       int it = 0;
       for (int c = 0; c < p.n_chunks; ++c)
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], p.n_tile * 128);
-          tma_load_2d(sB + s * p.n_tile * 128, &tmap_k, &full[s], kb * kBlockK,
-                      hh * p.n_sub + c * p.n_tile);
+          mbar_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(sB + s * stage_bytes, &tmap_k, &full[s], kb * BK, hh * p.n_sub + c * p.n_tile);
+          if (TF32)
+            tma_load_2d(sB + s * stage_bytes + p.n_tile * kRowBytes, &tmap_klo, &full[s], kb * BK,
+                        hh * p.n_sub + c * p.n_tile);
         }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, p.n_tile);
+      const uint32_t idesc = TF32 ? idesc_tf32(128, p.n_tile) : idesc_bf16(128, p.n_tile);
       mbar_wait(a_full, 0);
+      if (TF32) mbar_wait(a_ready, 0);
       tc_fence_after();
       int it = 0;
       for (int c = 0; c < p.n_chunks; ++c) {
         const int buf = c & 1;
         mbar_wait(&tempty[buf], ((c >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + buf * kMaxNTile;
+        const uint32_t d = tmem + buf * acc_stride;
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + kb * 16384);
-          const uint32_t b0 = smem_u32(sB + s * p.n_tile * 128);
+          const uint32_t b0 = smem_u32(sB + s * stage_bytes);
+          if constexpr (TF32) {
+            // 3xTF32: A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (the lo.lo term is below fp32 rounding)
+            const uint32_t b1 = b0 + p.n_tile * kRowBytes;
 #pragma unroll
-          for (int kk = 0; kk < kBlockK / 16; ++kk)
-            tc_mma(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t acc = (kb | kk) != 0;
+              tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, acc);
+              tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b1 + kk * 32), idesc, 1);
+              tc_mma_tf32_ts(d, tmem + alo_col + kb * BK + kk * 8, sw128_desc(b0 + kk * 32), idesc, 1);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              tc_mma(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+          }
           tc_commit(&empty[s]);
         }
         tc_commit(&tfull[buf]);
@@ -289,6 +359,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;     // query row within the tile
     const int tid = row;               // candidate buffer column
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    if constexpr (TF32) {
+      // split this row of the resident query tile: hi (TF32-exact) back into
+      // shared memory in place, lo = x - hi into TMEM columns [alo_col, +d_h)
+      mbar_wait(a_full, 0);
+      const int sw = row & 7;
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        float* arow = reinterpret_cast<float*>(sA + kb * 16384 + row * kRowBytes);
+        uint32_t lo[32];
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          float4* pc = reinterpret_cast<float4*>(arow) + (ch ^ sw);  // logical chunk ch
+          float4 x = *pc;
+          float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+          *pc = h;
+          lo[ch * 4 + 0] = __float_as_uint(x.x - h.x);
+          lo[ch * 4 + 1] = __float_as_uint(x.y - h.y);
+          lo[ch * 4 + 2] = __float_as_uint(x.z - h.z);
+          lo[ch * 4 + 3] = __float_as_uint(x.w - h.w);
+        }
+        tmem_st32(lane_base + alo_col + kb * BK, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_ready);
+    }
     constexpr int G = 2 * KT;
     constexpr int STEP = G > 32 ? G : 32;
     float gm[G];
@@ -302,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg_cols = nseg * p.n_tile;
       // TMEM address of segment column j
       auto taddr = [&](int j) -> uint32_t {
-        return lane_base + (uint32_t)(((c + j / p.n_tile) & 1) * kMaxNTile + (j % p.n_tile));
+        return lane_base + (uint32_t)(((c + j / p.n_tile) & 1) * acc_stride + (j % p.n_tile));
       };
       // pass A: group maxima (segment start is a multiple of G)
       if (seg_cols % 64 == 0) {
@@ -464,75 +561,126 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-int n_tile_for(int n_sub) { return n_sub < kMaxNTile ? n_sub : kMaxNTile; }
+bool is_tf32(const Shape& s) { return s.qk_dt == F32; }
 
-size_t smem_bytes(const Shape& s) {
-  const int nt = n_tile_for(s.n_sub);
-  return 1024 + (size_t)(s.d_h / kBlockK) * 16384 + (size_t)kStages * nt * 128 +
-         (size_t)(kCap + 1) * 128 * (4 + 2) + 8 * (1 + 2 * kStages + 4) + 16;
+// Largest N tile (<= 256, multiple of 32, dividing n_sub); TF32 also keeps
+// 2 accumulators + the A_lo operand (d_h columns) within 512 TMEM columns.
+int n_tile_for(const Shape& s) {
+  const int cap = is_tf32(s) ? (512 - s.d_h) / 2 : kMaxNTile;
+  for (int nt = cap - cap % 32; nt >= 32; nt -= 32)
+    if (s.n_sub % nt == 0) return nt;
+  return 0;
 }
 
-template <int KT>
-cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk, TcParams p,
-                      cudaStream_t st) {
+size_t smem_bytes(const Shape& s) {
+  const int nt = n_tile_for(s);
+  const int bk = is_tf32(s) ? 32 : 64;
+  const int parts = is_tf32(s) ? 2 : 1;
+  return 1024 + (size_t)(s.d_h / bk) * 16384 + (size_t)kStages * parts * nt * kRowBytes +
+         (size_t)(kCap + 1) * 128 * (4 + 2) + 8 * (1 + 2 * kStages + 5) + 16;
+}
+
+// K -> (K_hi, K_lo) for the 3xTF32 B operand.
+__global__ void split_tf32_kernel(const float* __restrict__ k, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float x = k[i];
+  const float h = tf32_hi(x);
+  hi[i] = h;
+  lo[i] = x - h;
+}
+
+template <int KT, bool TF32>
+cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+                      const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
   const size_t sm = smem_bytes(s);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT>,
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT, TF32>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
   dim3 grid((unsigned)((s.B + 127) / 128), s.H * 2);
-  select_tc_kernel<KT><<<grid, kThreads, sm, st>>>(mq, mk, p);
+  select_tc_kernel<KT, TF32><<<grid, kThreads, sm, st>>>(mq, mk, mklo, p);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+size_t select_tc_workspace_bytes(const Shape& s) {
+  return is_tf32(s) ? 2 * sizeof(float) * (size_t)s.H * 2 * s.n_sub * s.d_h : 0;
+}
+
 bool select_tc_supported(const Shape& s) {
-  if (s.qk_dt != BF16) return false;
-  if (s.d_h % kBlockK != 0 || s.d_h > 256) return false;
-  const int nt = n_tile_for(s.n_sub);
-  if (nt % 32 != 0 || s.n_sub % nt != 0 || s.n_sub > 65535) return false;
+  const bool tf = is_tf32(s);
+  if (s.qk_dt != BF16 && s.qk_dt != F32) return false;
+  const int bk = tf ? 32 : 64;
+  if (s.d_h % bk != 0 || s.d_h > (tf ? 128 : 256)) return false;
+  const int nt = n_tile_for(s);
+  if (nt == 0 || s.n_sub > 65535) return false;
   if (s.k > 32) return false;
   if (smem_bytes(s) > 227 * 1024) return false;
   return get_encode() != nullptr;
 }
 
 cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
-                             cudaStream_t st, int* launches) {
+                             void* ws, cudaStream_t st, int* launches) {
   if (!select_tc_supported(s)) return cudaErrorNotSupported;
+  const bool tf = is_tf32(s);
+  const int bk = tf ? 32 : 64;
+  const int esz = tf ? 4 : 2;
+  const CUtensorMapDataType dt = tf ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   EncodeTiledFn enc = get_encode();
-  CUtensorMap mq, mk;
+  CUtensorMap mq, mk, mklo;
   {
-    // Q [B, H*2, d_h]: dims (d_h, H*2, B); box (64, 1, 128)
+    // Q [B, H*2, d_h]: dims (d_h, H*2, B); box (one 128-B row, 1, 128)
     cuuint64_t dims[3] = {(cuuint64_t)s.d_h, (cuuint64_t)(s.H * 2), (cuuint64_t)s.B};
-    cuuint64_t strides[2] = {(cuuint64_t)s.d_h * 2, (cuuint64_t)s.H * 2 * s.d_h * 2};
-    cuuint32_t box[3] = {kBlockK, 1, 128};
+    cuuint64_t strides[2] = {(cuuint64_t)s.d_h * esz, (cuuint64_t)s.H * 2 * s.d_h * esz};
+    cuuint32_t box[3] = {(cuuint32_t)bk, 1, 128};
     cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(Q), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    if (enc(&mq, dt, 3, const_cast<void*>(Q), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  const int nt = n_tile_for(s.n_sub);
-  {
-    // K [H*2*n_sub, d_h]: dims (d_h, H*2*n_sub); box (64, n_tile)
+  const int nt = n_tile_for(s);
+  const int64_t kel = (int64_t)s.H * 2 * s.n_sub * s.d_h;
+  const void* kb_hi = K;
+  const void* kb_lo = K;
+  if (tf) {
+    float* hi = (float*)ws;
+    float* lo = hi + kel;
+    split_tf32_kernel<<<(unsigned)((kel + 255) / 256), 256, 0, st>>>((const float*)K, hi, lo, kel);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    kb_hi = hi;
+    kb_lo = lo;
+  }
+  auto kmap = [&](CUtensorMap* m, const void* base) -> bool {
+    // K [H*2*n_sub, d_h]: dims (d_h, H*2*n_sub); box (one 128-B row, n_tile)
     cuuint64_t dims[2] = {(cuuint64_t)s.d_h, (cuuint64_t)s.H * 2 * s.n_sub};
-    cuuint64_t strides[1] = {(cuuint64_t)s.d_h * 2};
-    cuuint32_t box[2] = {kBlockK, (cuuint32_t)nt};
+    cuuint64_t strides[1] = {(cuuint64_t)s.d_h * esz};
+    cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)nt};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(K), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
-  }
-  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / kBlockK, cd.v, cd.c, cd.n};
+    return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!kmap(&mk, kb_hi) || !kmap(&mklo, kb_lo)) return cudaErrorInvalidValue;
+  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / bk, cd.v, cd.c, cd.n};
   cudaError_t e;
-  if (s.k <= 8) e = launch_kt<8>(s, mq, mk, p, st);
-  else if (s.k <= 16) e = launch_kt<16>(s, mq, mk, p, st);
-  else e = launch_kt<32>(s, mq, mk, p, st);
+  if (tf) {
+    if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);
+    else if (s.k <= 16) e = launch_kt<16, true>(s, mq, mk, mklo, p, st);
+    else e = launch_kt<32, true>(s, mq, mk, mklo, p, st);
+  } else {
+    if (s.k <= 8) e = launch_kt<8, false>(s, mq, mk, mklo, p, st);
+    else if (s.k <= 16) e = launch_kt<16, false>(s, mq, mk, mklo, p, st);
+    else e = launch_kt<32, false>(s, mq, mk, mklo, p, st);
+  }
   if (e == cudaSuccess) ++*launches;
   return e;
 }
