@@ -53,15 +53,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps in hardware
+// instead of spinning, so the producer/MMA lanes do not steal issue slots
+// from the epilogue warps that share their SM sub-partitions.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -398,8 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int seg_cols = nseg * p.n_tile;
       // TMEM address of segment column j
-      auto taddr = [&](int j) -> uint32_t {
-        return lane_base + (uint32_t)(((c + j / p.n_tile) & 1) * acc_stride + (j % p.n_tile));
+      auto taddr = [&](int j) -> uint32_t {  // j < 2 * n_tile
+        const int hi = j >= p.n_tile ? 1 : 0;
+        return lane_base + (uint32_t)(((c + hi) & 1) * acc_stride + (j - hi * p.n_tile));
       };
       // pass A: group maxima (segment start is a multiple of G)
       if (seg_cols % 64 == 0) {
