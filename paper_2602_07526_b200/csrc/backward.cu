@@ -142,20 +142,31 @@ cudaError_t excl_scan(uint32_t* data, int64_t len, uint32_t* part, cudaStream_t 
 }
 
 // Stable scatter: items of a block are ranked per digit in input order with
-// warp match-any; warp totals are scanned per digit across the 8 warps.
+// warp match-any; warp totals are scanned per digit across the 8 warps; the
+// block's items are then reordered by digit in shared memory so that each
+// digit's run is written to its global range with coalesced stores.
 __global__ void __launch_bounds__(RS_THREADS) rs_scatter_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, int64_t n, int shift,
     int nb, const uint32_t* __restrict__ offs, int nblocks, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out) {
   constexpr int NW = RS_THREADS / 32;
-  extern __shared__ uint32_t cnt_raw[];  // [NW][nb + 1]
+  extern __shared__ uint32_t smem_rs[];
   const int stride_w = nb + 1;
+  uint32_t* cnt_raw = smem_rs;                 // [NW][nb + 1]
+  uint32_t* bstart = cnt_raw + NW * stride_w;  // [nb] block-local exclusive start per digit
+  uint32_t* goff = bstart + nb;                // [nb] global start of this block's digit run
+  uint32_t* skey = goff + nb;                  // [RS_TILE]
+  uint32_t* sval = skey + RS_TILE;             // [RS_TILE]
+  __shared__ uint32_t wsum[NW];
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int i = threadIdx.x; i < NW * stride_w; i += RS_THREADS) cnt_raw[i] = 0;
+  for (int d = threadIdx.x; d < nb; d += RS_THREADS) goff[d] = offs[(int64_t)d * nblocks + blockIdx.x];
   __syncthreads();
   uint32_t* cntw = cnt_raw + wid * stride_w;
   const uint32_t mask = (uint32_t)nb - 1u;
-  const int64_t base = (int64_t)blockIdx.x * RS_TILE + wid * (32 * RS_ITEMS);
+  const int64_t tile0 = (int64_t)blockIdx.x * RS_TILE;
+  const int64_t base = tile0 + wid * (32 * RS_ITEMS);
+  const int items = (int)((n - tile0) < RS_TILE ? (n - tile0) : RS_TILE);
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t key[RS_ITEMS], val[RS_ITEMS], dig[RS_ITEMS], rank[RS_ITEMS];
 #pragma unroll
@@ -174,7 +185,8 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_kernel(
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < nb; d += RS_THREADS) {  // exclusive scan across warps, per digit
+  // per digit: exclusive offsets across warps (in place) and the block total
+  for (int d = threadIdx.x; d < nb; d += RS_THREADS) {
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
@@ -182,14 +194,57 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_kernel(
       cnt_raw[w * stride_w + d] = run;
       run += c;
     }
+    bstart[d] = run;
+  }
+  __syncthreads();
+  // block-local exclusive scan of the digit totals (nb <= 2048, 8 per thread)
+  {
+    const int per = (nb + RS_THREADS - 1) / RS_THREADS;
+    const int d0 = threadIdx.x * per;
+    uint32_t loc[8];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int d = d0 + i;
+      loc[i] = (i < per && d < nb) ? bstart[d] : 0u;
+      sum += loc[i];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) wpre += (w < wid) ? wsum[w] : 0u;
+    uint32_t run = wpre + incl - sum;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int d = d0 + i;
+      if (i < per && d < nb) {
+        bstart[d] = run;
+        run += loc[i];
+      }
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     if (dig[j] == (uint32_t)nb) continue;
-    const uint32_t pos = offs[(int64_t)dig[j] * nblocks + blockIdx.x] + cntw[dig[j]] + rank[j];
-    keys_out[pos] = key[j];
-    vals_out[pos] = val[j];
+    const uint32_t local = bstart[dig[j]] + cntw[dig[j]] + rank[j];
+    skey[local] = key[j];
+    sval[local] = val[j];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < items; i += RS_THREADS) {
+    const uint32_t k = skey[i];
+    const uint32_t d = (k >> shift) & mask;
+    const uint32_t pos = goff[d] + (uint32_t)i - bstart[d];
+    keys_out[pos] = k;
+    vals_out[pos] = sval[i];
   }
 }
 
@@ -215,10 +270,11 @@ cudaError_t radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uin
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (RS_THREADS / 32) * ((1 << RS_MAX_BITS) + 1) * 4);
+                         ((RS_THREADS / 32) * ((1 << RS_MAX_BITS) + 1) + 2 * (1 << RS_MAX_BITS) +
+                          2 * RS_TILE) * 4);
     attr = true;
   }
-  const size_t smem_scatter = (size_t)(RS_THREADS / 32) * (nb + 1) * 4;
+  const size_t smem_scatter = ((size_t)(RS_THREADS / 32) * (nb + 1) + 2 * nb + 2 * RS_TILE) * 4;
   uint32_t *kin = keys_a, *vin = nullptr, *kout = keys_b, *vout = vals_b;
   for (int p = 0; p < passes; ++p) {
     const int shift = p * width;

@@ -24,6 +24,7 @@
 //               Rows whose buffer would overflow (massive exact ties) take an
 //               exact bitwise search for their KT-th score instead.
 #include <cuda.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -227,6 +228,7 @@ __device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
 }
 
 struct TcParams {
+  int dbg;  // profiling only (MSN_SELECT_DBG): 1 = epilogue skips all processing
   int64_t B;
   int H, n_sub, d_h, k;
   int n_tile, n_chunks, k_blocks;
@@ -399,6 +401,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nseg = (c == 0 && p.n_chunks >= 2) ? 2 : 1;  // first segment: both TMEM buffers
       for (int u = 0; u < nseg; ++u) mbar_wait(&tfull[(c + u) & 1], ((c + u) >> 1) & 1);
       tc_fence_after();
+      if (p.dbg == 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          for (int u = 0; u < nseg; ++u) mbar_arrive(&tempty[(c + u) & 1]);
+        c += nseg;
+        continue;
+      }
       const int seg_cols = nseg * p.n_tile;
       // TMEM address of segment column j
       auto taddr = [&](int j) -> uint32_t {  // j < 2 * n_tile
@@ -674,7 +684,8 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   if (!kmap(&mk, kb_hi) || !kmap(&mklo, kb_lo)) return cudaErrorInvalidValue;
-  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / bk, cd.v, cd.c, cd.n};
+  static const int dbg = getenv("MSN_SELECT_DBG") ? atoi(getenv("MSN_SELECT_DBG")) : 0;
+  TcParams p{dbg, s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / bk, cd.v, cd.c, cd.n};
   cudaError_t e;
   if (tf) {
     if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);
