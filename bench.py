@@ -310,6 +310,142 @@ def run_ours(args, rank, world, local_rank):
     return res
 
 
+def run_latency(args, rank, world, local_rank):
+    """C5 (configs[4]): latency-bound inference forward.  One forward per call,
+    replayed from a CUDA graph; per-call CUDA-event latency, p50/p99."""
+    from paper_2602_07526_b200 import workloads as wl
+    from paper_2602_07526_b200.pkm import PKMLookup, _ptr
+    from paper_2602_07526_b200._lib import check
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = wl.CONFIGS[args.workload]
+    Q, K, V = wl.make_queries(cfg, dev), wl.make_subkeys(cfg, dev), wl.make_values(cfg, dev)
+    lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, cfg.batch,
+                   cfg.qk_dtype, cfg.value_dtype, device=dev)
+    B = cfg.batch
+    out = torch.empty((B, cfg.d_value), dtype=torch.float32, device=dev)
+    idx = torch.empty((B, cfg.heads, cfg.k), dtype=torch.int32, device=dev)
+    w = torch.empty((B, cfg.heads, cfg.k), dtype=torch.float32, device=dev)
+    ws = lk.workspace(B)
+    s = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+
+    def fwd():
+        sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        check(lk.lib.msn_pkm_forward(lk._h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(out), _ptr(idx), _ptr(w),
+                                     _ptr(ws), ws.numel()))
+
+    with torch.cuda.stream(s):
+        for _ in range(max(3, args.warmup)):
+            fwd()
+    torch.cuda.synchronize()
+    launches = lk.last_launch_count()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fwd()
+    for _ in range(max(3, args.warmup)):
+        g.replay()
+    torch.cuda.synchronize()
+    n = max(args.steps, 1000)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    clocks = ClockSampler(dev.index or 0)
+    cur = torch.cuda.current_stream(dev)
+    with clocks:
+        for i in range(n):
+            evs[i][0].record(cur)
+            g.replay()
+            evs[i][1].record(cur)
+        torch.cuda.synchronize()
+    lat = sorted(a.elapsed_time(b) * 1e3 for a, b in evs)  # us
+    mean_us = sum(lat) / n
+    p50, p99 = lat[n // 2], lat[min(n - 1, int(0.99 * n))]
+    lookups = B * cfg.heads
+    esz = 2 if cfg.value_dtype == torch.bfloat16 else 4
+    gbytes = lookups * cfg.k * (cfg.d_value * esz + 8) + B * cfg.d_value * 4
+    peaks, kind = load_peaks()
+    res = {"metric": "PKM lookups/sec fwd (latency config, per-call)", "value": lookups / (mean_us / 1e6),
+           "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup, "ms_per_step": mean_us / 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg.value_dtype),
+           "data": "synthetic (seeded, BASELINE.json configs[4] recipe)",
+           "config": {"workload": cfg.name, "batch": B, "heads": cfg.heads, "n_sub": cfg.n_sub,
+                      "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
+                      "mode": "forward only, one CUDA-graph replay per call, back to back",
+                      "l2": "value table 1 GiB > L2: the gather streams from HBM; no flush"},
+           "latency_us": {"p50": p50, "p99": p99, "mean": mean_us, "min": lat[0], "calls": n},
+           "roofline": {"kernel": "whole forward call (HBM bytes of the gather)", "bound": "hbm",
+                        "achieved": gbytes / (mean_us / 1e6) / 1e9, "peak": float(peaks["hbm_gbs"]),
+                        "unit": "GB/s", "frac": gbytes / (mean_us / 1e6) / 1e9 / float(peaks["hbm_gbs"]),
+                        "traffic": None, "peak_kind": kind},
+           "gpu_launches": launches * n, "clocks": clocks.summary()}
+    return res if rank == 0 else None
+
+
+def run_sharded(args, rank, world, local_rank):
+    """C4 (configs[3]): the row-sharded table, strong scaling (fixed total
+    batch B = 32,768 split over the ranks).  Phases timed with CUDA events;
+    value = total lookups / max-over-ranks step time."""
+    import torch.distributed as dist
+    from paper_2602_07526_b200 import workloads as wl
+    from paper_2602_07526_b200.distributed import ShardedPKM
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29612")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    cfg = wl.CONFIGS[args.workload]
+    Q, K, V, dOut = wl.make_all(cfg, dev)  # every rank draws the same seeded tensors
+    B_l = cfg.batch // world
+    sp = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l,
+                    qk_dtype=cfg.qk_dtype, value_dtype=cfg.value_dtype, device=dev)
+    q_l = Q[rank * B_l:(rank + 1) * B_l].contiguous()
+    d_l = dOut[rank * B_l:(rank + 1) * B_l].contiguous()
+    Vs = sp.value_shard(V)
+    del V, Q, dOut
+    dVs = torch.zeros((sp.rows, cfg.d_value), dtype=torch.float32, device=dev)
+    dK = torch.zeros((cfg.heads, 2, cfg.n_sub, cfg.d_half), dtype=torch.float32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        out, tape = sp.forward(q_l, K, Vs)
+        sp.backward(d_l, q_l, K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
+        return out
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(dev.index or 0)
+    with clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank != 0:
+        return None
+    lookups = cfg.batch * cfg.heads
+    return {"metric": METRIC, "value": lookups / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": _dtype_name(cfg.value_dtype),
+            "data": "synthetic (seeded, BASELINE.json configs[3] recipe)",
+            "config": {"workload": cfg.name, "batch_total": cfg.batch, "batch_per_rank": B_l,
+                       "heads": cfg.heads, "n_sub": cfg.n_sub, "n_slots": cfg.n_slots,
+                       "rows_per_rank": sp.rows, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
+                       "parallelism": f"row-sharded table x{world} (all-gather idx/w, reduce-scatter partials)",
+                       "l2": "flushed before every step (512 MiB write, outside the timed events)"},
+            "clocks": clocks.summary()}
+
+
 def cpu_baseline(cfg, Q, K, V, dOut, queries=None):
     """The fp64 oracle (oracle/, as it stands) on a bounded sample of the same
     workload on the host cores: fwd + bwd over the first `queries` queries,
@@ -383,6 +519,7 @@ def main():
     ap.add_argument("--atomic", action="store_true", help="atomic (non-deterministic) dV scatter")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="C4 through the row-sharded path even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -398,10 +535,15 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = run_ours(args, rank, world, local_rank)
+    if args.workload.startswith("c5"):
+        res = run_latency(args, rank, world, local_rank)
+    elif args.workload.startswith("c4") and (world > 1 or args.sharded):
+        res = run_sharded(args, rank, world, local_rank)
+    else:
+        res = run_ours(args, rank, world, local_rank)
     if res is not None:
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 
