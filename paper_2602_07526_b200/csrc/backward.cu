@@ -824,6 +824,7 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   b += 2 * align256(sizeof(float) * tiles * D);
   b += align256(sizeof(float) * n_dk);
   b += align256(sizeof(float) * n_dv);
+  b += align256(dk_tc_workspace_bytes(s));
   return b;
 }
 
@@ -845,6 +846,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.part_last = (float*)p; p += align256(sizeof(float) * tiles * D);
   w.dsS = (float*)p; p += align256(sizeof(float) * n_dk);
   w.dw = (float*)p; p += align256(sizeof(float) * n_dv);
+  w.dk_ws = (void*)p; p += align256(dk_tc_workspace_bytes(s));
   return w;
 }
 
@@ -921,6 +923,8 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
+  if (dk_tc_supported(s))
+    return launch_dk_tc(s, Q, ws.keys_a, ws.dsS, dK, ws.dk_ws, st, launches);
   const int64_t n = 2 * L * s.k;
   uint32_t *ks, *vs;
   e = radix_sort(ws.keys_a, ws.vals_a, ws.keys_b, ws.vals_b, ws.hist, n, nrows, st, launches, &ks,

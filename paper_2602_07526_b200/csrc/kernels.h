@@ -58,7 +58,14 @@ struct BwdWorkspace {
   float* part_last;                             // tiles * D_max
   float* dsS;                                   // 2*B*H*k aggregated score grads
   float* dw;                                    // B*H*k (when the caller gives none)
+  void* dk_ws;                                  // tensor-core dK scratch (bf16 configs)
 };
+
+// a8 dK on the tensor cores (bf16 q/K): dK += dS^T . Q per (head, half).
+bool dk_tc_supported(const Shape& s);
+size_t dk_tc_workspace_bytes(const Shape& s);
+cudaError_t launch_dk_tc(const Shape& s, const void* Q, const uint32_t* rkeys, const float* dsS,
+                         float* dK, void* ws, cudaStream_t st, int* launches);
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 
