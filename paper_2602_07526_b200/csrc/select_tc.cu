@@ -24,6 +24,9 @@
 //               Rows whose buffer would overflow (massive exact ties) take an
 //               exact bitwise search for their KT-th score instead.
 #include <cuda.h>
+#include <algorithm>
+#include <vector>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -63,6 +66,12 @@ __device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
   }
 }
 
+__device__ unsigned long long g_dbg_ts[4096 * 32];
+__device__ __forceinline__ unsigned long long gclk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 struct TcParams {
   int dbg;  // profiling only (MSN_SELECT_DBG): 1 = epilogue skips all processing
   int64_t B;
@@ -88,9 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
   const int stage_bytes = B_PARTS * p.n_tile * kRowBytes;
-  float* cand_v = reinterpret_cast<float*>(sB + kStages * stage_bytes);
-  uint16_t* cand_c = reinterpret_cast<uint16_t*>(cand_v + (kCap + 1) * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cand_c + (kCap + 1) * 128);  // 8-aligned: (kCap+1)*128*6
+  uint2* cand = reinterpret_cast<uint2*>(sB + kStages * stage_bytes);  // [kCap+1][128] (score bits, column)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cand + (kCap + 1) * 128);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + kStages;
@@ -99,9 +107,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a_ready = tempty + 2;  // TF32: A split into (hi in smem, lo in TMEM)
   uint32_t* tmem_slot = (uint32_t*)(a_ready + 1);
 
+  const unsigned long long t_entry = gclk();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int hh = blockIdx.y;  // h*2 + half
-  const int64_t m0 = (int64_t)blockIdx.x * 128;
+  const int hh = blockIdx.x;  // h*2 + half
+  const int64_t m0 = (int64_t)blockIdx.y * 128;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap_q);
@@ -129,6 +138,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
+  const bool ts_on = p.dbg >= 1 && cta_lin < 4096;
+  if (ts_on && threadIdx.x == 0) {
+    g_dbg_ts[cta_lin * 32 + 0] = gclk();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_dbg_ts[cta_lin * 32 + 11] = smid;
+    g_dbg_ts[cta_lin * 32 + 13] = t_entry;
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -153,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = TF32 ? idesc_tf32(128, p.n_tile) : idesc_bf16(128, p.n_tile);
       mbar_wait(a_full, 0);
+      if (ts_on) g_dbg_ts[cta_lin * 32 + 1] = gclk();
       if (TF32) mbar_wait(a_ready, 0);
       tc_fence_after();
       int it = 0;
@@ -164,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
+          if (ts_on && it < 8) g_dbg_ts[cta_lin * 32 + 2 + it] = gclk();
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + kb * 16384);
           const uint32_t b0 = smem_u32(sB + s * stage_bytes);
@@ -229,10 +249,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     constexpr int G = 2 * KT;
     constexpr int STEP = G > 32 ? G : 32;
-    float gm[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) gm[j] = -INFINITY;
+    float tau = -INFINITY;  // lower bound on this row's KT-th score
     int cnt = 0;
+    // exact KT-th (index tie rule) over the buffered candidates -> new tau;
+    // keeps exactly the entries that can still be in the top-KT (<= KT).
+    auto tighten = [&]() {
+      float t[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) t[i] = i < cnt ? __uint_as_float(cand[i * 128 + tid].x) : -INFINITY;
+      bitonic_sort_vals<64>(t);
+      const float nt = t[KT - 1];
+      int gt = 0;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) gt += t[i] > nt ? 1 : 0;
+      int need = KT - gt;  // entries equal to nt that survive (earliest columns first)
+      const int mx = __reduce_max_sync(0xffffffffu, cnt);
+      int w = 0;
+      for (int i = 0; i < mx; ++i) {
+        if (i < cnt) {
+          const uint2 e = cand[i * 128 + tid];
+          const float v = __uint_as_float(e.x);
+          const bool keep = v > nt || (v == nt && need > 0);
+          if (v == nt && keep) --need;
+          if (keep) cand[w++ * 128 + tid] = e;
+        }
+      }
+      cnt = w;
+      tau = fmaxf(tau, nt);
+    };
     for (int c = 0; c < p.n_chunks;) {
       const int nseg = (c == 0 && p.n_chunks >= 2) ? 2 : 1;  // first segment: both TMEM buffers
       for (int u = 0; u < nseg; ++u) mbar_wait(&tfull[(c + u) & 1], ((c + u) >> 1) & 1);
@@ -246,110 +290,111 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       const int seg_cols = nseg * p.n_tile;
+      const bool first = c == 0;
+      const bool stamp = ts_on && warp == kEpiWarp0 && lane == 0 && first;
+      if (stamp) g_dbg_ts[cta_lin * 32 + 16] = gclk();
+      if (ts_on && warp == kEpiWarp0 && lane == 0 && c >= 2 && c < 8) g_dbg_ts[cta_lin * 32 + 18 + c] = gclk();
       // TMEM address of segment column j
       auto taddr = [&](int j) -> uint32_t {  // j < 2 * n_tile
         const int hi = j >= p.n_tile ? 1 : 0;
         return lane_base + (uint32_t)(((c + hi) & 1) * acc_stride + (j - hi * p.n_tile));
       };
-      // pass A: group maxima (segment start is a multiple of G)
-      if (seg_cols % 64 == 0) {
-        for (int j0 = 0; j0 < seg_cols; j0 += 64) {
-          uint32_t r[64];
-          tmem_ld64(taddr(j0), r);  // j0 % n_tile + 64 <= n_tile since n_tile % 64 == 0
+      if (first) {
+        // pass A: tau = KT-th largest of the 2KT strided group maxima of the
+        // first segment (KT distinct columns score >= tau, so the row's KT-th
+        // score is >= tau).  Segment start 0 is a multiple of G.
+        float gm[G];
 #pragma unroll
-          for (int jj = 0; jj < 64; ++jj) {
-            const int g = jj % G;  // == (col) % G: j0 % 64 == 0 and G | 64
-            gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
+        for (int j = 0; j < G; ++j) gm[j] = -INFINITY;
+        if (seg_cols % 64 == 0) {
+          for (int j0 = 0; j0 < seg_cols; j0 += 64) {
+            uint32_t r[64];
+            tmem_ld64(taddr(j0), r);  // n_tile % 64 == 0: never straddles a buffer
+#pragma unroll
+            for (int jj = 0; jj < 64; ++jj) gm[jj % G] = fmaxf(gm[jj % G], __uint_as_float(r[jj]));
           }
-        }
-      } else {
-        for (int j0 = 0; j0 < seg_cols; j0 += STEP) {
+        } else {
+          for (int j0 = 0; j0 < seg_cols; j0 += STEP) {
 #pragma unroll
-          for (int piece = 0; piece < STEP / 32; ++piece) {
-            const int j = j0 + piece * 32;
-            if (j < seg_cols) {
-              uint32_t r[32];
-              tmem_ld32(taddr(j), r);
+            for (int piece = 0; piece < STEP / 32; ++piece) {
+              const int j = j0 + piece * 32;
+              if (j < seg_cols) {
+                uint32_t r[32];
+                tmem_ld32(taddr(j), r);
 #pragma unroll
-              for (int jj = 0; jj < 32; ++jj) {
-                const int g = (piece * 32 + jj) % G;
-                gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
+                for (int jj = 0; jj < 32; ++jj) {
+                  const int g = (piece * 32 + jj) % G;
+                  gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
+                }
               }
             }
           }
         }
+        if (stamp) g_dbg_ts[cta_lin * 32 + 17] = gclk() + (unsigned long long)(gm[0] > 1e30f);
+        bitonic_sort_vals<G>(gm);
+        tau = gm[KT - 1];
+        if (stamp) g_dbg_ts[cta_lin * 32 + 18] = gclk() + (unsigned long long)(tau > 1e30f);
       }
-      float tau;
-      {
-        float t[G];
-#pragma unroll
-        for (int j = 0; j < G; ++j) t[j] = gm[j];
-        bitonic_sort_vals<G>(t);
-        tau = t[KT - 1];
-      }
-      // compact the buffer to entries >= tau (order preserved)
-      {
-        const int mx = __reduce_max_sync(0xffffffffu, cnt);
-        int w = 0;
-        for (int i = 0; i < mx; ++i) {
-          if (i < cnt) {
-            const float v = cand_v[i * 128 + tid];
-            const uint16_t cc = cand_c[i * 128 + tid];
-            if (v >= tau) {
-              cand_v[w * 128 + tid] = v;
-              cand_c[w * 128 + tid] = cc;
-              ++w;
-            }
-          }
-        }
-        cnt = w;
-      }
-      // pass B: collect segment columns >= tau (branch-free: unselected
-      // columns and overflow go to the dummy row kCap)
+      // pass B: buffer the columns that can still be in the top-KT.  In the
+      // first segment tau came from these same columns (ties kept: >=);
+      // later columns lose every tie to the KT earlier ones behind tau (>).
+      // Branch-free: every column is stored, unselected ones (and any
+      // first-segment overflow) into the dummy row kCap.
       const int cnt_old = cnt;
       const int col_base = c * p.n_tile;
-      for (int j0 = 0; j0 < seg_cols; j0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr(j0), r);
+      auto piece = [&](uint32_t (&r)[32], int j0) {
+        if (!first) {
+          int nsel = 0;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) nsel += (__uint_as_float(r[jj]) > tau) ? 1 : 0;
+          if (__any_sync(0xffffffffu, cnt + nsel > kCap)) tighten();  // cnt <= KT; tau only rises
+        }
+        const uint32_t colj = (uint32_t)(col_base + j0);
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const float v = __uint_as_float(r[jj]);
-          const bool sel = v >= tau;
+          const bool sel = first ? v >= tau : v > tau;
           const int slot = sel ? min(cnt, kCap) : kCap;
-          cand_v[slot * 128 + tid] = v;
-          cand_c[slot * 128 + tid] = (uint16_t)(col_base + j0 + jj);
+          cand[slot * 128 + tid] = make_uint2(r[jj], colj + jj);
           cnt += sel ? 1 : 0;
         }
+      };
+      for (int j0 = 0; j0 < seg_cols; j0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr(j0), r);
+        piece(r, j0);
       }
-      if (__any_sync(0xffffffffu, cnt > kCap)) {
+      const bool ovf = cnt > kCap;  // first segment only (later pieces tighten first)
+      if (ts_on && warp == kEpiWarp0 && lane == 0 && c >= 2 && c < 8) g_dbg_ts[cta_lin * 32 + 24 + c] = gclk();
+      if (stamp) g_dbg_ts[cta_lin * 32 + 20] = gclk();
+      if (stamp) g_dbg_ts[cta_lin * 32 + 19] = gclk() + (unsigned long long)(cnt > 100000);
+      if (__any_sync(0xffffffffu, ovf)) {
         // exact path: the KT-th largest ordered key t over buffer u segment
         auto count_ge = [&](uint32_t t) -> int {
           int n = 0;
-          for (int i = 0; i < cnt_old; ++i) n += ord_f32(cand_v[i * 128 + tid]) >= t;
+          for (int i = 0; i < cnt_old; ++i) n += ord_f32(__uint_as_float(cand[i * 128 + tid].x)) >= t ? 1 : 0;
           for (int j0 = 0; j0 < seg_cols; j0 += 32) {
             uint32_t r[32];
             tmem_ld32(taddr(j0), r);
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) n += ord_f32(__uint_as_float(r[jj])) >= t;
+            for (int jj = 0; jj < 32; ++jj) n += ord_f32(__uint_as_float(r[jj])) >= t ? 1 : 0;
           }
           return n;
         };
         uint32_t t = 0;
         for (int bit = 31; bit >= 0; --bit) {
-          const uint32_t cand = t | (1u << bit);
-          if (count_ge(cand) >= KT) t = cand;
+          const uint32_t ct = t | (1u << bit);
+          if (count_ge(ct) >= KT) t = ct;
         }
         const int gt = (t == 0xffffffffu) ? 0 : count_ge(t + 1);
         int need = KT - gt;
         int w = 0;
         for (int i = 0; i < cnt_old; ++i) {
-          const float v = cand_v[i * 128 + tid];
-          const uint32_t o = ord_f32(v);
+          const uint2 e = cand[i * 128 + tid];
+          const uint32_t o = ord_f32(__uint_as_float(e.x));
           if (o > t || (o == t && need > 0)) {
             if (o == t) --need;
-            cand_v[w * 128 + tid] = v;
-            cand_c[w * 128 + tid] = cand_c[i * 128 + tid];
-            ++w;
+            cand[w++ * 128 + tid] = e;
           }
         }
         for (int j0 = 0; j0 < seg_cols; j0 += 32) {
@@ -357,17 +402,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(taddr(j0), r);
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
-            const float v = __uint_as_float(r[jj]);
-            const uint32_t o = ord_f32(v);
+            const uint32_t o = ord_f32(__uint_as_float(r[jj]));
             if (o > t || (o == t && need > 0)) {
               if (o == t) --need;
-              cand_v[w * 128 + tid] = v;
-              cand_c[w * 128 + tid] = (uint16_t)(col_base + j0 + jj);
-              ++w;
+              cand[w++ * 128 + tid] = make_uint2(r[jj], (uint32_t)(col_base + j0 + jj));
             }
           }
         }
         cnt = w;  // <= KT
+        tau = fmaxf(tau, unord_f32(t));
       }
       tc_fence_before();
       __syncwarp();
@@ -375,21 +418,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = 0; u < nseg; ++u) mbar_arrive(&tempty[(c + u) & 1]);
       c += nseg;
     }
-    const int64_t b = m0 + row;
-    if (b < p.B) {
-      const int64_t rr = b * p.H * 2 + hh;
-      for (int i = 0; i < cnt; ++i) {
-        p.cv[rr * kCandCap + i] = cand_v[i * 128 + tid];
-        p.cc[rr * kCandCap + i] = (int32_t)cand_c[i * 128 + tid];
+    // coalesced write-out: the warp writes its 32 rows one after another
+    // (lane = candidate slot), instead of 32 rows per store instruction
+    for (int rr = 0; rr < 32; ++rr) {
+      const int n = __shfl_sync(0xffffffffu, cnt, rr);
+      const int trow = q * 32 + rr;
+      const int64_t b = m0 + trow;
+      if (b >= p.B) continue;
+      const int64_t orow = b * p.H * 2 + hh;
+      for (int i = lane; i < n; i += 32) {
+        const uint2 e = cand[i * 128 + trow];
+        p.cv[orow * kCandCap + i] = __uint_as_float(e.x);
+        p.cc[orow * kCandCap + i] = (int32_t)e.y;
       }
-      p.cn[rr] = cnt;
+      if (lane == 0) p.cn[orow] = n;
     }
+    if (ts_on && warp == kEpiWarp0 && lane == 0) g_dbg_ts[cta_lin * 32 + 14] = gclk();
   }
   tc_fence_before();
   __syncthreads();
+  if (ts_on && threadIdx.x == 0) g_dbg_ts[cta_lin * 32 + 10] = gclk();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if (ts_on && lane == 0) g_dbg_ts[cta_lin * 32 + 12] = gclk();
   }
 }
 
@@ -410,7 +462,7 @@ size_t smem_bytes(const Shape& s) {
   const int bk = is_tf32(s) ? 32 : 64;
   const int parts = is_tf32(s) ? 2 : 1;
   return 1024 + (size_t)(s.d_h / bk) * 16384 + (size_t)kStages * parts * nt * kRowBytes +
-         (size_t)(kCap + 1) * 128 * (4 + 2) + 8 * (1 + 2 * kStages + 5) + 16;
+         (size_t)(kCap + 1) * 128 * 8 + 8 * (1 + 2 * kStages + 5) + 16;
 }
 
 // K -> (K_hi, K_lo) for the 3xTF32 B operand.
@@ -435,7 +487,9 @@ cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  dim3 grid((unsigned)((s.B + 127) / 128), s.H * 2);
+  // x = head/half (fastest): concurrently resident CTAs spread over all 2H
+  // sub-key codebooks instead of hammering one codebook's lines in L2
+  dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128));
   select_tc_kernel<KT, TF32><<<grid, kThreads, sm, st>>>(mq, mk, mklo, p);
   return cudaGetLastError();
 }
@@ -516,6 +570,53 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
     else e = launch_kt<32, false>(s, mq, mk, mklo, p, st);
   }
   if (e == cudaSuccess) ++*launches;
+  if (dbg >= 2 && e == cudaSuccess) {
+    cudaStreamSynchronize(st);
+    static unsigned long long h[4096 * 32];
+    cudaMemcpyFromSymbol(h, g_dbg_ts, sizeof(h));
+    const int ncta = (int)std::min<int64_t>(4096, (s.B + 127) / 128 * s.H * 2);
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < ncta; ++c) t0 = std::min(t0, h[c * 32]);
+    double acc[16] = {0};
+    for (int c = 0; c < ncta; ++c)
+      for (int j = 0; j < 15; ++j) if (j != 11 && j != 13) acc[j] += ((double)h[c * 32 + j] - (double)h[c * 32]) / ncta;
+    double ph[4] = {0, 0, 0, 0};
+    for (int c = 0; c < ncta; ++c)
+      for (int j = 0; j < 4; ++j) ph[j] += ((double)h[c * 32 + 16 + j] - (double)h[c * 32]) / ncta;
+    fprintf(stderr, "epilogue: tfull seen %.0f, passA %.0f, tau %.0f, passB %.0f, done %.0f; dealloc %.0f ns after CTA start\n",
+            ph[0], ph[1], ph[2], ph[3], acc[14], acc[12]);
+    double ch[16] = {0};
+    for (int c = 0; c < ncta; ++c)
+      for (int j = 20; j < 32; ++j) ch[j - 20] += ((double)h[c * 32 + j] - (double)h[c * 32]) / ncta;
+    fprintf(stderr, "first seg passB stamp(20) %.0f; chunks 2..5 seen/done: %.0f/%.0f %.0f/%.0f %.0f/%.0f %.0f/%.0f\n",
+            ch[0], ch[0 + 2 - 2 + 2], ch[6 + 2], ch[3], ch[9], ch[4], ch[10], ch[5], ch[11]);
+    double span = 0;
+    for (int c = 0; c < ncta; ++c) span = std::max(span, (double)(h[c * 32 + 10] - t0));
+    {
+      std::vector<double> st(ncta), en(ncta);
+      for (int c = 0; c < ncta; ++c) { st[c] = (double)(h[c * 32] - t0); en[c] = (double)(h[c * 32 + 10] - t0); }
+      std::vector<double> ss = st; std::sort(ss.begin(), ss.end());
+      int per_sm[256] = {0};
+      for (int c = 0; c < ncta; ++c) per_sm[h[c * 32 + 11] & 255]++;
+      int maxc = 0, nsm = 0;
+      for (int i = 0; i < 256; ++i) { maxc = std::max(maxc, per_sm[i]); nsm += per_sm[i] > 0; }
+      // per SM: order CTAs by start, report gap between a CTA's dealloc and the next one's entry
+      double gap = 0, ent = 0; int ng = 0;
+      for (int c = 0; c < ncta; ++c) {
+        ent += (double)(h[c * 32] - h[c * 32 + 13]) / ncta;
+        int best = -1;
+        for (int d = 0; d < ncta; ++d)
+          if (h[d * 32 + 11] == h[c * 32 + 11] && h[d * 32 + 13] > h[c * 32 + 13] &&
+              (best < 0 || h[d * 32 + 13] < h[best * 32 + 13])) best = d;
+        if (best >= 0) { gap += (double)h[best * 32 + 13] - (double)h[c * 32 + 12]; ++ng; }
+      }
+      fprintf(stderr, "entry->start(alloc+init) %.0f ns; dealloc->next entry on same SM %.0f ns (n=%d)\n", ent, ng ? gap / ng : 0.0, ng);
+      fprintf(stderr, "starts: p0 %.0f p25 %.0f p50 %.0f p75 %.0f p100 %.0f ns; SMs used %d, max CTAs/SM %d\n",
+              ss[0], ss[ncta / 4], ss[ncta / 2], ss[3 * ncta / 4], ss[ncta - 1], nsm, maxc);
+    }
+    fprintf(stderr, "select_tc ts (ns, mean rel. to CTA start): Afull %.0f  full0..7 %.0f %.0f %.0f %.0f %.0f %.0f %.0f %.0f  end %.0f  | kernel span %.0f\n",
+            acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8], acc[9], acc[10], span);
+  }
   return e;
 }
 
