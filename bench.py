@@ -185,29 +185,37 @@ def run_ours(args, rank, world, local_rank):
     launches = [0]
 
     def step(evs=None):
+        # forward (scoring, then the fused Cartesian + gather kernel; the library
+        # records evs[1] at the stage boundary), backward phases separately
         n = 0
-        if evs: evs[0].record(stream)
-        check(lib.msn_pkm_select(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
+        if evs:
+            evs[0].record(stream)
+            arr = (ctypes.c_void_p * 2)(evs[1].cuda_event, evs[2].cuda_event)
+            check(lib.msn_pkm_set_trace_events(h, arr, 2))
+        check(lib.msn_pkm_forward(h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(out), _ptr(idx), _ptr(w),
+                                  _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
-        if evs: evs[1].record(stream)
-        check(lib.msn_pkm_gather(h, sp, B, _ptr(idx), _ptr(w), _ptr(V), _ptr(out)))
-        n += lk.last_launch_count()
-        if evs: evs[2].record(stream)
+        if evs:
+            check(lib.msn_pkm_set_trace_events(h, None, 0))
+            evs[3].record(stream)
         check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(dOut), _ptr(V), _ptr(dV), _ptr(dw),
                                   _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
-        if evs: evs[3].record(stream)
+        if evs: evs[4].record(stream)
         check(lib.msn_pkm_backward_keys(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(dw), _ptr(dQ),
                                         _ptr(dK), _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
-        if evs: evs[4].record(stream)
+        if evs: evs[5].record(stream)
         launches[0] = n
 
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    for e in evs:  # create the CUDA events up front (torch creates them lazily on record)
+        e[1].record(stream)
+        e[2].record(stream)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -221,7 +229,7 @@ def run_ours(args, rank, world, local_rank):
     t_wall = time.perf_counter() - t_wall
     if world > 1:
         torch.distributed.barrier()
-    phases = ["select", "gather", "scatter", "backward_keys"]
+    phases = ["select", "cartesian", "gather", "scatter", "backward_keys"]
     per = {p: 0.0 for p in phases}
     for e in evs:
         for j, p in enumerate(phases):
@@ -276,7 +284,9 @@ def run_ours(args, rank, world, local_rank):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(args.workload, {}).get("gather")
-    roof = {"kernel": "gather (a5, sparse gather + weighted sum)", "bound": "hbm",
+    fused = cfg.batch >= 8192 and cfg.heads * cfg.k <= 256
+    roof = {"kernel": ("cartesian_gather (a3+a4+a5 fused)" if fused else "gather (a5, sparse gather + weighted sum)"),
+            "bound": "hbm",
             "achieved": ab["gather"] / (g_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": ab["gather"] / (g_ms / 1e3) / 1e9 / hbm, "traffic": traffic,
             "algorithmic_bytes": ab["gather"], "peak_kind": peaks_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
@@ -293,7 +303,10 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg.value_dtype),
         "data": "synthetic (seeded, BASELINE.json configs[%d] recipe, DESIGN.md Inputs)" % cfg.index,
         "config": {"workload": cfg.name, "batch": cfg.batch, "heads": cfg.heads, "n_sub": cfg.n_sub,
-                   "n_slots": cfg.n_slots, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
+                   "n_slots": cfg.n_slots,
+                   "phases": "select = tcgen05 scoring + per-half candidates; cartesian = Cartesian top-k + softmax "
+                             "(0 when fused into the gather, B >= 8192); gather = sparse gather + weighted sum "
+                             "(the roofline kernel); scatter = dV/dw; backward_keys = ds, dQ, dK", "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
                    "lookups_per_step_per_gpu": cfg.batch * cfg.heads,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "backward": "atomic" if args.atomic else "deterministic sort-based",

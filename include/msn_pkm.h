@@ -156,6 +156,13 @@ msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B,
  * (for the bench's gpu_launches count). */
 int32_t msn_pkm_last_launch_count(msn_pkm_t h);
 
+/* Tracing: caller-created cudaEvent_t handles (n <= 4, n = 0 disables) that
+ * the library records on the call's stream at internal stage boundaries.
+ * events[0]: after the scoring + per-half top-k stage of msn_pkm_forward /
+ * msn_pkm_select; events[1]: after the Cartesian top-k + softmax stage (the
+ * same point as events[0] when forward fuses that stage into the gather). */
+msn_status msn_pkm_set_trace_events(msn_pkm_t h, void* const* events, int32_t n);
+
 const char* msn_pkm_status_string(msn_status s);
 const char* msn_pkm_last_error(void);
 

@@ -48,6 +48,7 @@ SIGNATURES = {
     "msn_pkm_scatter": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_backward_keys": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_last_launch_count": [_P],
+    "msn_pkm_set_trace_events": [_P, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32],
     "msn_pkm_status_string": [ctypes.c_int],
     "msn_pkm_last_error": [],
 }

@@ -14,6 +14,8 @@ using namespace msn;
 struct msn_pkm {
   msn_pkm_config cfg;
   int last_launches;
+  cudaEvent_t trace[4];  // optional stage-boundary events (msn_pkm_set_trace_events)
+  int ntrace;
 };
 
 namespace {
@@ -84,9 +86,11 @@ msn_status check_batch(msn_pkm_t h, int64_t B) {
     if (!aligned16(p)) return fail(MSN_ERR_INVALID_ARG, "%s is not 16-byte aligned", #p);   \
   } while (0)
 
+// a1 + a2 into per-half candidate lists; then either the Cartesian stage
+// alone (select) or fused with the gather (forward: values != NULL).
 msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
                      const void* subkeys, int32_t* idx, float* weights, void* ws, size_t ws_bytes,
-                     int* launches) {
+                     int* launches, const void* values = nullptr, float* out = nullptr) {
   const Shape s = shape_of(h->cfg, B);
   if (ws_bytes < fwd_bytes(s))
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
@@ -107,8 +111,16 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
     e = launch_select_simt(s, query, subkeys, (float*)p, cd, st, launches);
     if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half top-k)");
   }
+  if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);  // stage boundary: scoring done
+  if (values) {
+    if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);  // (fused: no separate Cartesian stage)
+    e = launch_cartesian_gather(s, cd, idx, weights, values, out, st, launches);
+    if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax + gather");
+    return MSN_OK;
+  }
   e = launch_cartesian(s, cd, idx, weights, st, launches);
   if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax");
+  if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);  // stage boundary: Cartesian + softmax done
   return MSN_OK;
 }
 
@@ -158,6 +170,7 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
   if (!h) return fail(MSN_ERR_INTERNAL, "out of host memory");
   h->cfg = *c;
   h->last_launches = 0;
+  h->ntrace = 0;
   *out = h;
   return MSN_OK;
 }
@@ -168,6 +181,15 @@ msn_status msn_pkm_destroy(msn_pkm_t h) {
 }
 
 int32_t msn_pkm_last_launch_count(msn_pkm_t h) { return h ? h->last_launches : -1; }
+
+msn_status msn_pkm_set_trace_events(msn_pkm_t h, void* const* events, int32_t n) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if (n < 0 || n > 4 || (n > 0 && !events)) return fail(MSN_ERR_INVALID_ARG, "0 <= n <= 4 events");
+  for (int i = 0; i < n; ++i) h->trace[i] = (cudaEvent_t)events[i];
+  h->ntrace = n;
+  return MSN_OK;
+}
 
 msn_status msn_pkm_workspace_size(msn_pkm_t h, int64_t B, int64_t gather_batch, size_t* fwd,
                                   size_t* bwd) {
@@ -235,6 +257,12 @@ msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B, const void* que
   REQUIRE_PTR(weights);
   REQUIRE_PTR(workspace);
   cudaStream_t cs = (cudaStream_t)stream;
+  // fused Cartesian + gather when there are enough queries to fill the GPU
+  // with warps (one warp per query); small batches keep one warp per lookup
+  if (h->cfg.heads * h->cfg.k <= 256 && B >= 8192) {
+    return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
+                     &h->last_launches, values, out);
+  }
   if ((st = do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
                       &h->last_launches)))
     return st;

@@ -29,6 +29,7 @@ namespace msn {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+constexpr int kMaxHK = 256;  // H*k staged per warp in the fused kernel
 
 // Warp-wide bitonic sort of 64 (score, index) pairs held as (v[r], ix[r]),
 // element e = r*32 + lane; result in (score desc, index asc) order.
@@ -66,21 +67,27 @@ __device__ __forceinline__ void warp_sort64(float (&v)[2], int32_t (&ix)[2]) {
   }
 }
 
+// Per-warp scratch of one lookup's Cartesian stage.
 template <int KMAX, int MAXC>
-__global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict__ cand_v,
-                                                        const int32_t* __restrict__ cand_c,
-                                                        const int32_t* __restrict__ cand_n,
-                                                        int64_t L, int n_sub, int k,
-                                                        int32_t* __restrict__ idx,
-                                                        float* __restrict__ w) {
+struct CartSmem {
+  float sv2[KMAX];
+  int32_t si2[KMAX];
+  uint64_t cand[MAXC];
+  uint64_t res[KMAX];
+};
+
+// One warp computes lookup l: writes idx/w[l*k + t] to global and, when
+// s_idx/s_w are given, to shared memory too (for a fused gather).
+template <int KMAX, int MAXC>
+__device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64_t l,
+                                                 const float* __restrict__ cand_v,
+                                                 const int32_t* __restrict__ cand_c,
+                                                 const int32_t* __restrict__ cand_n, int n_sub,
+                                                 int k, int32_t* __restrict__ idx,
+                                                 float* __restrict__ w, int32_t* s_idx,
+                                                 float* s_w) {
   constexpr int APL = KMAX / 32;  // rows a per lane
-  __shared__ float sv2[kWarpsPerBlock][KMAX];
-  __shared__ int32_t si2[kWarpsPerBlock][KMAX];
-  __shared__ uint64_t cand[kWarpsPerBlock][MAXC];
-  __shared__ uint64_t res[kWarpsPerBlock][KMAX];
-  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
-  if (l >= L) return;
+  const int lane = threadIdx.x % 32;
 
   float va[APL];
   int32_t ia[APL];
@@ -110,8 +117,8 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
       for (int u = 0; u < APL; ++u) {
         const int a = lane + 32 * u;
         if (a < k) {
-          sv2[wid][a] = v[u];
-          si2[wid][a] = ix[u];
+          sm.sv2[a] = v[u];
+          sm.si2[a] = ix[u];
         }
       }
     }
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
     const int a = lane + 32 * u;
     if (a < k) {
       const int ba = (k + a) / (a + 1) - 1;  // ceil(k/(a+1)) - 1 <= k-1
-      tau = fmaxf(tau, va[u] + sv2[wid][ba]);
+      tau = fmaxf(tau, va[u] + sm.sv2[ba]);
     }
   }
   tau = warp_max(tau);
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
     p[u] = 0;
     if (a < k) {
       const int lim = k / (a + 1);
-      while (p[u] < lim && va[u] + sv2[wid][p[u]] >= tau) ++p[u];
+      while (p[u] < lim && va[u] + sm.sv2[p[u]] >= tau) ++p[u];
     }
     mine += p[u];
   }
@@ -153,28 +160,28 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
 #pragma unroll
   for (int u = 0; u < APL; ++u) {
     for (int q = 0; q < p[u]; ++q) {
-      const float c = va[u] + sv2[wid][q];
-      const uint32_t flat = (uint32_t)ia[u] * (uint32_t)n_sub + (uint32_t)si2[wid][q];
-      cand[wid][off++] = sel_key(c, flat);
+      const float c = va[u] + sm.sv2[q];
+      const uint32_t flat = (uint32_t)ia[u] * (uint32_t)n_sub + (uint32_t)sm.si2[q];
+      sm.cand[off++] = sel_key(c, flat);
     }
   }
   __syncwarp();
   // exact rank by composite key; keys are distinct (flat ids are distinct)
   for (int x = lane; x < m; x += 32) {
-    const uint64_t kx = cand[wid][x];
+    const uint64_t kx = sm.cand[x];
     int r = 0;
-    for (int y = 0; y < m; ++y) r += cand[wid][y] > kx;
-    if (r < k) res[wid][r] = kx;
+    for (int y = 0; y < m; ++y) r += sm.cand[y] > kx;
+    if (r < k) sm.res[r] = kx;
   }
   __syncwarp();
   // softmax over the k selected scores, max = the first (reading R1)
-  const float c0 = sel_key_score(res[wid][0]);
+  const float c0 = sel_key_score(sm.res[0]);
   float e[APL];
   float z = 0.f;
 #pragma unroll
   for (int u = 0; u < APL; ++u) {
     const int t = lane + 32 * u;
-    e[u] = t < k ? expf(sel_key_score(res[wid][t]) - c0) : 0.f;
+    e[u] = t < k ? expf(sel_key_score(sm.res[t]) - c0) : 0.f;
     z += e[u];
   }
   z = warp_sum(z);
@@ -183,13 +190,145 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
   for (int u = 0; u < APL; ++u) {
     const int t = lane + 32 * u;
     if (t < k) {
-      idx[l * k + t] = (int32_t)sel_key_index(res[wid][t]);
-      w[l * k + t] = e[u] * inv;
+      const int32_t f = (int32_t)sel_key_index(sm.res[t]);
+      const float wt = e[u] * inv;
+      idx[l * k + t] = f;
+      w[l * k + t] = wt;
+      if (s_idx) {
+        s_idx[t] = f;
+        s_w[t] = wt;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int KMAX, int MAXC>
+__global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict__ cand_v,
+                                                        const int32_t* __restrict__ cand_c,
+                                                        const int32_t* __restrict__ cand_n,
+                                                        int64_t L, int n_sub, int k,
+                                                        int32_t* __restrict__ idx,
+                                                        float* __restrict__ w) {
+  __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
+  const int wid = threadIdx.x / 32;
+  const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
+  if (l >= L) return;
+  cartesian_lookup<KMAX, MAXC>(sm[wid], l, cand_v, cand_c, cand_n, n_sub, k, idx, w, nullptr, nullptr);
+}
+
+// a3 + a4 + a5 fused: one warp per query runs the Cartesian stage of its H
+// lookups (ALU-bound) and then streams their H*k value rows (HBM-bound);
+// warps in different phases overlap the two.  Same arithmetic and
+// summation order as cartesian_kernel + gather_kernel.
+template <int KMAX, int MAXC, typename VT, int VPL, int G, int U>
+__global__ void __launch_bounds__(256) cartesian_gather_kernel(
+    const float* __restrict__ cand_v, const int32_t* __restrict__ cand_c,
+    const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
+    int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
+    float* __restrict__ out, int d_v) {
+  constexpr int PER = elem<VT>::per16;
+  constexpr int LG = 32 / G;
+  __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
+  __shared__ int32_t s_idx[kWarpsPerBlock][kMaxHK];
+  __shared__ float s_w[kWarpsPerBlock][kMaxHK];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
+  if (b >= B) return;
+  for (int h = 0; h < H; ++h)
+    cartesian_lookup<KMAX, MAXC>(sm[wid], b * H + h, cand_v, cand_c, cand_n, n_sub, k, idx, w,
+                                 &s_idx[wid][h * k], &s_w[wid][h * k]);
+  const int HK = H * k;
+  const int g = lane / LG, gl = lane % LG;
+  float acc[VPL][PER];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v)
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[v][e] = 0.f;
+  const int row_vecs = d_v / PER;
+  for (int base = g; base < HK; base += G * U) {
+    uint4 x[U][VPL];
+    float wt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = base + u * G;
+      const int f = r < HK ? s_idx[wid][r] : -1;
+      wt[u] = f >= 0 ? s_w[wid][r] : 0.f;
+      const VT* row = V + (int64_t)(f >= 0 ? f : 0) * d_v;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int vec = gl * VPL + v;
+        if (f >= 0 && vec < row_vecs) x[u][v] = ldg_nc_v4(row + vec * PER);
+        else x[u][v] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        float f[PER];
+        unpack16<VT>(x[u][v], f);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[v][e] = fmaf(wt[u], f[e], acc[v][e]);
+      }
+  }
+#pragma unroll
+  for (int m = LG; m < 32; m <<= 1)
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[v][e] += __shfl_xor_sync(0xffffffffu, acc[v][e], m);
+  if (g == 0) {
+    float* o = out + b * d_v;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int vec = gl * VPL + v;
+      if (vec < row_vecs) {
+#pragma unroll
+        for (int e = 0; e < PER; e += 4)
+          *reinterpret_cast<float4*>(o + vec * PER + e) =
+              make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
+      }
     }
   }
 }
 
+template <int KMAX, int MAXC, typename VT>
+cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float* w, const VT* V,
+                           float* out, cudaStream_t st) {
+  const int R = s.d_v * (int)sizeof(VT) / 16;
+  const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
+#define FUSED(VPL, G, U)                                                                      \
+  cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U><<<blocks, 256, 0, st>>>(                  \
+      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v)
+  if (R >= 128) { if (R > 128) return cudaErrorNotSupported; FUSED(4, 1, 4); }
+  else if (R > 32) FUSED(2, 1, 8);
+  else if (R > 16) FUSED(1, 1, 8);
+  else if (R > 8) FUSED(1, 2, 8);
+  else if (R > 4) FUSED(1, 4, 8);
+  else if (R > 2) FUSED(1, 8, 8);
+  else if (R > 1) FUSED(1, 16, 8);
+  else FUSED(1, 32, 8);
+#undef FUSED
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* idx, float* w,
+                                    const void* V, float* out, cudaStream_t st, int* launches) {
+  if (s.H * s.k > kMaxHK || s.row_begin != 0) return cudaErrorNotSupported;
+  cudaError_t e;
+  if (s.k <= 32) {
+    e = s.v_dt == F32 ? dispatch_fused<32, 119, float>(s, cd, idx, w, (const float*)V, out, st)
+                      : dispatch_fused<32, 119, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st);
+  } else {
+    e = s.v_dt == F32 ? dispatch_fused<64, 280, float>(s, cd, idx, w, (const float*)V, out, st)
+                      : dispatch_fused<64, 280, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st);
+  }
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
 
 cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, float* w,
                              cudaStream_t st, int* launches) {

@@ -46,6 +46,11 @@ size_t select_tc_workspace_bytes(const Shape& s);
 cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, float* w,
                              cudaStream_t st, int* launches);
 
+// a2 (ordering) + a3 + a4 + a5 fused (unsharded forward): Cartesian stage of
+// each query's H lookups, then the gather of their H*k rows.
+cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* idx, float* w,
+                                    const void* V, float* out, cudaStream_t st, int* launches);
+
 // a5: out[b] = sum over local rows of w * V[idx - row_begin] (=).
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
                           float* out, cudaStream_t st, int* launches);
