@@ -658,7 +658,11 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
 // For each half, the dS of every distinct sub-key index r is summed over the
 // t with r_t = r in t order; dQ[b,h,half] = sum_r dS_r K[h,half,r]; one dK
 // record per distinct r (first occurrence), others get the sentinel key.
-template <typename QT, int KPL, int EPL>
+// DENSE: instead of records, the dS of the lookup-half is written as one
+// dense bf16 row dSd[b, h*2 + half, 0:n_sub] (zeros elsewhere) for the
+// tensor-core dK (dk_tc.cu); n_sub <= kDenseMax.
+constexpr int kDenseMax = 1024;
+template <typename QT, int KPL, int EPL, bool DENSE>
 __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     const int32_t* __restrict__ idx,
                                                     const float* __restrict__ w,
@@ -666,10 +670,12 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     int H, int n_sub, int d_h, int k,
                                                     float* __restrict__ dQ,
                                                     uint32_t* __restrict__ rkeys,
-                                                    float* __restrict__ dsS, uint32_t sentinel) {
+                                                    float* __restrict__ dsS, uint32_t sentinel,
+                                                    uint16_t* __restrict__ dSd) {
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   __shared__ int32_t s_r[8][64];
   __shared__ float s_d[8][64];
+  __shared__ __align__(16) uint16_t s_row[DENSE ? 8 : 1][DENSE ? kDenseMax : 8];
   const int lane = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (l >= L) return;
@@ -710,13 +716,15 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       }
     }
     // records
+    if constexpr (!DENSE) {
 #pragma unroll
-    for (int u = 0; u < KPL; ++u) {
-      const int t = lane + 32 * u;
-      if (t < k) {
-        const int64_t rec = (l * k + t) * 2 + half;
-        rkeys[rec] = first[u] ? (uint32_t)((h * 2 + half) * n_sub + r[u]) : sentinel;
-        dsS[rec] = dS[u];
+      for (int u = 0; u < KPL; ++u) {
+        const int t = lane + 32 * u;
+        if (t < k) {
+          const int64_t rec = (l * k + t) * 2 + half;
+          rkeys[rec] = first[u] ? (uint32_t)((h * 2 + half) * n_sub + r[u]) : sentinel;
+          dsS[rec] = dS[u];
+        }
       }
     }
     // dQ: lanes over d_h.  The distinct sub-keys of this half are compacted
@@ -736,6 +744,18 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       m += __popc(bm);
     }
     __syncwarp();
+    if constexpr (DENSE) {
+      // dense row: zero, place the m distinct values, copy out (16 B per lane)
+      uint4* row4 = reinterpret_cast<uint4*>(s_row[wid]);
+      const int n16 = n_sub / 8;
+      for (int c = lane; c < n16; c += 32) row4[c] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      for (int c = lane; c < m; c += 32)
+        s_row[wid][s_r[wid][c]] = __bfloat16_as_ushort(__float2bfloat16_rn(s_d[wid][c]));
+      __syncwarp();
+      uint4* g4 = reinterpret_cast<uint4*>(dSd + (l * 2 + half) * (int64_t)n_sub);
+      for (int c = lane; c < n16; c += 32) g4[c] = row4[c];
+    }
     float acc[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
@@ -906,9 +926,16 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   const uint32_t nrows = (uint32_t)(s.H * 2 * s.n_sub);
   const unsigned blocks = (unsigned)((L + 7) / 8);
   const int E = epl_of(s.d_h);
+  const bool dense = dk_tc_supported(s);
 #define DSDQ(QT, KPL, E_)                                                                      \
-  ds_dq_kernel<QT, KPL, E_><<<blocks, 256, 0, st>>>((const QT*)K, idx, w, dw, L, s.H, s.n_sub, \
-                                                    s.d_h, s.k, dQ, ws.keys_a, ws.dsS, nrows)
+  if (dense)                                                                                   \
+    ds_dq_kernel<QT, KPL, E_, true><<<blocks, 256, 0, st>>>(                                   \
+        (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, ws.keys_a, ws.dsS, nrows,    \
+        (uint16_t*)ws.dk_ws);                                                                  \
+  else                                                                                         \
+    ds_dq_kernel<QT, KPL, E_, false><<<blocks, 256, 0, st>>>(                                  \
+        (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, ws.keys_a, ws.dsS, nrows,    \
+        nullptr)
 #define DSDQ_E(QT, KPL)                                                                        \
   switch (E) { case 1: DSDQ(QT, KPL, 1); break; case 2: DSDQ(QT, KPL, 2); break;              \
     case 4: DSDQ(QT, KPL, 4); break; case 8: DSDQ(QT, KPL, 8); break;                          \
@@ -923,8 +950,7 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
-  if (dk_tc_supported(s))
-    return launch_dk_tc(s, Q, ws.keys_a, ws.dsS, dK, ws.dk_ws, st, launches);
+  if (dense) return launch_dk_tc(s, Q, dK, ws.dk_ws, st, launches);
   const int64_t n = 2 * L * s.k;
   uint32_t *ks, *vs;
   e = radix_sort(ws.keys_a, ws.vals_a, ws.keys_b, ws.vals_b, ws.hist, n, nrows, st, launches, &ks,

@@ -54,6 +54,9 @@ SWEEP = [
     (37, 2, 128, 32, 64, 64, torch.float32, torch.float32),
     (50, 2, 64, 64, 32, 64, torch.bfloat16, torch.float32),
     (300, 4, 512, 256, 256, 32, torch.bfloat16, torch.bfloat16),
+    # tensor-core dK: d_h 64, split-K with a ragged last split
+    (1000, 2, 256, 64, 64, 16, torch.bfloat16, torch.bfloat16),
+    (70, 2, 128, 64, 64, 16, torch.bfloat16, torch.bfloat16),
 ]
 
 
