@@ -660,7 +660,8 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
 // record per distinct r (first occurrence), others get the sentinel key.
 // DENSE: instead of records, the dS of the lookup-half is written as one
 // dense bf16 row dSd[b, h*2 + half, 0:n_sub] (zeros elsewhere) for the
-// tensor-core dK (dk_tc.cu); n_sub <= kDenseMax.
+// tensor-core dQ and dK (dk_tc.cu), and dQ is not computed here;
+// n_sub <= kDenseMax.
 constexpr int kDenseMax = 1024;
 template <typename QT, int KPL, int EPL, bool DENSE>
 __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
@@ -755,6 +756,10 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       __syncwarp();
       uint4* g4 = reinterpret_cast<uint4*>(dSd + (l * 2 + half) * (int64_t)n_sub);
       for (int c = lane; c < n16; c += 32) g4[c] = row4[c];
+    }
+    if constexpr (DENSE) {
+      __syncwarp();
+      continue;  // dQ = dSd . K runs on the tensor cores (dk_tc.cu)
     }
     float acc[EPL];
 #pragma unroll
@@ -950,7 +955,7 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
-  if (dense) return launch_dk_tc(s, Q, dK, ws.dk_ws, st, launches);
+  if (dense) return launch_dk_tc(s, Q, K, dQ, dK, ws.dk_ws, st, launches);
   const int64_t n = 2 * L * s.k;
   uint32_t *ks, *vs;
   e = radix_sort(ws.keys_a, ws.vals_a, ws.keys_b, ws.vals_b, ws.hist, n, nrows, st, launches, &ks,

@@ -106,6 +106,12 @@ __device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4& v, float* f
   }
 }
 
+// Bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) into L2: puts a
+// gathered row's HBM read in flight without holding registers.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // fire-and-forget vector fp32 add into global memory (sm_90+).
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),

@@ -1,7 +1,8 @@
-// dk_tc.cu -- step a8's sub-key gradient on the tensor cores (bf16 configs):
+// dk_tc.cu -- steps a7 (dq) and a8 (dK) on the tensor cores (bf16 configs):
+//   dQ_half[b]  = dS[b,h,half] . K[h,half]      (= ; the query gradient)
 //   dK[h,half] += dS[h,half]^T . Q_half      (only the
 //   selected sub-keys receive gradient; dS is their aggregated score grad)
-// as a dense tcgen05 GEMM.
+// as two dense tcgen05 GEMMs over the same dense score-gradient matrix.
 //
 // ds_dq_kernel (backward.cu) writes the aggregated score gradients as a
 // dense bf16 matrix dSd [B, H*2, n_sub] (zeros for unselected sub-keys; one
@@ -166,6 +167,121 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// dQ[b, hh, :] = sum_i dSd[b, hh, i] K[hh, i, :]  (the dq half of step a7,
+// dq_row = sum_i dS_row[i] K_row[i]) on the tensor cores: M = 128 queries,
+// N = d_h, K = n_sub in blocks of 64.  A = dSd[b0:b0+128, hh, i-block] is
+// K-major (contiguous along i), B = K[hh, i-block, :] is MN-major
+// (contiguous along e) -- both straight from their natural layouts by TMA.
+// Written (=), one fixed k-block order: deterministic.
+struct DqParams {
+  int64_t B;
+  int H, n_sub, d_h;
+  float* dQ;  // [B, H*2, d_h]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dq_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                   const __grid_constant__ CUtensorMap tmap_k, const DqParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  const int nb = p.d_h / 64;                      // B atoms per stage
+  constexpr int kABytes = 128 * 128;              // 128 queries x 64 sub-keys bf16
+  uint8_t* sA = smem_raw + pad;                   // kStages x 16 KB
+  uint8_t* sB = sA + kStages * kABytes;           // kStages x nb atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * nb * kAtom);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* tdone = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.x * 128;
+  const int hh = blockIdx.y;
+  const int nkb = p.n_sub / 64;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_k);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tdone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)kABytes + (uint32_t)nb * kAtom;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], bytes);
+        // queries >= B (ragged last tile) are zero-filled by TMA
+        tma_load_3d(sA + s * kABytes, &tmap_a, &full[s], kb * 64, hh, m0);
+        for (int j = 0; j < nb; ++j)
+          tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_k, &full[s], 64 * j, kb * 64, hh);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(128, p.d_h) | (1u << 16);  // B MN-major
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&full[s], (kb / kStages) & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + s * kABytes);
+        const uint32_t b0 = smem_u32(sB + s * nb * kAtom);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // 16 sub-keys: +32 B in the A row, +2 KB in B
+          tc_mma(tmem, sw128_desc(a0 + kk * 32), sw128_mn_desc(b0 + kk * 2048), idesc,
+                 (kb | kk) != 0);
+        tc_commit(&empty[s]);
+      }
+      tc_commit(tdone);
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int64_t b = (int64_t)m0 + row;
+    float* dst = p.dQ + (b * (2 * p.H) + hh) * (int64_t)p.d_h;
+    mbar_wait(tdone, 0);
+    tc_fence_after();
+    for (int c0 = 0; c0 < p.d_h; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + c0, r);
+      if (b < p.B) {
+        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                              __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+size_t dq_smem_bytes(const Shape& s) {
+  return 1024 + (size_t)kStages * (128 * 128 + (s.d_h / 64) * kAtom) + 8 * (2 * kStages + 1) + 16;
+}
+
 // dK += sum_s part[s] (fixed split order)
 __global__ void dk_reduce_kernel(const float4* __restrict__ part, float4* __restrict__ dK,
                                  int64_t n4, int S) {
@@ -204,7 +320,7 @@ bool dk_tc_supported(const Shape& s) {
   // worth it while n_sub is small (C2: 512); C4 (2048) keeps the sort path.
   return s.qk_dt == BF16 && s.n_sub <= 1024 && s.n_sub % kBM == 0 && s.d_h % 64 == 0 &&
          s.d_h >= 64 && s.d_h <= 256 && s.k <= 64 && dk_smem_bytes(s) <= 227 * 1024 &&
-         get_encode() != nullptr;
+         dq_smem_bytes(s) <= 227 * 1024 && get_encode() != nullptr;
 }
 
 size_t dk_tc_workspace_bytes(const Shape& s) {
@@ -214,8 +330,8 @@ size_t dk_tc_workspace_bytes(const Shape& s) {
   return dense_ds_bytes(s) + part;
 }
 
-cudaError_t launch_dk_tc(const Shape& s, const void* Q, float* dK, void* ws, cudaStream_t st,
-                         int* launches) {
+cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* dQ, float* dK,
+                         void* ws, cudaStream_t st, int* launches) {
   if (!dk_tc_supported(s)) return cudaErrorNotSupported;
   const uint16_t* dSd = (const uint16_t*)ws;
   float* part = (float*)((char*)ws + dense_ds_bytes(s));
@@ -244,6 +360,42 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, float* dK, void* ws, cud
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+  }
+  // dQ = dSd . K per (head, half) on the tensor cores
+  {
+    CUtensorMap ma, mk;
+    // dSd [B, HH, n_sub] as the K-major A operand: dims (n_sub, HH, B), box (64, 1, 128)
+    cuuint64_t dims[3] = {(cuuint64_t)s.n_sub, (cuuint64_t)HH, (cuuint64_t)s.B};
+    cuuint64_t strides[2] = {(cuuint64_t)s.n_sub * 2, (cuuint64_t)HH * s.n_sub * 2};
+    cuuint32_t box[3] = {64, 1, 128};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (get_encode()(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)dSd, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    // K [HH, n_sub, d_h] as the MN-major B operand: dims (d_h, n_sub, HH), box (64, 64, 1)
+    cuuint64_t kdims[3] = {(cuuint64_t)s.d_h, (cuuint64_t)s.n_sub, (cuuint64_t)HH};
+    cuuint64_t kstrides[2] = {(cuuint64_t)s.d_h * 2, (cuuint64_t)s.n_sub * s.d_h * 2};
+    cuuint32_t kbox[3] = {64, 64, 1};
+    if (get_encode()(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(Kp), kdims,
+                     kstrides, kbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    static bool qattr = false;
+    if (!qattr) {
+      cudaError_t e0 = cudaFuncSetAttribute(dq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            227 * 1024);
+      if (e0 != cudaSuccess) return e0;
+      qattr = true;
+    }
+    DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ};
+    dim3 qgrid((unsigned)((s.B + 127) / 128), HH);
+    dq_gemm_kernel<<<qgrid, kThreads, dq_smem_bytes(s), st>>>(ma, mk, qp);
+    cudaError_t e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) return e1;
+    ++*launches;
   }
   const int S = splits_for(s);
   const int64_t kblocks = (s.B + kBK - 1) / kBK;

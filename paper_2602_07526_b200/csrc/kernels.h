@@ -66,13 +66,14 @@ struct BwdWorkspace {
   void* dk_ws;                                  // tensor-core dK scratch (bf16 configs)
 };
 
-// a8 dK on the tensor cores (bf16 q/K): dK += dS^T . Q per (head, half).
+// a7 dQ + a8 dK on the tensor cores (bf16 q/K): dQ = dS . K, dK += dS^T . Q per (head, half).
 bool dk_tc_supported(const Shape& s);
 size_t dk_tc_workspace_bytes(const Shape& s);
 // ws starts with the dense bf16 score-gradient matrix dSd [B, H*2, n_sub]
 // that ds_dq_kernel writes (dense mode).
-cudaError_t launch_dk_tc(const Shape& s, const void* Q, float* dK, void* ws, cudaStream_t st,
-                         int* launches);
+// Also writes dQ = dSd . K (=) on the tensor cores.
+cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* K, float* dQ, float* dK,
+                         void* ws, cudaStream_t st, int* launches);
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 

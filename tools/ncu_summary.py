@@ -10,10 +10,10 @@ COLS = [("gpu__time_duration.sum", "us", 1e-3),
         ("dram__bytes_read.sum", "MB_rd", 1e-6),
         ("dram__bytes_write.sum", "MB_wr", 1e-6),
         ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem%", 1),
-        ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1),
+        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1),
         ("lts__t_sectors_op_read.sum", "L2rd_sec", 1e-6),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%", 1),
-        ("sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active", "tc%", 1),
+        ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tc%", 1),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%", 1),
         ("launch__registers_per_thread", "regs", 1),
         ("smsp__inst_executed.sum", "Minst", 1e-6)]
@@ -45,6 +45,9 @@ def main():
                 u = units[i]
                 v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
                 sc = 1
+            elif v is not None and units[i].endswith("byte"):
+                # normalise to bytes, then the column scale (1e-6 -> MB)
+                v = v * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1.0)
             line += "%10.2f" % (v * sc) if v is not None else "%10s" % "-"
         print(line)
 
