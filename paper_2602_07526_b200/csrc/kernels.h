@@ -57,13 +57,14 @@ cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, co
 
 // ---- backward ----
 struct BwdWorkspace {
-  uint32_t *keys_a, *keys_b, *vals_a, *vals_b;  // radix sort ping-pong, n_max entries
-  uint32_t* hist;                               // 256 * max_blocks
-  float* part_first;                            // tiles * D_max
-  float* part_last;                             // tiles * D_max
-  float* dsS;                                   // 2*B*H*k aggregated score grads
-  float* dw;                                    // B*H*k (when the caller gives none)
-  void* dk_ws;                                  // tensor-core dK scratch (bf16 configs)
+  uint32_t *cnt, *off;            // per-row counts / segment offsets (grouping)
+  uint32_t *rank, *keys, *ent;    // per-contribution rank, row key, grouped record ids
+  float* went;                    // grouped weights
+  uint4 *runs_short, *runs_long;  // run records {offset, length, row}
+  uint32_t* ctl;                  // grouping counters
+  float* dsS;                     // 2*B*H*k aggregated score grads
+  float* dw;                      // B*H*k (when the caller gives none)
+  void* dk_ws;                    // tensor-core dQ/dK scratch (bf16 configs)
 };
 
 // a7 dQ + a8 dK on the tensor cores (bf16 q/K): dQ = dS . K, dK += dS^T . Q per (head, half).
@@ -77,7 +78,7 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* K, float* dQ
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 
-// a6 deterministic: sort (idx -> cid) then fused row-major dV += / dw.
+// a6 deterministic: group (idx -> cid) by row, then fused row-major dV += / dw.
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
                                   const BwdWorkspace& ws, cudaStream_t st, int* launches);
