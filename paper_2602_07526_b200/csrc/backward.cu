@@ -58,38 +58,79 @@ constexpr int GRP_SHORT = 32;     // runs up to this length: one warp, one entry
 constexpr int GRP_SMEM_MAX = 16384;  // long runs sorted in shared memory up to this length
 enum { CTL_TOTAL = 0, CTL_NSHORT = 1, CTL_NLONG = 2, CTL_WORDS = 8 };
 
+// Each block owns a contiguous range of rows: pass 1 counts its entries and
+// short/long runs, one atomic per counter per block reserves its output
+// ranges, pass 2 writes offsets and run records (block-ordered: a block
+// scan over 256-row rounds).
 __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restrict__ cnt,
                                                        uint32_t nrows, uint32_t* __restrict__ off,
                                                        uint4* __restrict__ runs_short,
                                                        uint4* __restrict__ runs_long,
                                                        uint32_t* __restrict__ ctl) {
-  const int lane = threadIdx.x % 32;
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x; r0 < nrows; r0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = r0 + threadIdx.x;
-    const uint32_t c = r < nrows ? cnt[r] : 0u;
-    uint32_t incl = c;
+  __shared__ uint32_t sh[3][8];
+  __shared__ uint32_t s_base[3];
+  const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
+  const int64_t per = ((int64_t)nrows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = r0 + per;
+  if (r1 > nrows) r1 = nrows;
+  if (r0 >= r1) return;
+  // pass 1: block totals
+  uint32_t tot = 0, ns = 0, nl = 0;
+  for (int64_t r = r0 + tid; r < r1; r += 256) {
+    const uint32_t c = cnt[r];
+    tot += c;
+    ns += (c > 0 && c <= GRP_SHORT);
+    nl += (c > GRP_SHORT);
+  }
+  tot = (uint32_t)warp_sum_int((int)tot);
+  ns = (uint32_t)warp_sum_int((int)ns);
+  nl = (uint32_t)warp_sum_int((int)nl);
+  if (lane == 0) { sh[0][wid] = tot; sh[1][wid] = ns; sh[2][wid] = nl; }
+  __syncthreads();
+  if (tid < 3) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += sh[tid][w];
+    s_base[tid] = t ? atomicAdd(&ctl[tid == 0 ? CTL_TOTAL : (tid == 1 ? CTL_NSHORT : CTL_NLONG)], t) : 0u;
+  }
+  __syncthreads();
+  uint32_t base = s_base[0], sb = s_base[1], lb = s_base[2];
+  __syncthreads();
+  // pass 2: ordered rounds of 256 rows
+  for (int64_t rr = r0; rr < r1; rr += 256) {
+    const int64_t r = rr + tid;
+    const uint32_t c = r < r1 ? cnt[r] : 0u;
+    const uint32_t is = (c > 0 && c <= GRP_SHORT), il = (c > GRP_SHORT);
+    // block exclusive scans of (c, is, il), packed: c < 2^32 needs its own scan
+    uint32_t xc = c, xs = is | (il << 16);
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += o;
+      const uint32_t o1 = __shfl_up_sync(0xffffffffu, xc, d);
+      const uint32_t o2 = __shfl_up_sync(0xffffffffu, xs, d);
+      if (lane >= d) { xc += o1; xs += o2; }
     }
-    const unsigned bs = __ballot_sync(0xffffffffu, c > 0 && c <= GRP_SHORT);
-    const unsigned bl = __ballot_sync(0xffffffffu, c > GRP_SHORT);
-    uint32_t base = 0, sb = 0, lb = 0;
-    if (lane == 31 && incl) base = atomicAdd(&ctl[CTL_TOTAL], incl);
-    if (lane == 0 && bs) sb = atomicAdd(&ctl[CTL_NSHORT], (uint32_t)__popc(bs));
-    if (lane == 0 && bl) lb = atomicAdd(&ctl[CTL_NLONG], (uint32_t)__popc(bl));
-    base = __shfl_sync(0xffffffffu, base, 31);
-    sb = __shfl_sync(0xffffffffu, sb, 0);
-    lb = __shfl_sync(0xffffffffu, lb, 0);
+    if (lane == 31) { sh[0][wid] = xc; sh[1][wid] = xs; }
+    __syncthreads();
+    uint32_t pc = 0, ps = 0, tc = 0, ts = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t a0 = sh[0][w], a1 = sh[1][w];
+      if (w < wid) { pc += a0; ps += a1; }
+      tc += a0;
+      ts += a1;
+    }
+    __syncthreads();
+    const uint32_t ec = base + pc + xc - c;
+    const uint32_t es = ps + xs - (is | (il << 16));
     if (c > 0) {
-      const uint32_t o = base + incl - c;
-      off[r] = o;
-      const uint4 rec = make_uint4(o, c, (uint32_t)r, 0u);
-      if (c <= GRP_SHORT) runs_short[sb + __popc(bs & lt)] = rec;
-      else runs_long[lb + __popc(bl & lt)] = rec;
+      off[r] = ec;
+      const uint4 rec = make_uint4(ec, c, (uint32_t)r, 0u);
+      if (is) runs_short[sb + (es & 0xffffu)] = rec;
+      else runs_long[lb + (es >> 16)] = rec;
     }
+    base += tc;
+    sb += ts & 0xffffu;
+    lb += ts >> 16;
   }
 }
 
@@ -126,7 +167,7 @@ struct GrpArgs {
   float* dots;            // dw (MODE_DV)
   float* G;               // gradient rows (+=)
   uint32_t* ent_rw;       // = ent (in-place sort of very long runs)
-  int H, k;
+  FastDiv div_hk, div_k;  // record -> query: / (H k), / k
 };
 
 // Batched butterfly: U per-lane partial sums -> full warp sums, with
@@ -183,6 +224,17 @@ __device__ __forceinline__ void ldg_vec(const T* p, float* f) {
     }
   }
 }
+// G += v for a row that receives exactly this one update: a fire-and-forget
+// reduction performed in L2 (no load round trip on the SM); with a single
+// addend per element the result is bitwise that of G = G + v.
+template <int VW>
+__device__ __forceinline__ void red_vec(float* p, const float* v) {
+  if constexpr (VW == 4) red_add_v4(p, v[0], v[1], v[2], v[3]);
+  else {
+#pragma unroll
+    for (int i = 0; i < VW; ++i) atomicAdd(p + i, v[i]);
+  }
+}
 template <int VW>
 __device__ __forceinline__ void stg_vec(float* p, const float* v) {
   if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
@@ -192,8 +244,8 @@ __device__ __forceinline__ void stg_vec(float* p, const float* v) {
 
 template <int MODE>
 __device__ __forceinline__ uint32_t grp_xrow(const GrpArgs& a, uint32_t rec) {
-  if constexpr (MODE == MODE_DV) return rec / (uint32_t)(a.H * a.k);
-  else return (rec >> 1) / (uint32_t)a.k * 2u + (rec & 1u);
+  if constexpr (MODE == MODE_DV) return a.div_hk.div(rec);
+  else return a.div_k.div(rec >> 1) * 2u + (rec & 1u);
 }
 
 // Sums the entries src(j), j in [j0, j1), of one row into acc (in j order),
@@ -253,12 +305,13 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // Short runs (<= 32 entries): one warp per run, persistent grid-stride over
 // the short-run list.  Lane j holds entry j; the warp ranks the record ids
 // (entries are then consumed in ascending record order).  The value row
-// (MODE_DV), the gradient row and the first U x rows of a run are requested
-// together; the next run's record, ids and weights are loaded one iteration
-// ahead (the record after that two ahead), so a run costs about one memory
-// round trip.  G = G + sum, one read and one coalesced write per row.
+// (MODE_DV) and the first U x rows of a run are requested together; the next
+// run's record, ids and weights are loaded one iteration ahead (the record
+// after that two ahead), so a run costs about one memory round trip.  The
+// row sum is added to G by one vector reduction per lane (red.global.add,
+// performed in L2): the row's only update, so G = G + sum bitwise.
 template <int MODE, typename XT, typename YT, int EPL>
-__global__ void __launch_bounds__(256, 4) grp_reduce_short_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : 4)) grp_reduce_short_kernel(GrpArgs a) {
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
@@ -282,13 +335,11 @@ __global__ void __launch_bounds__(256, 4) grp_reduce_short_kernel(GrpArgs a) {
     const int len = (int)cur.y;
     const uint32_t ce = me;
     const float cw = mw;
-    float y[MODE == MODE_DV ? EPL : 1], g[EPL], acc[EPL];
+    float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
       for (int i = 0; i < NVEC; ++i) ldg_vec<YT, VW>(Y + (int64_t)key * D + i * 32 * VW, y + i * VW);
     }
-#pragma unroll
-    for (int i = 0; i < NVEC; ++i) ldg_vec<float, VW>(Gl + (int64_t)key * D + i * 32 * VW, g + i * VW);
     // next run's entries and the record after it
     const uint4 nn = c + 2 * nw < nruns ? a.runs_short[c + 2 * nw] : make_uint4(0, 0, 0, 0);
     me = 0xffffffffu;
@@ -312,9 +363,7 @@ __global__ void __launch_bounds__(256, 4) grp_reduce_short_kernel(GrpArgs a) {
         },
         y, acc);
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) acc[i] += g[i];
-#pragma unroll
-    for (int i = 0; i < NVEC; ++i) stg_vec<VW>(Gl + (int64_t)key * D + i * 32 * VW, acc + i * VW);
+    for (int i = 0; i < NVEC; ++i) red_vec<VW>(Gl + (int64_t)key * D + i * 32 * VW, acc + i * VW);
     cur = nxt;
     nxt = nn;
   }
@@ -402,8 +451,7 @@ __global__ void __launch_bounds__(256) grp_reduce_long_kernel(GrpArgs a) {
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) t += s_part[w * D + e];
-      float* gp = a.G + (int64_t)key * D + e;
-      *gp = *gp + t;
+      atomicAdd(a.G + (int64_t)key * D + e, t);  // the row's only update: deterministic
     }
     __syncthreads();
   }
@@ -445,7 +493,7 @@ template <int MODE, typename XT, typename YT, int EPL>
 cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream_t st,
                          int* launches) {
   const int sms = num_sms();
-  int64_t sb = (int64_t)sms * 4;
+  int64_t sb = (int64_t)sms * (EPL >= 16 ? 2 : 4);
   const int64_t sneed = ((n < (int64_t)nrows ? n : (int64_t)nrows) + 7) / 8;
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
@@ -473,15 +521,16 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
                        const void* X, const void* Y, float* dots, float* G, int H, int k, int D,
                        cudaStream_t st, int* launches) {
   if (n == 0 || nrows == 0) return cudaSuccess;
-  int64_t rb = ((int64_t)nrows + 255) / 256;
-  if (rb > (int64_t)num_sms() * 8) rb = (int64_t)num_sms() * 8;
+  int64_t rb = ((int64_t)nrows + 1023) / 1024;
+  if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
   grp_runs_kernel<<<(unsigned)rb, 256, 0, st>>>(g.cnt, nrows, g.off, g.runs_short, g.runs_long, g.ctl);
   grp_place_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g.keys, g.rank, g.off, wts, n, nrows,
                                                                 g.ent, g.went);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 2;
-  GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.ctl, X, Y, dots, G, g.ent, H, k};
+  GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.ctl, X, Y, dots, G, g.ent,
+            FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
   switch (D / 32) {
     case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches);
     case 2: return grp_reduce_t<MODE, XT, YT, 2>(a, n, nrows, st, launches);

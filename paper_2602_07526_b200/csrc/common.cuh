@@ -61,6 +61,23 @@ __device__ __forceinline__ int warp_sum_int(int v) {
   return v;
 }
 
+// Division by a runtime constant d >= 1 without the integer-divide sequence:
+// q = (umulhi(n, m) + n) >> s with s = ceil(log2 d) and
+// m = floor(2^32 (2^s - d) / d) + 1, exact for every 32-bit n
+// (Granlund-Montgomery); set up once on the host.
+struct FastDiv {
+  uint32_t m, s, d;
+  __host__ FastDiv() : m(0), s(0), d(1) {}
+  __host__ explicit FastDiv(uint32_t d_) : d(d_) {
+    s = 0;
+    while ((1ull << s) < d) ++s;
+    m = (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
+  }
+};
+
 // ---- element loads/conversions --------------------------------------------
 template <typename T> struct elem;
 template <> struct elem<float> {
