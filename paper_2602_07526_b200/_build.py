@@ -8,11 +8,13 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libmsn_pkm.so")
+BUILD = os.environ.get("MSN_BUILD_DIR", os.path.join(HERE, "build"))
+LIB = os.environ.get("MSN_LIB_OUT", os.path.join(HERE, "libmsn_pkm.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# experiment variants only (e.g. "-DMSN_SHORT_U=4"), built into MSN_BUILD_DIR / MSN_LIB_OUT
+FLAGS += os.environ.get("MSN_EXTRA_FLAGS", "").split()
 
 
 def _stale(obj, src):

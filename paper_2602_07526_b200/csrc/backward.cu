@@ -15,7 +15,7 @@
 //   3. ds = w (dw - sum w dw) (softmax Jacobian), dQ (=) per lookup, and one
 //      record per distinct (lookup, half, sub-key) with the aggregated dS;
 //   4. group the records by sub-key row and reduce them into dK (+=) the same
-//      way (bf16 configs with n_sub <= 1024 use the tensor cores instead).
+//      way (bf16 configs with n_sub <= 2048 use the tensor cores instead).
 // Atomic path (MSN_FLAG_ATOMIC_BWD): query-major re-gather with
 // red.global.add.v4.f32 into dV (non-deterministic summation order).
 #include <stdlib.h>
@@ -54,21 +54,35 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 // the reducers sort each run's record ids before summing, so every gradient
 // row is summed in a fixed order (ascending record id inside a warp's slice)
 // -- bitwise repeatable, independent of the atomics.
+#ifndef MSN_SHORT_U
+#define MSN_SHORT_U 2  // x rows in flight per warp in the short-run reducer (8 values/lane)
+#endif
+#ifndef MSN_SHORT_BPS
+#define MSN_SHORT_BPS 4  // resident blocks per SM of the short-run reducer (8 values/lane)
+#endif
 constexpr int GRP_SHORT = 32;     // runs up to this length: one warp, one entry per lane
-constexpr int GRP_SMEM_MAX = 16384;  // long runs sorted in shared memory up to this length
-enum { CTL_TOTAL = 0, CTL_NSHORT = 1, CTL_NLONG = 2, CTL_WORDS = 8 };
+constexpr int GRP_PIECE = 256;       // long runs are reduced in pieces of this many entries
+constexpr int GRP_SORT_SMEM = 16384;  // long runs sorted in shared memory up to this length
+enum { CTL_TOTAL = 0, CTL_NSHORT = 1, CTL_NLONG = 2, CTL_NPIECES = 3, CTL_WORDS = 8 };
+__host__ __device__ __forceinline__ uint32_t grp_npieces(uint32_t c) {
+  return c > GRP_SHORT ? (c + GRP_PIECE - 1) / GRP_PIECE : 0u;
+}
+// sum of grp_npieces over runs of total length n: <= n / 33 + 1 pieces
+inline int64_t grp_pieces_max(int64_t n) { return n / (GRP_SHORT + 1) + 1; }
 
-// Each block owns a contiguous range of rows: pass 1 counts its entries and
-// short/long runs, one atomic per counter per block reserves its output
-// ranges, pass 2 writes offsets and run records (block-ordered: a block
-// scan over 256-row rounds).
+// Each block owns a contiguous range of rows: pass 1 counts its entries,
+// short and long runs and long-run pieces; one atomic per counter per block
+// reserves its output ranges; pass 2 writes the offsets, the run records
+// {offset, length, row, first piece} and the piece records {long run, j}
+// (block-ordered: block scans over 256-row rounds).
 __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restrict__ cnt,
                                                        uint32_t nrows, uint32_t* __restrict__ off,
                                                        uint4* __restrict__ runs_short,
                                                        uint4* __restrict__ runs_long,
+                                                       uint2* __restrict__ pieces,
                                                        uint32_t* __restrict__ ctl) {
-  __shared__ uint32_t sh[3][8];
-  __shared__ uint32_t s_base[3];
+  __shared__ uint32_t sh[4][8];
+  __shared__ uint32_t s_base[4];
   const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
   const int64_t per = ((int64_t)nrows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = (int64_t)blockIdx.x * per;
@@ -76,61 +90,73 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
   if (r1 > nrows) r1 = nrows;
   if (r0 >= r1) return;
   // pass 1: block totals
-  uint32_t tot = 0, ns = 0, nl = 0;
+  uint32_t t4[4] = {0, 0, 0, 0};
   for (int64_t r = r0 + tid; r < r1; r += 256) {
     const uint32_t c = cnt[r];
-    tot += c;
-    ns += (c > 0 && c <= GRP_SHORT);
-    nl += (c > GRP_SHORT);
+    t4[0] += c;
+    t4[1] += (c > 0 && c <= GRP_SHORT);
+    t4[2] += (c > GRP_SHORT);
+    t4[3] += grp_npieces(c);
   }
-  tot = (uint32_t)warp_sum_int((int)tot);
-  ns = (uint32_t)warp_sum_int((int)ns);
-  nl = (uint32_t)warp_sum_int((int)nl);
-  if (lane == 0) { sh[0][wid] = tot; sh[1][wid] = ns; sh[2][wid] = nl; }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    t4[i] = (uint32_t)warp_sum_int((int)t4[i]);
+    if (lane == 0) sh[i][wid] = t4[i];
+  }
   __syncthreads();
-  if (tid < 3) {
+  if (tid < 4) {
     uint32_t t = 0;
     for (int w = 0; w < 8; ++w) t += sh[tid][w];
-    s_base[tid] = t ? atomicAdd(&ctl[tid == 0 ? CTL_TOTAL : (tid == 1 ? CTL_NSHORT : CTL_NLONG)], t) : 0u;
+    s_base[tid] = t ? atomicAdd(&ctl[tid], t) : 0u;  // CTL_TOTAL, CTL_NSHORT, CTL_NLONG, CTL_NPIECES
   }
   __syncthreads();
-  uint32_t base = s_base[0], sb = s_base[1], lb = s_base[2];
+  uint32_t base = s_base[0], sb = s_base[1], lb = s_base[2], pb = s_base[3];
   __syncthreads();
   // pass 2: ordered rounds of 256 rows
   for (int64_t rr = r0; rr < r1; rr += 256) {
     const int64_t r = rr + tid;
     const uint32_t c = r < r1 ? cnt[r] : 0u;
-    const uint32_t is = (c > 0 && c <= GRP_SHORT), il = (c > GRP_SHORT);
-    // block exclusive scans of (c, is, il), packed: c < 2^32 needs its own scan
-    uint32_t xc = c, xs = is | (il << 16);
+    const uint32_t is = (c > 0 && c <= GRP_SHORT), il = (c > GRP_SHORT), np = grp_npieces(c);
+    // block exclusive scans of c, (is | il << 16) and np
+    uint32_t x[3] = {c, is | (il << 16), np};
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t o1 = __shfl_up_sync(0xffffffffu, xc, d);
-      const uint32_t o2 = __shfl_up_sync(0xffffffffu, xs, d);
-      if (lane >= d) { xc += o1; xs += o2; }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, x[i], d);
+        if (lane >= d) x[i] += o;
+      }
     }
-    if (lane == 31) { sh[0][wid] = xc; sh[1][wid] = xs; }
+    if (lane == 31) { sh[0][wid] = x[0]; sh[1][wid] = x[1]; sh[2][wid] = x[2]; }
     __syncthreads();
-    uint32_t pc = 0, ps = 0, tc = 0, ts = 0;
+    uint32_t pre[3] = {0, 0, 0}, tot[3] = {0, 0, 0};
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      const uint32_t a0 = sh[0][w], a1 = sh[1][w];
-      if (w < wid) { pc += a0; ps += a1; }
-      tc += a0;
-      ts += a1;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint32_t v = sh[i][w];
+        if (w < wid) pre[i] += v;
+        tot[i] += v;
+      }
     }
     __syncthreads();
-    const uint32_t ec = base + pc + xc - c;
-    const uint32_t es = ps + xs - (is | (il << 16));
+    const uint32_t ec = base + pre[0] + x[0] - c;
+    const uint32_t es = pre[1] + x[1] - (is | (il << 16));
+    const uint32_t ep = pb + pre[2] + x[2] - np;
     if (c > 0) {
       off[r] = ec;
-      const uint4 rec = make_uint4(ec, c, (uint32_t)r, 0u);
-      if (is) runs_short[sb + (es & 0xffffu)] = rec;
-      else runs_long[lb + (es >> 16)] = rec;
+      if (is) {
+        runs_short[sb + (es & 0xffffu)] = make_uint4(ec, c, (uint32_t)r, 0u);
+      } else {
+        const uint32_t li = lb + (es >> 16);
+        runs_long[li] = make_uint4(ec, c, (uint32_t)r, ep);
+        for (uint32_t j = 0; j < np; ++j) pieces[ep + j] = make_uint2(li, j);
+      }
     }
-    base += tc;
-    sb += ts & 0xffffu;
-    lb += ts >> 16;
+    base += tot[0];
+    sb += tot[1] & 0xffffu;
+    lb += tot[1] >> 16;
+    pb += tot[2];
   }
 }
 
@@ -161,6 +187,8 @@ struct GrpArgs {
   const float* wts;       // weight by record id
   const uint4* runs_short;
   const uint4* runs_long;
+  const uint2* pieces;    // long-run pieces {long run, j}
+  float* part;            // per-piece partial rows (runs with >= 2 pieces)
   const uint32_t* ctl;
   const void* X;          // x rows (dOut fp32 or Q)
   const void* Y;          // V (MODE_DV dot)
@@ -311,11 +339,11 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // row sum is added to G by one vector reduction per lane (red.global.add,
 // performed in L2): the row's only update, so G = G + sum bitwise.
 template <int MODE, typename XT, typename YT, int EPL>
-__global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : 4)) grp_reduce_short_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4))) grp_reduce_short_kernel(GrpArgs a) {
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
-  constexpr int U = EPL >= 8 ? 2 : 4;
+  constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_U : 4);
   const int lane = threadIdx.x % 32;
   const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
   int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
@@ -373,14 +401,13 @@ __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : 4)) grp_reduce_short_ker
 // by the block, in shared or global memory; the variant whose every
 // compare-exchange puts the minimum at the lower index, so elements past
 // the real length (treated as +inf) never move and need no storage.
-template <bool SHARED>
-__device__ void block_bitonic(uint32_t* v, int64_t L, int64_t P) {
-  for (int64_t k = 2; k <= P; k <<= 1) {
-    for (int64_t j = k >> 1; j > 0; j >>= 1) {
-      for (int64_t i = threadIdx.x; i < P / 2; i += blockDim.x) {
-        const int64_t lo = (i / j) * 2 * j + (i % j);
+__device__ void block_bitonic(uint32_t* v, int L, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // (i / j) * 2j + i % j
         // first step of a stage compares lo with its mirror inside the k-block
-        const int64_t b = (j == (k >> 1)) ? ((lo & ~(k - 1)) + (k - 1 - (lo & (k - 1)))) : lo + j;
+        const int b = (j == (k >> 1)) ? ((lo & ~(k - 1)) | (k - 1 - (lo & (k - 1)))) : lo + j;
         if (b >= L) continue;  // partner is +inf padding: nothing moves
         const uint32_t x = v[lo], y = v[b];
         if (y < x) {
@@ -393,40 +420,51 @@ __device__ void block_bitonic(uint32_t* v, int64_t L, int64_t P) {
   }
 }
 
-// Long runs (> 32 entries): one CTA (8 warps) per run, grid-stride over the
-// long-run list.  The run's record ids are sorted ascending (shared memory
-// up to GRP_SMEM_MAX, else in place in global memory); warp w sums the w-th
-// contiguous slice in order; the 8 slice sums are added in warp order, plus
-// the old gradient row: a fixed, scheduling-independent summation order.
+// Long runs (> 32 entries), step 1: one CTA per run sorts its record ids
+// ascending in place (shared memory up to GRP_SORT_SMEM entries, else in
+// global memory), fixing the run's summation order.
+__global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
+  extern __shared__ __align__(16) uint32_t s_sort[];  // [GRP_SORT_SMEM]
+  const int64_t nruns = a.ctl[CTL_NLONG];
+  for (int64_t r = blockIdx.x; r < nruns; r += gridDim.x) {
+    const uint4 run = a.runs_long[r];
+    const int L = (int)run.y;
+    int P = 1;
+    while (P < L) P <<= 1;
+    uint32_t* g = a.ent_rw + run.x;
+    if (P <= GRP_SORT_SMEM) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) s_sort[i] = i < L ? g[i] : 0xffffffffu;
+      __syncthreads();
+      block_bitonic(s_sort, P, P);
+      for (int i = threadIdx.x; i < L; i += blockDim.x) g[i] = s_sort[i];
+      __syncthreads();
+    } else {
+      block_bitonic(g, L, P);
+    }
+  }
+}
+
+// Step 2: one CTA per piece of GRP_PIECE consecutive sorted entries (many
+// pieces in flight); warp w sums the w-th 32-entry slice in order, the CTA
+// adds the 8 slice sums in warp order.  A run of one piece adds its sum to G
+// directly (its only update); longer runs leave the piece sum for step 3.
 template <int MODE, typename XT, typename YT, int EPL>
-__global__ void __launch_bounds__(256) grp_reduce_long_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
   constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
-  extern __shared__ __align__(16) uint8_t grp_smem[];
-  uint32_t* s_e = reinterpret_cast<uint32_t*>(grp_smem);                 // [GRP_SMEM_MAX]
-  float* s_part = reinterpret_cast<float*>(s_e + GRP_SMEM_MAX);          // [8][D]
+  __shared__ __align__(16) float s_part[8 * D];
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t nruns = a.ctl[CTL_NLONG];
+  const int64_t np = a.ctl[CTL_NPIECES];
   const YT* __restrict__ Y = reinterpret_cast<const YT*>(a.Y) + lane * VW;
-  for (int64_t r = blockIdx.x; r < nruns; r += gridDim.x) {
-    const uint4 run = a.runs_long[r];
-    const int64_t L = run.y;
+  for (int64_t pc = blockIdx.x; pc < np; pc += gridDim.x) {
+    const uint2 piece = a.pieces[pc];
+    const uint4 run = a.runs_long[piece.x];
+    const int L = (int)run.y;
     const uint32_t key = run.z;
-    int64_t P = 1;
-    while (P < L) P <<= 1;
-    const uint32_t* src;
-    if (P <= GRP_SMEM_MAX) {
-      for (int64_t i = threadIdx.x; i < P; i += blockDim.x) s_e[i] = i < L ? a.ent[run.x + i] : 0xffffffffu;
-      __syncthreads();
-      block_bitonic<true>(s_e, P, P);
-      src = s_e;
-    } else {
-      uint32_t* g = a.ent_rw + run.x;
-      block_bitonic<false>(g, L, P);
-      src = g;
-    }
+    const int j0 = (int)piece.y * GRP_PIECE + wid * 32;
+    const int j1 = min(j0 + 32, min(L, ((int)piece.y + 1) * GRP_PIECE));
     float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
@@ -434,26 +472,57 @@ __global__ void __launch_bounds__(256) grp_reduce_long_kernel(GrpArgs a) {
     }
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
-    const int j0 = (int)(L * wid / 8), j1 = (int)(L * (wid + 1) / 8);
+    // the slice's ids, one per lane, then consumed in order
+    const uint32_t myid = j0 + lane < j1 ? a.ent[run.x + j0 + lane] : 0u;
+    const float myw = j0 + lane < j1 ? a.wts[myid] : 0.f;
     grp_accumulate<MODE, XT, EPL, U>(
         a, j0, j1,
         [&](int j, float& w_) {
-          const uint32_t e = src[j];
-          w_ = a.wts[e];
-          return e;
+          w_ = __shfl_sync(0xffffffffu, myw, (j - j0) & 31);
+          return __shfl_sync(0xffffffffu, myid, (j - j0) & 31);
         },
         y, acc);
 #pragma unroll
     for (int i = 0; i < NVEC; ++i) stg_vec<VW>(s_part + wid * D + lane * VW + i * 32 * VW, acc + i * VW);
     __syncthreads();
-    // slice sums in warp order, plus the old gradient row
+    const bool single = L <= GRP_PIECE;
     for (int e = threadIdx.x; e < D; e += blockDim.x) {
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) t += s_part[w * D + e];
-      atomicAdd(a.G + (int64_t)key * D + e, t);  // the row's only update: deterministic
+      if (single) atomicAdd(a.G + (int64_t)key * D + e, t);  // the row's only update
+      else a.part[pc * D + e] = t;
     }
     __syncthreads();
+  }
+}
+
+// Step 3: one warp per long run of >= 2 pieces: G += the piece sums, added
+// in piece order (one update per element).
+template <int EPL>
+__global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
+  constexpr int VW = EPL < 4 ? EPL : 4;
+  constexpr int NVEC = EPL / VW;
+  constexpr int D = 32 * EPL;
+  const int lane = threadIdx.x % 32;
+  const int64_t nruns = a.ctl[CTL_NLONG];
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < nruns; r += nw) {
+    const uint4 run = a.runs_long[r];
+    const int npc = (int)grp_npieces(run.y);
+    if (npc < 2) continue;
+    float acc[EPL], v[EPL];
+#pragma unroll
+    for (int i = 0; i < NVEC; ++i) ldg_vec<float, VW>(a.part + (int64_t)run.w * D + lane * VW + i * 32 * VW, acc + i * VW);
+    for (int j = 1; j < npc; ++j) {
+#pragma unroll
+      for (int i = 0; i < NVEC; ++i)
+        ldg_vec<float, VW>(a.part + (int64_t)(run.w + j) * D + lane * VW + i * 32 * VW, v + i * VW);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) acc[i] += v[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NVEC; ++i) red_vec<VW>(a.G + (int64_t)run.z * D + lane * VW + i * 32 * VW, acc + i * VW);
   }
 }
 
@@ -478,6 +547,8 @@ struct GrpScratch {
   float* went;      // [n]
   uint4* runs_short;  // [min(n, rows)]
   uint4* runs_long;   // [n / 33 + 1]
+  uint2* pieces;    // [grp_pieces_max(n)]
+  float* part;      // [grp_pieces_max(n) * D]
   uint32_t* ctl;    // CTL_WORDS
 };
 
@@ -493,25 +564,32 @@ template <int MODE, typename XT, typename YT, int EPL>
 cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream_t st,
                          int* launches) {
   const int sms = num_sms();
-  int64_t sb = (int64_t)sms * (EPL >= 16 ? 2 : 4);
+  int64_t sb = (int64_t)sms * (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4));
   const int64_t sneed = ((n < (int64_t)nrows ? n : (int64_t)nrows) + 7) / 8;
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
   grp_reduce_short_kernel<MODE, XT, YT, EPL><<<(unsigned)sb, 256, 0, st>>>(a);
-  const size_t smem = (size_t)GRP_SMEM_MAX * 4 + 8 * 32 * EPL * 4;
+  // long runs: sort, pieces, combine
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grp_reduce_long_kernel<MODE, XT, YT, EPL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(grp_sort_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GRP_SORT_SMEM * 4);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int64_t lb = (int64_t)sms * 2;
+  int64_t lb = (int64_t)sms * 3;
   const int64_t lneed = n / (GRP_SHORT + 1) + 1;
   if (lb > lneed) lb = lneed;
-  grp_reduce_long_kernel<MODE, XT, YT, EPL><<<(unsigned)lb, 256, smem, st>>>(a);
+  grp_sort_long_kernel<<<(unsigned)lb, 256, GRP_SORT_SMEM * 4, st>>>(a);
+  int64_t pb = (int64_t)sms * 8;
+  const int64_t pneed = grp_pieces_max(n);
+  if (pb > pneed) pb = pneed;
+  grp_reduce_piece_kernel<MODE, XT, YT, EPL><<<(unsigned)pb, 256, 0, st>>>(a);
+  int64_t cb = (lneed + 7) / 8;
+  if (cb > (int64_t)sms * 4) cb = (int64_t)sms * 4;
+  grp_combine_long_kernel<EPL><<<(unsigned)cb, 256, 0, st>>>(a);
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) *launches += 2;
+  if (e == cudaSuccess) *launches += 4;
   return e;
 }
 
@@ -523,13 +601,14 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   if (n == 0 || nrows == 0) return cudaSuccess;
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
-  grp_runs_kernel<<<(unsigned)rb, 256, 0, st>>>(g.cnt, nrows, g.off, g.runs_short, g.runs_long, g.ctl);
+  grp_runs_kernel<<<(unsigned)rb, 256, 0, st>>>(g.cnt, nrows, g.off, g.runs_short, g.runs_long,
+                                                g.pieces, g.ctl);
   grp_place_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g.keys, g.rank, g.off, wts, n, nrows,
                                                                 g.ent, g.went);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 2;
-  GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.ctl, X, Y, dots, G, g.ent,
+  GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
   switch (D / 32) {
     case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches);
@@ -569,7 +648,7 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
 // dense bf16 row dSd[b, h*2 + half, 0:n_sub] (zeros elsewhere) for the
 // tensor-core dQ and dK (dk_tc.cu), and dQ is not computed here;
 // n_sub <= kDenseMax.
-constexpr int kDenseMax = 1024;
+constexpr int kDenseMax = 2048;
 template <typename QT, int KPL, int EPL, bool DENSE>
 __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     const int32_t* __restrict__ idx,
@@ -749,14 +828,14 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 namespace {
 struct WsPlan {
-  int64_t n, rows;
+  int64_t n, rows, D;
 };
 WsPlan ws_plan(const Shape& s, int64_t gather_batch) {
   const int64_t n_dv = gather_batch * s.H * s.k;
   const int64_t n_dk = 2 * s.B * s.H * s.k;
   const int64_t r_dv = s.row_end - s.row_begin;
   const int64_t r_dk = (int64_t)s.H * 2 * s.n_sub;
-  return WsPlan{n_dv > n_dk ? n_dv : n_dk, r_dv > r_dk ? r_dv : r_dk};
+  return WsPlan{n_dv > n_dk ? n_dv : n_dk, r_dv > r_dk ? r_dv : r_dk, s.d_v > s.d_h ? s.d_v : s.d_h};
 }
 }  // namespace
 
@@ -770,6 +849,8 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   b += 4 * align256(sizeof(uint32_t) * pl.n);               // rank, keys, ent, went
   b += align256(sizeof(uint4) * nshort);                    // runs_short
   b += align256(sizeof(uint4) * (pl.n / (GRP_SHORT + 1) + 1));  // runs_long
+  b += align256(sizeof(uint2) * grp_pieces_max(pl.n));             // pieces
+  b += align256(sizeof(float) * grp_pieces_max(pl.n) * pl.D);      // piece partials
   b += align256(sizeof(uint32_t) * CTL_WORDS);
   b += align256(sizeof(float) * n_dk);                      // dsS
   b += align256(sizeof(float) * n_dv);                      // dw
@@ -792,6 +873,8 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.went = (float*)p; p += align256(sizeof(uint32_t) * pl.n);
   w.runs_short = (uint4*)p; p += align256(sizeof(uint4) * nshort);
   w.runs_long = (uint4*)p; p += align256(sizeof(uint4) * (pl.n / (GRP_SHORT + 1) + 1));
+  w.pieces = (uint2*)p; p += align256(sizeof(uint2) * grp_pieces_max(pl.n));
+  w.part = (float*)p; p += align256(sizeof(float) * grp_pieces_max(pl.n) * pl.D);
   w.ctl = (uint32_t*)p; p += align256(sizeof(uint32_t) * CTL_WORDS);
   w.dsS = (float*)p; p += align256(sizeof(float) * n_dk);
   w.dw = (float*)p; p += align256(sizeof(float) * n_dv);
@@ -802,7 +885,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
 // ------------------------------------------------------------ launchers ---
 static GrpScratch grp_scratch(const BwdWorkspace& ws) {
   return GrpScratch{ws.cnt, ws.off, ws.rank, ws.keys, ws.ent, ws.went, ws.runs_short, ws.runs_long,
-                    ws.ctl};
+                    ws.pieces, ws.part, ws.ctl};
 }
 
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,

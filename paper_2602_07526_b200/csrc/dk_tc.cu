@@ -318,7 +318,7 @@ size_t dense_ds_bytes(const Shape& s) {
 bool dk_tc_supported(const Shape& s) {
   // dense work = 2 n_sub d_h per (query, half) vs ~2 k d_h for the sparse path:
   // worth it while n_sub is small (C2: 512); C4 (2048) keeps the sort path.
-  return s.qk_dt == BF16 && s.n_sub <= 1024 && s.n_sub % kBM == 0 && s.d_h % 64 == 0 &&
+  return s.qk_dt == BF16 && s.n_sub <= 2048 && s.n_sub % kBM == 0 && s.d_h % 64 == 0 &&
          s.d_h >= 64 && s.d_h <= 256 && s.k <= 64 && dk_smem_bytes(s) <= 227 * 1024 &&
          dq_smem_bytes(s) <= 227 * 1024 && get_encode() != nullptr;
 }

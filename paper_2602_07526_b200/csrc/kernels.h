@@ -60,7 +60,9 @@ struct BwdWorkspace {
   uint32_t *cnt, *off;            // per-row counts / segment offsets (grouping)
   uint32_t *rank, *keys, *ent;    // per-contribution rank, row key, grouped record ids
   float* went;                    // grouped weights
-  uint4 *runs_short, *runs_long;  // run records {offset, length, row}
+  uint4 *runs_short, *runs_long;  // run records {offset, length, row, first piece}
+  uint2* pieces;                  // long-run pieces {long run, j}
+  float* part;                    // piece partial rows
   uint32_t* ctl;                  // grouping counters
   float* dsS;                     // 2*B*H*k aggregated score grads
   float* dw;                      // B*H*k (when the caller gives none)
