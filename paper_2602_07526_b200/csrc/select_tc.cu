@@ -342,22 +342,61 @@ __global__ void __launch_bounds__(kThreads, 1)
       // first-segment overflow) into the dummy row kCap.
       const int cnt_old = cnt;
       const int col_base = c * p.n_tile;
-      auto piece = [&](uint32_t (&r)[32], int j0) {
-        if (!first) {
-          int nsel = 0;
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) nsel += (__uint_as_float(r[jj]) > tau) ? 1 : 0;
-          if (__any_sync(0xffffffffu, cnt + nsel > kCap)) tighten();  // cnt <= KT; tau only rises
-        }
+      // Fast path (no overflow possible in this piece: cnt + 32 <= kCap):
+      // per column one compare, one predicated shared store and one
+      // predicated pointer increment -- no branches.  Otherwise the exact hit
+      // count decides (later segments tighten the buffer first; first-segment
+      // overflow goes to the dummy row kCap and the exact path below).
+      auto piece = [&](const uint32_t (&r)[32], int j0) {
         const uint32_t colj = (uint32_t)(col_base + j0);
+        if (__any_sync(0xffffffffu, cnt + 32 > kCap)) {
+          int nsel = 0;
+          if (first) {
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const float v = __uint_as_float(r[jj]);
-          const bool sel = first ? v >= tau : v > tau;
-          const int slot = sel ? min(cnt, kCap) : kCap;
-          cand[slot * 128 + tid] = make_uint2(r[jj], colj + jj);
-          cnt += sel ? 1 : 0;
+            for (int jj = 0; jj < 32; ++jj) nsel += __uint_as_float(r[jj]) >= tau ? 1 : 0;
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) nsel += __uint_as_float(r[jj]) > tau ? 1 : 0;
+            if (__any_sync(0xffffffffu, cnt + nsel > kCap)) tighten();  // cnt <= KT; tau only rises
+          }
+          if (__any_sync(0xffffffffu, cnt + 32 > kCap)) {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const float v = __uint_as_float(r[jj]);
+              const bool sel = first ? v >= tau : v > tau;
+              const int slot = sel ? min(cnt, kCap) : kCap;
+              cand[slot * 128 + tid] = make_uint2(r[jj], colj + jj);
+              cnt += sel ? 1 : 0;
+            }
+            return;
+          }
         }
+        uint32_t ptr = smem_u32(cand + cnt * 128 + tid);
+        const uint32_t ptr0 = ptr;
+        if (first) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            asm volatile(
+                "{\n.reg .pred p;\n"
+                "setp.ge.f32 p, %1, %2;\n"
+                "@p st.shared.v2.u32 [%0], {%3, %4};\n"
+                "@p add.u32 %0, %0, 1024;\n}\n"
+                : "+r"(ptr)
+                : "f"(__uint_as_float(r[jj])), "f"(tau), "r"(r[jj]), "r"(colj + jj)
+                : "memory");
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            asm volatile(
+                "{\n.reg .pred p;\n"
+                "setp.gt.f32 p, %1, %2;\n"
+                "@p st.shared.v2.u32 [%0], {%3, %4};\n"
+                "@p add.u32 %0, %0, 1024;\n}\n"
+                : "+r"(ptr)
+                : "f"(__uint_as_float(r[jj])), "f"(tau), "r"(r[jj]), "r"(colj + jj)
+                : "memory");
+        }
+        cnt += (int)((ptr - ptr0) >> 10);
       };
       for (int j0 = 0; j0 < seg_cols; j0 += 32) {
         uint32_t r[32];
@@ -420,18 +459,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // coalesced write-out: the warp writes its 32 rows one after another
     // (lane = candidate slot), instead of 32 rows per store instruction
-    for (int rr = 0; rr < 32; ++rr) {
-      const int n = __shfl_sync(0xffffffffu, cnt, rr);
-      const int trow = q * 32 + rr;
-      const int64_t b = m0 + trow;
-      if (b >= p.B) continue;
-      const int64_t orow = b * p.H * 2 + hh;
-      for (int i = lane; i < n; i += 32) {
-        const uint2 e = cand[i * 128 + trow];
-        p.cv[orow * kCandCap + i] = __uint_as_float(e.x);
-        p.cc[orow * kCandCap + i] = (int32_t)e.y;
+    // (row, slot half) tasks, 8 in flight: their shared-memory reads and
+    // global stores are independent
+    {
+      const int64_t b_me = m0 + q * 32 + lane;
+      if (b_me < p.B) p.cn[b_me * p.H * 2 + hh] = cnt;
+    }
+    for (int t0 = 0; t0 < 64; t0 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u, rr = t >> 1, i = (t & 1) * 32 + lane;
+        const int n = __shfl_sync(0xffffffffu, cnt, rr);
+        const int trow = q * 32 + rr;
+        const int64_t b = m0 + trow;
+        if (b < p.B && i < n) {
+          const uint2 e = cand[i * 128 + trow];
+          const int64_t o = (b * p.H * 2 + hh) * kCandCap + i;
+          p.cv[o] = __uint_as_float(e.x);
+          p.cc[o] = (int32_t)e.y;
+        }
       }
-      if (lane == 0) p.cn[orow] = n;
     }
     if (ts_on && warp == kEpiWarp0 && lane == 0) g_dbg_ts[cta_lin * 32 + 14] = gclk();
   }
