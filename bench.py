@@ -39,11 +39,15 @@ def _dtype_name(dt):
 
 
 def load_peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the
+    fallback figures of /opt/skills/guides/B200_PROFILING.md (6.65 TB/s,
+    1.59 PFLOP/s bf16 burst, ~1.4 sustained)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d, "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        return d, "of measured (MEASURED_PEAKS.json)"
+    return ({"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0},
+            "of fallback (B200_PROFILING.md: no MEASURED_PEAKS.json on this box)")
 
 
 # ------------------------------------------------------------- clocks -----
@@ -198,10 +202,15 @@ def run_ours(args, rank, world, local_rank):
         if evs:
             check(lib.msn_pkm_set_trace_events(h, None, 0))
             evs[3].record(stream)
+        if evs:
+            arr = (ctypes.c_void_p * 2)(evs[6].cuda_event, evs[7].cuda_event)
+            check(lib.msn_pkm_set_trace_events(h, arr, 2))
         check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(dOut), _ptr(V), _ptr(dV), _ptr(dw),
                                   _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
-        if evs: evs[4].record(stream)
+        if evs:
+            check(lib.msn_pkm_set_trace_events(h, None, 0))
+            evs[4].record(stream)
         check(lib.msn_pkm_backward_keys(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(dw), _ptr(dQ),
                                         _ptr(dK), _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
@@ -212,10 +221,10 @@ def run_ours(args, rank, world, local_rank):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
     for e in evs:  # create the CUDA events up front (torch creates them lazily on record)
-        e[1].record(stream)
-        e[2].record(stream)
+        for j in (1, 2, 6, 7):
+            e[j].record(stream)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -235,6 +244,9 @@ def run_ours(args, rank, world, local_rank):
         for j, p in enumerate(phases):
             per[p] += e[j].elapsed_time(e[j + 1])
     total_ms = sum(per.values())
+    # the short-run dV reducer alone (events recorded inside msn_pkm_scatter);
+    # 0 when the atomic backward runs
+    reduce_ms = sum(e[6].elapsed_time(e[7]) for e in evs) / args.steps if not args.atomic else 0.0
     ms_step = total_ms / args.steps
     t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
     if world > 1:
@@ -285,17 +297,42 @@ def run_ours(args, rank, world, local_rank):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(args.workload, {}).get("gather")
     fused = cfg.batch >= 8192 and cfg.heads * cfg.k <= 256
-    roof = {"kernel": ("cartesian_gather (a3+a4+a5 fused)" if fused else "gather (a5, sparse gather + weighted sum)"),
-            "bound": "hbm",
-            "achieved": ab["gather"] / (g_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": ab["gather"] / (g_ms / 1e3) / 1e9 / hbm, "traffic": traffic,
-            "algorithmic_bytes": ab["gather"], "peak_kind": peaks_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
+    sel_ms = per["select"] / args.steps
+    tf32 = cfg.qk_dtype == torch.float32
+    # candidate roofline kernels, each with its own bound; the dominant one
+    # (longest per step) is reported as "roofline"
+    bf16_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+    cands = {
+        "gather": {"kernel": ("cartesian_gather (a3+a4+a5 fused)" if fused else "gather_kernel (a5)"),
+                   "bound": "hbm", "ms": g_ms, "work": ab["gather"], "peak": hbm, "unit": "GB/s",
+                   "traffic": traffic},
+        "dv_reduce": {"kernel": "grp_reduce_short_kernel (a6: dV += w dOut, dw, runs <= 32)",
+                      "bound": "hbm", "ms": reduce_ms, "work": ab["scatter"], "peak": hbm, "unit": "GB/s",
+                      "traffic": None},
+        "select": {"kernel": "select_tc_kernel (a1+a2, tcgen05 %s)" % ("3xTF32" if tf32 else "bf16"),
+                   "bound": "tensor", "ms": sel_ms,
+                   "work": ab["select_flops"] * (3 if tf32 else 1),
+                   # TF32 dense peak = bf16 / 2 (nominal ratio, B200_PROFILING.md)
+                   "peak": bf16_peak / (2 if tf32 else 1), "unit": "TFLOP/s", "traffic": None},
+    }
+    dom = max((c for c in cands if cands[c]["ms"] > 0), key=lambda c: cands[c]["ms"])
+    rl = {}
+    for name, c in cands.items():
+        if c["ms"] <= 0:
+            continue
+        scale = 1e9 if c["unit"] == "GB/s" else 1e12
+        ach = c["work"] / (c["ms"] / 1e3) / scale
+        rl[name] = {"kernel": c["kernel"], "bound": c["bound"], "achieved": ach, "peak": c["peak"],
+                    "unit": c["unit"], "frac": ach / c["peak"], "traffic": c["traffic"],
+                    "ms": c["ms"], "algorithmic": c["work"], "peak_kind": peaks_kind}
+    roof = dict(rl[dom])
+    roof["dominant_of"] = sorted(rl)
     kernels = {p: {"ms": per[p] / args.steps, "share": per[p] / total_ms} for p in phases}
-    kernels["gather"]["GBps"] = roof["achieved"]
+    kernels["rooflines"] = rl
+    kernels["gather"]["GBps"] = rl["gather"]["achieved"]
     kernels["scatter"]["GBps"] = ab["scatter"] / (s_ms / 1e3) / 1e9
     kernels["scatter"]["algorithmic_bytes"] = ab["scatter"]
     kernels["scatter"]["unique_rows"] = ab["unique_rows"]
-    sel_ms = per["select"] / args.steps
     kernels["select"]["TFLOPs"] = ab["select_flops"] / (sel_ms / 1e3) / 1e12
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -298,7 +298,8 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* 
       return fail(MSN_ERR_WORKSPACE, "scatter workspace %zu < %zu bytes", workspace_bytes, need);
     const BwdWorkspace ws = carve_bwd_workspace(shape_of(h->cfg, 0), B, workspace);
     e = launch_scatter_sorted(s, idx, weights, d_out, values, d_values, dw, ws, cs,
-                              &h->last_launches);
+                              &h->last_launches,
+                              TraceEvents{h->trace, h->ntrace});
   }
   if (e != cudaSuccess) return cuda_fail(e, "scatter (dV, dw)");
   return MSN_OK;

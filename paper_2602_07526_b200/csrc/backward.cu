@@ -420,15 +420,74 @@ __device__ void block_bitonic(uint32_t* v, int L, int P) {
   }
 }
 
-// Long runs (> 32 entries), step 1: one CTA per run sorts its record ids
-// ascending in place (shared memory up to GRP_SORT_SMEM entries, else in
-// global memory), fixing the run's summation order.
+// Warp-wide ascending bitonic sort of 32*R keys held as x[r] (element
+// e = r*32 + lane): shuffles for strides < 32, register swaps above.
+template <int R>
+__device__ __forceinline__ void warp_sort_asc(uint32_t (&x)[R]) {
+  const int lane = threadIdx.x % 32;
+#pragma unroll
+  for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int r2 = r ^ (stride / 32);
+          if (r2 > r) {
+            const bool asc = ((r * 32 + lane) & size) == 0;
+            const uint32_t a = x[r], b = x[r2];
+            const bool sw = asc ? (a > b) : (a < b);
+            x[r] = sw ? b : a;
+            x[r2] = sw ? a : b;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = r * 32 + lane;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, x[r], stride);
+          const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
+          x[r] = keep_min ? min(x[r], o) : max(x[r], o);
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sort_run(uint32_t* g, int L) {
+  const int lane = threadIdx.x % 32;
+  uint32_t x[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) x[r] = r * 32 + lane < L ? g[r * 32 + lane] : 0xffffffffu;
+  warp_sort_asc<R>(x);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r * 32 + lane < L) g[r * 32 + lane] = x[r];
+}
+
+// Long runs (> 32 entries), step 1: every run's record ids are sorted
+// ascending in place, fixing its summation order.  Runs of <= 1024 entries:
+// one warp each, in registers; longer runs (then): one CTA each, in shared
+// memory up to GRP_SORT_SMEM entries, else in place in global memory.
 __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
   extern __shared__ __align__(16) uint32_t s_sort[];  // [GRP_SORT_SMEM]
   const int64_t nruns = a.ctl[CTL_NLONG];
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < nruns; r += nw) {
+    const uint4 run = a.runs_long[r];
+    const int L = (int)run.y;
+    uint32_t* g = a.ent_rw + run.x;
+    if (L <= 64) warp_sort_run<2>(g, L);
+    else if (L <= 128) warp_sort_run<4>(g, L);
+    else if (L <= 256) warp_sort_run<8>(g, L);
+    else if (L <= 512) warp_sort_run<16>(g, L);
+    else if (L <= 1024) warp_sort_run<32>(g, L);
+  }
   for (int64_t r = blockIdx.x; r < nruns; r += gridDim.x) {
     const uint4 run = a.runs_long[r];
     const int L = (int)run.y;
+    if (L <= 1024) continue;
     int P = 1;
     while (P < L) P <<= 1;
     uint32_t* g = a.ent_rw + run.x;
@@ -562,13 +621,15 @@ cudaError_t grp_begin(const GrpScratch& g, uint32_t nrows, cudaStream_t st) {
 
 template <int MODE, typename XT, typename YT, int EPL>
 cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream_t st,
-                         int* launches) {
+                         int* launches, const TraceEvents& tr) {
   const int sms = num_sms();
   int64_t sb = (int64_t)sms * (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4));
   const int64_t sneed = ((n < (int64_t)nrows ? n : (int64_t)nrows) + 7) / 8;
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
+  if (tr.n > 0) cudaEventRecord(tr.ev[0], st);  // profiling: the short-run reducer alone
   grp_reduce_short_kernel<MODE, XT, YT, EPL><<<(unsigned)sb, 256, 0, st>>>(a);
+  if (tr.n > 1) cudaEventRecord(tr.ev[1], st);
   // long runs: sort, pieces, combine
   static bool attr = false;
   if (!attr) {
@@ -577,9 +638,9 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int64_t lb = (int64_t)sms * 3;
   const int64_t lneed = n / (GRP_SHORT + 1) + 1;
-  if (lb > lneed) lb = lneed;
+  int64_t lb = (lneed + 7) / 8;
+  if (lb > (int64_t)sms * 3) lb = (int64_t)sms * 3;
   grp_sort_long_kernel<<<(unsigned)lb, 256, GRP_SORT_SMEM * 4, st>>>(a);
   int64_t pb = (int64_t)sms * 8;
   const int64_t pneed = grp_pieces_max(n);
@@ -597,7 +658,7 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
 template <int MODE, typename XT, typename YT>
 cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const float* wts,
                        const void* X, const void* Y, float* dots, float* G, int H, int k, int D,
-                       cudaStream_t st, int* launches) {
+                       cudaStream_t st, int* launches, const TraceEvents& tr = TraceEvents{}) {
   if (n == 0 || nrows == 0) return cudaSuccess;
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
@@ -611,11 +672,11 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
   switch (D / 32) {
-    case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches);
-    case 2: return grp_reduce_t<MODE, XT, YT, 2>(a, n, nrows, st, launches);
-    case 4: return grp_reduce_t<MODE, XT, YT, 4>(a, n, nrows, st, launches);
-    case 8: return grp_reduce_t<MODE, XT, YT, 8>(a, n, nrows, st, launches);
-    case 16: return grp_reduce_t<MODE, XT, YT, 16>(a, n, nrows, st, launches);
+    case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches, tr);
+    case 2: return grp_reduce_t<MODE, XT, YT, 2>(a, n, nrows, st, launches, tr);
+    case 4: return grp_reduce_t<MODE, XT, YT, 4>(a, n, nrows, st, launches, tr);
+    case 8: return grp_reduce_t<MODE, XT, YT, 8>(a, n, nrows, st, launches, tr);
+    case 16: return grp_reduce_t<MODE, XT, YT, 16>(a, n, nrows, st, launches, tr);
     default: return cudaErrorNotSupported;
   }
 }
@@ -890,7 +951,8 @@ static GrpScratch grp_scratch(const BwdWorkspace& ws) {
 
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
-                                  const BwdWorkspace& ws, cudaStream_t st, int* launches) {
+                                  const BwdWorkspace& ws, cudaStream_t st, int* launches,
+                                  const TraceEvents& tr) {
   if (!epl_ok(s.d_v)) return cudaErrorNotSupported;
   const int64_t n = s.B * s.H * s.k;  // s.B is the gather batch here
   if (n == 0) return cudaSuccess;
@@ -905,9 +967,9 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
   ++*launches;
   if (s.v_dt == F32)
     return grp_finish<MODE_DV, float, float>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k, s.d_v, st,
-                                             launches);
+                                             launches, tr);
   return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k,
-                                                   s.d_v, st, launches);
+                                                   s.d_v, st, launches, tr);
 }
 
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,

@@ -80,10 +80,18 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* K, float* dQ
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 
+// Optional profiling events recorded around an internal stage.
+struct TraceEvents {
+  const cudaEvent_t* ev = nullptr;
+  int n = 0;
+};
+
 // a6 deterministic: group (idx -> cid) by row, then fused row-major dV += / dw.
+// tr: events around the short-run reducer (profiling only).
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
-                                  const BwdWorkspace& ws, cudaStream_t st, int* launches);
+                                  const BwdWorkspace& ws, cudaStream_t st, int* launches,
+                                  const TraceEvents& tr = TraceEvents{});
 // a6 atomic: query-major re-gather + red.global.add.v4.f32.
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
