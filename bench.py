@@ -292,10 +292,11 @@ def run_ours(args, rank, world, local_rank):
     g_ms = per["gather"] / args.steps
     s_ms = per["scatter"] / args.steps
     hbm = float(peaks["hbm_gbs"])
-    traffic = None
+    traffic, traffic_dv = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(args.workload, {}).get("gather")
+        tj = json.load(open(tp)).get(args.workload, {})
+        traffic, traffic_dv = tj.get("gather"), tj.get("dv_reduce")
     fused = cfg.batch >= 8192 and cfg.heads * cfg.k <= 256
     sel_ms = per["select"] / args.steps
     tf32 = cfg.qk_dtype == torch.float32
@@ -308,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
                    "traffic": traffic},
         "dv_reduce": {"kernel": "grp_reduce_short_kernel (a6: dV += w dOut, dw, runs <= 32)",
                       "bound": "hbm", "ms": reduce_ms, "work": ab["scatter"], "peak": hbm, "unit": "GB/s",
-                      "traffic": None},
+                      "traffic": traffic_dv},
         "select": {"kernel": "select_tc_kernel (a1+a2, tcgen05 %s)" % ("3xTF32" if tf32 else "bf16"),
                    "bound": "tensor", "ms": sel_ms,
                    "work": ab["select_flops"] * (3 if tf32 else 1),
