@@ -168,6 +168,28 @@ def test_full_size_invariants(name):
                      parity.rtol_for(cfg.value_dtype), (~aff).reshape(-1), "dw (sampled)")
 
 
+# --------------------------------------------------- hot rows (grouping) --
+@pytest.mark.parametrize("B,H,dt", [(400, 2, torch.float32),     # runs of 33..1024: warp sort, pieces
+                                    (3000, 2, torch.float32),    # > 1024: CTA sort in shared memory
+                                    (20000, 1, torch.float32)])  # > 16384: in-place sort in global memory
+def test_hot_rows_long_runs(B, H, dt):
+    """Near-identical queries: every lookup selects (almost) the same slots,
+    so a few dV rows and dK rows receive thousands of contributions each --
+    the long-run grouping paths.  Oracle parity and bitwise repeatability."""
+    cfg = wl.tiny_config(B, H, 32, 64, 32, 4, dt, dt, index=11)
+    _, K, V, dOut = wl.make_all(cfg, DEV)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    base = torch.randn((1, H, 2, 32), generator=g)
+    Q = (base + 1e-3 * torch.randn((B, H, 2, 32), generator=g)).to(dt).to(DEV)
+    r1 = run_fwd_bwd(cfg, Q, K, V, dOut)
+    rows, counts = torch.unique(r1["idx"].reshape(-1), return_counts=True)
+    assert int(counts.max()) > {400: 32, 3000: 1024, 20000: 16384}[B]
+    r2 = run_fwd_bwd(cfg, Q, K, V, dOut)
+    for key in ("dQ", "dK", "dV", "dw"):
+        assert torch.equal(r1[key], r2[key]), key
+    check_all(cfg, Q, K, V, dOut, r1)
+
+
 # ---------------------------------------------------------- properties ----
 def test_determinism_bitwise():
     cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=1024)
