@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
                                                        uint4* __restrict__ runs_long,
                                                        uint2* __restrict__ pieces,
                                                        uint32_t* __restrict__ ctl) {
+  pdl_enter();
   __shared__ uint32_t sh[4][8];
   __shared__ uint32_t s_base[4];
   const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(256) grp_place_kernel(const uint32_t* __restri
                                                         const float* __restrict__ wts, int64_t n,
                                                         uint32_t nrows, uint32_t* __restrict__ ent,
                                                         float* __restrict__ went) {
+  pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t k = keys[p];
@@ -340,6 +342,7 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // performed in L2): the row's only update, so G = G + sum bitwise.
 template <int MODE, typename XT, typename YT, int EPL>
 __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4))) grp_reduce_short_kernel(GrpArgs a) {
+  pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
@@ -471,6 +474,7 @@ __device__ __forceinline__ void warp_sort_run(uint32_t* g, int L) {
 // one warp each, in registers; longer runs (then): one CTA each, in shared
 // memory up to GRP_SORT_SMEM entries, else in place in global memory.
 __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
+  pdl_enter();
   extern __shared__ __align__(16) uint32_t s_sort[];  // [GRP_SORT_SMEM]
   const int64_t nruns = a.ctl[CTL_NLONG];
   const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
@@ -509,6 +513,7 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
 // directly (its only update); longer runs leave the piece sum for step 3.
 template <int MODE, typename XT, typename YT, int EPL>
 __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
+  pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
@@ -560,6 +565,7 @@ __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
 // in piece order (one update per element).
 template <int EPL>
 __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
+  pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
@@ -613,10 +619,21 @@ struct GrpScratch {
 
 // zero the row counters and the control words (the counts are accumulated by
 // the kernel that produces the keys)
+__global__ void __launch_bounds__(256) grp_zero_kernel(uint32_t* __restrict__ a, int64_t na,
+                                                       uint32_t* __restrict__ b, int64_t nb) {
+  pdl_enter();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += stride) {
+    if (i < na) a[i] = 0u;
+    else b[i - na] = 0u;
+  }
+}
+
 cudaError_t grp_begin(const GrpScratch& g, uint32_t nrows, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(g.ctl, 0, CTL_WORDS * sizeof(uint32_t), st);
-  if (e != cudaSuccess) return e;
-  return cudaMemsetAsync(g.cnt, 0, sizeof(uint32_t) * (size_t)nrows, st);
+  int64_t blocks = ((int64_t)nrows + CTL_WORDS + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  return launch_pdl(grp_zero_kernel, (unsigned)blocks, 256, 0, st, g.ctl, (int64_t)CTL_WORDS, g.cnt,
+                    (int64_t)nrows);
 }
 
 template <int MODE, typename XT, typename YT, int EPL>
@@ -628,7 +645,7 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
   if (tr.n > 0) cudaEventRecord(tr.ev[0], st);  // profiling: the short-run reducer alone
-  grp_reduce_short_kernel<MODE, XT, YT, EPL><<<(unsigned)sb, 256, 0, st>>>(a);
+  launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL>, (unsigned)sb, 256, 0, st, a);
   if (tr.n > 1) cudaEventRecord(tr.ev[1], st);
   // long runs: sort, pieces, combine
   static bool attr = false;
@@ -641,14 +658,14 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   const int64_t lneed = n / (GRP_SHORT + 1) + 1;
   int64_t lb = (lneed + 7) / 8;
   if (lb > (int64_t)sms * 3) lb = (int64_t)sms * 3;
-  grp_sort_long_kernel<<<(unsigned)lb, 256, GRP_SORT_SMEM * 4, st>>>(a);
+  launch_pdl(grp_sort_long_kernel, (unsigned)lb, 256, GRP_SORT_SMEM * 4, st, a);
   int64_t pb = (int64_t)sms * 8;
   const int64_t pneed = grp_pieces_max(n);
   if (pb > pneed) pb = pneed;
-  grp_reduce_piece_kernel<MODE, XT, YT, EPL><<<(unsigned)pb, 256, 0, st>>>(a);
+  launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL>, (unsigned)pb, 256, 0, st, a);
   int64_t cb = (lneed + 7) / 8;
   if (cb > (int64_t)sms * 4) cb = (int64_t)sms * 4;
-  grp_combine_long_kernel<EPL><<<(unsigned)cb, 256, 0, st>>>(a);
+  launch_pdl(grp_combine_long_kernel<EPL>, (unsigned)cb, 256, 0, st, a);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) *launches += 4;
   return e;
@@ -662,9 +679,9 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   if (n == 0 || nrows == 0) return cudaSuccess;
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
-  grp_runs_kernel<<<(unsigned)rb, 256, 0, st>>>(g.cnt, nrows, g.off, g.runs_short, g.runs_long,
+  launch_pdl(grp_runs_kernel, (unsigned)rb, 256, 0, st, g.cnt, nrows, g.off, g.runs_short, g.runs_long,
                                                 g.pieces, g.ctl);
-  grp_place_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g.keys, g.rank, g.off, wts, n, nrows,
+  launch_pdl(grp_place_kernel, (unsigned)((n + 255) / 256), 256, 0, st, g.keys, g.rank, g.off, wts, n, nrows,
                                                                 g.ent, g.went);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -689,6 +706,7 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
                                int64_t row_end, uint32_t sentinel, uint32_t* __restrict__ keys,
                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ rank,
                                float* __restrict__ dw) {
+  pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int64_t f = idx[p];
@@ -722,6 +740,7 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     uint32_t* __restrict__ cnt,
                                                     uint32_t* __restrict__ rank,
                                                     uint16_t* __restrict__ dSd) {
+  pdl_enter();
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   __shared__ int32_t s_r[8][64];
   __shared__ float s_d[8][64];
@@ -846,6 +865,7 @@ __global__ void __launch_bounds__(256) scatter_atomic_kernel(const int32_t* __re
                                                              float* __restrict__ dw, int64_t B,
                                                              int HK, int d_v, int64_t row_begin,
                                                              int64_t row_end) {
+  pdl_enter();
   const int lane = threadIdx.x % 32;
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (b >= B) return;
@@ -960,7 +980,7 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
   const GrpScratch g = grp_scratch(ws);
   cudaError_t e = grp_begin(g, nrows, st);
   if (e != cudaSuccess) return e;
-  dv_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n, s.row_begin, s.row_end,
+  launch_pdl(dv_keys_kernel, (unsigned)((n + 255) / 256), 256, 0, st, idx, n, s.row_begin, s.row_end,
                                                               nrows, g.keys, g.cnt, g.rank, dw);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -979,7 +999,7 @@ cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const floa
   const unsigned blocks = (unsigned)((s.B + 7) / 8);
   const int HK = s.H * s.k;
 #define ATOMIC(VT, E)                                                                          \
-  scatter_atomic_kernel<VT, E><<<blocks, 256, 0, st>>>(idx, w, dOut, (const VT*)V, dV, dw, s.B, \
+  launch_pdl(scatter_atomic_kernel<VT, E>, blocks, 256, 0, st, idx, w, dOut, (const VT*)V, dV, dw, s.B, \
                                                        HK, s.d_v, s.row_begin, s.row_end)
   const int E = epl_of(s.d_v);
   if (s.v_dt == F32) {
@@ -1015,11 +1035,11 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   }
 #define DSDQ(QT, KPL, E_)                                                                      \
   if (dense)                                                                                   \
-    ds_dq_kernel<QT, KPL, E_, true><<<blocks, 256, 0, st>>>(                                   \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, true>, blocks, 256, 0, st,                                    \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, (uint16_t*)ws.dk_ws);                                                   \
   else                                                                                         \
-    ds_dq_kernel<QT, KPL, E_, false><<<blocks, 256, 0, st>>>(                                  \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, false>, blocks, 256, 0, st,                                   \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, nullptr)
 #define DSDQ_E(QT, KPL)                                                                        \

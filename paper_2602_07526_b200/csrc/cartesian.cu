@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w) {
+  pdl_enter();
   __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
     float* __restrict__ out, int d_v) {
+  pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;
   __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
@@ -299,7 +301,7 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
   const int R = s.d_v * (int)sizeof(VT) / 16;
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
-  cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U><<<blocks, 256, 0, st>>>(                  \
+  launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
       cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v)
   if (R >= 128) { if (R > 128) return cudaErrorNotSupported; FUSED(4, 1, 4); }
   else if (R > 32) FUSED(2, 1, 8);
@@ -335,9 +337,9 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
   const int64_t L = s.B * s.H;
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (s.k <= 32)
-    cartesian_kernel<32, 119><<<blocks, 256, 0, st>>>(cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w);
+    launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w);
   else if (s.k <= 64)
-    cartesian_kernel<64, 280><<<blocks, 256, 0, st>>>(cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w);
+    launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w);
   else
     return cudaErrorNotSupported;
   cudaError_t e = cudaGetLastError();

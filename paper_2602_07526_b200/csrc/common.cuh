@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #ifndef __CUDACC__
 #error "CUDA only"
@@ -11,6 +12,37 @@
 namespace msn {
 
 constexpr int kWarp = 32;
+
+// Programmatic dependent launch.  Every kernel of the library starts with
+// pdl_enter(): wait until the previous grid in the stream has completed (and
+// its writes are visible), then allow the next grid to be scheduled -- so a
+// kernel's launch and prologue overlap its predecessor's tail, and, since
+// every kernel waits, completion stays ordered transitively.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// Wait only: the next grid is scheduled when this one exits (for a kernel
+// whose CTAs must not share the machine with the next grid's waiting CTAs).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Host side: launch with programmatic stream serialization.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool off = getenv("MSN_NO_PDL") != nullptr;  // A/B measurements only
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
 
 // Order-preserving map fp32 -> uint32 (larger float -> larger uint).  -0 is
 // canonicalised to +0 first so equal scores tie-break on the index

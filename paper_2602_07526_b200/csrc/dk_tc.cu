@@ -55,6 +55,7 @@ constexpr uint32_t idesc_bf16_mn(int M, int N) {
 __global__ void __launch_bounds__(kThreads, 1)
     dk_gemm_kernel(const __grid_constant__ CUtensorMap tmap_ds,
                    const __grid_constant__ CUtensorMap tmap_q, const DkParams p) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   const int nb = p.d_h / 64;                          // B atoms per stage
@@ -182,6 +183,7 @@ struct DqParams {
 __global__ void __launch_bounds__(kThreads, 1)
     dq_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_k, const DqParams p) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   const int nb = p.d_h / 64;                      // B atoms per stage
@@ -285,6 +287,7 @@ size_t dq_smem_bytes(const Shape& s) {
 // dK += sum_s part[s] (fixed split order)
 __global__ void dk_reduce_kernel(const float4* __restrict__ part, float4* __restrict__ dK,
                                  int64_t n4, int S) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   float4 acc = part[i];
@@ -392,7 +395,7 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
     }
     DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ};
     dim3 qgrid((unsigned)((s.B + 127) / 128), HH);
-    dq_gemm_kernel<<<qgrid, kThreads, dq_smem_bytes(s), st>>>(ma, mk, qp);
+    launch_pdl(dq_gemm_kernel, qgrid, kThreads, dq_smem_bytes(s), st, ma, mk, qp);
     cudaError_t e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return e1;
     ++*launches;
@@ -409,13 +412,13 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
     attr = true;
   }
   dim3 grid(s.n_sub / kBM, HH, S);
-  dk_gemm_kernel<<<grid, kThreads, dk_smem_bytes(s), st>>>(mds, mq, p);
+  launch_pdl(dk_gemm_kernel, grid, kThreads, dk_smem_bytes(s), st, mds, mq, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
   if (S > 1) {
     const int64_t n4 = (int64_t)HH * s.n_sub * s.d_h / 4;
-    dk_reduce_kernel<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>((const float4*)part, (float4*)dK,
+    launch_pdl(dk_reduce_kernel, (unsigned)((n4 + 255) / 256), 256, 0, st, (const float4*)part, (float4*)dK,
                                                                    n4, S);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
                                                      float* __restrict__ out, int64_t B, int HK,
                                                      int d_v, int64_t row_begin,
                                                      int64_t row_end) {
+  pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;  // lanes per row
   __shared__ int32_t s_idx[kWarps][kMaxHK];
@@ -100,7 +101,7 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
   const int HK = s.H * s.k;
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);
 #define GATHER(VPL, G, U)                                                                      \
-  gather_kernel<VT, VPL, G, U><<<blocks, 256, 0, st>>>(idx, w, V, out, s.B, HK, s.d_v,         \
+  launch_pdl(gather_kernel<VT, VPL, G, U>, blocks, 256, 0, st, idx, w, V, out, s.B, HK, s.d_v,         \
                                                        s.row_begin, s.row_end)
   if (R >= 128) { if (R > 128) return cudaErrorNotSupported; GATHER(4, 1, 4); }
   else if (R > 32) GATHER(2, 1, 8);

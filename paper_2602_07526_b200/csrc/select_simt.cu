@@ -20,6 +20,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) score_kernel(const T* __restrict__ Q, const T* __restrict__ K,
                                                     float* __restrict__ S, int64_t B, int H,
                                                     int n_sub, int d_h) {
+  pdl_enter();
   __shared__ float As[TK][TB + 4];
   __shared__ float Bs[TK][TN + 4];
   const int hh = blockIdx.z;  // h*2 + half
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict_
                                                         int n_sub, int k, float* __restrict__ cv,
                                                         int32_t* __restrict__ cc,
                                                         int32_t* __restrict__ cn) {
+  pdl_enter();
   const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= rows) return;
@@ -105,7 +107,7 @@ template <int NPL>
 cudaError_t launch_topk(const float* S, int64_t rows, int n_sub, int k, const Cands& cd,
                         cudaStream_t st) {
   const int64_t blocks = (rows + 7) / 8;
-  topk_rows_kernel<NPL><<<(unsigned)blocks, 256, 0, st>>>(S, rows, n_sub, k, cd.v, cd.c, cd.n);
+  launch_pdl(topk_rows_kernel<NPL>, (unsigned)blocks, 256, 0, st, S, rows, n_sub, k, cd.v, cd.c, cd.n);
   return cudaGetLastError();
 }
 
@@ -115,10 +117,10 @@ cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, flo
                                const Cands& cd, cudaStream_t st, int* launches) {
   dim3 grid((s.n_sub + TN - 1) / TN, (unsigned)((s.B + TB - 1) / TB), s.H * 2);
   if (s.qk_dt == F32)
-    score_kernel<float><<<grid, 256, 0, st>>>((const float*)Q, (const float*)K, scores_ws, s.B, s.H,
+    launch_pdl(score_kernel<float>, grid, 256, 0, st, (const float*)Q, (const float*)K, scores_ws, s.B, s.H,
                                               s.n_sub, s.d_h);
   else
-    score_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)Q,
+    launch_pdl(score_kernel<__nv_bfloat16>, grid, 256, 0, st, (const __nv_bfloat16*)Q,
                                                       (const __nv_bfloat16*)K, scores_ws, s.B,
                                                       s.H, s.n_sub, s.d_h);
   cudaError_t e = cudaGetLastError();

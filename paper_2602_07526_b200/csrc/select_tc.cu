@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     select_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                      const __grid_constant__ CUtensorMap tmap_k,
                      const __grid_constant__ CUtensorMap tmap_klo, const TcParams p) {
+  pdl_wait();
   constexpr int BK = TF32 ? 32 : 64;            // elements per k-block (one 128-B row)
   constexpr int B_PARTS = TF32 ? 2 : 1;         // B tiles per stage: (K_hi, K_lo) or K
   const int acc_stride = TF32 ? p.n_tile : kMaxNTile;  // TMEM columns between accumulators
@@ -515,6 +516,7 @@ size_t smem_bytes(const Shape& s) {
 // K -> (K_hi, K_lo) for the 3xTF32 B operand.
 __global__ void split_tf32_kernel(const float* __restrict__ k, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t n) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float x = k[i];
@@ -537,7 +539,7 @@ cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& 
   // x = head/half (fastest): concurrently resident CTAs spread over all 2H
   // sub-key codebooks instead of hammering one codebook's lines in L2
   dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128));
-  select_tc_kernel<KT, TF32><<<grid, kThreads, sm, st>>>(mq, mk, mklo, p);
+  launch_pdl(select_tc_kernel<KT, TF32>, grid, kThreads, sm, st, mq, mk, mklo, p);
   return cudaGetLastError();
 }
 
@@ -586,7 +588,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
   if (tf) {
     float* hi = (float*)ws;
     float* lo = hi + kel;
-    split_tf32_kernel<<<(unsigned)((kel + 255) / 256), 256, 0, st>>>((const float*)K, hi, lo, kel);
+    launch_pdl(split_tf32_kernel, (unsigned)((kel + 255) / 256), 256, 0, st, (const float*)K, hi, lo, kel);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ++*launches;
