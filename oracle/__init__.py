@@ -7,6 +7,8 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 * oracle.pkm_oracle.c  -- plain C fp64 forward / backward / slot scores
 * oracle.oracle         -- ctypes wrapper (numpy in, numpy out)
 * oracle.brute          -- numpy exhaustive full-memory scorer for tiny tables
+* oracle.gate           -- memory-gated fusion x~ = x (.) g(v_o) and its
+                           backward
 
 Parity pins: every function here is pinned by tests/test_oracle_pins.py
 against brute force, closed forms, invariants, finite differences and the
