@@ -161,6 +161,10 @@ def algorithmic_bytes(cfg, idx=None):
     return out
 
 
+def _lib_gate(name):
+    return {"none": 0, "tanh": 1, "sigmoid": 2, "identity": 3}[name]
+
+
 def run_ours(args, rank, world, local_rank):
     from paper_2602_07526_b200 import workloads as wl
     from paper_2602_07526_b200.pkm import PKMLookup, _ptr
@@ -181,6 +185,14 @@ def run_ours(args, rank, world, local_rank):
     dK = torch.zeros((cfg.heads, 2, cfg.n_sub, cfg.d_half), dtype=torch.float32, device=dev)
     dV = torch.zeros((cfg.n_slots, cfg.d_value), dtype=torch.float32, device=dev)
     ws = lk.workspace(B)
+    gate = _lib_gate(args.gate)
+    if gate:
+        # memory-gated fusion: x~ = x * g(v_o), upstream grad on x~
+        gx = torch.Generator(device="cpu").manual_seed(7526 + 6)
+        x_in = torch.randn((B, cfg.d_value), generator=gx).to(dev)
+        x_t = torch.empty_like(x_in)
+        d_xin = torch.empty_like(x_in)
+        d_vo = torch.empty_like(x_in)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -196,16 +208,26 @@ def run_ours(args, rank, world, local_rank):
             evs[0].record(stream)
             arr = (ctypes.c_void_p * 2)(evs[1].cuda_event, evs[2].cuda_event)
             check(lib.msn_pkm_set_trace_events(h, arr, 2))
-        check(lib.msn_pkm_forward(h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(out), _ptr(idx), _ptr(w),
-                                  _ptr(ws), ws.numel()))
+        if gate:
+            check(lib.msn_pkm_forward_gated(h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(x_in), gate,
+                                            _ptr(out), _ptr(x_t), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
+        else:
+            check(lib.msn_pkm_forward(h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(out), _ptr(idx), _ptr(w),
+                                      _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
         if evs:
             check(lib.msn_pkm_set_trace_events(h, None, 0))
             evs[3].record(stream)
+        d_up = dOut
+        if gate:  # the gate backward turns the upstream gradient on x~ into d v_o (counted in scatter)
+            check(lib.msn_pkm_gate_backward(h, sp, B, gate, _ptr(x_in), _ptr(out), _ptr(dOut), _ptr(d_xin),
+                                            _ptr(d_vo)))
+            n += lk.last_launch_count()
+            d_up = d_vo
         if evs:
             arr = (ctypes.c_void_p * 2)(evs[6].cuda_event, evs[7].cuda_event)
             check(lib.msn_pkm_set_trace_events(h, arr, 2))
-        check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(dOut), _ptr(V), _ptr(dV), _ptr(dw),
+        check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(d_up), _ptr(V), _ptr(dV), _ptr(dw),
                                   _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
         if evs:
@@ -347,7 +369,8 @@ def run_ours(args, rank, world, local_rank):
                              "(the roofline kernel); scatter = dV/dw; backward_keys = ds, dQ, dK", "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
                    "lookups_per_step_per_gpu": cfg.batch * cfg.heads,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "backward": "atomic" if args.atomic else "deterministic sort-based",
+                   "backward": "atomic" if args.atomic else "deterministic (grouped by row, per-row id order)",
+                   "gate": args.gate,
                    "l2": "flushed before every step (512 MiB write, outside the timed events)"},
         "roofline": roof,
         "kernels": kernels,
@@ -571,6 +594,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="C4 through the row-sharded path even at N=1")
+    ap.add_argument("--gate", choices=["none", "tanh", "sigmoid", "identity"], default="none",
+                    help="include the memory-gated fusion (SURVEY 8(f) f1) in the step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -70,6 +70,11 @@ typedef enum {
 
 typedef enum { MSN_F32 = 0, MSN_BF16 = 1 } msn_dtype;
 
+/* Memory-gated fusion gate g: x~ = x_in (.) g(v_o),
+ * Eq. gating PAPER.md:318-322 (tanh); sigmoid and identity are the
+ * alternatives of the paper's gate ablation. */
+typedef enum { MSN_GATE_TANH = 1, MSN_GATE_SIGMOID = 2, MSN_GATE_IDENTITY = 3 } msn_gate;
+
 /* flags */
 #define MSN_FLAG_ATOMIC_BWD 0x1u /* value-gradient scatter with red.global.add
                                     (non-deterministic order) instead of the
@@ -110,6 +115,29 @@ msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B,
                            const void* query, const void* subkeys, const void* values,
                            float* out, int32_t* idx, float* weights,
                            void* workspace, size_t workspace_bytes);
+
+/* Forward with the memory-gated fusion fused into the
+ * kernel that produces v_o: everything msn_pkm_forward does, plus
+ *   x_tilde = x_in (.) g(v_o)          (gate per msn_gate)
+ * x_in, x_tilde: [B, d_value] fp32, 16-byte aligned device pointers (the
+ * gate is elementwise, so x_in has the memory output's width).  out (= v_o,
+ * sum over heads) is still written: the gate backward needs it.  Same errors
+ * as msn_pkm_forward; an unknown gate -> MSN_ERR_INVALID_ARG. */
+msn_status msn_pkm_forward_gated(msn_pkm_t h, void* stream, int64_t B,
+                                 const void* query, const void* subkeys, const void* values,
+                                 const float* x_in, int32_t gate, float* out, float* x_tilde,
+                                 int32_t* idx, float* weights,
+                                 void* workspace, size_t workspace_bytes);
+
+/* Backward of the gate for the upstream gradient d_x_tilde [B, d_value]:
+ *   d_x_in = d_x_tilde (.) g(v_o)                       (written, =)
+ *   d_out  = d_x_tilde (.) x_in (.) g'(v_o)             (written, =)
+ * where v_o is the forward's out; d_out is then the upstream gradient of
+ * msn_pkm_backward / msn_pkm_scatter.  All [B, d_value] fp32 device
+ * pointers, 16-byte aligned.  One elementwise kernel; no workspace. */
+msn_status msn_pkm_gate_backward(msn_pkm_t h, void* stream, int64_t B, int32_t gate,
+                                 const float* x_in, const float* v_o, const float* d_x_tilde,
+                                 float* d_x_in, float* d_out);
 
 /* Full backward, steps a6-a8 (unsharded), for the loss with upstream
  * gradient d_out.  d_query is written; d_subkeys and d_values are

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libmsn_pkm.so")
 ABI_VERSION = 1
 MSN_F32, MSN_BF16 = 0, 1
 FLAG_ATOMIC_BWD = 0x1
+GATES = {"tanh": 1, "sigmoid": 2, "identity": 3}  # msn_gate (include/msn_pkm.h)
 
 STATUS = {0: "MSN_OK", 1: "MSN_ERR_INVALID_ARG", 2: "MSN_ERR_UNSUPPORTED", 3: "MSN_ERR_CUDA",
           5: "MSN_ERR_WORKSPACE", 6: "MSN_ERR_INTERNAL"}
@@ -42,6 +43,8 @@ SIGNATURES = {
     "msn_pkm_destroy": [_P],
     "msn_pkm_workspace_size": [_P, _I64, _I64, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)],
     "msn_pkm_forward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
+    "msn_pkm_forward_gated": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P, _SZ],
+    "msn_pkm_gate_backward": [_P, _P, _I64, ctypes.c_int32, _P, _P, _P, _P, _P],
     "msn_pkm_backward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_select": [_P, _P, _I64, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_gather": [_P, _P, _I64, _P, _P, _P, _P],

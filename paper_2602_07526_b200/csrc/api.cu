@@ -90,7 +90,8 @@ msn_status check_batch(msn_pkm_t h, int64_t B) {
 // alone (select) or fused with the gather (forward: values != NULL).
 msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
                      const void* subkeys, int32_t* idx, float* weights, void* ws, size_t ws_bytes,
-                     int* launches, const void* values = nullptr, float* out = nullptr) {
+                     int* launches, const void* values = nullptr, float* out = nullptr,
+                     const Gate& gate = Gate{}) {
   const Shape s = shape_of(h->cfg, B);
   if (ws_bytes < fwd_bytes(s))
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
@@ -114,7 +115,7 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);  // stage boundary: scoring done
   if (values) {
     if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);  // (fused: no separate Cartesian stage)
-    e = launch_cartesian_gather(s, cd, idx, weights, values, out, st, launches);
+    e = launch_cartesian_gather(s, cd, idx, weights, values, out, st, launches, gate);
     if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax + gather");
     return MSN_OK;
   }
@@ -238,9 +239,10 @@ msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B, const int32_t* i
   return MSN_OK;
 }
 
-msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B, const void* query,
-                           const void* subkeys, const void* values, float* out, int32_t* idx,
-                           float* weights, void* workspace, size_t workspace_bytes) {
+static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                             const void* subkeys, const void* values, float* out, int32_t* idx,
+                             float* weights, void* workspace, size_t workspace_bytes,
+                             const Gate& gate) {
   msn_status st = check_handle(h);
   if (st) return st;
   if ((st = check_batch(h, B))) return st;
@@ -261,14 +263,60 @@ msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B, const void* que
   // with warps (one warp per query); small batches keep one warp per lookup
   if (h->cfg.heads * h->cfg.k <= 256 && B >= 8192) {
     return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
-                     &h->last_launches, values, out);
+                     &h->last_launches, values, out, gate);
   }
   if ((st = do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
                       &h->last_launches)))
     return st;
   cudaError_t e = launch_gather(shape_of(h->cfg, B), idx, weights, values, out, cs,
-                                &h->last_launches);
+                                &h->last_launches, gate);
   if (e != cudaSuccess) return cuda_fail(e, "gather");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                           const void* subkeys, const void* values, float* out, int32_t* idx,
+                           float* weights, void* workspace, size_t workspace_bytes) {
+  return do_forward(h, stream, B, query, subkeys, values, out, idx, weights, workspace,
+                    workspace_bytes, Gate{});
+}
+
+msn_status msn_pkm_forward_gated(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                                 const void* subkeys, const void* values, const float* x_in,
+                                 int32_t gate, float* out, float* x_tilde, int32_t* idx,
+                                 float* weights, void* workspace, size_t workspace_bytes) {
+  if (gate < MSN_GATE_TANH || gate > MSN_GATE_IDENTITY)
+    return fail(MSN_ERR_INVALID_ARG, "gate %d is not MSN_GATE_TANH/SIGMOID/IDENTITY", gate);
+  if (B > 0) {
+    REQUIRE_PTR(x_in);
+    REQUIRE_PTR(x_tilde);
+  }
+  Gate g;
+  g.x = x_in;
+  g.xt = x_tilde;
+  g.kind = gate;
+  return do_forward(h, stream, B, query, subkeys, values, out, idx, weights, workspace,
+                    workspace_bytes, g);
+}
+
+msn_status msn_pkm_gate_backward(msn_pkm_t h, void* stream, int64_t B, int32_t gate,
+                                 const float* x_in, const float* v_o, const float* d_x_tilde,
+                                 float* d_x_in, float* d_out) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, B))) return st;
+  h->last_launches = 0;
+  if (gate < MSN_GATE_TANH || gate > MSN_GATE_IDENTITY)
+    return fail(MSN_ERR_INVALID_ARG, "gate %d is not MSN_GATE_TANH/SIGMOID/IDENTITY", gate);
+  if (B == 0) return MSN_OK;
+  REQUIRE_PTR(x_in);
+  REQUIRE_PTR(v_o);
+  REQUIRE_PTR(d_x_tilde);
+  REQUIRE_PTR(d_x_in);
+  REQUIRE_PTR(d_out);
+  cudaError_t e = launch_gate_backward(B, h->cfg.d_value, gate, x_in, v_o, d_x_tilde, d_x_in, d_out,
+                                       (cudaStream_t)stream, &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "gate backward");
   return MSN_OK;
 }
 

@@ -24,6 +24,7 @@
 // parity rule.
 #include "common.cuh"
 #include "kernels.h"
+#include "gate.cuh"
 
 namespace msn {
 namespace {
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
     const float* __restrict__ cand_v, const int32_t* __restrict__ cand_c,
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
-    float* __restrict__ out, int d_v) {
+    float* __restrict__ out, int d_v, Gate gate) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;
@@ -292,17 +293,18 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
               make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
       }
     }
+    if (gate.kind) store_gated<VPL, PER>(gate, b, d_v, gl, row_vecs, acc);
   }
 }
 
 template <int KMAX, int MAXC, typename VT>
 cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float* w, const VT* V,
-                           float* out, cudaStream_t st) {
+                           float* out, cudaStream_t st, const Gate& gate) {
   const int R = s.d_v * (int)sizeof(VT) / 16;
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
   launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
-      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v)
+      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate)
   if (R >= 128) { if (R > 128) return cudaErrorNotSupported; FUSED(4, 1, 4); }
   else if (R > 32) FUSED(2, 1, 8);
   else if (R > 16) FUSED(1, 1, 8);
@@ -318,15 +320,16 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
 }  // namespace
 
 cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* idx, float* w,
-                                    const void* V, float* out, cudaStream_t st, int* launches) {
+                                    const void* V, float* out, cudaStream_t st, int* launches,
+                                    const Gate& gate) {
   if (s.H * s.k > kMaxHK || s.row_begin != 0) return cudaErrorNotSupported;
   cudaError_t e;
   if (s.k <= 32) {
-    e = s.v_dt == F32 ? dispatch_fused<32, 119, float>(s, cd, idx, w, (const float*)V, out, st)
-                      : dispatch_fused<32, 119, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st);
+    e = s.v_dt == F32 ? dispatch_fused<32, 119, float>(s, cd, idx, w, (const float*)V, out, st, gate)
+                      : dispatch_fused<32, 119, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st, gate);
   } else {
-    e = s.v_dt == F32 ? dispatch_fused<64, 280, float>(s, cd, idx, w, (const float*)V, out, st)
-                      : dispatch_fused<64, 280, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st);
+    e = s.v_dt == F32 ? dispatch_fused<64, 280, float>(s, cd, idx, w, (const float*)V, out, st, gate)
+                      : dispatch_fused<64, 280, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st, gate);
   }
   if (e == cudaSuccess) ++*launches;
   return e;

@@ -161,6 +161,26 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Memory-gated fusion gate g and its derivative (tanh;
+// the ablation's sigmoid and identity).  kind: 1 tanh,
+// 2 sigmoid, 3 identity.
+__device__ __forceinline__ float gate_g(float v, int kind) {
+  if (kind == 1) return tanhf(v);
+  if (kind == 2) return 1.0f / (1.0f + expf(-v));
+  return v;
+}
+__device__ __forceinline__ float gate_dg(float v, int kind) {
+  if (kind == 1) {
+    const float t = tanhf(v);
+    return 1.0f - t * t;
+  }
+  if (kind == 2) {
+    const float sg = 1.0f / (1.0f + expf(-v));
+    return sg * (1.0f - sg);
+  }
+  return 1.0f;
+}
+
 // fire-and-forget vector fp32 add into global memory (sm_90+).
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),

@@ -10,6 +10,7 @@
 // vectors per lane when R > 32).
 #include "common.cuh"
 #include "kernels.h"
+#include "gate.cuh"
 
 namespace msn {
 namespace {
@@ -23,7 +24,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
                                                      const VT* __restrict__ V,
                                                      float* __restrict__ out, int64_t B, int HK,
                                                      int d_v, int64_t row_begin,
-                                                     int64_t row_end) {
+                                                     int64_t row_end, Gate gate) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;  // lanes per row
@@ -91,18 +92,19 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
               make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
       }
     }
+    if (gate.kind) store_gated<VPL, PER>(gate, b, d_v, gl, row_vecs, acc);
   }
 }
 
 template <typename VT>
 cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const VT* V, float* out,
-                     cudaStream_t st) {
+                     cudaStream_t st, const Gate& gate) {
   const int R = s.d_v * (int)sizeof(VT) / 16;
   const int HK = s.H * s.k;
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);
 #define GATHER(VPL, G, U)                                                                      \
   launch_pdl(gather_kernel<VT, VPL, G, U>, blocks, 256, 0, st, idx, w, V, out, s.B, HK, s.d_v,         \
-                                                       s.row_begin, s.row_end)
+                                                       s.row_begin, s.row_end, gate)
   if (R >= 128) { if (R > 128) return cudaErrorNotSupported; GATHER(4, 1, 4); }
   else if (R > 32) GATHER(2, 1, 8);
   else if (R > 16) GATHER(1, 1, 8);
@@ -118,10 +120,10 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
 }  // namespace
 
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
-                          float* out, cudaStream_t st, int* launches) {
+                          float* out, cudaStream_t st, int* launches, const Gate& gate) {
   if (s.H * s.k > kMaxHK) return cudaErrorNotSupported;
-  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, out, st)
-                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, out, st);
+  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, out, st, gate)
+                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, out, st, gate);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

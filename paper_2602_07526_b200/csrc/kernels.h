@@ -41,6 +41,14 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
 bool select_tc_supported(const Shape& s);
 size_t select_tc_workspace_bytes(const Shape& s);
 
+// Memory-gated fusion: x~ = x (.) g(v_o), applied in the
+// epilogue of the kernel that produces v_o (kind 0: none).
+struct Gate {
+  const float* x = nullptr;  // [B, d_v]
+  float* xt = nullptr;       // [B, d_v]
+  int kind = 0;              // 1 tanh, 2 sigmoid, 3 identity
+};
+
 // a2 (ordering) + a3 + a4: per-half top-k from the candidate lists, Cartesian
 // top-k over I x J + softmax.  idx/w [B,H,k].
 cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, float* w,
@@ -49,11 +57,17 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
 // a2 (ordering) + a3 + a4 + a5 fused (unsharded forward): Cartesian stage of
 // each query's H lookups, then the gather of their H*k rows.
 cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* idx, float* w,
-                                    const void* V, float* out, cudaStream_t st, int* launches);
+                                    const void* V, float* out, cudaStream_t st, int* launches,
+                                    const Gate& gate = Gate{});
 
 // a5: out[b] = sum over local rows of w * V[idx - row_begin] (=).
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
-                          float* out, cudaStream_t st, int* launches);
+                          float* out, cudaStream_t st, int* launches, const Gate& gate = Gate{});
+
+// f1 backward: dx = dxt (.) g(v_o) (=), dvo = dxt (.) x (.) g'(v_o) (=).
+cudaError_t launch_gate_backward(int64_t B, int d_v, int kind, const float* x, const float* vo,
+                                 const float* dxt, float* dx, float* dvo, cudaStream_t st,
+                                 int* launches);
 
 // ---- backward ----
 struct BwdWorkspace {

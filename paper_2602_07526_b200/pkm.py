@@ -117,6 +117,37 @@ class PKMLookup:
             return out.cpu(), idx.cpu(), w.cpu()
         return out, idx, w
 
+    def forward_gated(self, query: torch.Tensor, subkeys: torch.Tensor, values: torch.Tensor,
+                      x_in: torch.Tensor, gate: str = "tanh"):
+        """a1-a5 plus the memory-gated fusion x~ = x_in * g(v_o) (SURVEY 8(f)
+        f1, PAPER.md:318-322; gate in tanh / sigmoid / identity, PAPER.md:492),
+        fused into the kernel that produces v_o.  Returns (x~, v_o, idx, w)."""
+        self._check_inputs(query, subkeys, values)
+        q, K, V = self._dev(query), self._dev(subkeys), self._dev(values)
+        B = q.shape[0]
+        x = self._dev(x_in).float().contiguous()
+        if tuple(x.shape) != (B, self.d_value):
+            raise ValueError(f"x_in must be [{B},{self.d_value}]")
+        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        xt = torch.empty_like(out)
+        idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        ws = self.workspace(B)
+        _lib.check(self.lib.msn_pkm_forward_gated(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(V), _ptr(x),
+                                                  _lib.GATES[gate], _ptr(out), _ptr(xt), _ptr(idx), _ptr(w),
+                                                  _ptr(ws), ws.numel()))
+        return xt, out, idx, w
+
+    def gate_backward(self, d_xt: torch.Tensor, x_in: torch.Tensor, v_o: torch.Tensor, gate: str = "tanh"):
+        """Backward of the gate: (d_x_in, d_v_o); d_v_o is the d_out of backward()."""
+        d, x, v = (self._dev(t).float().contiguous() for t in (d_xt, x_in, v_o))
+        B = d.shape[0]
+        dx = torch.empty_like(d)
+        dvo = torch.empty_like(d)
+        _lib.check(self.lib.msn_pkm_gate_backward(self._h, _stream(), B, _lib.GATES[gate], _ptr(x), _ptr(v),
+                                                  _ptr(d), _ptr(dx), _ptr(dvo)))
+        return dx, dvo
+
     def select(self, query: torch.Tensor, subkeys: torch.Tensor):
         """a1-a4 only: (idx, w)."""
         self._check_inputs(query, subkeys)

@@ -168,6 +168,45 @@ def test_full_size_invariants(name):
                      parity.rtol_for(cfg.value_dtype), (~aff).reshape(-1), "dw (sampled)")
 
 
+# ------------------------------------------- memory-gated fusion (f1) ----
+@pytest.mark.parametrize("gate", ["tanh", "sigmoid", "identity"])
+@pytest.mark.parametrize("name,B", [("tiny_fp32", 300), ("c2_mid_bf16", 512), ("c3_train_fp32_zipf", 8192)])
+def test_gated_fusion_fwd_bwd(gate, name, B):
+    """x~ = x * g(v_o) fused into the gather epilogue (B >= 8192: into the
+    fused Cartesian + gather kernel), and its backward feeding the lookup
+    backward, against oracle/gate.py on top of the fp64 oracle."""
+    from oracle import gate as og
+    if name == "tiny_fp32":
+        cfg = wl.tiny_config(B, 2, 32, 64, 64, 8, torch.float32, torch.float32, index=12)
+        Q, K, V, dXt = wl.make_all(cfg, DEV)
+    else:
+        cfg = wl.CONFIGS[name]
+        Q = wl.make_queries(cfg, DEV)[:B].contiguous()
+        K, V = wl.make_subkeys(cfg, DEV), wl.make_values(cfg, DEV)
+        dXt = wl.make_dout(cfg, DEV)[:B].contiguous()
+    g = torch.Generator(device="cpu").manual_seed(5)
+    X = torch.randn((B, cfg.d_value), generator=g).to(DEV)
+    lk = lookup_for(cfg, B)
+    xt, vo, idx, w = lk.forward_gated(Q, K, V, X, gate)
+    out2, idx2, w2 = lk.forward(Q, K, V)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, idx2) and torch.equal(w, w2) and torch.equal(vo, out2)
+    if B > 1024:  # oracle on a sample of the queries (full table)
+        sel = slice(0, 512)
+        Qs, dXs, Xs = Q[sel].contiguous(), dXt[sel].contiguous(), X[sel]
+        vo_s, xt_s, idx_s, w_s = vo[sel], xt[sel], idx[sel], w[sel]
+    else:
+        Qs, dXs, Xs, vo_s, xt_s, idx_s, w_s = Q, dXt, X, vo, xt, idx, w
+    rt = parity.rtol_for(cfg.value_dtype)
+    o, aff, _ = parity.check_forward(Qs.cpu(), K.cpu(), V.cpu(), cfg.k, vo_s, idx_s, w_s)
+    ok = ~aff.any(axis=1)
+    parity.row_close(xt_s.cpu().numpy(), og.forward(o["out"], Xs.cpu(), gate), rt, ok, "x~")
+    dx, dvo = lk.gate_backward(dXs, Xs, vo_s, gate)
+    dx_ref, dvo_ref = og.backward(o["out"], Xs.cpu(), dXs.cpu(), gate)
+    parity.row_close(dx.cpu().numpy(), dx_ref, rt, ok, "dx_in")
+    parity.row_close(dvo.cpu().numpy(), dvo_ref, rt, ok, "dv_o")
+
+
 # --------------------------------------------------- hot rows (grouping) --
 @pytest.mark.parametrize("B,H,dt", [(400, 2, torch.float32),     # runs of 33..1024: warp sort, pieces
                                     (3000, 2, torch.float32),    # > 1024: CTA sort in shared memory
