@@ -143,7 +143,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------- our arm ----------
-def algorithmic_bytes(cfg, idx=None):
+def algorithmic_bytes(cfg, idx=None, update="none"):
     """Per-phase algorithmic bytes."""
     esz = 2 if cfg.value_dtype == torch.bfloat16 else 4
     qsz = 2 if cfg.qk_dtype == torch.bfloat16 else 4
@@ -156,6 +156,9 @@ def algorithmic_bytes(cfg, idx=None):
         out["unique_rows"] = uniq
         # V rows read once, dV read+written once (fp32), idx/w/dw, dOut once
         out["scatter"] = uniq * cfg.d_value * (esz + 8) + contrib * 12 + cfg.batch * cfg.d_value * 4
+        if update != "none":  # V read + V written (+ Adagrad state read + written), no dV
+            out["scatter"] = (uniq * cfg.d_value * (2 * esz + (8 if update == "adagrad" else 0))
+                              + contrib * 12 + cfg.batch * cfg.d_value * 4)
     out["select_flops"] = 4 * L * cfg.n_sub * cfg.d_half
     out["select_bytes"] = L * 2 * cfg.d_half * qsz + contrib * 8
     return out
@@ -193,6 +196,8 @@ def run_ours(args, rank, world, local_rank):
         x_t = torch.empty_like(x_in)
         d_xin = torch.empty_like(x_in)
         d_vo = torch.empty_like(x_in)
+    upd = {"none": 0, "sgd": 1, "adagrad": 2}[args.update]
+    ada = torch.zeros((cfg.n_slots, cfg.d_value), dtype=torch.float32, device=dev) if upd == 2 else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -227,8 +232,12 @@ def run_ours(args, rank, world, local_rank):
         if evs:
             arr = (ctypes.c_void_p * 2)(evs[6].cuda_event, evs[7].cuda_event)
             check(lib.msn_pkm_set_trace_events(h, arr, 2))
-        check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(d_up), _ptr(V), _ptr(dV), _ptr(dw),
-                                  _ptr(ws), ws.numel()))
+        if upd:  # f3: the optimiser step fused into the row reduction (no dV buffer)
+            check(lib.msn_pkm_scatter_update(h, sp, B, _ptr(idx), _ptr(w), _ptr(d_up), _ptr(V), upd,
+                                             1e-3, 1e-10, _ptr(ada), _ptr(dw), _ptr(ws), ws.numel()))
+        else:
+            check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(d_up), _ptr(V), _ptr(dV), _ptr(dw),
+                                      _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
         if evs:
             check(lib.msn_pkm_set_trace_events(h, None, 0))
@@ -310,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return None
     peaks, peaks_kind = load_peaks()
-    ab = algorithmic_bytes(cfg, idx)
+    ab = algorithmic_bytes(cfg, idx, args.update)
     g_ms = per["gather"] / args.steps
     s_ms = per["scatter"] / args.steps
     hbm = float(peaks["hbm_gbs"])
@@ -371,6 +380,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "backward": "atomic" if args.atomic else "deterministic (grouped by row, per-row id order)",
                    "gate": args.gate,
+                   "update": args.update,
                    "l2": "flushed before every step (512 MiB write, outside the timed events)"},
         "roofline": roof,
         "kernels": kernels,
@@ -478,6 +488,8 @@ def run_sharded(args, rank, world, local_rank):
     del V, Q, dOut
     dVs = torch.zeros((sp.rows, cfg.d_value), dtype=torch.float32, device=dev)
     dK = torch.zeros((cfg.heads, 2, cfg.n_sub, cfg.d_half), dtype=torch.float32, device=dev)
+    upd = {"none": 0, "sgd": 1, "adagrad": 2}[args.update]
+    ada = torch.zeros((cfg.n_slots, cfg.d_value), dtype=torch.float32, device=dev) if upd == 2 else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -594,6 +606,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="C4 through the row-sharded path even at N=1")
+    ap.add_argument("--update", choices=["none", "sgd", "adagrad"], default="none",
+                    help="fuse the optimiser step into the value-row reduction (SURVEY 8(f) f3)")
     ap.add_argument("--gate", choices=["none", "tanh", "sigmoid", "identity"], default="none",
                     help="include the memory-gated fusion (SURVEY 8(f) f1) in the step")
     args = ap.parse_args()

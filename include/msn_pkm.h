@@ -75,6 +75,10 @@ typedef enum { MSN_F32 = 0, MSN_BF16 = 1 } msn_dtype;
  * alternatives of the paper's gate ablation. */
 typedef enum { MSN_GATE_TANH = 1, MSN_GATE_SIGMOID = 2, MSN_GATE_IDENTITY = 3 } msn_gate;
 
+/* Fused sparse optimiser update (the "gradient updates"
+ * of the paper's Sparse-Gather op), reading R20. */
+typedef enum { MSN_UPDATE_SGD = 1, MSN_UPDATE_ADAGRAD = 2 } msn_update;
+
 /* flags */
 #define MSN_FLAG_ATOMIC_BWD 0x1u /* value-gradient scatter with red.global.add
                                     (non-deterministic order) instead of the
@@ -128,6 +132,24 @@ msn_status msn_pkm_forward_gated(msn_pkm_t h, void* stream, int64_t B,
                                  const float* x_in, int32_t gate, float* out, float* x_tilde,
                                  int32_t* idx, float* weights,
                                  void* workspace, size_t workspace_bytes);
+
+/* Step a6 with the optimiser step fused into the row reduction (SURVEY 8(f)
+ * f3): the value gradient g_r of every touched row r (this handle's rows) is
+ * applied to the table in place instead of being accumulated into a
+ * gradient buffer:
+ *   MSN_UPDATE_SGD      values[r] -= lr * g_r
+ *   MSN_UPDATE_ADAGRAD  state[r] += g_r^2;  values[r] -= lr * g_r / (sqrt(state[r]) + eps)
+ * elementwise in fp32, rounded once (RNE) to value_dtype; untouched rows and
+ * their state are not written.  dw (d loss / d weights) is computed from the
+ * values BEFORE the update, exactly as msn_pkm_scatter does.
+ *   values  [row_end-row_begin, d_value] value_dtype, read and written
+ *   state   [row_end-row_begin, d_value] fp32 (+=), Adagrad only (else may be NULL)
+ * Deterministic (grouped) backward only: with MSN_FLAG_ATOMIC_BWD it returns
+ * MSN_ERR_UNSUPPORTED.  lr, eps >= 0 (else MSN_ERR_INVALID_ARG). */
+msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                                  const float* weights, const float* d_out, void* values,
+                                  int32_t update, float lr, float eps, float* state, float* dw,
+                                  void* workspace, size_t workspace_bytes);
 
 /* Backward of the gate for the upstream gradient d_x_tilde [B, d_value]:
  *   d_x_in = d_x_tilde (.) g(v_o)                       (written, =)

@@ -15,6 +15,7 @@ ABI_VERSION = 1
 MSN_F32, MSN_BF16 = 0, 1
 FLAG_ATOMIC_BWD = 0x1
 GATES = {"tanh": 1, "sigmoid": 2, "identity": 3}  # msn_gate (include/msn_pkm.h)
+UPDATES = {"sgd": 1, "adagrad": 2}                # msn_update
 
 STATUS = {0: "MSN_OK", 1: "MSN_ERR_INVALID_ARG", 2: "MSN_ERR_UNSUPPORTED", 3: "MSN_ERR_CUDA",
           5: "MSN_ERR_WORKSPACE", 6: "MSN_ERR_INTERNAL"}
@@ -45,6 +46,8 @@ SIGNATURES = {
     "msn_pkm_forward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_forward_gated": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_gate_backward": [_P, _P, _I64, ctypes.c_int32, _P, _P, _P, _P, _P],
+    "msn_pkm_scatter_update": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, ctypes.c_float,
+                               ctypes.c_float, _P, _P, _P, _SZ],
     "msn_pkm_backward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_select": [_P, _P, _I64, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_gather": [_P, _P, _I64, _P, _P, _P, _P],

@@ -353,6 +353,40 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* 
   return MSN_OK;
 }
 
+msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                                  const float* weights, const float* d_out, void* values,
+                                  int32_t update, float lr, float eps, float* state, float* dw,
+                                  void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
+  if (update != MSN_UPDATE_SGD && update != MSN_UPDATE_ADAGRAD)
+    return fail(MSN_ERR_INVALID_ARG, "update %d is not MSN_UPDATE_SGD/ADAGRAD", update);
+  if (!(lr >= 0.f) || !(eps >= 0.f)) return fail(MSN_ERR_INVALID_ARG, "lr and eps must be >= 0");
+  if (h->cfg.flags & MSN_FLAG_ATOMIC_BWD)
+    return fail(MSN_ERR_UNSUPPORTED, "the fused update needs the deterministic (grouped) backward");
+  if (B == 0) return MSN_OK;
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(d_out);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(dw);
+  REQUIRE_PTR(workspace);
+  if (update == MSN_UPDATE_ADAGRAD) REQUIRE_PTR(state);
+  const Shape s = shape_of(h->cfg, B);
+  const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
+  if (workspace_bytes < need)
+    return fail(MSN_ERR_WORKSPACE, "scatter workspace %zu < %zu bytes", workspace_bytes, need);
+  const BwdWorkspace ws = carve_bwd_workspace(shape_of(h->cfg, 0), B, workspace);
+  cudaError_t e = launch_scatter_sorted(s, idx, weights, d_out, values, nullptr, dw, ws,
+                                        (cudaStream_t)stream, &h->last_launches,
+                                        TraceEvents{h->trace, h->ntrace}, update, lr, eps,
+                                        update == MSN_UPDATE_ADAGRAD ? state : nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "scatter with fused update");
+  return MSN_OK;
+}
+
 msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B, const void* query,
                                  const void* subkeys, const int32_t* idx, const float* weights,
                                  const float* dw, float* d_query, float* d_subkeys,

@@ -198,7 +198,50 @@ struct GrpArgs {
   float* G;               // gradient rows (+=)
   uint32_t* ent_rw;       // = ent (in-place sort of very long runs)
   FastDiv div_hk, div_k;  // record -> query: / (H k), / k
+  // MODE_DV fused optimiser update: instead of G += g,
+  // V[row] <- V[row] - lr g (upd 1, SGD) or, with s[row] += g^2,
+  // V[row] - lr g / (sqrt(s[row]) + eps) (upd 2, Adagrad); 0: G += g.
+  int upd = 0;
+  float lr = 0.f, eps = 0.f;
+  float* state = nullptr;  // Adagrad accumulator [rows, D]
+  void* Vw = nullptr;      // the value table, written in place
 };
+
+// Applies the fused update to VW consecutive elements at element offset off
+// of the value table: y = their current values, g = their gradients.
+template <typename YT, int VW>
+__device__ __forceinline__ void update_vec(const GrpArgs& a, int64_t off, const float* y,
+                                           const float* g) {
+  float nv[VW];
+#pragma unroll
+  for (int v = 0; v < VW; ++v) {
+    if (a.upd == 2) {
+      const float s = a.state[off + v] + g[v] * g[v];
+      a.state[off + v] = s;
+      nv[v] = y[v] - a.lr * g[v] / (sqrtf(s) + a.eps);
+    } else {
+      nv[v] = y[v] - a.lr * g[v];
+    }
+  }
+  YT* p = reinterpret_cast<YT*>(a.Vw) + off;
+  if constexpr (sizeof(YT) == 4) {
+    if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(nv[0], nv[1], nv[2], nv[3]);
+    else {
+#pragma unroll
+      for (int v = 0; v < VW; ++v) reinterpret_cast<float*>(p)[v] = nv[v];
+    }
+  } else {
+    if constexpr (VW == 4) {
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(nv[0], nv[1]);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(nv[2], nv[3]);
+      *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<const uint32_t*>(&lo),
+                                                *reinterpret_cast<const uint32_t*>(&hi));
+    } else {
+#pragma unroll
+      for (int v = 0; v < VW; ++v) p[v] = __float2bfloat16_rn(nv[v]);
+    }
+  }
+}
 
 // Batched butterfly: U per-lane partial sums -> full warp sums, with
 // (U - 1) + log2(32 / U) shuffles instead of 5U.  Dot u ends in lane
@@ -340,7 +383,7 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // after that two ahead), so a run costs about one memory round trip.  The
 // row sum is added to G by one vector reduction per lane (red.global.add,
 // performed in L2): the row's only update, so G = G + sum bitwise.
-template <int MODE, typename XT, typename YT, int EPL>
+template <int MODE, typename XT, typename YT, int EPL, bool UPD>
 __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4))) grp_reduce_short_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
@@ -393,8 +436,14 @@ __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BP
           return __shfl_sync(0xffffffffu, ce, s);
         },
         y, acc);
+    if constexpr (MODE == MODE_DV && UPD) {
 #pragma unroll
-    for (int i = 0; i < NVEC; ++i) red_vec<VW>(Gl + (int64_t)key * D + i * 32 * VW, acc + i * VW);
+      for (int i = 0; i < NVEC; ++i)
+        update_vec<YT, VW>(a, (int64_t)key * D + (i * 32 + lane) * VW, y + i * VW, acc + i * VW);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NVEC; ++i) red_vec<VW>(Gl + (int64_t)key * D + i * 32 * VW, acc + i * VW);
+    }
     cur = nxt;
     nxt = nn;
   }
@@ -554,8 +603,15 @@ __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) t += s_part[w * D + e];
-      if (single) atomicAdd(a.G + (int64_t)key * D + e, t);  // the row's only update
-      else a.part[pc * D + e] = t;
+      if (!single) {
+        a.part[pc * D + e] = t;
+      } else if (MODE == MODE_DV && a.upd) {
+        const int64_t off = (int64_t)key * D + e;
+        const float yv = elem<YT>::to_f(reinterpret_cast<const YT*>(a.Vw)[off]);
+        update_vec<YT, 1>(a, off, &yv, &t);
+      } else {
+        atomicAdd(a.G + (int64_t)key * D + e, t);  // the row's only update
+      }
     }
     __syncthreads();
   }
@@ -563,7 +619,7 @@ __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
 
 // Step 3: one warp per long run of >= 2 pieces: G += the piece sums, added
 // in piece order (one update per element).
-template <int EPL>
+template <typename YT, int EPL>
 __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
@@ -586,8 +642,18 @@ __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
 #pragma unroll
       for (int i = 0; i < EPL; ++i) acc[i] += v[i];
     }
+    if (a.upd) {
 #pragma unroll
-    for (int i = 0; i < NVEC; ++i) red_vec<VW>(a.G + (int64_t)run.z * D + lane * VW + i * 32 * VW, acc + i * VW);
+      for (int i = 0; i < NVEC; ++i) {
+        const int64_t off = (int64_t)run.z * D + (i * 32 + lane) * VW;
+        float y[VW];
+        ldg_vec<YT, VW>(reinterpret_cast<const YT*>(a.Vw) + off, y);
+        update_vec<YT, VW>(a, off, y, acc + i * VW);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NVEC; ++i) red_vec<VW>(a.G + (int64_t)run.z * D + lane * VW + i * 32 * VW, acc + i * VW);
+    }
   }
 }
 
@@ -645,7 +711,10 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
   if (tr.n > 0) cudaEventRecord(tr.ev[0], st);  // profiling: the short-run reducer alone
-  launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL>, (unsigned)sb, 256, 0, st, a);
+  if (MODE == MODE_DV && a.upd)
+    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, true>, (unsigned)sb, 256, 0, st, a);
+  else
+    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false>, (unsigned)sb, 256, 0, st, a);
   if (tr.n > 1) cudaEventRecord(tr.ev[1], st);
   // long runs: sort, pieces, combine
   static bool attr = false;
@@ -665,17 +734,24 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL>, (unsigned)pb, 256, 0, st, a);
   int64_t cb = (lneed + 7) / 8;
   if (cb > (int64_t)sms * 4) cb = (int64_t)sms * 4;
-  launch_pdl(grp_combine_long_kernel<EPL>, (unsigned)cb, 256, 0, st, a);
+  launch_pdl(grp_combine_long_kernel<YT, EPL>, (unsigned)cb, 256, 0, st, a);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) *launches += 4;
   return e;
 }
 
 // runs + placement + reducers, after the keys and counts exist
+struct UpdateArgs {
+  int kind = 0;  // 0: G += g; 1 SGD; 2 Adagrad (on Y in place)
+  float lr = 0.f, eps = 0.f;
+  float* state = nullptr;
+};
+
 template <int MODE, typename XT, typename YT>
 cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const float* wts,
                        const void* X, const void* Y, float* dots, float* G, int H, int k, int D,
-                       cudaStream_t st, int* launches, const TraceEvents& tr = TraceEvents{}) {
+                       cudaStream_t st, int* launches, const TraceEvents& tr = TraceEvents{},
+                       const UpdateArgs& up = UpdateArgs{}) {
   if (n == 0 || nrows == 0) return cudaSuccess;
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
@@ -688,6 +764,11 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   *launches += 2;
   GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
+  a.upd = up.kind;
+  a.lr = up.lr;
+  a.eps = up.eps;
+  a.state = up.state;
+  a.Vw = const_cast<void*>(Y);
   switch (D / 32) {
     case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches, tr);
     case 2: return grp_reduce_t<MODE, XT, YT, 2>(a, n, nrows, st, launches, tr);
@@ -972,7 +1053,8 @@ static GrpScratch grp_scratch(const BwdWorkspace& ws) {
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
-                                  const TraceEvents& tr) {
+                                  const TraceEvents& tr, int upd, float lr, float eps,
+                                  float* state) {
   if (!epl_ok(s.d_v)) return cudaErrorNotSupported;
   const int64_t n = s.B * s.H * s.k;  // s.B is the gather batch here
   if (n == 0) return cudaSuccess;
@@ -987,9 +1069,9 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
   ++*launches;
   if (s.v_dt == F32)
     return grp_finish<MODE_DV, float, float>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k, s.d_v, st,
-                                             launches, tr);
+                                             launches, tr, UpdateArgs{upd, lr, eps, state});
   return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k,
-                                                   s.d_v, st, launches, tr);
+                                                   s.d_v, st, launches, tr, UpdateArgs{upd, lr, eps, state});
 }
 
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,

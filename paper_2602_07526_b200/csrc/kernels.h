@@ -102,10 +102,13 @@ struct TraceEvents {
 
 // a6 deterministic: group (idx -> cid) by row, then fused row-major dV += / dw.
 // tr: events around the short-run reducer (profiling only).
+// upd: 0 -> dV += g; 1 -> SGD, 2 -> Adagrad applied to V in
+// place (dV unused; state = the Adagrad accumulator [rows, d_v]).
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
-                                  const TraceEvents& tr = TraceEvents{});
+                                  const TraceEvents& tr = TraceEvents{}, int upd = 0,
+                                  float lr = 0.f, float eps = 0.f, float* state = nullptr);
 // a6 atomic: query-major re-gather + red.global.add.v4.f32.
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,

@@ -206,6 +206,23 @@ class PKMLookup:
                                             _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
         return dw
 
+    def scatter_update(self, idx, w, d_out, values, update: str = "sgd", lr: float = 1e-3,
+                       eps: float = 1e-10, state: Optional[torch.Tensor] = None):
+        """a6 with the optimiser step fused: values is updated
+        IN PLACE (SGD / Adagrad on the touched rows, state += g^2 for Adagrad);
+        returns dw (computed from the values before the update)."""
+        idx, w, d = self._dev(idx), self._dev(w), self._dev(d_out)
+        Bg = idx.shape[0]
+        dw = torch.empty((Bg, self.heads, self.k), dtype=torch.float32, device=self.device)
+        f, b = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(self.lib.msn_pkm_workspace_size(self._h, 0, Bg, ctypes.byref(f), ctypes.byref(b)))
+        ws = torch.empty(max(b.value, 1), dtype=torch.uint8, device=self.device) \
+            if self._ws is None or self._ws.numel() < b.value else self._ws
+        _lib.check(self.lib.msn_pkm_scatter_update(self._h, _stream(), Bg, _ptr(idx), _ptr(w), _ptr(d),
+                                                   _ptr(values), _lib.UPDATES[update], float(lr), float(eps),
+                                                   _ptr(state), _ptr(dw), _ptr(ws), ws.numel()))
+        return dw
+
     def backward_keys(self, query, subkeys, idx, w, dw, d_subkeys: Optional[torch.Tensor] = None):
         """a7-a8 given the full dw: (d_query, d_subkeys)."""
         q, K, idx, w, dw = (self._dev(t) for t in (query, subkeys, idx, w, dw))

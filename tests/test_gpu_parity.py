@@ -207,6 +207,62 @@ def test_gated_fusion_fwd_bwd(gate, name, B):
     parity.row_close(dvo.cpu().numpy(), dvo_ref, rt, ok, "dv_o")
 
 
+# ------------------------------------------- fused optimiser update (f3) -
+@pytest.mark.parametrize("update", ["sgd", "adagrad"])
+@pytest.mark.parametrize("name,B", [("tiny_fp32", 300), ("hot_fp32", 3000), ("c2_mid_bf16", 4096)])
+def test_fused_update(update, name, B):
+    """msn_pkm_scatter_update against oracle/update.py applied to the oracle's
+    value gradient: the change of every touched row (and of the Adagrad
+    state), dw, and untouched rows bit-for-bit unchanged."""
+    from oracle import oracle as orc
+    from oracle import update as ou
+    if name == "c2_mid_bf16":
+        cfg = wl.CONFIGS[name]
+        Q, K, V, dOut = wl.make_all(cfg, DEV)
+        lr = 0.5   # bf16 values: steps well above the storage rounding
+    else:
+        cfg = wl.tiny_config(B, 2, 32, 64, 64, 8, torch.float32, torch.float32, index=13)
+        Q, K, V, dOut = wl.make_all(cfg, DEV)
+        if name == "hot_fp32":  # long runs (piece + combine path)
+            g = torch.Generator(device="cpu").manual_seed(13)
+            base = torch.randn((1, 2, 2, 32), generator=g)
+            Q = (base + 1e-3 * torch.randn((B, 2, 2, 32), generator=g)).to(DEV)
+        lr = 1e-2
+    eps = 1e-6
+    lk = lookup_for(cfg, B)
+    out, idx, w = lk.forward(Q, K, V)
+    V0 = V.clone()
+    st = torch.rand(V.shape, generator=torch.Generator(device="cpu").manual_seed(3)).to(DEV) \
+        if update == "adagrad" else None
+    st0 = st.clone() if st is not None else None
+    dw = lk.scatter_update(idx, w, dOut, V, update, lr, eps, st)
+    torch.cuda.synchronize()
+    o = orc.forward(Q.cpu(), K.cpu(), V0.cpu(), cfg.k)
+    gi = idx.cpu().numpy().astype(np.int64)
+    aff, _ = parity.compare_selection(Q.cpu(), K.cpu(), gi, o, cfg.n_sub)
+    assert aff.mean() <= 0.01
+    # the oracle's own selection; rows touched by a lookup whose selection
+    # differs at a tie (either side's slots) are excluded from the comparison
+    bw = orc.backward(Q.cpu(), K.cpu(), V0.cpu(), o["idx"], dOut.cpu(), want_dense_dv=False)
+    Vn, sn = ou.apply(V0.cpu().double().numpy(), bw["rows"], bw["dV"], update, lr, eps,
+                      None if st0 is None else st0.cpu().double().numpy())
+    skip = np.union1d(gi[aff].reshape(-1), o["idx"][aff].reshape(-1))
+    rows = np.setdiff1d(bw["rows"], skip)
+    rt = parity.rtol_for(cfg.value_dtype)
+    delta_gpu = (V.double() - V0.double()).cpu().numpy()[rows]
+    delta_ref = Vn[rows] - V0.cpu().double().numpy()[rows]
+    # bf16 storage: the new value is rounded once (half an ulp of |V_new|)
+    slack = np.abs(Vn[rows]) * (2.0 ** -8 if cfg.value_dtype == torch.bfloat16 else 2.0 ** -23)
+    err = np.abs(delta_gpu - delta_ref)
+    assert (err <= rt * np.abs(delta_ref).max(axis=1, keepdims=True) + slack + 1e-30).all(), float(err.max())
+    untouched = np.setdiff1d(np.arange(V.shape[0]), np.union1d(bw["rows"], gi.reshape(-1)))
+    assert torch.equal(V[torch.as_tensor(untouched, device=DEV)], V0[torch.as_tensor(untouched, device=DEV)])
+    if st is not None:
+        parity.row_close(st.cpu().numpy()[rows], sn[rows], 1e-5, what="adagrad state")
+    parity.row_close(dw.cpu().numpy().reshape(-1, cfg.k), bw["dw"].reshape(-1, cfg.k), rt,
+                     ~aff.reshape(-1), what="dw")
+
+
 # --------------------------------------------------- hot rows (grouping) --
 @pytest.mark.parametrize("B,H,dt", [(400, 2, torch.float32),     # runs of 33..1024: warp sort, pieces
                                     (3000, 2, torch.float32),    # > 1024: CTA sort in shared memory
