@@ -414,8 +414,21 @@ __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BP
 #pragma unroll
       for (int i = 0; i < NVEC; ++i) ldg_vec<YT, VW>(Y + (int64_t)key * D + i * 32 * VW, y + i * VW);
     }
-    // next run's entries and the record after it
+    // next run's entries and the record after it; that run's value row is
+    // pulled into L2 now (two iterations ahead of its use, no registers held)
     const uint4 nn = c + 2 * nw < nruns ? a.runs_short[c + 2 * nw] : make_uint4(0, 0, 0, 0);
+    if constexpr (MODE == MODE_DV) {
+      constexpr int LINES = (D * (int)sizeof(YT) + 127) / 128;
+      if (lane < LINES && c + 2 * nw < nruns)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.Y) +
+                                                       (int64_t)nn.z * D * (int)sizeof(YT) + lane * 128));
+    }
+    {  // ... and its gradient row, which the row's single reduction updates in L2
+      constexpr int GLINES = (D * 4 + 127) / 128;
+      if (!UPD && lane >= 32 - GLINES && c + 2 * nw < nruns)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.G) +
+                                                       (int64_t)nn.z * D * 4 + (31 - lane) * 128));
+    }
     me = 0xffffffffu;
     mw = 0.f;
     if (lane < (int)nxt.y) {
