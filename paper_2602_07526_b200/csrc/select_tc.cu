@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int cnt = 0;
     // exact KT-th (index tie rule) over the buffered candidates -> new tau;
     // keeps exactly the entries that can still be in the top-KT (<= KT).
+    int n_tight = 0;  // profiling (MSN_SELECT_DBG): buffer compactions of this thread
     auto tighten = [&]() {
+      ++n_tight;
       float t[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) t[i] = i < cnt ? __uint_as_float(cand[i * 128 + tid].x) : -INFINITY;
@@ -343,61 +345,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       // first-segment overflow) into the dummy row kCap.
       const int cnt_old = cnt;
       const int col_base = c * p.n_tile;
-      // Fast path (no overflow possible in this piece: cnt + 32 <= kCap):
-      // per column one compare, one predicated shared store and one
-      // predicated pointer increment -- no branches.  Otherwise the exact hit
-      // count decides (later segments tighten the buffer first; first-segment
-      // overflow goes to the dummy row kCap and the exact path below).
+      // One compact code path per 32-column piece (the unrolled variants did
+      // not fit the instruction cache): a column is a hit when v > te, where
+      // te = tau in later segments and the largest float below tau in the
+      // first (ties with tau kept there).  Hit mask; if a later segment's
+      // hits would not fit, compact the buffer first (tau rises) and redo the
+      // mask; then every hit goes to slot cnt + (hits before it), with no
+      // dependency between the stores.  A first-segment overflow stores what
+      // fits and leaves the rest to the exact path below (cnt > kCap).
       auto piece = [&](const uint32_t (&r)[32], int j0) {
         const uint32_t colj = (uint32_t)(col_base + j0);
-        if (__any_sync(0xffffffffu, cnt + 32 > kCap)) {
-          int nsel = 0;
-          if (first) {
+        uint32_t m;
+        for (;;) {
+          const float te = first ? nextafterf(tau, -INFINITY) : tau;
+          m = 0;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) nsel += __uint_as_float(r[jj]) >= tau ? 1 : 0;
-          } else {
+          for (int jj = 0; jj < 32; ++jj) m |= (__uint_as_float(r[jj]) > te ? 1u : 0u) << jj;
+          if (first || !__any_sync(0xffffffffu, cnt + __popc(m) > kCap)) break;
+          tighten();  // cnt <= KT; tau only rises
+        }
+        if (m) {
+          const uint32_t base = smem_u32(cand + tid);
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) nsel += __uint_as_float(r[jj]) > tau ? 1 : 0;
-            if (__any_sync(0xffffffffu, cnt + nsel > kCap)) tighten();  // cnt <= KT; tau only rises
-          }
-          if (__any_sync(0xffffffffu, cnt + 32 > kCap)) {
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              const float v = __uint_as_float(r[jj]);
-              const bool sel = first ? v >= tau : v > tau;
-              const int slot = sel ? min(cnt, kCap) : kCap;
-              cand[slot * 128 + tid] = make_uint2(r[jj], colj + jj);
-              cnt += sel ? 1 : 0;
-            }
-            return;
+          for (int jj = 0; jj < 32; ++jj) {
+            const uint32_t slot = (uint32_t)cnt + (uint32_t)__popc(m & ((1u << jj) - 1u));
+            asm volatile(
+                "{\n.reg .pred p, q;\n"
+                "setp.ne.u32 p, %1, 0;\n"
+                "setp.lt.and.u32 q, %2, %5, p;\n"
+                "@q st.shared.v2.u32 [%0], {%3, %4};\n}\n" ::"r"(base + (slot << 10)),
+                "r"(m & (1u << jj)), "r"(slot), "r"(r[jj]), "r"(colj + jj), "r"((uint32_t)kCap)
+                : "memory");
           }
         }
-        uint32_t ptr = smem_u32(cand + cnt * 128 + tid);
-        const uint32_t ptr0 = ptr;
-        if (first) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            asm volatile(
-                "{\n.reg .pred p;\n"
-                "setp.ge.f32 p, %1, %2;\n"
-                "@p st.shared.v2.u32 [%0], {%3, %4};\n"
-                "@p add.u32 %0, %0, 1024;\n}\n"
-                : "+r"(ptr)
-                : "f"(__uint_as_float(r[jj])), "f"(tau), "r"(r[jj]), "r"(colj + jj)
-                : "memory");
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            asm volatile(
-                "{\n.reg .pred p;\n"
-                "setp.gt.f32 p, %1, %2;\n"
-                "@p st.shared.v2.u32 [%0], {%3, %4};\n"
-                "@p add.u32 %0, %0, 1024;\n}\n"
-                : "+r"(ptr)
-                : "f"(__uint_as_float(r[jj])), "f"(tau), "r"(r[jj]), "r"(colj + jj)
-                : "memory");
-        }
-        cnt += (int)((ptr - ptr0) >> 10);
+        cnt += __popc(m);
       };
       for (int j0 = 0; j0 < seg_cols; j0 += 32) {
         uint32_t r[32];
@@ -482,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (ts_on && warp == kEpiWarp0 && lane == 0) g_dbg_ts[cta_lin * 32 + 14] = gclk();
+    if (ts_on && warp == kEpiWarp0 && lane == 0) g_dbg_ts[cta_lin * 32 + 15] = (unsigned long long)n_tight;
   }
   tc_fence_before();
   __syncthreads();
@@ -628,7 +610,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
     for (int c = 0; c < ncta; ++c) t0 = std::min(t0, h[c * 32]);
     double acc[16] = {0};
     for (int c = 0; c < ncta; ++c)
-      for (int j = 0; j < 15; ++j) if (j != 11 && j != 13) acc[j] += ((double)h[c * 32 + j] - (double)h[c * 32]) / ncta;
+      for (int j = 0; j < 15; ++j) if (j != 11 && j != 13 && j != 15) acc[j] += ((double)h[c * 32 + j] - (double)h[c * 32]) / ncta;
     double ph[4] = {0, 0, 0, 0};
     for (int c = 0; c < ncta; ++c)
       for (int j = 0; j < 4; ++j) ph[j] += ((double)h[c * 32 + 16 + j] - (double)h[c * 32]) / ncta;
@@ -662,6 +644,11 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
       fprintf(stderr, "entry->start(alloc+init) %.0f ns; dealloc->next entry on same SM %.0f ns (n=%d)\n", ent, ng ? gap / ng : 0.0, ng);
       fprintf(stderr, "starts: p0 %.0f p25 %.0f p50 %.0f p75 %.0f p100 %.0f ns; SMs used %d, max CTAs/SM %d\n",
               ss[0], ss[ncta / 4], ss[ncta / 2], ss[3 * ncta / 4], ss[ncta - 1], nsm, maxc);
+    }
+    {
+      double nt = 0;
+      for (int c = 0; c < ncta; ++c) nt += (double)h[c * 32 + 15] / ncta;
+      fprintf(stderr, "tighten calls per epilogue warp (warp 4): %.2f\n", nt);
     }
     fprintf(stderr, "select_tc ts (ns, mean rel. to CTA start): Afull %.0f  full0..7 %.0f %.0f %.0f %.0f %.0f %.0f %.0f %.0f  end %.0f  | kernel span %.0f\n",
             acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8], acc[9], acc[10], span);
