@@ -24,7 +24,7 @@
  *   subkeys  [H, 2, n_sub, d_half]  qk_dtype
  *   values   [row_end-row_begin, d_value] value_dtype  (the local rows of the
  *            n_sub^2-row table; row_begin=0,row_end=n_sub^2 when unsharded)
- *   out      [B, d_value] fp32      sum over heads
+ *   out      [B, d_value] fp32      sum over heads ([B, G, d_value] with head_groups G > 1)
  *   idx      [B, H, k]   int32      global flat slot ids i*n_sub + j
  *   weights  [B, H, k]   fp32       softmax weights, same order as idx
  *   d_out    [B, d_value] fp32
@@ -82,7 +82,12 @@ typedef enum { MSN_UPDATE_SGD = 1, MSN_UPDATE_ADAGRAD = 2 } msn_update;
 /* flags */
 #define MSN_FLAG_ATOMIC_BWD 0x1u /* value-gradient scatter with red.global.add
                                     (non-deterministic order) instead of the
-                                    default deterministic sort-based reduce */
+                                    default deterministic grouped reduce */
+#define MSN_FLAG_GROUP_TABLES 0x2u /* every head group has its
+                                      own value table (per-token V):
+                                      values hold G * n_sub^2 rows, group g's
+                                      slots at rows g*n_sub^2 + i*n_sub + j, and
+                                      idx reports those global rows */
 
 typedef struct msn_pkm* msn_pkm_t;
 
@@ -97,7 +102,13 @@ typedef struct {
   int32_t qk_dtype;    /* msn_dtype of query and sub-keys */
   int32_t value_dtype; /* msn_dtype of the value table */
   uint32_t flags;      /* MSN_FLAG_* */
-  int32_t reserved;
+  int32_t head_groups; /* G (token-specific sub-keys):
+                          0 or 1 = one group (out = sum over all heads); else H % G
+                          == 0, consecutive blocks of H/G heads form a group (a
+                          token with its own sub-key codebooks) and
+                          out[b, g] = sum over the group's heads: out and d_out
+                          are [B, G, d_value].  G > 1 needs the unsharded table
+                          and the deterministic backward. */
   int64_t row_begin;   /* this process holds value rows [row_begin, row_end) */
   int64_t row_end;     /* (row-sharded table); 0 and n_sub^2 when unsharded */
 } msn_pkm_config;

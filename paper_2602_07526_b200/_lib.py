@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libmsn_pkm.so")
 ABI_VERSION = 1
 MSN_F32, MSN_BF16 = 0, 1
 FLAG_ATOMIC_BWD = 0x1
+FLAG_GROUP_TABLES = 0x2
 GATES = {"tanh": 1, "sigmoid": 2, "identity": 3}  # msn_gate (include/msn_pkm.h)
 UPDATES = {"sgd": 1, "adagrad": 2}                # msn_update
 
@@ -33,7 +34,7 @@ class Config(ctypes.Structure):
                 ("d_value", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("max_batch", ctypes.c_int64), ("qk_dtype", ctypes.c_int32),
                 ("value_dtype", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("reserved", ctypes.c_int32), ("row_begin", ctypes.c_int64),
+                ("head_groups", ctypes.c_int32), ("row_begin", ctypes.c_int64),
                 ("row_end", ctypes.c_int64)]
 
 

@@ -54,6 +54,8 @@ Shape shape_of(const msn_pkm_config& c, int64_t B) {
   s.v_dt = c.value_dtype;
   s.row_begin = c.row_begin;
   s.row_end = c.row_end;
+  s.og = c.head_groups > 1 ? c.head_groups : 1;
+  s.tab_stride = (c.flags & MSN_FLAG_GROUP_TABLES) ? (int64_t)c.n_sub * c.n_sub : 0;
   return s;
 }
 
@@ -162,10 +164,19 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
   if (c->d_value < 1 || (c->d_value * vsz) % 16)
     return fail(MSN_ERR_INVALID_ARG, "d_value * sizeof(value) must be a multiple of 16 bytes");
   if (c->max_batch < 0) return fail(MSN_ERR_INVALID_ARG, "max_batch < 0");
-  const int64_t n = (int64_t)c->n_sub * c->n_sub;
+  if (c->flags & ~(MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES))
+    return fail(MSN_ERR_INVALID_ARG, "unknown flags");
+  const int G = c->head_groups > 1 ? c->head_groups : 1;
+  if (c->head_groups < 0 || c->heads % G)
+    return fail(MSN_ERR_INVALID_ARG, "head_groups must be >= 0 and divide heads");
+  const int64_t n = (int64_t)c->n_sub * c->n_sub * ((c->flags & MSN_FLAG_GROUP_TABLES) ? G : 1);
+  if (n >= (int64_t(1) << 31)) return fail(MSN_ERR_INVALID_ARG, "table rows must be < 2^31");
   if (c->row_begin < 0 || c->row_end > n || c->row_begin >= c->row_end)
-    return fail(MSN_ERR_INVALID_ARG, "need 0 <= row_begin < row_end <= n_sub^2");
-  if (c->flags & ~MSN_FLAG_ATOMIC_BWD) return fail(MSN_ERR_INVALID_ARG, "unknown flags");
+    return fail(MSN_ERR_INVALID_ARG, "need 0 <= row_begin < row_end <= table rows");
+  if (G > 1 && (c->row_begin != 0 || c->row_end != n))
+    return fail(MSN_ERR_UNSUPPORTED, "head groups need the unsharded table");
+  if (G > 1 && (c->flags & MSN_FLAG_ATOMIC_BWD))
+    return fail(MSN_ERR_UNSUPPORTED, "head groups need the deterministic backward");
   if (c->n_sub > 2048) return fail(MSN_ERR_UNSUPPORTED, "n_sub > 2048 is not supported");
   msn_pkm* h = new (std::nothrow) msn_pkm;
   if (!h) return fail(MSN_ERR_INTERNAL, "out of host memory");
@@ -248,7 +259,8 @@ static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* q
   if ((st = check_batch(h, B))) return st;
   h->last_launches = 0;
   if (B == 0) return MSN_OK;
-  const int64_t n = (int64_t)h->cfg.n_sub * h->cfg.n_sub;
+  const Shape s0 = shape_of(h->cfg, 0);
+  const int64_t n = (int64_t)h->cfg.n_sub * h->cfg.n_sub * (s0.tab_stride ? s0.og : 1);
   if (h->cfg.row_begin != 0 || h->cfg.row_end != n)
     return fail(MSN_ERR_INVALID_ARG, "msn_pkm_forward needs the whole table; use the phase calls when sharded");
   REQUIRE_PTR(query);
@@ -314,7 +326,8 @@ msn_status msn_pkm_gate_backward(msn_pkm_t h, void* stream, int64_t B, int32_t g
   REQUIRE_PTR(d_x_tilde);
   REQUIRE_PTR(d_x_in);
   REQUIRE_PTR(d_out);
-  cudaError_t e = launch_gate_backward(B, h->cfg.d_value, gate, x_in, v_o, d_x_tilde, d_x_in, d_out,
+  const int64_t rows = B * shape_of(h->cfg, 0).og;  // out is [B, G, d_value]
+  cudaError_t e = launch_gate_backward(rows, h->cfg.d_value, gate, x_in, v_o, d_x_tilde, d_x_in, d_out,
                                        (cudaStream_t)stream, &h->last_launches);
   if (e != cudaSuccess) return cuda_fail(e, "gate backward");
   return MSN_OK;
@@ -425,7 +438,8 @@ msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B, const float* d
   if ((st = check_batch(h, B))) return st;
   h->last_launches = 0;
   if (B == 0) return MSN_OK;
-  const int64_t n = (int64_t)h->cfg.n_sub * h->cfg.n_sub;
+  const Shape s0 = shape_of(h->cfg, 0);
+  const int64_t n = (int64_t)h->cfg.n_sub * h->cfg.n_sub * (s0.tab_stride ? s0.og : 1);
   if (h->cfg.row_begin != 0 || h->cfg.row_end != n)
     return fail(MSN_ERR_INVALID_ARG, "msn_pkm_backward needs the whole table; use the phase calls when sharded");
   REQUIRE_PTR(d_out);

@@ -198,6 +198,9 @@ struct GrpArgs {
   float* G;               // gradient rows (+=)
   uint32_t* ent_rw;       // = ent (in-place sort of very long runs)
   FastDiv div_hk, div_k;  // record -> query: / (H k), / k
+  // head groups: the x row of record cid is (b, group of h)
+  int og = 1, H = 1;
+  FastDiv div_h, div_hg;  // / H, / (H / og)
   // MODE_DV fused optimiser update: instead of G += g,
   // V[row] <- V[row] - lr g (upd 1, SGD) or, with s[row] += g^2,
   // V[row] - lr g / (sqrt(s[row]) + eps) (upd 2, Adagrad); 0: G += g.
@@ -317,8 +320,14 @@ __device__ __forceinline__ void stg_vec(float* p, const float* v) {
 
 template <int MODE>
 __device__ __forceinline__ uint32_t grp_xrow(const GrpArgs& a, uint32_t rec) {
-  if constexpr (MODE == MODE_DV) return a.div_hk.div(rec);
-  else return a.div_k.div(rec >> 1) * 2u + (rec & 1u);
+  if constexpr (MODE == MODE_DV) {
+    if (a.og == 1) return a.div_hk.div(rec);
+    const uint32_t bh = a.div_k.div(rec);  // b * H + h
+    const uint32_t b = a.div_h.div(bh);
+    return b * (uint32_t)a.og + a.div_hg.div(bh - b * (uint32_t)a.H);
+  } else {
+    return a.div_k.div(rec >> 1) * 2u + (rec & 1u);
+  }
 }
 
 // Sums the entries src(j), j in [j0, j1), of one row into acc (in j order),
@@ -764,7 +773,7 @@ template <int MODE, typename XT, typename YT>
 cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const float* wts,
                        const void* X, const void* Y, float* dots, float* G, int H, int k, int D,
                        cudaStream_t st, int* launches, const TraceEvents& tr = TraceEvents{},
-                       const UpdateArgs& up = UpdateArgs{}) {
+                       const UpdateArgs& up = UpdateArgs{}, int og = 1) {
   if (n == 0 || nrows == 0) return cudaSuccess;
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
@@ -777,6 +786,10 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   *launches += 2;
   GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
+  a.og = og;
+  a.H = H;
+  a.div_h = FastDiv((uint32_t)H);
+  a.div_hg = FastDiv((uint32_t)(H / og));
   a.upd = up.kind;
   a.lr = up.lr;
   a.eps = up.eps;
@@ -833,7 +846,8 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     float* __restrict__ dsS, uint32_t sentinel,
                                                     uint32_t* __restrict__ cnt,
                                                     uint32_t* __restrict__ rank,
-                                                    uint16_t* __restrict__ dSd) {
+                                                    uint16_t* __restrict__ dSd, int hg,
+                                                    int32_t tab_stride) {
   pdl_enter();
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   __shared__ int32_t s_r[8][64];
@@ -851,7 +865,8 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
     const int t = lane + 32 * u;
     wt[u] = t < k ? w[l * k + t] : 0.f;
     g[u] = t < k ? dw[l * k + t] : 0.f;
-    f[u] = t < k ? idx[l * k + t] : 0;
+    // slot within the group's table (per-group tables)
+    f[u] = t < k ? idx[l * k + t] - (h / hg) * tab_stride : 0;
     part = fmaf(wt[u], g[u], part);
   }
   const float gbar = warp_sum(part);
@@ -1082,9 +1097,10 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
   ++*launches;
   if (s.v_dt == F32)
     return grp_finish<MODE_DV, float, float>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k, s.d_v, st,
-                                             launches, tr, UpdateArgs{upd, lr, eps, state});
+                                             launches, tr, UpdateArgs{upd, lr, eps, state}, s.og);
   return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k,
-                                                   s.d_v, st, launches, tr, UpdateArgs{upd, lr, eps, state});
+                                                   s.d_v, st, launches, tr, UpdateArgs{upd, lr, eps, state},
+                                                   s.og);
 }
 
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
@@ -1132,11 +1148,11 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   if (dense)                                                                                   \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, true>, blocks, 256, 0, st,                                    \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, (uint16_t*)ws.dk_ws);                                                   \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride);                 \
   else                                                                                         \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, false>, blocks, 256, 0, st,                                   \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, nullptr)
+        g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride)
 #define DSDQ_E(QT, KPL)                                                                        \
   switch (E) { case 1: DSDQ(QT, KPL, 1); break; case 2: DSDQ(QT, KPL, 2); break;              \
     case 4: DSDQ(QT, KPL, 4); break; case 8: DSDQ(QT, KPL, 8); break;                          \

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
                                                      const VT* __restrict__ V,
                                                      float* __restrict__ out, int64_t B, int HK,
                                                      int d_v, int64_t row_begin,
-                                                     int64_t row_end, Gate gate) {
+                                                     int64_t row_end, Gate gate, int og) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;  // lanes per row
@@ -41,19 +41,21 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
   }
   __syncwarp();
   const int g = lane / LG, gl = lane % LG;
+  const int E = HK / og;  // entries of one output group (og = 1: all)
+  for (int grp = 0; grp < og; ++grp) {
   float acc[VPL][PER];
 #pragma unroll
   for (int v = 0; v < VPL; ++v)
 #pragma unroll
     for (int e = 0; e < PER; ++e) acc[v][e] = 0.f;
   const int row_vecs = d_v / PER;  // 16-byte vectors per row
-  for (int base = g; base < HK; base += G * U) {
+  for (int base = grp * E + g; base < (grp + 1) * E; base += G * U) {
     uint4 x[U][VPL];
     float wt[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int r = base + u * G;
-      const int f = r < HK ? s_idx[wid][r] : -1;
+      const int f = r < (grp + 1) * E ? s_idx[wid][r] : -1;
       wt[u] = f >= 0 ? s_w[wid][r] : 0.f;
       const VT* row = V + (int64_t)(f >= 0 ? f : 0) * d_v;
 #pragma unroll
@@ -81,7 +83,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
 #pragma unroll
       for (int e = 0; e < PER; ++e) acc[v][e] += __shfl_xor_sync(0xffffffffu, acc[v][e], m);
   if (g == 0) {
-    float* o = out + b * d_v;
+    const int64_t orow = b * og + grp;
+    float* o = out + orow * d_v;
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
       const int vec = gl * VPL + v;
@@ -92,8 +95,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
               make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
       }
     }
-    if (gate.kind) store_gated<VPL, PER>(gate, b, d_v, gl, row_vecs, acc);
+    if (gate.kind) store_gated<VPL, PER>(gate, orow, d_v, gl, row_vecs, acc);
   }
+  }  // output groups
 }
 
 template <typename VT>
@@ -104,7 +108,7 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);
 #define GATHER(VPL, G, U)                                                                      \
   launch_pdl(gather_kernel<VT, VPL, G, U>, blocks, 256, 0, st, idx, w, V, out, s.B, HK, s.d_v,         \
-                                                       s.row_begin, s.row_end, gate)
+                                                       s.row_begin, s.row_end, gate, s.og)
   if (R >= 128) { if (R > 128) return cudaErrorNotSupported; GATHER(4, 1, 4); }
   else if (R > 32) GATHER(2, 1, 8);
   else if (R > 16) GATHER(1, 1, 8);

@@ -14,6 +14,8 @@ struct Shape {
   int H, n_sub, d_h, d_v, k;
   int qk_dt, v_dt;
   int64_t row_begin, row_end;  // local value rows
+  int og = 1;                  // output head groups: out [B, og, d_v]
+  int64_t tab_stride = 0;      // per-group tables: group g's rows start at g * tab_stride
 };
 
 // Per-half candidate lists, the hand-off between a1+a2 and a3: for every

@@ -39,17 +39,23 @@ class PKMLookup:
     def __init__(self, heads: int, n_sub: int, d_half: int, d_value: int, k: int,
                  max_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
                  atomic_bwd: bool = False, row_begin: int = 0, row_end: Optional[int] = None,
-                 device=None):
+                 device=None, head_groups: int = 1, group_tables: bool = False):
+        """head_groups G > 1: consecutive blocks of heads/G
+        heads form a group (a token with its own codebooks); out is [B, G, d_v].
+        group_tables: every group has its own table (values [G*n_sub^2, d_v])."""
         self.lib = _lib.load()
         self.heads, self.n_sub, self.d_half, self.d_value, self.k = heads, n_sub, d_half, d_value, k
         self.max_batch = max_batch
         self.qk_dtype, self.value_dtype = qk_dtype, value_dtype
+        self.head_groups, self.group_tables = max(1, head_groups), group_tables
+        self.table_rows = n_sub * n_sub * (self.head_groups if group_tables else 1)
         self.row_begin = row_begin
-        self.row_end = n_sub * n_sub if row_end is None else row_end
+        self.row_end = self.table_rows if row_end is None else row_end
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        flags = (_lib.FLAG_ATOMIC_BWD if atomic_bwd else 0) | (_lib.FLAG_GROUP_TABLES if group_tables else 0)
         cfg = _lib.Config(_lib.ABI_VERSION, heads, n_sub, d_half, d_value, k, max_batch,
-                          _DT[qk_dtype], _DT[value_dtype],
-                          _lib.FLAG_ATOMIC_BWD if atomic_bwd else 0, 0, self.row_begin, self.row_end)
+                          _DT[qk_dtype], _DT[value_dtype], flags, self.head_groups,
+                          self.row_begin, self.row_end)
         h = ctypes.c_void_p()
         _lib.check(self.lib.msn_pkm_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
@@ -67,7 +73,10 @@ class PKMLookup:
     # ---------------------------------------------------------------- utils
     @property
     def sharded(self) -> bool:
-        return not (self.row_begin == 0 and self.row_end == self.n_sub * self.n_sub)
+        return not (self.row_begin == 0 and self.row_end == self.table_rows)
+
+    def _out_shape(self, B: int):
+        return (B, self.d_value) if self.head_groups == 1 else (B, self.head_groups, self.d_value)
 
     def workspace_bytes(self, B: int, gather_batch: Optional[int] = None) -> Tuple[int, int]:
         f, b = ctypes.c_size_t(), ctypes.c_size_t()
@@ -107,7 +116,7 @@ class PKMLookup:
         self._check_inputs(query, subkeys, values)
         q, K, V = self._dev(query), self._dev(subkeys), self._dev(values)
         B = q.shape[0]
-        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        out = torch.empty(self._out_shape(B), dtype=torch.float32, device=self.device)
         idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
         w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
         ws = self.workspace(B)
@@ -126,9 +135,9 @@ class PKMLookup:
         q, K, V = self._dev(query), self._dev(subkeys), self._dev(values)
         B = q.shape[0]
         x = self._dev(x_in).float().contiguous()
-        if tuple(x.shape) != (B, self.d_value):
-            raise ValueError(f"x_in must be [{B},{self.d_value}]")
-        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        if tuple(x.shape) != self._out_shape(B):
+            raise ValueError(f"x_in must be {self._out_shape(B)}")
+        out = torch.empty(self._out_shape(B), dtype=torch.float32, device=self.device)
         xt = torch.empty_like(out)
         idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
         w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
@@ -164,7 +173,7 @@ class PKMLookup:
         """a5 over this process's rows (rows of other shards contribute 0)."""
         idx, w, V = self._dev(idx), self._dev(w), self._dev(values)
         B = idx.shape[0]
-        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        out = torch.empty(self._out_shape(B), dtype=torch.float32, device=self.device)
         _lib.check(self.lib.msn_pkm_gather(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(V), _ptr(out)))
         return out
 
@@ -245,13 +254,13 @@ class PKMLookup:
         Returns (out_h, d_query_h)."""
         B = query_h.shape[0]
         if out_h is None:
-            out_h = torch.empty((B, self.d_value), dtype=torch.float32).pin_memory()
+            out_h = torch.empty(self._out_shape(B), dtype=torch.float32).pin_memory()
         if d_query_h is None:
             d_query_h = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32).pin_memory()
         q = query_h.to(self.device, non_blocking=True)
         d = d_out_h.to(self.device, non_blocking=True)
         self._check_inputs(q, subkeys, values)
-        out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        out = torch.empty(self._out_shape(B), dtype=torch.float32, device=self.device)
         idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
         w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
         dq = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=self.device)

@@ -263,6 +263,64 @@ def test_fused_update(update, name, B):
                      ~aff.reshape(-1), what="dw")
 
 
+# ------------------------------------------ head groups / tokens (f4) ----
+@pytest.mark.parametrize("tables", [False, True])
+@pytest.mark.parametrize("B,dt,G,H", [(300, torch.float32, 4, 8), (2048, torch.bfloat16, 16, 16),
+                                      (9000, torch.float32, 2, 4)])
+def test_head_groups(B, dt, G, H, tables):
+    """Token-specific codebooks: G groups of H/G heads with a
+    shared table (or one table per group), out [B, G, d_v].  The reference is
+    G independent fp64 oracle lookups -- group g's heads, its table -- and the
+    backward the same with d_out[:, g]; dV rows, dK and dQ compared per group."""
+    from oracle import oracle as orc
+    n_sub, d_h, d_v, k = 64, 32, 64, 8
+    cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, dt, dt, index=14)
+    Q, K, V1, _ = wl.make_all(cfg, DEV)
+    n = n_sub * n_sub
+    gv = torch.Generator(device="cpu").manual_seed(15)
+    V = (0.02 * torch.randn((G * n if tables else n, d_v), generator=gv)).to(dt).to(DEV)
+    dOut = torch.randn((B, G, d_v), generator=gv).to(DEV)
+    lk = PKMLookup(H, n_sub, d_h, d_v, k, max_batch=B, qk_dtype=dt, value_dtype=dt,
+                   head_groups=G, group_tables=tables)
+    out, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, dw = lk.backward(dOut, Q, K, V, idx, w)
+    torch.cuda.synchronize()
+    assert tuple(out.shape) == (B, G, d_v)
+    hg = H // G
+    rt = parity.rtol_for(dt)
+    Qc, Kc, Vc = Q.cpu(), K.cpu(), V.cpu()
+    for g in range(G):
+        hs = slice(g * hg, (g + 1) * hg)
+        Vg = Vc[g * n:(g + 1) * n] if tables else Vc
+        off = g * n if tables else 0
+        ig = idx[:, hs].cpu().numpy().astype(np.int64) - off
+        assert (ig >= 0).all() and (ig < n).all()
+        o, aff, _ = parity.check_forward(Qc[:, hs].contiguous(), Kc[hs].contiguous(), Vg, k,
+                                         out[:, g].contiguous(), torch.as_tensor(ig).int(), w[:, hs].contiguous())
+        ok = ~aff.any(axis=1)
+        bw = orc.backward(Qc[:, hs].contiguous(), Kc[hs].contiguous(), Vg, o["idx"], dOut[:, g].cpu(),
+                          want_dense_dv=False)
+        parity.row_close(dw[:, hs].cpu().numpy().reshape(-1, k), bw["dw"].reshape(-1, k), rt,
+                         np.repeat(ok, hg), "dw")
+        absq, absk = parity.grad_key_magnitudes(Qc[:, hs].contiguous(), Kc[hs].contiguous(), o, bw, n_sub)
+        parity.row_close(dq[:, hs].cpu().numpy().reshape(-1, d_h), bw["dQ"].reshape(-1, d_h), rt,
+                         np.repeat(np.repeat(ok, hg), 2), "dQ", absmag=absq.reshape(-1, d_h))
+        if tables and not aff.any():
+            rows = bw["rows"]
+            parity.row_close(dV[off + rows].cpu().numpy(), bw["dV"], rt, what="dV (group table)")
+    if not tables:  # shared table: dV = sum over groups of the per-group oracle dV
+        tot = np.zeros((n, d_v))
+        clean = True
+        for g in range(G):
+            hs = slice(g * hg, (g + 1) * hg)
+            o = orc.forward(Qc[:, hs].contiguous(), Kc[hs].contiguous(), Vc, k)
+            clean &= np.array_equal(o["idx"], idx[:, hs].cpu().numpy())
+            bw = orc.backward(Qc[:, hs].contiguous(), Kc[hs].contiguous(), Vc, o["idx"], dOut[:, g].cpu())
+            tot += bw["dV"]
+        if clean:
+            parity.row_close(dV.cpu().numpy(), tot, rt, what="dV (shared table)")
+
+
 # --------------------------------------------------- hot rows (grouping) --
 @pytest.mark.parametrize("B,H,dt", [(400, 2, torch.float32),     # runs of 33..1024: warp sort, pieces
                                     (3000, 2, torch.float32),    # > 1024: CTA sort in shared memory
