@@ -149,16 +149,17 @@ def algorithmic_bytes(cfg, idx=None, update="none"):
     qsz = 2 if cfg.qk_dtype == torch.bfloat16 else 4
     L = cfg.batch * cfg.heads
     contrib = L * cfg.k
-    gather = contrib * cfg.d_value * esz + contrib * 8 + cfg.batch * cfg.d_value * 4
+    out_elems = cfg.batch * cfg.d_value * cfg.head_groups
+    gather = contrib * cfg.d_value * esz + contrib * 8 + out_elems * 4
     out = {"gather": gather}
     if idx is not None:
         uniq = int(torch.unique(idx).numel())
         out["unique_rows"] = uniq
         # V rows read once, dV read+written once (fp32), idx/w/dw, dOut once
-        out["scatter"] = uniq * cfg.d_value * (esz + 8) + contrib * 12 + cfg.batch * cfg.d_value * 4
+        out["scatter"] = uniq * cfg.d_value * (esz + 8) + contrib * 12 + out_elems * 4
         if update != "none":  # V read + V written (+ Adagrad state read + written), no dV
             out["scatter"] = (uniq * cfg.d_value * (2 * esz + (8 if update == "adagrad" else 0))
-                              + contrib * 12 + cfg.batch * cfg.d_value * 4)
+                              + contrib * 12 + out_elems * 4)
     out["select_flops"] = 4 * L * cfg.n_sub * cfg.d_half
     out["select_bytes"] = L * 2 * cfg.d_half * qsz + contrib * 8
     return out
@@ -177,10 +178,11 @@ def run_ours(args, rank, world, local_rank):
     cfg = wl.CONFIGS[args.workload]
     Q, K, V, dOut = wl.make_all(cfg, dev)
     lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, cfg.batch,
-                   cfg.qk_dtype, cfg.value_dtype, atomic_bwd=args.atomic, device=dev)
+                   cfg.qk_dtype, cfg.value_dtype, atomic_bwd=args.atomic, device=dev,
+                   head_groups=cfg.head_groups, group_tables=cfg.group_tables)
     lib, h = lk.lib, lk._h
     B = cfg.batch
-    out = torch.empty((B, cfg.d_value), dtype=torch.float32, device=dev)
+    out = torch.empty((B,) + tuple(cfg.out_shape_tail), dtype=torch.float32, device=dev)
     idx = torch.empty((B, cfg.heads, cfg.k), dtype=torch.int32, device=dev)
     w = torch.empty((B, cfg.heads, cfg.k), dtype=torch.float32, device=dev)
     dw = torch.empty_like(w)
@@ -192,7 +194,7 @@ def run_ours(args, rank, world, local_rank):
     if gate:
         # memory-gated fusion: x~ = x * g(v_o), upstream grad on x~
         gx = torch.Generator(device="cpu").manual_seed(7526 + 6)
-        x_in = torch.randn((B, cfg.d_value), generator=gx).to(dev)
+        x_in = torch.randn((B,) + tuple(cfg.out_shape_tail), generator=gx).to(dev)
         x_t = torch.empty_like(x_in)
         d_xin = torch.empty_like(x_in)
         d_vo = torch.empty_like(x_in)
@@ -291,7 +293,7 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         Qh = Q.cpu().pin_memory()
         dOh = dOut.cpu().pin_memory()
-        out_h = torch.empty((B, cfg.d_value), dtype=torch.float32).pin_memory()
+        out_h = torch.empty((B,) + tuple(cfg.out_shape_tail), dtype=torch.float32).pin_memory()
         dq_h = torch.empty((B, cfg.heads, 2, cfg.d_half), dtype=torch.float32).pin_memory()
         n_e2e = max(3, min(args.steps, 20))
         for _ in range(3):
@@ -488,8 +490,6 @@ def run_sharded(args, rank, world, local_rank):
     del V, Q, dOut
     dVs = torch.zeros((sp.rows, cfg.d_value), dtype=torch.float32, device=dev)
     dK = torch.zeros((cfg.heads, 2, cfg.n_sub, cfg.d_half), dtype=torch.float32, device=dev)
-    upd = {"none": 0, "sgd": 1, "adagrad": 2}[args.update]
-    ada = torch.zeros((cfg.n_slots, cfg.d_value), dtype=torch.float32, device=dev) if upd == 2 else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -541,8 +541,18 @@ def cpu_baseline(cfg, Q, K, V, dOut, queries=None):
     q, k_, v, d = Q[:n].cpu(), K.cpu(), V.cpu(), dOut[:n].cpu()
     cores = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
-    o = orc.forward(q, k_, v, cfg.k, nthreads=cores)
-    orc.backward(q, k_, v, o["idx"], d, want_dense_dv=False, nthreads=cores)
+    G = cfg.head_groups
+    if G == 1:
+        o = orc.forward(q, k_, v, cfg.k, nthreads=cores)
+        orc.backward(q, k_, v, o["idx"], d, want_dense_dv=False, nthreads=cores)
+    else:  # head groups (f4): G independent lookups, group g's heads and table
+        hg, nn = cfg.heads // G, cfg.n_sub * cfg.n_sub
+        for g in range(G):
+            hs = slice(g * hg, (g + 1) * hg)
+            vg = v[g * nn:(g + 1) * nn] if cfg.group_tables else v
+            qg, kg = q[:, hs].contiguous(), k_[hs].contiguous()
+            o = orc.forward(qg, kg, vg, cfg.k, nthreads=cores)
+            orc.backward(qg, kg, vg, o["idx"], d[:, g].contiguous(), want_dense_dv=False, nthreads=cores)
     t = time.perf_counter() - t0
     return {"value": n * cfg.heads / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {n} of {cfg.batch} queries x {cfg.heads} heads = {n * cfg.heads} lookups, "

@@ -43,10 +43,17 @@ class PKMConfig:
     zipf_sigma: float = 0.5
     backward: bool = True
     deterministic: bool = True
+    head_groups: int = 1          # f4: tokens (groups of heads/groups heads), out [B, G, d_v]
+    group_tables: bool = False    # f4: one value table per group
 
     @property
     def n_slots(self) -> int:
-        return self.n_sub * self.n_sub
+        """Rows of the value table (all groups' tables when group_tables)."""
+        return self.n_sub * self.n_sub * (self.head_groups if self.group_tables else 1)
+
+    @property
+    def out_shape_tail(self):
+        return (self.d_value,) if self.head_groups == 1 else (self.head_groups, self.d_value)
 
     @property
     def lookups(self) -> int:
@@ -75,6 +82,19 @@ CONFIGS = {
     "c5_latency_bf16": PKMConfig("c5_latency_bf16", 4, 512, 4, 128, 1024, 512, 32,
                                  torch.bfloat16, torch.bfloat16, key_std=1.0,
                                  backward=False),
+    # the paper's deployed design -- token-specific query
+    # networks and sub-keys, one value table shared by the layer's tokens
+    # (hybrid allocation), n = 256^2, k = 32, a
+    # batch of 2048 x 16 tokens.  d_v = 512 (the
+    # paper's width is not stated; SURVEY E8 infers ~1024, above this build's
+    # 512-wide reducer), d_h = 128.  One head per token: 16 groups.
+    "f4_tokens_bf16": PKMConfig("f4_tokens_bf16", 5, 2048, 16, 128, 256, 512, 32,
+                                torch.bfloat16, torch.bfloat16, key_std=1.0, head_groups=16),
+    # ... and the per-token value tables of the paper's "per-token V" ablation
+    # (PAPER.md:446): 16 tables of 256^2 rows.
+    "f4_tokens_pertable_bf16": PKMConfig("f4_tokens_pertable_bf16", 6, 2048, 16, 128, 256, 512, 32,
+                                         torch.bfloat16, torch.bfloat16, key_std=1.0, head_groups=16,
+                                         group_tables=True),
 }
 
 
@@ -128,7 +148,7 @@ def make_subkeys(cfg: PKMConfig, device="cpu") -> torch.Tensor:
 
 
 def make_values(cfg: PKMConfig, device="cpu") -> torch.Tensor:
-    """V [n_sub^2, d_v] ~ N(0, 0.02^2)."""
+    """V [n_slots, d_v] ~ N(0, 0.02^2) (n_slots = G n_sub^2 with group tables)."""
     base = 7526 + cfg.index
     v = _randn((cfg.n_slots, cfg.d_value), base + 3, device)
     v.mul_(0.02)
@@ -136,10 +156,11 @@ def make_values(cfg: PKMConfig, device="cpu") -> torch.Tensor:
 
 
 def make_dout(cfg: PKMConfig, device="cpu", batch: Optional[int] = None) -> torch.Tensor:
-    """dOut [B, d_v] fp32 ~ N(0,1) (the dense upstream gradient of configs[1..3])."""
+    """dOut [B, d_v] (or [B, G, d_v] with head groups) fp32 ~ N(0,1) (the
+    dense upstream gradient of configs[1..3])."""
     B = cfg.batch if batch is None else batch
     base = 7526 + cfg.index
-    return _randn((B, cfg.d_value), base + 4, device).contiguous()
+    return _randn((B,) + tuple(cfg.out_shape_tail), base + 4, device).contiguous()
 
 
 def make_all(cfg: PKMConfig, device="cpu", batch: Optional[int] = None):
