@@ -7,6 +7,9 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 * oracle.pkm_oracle.c  -- plain C fp64 forward / backward / slot scores
 * oracle.oracle         -- ctypes wrapper (numpy in, numpy out)
 * oracle.brute          -- numpy exhaustive full-memory scorer for tiny tables
+* oracle.prologue       -- LayerNorm of queries/sub-keys and the key
+                           over-parameterisation K~ = Theta K with gradients
+                           
 * oracle.update         -- fused sparse SGD / Adagrad on the touched value
                            rows ("gradient updates")
 * oracle.gate           -- memory-gated fusion x~ = x (.) g(v_o) and its
