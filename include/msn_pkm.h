@@ -162,6 +162,33 @@ msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const in
                                   int32_t update, float lr, float eps, float* state, float* dw,
                                   void* workspace, size_t workspace_bytes);
 
+/* Query / key prologue, composed by the caller around
+ * the lookup:  q^ = LN(q), k^ = LN(k) (reading R23: no affine,
+ * eps = 1e-5), K~ = Theta k^ per (head, half), then the
+ * lookup on (q^, K~); its d_query / d_subkeys are the gradients w.r.t. q^
+ * and K~, which the backward calls below carry back to q, k and Theta
+ * (PAPER.md:296-302).
+ *
+ * msn_pkm_layernorm: y = LN(x) row by row; x, y [rows, d_half] qk_dtype
+ *   (queries: rows = B*H*2; sub-keys: rows = H*2*n_sub); output rounded once
+ *   (RNE) to qk_dtype.  d_half in {32, 64, 128, 256} else MSN_ERR_UNSUPPORTED.
+ * msn_pkm_layernorm_backward: dx = d LN(x)^T dy; x qk_dtype, dy and dx fp32
+ *   [rows, d_half], dx written (=).
+ * msn_pkm_key_transform: k_eff[h,c,i,:] = Theta[h,c] k_hat[h,c,i,:];
+ *   k_hat, k_eff [H, 2, n_sub, d_half] qk_dtype; theta [H, 2, d_half, d_half]
+ *   fp32 row-major (theta[h,c,r,col] multiplies k_hat component col).
+ * msn_pkm_key_transform_backward: d_k_hat = Theta^T d_k_eff (=, fp32
+ *   [H,2,n_sub,d_half]); d_theta += sum_i d_k_eff_i k_hat_i^T (fp32
+ *   [H,2,d_half,d_half]).  All device pointers, 16-byte aligned. */
+msn_status msn_pkm_layernorm(msn_pkm_t h, void* stream, int64_t rows, const void* x, void* y);
+msn_status msn_pkm_layernorm_backward(msn_pkm_t h, void* stream, int64_t rows, const void* x,
+                                      const float* dy, float* dx);
+msn_status msn_pkm_key_transform(msn_pkm_t h, void* stream, const void* k_hat, const float* theta,
+                                 void* k_eff);
+msn_status msn_pkm_key_transform_backward(msn_pkm_t h, void* stream, const void* k_hat,
+                                          const float* theta, const float* d_k_eff, float* d_k_hat,
+                                          float* d_theta);
+
 /* Backward of the gate for the upstream gradient d_x_tilde [B, d_value]:
  *   d_x_in = d_x_tilde (.) g(v_o)                       (written, =)
  *   d_out  = d_x_tilde (.) x_in (.) g'(v_o)             (written, =)

@@ -47,6 +47,10 @@ SIGNATURES = {
     "msn_pkm_forward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_forward_gated": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_gate_backward": [_P, _P, _I64, ctypes.c_int32, _P, _P, _P, _P, _P],
+    "msn_pkm_layernorm": [_P, _P, _I64, _P, _P],
+    "msn_pkm_layernorm_backward": [_P, _P, _I64, _P, _P, _P],
+    "msn_pkm_key_transform": [_P, _P, _P, _P, _P],
+    "msn_pkm_key_transform_backward": [_P, _P, _P, _P, _P, _P, _P],
     "msn_pkm_scatter_update": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, ctypes.c_float,
                                ctypes.c_float, _P, _P, _P, _SZ],
     "msn_pkm_backward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],

@@ -471,4 +471,69 @@ msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B, const float* d
   return MSN_OK;
 }
 
+
+// ------------------------------------------------ prologue --
+msn_status msn_pkm_layernorm(msn_pkm_t h, void* stream, int64_t rows, const void* x, void* y) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (rows < 0) return fail(MSN_ERR_INVALID_ARG, "rows < 0");
+  if (rows == 0) return MSN_OK;
+  REQUIRE_PTR(x);
+  REQUIRE_PTR(y);
+  const Shape s = shape_of(h->cfg, 0);
+  if (!prologue_supported(s)) return fail(MSN_ERR_UNSUPPORTED, "layernorm needs d_half in {32, 64, 128, 256}");
+  cudaError_t e = launch_layernorm(s, rows, x, y, nullptr, nullptr, (cudaStream_t)stream, &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "layernorm");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_layernorm_backward(msn_pkm_t h, void* stream, int64_t rows, const void* x,
+                                      const float* dy, float* dx) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (rows < 0) return fail(MSN_ERR_INVALID_ARG, "rows < 0");
+  if (rows == 0) return MSN_OK;
+  REQUIRE_PTR(x);
+  REQUIRE_PTR(dy);
+  REQUIRE_PTR(dx);
+  const Shape s = shape_of(h->cfg, 0);
+  if (!prologue_supported(s)) return fail(MSN_ERR_UNSUPPORTED, "layernorm needs d_half in {32, 64, 128, 256}");
+  cudaError_t e = launch_layernorm(s, rows, x, nullptr, dy, dx, (cudaStream_t)stream, &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "layernorm backward");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_key_transform(msn_pkm_t h, void* stream, const void* k_hat, const float* theta,
+                                 void* k_eff) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  REQUIRE_PTR(k_hat);
+  REQUIRE_PTR(theta);
+  REQUIRE_PTR(k_eff);
+  cudaError_t e = launch_key_transform(shape_of(h->cfg, 0), k_hat, theta, k_eff, (cudaStream_t)stream,
+                                       &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "key transform");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_key_transform_backward(msn_pkm_t h, void* stream, const void* k_hat,
+                                          const float* theta, const float* d_k_eff, float* d_k_hat,
+                                          float* d_theta) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  REQUIRE_PTR(k_hat);
+  REQUIRE_PTR(theta);
+  REQUIRE_PTR(d_k_eff);
+  REQUIRE_PTR(d_k_hat);
+  REQUIRE_PTR(d_theta);
+  cudaError_t e = launch_key_transform_backward(shape_of(h->cfg, 0), k_hat, theta, d_k_eff, d_k_hat,
+                                                d_theta, (cudaStream_t)stream, &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "key transform backward");
+  return MSN_OK;
+}
+
 }  // extern "C"

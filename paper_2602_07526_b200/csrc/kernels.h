@@ -121,4 +121,18 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
                                  float* dK, const BwdWorkspace& ws, cudaStream_t st,
                                  int* launches);
 
+// ---- prologue (prologue.cu) ----
+bool prologue_supported(const Shape& s);
+// LayerNorm of `rows` rows of width d_h (qk dtype): y = LN(x); with dy given,
+// the backward dx (fp32, =) instead.
+cudaError_t launch_layernorm(const Shape& s, int64_t rows, const void* x, void* y, const float* dy,
+                             float* dx, cudaStream_t st, int* launches);
+// K~ = K^ Theta^T per codebook (qk dtype in and out, Theta fp32 [2H, d, d]).
+cudaError_t launch_key_transform(const Shape& s, const void* khat, const float* theta, void* keff,
+                                 cudaStream_t st, int* launches);
+// dK^ = dK~ Theta (=), dTheta += dK~^T K^ (fp32).
+cudaError_t launch_key_transform_backward(const Shape& s, const void* khat, const float* theta,
+                                          const float* dkeff, float* dkhat, float* dtheta,
+                                          cudaStream_t st, int* launches);
+
 }  // namespace msn

@@ -157,6 +157,40 @@ class PKMLookup:
                                                   _ptr(d), _ptr(dx), _ptr(dvo)))
         return dx, dvo
 
+    # ------------------------------------------- prologue
+    def layernorm(self, x: torch.Tensor) -> torch.Tensor:
+        """LN over the last axis (width d_half), qk dtype in and out."""
+        x = self._dev(x)
+        y = torch.empty_like(x)
+        rows = x.numel() // self.d_half
+        _lib.check(self.lib.msn_pkm_layernorm(self._h, _stream(), rows, _ptr(x), _ptr(y)))
+        return y
+
+    def layernorm_backward(self, x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
+        x, dy = self._dev(x), self._dev(dy).float().contiguous()
+        dx = torch.empty(x.shape, dtype=torch.float32, device=self.device)
+        rows = x.numel() // self.d_half
+        _lib.check(self.lib.msn_pkm_layernorm_backward(self._h, _stream(), rows, _ptr(x), _ptr(dy), _ptr(dx)))
+        return dx
+
+    def key_transform(self, k_hat: torch.Tensor, theta: torch.Tensor) -> torch.Tensor:
+        """K~ = Theta k^ per (head, half); theta [H,2,d,d] fp32."""
+        k_hat, theta = self._dev(k_hat), self._dev(theta).float().contiguous()
+        k_eff = torch.empty_like(k_hat)
+        _lib.check(self.lib.msn_pkm_key_transform(self._h, _stream(), _ptr(k_hat), _ptr(theta), _ptr(k_eff)))
+        return k_eff
+
+    def key_transform_backward(self, k_hat, theta, d_k_eff, d_theta: Optional[torch.Tensor] = None):
+        """-> (d_k_hat, d_theta); d_theta accumulated into when given."""
+        k_hat, theta = self._dev(k_hat), self._dev(theta).float().contiguous()
+        d = self._dev(d_k_eff).float().contiguous()
+        d_k_hat = torch.empty(k_hat.shape, dtype=torch.float32, device=self.device)
+        if d_theta is None:
+            d_theta = torch.zeros(theta.shape, dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.msn_pkm_key_transform_backward(self._h, _stream(), _ptr(k_hat), _ptr(theta), _ptr(d),
+                                                           _ptr(d_k_hat), _ptr(d_theta)))
+        return d_k_hat, d_theta
+
     def select(self, query: torch.Tensor, subkeys: torch.Tensor):
         """a1-a4 only: (idx, w)."""
         self._check_inputs(query, subkeys)

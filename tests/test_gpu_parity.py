@@ -321,6 +321,95 @@ def test_head_groups(B, dt, G, H, tables):
             parity.row_close(dV.cpu().numpy(), tot, rt, what="dV (shared table)")
 
 
+# --------------------------------------------- query/key prologue (f2) ----
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d_h", [32, 128, 256])
+def test_prologue_stages(dt, d_h):
+    """Each prologue stage on seeded inputs against oracle/prologue.py:
+    LayerNorm and its backward, K~ = Theta k^ and its
+    gradients (PAPER.md:287-302)."""
+    from oracle import prologue as op
+    H, n_sub = 2, 192
+    g = torch.Generator(device="cpu").manual_seed(21)
+    lk = PKMLookup(H, n_sub, d_h, 64, 8, max_batch=64, qk_dtype=dt, value_dtype=dt)
+    rt = parity.rtol_for(dt)
+    x = (3.0 * torch.randn((300, H, 2, d_h), generator=g) + 0.5).to(dt).to(DEV)
+    y = lk.layernorm(x)
+    parity.row_close(y.cpu().reshape(-1, d_h).float().numpy(), op.layernorm(x.cpu()).reshape(-1, d_h), rt,
+                     what="LN")
+    dy = torch.randn(x.shape, generator=g).to(DEV)
+    dx = lk.layernorm_backward(x, dy)
+    parity.row_close(dx.cpu().reshape(-1, d_h).numpy(), op.layernorm_backward(x.cpu(), dy.cpu()).reshape(-1, d_h),
+                     rt, what="LN backward")
+    k_hat = torch.randn((H, 2, n_sub, d_h), generator=g).to(dt).to(DEV)
+    theta = (torch.randn((H, 2, d_h, d_h), generator=g) / d_h ** 0.5).to(DEV)
+    k_eff = lk.key_transform(k_hat, theta)
+    parity.row_close(k_eff.cpu().float().reshape(-1, d_h).numpy(),
+                     op.key_transform(k_hat.cpu(), theta.cpu()).reshape(-1, d_h), rt, what="K~")
+    d_k_eff = torch.randn((H, 2, n_sub, d_h), generator=g).to(DEV)
+    d0 = torch.randn(theta.shape, generator=g).to(DEV)
+    dkh, dth = lk.key_transform_backward(k_hat, theta, d_k_eff, d_theta=d0.clone())
+    rk, rth = op.key_transform_backward(k_hat.cpu(), theta.cpu(), d_k_eff.cpu())
+    parity.row_close(dkh.cpu().reshape(-1, d_h).numpy(), rk.reshape(-1, d_h), 1e-4, what="dK^")
+    parity.row_close((dth - d0).cpu().reshape(-1, d_h).numpy(), rth.reshape(-1, d_h), 1e-4, what="dTheta")
+
+
+def test_prologue_chain_fp32():
+    """q^ = LN(q), K~ = Theta LN(k), lookup, backward, back through the
+    prologue -- the whole chain on the GPU against the fp64 oracle chain."""
+    from oracle import oracle as orc
+    from oracle import prologue as op
+    B, H, n_sub, d_h, d_v, k = 500, 2, 128, 64, 64, 8
+    cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, torch.float32, torch.float32, index=22)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    g = torch.Generator(device="cpu").manual_seed(22)
+    theta = (torch.eye(d_h) + 0.1 * torch.randn((H, 2, d_h, d_h), generator=g)).to(DEV)
+    lk = lookup_for(cfg, B)
+    qh = lk.layernorm(Q)
+    kh = lk.layernorm(K)
+    ke = lk.key_transform(kh, theta)
+    out, idx, w = lk.forward(qh, ke, V)
+    dqh, dke, dV, dw = lk.backward(dOut, qh, ke, V, idx, w)
+    dq = lk.layernorm_backward(Q, dqh)
+    dkh, dth = lk.key_transform_backward(kh, theta, dke)
+    dk = lk.layernorm_backward(K, dkh)
+    torch.cuda.synchronize()
+    # fp64 oracle chain from the raw inputs
+    qh_o = op.layernorm(Q.cpu())
+    kh_o = op.layernorm(K.cpu())
+    ke_o = op.key_transform(kh_o, theta.cpu())
+    o = orc.forward(qh_o, ke_o, V.cpu(), k)
+    aff, _ = parity.compare_selection(qh_o, ke_o, idx.cpu().numpy().astype(np.int64), o, n_sub)
+    ok = ~aff.any(axis=1)
+    parity.row_close(out.cpu().numpy(), o["out"], 1e-4, ok, "out")
+    if aff.any():
+        return  # a near-tie changed the selection: the chain's gradients differ by construction
+    bw = orc.backward(qh_o, ke_o, V.cpu(), o["idx"], dOut.cpu())
+    dq_o = op.layernorm_backward(Q.cpu(), bw["dQ"])
+    dkh_o, dth_o = op.key_transform_backward(kh_o, theta.cpu(), bw["dK"])
+    dk_o = op.layernorm_backward(K.cpu(), dkh_o)
+    # condition-aware scales (R14): the sums of |terms| behind every element,
+    # carried through the linear backward maps with absolute values
+    absq, absk = parity.grad_key_magnitudes(qh_o, ke_o, o, bw, n_sub)
+
+    def ln_mag(x, a):  # |d LN(x)^T dy| <= r (a + mean a + |x^| mean(a |x^|)) for |dy| <= a
+        x = x.cpu().double().numpy()
+        mu = x.mean(-1, keepdims=True)
+        r = 1.0 / np.sqrt(((x - mu) ** 2).mean(-1, keepdims=True) + op.EPS)
+        xh = np.abs((x - mu) * r)
+        return r * (a + a.mean(-1, keepdims=True) + xh * (a * xh).mean(-1, keepdims=True))
+
+    th = np.abs(theta.cpu().double().numpy())
+    mag_dkh = np.einsum("hcie,hced->hcid", absk, th)
+    mag_dth = np.einsum("hcie,hcid->hced", absk, np.abs(kh_o))
+    parity.row_close(dq.cpu().reshape(-1, d_h).numpy(), dq_o.reshape(-1, d_h), 1e-4, what="dq",
+                     absmag=ln_mag(Q, absq).reshape(-1, d_h))
+    parity.row_close(dth.cpu().reshape(-1, d_h).numpy(), dth_o.reshape(-1, d_h), 1e-4, what="dTheta",
+                     absmag=mag_dth.reshape(-1, d_h))
+    parity.row_close(dk.cpu().reshape(-1, d_h).numpy(), dk_o.reshape(-1, d_h), 1e-4, what="dk",
+                     absmag=ln_mag(K, mag_dkh).reshape(-1, d_h))
+
+
 # --------------------------------------------------- hot rows (grouping) --
 @pytest.mark.parametrize("B,H,dt", [(400, 2, torch.float32),     # runs of 33..1024: warp sort, pieces
                                     (3000, 2, torch.float32),    # > 1024: CTA sort in shared memory
