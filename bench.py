@@ -198,6 +198,19 @@ def run_ours(args, rank, world, local_rank):
         x_t = torch.empty_like(x_in)
         d_xin = torch.empty_like(x_in)
         d_vo = torch.empty_like(x_in)
+    if args.prologue:
+        # f2: q^ = LN(q), K~ = Theta LN(k) before the lookup; back through them after
+        g2 = torch.Generator(device="cpu").manual_seed(7526 + 7)
+        theta = (torch.eye(cfg.d_half) + 0.05 * torch.randn((cfg.heads, 2, cfg.d_half, cfg.d_half),
+                                                             generator=g2)).to(dev)
+        Q_raw, K_raw = Q, K
+        Q = torch.empty_like(Q_raw)
+        K_hat = torch.empty_like(K_raw)
+        K = torch.empty_like(K_raw)
+        d_theta = torch.zeros_like(theta)
+        d_khat = torch.empty(K_raw.shape, dtype=torch.float32, device=dev)
+        d_kraw = torch.empty(K_raw.shape, dtype=torch.float32, device=dev)
+        d_qraw = torch.empty(Q_raw.shape, dtype=torch.float32, device=dev)
     upd = {"none": 0, "sgd": 1, "adagrad": 2}[args.update]
     ada = torch.zeros((cfg.n_slots, cfg.d_value), dtype=torch.float32, device=dev) if upd == 2 else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -215,6 +228,13 @@ def run_ours(args, rank, world, local_rank):
             evs[0].record(stream)
             arr = (ctypes.c_void_p * 2)(evs[1].cuda_event, evs[2].cuda_event)
             check(lib.msn_pkm_set_trace_events(h, arr, 2))
+        if args.prologue:
+            check(lib.msn_pkm_layernorm(h, sp, Q_raw.numel() // cfg.d_half, _ptr(Q_raw), _ptr(Q)))
+            n += lk.last_launch_count()
+            check(lib.msn_pkm_layernorm(h, sp, K_raw.numel() // cfg.d_half, _ptr(K_raw), _ptr(K_hat)))
+            n += lk.last_launch_count()
+            check(lib.msn_pkm_key_transform(h, sp, _ptr(K_hat), _ptr(theta), _ptr(K)))
+            n += lk.last_launch_count()
         if gate:
             check(lib.msn_pkm_forward_gated(h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(x_in), gate,
                                             _ptr(out), _ptr(x_t), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
@@ -247,6 +267,16 @@ def run_ours(args, rank, world, local_rank):
         check(lib.msn_pkm_backward_keys(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(dw), _ptr(dQ),
                                         _ptr(dK), _ptr(ws), ws.numel()))
         n += lk.last_launch_count()
+        if args.prologue:  # counted in backward_keys
+            check(lib.msn_pkm_key_transform_backward(h, sp, _ptr(K_hat), _ptr(theta), _ptr(dK), _ptr(d_khat),
+                                                     _ptr(d_theta)))
+            n += lk.last_launch_count()
+            check(lib.msn_pkm_layernorm_backward(h, sp, K_raw.numel() // cfg.d_half, _ptr(K_raw), _ptr(d_khat),
+                                                 _ptr(d_kraw)))
+            n += lk.last_launch_count()
+            check(lib.msn_pkm_layernorm_backward(h, sp, Q_raw.numel() // cfg.d_half, _ptr(Q_raw), _ptr(dQ),
+                                                 _ptr(d_qraw)))
+            n += lk.last_launch_count()
         if evs: evs[5].record(stream)
         launches[0] = n
 
@@ -382,6 +412,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "backward": "atomic" if args.atomic else "deterministic (grouped by row, per-row id order)",
                    "gate": args.gate,
+                   "prologue": bool(args.prologue),
                    "update": args.update,
                    "l2": "flushed before every step (512 MiB write, outside the timed events)"},
         "roofline": roof,
@@ -616,6 +647,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="C4 through the row-sharded path even at N=1")
+    ap.add_argument("--prologue", action="store_true",
+                    help="include LayerNorm(q), K~ = Theta LayerNorm(k) and their backward (SURVEY 8(f) f2)")
     ap.add_argument("--update", choices=["none", "sgd", "adagrad"], default="none",
                     help="fuse the optimiser step into the value-row reduction (SURVEY 8(f) f3)")
     ap.add_argument("--gate", choices=["none", "tanh", "sigmoid", "identity"], default="none",

@@ -108,13 +108,23 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const TA
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   for (int k0 = 0; k0 < K; k0 += 16) {
+    // 16 x 64 elements per operand tile, 4 per thread; consecutive threads
+    // walk the operand's contiguous dimension (coalesced loads)
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * 256;  // 1024 = 16 x 64 elements
-      const int kk = e / 64, ii = e % 64;
+      const int e = tid + u * 256;
+      const bool a_k = a_cs == 1;  // A contiguous along k
+      const int kk = a_k ? e % 16 : e / 64, ii = a_k ? e / 16 : e % 64;
       const int gk = k0 + kk;
       As[kk][ii] = (m0 + ii < M && gk < K) ? ld_f(A + (int64_t)(m0 + ii) * a_rs + (int64_t)gk * a_cs) : 0.f;
-      Bs[kk][ii] = (n0 + ii < N && gk < K) ? ld_f(B + (int64_t)gk * b_rs + (int64_t)(n0 + ii) * b_cs) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + u * 256;
+      const bool b_k = b_rs == 1;  // B contiguous along k
+      const int kk = b_k ? e % 16 : e / 64, jj = b_k ? e / 16 : e % 64;
+      const int gk = k0 + kk;
+      Bs[kk][jj] = (n0 + jj < N && gk < K) ? ld_f(B + (int64_t)gk * b_rs + (int64_t)(n0 + jj) * b_cs) : 0.f;
     }
     __syncthreads();
 #pragma unroll
