@@ -106,6 +106,10 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   p += align256(sizeof(int32_t) * rows * kCandCap);
   cd.n = (int32_t*)p;
   p += align256(sizeof(int32_t) * rows);
+  cd.rq.Q = query;
+  cd.rq.K = subkeys;
+  cd.rq.d_h = s.d_h;
+  cd.rq.qk_dt = s.qk_dt;
   cudaError_t e;
   if (select_tc_supported(s)) {
     e = launch_select_tc(s, query, subkeys, cd, p, st, launches);

@@ -25,48 +25,13 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "gate.cuh"
+#include "warp_sort.cuh"
 
 namespace msn {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kMaxHK = 256;  // H*k staged per warp in the fused kernel
-
-// Warp-wide bitonic sort of 64 (score, index) pairs held as (v[r], ix[r]),
-// element e = r*32 + lane; result in (score desc, index asc) order.
-__device__ __forceinline__ bool before(float av, int32_t ai, float bv, int32_t bi) {
-  return av > bv || (av == bv && ai < bi);
-}
-__device__ __forceinline__ void warp_sort64(float (&v)[2], int32_t (&ix)[2]) {
-  const int lane = threadIdx.x % 32;
-#pragma unroll
-  for (int size = 2; size <= 64; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride == 32) {
-        // partner is the other register of the same lane (e ^ 32)
-        const bool desc = true;  // size == 64: the whole sequence is sorted descending
-        (void)desc;
-        const bool sw = before(v[1], ix[1], v[0], ix[0]);
-        const float a = sw ? v[1] : v[0], b = sw ? v[0] : v[1];
-        const int32_t c = sw ? ix[1] : ix[0], d = sw ? ix[0] : ix[1];
-        v[0] = a; v[1] = b; ix[0] = c; ix[1] = d;
-      } else {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int e = r * 32 + lane;
-          const float ov = __shfl_xor_sync(0xffffffffu, v[r], stride);
-          const int32_t oi = __shfl_xor_sync(0xffffffffu, ix[r], stride);
-          const bool lower = (e & stride) == 0;
-          const bool desc = (e & size) == 0;
-          const bool want_better = desc == lower;
-          const bool other_better = before(ov, oi, v[r], ix[r]);
-          if (want_better == other_better) { v[r] = ov; ix[r] = oi; }
-        }
-      }
-    }
-  }
-}
 
 // Per-warp scratch of one lookup's Cartesian stage.
 template <int KMAX, int MAXC>
@@ -86,7 +51,8 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
                                                  const int32_t* __restrict__ cand_n, int n_sub,
                                                  int k, int32_t* __restrict__ idx,
                                                  float* __restrict__ w, int32_t* s_idx,
-                                                 float* s_w, int32_t tab_off) {
+                                                 float* s_w, int32_t tab_off, const Rescore& rq,
+                                                 int H) {
   constexpr int APL = KMAX / 32;  // rows a per lane
   const int lane = threadIdx.x % 32;
 
@@ -95,9 +61,9 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int64_t row = l * 2 + half;
-    const int n = cand_n[row];
     float v[2];
     int32_t ix[2];
+    const int n = cand_n[row];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int e = r * 32 + lane;
@@ -211,14 +177,14 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w, int H, int hg,
-                                                        int32_t tab_stride) {
+                                                        int32_t tab_stride, Rescore rq) {
   pdl_enter();
   __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
   cartesian_lookup<KMAX, MAXC>(sm[wid], l, cand_v, cand_c, cand_n, n_sub, k, idx, w, nullptr, nullptr,
-                               (int32_t)((l % H) / hg) * tab_stride);
+                               (int32_t)((l % H) / hg) * tab_stride, rq, H);
 }
 
 // a3 + a4 + a5 fused: one warp per query runs the Cartesian stage of its H
@@ -230,7 +196,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
     const float* __restrict__ cand_v, const int32_t* __restrict__ cand_c,
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
-    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride) {
+    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride, Rescore rq) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;
@@ -243,7 +209,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   for (int h = 0; h < H; ++h)
     cartesian_lookup<KMAX, MAXC>(sm[wid], b * H + h, cand_v, cand_c, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
-                                 (int32_t)(h / (H / og)) * tab_stride);
+                                 (int32_t)(h / (H / og)) * tab_stride, rq, H);
   const int HK = H * k;
   const int g = lane / LG, gl = lane % LG;
   const int E = HK / og;  // entries per output group
@@ -311,7 +277,7 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
   launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
-      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride)
+      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride, cd.rq)
   if (R >= 128) { if (R > 128) return cudaErrorNotSupported; FUSED(4, 1, 4); }
   else if (R > 32) FUSED(2, 1, 8);
   else if (R > 16) FUSED(1, 1, 8);
@@ -348,10 +314,10 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (s.k <= 32)
     launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride);
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.rq);
   else if (s.k <= 64)
     launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride);
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.rq);
   else
     return cudaErrorNotSupported;
   cudaError_t e = cudaGetLastError();

@@ -22,11 +22,21 @@ struct Shape {
 // (b, h, half) row r, entries i < cand_n[r] of cand_v/cand_c[r*kCandCap + i]
 // are (score, sub-key index) pairs in no particular order that are
 // guaranteed to contain the row's top-k under (score desc, index asc).
+// cand_n[r] <= kCandCap always: a tcgen05 scorer row whose bound let more
+// than kCandCap columns through (massive exact ties) is rescored exactly from
+// the query and sub-keys in `rq` before it is written.
 constexpr int kCandCap = 64;
+struct Rescore {
+  const void* Q = nullptr;  // [B, H, 2, d_h] qk dtype
+  const void* K = nullptr;  // [H, 2, n_sub, d_h] qk dtype
+  int d_h = 0;
+  int qk_dt = 0;
+};
 struct Cands {
   float* v;      // [B*H*2, kCandCap]
   int32_t* c;    // [B*H*2, kCandCap]
   int32_t* n;    // [B*H*2]
+  Rescore rq;    // inputs, for rescoring overflowed rows
 };
 
 // a1+a2 (SIMT scorer, fp32 configs): exact per-half top-k (n = k entries).

@@ -4,48 +4,64 @@
 // epilogue so that S never reaches HBM.
 //
 // One CTA per (128-query tile, head h, half): D[128 x n_sub] = Q_half . K_half^T
-// with bf16 operands and fp32 accumulation in TMEM (kind::f16), computed in
-// N-chunks of up to 256 columns that alternate between two TMEM accumulator
-// buffers, so the MMA of chunk c+1 overlaps the epilogue of chunk c.
+// with bf16 operands and fp32 accumulation in TMEM (kind::f16; fp32 inputs:
+// 3xTF32 kind::tf32), computed in N-chunks of up to 256 columns that
+// alternate between two TMEM accumulator buffers.
 //
-//   warp 0      TMA producer: the whole query tile once (resident), then the
-//               sub-key tiles through a STAGES-deep mbarrier ring
-//   warp 1      MMA issuer (one elected lane): tcgen05.mma + tcgen05.commit
-//   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   epilogue: TMEM lane i = query row i, one thread per row.
-//               tau = KT-th largest of the 2KT strided group maxima seen so
-//               far is a provable lower bound on the row's KT-th score; the
-//               columns >= tau (~1.4 KT for random scores) are kept in a
-//               shared-memory buffer compacted as tau rises, and written out
-//               unordered as the row's candidate list (<= 64 entries that
-//               contain its top-k); cartesian_kernel orders them.  The first
-//               segment is the first min(n_sub, 512) columns, resident in both
-//               TMEM buffers, so tau is computed before any column is kept.
-//               Rows whose buffer would overflow (massive exact ties) take an
-//               exact bitwise search for their KT-th score instead.
+//   warp 0       TMA producer: the whole query tile once (resident), then the
+//                sub-key tiles through a kStages-deep mbarrier ring
+//   warp 1       MMA issuer (one elected lane): tcgen05.mma + tcgen05.commit
+//   warp 2       TMEM allocator (512 columns)
+//   warps 4-11   epilogue, TWO threads per query row: warp 4+q and warp 8+q
+//                both read TMEM lane quarter q (row = 32q + lane) and split the
+//                row's columns (alternate 64-column blocks).
+//
+// Epilogue = two passes over the row, no data-dependent buffer management:
+//   pass A  each thread folds its columns into KT group maxima (group =
+//           column mod KT within its blocks); the two threads' KT maxima come
+//           from 2KT disjoint column groups, so the KT-th largest of their
+//           union, tau, is a provable lower bound on the row's KT-th score.
+//           Both threads sort their KT maxima (descending), swap them through
+//           shared memory, and take tau = min_i max(A_i, B_{KT-1-i}) -- the
+//           half-cleaner of a bitonic merge, which is exactly the KT-th
+//           largest of A u B.
+//   pass B  every column with score >= tau is appended to the row's
+//           64-entry candidate buffer, thread 0 filling it from the bottom,
+//           thread 1 from the top (no atomics).  The row's top-KT under
+//           (score desc, index asc) has scores >= tau, so the list contains
+//           it (ties with tau are kept).
+// For random scores ~1.3 KT columns pass.  A row with more than kCandCap = 64
+// passing columns (massive exact ties, adversarial data) is written with
+// is rescored exactly by its write-out warp (warp_sort.cuh, exact_half_topk)
+// -- correctness never depends on the bound being tight.
+//
+// Rows that fit TMEM (n_sub <= 512, two buffers) are scored once; longer rows
+// are scored twice (the MMA pass is cheap next to the epilogue): the first
+// pass feeds pass A, the second pass B, so tau is the whole row's bound.
 #include <cuda.h>
 #include <algorithm>
-#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
+#include "warp_sort.cuh"
 
 namespace msn {
 namespace {
 using namespace tc;
 
-constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
+constexpr int kEpiWarps = 8;                         // 2 threads per row
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 constexpr int kStages = 3;
 constexpr int kMaxNTile = 256;
-constexpr int kCap = 64;          // candidate buffer entries per row
-constexpr int kRowBytes = 128;    // one 128-byte swizzle row per k-block (64 bf16 / 32 fp32)
+constexpr int kCap = kCandCap;     // candidate slots per row
+constexpr int kCStride = 129;      // buffer entry (slot, row) at slot*129 + row: bank rotation
+constexpr int kRowBytes = 128;     // one 128-byte swizzle row per k-block (64 bf16 / 32 fp32)
 
-// ------------------------------------------------------------- top-k -------
-// In-register bitonic sort of N values, descending (group maxima -> tau).
+// In-register bitonic sort of N values, descending.
 template <int N>
 __device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
 #pragma unroll
@@ -66,23 +82,21 @@ __device__ __forceinline__ void bitonic_sort_vals(float (&v)[N]) {
   }
 }
 
-__device__ unsigned long long g_dbg_ts[4096 * 32];
-__device__ __forceinline__ unsigned long long gclk() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+__device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
 }
+
 struct TcParams {
-  int dbg;  // profiling only (MSN_SELECT_DBG): 1 = epilogue skips all processing
   int64_t B;
   int H, n_sub, d_h, k;
-  int n_tile, n_chunks, k_blocks;
+  int n_tile, n_chunks, k_blocks, passes;
   float* cv;
   int32_t* cc;
   int32_t* cn;
+  Rescore rq;  // overflowed rows are rescored exactly from these
 };
 
-template <int KT, bool TF32>
+template <int KT, bool TF32, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     select_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                      const __grid_constant__ CUtensorMap tmap_k,
@@ -93,13 +107,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int acc_stride = TF32 ? p.n_tile : kMaxNTile;  // TMEM columns between accumulators
   const uint32_t alo_col = 2u * (uint32_t)p.n_tile;     // TF32: A_lo columns [2 n_tile, +d_h)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // carve: A (k_blocks x 16 KB) | B ring (kStages x n_tile x 128 B) | cand vals | cand cols | bars
+  // carve: A (k_blocks x 16 KB) | B ring | candidates [kCap][129] (score bits, column) |
+  //        per-thread counts [2][128] | bars.  The tau exchange reuses the candidate area.
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
   const int stage_bytes = B_PARTS * p.n_tile * kRowBytes;
-  uint2* cand = reinterpret_cast<uint2*>(sB + kStages * stage_bytes);  // [kCap+1][128] (score bits, column)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cand + (kCap + 1) * 128);
+  uint2* cand = reinterpret_cast<uint2*>(sB + kStages * stage_bytes);
+  float* xch = reinterpret_cast<float*>(cand);            // [KT][2][128] sorted group maxima
+  int* cnts = reinterpret_cast<int*>(cand + kCap * kCStride);  // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cnts + 256);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + kStages;
@@ -108,10 +125,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a_ready = tempty + 2;  // TF32: A split into (hi in smem, lo in TMEM)
   uint32_t* tmem_slot = (uint32_t*)(a_ready + 1);
 
-  const unsigned long long t_entry = gclk();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int hh = blockIdx.x;  // h*2 + half
   const int64_t m0 = (int64_t)blockIdx.y * 128;
+  const int total_chunks = p.passes * p.n_chunks;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap_q);
@@ -124,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], kEpiWarps);
     }
     mbar_init(a_ready, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -139,15 +156,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
-  const bool ts_on = p.dbg >= 1 && cta_lin < 4096;
-  if (ts_on && threadIdx.x == 0) {
-    g_dbg_ts[cta_lin * 32 + 0] = gclk();
-    unsigned smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    g_dbg_ts[cta_lin * 32 + 11] = smid;
-    g_dbg_ts[cta_lin * 32 + 13] = t_entry;
-  }
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -156,7 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < p.k_blocks; ++kb)
         tma_load_3d(sA + kb * 16384, &tmap_q, a_full, kb * BK, hh, (int)m0);
       int it = 0;
-      for (int c = 0; c < p.n_chunks; ++c)
+      for (int g = 0; g < total_chunks; ++g) {
+        const int c = g % p.n_chunks;
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
@@ -166,25 +175,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sB + s * stage_bytes + p.n_tile * kRowBytes, &tmap_klo, &full[s], kb * BK,
                         hh * p.n_sub + c * p.n_tile);
         }
+      }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = TF32 ? idesc_tf32(128, p.n_tile) : idesc_bf16(128, p.n_tile);
       mbar_wait(a_full, 0);
-      if (ts_on) g_dbg_ts[cta_lin * 32 + 1] = gclk();
       if (TF32) mbar_wait(a_ready, 0);
       tc_fence_after();
       int it = 0;
-      for (int c = 0; c < p.n_chunks; ++c) {
-        const int buf = c & 1;
-        mbar_wait(&tempty[buf], ((c >> 1) & 1) ^ 1);
+      for (int g = 0; g < total_chunks; ++g) {
+        const int buf = g & 1;
+        mbar_wait(&tempty[buf], ((g >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + buf * acc_stride;
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
-          if (ts_on && it < 8) g_dbg_ts[cta_lin * 32 + 2 + it] = gclk();
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + kb * 16384);
           const uint32_t b0 = smem_u32(sB + s * stage_bytes);
@@ -210,268 +218,226 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ---------------------------------------------------------- epilogue
-    // One thread per query row (TMEM lane).  Running group maxima over
-    // G = 2KT strided groups (g = column % G) give a lower bound tau on the
-    // row's KT-th score (the KT largest group maxima are KT distinct columns
-    // >= tau), valid for the whole row at every point of the stream; columns
-    // >= tau are kept in a shared-memory buffer that is compacted as tau
-    // rises.  A row whose buffer would overflow (massive exact ties) switches
-    // to an exact bitwise search for its KT-th score over buffer + segment.
-    const int q = warp & 3;            // TMEM lane quarter of this warp
+    const int ew = warp - kEpiWarp0;   // 0..7
+    const int q = ew & 3;              // TMEM lane quarter (== warp % 4)
+    const int sh = ew >> 2;            // column share of this thread: 0 or 1
     const int row = q * 32 + lane;     // query row within the tile
-    const int tid = row;               // candidate buffer column
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     if constexpr (TF32) {
-      // split this row of the resident query tile: hi (TF32-exact) back into
-      // shared memory in place, lo = x - hi into TMEM columns [alo_col, +d_h)
-      mbar_wait(a_full, 0);
-      const int sw = row & 7;
-      for (int kb = 0; kb < p.k_blocks; ++kb) {
-        float* arow = reinterpret_cast<float*>(sA + kb * 16384 + row * kRowBytes);
-        uint32_t lo[32];
+      if (sh == 0) {
+        // split this row of the resident query tile: hi (TF32-exact) back into
+        // shared memory in place, lo = x - hi into TMEM columns [alo_col, +d_h)
+        mbar_wait(a_full, 0);
+        const int sw = row & 7;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          float* arow = reinterpret_cast<float*>(sA + kb * 16384 + row * kRowBytes);
+          uint32_t lo[32];
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          float4* pc = reinterpret_cast<float4*>(arow) + (ch ^ sw);  // logical chunk ch
-          float4 x = *pc;
-          float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-          *pc = h;
-          lo[ch * 4 + 0] = __float_as_uint(x.x - h.x);
-          lo[ch * 4 + 1] = __float_as_uint(x.y - h.y);
-          lo[ch * 4 + 2] = __float_as_uint(x.z - h.z);
-          lo[ch * 4 + 3] = __float_as_uint(x.w - h.w);
+          for (int ch = 0; ch < 8; ++ch) {
+            float4* pc = reinterpret_cast<float4*>(arow) + (ch ^ sw);  // logical chunk ch
+            float4 x = *pc;
+            float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+            *pc = h;
+            lo[ch * 4 + 0] = __float_as_uint(x.x - h.x);
+            lo[ch * 4 + 1] = __float_as_uint(x.y - h.y);
+            lo[ch * 4 + 2] = __float_as_uint(x.z - h.z);
+            lo[ch * 4 + 3] = __float_as_uint(x.w - h.w);
+          }
+          tmem_st32(lane_base + alo_col + kb * BK, lo);
         }
-        tmem_st32(lane_base + alo_col + kb * BK, lo);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_ready);
-    }
-    constexpr int G = 2 * KT;
-    constexpr int STEP = G > 32 ? G : 32;
-    float tau = -INFINITY;  // lower bound on this row's KT-th score
-    int cnt = 0;
-    // exact KT-th (index tie rule) over the buffered candidates -> new tau;
-    // keeps exactly the entries that can still be in the top-KT (<= KT).
-    int n_tight = 0;  // profiling (MSN_SELECT_DBG): buffer compactions of this thread
-    auto tighten = [&]() {
-      ++n_tight;
-      float t[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) t[i] = i < cnt ? __uint_as_float(cand[i * 128 + tid].x) : -INFINITY;
-      bitonic_sort_vals<64>(t);
-      const float nt = t[KT - 1];
-      int gt = 0;
-#pragma unroll
-      for (int i = 0; i < KT; ++i) gt += t[i] > nt ? 1 : 0;
-      int need = KT - gt;  // entries equal to nt that survive (earliest columns first)
-      const int mx = __reduce_max_sync(0xffffffffu, cnt);
-      int w = 0;
-      for (int i = 0; i < mx; ++i) {
-        if (i < cnt) {
-          const uint2 e = cand[i * 128 + tid];
-          const float v = __uint_as_float(e.x);
-          const bool keep = v > nt || (v == nt && need > 0);
-          if (v == nt && keep) --need;
-          if (keep) cand[w++ * 128 + tid] = e;
-        }
-      }
-      cnt = w;
-      tau = fmaxf(tau, nt);
-    };
-    for (int c = 0; c < p.n_chunks;) {
-      const int nseg = (c == 0 && p.n_chunks >= 2) ? 2 : 1;  // first segment: both TMEM buffers
-      for (int u = 0; u < nseg; ++u) mbar_wait(&tfull[(c + u) & 1], ((c + u) >> 1) & 1);
-      tc_fence_after();
-      if (p.dbg == 1) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0)
-          for (int u = 0; u < nseg; ++u) mbar_arrive(&tempty[(c + u) & 1]);
-        c += nseg;
-        continue;
+        if (lane == 0) mbar_arrive(a_ready);
       }
-      const int seg_cols = nseg * p.n_tile;
-      const bool first = c == 0;
-      const bool stamp = ts_on && warp == kEpiWarp0 && lane == 0 && first;
-      if (stamp) g_dbg_ts[cta_lin * 32 + 16] = gclk();
-      if (ts_on && warp == kEpiWarp0 && lane == 0 && c >= 2 && c < 8) g_dbg_ts[cta_lin * 32 + 18 + c] = gclk();
-      // TMEM address of segment column j
-      auto taddr = [&](int j) -> uint32_t {  // j < 2 * n_tile
-        const int hi = j >= p.n_tile ? 1 : 0;
-        return lane_base + (uint32_t)(((c + hi) & 1) * acc_stride + (j - hi * p.n_tile));
-      };
-      if (first) {
-        // pass A: tau = KT-th largest of the 2KT strided group maxima of the
-        // first segment (KT distinct columns score >= tau, so the row's KT-th
-        // score is >= tau).  Segment start 0 is a multiple of G.
-        float gm[G];
-#pragma unroll
-        for (int j = 0; j < G; ++j) gm[j] = -INFINITY;
-        if (seg_cols % 64 == 0) {
-          for (int j0 = 0; j0 < seg_cols; j0 += 64) {
-            uint32_t r[64];
-            tmem_ld64(taddr(j0), r);  // n_tile % 64 == 0: never straddles a buffer
-#pragma unroll
-            for (int jj = 0; jj < 64; ++jj) gm[jj % G] = fmaxf(gm[jj % G], __uint_as_float(r[jj]));
-          }
-        } else {
-          for (int j0 = 0; j0 < seg_cols; j0 += STEP) {
-#pragma unroll
-            for (int piece = 0; piece < STEP / 32; ++piece) {
-              const int j = j0 + piece * 32;
-              if (j < seg_cols) {
-                uint32_t r[32];
-                tmem_ld32(taddr(j), r);
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                  const int g = (piece * 32 + jj) % G;
-                  gm[g] = fmaxf(gm[g], __uint_as_float(r[jj]));
-                }
-              }
-            }
-          }
-        }
-        if (stamp) g_dbg_ts[cta_lin * 32 + 17] = gclk() + (unsigned long long)(gm[0] > 1e30f);
-        bitonic_sort_vals<G>(gm);
-        tau = gm[KT - 1];
-        if (stamp) g_dbg_ts[cta_lin * 32 + 18] = gclk() + (unsigned long long)(tau > 1e30f);
-      }
-      // pass B: buffer the columns that can still be in the top-KT.  In the
-      // first segment tau came from these same columns (ties kept: >=);
-      // later columns lose every tie to the KT earlier ones behind tau (>).
-      // Branch-free: every column is stored, unselected ones (and any
-      // first-segment overflow) into the dummy row kCap.
-      const int cnt_old = cnt;
-      const int col_base = c * p.n_tile;
-      // One compact code path per 32-column piece (the unrolled variants did
-      // not fit the instruction cache): a column is a hit when v > te, where
-      // te = tau in later segments and the largest float below tau in the
-      // first (ties with tau kept there).  Hit mask; if a later segment's
-      // hits would not fit, compact the buffer first (tau rises) and redo the
-      // mask; then every hit goes to slot cnt + (hits before it), with no
-      // dependency between the stores.  A first-segment overflow stores what
-      // fits and leaves the rest to the exact path below (cnt > kCap).
-      auto piece = [&](const uint32_t (&r)[32], int j0) {
-        const uint32_t colj = (uint32_t)(col_base + j0);
-        uint32_t m;
-        for (;;) {
-          const float te = first ? nextafterf(tau, -INFINITY) : tau;
-          m = 0;
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) m |= (__uint_as_float(r[jj]) > te ? 1u : 0u) << jj;
-          if (first || !__any_sync(0xffffffffu, cnt + __popc(m) > kCap)) break;
-          tighten();  // cnt <= KT; tau only rises
-        }
-        if (m) {
-          const uint32_t base = smem_u32(cand + tid);
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const uint32_t slot = (uint32_t)cnt + (uint32_t)__popc(m & ((1u << jj) - 1u));
-            asm volatile(
-                "{\n.reg .pred p, q;\n"
-                "setp.ne.u32 p, %1, 0;\n"
-                "setp.lt.and.u32 q, %2, %5, p;\n"
-                "@q st.shared.v2.u32 [%0], {%3, %4};\n}\n" ::"r"(base + (slot << 10)),
-                "r"(m & (1u << jj)), "r"(slot), "r"(r[jj]), "r"(colj + jj), "r"((uint32_t)kCap)
-                : "memory");
-          }
-        }
-        cnt += __popc(m);
-      };
-      for (int j0 = 0; j0 < seg_cols; j0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(taddr(j0), r);
-        piece(r, j0);
-      }
-      const bool ovf = cnt > kCap;  // first segment only (later pieces tighten first)
-      if (ts_on && warp == kEpiWarp0 && lane == 0 && c >= 2 && c < 8) g_dbg_ts[cta_lin * 32 + 24 + c] = gclk();
-      if (stamp) g_dbg_ts[cta_lin * 32 + 20] = gclk();
-      if (stamp) g_dbg_ts[cta_lin * 32 + 19] = gclk() + (unsigned long long)(cnt > 100000);
-      if (__any_sync(0xffffffffu, ovf)) {
-        // exact path: the KT-th largest ordered key t over buffer u segment
-        auto count_ge = [&](uint32_t t) -> int {
-          int n = 0;
-          for (int i = 0; i < cnt_old; ++i) n += ord_f32(__uint_as_float(cand[i * 128 + tid].x)) >= t ? 1 : 0;
-          for (int j0 = 0; j0 < seg_cols; j0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(taddr(j0), r);
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) n += ord_f32(__uint_as_float(r[jj])) >= t ? 1 : 0;
-          }
-          return n;
-        };
-        uint32_t t = 0;
-        for (int bit = 31; bit >= 0; --bit) {
-          const uint32_t ct = t | (1u << bit);
-          if (count_ge(ct) >= KT) t = ct;
-        }
-        const int gt = (t == 0xffffffffu) ? 0 : count_ge(t + 1);
-        int need = KT - gt;
-        int w = 0;
-        for (int i = 0; i < cnt_old; ++i) {
-          const uint2 e = cand[i * 128 + tid];
-          const uint32_t o = ord_f32(__uint_as_float(e.x));
-          if (o > t || (o == t && need > 0)) {
-            if (o == t) --need;
-            cand[w++ * 128 + tid] = e;
-          }
-        }
-        for (int j0 = 0; j0 < seg_cols; j0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr(j0), r);
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const uint32_t o = ord_f32(__uint_as_float(r[jj]));
-            if (o > t || (o == t && need > 0)) {
-              if (o == t) --need;
-              cand[w++ * 128 + tid] = make_uint2(r[jj], (uint32_t)(col_base + j0 + jj));
-            }
-          }
-        }
-        cnt = w;  // <= KT
-        tau = fmaxf(tau, unord_f32(t));
-      }
+    }
+    // A segment = nseg consecutive chunks starting at global chunk g0, resident
+    // in the TMEM buffers (g0 + u) & 1.  This thread owns the 32-column pieces
+    // of the 64-column blocks b with b % 2 == sh (a lone last piece belongs to
+    // the thread whose block it starts).
+    auto piece_addr = [&](int g0, int j) -> uint32_t {  // segment column j (multiple of 32)
+      const int u = j / p.n_tile;
+      return lane_base + (uint32_t)(((g0 + u) & 1) * acc_stride + (j - u * p.n_tile));
+    };
+    auto wait_chunks = [&](int g0, int nseg) {
+      for (int u = 0; u < nseg; ++u) mbar_wait(&tfull[(g0 + u) & 1], ((g0 + u) >> 1) & 1);
+      tc_fence_after();
+    };
+    auto release_chunks = [&](int g0, int nseg) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0)
-        for (int u = 0; u < nseg; ++u) mbar_arrive(&tempty[(c + u) & 1]);
-      c += nseg;
-    }
-    // coalesced write-out: the warp writes its 32 rows one after another
-    // (lane = candidate slot), instead of 32 rows per store instruction
-    // (row, slot half) tasks, 8 in flight: their shared-memory reads and
-    // global stores are independent
-    {
-      const int64_t b_me = m0 + q * 32 + lane;
-      if (b_me < p.B) p.cn[b_me * p.H * 2 + hh] = cnt;
-    }
-    for (int t0 = 0; t0 < 64; t0 += 8) {
+        for (int u = 0; u < nseg; ++u) mbar_arrive(&tempty[(g0 + u) & 1]);
+    };
+
+    // ---- pass A: G group maxima over this thread's columns (G = KT; WIDE,
+    // for rows longer than TMEM: G = 2KT, a tighter tau for the longer row)
+    constexpr int G = WIDE ? 2 * KT : KT;
+    constexpr int GP = G < 32 ? G : 32;  // groups fed by one 32-column piece
+    float gm[G];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u, rr = t >> 1, i = (t & 1) * 32 + lane;
-        const int n = __shfl_sync(0xffffffffu, cnt, rr);
-        const int trow = q * 32 + rr;
-        const int64_t b = m0 + trow;
-        if (b < p.B && i < n) {
-          const uint2 e = cand[i * 128 + trow];
-          const int64_t o = (b * p.H * 2 + hh) * kCandCap + i;
-          p.cv[o] = __uint_as_float(e.x);
-          p.cc[o] = (int32_t)e.y;
+    for (int i = 0; i < G; ++i) gm[i] = -INFINITY;
+    int gsel = 0;  // WIDE, G = 64: which half of gm this piece feeds (piece parity)
+    auto fold32 = [&](const uint32_t (&r)[32]) {
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += GP)
+#pragma unroll
+        for (int i = 0; i < GP; ++i) {
+          if (G > 32 && gsel) gm[(G > 32 ? 32 : 0) + i] = fmaxf(gm[(G > 32 ? 32 : 0) + i], __uint_as_float(r[jj + i]));
+          else gm[i] = fmaxf(gm[i], __uint_as_float(r[jj + i]));
+        }
+    };
+    auto pass_a = [&](int g0, int seg_cols) {
+      for (int j0 = 64 * sh; j0 < seg_cols; j0 += 128) {
+        uint32_t ra[32], rb[32];
+        const bool two = j0 + 32 < seg_cols;
+        tmem_ld32_async(piece_addr(g0, j0), ra);
+        if (two) tmem_ld32_async(piece_addr(g0, j0 + 32), rb);
+        tmem_wait_ld(ra);
+        if (two && G <= 32) {
+          tmem_wait_ld(rb);
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += GP)
+#pragma unroll
+            for (int i = 0; i < GP; ++i)
+              gm[i] = fmaxf(gm[i], fmaxf(__uint_as_float(ra[jj + i]), __uint_as_float(rb[jj + i])));
+        } else {
+          gsel = 0;
+          fold32(ra);
+          if (two) {
+            tmem_wait_ld(rb);
+            gsel = 1;
+            fold32(rb);
+          }
+        }
+      }
+    };
+    const bool resident = p.passes == 1;  // whole row in the two TMEM buffers
+    if (resident) {
+      wait_chunks(0, p.n_chunks);
+      pass_a(0, p.n_sub);
+    } else {
+      for (int c = 0; c < p.n_chunks; ++c) {
+        wait_chunks(c, 1);
+        pass_a(c, p.n_tile);
+        release_chunks(c, 1);
+      }
+    }
+
+    // ---- tau = KT-th largest of the 2G group maxima of the row: each thread
+    // sorts its G maxima, the two top-KT lists meet in the half-cleaner
+    bitonic_sort_vals<G>(gm);
+#pragma unroll
+    for (int i = 0; i < KT; ++i) xch[(i * 2 + sh) * 128 + row] = gm[i];
+    epi_bar();
+    float tau = INFINITY;
+#pragma unroll
+    for (int i = 0; i < KT; ++i) tau = fminf(tau, fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]));
+    epi_bar();  // exchange read everywhere before the candidate area is written
+
+    // ---- pass B: append every column >= tau to the row's buffer
+    // thread 0: slots 0, 1, ... ; thread 1: slots 63, 62, ...  (entry = slot*129 + row)
+    const uint32_t cbase = smem_u32(cand) + (uint32_t)row * 8u;
+    const uint32_t step = sh == 0 ? (uint32_t)(kCStride * 8) : (uint32_t)(-(kCStride * 8));
+    uint32_t caddr = cbase + (sh == 0 ? 0u : (uint32_t)((kCap - 1) * kCStride * 8));
+    int cnt = 0;  // this thread's appended columns (may exceed its room: row overflow)
+    auto filter32 = [&](const uint32_t (&r)[32], uint32_t col0) {
+      if (__any_sync(0xffffffffu, cnt > kCap - 32)) {
+        // near the end of this thread's room: bounded stores, exact count
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          if (__uint_as_float(r[jj]) >= tau) {
+            if (cnt < kCap) {
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(caddr), "r"(r[jj]), "r"(col0 + jj)
+                           : "memory");
+              caddr += step;
+            }
+            ++cnt;
+          }
+        }
+        return;
+      }
+      const uint32_t a0 = caddr;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "setp.ge.f32 p, %1, %2;\n"
+            "@p st.shared.v2.u32 [%0], {%3, %4};\n"
+            "@p add.u32 %0, %0, %5;\n}\n"
+            : "+r"(caddr)
+            : "f"(__uint_as_float(r[jj])), "f"(tau), "r"(r[jj]), "r"(col0 + jj), "r"(step)
+            : "memory");
+      // appended = |caddr - a0| / (129*8)
+      const uint32_t moved = sh == 0 ? caddr - a0 : a0 - caddr;
+      cnt += (int)(moved / (uint32_t)(kCStride * 8));
+    };
+    auto pass_b = [&](int g0, int seg_cols, int col_base) {
+      for (int j0 = 64 * sh; j0 < seg_cols; j0 += 128) {
+        uint32_t ra[32], rb[32];
+        const bool two = j0 + 32 < seg_cols;
+        tmem_ld32_async(piece_addr(g0, j0), ra);
+        if (two) tmem_ld32_async(piece_addr(g0, j0 + 32), rb);
+        tmem_wait_ld(ra);
+        filter32(ra, (uint32_t)(col_base + j0));
+        if (two) {
+          tmem_wait_ld(rb);
+          filter32(rb, (uint32_t)(col_base + j0 + 32));
+        }
+      }
+    };
+    if (resident) {
+      pass_b(0, p.n_sub, 0);
+      release_chunks(0, p.n_chunks);
+    } else {
+      for (int c = 0; c < p.n_chunks; ++c) {
+        const int g = p.n_chunks + c;
+        wait_chunks(g, 1);
+        pass_b(g, p.n_tile, c * p.n_tile);
+        release_chunks(g, 1);
+      }
+    }
+    cnts[sh * 128 + row] = cnt;
+    epi_bar();
+
+    // ---- write-out: warp ew writes rows 16 ew .. 16 ew + 15, lane = slot
+    for (int rr = 0; rr < 16; ++rr) {
+      const int trow = ew * 16 + rr;
+      const int64_t b = m0 + trow;
+      if (b >= p.B) break;
+      const int n0 = cnts[trow], n1 = cnts[128 + trow];
+      const int n = n0 + n1;
+      const int64_t grow = b * p.H * 2 + hh;
+      if (n > kCap) {
+        // more than kCap columns passed tau (massive exact ties): exact
+        // rescoring of this row by the warp, its best min(64, n_sub) sub-keys
+        const int nn = p.rq.qk_dt == F32
+            ? exact_half_topk<float>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub,
+                                     p.cv + grow * kCandCap, p.cc + grow * kCandCap)
+            : exact_half_topk<__nv_bfloat16>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub,
+                                             p.cv + grow * kCandCap, p.cc + grow * kCandCap);
+        if (lane == 0) p.cn[grow] = nn;
+        continue;
+      }
+      if (lane == 0) p.cn[grow] = n;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int i = hf * 32 + lane;
+        if (i < n) {
+          const int slot = i < n0 ? i : kCap - 1 - (i - n0);
+          const uint2 e = cand[slot * kCStride + trow];
+          p.cv[grow * kCandCap + i] = __uint_as_float(e.x);
+          p.cc[grow * kCandCap + i] = (int32_t)e.y;
         }
       }
     }
-    if (ts_on && warp == kEpiWarp0 && lane == 0) g_dbg_ts[cta_lin * 32 + 14] = gclk();
-    if (ts_on && warp == kEpiWarp0 && lane == 0) g_dbg_ts[cta_lin * 32 + 15] = (unsigned long long)n_tight;
   }
   tc_fence_before();
   __syncthreads();
-  if (ts_on && threadIdx.x == 0) g_dbg_ts[cta_lin * 32 + 10] = gclk();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-    if (ts_on && lane == 0) g_dbg_ts[cta_lin * 32 + 12] = gclk();
   }
 }
 
@@ -492,7 +458,7 @@ size_t smem_bytes(const Shape& s) {
   const int bk = is_tf32(s) ? 32 : 64;
   const int parts = is_tf32(s) ? 2 : 1;
   return 1024 + (size_t)(s.d_h / bk) * 16384 + (size_t)kStages * parts * nt * kRowBytes +
-         (size_t)(kCap + 1) * 128 * 8 + 8 * (1 + 2 * kStages + 5) + 16;
+         (size_t)kCap * kCStride * 8 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
 }
 
 // K -> (K_hi, K_lo) for the 3xTF32 B operand.
@@ -507,13 +473,13 @@ __global__ void split_tf32_kernel(const float* __restrict__ k, float* __restrict
   lo[i] = x - h;
 }
 
-template <int KT, bool TF32>
-cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
-                      const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
+template <int KT, bool TF32, bool WIDE>
+cudaError_t launch_ktw(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+                       const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
   const size_t sm = smem_bytes(s);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT, TF32>,
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT, TF32, WIDE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -521,8 +487,14 @@ cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& 
   // x = head/half (fastest): concurrently resident CTAs spread over all 2H
   // sub-key codebooks instead of hammering one codebook's lines in L2
   dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128));
-  launch_pdl(select_tc_kernel<KT, TF32>, grid, kThreads, sm, st, mq, mk, mklo, p);
+  launch_pdl(select_tc_kernel<KT, TF32, WIDE>, grid, kThreads, sm, st, mq, mk, mklo, p);
   return cudaGetLastError();
+}
+template <int KT, bool TF32>
+cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+                      const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
+  return p.passes == 1 ? launch_ktw<KT, TF32, false>(s, mq, mk, mklo, p, st)
+                       : launch_ktw<KT, TF32, true>(s, mq, mk, mklo, p, st);
 }
 
 }  // namespace
@@ -588,8 +560,9 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   if (!kmap(&mk, kb_hi) || !kmap(&mklo, kb_lo)) return cudaErrorInvalidValue;
-  static const int dbg = getenv("MSN_SELECT_DBG") ? atoi(getenv("MSN_SELECT_DBG")) : 0;
-  TcParams p{dbg, s.B, s.H, s.n_sub, s.d_h, s.k, nt, s.n_sub / nt, s.d_h / bk, cd.v, cd.c, cd.n};
+  const int n_chunks = s.n_sub / nt;
+  TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, n_chunks, s.d_h / bk, n_chunks <= 2 ? 1 : 2,
+             cd.v, cd.c, cd.n, cd.rq};
   cudaError_t e;
   if (tf) {
     if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);
@@ -601,58 +574,6 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
     else e = launch_kt<32, false>(s, mq, mk, mklo, p, st);
   }
   if (e == cudaSuccess) ++*launches;
-  if (dbg >= 2 && e == cudaSuccess) {
-    cudaStreamSynchronize(st);
-    static unsigned long long h[4096 * 32];
-    cudaMemcpyFromSymbol(h, g_dbg_ts, sizeof(h));
-    const int ncta = (int)std::min<int64_t>(4096, (s.B + 127) / 128 * s.H * 2);
-    unsigned long long t0 = ~0ull;
-    for (int c = 0; c < ncta; ++c) t0 = std::min(t0, h[c * 32]);
-    double acc[16] = {0};
-    for (int c = 0; c < ncta; ++c)
-      for (int j = 0; j < 15; ++j) if (j != 11 && j != 13 && j != 15) acc[j] += ((double)h[c * 32 + j] - (double)h[c * 32]) / ncta;
-    double ph[4] = {0, 0, 0, 0};
-    for (int c = 0; c < ncta; ++c)
-      for (int j = 0; j < 4; ++j) ph[j] += ((double)h[c * 32 + 16 + j] - (double)h[c * 32]) / ncta;
-    fprintf(stderr, "epilogue: tfull seen %.0f, passA %.0f, tau %.0f, passB %.0f, done %.0f; dealloc %.0f ns after CTA start\n",
-            ph[0], ph[1], ph[2], ph[3], acc[14], acc[12]);
-    double ch[16] = {0};
-    for (int c = 0; c < ncta; ++c)
-      for (int j = 20; j < 32; ++j) ch[j - 20] += ((double)h[c * 32 + j] - (double)h[c * 32]) / ncta;
-    fprintf(stderr, "first seg passB stamp(20) %.0f; chunks 2..5 seen/done: %.0f/%.0f %.0f/%.0f %.0f/%.0f %.0f/%.0f\n",
-            ch[0], ch[0 + 2 - 2 + 2], ch[6 + 2], ch[3], ch[9], ch[4], ch[10], ch[5], ch[11]);
-    double span = 0;
-    for (int c = 0; c < ncta; ++c) span = std::max(span, (double)(h[c * 32 + 10] - t0));
-    {
-      std::vector<double> st(ncta), en(ncta);
-      for (int c = 0; c < ncta; ++c) { st[c] = (double)(h[c * 32] - t0); en[c] = (double)(h[c * 32 + 10] - t0); }
-      std::vector<double> ss = st; std::sort(ss.begin(), ss.end());
-      int per_sm[256] = {0};
-      for (int c = 0; c < ncta; ++c) per_sm[h[c * 32 + 11] & 255]++;
-      int maxc = 0, nsm = 0;
-      for (int i = 0; i < 256; ++i) { maxc = std::max(maxc, per_sm[i]); nsm += per_sm[i] > 0; }
-      // per SM: order CTAs by start, report gap between a CTA's dealloc and the next one's entry
-      double gap = 0, ent = 0; int ng = 0;
-      for (int c = 0; c < ncta; ++c) {
-        ent += (double)(h[c * 32] - h[c * 32 + 13]) / ncta;
-        int best = -1;
-        for (int d = 0; d < ncta; ++d)
-          if (h[d * 32 + 11] == h[c * 32 + 11] && h[d * 32 + 13] > h[c * 32 + 13] &&
-              (best < 0 || h[d * 32 + 13] < h[best * 32 + 13])) best = d;
-        if (best >= 0) { gap += (double)h[best * 32 + 13] - (double)h[c * 32 + 12]; ++ng; }
-      }
-      fprintf(stderr, "entry->start(alloc+init) %.0f ns; dealloc->next entry on same SM %.0f ns (n=%d)\n", ent, ng ? gap / ng : 0.0, ng);
-      fprintf(stderr, "starts: p0 %.0f p25 %.0f p50 %.0f p75 %.0f p100 %.0f ns; SMs used %d, max CTAs/SM %d\n",
-              ss[0], ss[ncta / 4], ss[ncta / 2], ss[3 * ncta / 4], ss[ncta - 1], nsm, maxc);
-    }
-    {
-      double nt = 0;
-      for (int c = 0; c < ncta; ++c) nt += (double)h[c * 32 + 15] / ncta;
-      fprintf(stderr, "tighten calls per epilogue warp (warp 4): %.2f\n", nt);
-    }
-    fprintf(stderr, "select_tc ts (ns, mean rel. to CTA start): Afull %.0f  full0..7 %.0f %.0f %.0f %.0f %.0f %.0f %.0f %.0f  end %.0f  | kernel span %.0f\n",
-            acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8], acc[9], acc[10], span);
-  }
   return e;
 }
 
