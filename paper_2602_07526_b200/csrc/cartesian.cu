@@ -26,6 +26,7 @@
 #include "kernels.h"
 #include "gate.cuh"
 #include "warp_sort.cuh"
+#include "gather_rows.cuh"
 
 namespace msn {
 namespace {
@@ -51,8 +52,7 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
                                                  const int32_t* __restrict__ cand_n, int n_sub,
                                                  int k, int32_t* __restrict__ idx,
                                                  float* __restrict__ w, int32_t* s_idx,
-                                                 float* s_w, int32_t tab_off, const Rescore& rq,
-                                                 int H) {
+                                                 float* s_w, int32_t tab_off) {
   constexpr int APL = KMAX / 32;  // rows a per lane
   const int lane = threadIdx.x % 32;
 
@@ -177,14 +177,14 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w, int H, int hg,
-                                                        int32_t tab_stride, Rescore rq) {
+                                                        int32_t tab_stride) {
   pdl_enter();
   __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
   cartesian_lookup<KMAX, MAXC>(sm[wid], l, cand_v, cand_c, cand_n, n_sub, k, idx, w, nullptr, nullptr,
-                               (int32_t)((l % H) / hg) * tab_stride, rq, H);
+                               (int32_t)((l % H) / hg) * tab_stride);
 }
 
 // a3 + a4 + a5 fused: one warp per query runs the Cartesian stage of its H
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
     const float* __restrict__ cand_v, const int32_t* __restrict__ cand_c,
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
-    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride, Rescore rq) {
+    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;
@@ -209,64 +209,29 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   for (int h = 0; h < H; ++h)
     cartesian_lookup<KMAX, MAXC>(sm[wid], b * H + h, cand_v, cand_c, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
-                                 (int32_t)(h / (H / og)) * tab_stride, rq, H);
+                                 (int32_t)(h / (H / og)) * tab_stride);
   const int HK = H * k;
   const int g = lane / LG, gl = lane % LG;
   const int E = HK / og;  // entries per output group
-  for (int grp = 0; grp < og; ++grp) {
-  float acc[VPL][PER];
-#pragma unroll
-  for (int v = 0; v < VPL; ++v)
-#pragma unroll
-    for (int e = 0; e < PER; ++e) acc[v][e] = 0.f;
   const int row_vecs = d_v / PER;
-  for (int base = grp * E + g; base < (grp + 1) * E; base += G * U) {
-    uint4 x[U][VPL];
-    float wt[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = base + u * G;
-      const int f = r < (grp + 1) * E ? s_idx[wid][r] : -1;
-      wt[u] = f >= 0 ? s_w[wid][r] : 0.f;
-      const VT* row = V + (int64_t)(f >= 0 ? f : 0) * d_v;
+  for (int grp = 0; grp < og; ++grp) {
+    float acc[VPL][PER];
+    gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * E, (grp + 1) * E, V, d_v, acc);
+    if (g == 0) {
+      const int64_t orow = b * og + grp;
+      float* o = out + orow * d_v;
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int vec = gl * VPL + v;
-        if (f >= 0 && vec < row_vecs) x[u][v] = ldg_nc_v4(row + vec * PER);
-        else x[u][v] = make_uint4(0, 0, 0, 0);
+        if (vec < row_vecs) {
+#pragma unroll
+          for (int e = 0; e < PER; e += 4)
+            *reinterpret_cast<float4*>(o + vec * PER + e) =
+                make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
+        }
       }
+      if (gate.kind) store_gated<VPL, PER>(gate, orow, d_v, gl, row_vecs, acc);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        float f[PER];
-        unpack16<VT>(x[u][v], f);
-#pragma unroll
-        for (int e = 0; e < PER; ++e) acc[v][e] = fmaf(wt[u], f[e], acc[v][e]);
-      }
-  }
-#pragma unroll
-  for (int m = LG; m < 32; m <<= 1)
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-#pragma unroll
-      for (int e = 0; e < PER; ++e) acc[v][e] += __shfl_xor_sync(0xffffffffu, acc[v][e], m);
-  if (g == 0) {
-    const int64_t orow = b * og + grp;
-    float* o = out + orow * d_v;
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vec = gl * VPL + v;
-      if (vec < row_vecs) {
-#pragma unroll
-        for (int e = 0; e < PER; e += 4)
-          *reinterpret_cast<float4*>(o + vec * PER + e) =
-              make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
-      }
-    }
-    if (gate.kind) store_gated<VPL, PER>(gate, orow, d_v, gl, row_vecs, acc);
-  }
   }  // output groups
 }
 
@@ -277,15 +242,8 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
   launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
-      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride, cd.rq)
-  if (R >= 128) { if (R > 128) return cudaErrorNotSupported; FUSED(4, 1, 4); }
-  else if (R > 32) FUSED(2, 1, 8);
-  else if (R > 16) FUSED(1, 1, 8);
-  else if (R > 8) FUSED(1, 2, 8);
-  else if (R > 4) FUSED(1, 4, 8);
-  else if (R > 2) FUSED(1, 8, 8);
-  else if (R > 1) FUSED(1, 16, 8);
-  else FUSED(1, 32, 8);
+      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride)
+  MSN_GATHER_DISPATCH(R, FUSED);
 #undef FUSED
   return cudaGetLastError();
 }
@@ -314,10 +272,10 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (s.k <= 32)
     launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.rq);
+               s.H, s.H / s.og, (int32_t)s.tab_stride);
   else if (s.k <= 64)
     launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.rq);
+               s.H, s.H / s.og, (int32_t)s.tab_stride);
   else
     return cudaErrorNotSupported;
   cudaError_t e = cudaGetLastError();

@@ -543,3 +543,20 @@ def test_invalid_arguments_raise():
     big = wl.make_queries(cfg.scaled(batch=17), DEV)
     with pytest.raises(MsnError):
         lk.forward(big, K, V)
+
+
+@pytest.mark.parametrize("name,B,groups", [("c2_mid_bf16", 8192 + 37, 1), ("c3_train_fp32_zipf", 8192 + 5, 1),
+                                           ("f4_tokens_bf16", 40, 16)])
+def test_fused_forward_matches_phases(name, B, groups):
+    """msn_pkm_forward (fused Cartesian + gather for B >= 8192) and the phase
+    calls select + gather add in the same order (gather_rows.cuh): bitwise
+    equal idx, weights and outputs."""
+    cfg = wl.CONFIGS[name].scaled(batch=B)
+    Q, K, V, _ = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg, head_groups=groups)
+    out, idx, w = lk.forward(Q, K, V)
+    i2, w2 = lk.select(Q, K)
+    o2 = lk.gather(i2, w2, V)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, i2) and torch.equal(w, w2)
+    assert torch.equal(out, o2)
