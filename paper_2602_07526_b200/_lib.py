@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsn_pkm.so")
+# MSN_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("MSN_LIB", os.path.join(_HERE, "libmsn_pkm.so"))
 
 ABI_VERSION = 1
 MSN_F32, MSN_BF16 = 0, 1

@@ -59,11 +59,10 @@ Shape shape_of(const msn_pkm_config& c, int64_t B) {
   return s;
 }
 
-// forward workspace layout: [cand_v | cand_c | cand_n | scores (SIMT scorer only)]
+// forward workspace layout: [cand (score, index) | cand_n | scores (SIMT scorer only)]
 size_t fwd_bytes(const Shape& s) {
   const int64_t rows = s.B * s.H * 2;
-  size_t b = align256(sizeof(float) * rows * kCandCap) + align256(sizeof(int32_t) * rows * kCandCap) +
-             align256(sizeof(int32_t) * rows);
+  size_t b = align256(sizeof(uint2) * rows * kCandCap) + align256(sizeof(int32_t) * rows);
   if (!select_tc_supported(s)) b += align256(sizeof(float) * rows * s.n_sub);
   else b += align256(select_tc_workspace_bytes(s));
   return b;
@@ -100,10 +99,8 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   const int64_t rows = B * s.H * 2;
   char* p = (char*)ws;
   Cands cd;
-  cd.v = (float*)p;
-  p += align256(sizeof(float) * rows * kCandCap);
-  cd.c = (int32_t*)p;
-  p += align256(sizeof(int32_t) * rows * kCandCap);
+  cd.vc = (uint2*)p;
+  p += align256(sizeof(uint2) * rows * kCandCap);
   cd.n = (int32_t*)p;
   p += align256(sizeof(int32_t) * rows);
   cd.rq.Q = query;

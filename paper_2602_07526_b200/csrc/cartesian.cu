@@ -47,8 +47,7 @@ struct CartSmem {
 // s_idx/s_w are given, to shared memory too (for a fused gather).
 template <int KMAX, int MAXC>
 __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64_t l,
-                                                 const float* __restrict__ cand_v,
-                                                 const int32_t* __restrict__ cand_c,
+                                                 const uint2* __restrict__ cand,
                                                  const int32_t* __restrict__ cand_n, int n_sub,
                                                  int k, int32_t* __restrict__ idx,
                                                  float* __restrict__ w, int32_t* s_idx,
@@ -68,8 +67,9 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     for (int r = 0; r < 2; ++r) {
       const int e = r * 32 + lane;
       const bool ok = e < n;
-      v[r] = ok ? cand_v[row * kCandCap + e] : -INFINITY;
-      ix[r] = ok ? cand_c[row * kCandCap + e] : 0x7fffffff;
+      const uint2 c = ok ? cand[row * kCandCap + e] : make_uint2(__float_as_uint(-INFINITY), 0x7fffffffu);
+      v[r] = __uint_as_float(c.x);
+      ix[r] = (int32_t)c.y;
     }
     warp_sort64(v, ix);
     if (half == 0) {
@@ -171,8 +171,7 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
 }
 
 template <int KMAX, int MAXC>
-__global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict__ cand_v,
-                                                        const int32_t* __restrict__ cand_c,
+__global__ void __launch_bounds__(256) cartesian_kernel(const uint2* __restrict__ cand,
                                                         const int32_t* __restrict__ cand_n,
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
@@ -183,7 +182,7 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
-  cartesian_lookup<KMAX, MAXC>(sm[wid], l, cand_v, cand_c, cand_n, n_sub, k, idx, w, nullptr, nullptr,
+  cartesian_lookup<KMAX, MAXC>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, nullptr, nullptr,
                                (int32_t)((l % H) / hg) * tab_stride);
 }
 
@@ -193,7 +192,7 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const float* __restrict_
 // summation order as cartesian_kernel + gather_kernel.
 template <int KMAX, int MAXC, typename VT, int VPL, int G, int U>
 __global__ void __launch_bounds__(256) cartesian_gather_kernel(
-    const float* __restrict__ cand_v, const int32_t* __restrict__ cand_c,
+    const uint2* __restrict__ cand,
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
     float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride) {
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (b >= B) return;
   for (int h = 0; h < H; ++h)
-    cartesian_lookup<KMAX, MAXC>(sm[wid], b * H + h, cand_v, cand_c, cand_n, n_sub, k, idx, w,
+    cartesian_lookup<KMAX, MAXC>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
                                  (int32_t)(h / (H / og)) * tab_stride);
   const int HK = H * k;
@@ -242,7 +241,7 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
   launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
-      cd.v, cd.c, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride)
+      cd.vc, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride)
   MSN_GATHER_DISPATCH(R, FUSED);
 #undef FUSED
   return cudaGetLastError();
@@ -271,10 +270,10 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
   const int64_t L = s.B * s.H;
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (s.k <= 32)
-    launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w,
+    launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
                s.H, s.H / s.og, (int32_t)s.tab_stride);
   else if (s.k <= 64)
-    launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.v, cd.c, cd.n, L, s.n_sub, s.k, idx, w,
+    launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
                s.H, s.H / s.og, (int32_t)s.tab_stride);
   else
     return cudaErrorNotSupported;

@@ -19,8 +19,8 @@ struct Shape {
 };
 
 // Per-half candidate lists, the hand-off between a1+a2 and a3: for every
-// (b, h, half) row r, entries i < cand_n[r] of cand_v/cand_c[r*kCandCap + i]
-// are (score, sub-key index) pairs in no particular order that are
+// (b, h, half) row r, entries i < cand_n[r] of vc[r*kCandCap + i] are
+// (score bits, sub-key index) pairs in no particular order that are
 // guaranteed to contain the row's top-k under (score desc, index asc).
 // cand_n[r] <= kCandCap always: a tcgen05 scorer row whose bound let more
 // than kCandCap columns through (massive exact ties) is rescored exactly from
@@ -33,8 +33,7 @@ struct Rescore {
   int qk_dt = 0;
 };
 struct Cands {
-  float* v;      // [B*H*2, kCandCap]
-  int32_t* c;    // [B*H*2, kCandCap]
+  uint2* vc;     // [B*H*2, kCandCap] (float bits of the score, sub-key index)
   int32_t* n;    // [B*H*2]
   Rescore rq;    // inputs, for rescoring overflowed rows
 };

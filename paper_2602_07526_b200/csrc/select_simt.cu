@@ -73,8 +73,7 @@ __global__ void __launch_bounds__(256) score_kernel(const T* __restrict__ Q, con
 // composite (score desc, index asc) keys held in registers.
 template <int NPL>
 __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict__ S, int64_t rows,
-                                                        int n_sub, int k, float* __restrict__ cv,
-                                                        int32_t* __restrict__ cc,
+                                                        int n_sub, int k, uint2* __restrict__ vc,
                                                         int32_t* __restrict__ cn) {
   pdl_enter();
   const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
@@ -96,8 +95,7 @@ __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict_
     for (int j = 0; j < NPL; ++j)
       if (c[j] == best) c[j] = 0ull;
     if (lane == 0) {
-      cv[row * kCandCap + t] = sel_key_score(best);
-      cc[row * kCandCap + t] = (int32_t)sel_key_index(best);
+      vc[row * kCandCap + t] = make_uint2(__float_as_uint(sel_key_score(best)), sel_key_index(best));
     }
   }
   if (lane == 0) cn[row] = k;
@@ -107,7 +105,7 @@ template <int NPL>
 cudaError_t launch_topk(const float* S, int64_t rows, int n_sub, int k, const Cands& cd,
                         cudaStream_t st) {
   const int64_t blocks = (rows + 7) / 8;
-  launch_pdl(topk_rows_kernel<NPL>, (unsigned)blocks, 256, 0, st, S, rows, n_sub, k, cd.v, cd.c, cd.n);
+  launch_pdl(topk_rows_kernel<NPL>, (unsigned)blocks, 256, 0, st, S, rows, n_sub, k, cd.vc, cd.n);
   return cudaGetLastError();
 }
 

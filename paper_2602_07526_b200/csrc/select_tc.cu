@@ -86,12 +86,28 @@ __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
 }
 
+// MSN_SELECT_TS builds (profiling only): globaltimer stamps per CTA at the
+// epilogue's phase boundaries (warp 4, lane 0), summarised by tools/select_ts.py.
+#ifdef MSN_SELECT_TS
+__device__ unsigned long long g_sel_ts[65536 * 8];
+#define SEL_TS(i)                                                                   \
+  do {                                                                              \
+    if (threadIdx.x == 32 * kEpiWarp0) {                                            \
+      unsigned long long t_;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+      const int c_ = blockIdx.y * gridDim.x + blockIdx.x;                           \
+      if (c_ < 65536) g_sel_ts[c_ * 8 + (i)] = t_;                                  \
+    }                                                                               \
+  } while (0)
+#else
+#define SEL_TS(i) do {} while (0)
+#endif
+
 struct TcParams {
   int64_t B;
   int H, n_sub, d_h, k;
   int n_tile, n_chunks, k_blocks, passes;
-  float* cv;
-  int32_t* cc;
+  uint2* vc;
   int32_t* cn;
   Rescore rq;  // overflowed rows are rescored exactly from these
 };
@@ -156,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  SEL_TS(0);
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -316,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool resident = p.passes == 1;  // whole row in the two TMEM buffers
     if (resident) {
       wait_chunks(0, p.n_chunks);
+      SEL_TS(1);
       pass_a(0, p.n_sub);
     } else {
       for (int c = 0; c < p.n_chunks; ++c) {
@@ -325,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 
+    SEL_TS(2);
     // ---- tau = KT-th largest of the 2G group maxima of the row: each thread
     // sorts its G maxima, the two top-KT lists meet in the half-cleaner
     bitonic_sort_vals<G>(gm);
@@ -335,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < KT; ++i) tau = fminf(tau, fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]));
     epi_bar();  // exchange read everywhere before the candidate area is written
+    SEL_TS(3);
 
     // ---- pass B: append every column >= tau to the row's buffer
     // thread 0: slots 0, 1, ... ; thread 1: slots 63, 62, ...  (entry = slot*129 + row)
@@ -358,6 +378,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return;
       }
+#ifndef MSN_PASSB_CHAIN
+      // hit mask, then four independent store chains (columns g*8 .. g*8+7),
+      // each starting at its prefix of the mask: no serial dependency across
+      // the 32 columns
+      uint32_t m = 0;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) m |= (__uint_as_float(r[jj]) >= tau ? 1u : 0u) << jj;
+      uint32_t ca[4];
+      ca[0] = caddr;
+      ca[1] = ca[0] + (uint32_t)__popc(m & 0xffu) * step;
+      ca[2] = ca[1] + (uint32_t)__popc(m & 0xff00u) * step;
+      ca[3] = ca[2] + (uint32_t)__popc(m & 0xff0000u) * step;
+      caddr = ca[3] + (uint32_t)__popc(m >> 24) * step;
+      cnt += __popc(m);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int col = g * 8 + jj;
+          asm volatile(
+              "{\n.reg .pred p;\n.reg .b32 t;\n"
+              "and.b32 t, %1, %5;\n"
+              "setp.ne.b32 p, t, 0;\n"
+              "@p st.shared.v2.u32 [%0], {%2, %3};\n"
+              "@p add.u32 %0, %0, %4;\n}\n"
+              : "+r"(ca[g])
+              : "r"(m), "r"(r[col]), "r"(col0 + col), "r"(step), "r"(1u << col)
+              : "memory");
+        }
+#else
       const uint32_t a0 = caddr;
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj)
@@ -372,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // appended = |caddr - a0| / (129*8)
       const uint32_t moved = sh == 0 ? caddr - a0 : a0 - caddr;
       cnt += (int)(moved / (uint32_t)(kCStride * 8));
+#endif
     };
     auto pass_b = [&](int g0, int seg_cols, int col_base) {
       for (int j0 = 64 * sh; j0 < seg_cols; j0 += 128) {
@@ -399,40 +450,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     cnts[sh * 128 + row] = cnt;
+    SEL_TS(4);
     epi_bar();
+    SEL_TS(5);
 
-    // ---- write-out: warp ew writes rows 16 ew .. 16 ew + 15, lane = slot
+    // ---- write-out: warp ew writes rows 16 ew .. 16 ew + 15, lane = slot;
+    // the 16 rows' counts come in with one shared load per lane
+    const int r0 = ew * 16;
+    const int cn_l = cnts[(lane >> 4) * 128 + r0 + (lane & 15)];
+    bool any_ovf = false;
+#pragma unroll 4
     for (int rr = 0; rr < 16; ++rr) {
-      const int trow = ew * 16 + rr;
+      const int trow = r0 + rr;
       const int64_t b = m0 + trow;
-      if (b >= p.B) break;
-      const int n0 = cnts[trow], n1 = cnts[128 + trow];
-      const int n = n0 + n1;
+      const int n0 = __shfl_sync(0xffffffffu, cn_l, rr);
+      const int n = n0 + __shfl_sync(0xffffffffu, cn_l, 16 + rr);
+      if (b >= p.B) continue;
+      if (n > kCap) { any_ovf = true; continue; }
       const int64_t grow = b * p.H * 2 + hh;
-      if (n > kCap) {
-        // more than kCap columns passed tau (massive exact ties): exact
-        // rescoring of this row by the warp, its best min(64, n_sub) sub-keys
-        const int nn = p.rq.qk_dt == F32
-            ? exact_half_topk<float>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub,
-                                     p.cv + grow * kCandCap, p.cc + grow * kCandCap)
-            : exact_half_topk<__nv_bfloat16>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub,
-                                             p.cv + grow * kCandCap, p.cc + grow * kCandCap);
-        if (lane == 0) p.cn[grow] = nn;
-        continue;
-      }
       if (lane == 0) p.cn[grow] = n;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int i = hf * 32 + lane;
         if (i < n) {
           const int slot = i < n0 ? i : kCap - 1 - (i - n0);
-          const uint2 e = cand[slot * kCStride + trow];
-          p.cv[grow * kCandCap + i] = __uint_as_float(e.x);
-          p.cc[grow * kCandCap + i] = (int32_t)e.y;
+          p.vc[grow * kCandCap + i] = cand[slot * kCStride + trow];
         }
       }
     }
+    if (any_ovf) {
+      // more than kCap columns passed tau (massive exact ties): exact
+      // rescoring of those rows by the warp, their best min(64, n_sub) sub-keys
+      for (int rr = 0; rr < 16; ++rr) {
+        const int64_t b = m0 + r0 + rr;
+        const int n = __shfl_sync(0xffffffffu, cn_l, rr) + __shfl_sync(0xffffffffu, cn_l, 16 + rr);
+        if (b >= p.B || n <= kCap) continue;
+        const int64_t grow = b * p.H * 2 + hh;
+        const int nn = p.rq.qk_dt == F32
+            ? exact_half_topk<float>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub, p.vc + grow * kCandCap)
+            : exact_half_topk<__nv_bfloat16>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub,
+                                             p.vc + grow * kCandCap);
+        if (lane == 0) p.cn[grow] = nn;
+      }
+    }
   }
+  SEL_TS(6);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -499,6 +561,17 @@ cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& 
 
 }  // namespace
 
+// Profiling builds only: copies the per-CTA stamps (8 per CTA) to host.
+extern "C" int msn_select_ts_dump(unsigned long long* host, int n) {
+#ifdef MSN_SELECT_TS
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, g_sel_ts, sizeof(unsigned long long) * (size_t)n * 8) == cudaSuccess ? n : -1;
+#else
+  (void)host; (void)n;
+  return -1;
+#endif
+}
+
 size_t select_tc_workspace_bytes(const Shape& s) {
   return is_tf32(s) ? 2 * sizeof(float) * (size_t)s.H * 2 * s.n_sub * s.d_h : 0;
 }
@@ -562,7 +635,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
   if (!kmap(&mk, kb_hi) || !kmap(&mklo, kb_lo)) return cudaErrorInvalidValue;
   const int n_chunks = s.n_sub / nt;
   TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, n_chunks, s.d_h / bk, n_chunks <= 2 ? 1 : 2,
-             cd.v, cd.c, cd.n, cd.rq};
+             cd.vc, cd.n, cd.rq};
   cudaError_t e;
   if (tf) {
     if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);

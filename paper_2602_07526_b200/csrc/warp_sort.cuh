@@ -66,7 +66,7 @@ __device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, flo
 }
 template <typename T>
 __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int half, int H, int n_sub,
-                                            float* cv, int32_t* cc) {
+                                            uint2* vc) {
   const int lane = threadIdx.x % 32;
   float v[2];
   int32_t ix[2];
@@ -126,10 +126,7 @@ __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int 
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int e = r * 32 + lane;
-    if (e < n) {
-      cv[e] = v[r];
-      cc[e] = ix[r];
-    }
+    if (e < n) vc[e] = make_uint2(__float_as_uint(v[r]), (uint32_t)ix[r]);
   }
   __syncwarp();
   return n;

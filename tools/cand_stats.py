@@ -1,6 +1,6 @@
 """Per-half candidate-list statistics of the tcgen05 scorer (profiling aid):
 runs msn_pkm_select on a workload and reads cand_n back from the forward
-workspace (layout in api.cu: cand_v | cand_c | cand_n, 256-B aligned).
+workspace (layout in api.cu: cand (score, index) | cand_n, 256-B aligned).
 
     python tools/cand_stats.py c4_large_sharded_bf16 [B]
 """
@@ -28,7 +28,7 @@ lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B, cfg.qk_d
 lk.select(Q, K)
 torch.cuda.synchronize()
 rows = B * cfg.heads * 2
-off = a256(4 * rows * 64) * 2
+off = a256(8 * rows * 64)
 n = lk._ws[off: off + 4 * rows].view(torch.int32).cpu()
 print(name, "rows", rows, "mean", n.float().mean().item(), "max", n.max().item(),
       "overflow(>64)", int((n > 64).sum()), "p99", n.float().quantile(0.99).item())
