@@ -26,8 +26,16 @@ namespace msn {
 namespace {
 using namespace tc;
 
-constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 TMEM alloc + epilogue
-constexpr int kStages = 4;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 TMEM alloc + epilogue (tile (w-2)/4)
+constexpr int kCtasPerSm = 1;
+// MT 128-row tiles per CTA share every B stage (M = 128 MT): stages of
+// (16 MT + 32) KB at d_h = 256, up to ~192 KB of ring
+__host__ __device__ constexpr int stages_for(int MT) { return MT == 1 ? 4 : 3; }
+__host__ __device__ inline uint32_t tmem_cols(int n) {  // power of 2 >= 32
+  uint32_t c = 32;
+  while (c < (uint32_t)n) c <<= 1;
+  return c;
+}
 constexpr int kBM = 128;  // sub-key rows per tile
 constexpr int kBK = 64;   // queries per k-block
 constexpr int kAtom = 64 * 64 * 2;  // one TMA box: 64 elements x 64 queries, bf16 = 8 KB
@@ -52,23 +60,26 @@ constexpr uint32_t idesc_bf16_mn(int M, int N) {
   return idesc_bf16(M, N) | (1u << 15) | (1u << 16);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int MT>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     dk_gemm_kernel(const __grid_constant__ CUtensorMap tmap_ds,
                    const __grid_constant__ CUtensorMap tmap_q, const DkParams p) {
   pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   const int nb = p.d_h / 64;                          // B atoms per stage
-  uint8_t* sA = smem_raw + pad;                       // kStages x 2 atoms (16 KB)
-  uint8_t* sB = sA + kStages * 2 * kAtom;             // kStages x nb atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * nb * kAtom);
+  constexpr int kStg = stages_for(MT);
+  uint8_t* sA = smem_raw + pad;                       // kStg x MT x 2 atoms (16 KB each tile)
+  uint8_t* sB = sA + kStg * MT * 2 * kAtom;           // kStg x nb atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStg * nb * kAtom);
   uint64_t* full = bars;
-  uint64_t* empty = full + kStages;
-  uint64_t* tdone = empty + kStages;
+  uint64_t* empty = full + kStg;
+  uint64_t* tdone = empty + kStg;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
+  const uint32_t tcols = tmem_cols(MT * p.d_h);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int i0 = blockIdx.x * kBM;
+  const int i0 = blockIdx.x * kBM * MT;
   const int hh = blockIdx.y;
   const int64_t q0 = (int64_t)blockIdx.z * p.q_per_split;
   int64_t q1 = q0 + p.q_per_split;
@@ -78,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap_ds);
     prefetch_tmap(&tmap_q);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kStg; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -87,8 +98,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -98,15 +109,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(2 + nb) * kAtom;
+      const uint32_t bytes = (uint32_t)(2 * MT + nb) * kAtom;
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
+        const int s = kb % kStg;
+        mbar_wait(&empty[s], ((kb / kStg) & 1) ^ 1);
         mbar_expect_tx(&full[s], bytes);
         const int b0 = (int)(q0 + (int64_t)kb * kBK);
         // queries >= B (ragged last block) are zero-filled by TMA
-        tma_load_3d(sA + s * 2 * kAtom, &tmap_ds, &full[s], i0, hh, b0);
-        tma_load_3d(sA + s * 2 * kAtom + kAtom, &tmap_ds, &full[s], i0 + 64, hh, b0);
+#pragma unroll
+        for (int t = 0; t < 2 * MT; ++t)
+          tma_load_3d(sA + (s * MT * 2 + t) * kAtom, &tmap_ds, &full[s], i0 + 64 * t, hh, b0);
         for (int j = 0; j < nb; ++j)
           tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_q, &full[s], 64 * j, hh, b0);
       }
@@ -115,26 +127,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16_mn(kBM, p.d_h);
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+        const int s = kb % kStg;
+        mbar_wait(&full[s], (kb / kStg) & 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + s * 2 * kAtom);
         const uint32_t b0 = smem_u32(sB + s * nb * kAtom);
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk)  // 16 queries = two 8-row groups = 2 KB
-          tc_mma(tmem, sw128_mn_desc(a0 + kk * 2048), sw128_mn_desc(b0 + kk * 2048), idesc,
-                 (kb | kk) != 0);
+#pragma unroll
+          for (int t = 0; t < MT; ++t)          // the MT sub-key tiles share the Q block
+            tc_mma(tmem + t * p.d_h, sw128_mn_desc(smem_u32(sA + (s * MT + t) * 2 * kAtom) + kk * 2048),
+                   sw128_mn_desc(b0 + kk * 2048), idesc, (kb | kk) != 0);
         tc_commit(&empty[s]);
       }
       tc_commit(tdone);
     }
-  } else {
-    // ----- epilogue (warps 2-5 -> TMEM lane quarters warp % 4): row i0 + row
+  } else if ((warp - 2) / 4 < MT) {
+    // ----- epilogue (warps 2..: TMEM lane quarter warp % 4, tile (warp - 2) / 4): row i0 + 128 t + row
     const int q = warp & 3;
+    const int t = (warp - 2) / 4;
     const int row = q * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + t * p.d_h;
     float* dst = p.out + ((int64_t)blockIdx.z * (gridDim.y) + hh) * (int64_t)p.n_sub * p.d_h +
-                 (int64_t)(i0 + row) * p.d_h;
+                 (int64_t)(i0 + t * kBM + row) * p.d_h;
     if (nkb > 0) {
       mbar_wait(tdone, 0);
       tc_fence_after();
@@ -164,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
   }
 }
 
@@ -180,7 +194,8 @@ struct DqParams {
   float* dQ;  // [B, H*2, d_h]
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int MT>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     dq_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_k, const DqParams p) {
   pdl_enter();
@@ -188,23 +203,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   const int nb = p.d_h / 64;                      // B atoms per stage
   constexpr int kABytes = 128 * 128;              // 128 queries x 64 sub-keys bf16
-  uint8_t* sA = smem_raw + pad;                   // kStages x 16 KB
-  uint8_t* sB = sA + kStages * kABytes;           // kStages x nb atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * nb * kAtom);
+  constexpr int kStg = stages_for(MT);
+  uint8_t* sA = smem_raw + pad;                   // kStg x MT x 16 KB
+  uint8_t* sB = sA + kStg * MT * kABytes;         // kStg x nb atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStg * nb * kAtom);
   uint64_t* full = bars;
-  uint64_t* empty = full + kStages;
-  uint64_t* tdone = empty + kStages;
+  uint64_t* empty = full + kStg;
+  uint64_t* tdone = empty + kStg;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
+  const uint32_t tcols = tmem_cols(MT * p.d_h);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * 128;
+  const int m0 = blockIdx.x * 128 * MT;
   const int hh = blockIdx.y;
   const int nkb = p.n_sub / 64;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_k);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kStg; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -213,8 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -224,13 +241,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)kABytes + (uint32_t)nb * kAtom;
+      const uint32_t bytes = (uint32_t)(MT * kABytes) + (uint32_t)nb * kAtom;
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
+        const int s = kb % kStg;
+        mbar_wait(&empty[s], ((kb / kStg) & 1) ^ 1);
         mbar_expect_tx(&full[s], bytes);
         // queries >= B (ragged last tile) are zero-filled by TMA
-        tma_load_3d(sA + s * kABytes, &tmap_a, &full[s], kb * 64, hh, m0);
+#pragma unroll
+        for (int t = 0; t < MT; ++t)
+          tma_load_3d(sA + (s * MT + t) * kABytes, &tmap_a, &full[s], kb * 64, hh, m0 + 128 * t);
         for (int j = 0; j < nb; ++j)
           tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_k, &full[s], 64 * j, kb * 64, hh);
       }
@@ -239,24 +258,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(128, p.d_h) | (1u << 16);  // B MN-major
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+        const int s = kb % kStg;
+        mbar_wait(&full[s], (kb / kStg) & 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + s * kABytes);
         const uint32_t b0 = smem_u32(sB + s * nb * kAtom);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // 16 sub-keys: +32 B in the A row, +2 KB in B
-          tc_mma(tmem, sw128_desc(a0 + kk * 32), sw128_mn_desc(b0 + kk * 2048), idesc,
-                 (kb | kk) != 0);
+#pragma unroll
+          for (int t = 0; t < MT; ++t)  // the MT query tiles share the K block
+            tc_mma(tmem + t * p.d_h, sw128_desc(smem_u32(sA + (s * MT + t) * kABytes) + kk * 32),
+                   sw128_mn_desc(b0 + kk * 2048), idesc, (kb | kk) != 0);
         tc_commit(&empty[s]);
       }
       tc_commit(tdone);
     }
-  } else {
+  } else if ((warp - 2) / 4 < MT) {
     const int q = warp & 3;
+    const int t = (warp - 2) / 4;
     const int row = q * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    const int64_t b = (int64_t)m0 + row;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + t * p.d_h;
+    const int64_t b = (int64_t)m0 + t * 128 + row;
     float* dst = p.dQ + (b * (2 * p.H) + hh) * (int64_t)p.d_h;
     mbar_wait(tdone, 0);
     tc_fence_after();
@@ -276,12 +297,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
   }
 }
 
-size_t dq_smem_bytes(const Shape& s) {
-  return 1024 + (size_t)kStages * (128 * 128 + (s.d_h / 64) * kAtom) + 8 * (2 * kStages + 1) + 16;
+// Tiles per CTA.  Measured on the B200 (bench.py, MSN_DQ_MT / MSN_DK_MT
+// override for A/B runs): dQ gains nothing from MT = 2 (C2 +1.7 us, C4 0);
+// dK gains on long codebooks (C4, n_sub 2048: -21 us) and loses on short ones
+// (C2, n_sub 512: +7.5 us, too few k-blocks per split).
+int env_int(const char* n, int d) { const char* v = getenv(n); return v ? atoi(v) : d; }
+int dq_mt(const Shape& s) {
+  static const int f = env_int("MSN_DQ_MT", 1);
+  return (f >= 2 && s.B > 128) ? 2 : 1;
+}
+int dk_mt(const Shape& s) {
+  static const int f = env_int("MSN_DK_MT", 0);
+  const bool want = f == 0 ? s.n_sub >= 1024 : f >= 2;
+  return (want && s.n_sub % (2 * kBM) == 0) ? 2 : 1;
+}
+
+size_t dq_smem_bytes(const Shape& s, int MT) {
+  const int st = stages_for(MT);
+  return 1024 + (size_t)st * (MT * 128 * 128 + (s.d_h / 64) * kAtom) + 8 * (2 * st + 1) + 16;
 }
 
 // dK += sum_s part[s] (fixed split order)
@@ -301,15 +338,16 @@ __global__ void dk_reduce_kernel(const float4* __restrict__ part, float4* __rest
 }
 
 int splits_for(const Shape& s) {
-  const int tiles = (s.n_sub / kBM) * s.H * 2;
+  const int tiles = (s.n_sub / (kBM * dk_mt(s))) * s.H * 2;
   const int64_t kblocks = (s.B + kBK - 1) / kBK;
   int S = 1;
-  while (tiles * S * 2 <= 148 && kblocks / (S * 2) >= 4) S *= 2;
+  while (tiles * S * 2 <= 148 * kCtasPerSm && kblocks / (S * 2) >= 4) S *= 2;
   return S;
 }
 
-size_t dk_smem_bytes(const Shape& s) {
-  return 1024 + (size_t)kStages * (2 + s.d_h / 64) * kAtom + 8 * (2 * kStages + 1) + 16;
+size_t dk_smem_bytes(const Shape& s, int MT) {
+  const int st = stages_for(MT);
+  return 1024 + (size_t)st * (2 * MT + s.d_h / 64) * kAtom + 8 * (2 * st + 1) + 16;
 }
 
 size_t dense_ds_bytes(const Shape& s) {
@@ -322,8 +360,8 @@ bool dk_tc_supported(const Shape& s) {
   // dense work = 2 n_sub d_h per (query, half) vs ~2 k d_h for the sparse path:
   // worth it while n_sub is small (C2: 512); C4 (2048) keeps the sort path.
   return s.qk_dt == BF16 && s.n_sub <= 2048 && s.n_sub % kBM == 0 && s.d_h % 64 == 0 &&
-         s.d_h >= 64 && s.d_h <= 256 && s.k <= 64 && dk_smem_bytes(s) <= 227 * 1024 &&
-         dq_smem_bytes(s) <= 227 * 1024 && get_encode() != nullptr;
+         s.d_h >= 64 && s.d_h <= 256 && s.k <= 64 && dk_smem_bytes(s, dk_mt(s)) <= 227 * 1024 &&
+         dq_smem_bytes(s, dq_mt(s)) <= 227 * 1024 && get_encode() != nullptr;
 }
 
 size_t dk_tc_workspace_bytes(const Shape& s) {
@@ -386,16 +424,17 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-    static bool qattr = false;
-    if (!qattr) {
-      cudaError_t e0 = cudaFuncSetAttribute(dq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            227 * 1024);
-      if (e0 != cudaSuccess) return e0;
-      qattr = true;
-    }
     DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ};
-    dim3 qgrid((unsigned)((s.B + 127) / 128), HH);
-    launch_pdl(dq_gemm_kernel, qgrid, kThreads, dq_smem_bytes(s), st, ma, mk, qp);
+    const int mtq = dq_mt(s);
+    auto dqk = mtq == 2 ? dq_gemm_kernel<2> : dq_gemm_kernel<1>;
+    static bool qattr[2] = {false, false};
+    if (!qattr[mtq - 1]) {
+      cudaError_t e0 = cudaFuncSetAttribute(dqk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e0 != cudaSuccess) return e0;
+      qattr[mtq - 1] = true;
+    }
+    dim3 qgrid((unsigned)((s.B + 128 * mtq - 1) / (128 * mtq)), HH);
+    launch_pdl(dqk, qgrid, kThreads, dq_smem_bytes(s, mtq), st, ma, mk, qp);
     cudaError_t e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return e1;
     ++*launches;
@@ -404,15 +443,17 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
   const int64_t kblocks = (s.B + kBK - 1) / kBK;
   const int64_t qps = ((kblocks + S - 1) / S) * kBK;
   DkParams p{s.B, s.H, s.n_sub, s.d_h, qps, S > 1 ? part : dK, S > 1 ? 0 : 1};
-  static bool attr = false;
+  const int mtk = dk_mt(s);
+  auto dkk = mtk == 2 ? dk_gemm_kernel<2> : dk_gemm_kernel<1>;
+  static bool attr[2] = {false, false};
   cudaError_t e;
-  if (!attr) {
-    e = cudaFuncSetAttribute(dk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (!attr[mtk - 1]) {
+    e = cudaFuncSetAttribute(dkk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[mtk - 1] = true;
   }
-  dim3 grid(s.n_sub / kBM, HH, S);
-  launch_pdl(dk_gemm_kernel, grid, kThreads, dk_smem_bytes(s), st, mds, mq, p);
+  dim3 grid(s.n_sub / (kBM * mtk), HH, S);
+  launch_pdl(dkk, grid, kThreads, dk_smem_bytes(s, mtk), st, mds, mq, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
