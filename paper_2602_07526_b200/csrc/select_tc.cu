@@ -38,6 +38,11 @@
 // Rows that fit TMEM (n_sub <= 512, two buffers) are scored once; longer rows
 // are scored twice (the MMA pass is cheap next to the epilogue): the first
 // pass feeds pass A, the second pass B, so tau is the whole row's bound.
+// fp32 inputs score the first pass with ONE TF32 product (hi.hi) instead of
+// three: |S_1x - S_3x| <= 2^-9 sum_e |q_e||k_e| + accumulation rounding
+// (|x - hi(x)| < 2^-10 |x|), so with d = 2^-8 ||q|| max_i ||k_i|| every
+// first-pass group maximum exceeds a column whose 3xTF32 score is >= it - d,
+// and tau - d (rounded down) bounds the 3xTF32 KT-th score from below.
 #include <cuda.h>
 #include <algorithm>
 #include <cstdio>
@@ -109,7 +114,8 @@ struct TcParams {
   int n_tile, n_chunks, k_blocks, passes;
   uint2* vc;
   int32_t* cn;
-  Rescore rq;  // overflowed rows are rescored exactly from these
+  Rescore rq;
+  const float* knorm;  // TF32, two sweeps: ||k_i|| (rounded up) per sub-key row [H*2*n_sub]  // overflowed rows are rescored exactly from these
 };
 
 template <int KT, bool TF32, bool WIDE>
@@ -183,12 +189,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       for (int g = 0; g < total_chunks; ++g) {
         const int c = g % p.n_chunks;
+        const bool lo = TF32 && !(WIDE && g < p.n_chunks);  // 1xTF32 first sweep: K_hi only
         for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], stage_bytes);
+          mbar_expect_tx(&full[s], lo ? stage_bytes : p.n_tile * kRowBytes);
           tma_load_2d(sB + s * stage_bytes, &tmap_k, &full[s], kb * BK, hh * p.n_sub + c * p.n_tile);
-          if (TF32)
+          if (lo)
             tma_load_2d(sB + s * stage_bytes + p.n_tile * kRowBytes, &tmap_klo, &full[s], kb * BK,
                         hh * p.n_sub + c * p.n_tile);
         }
@@ -214,14 +221,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a0 = smem_u32(sA + kb * 16384);
           const uint32_t b0 = smem_u32(sB + s * stage_bytes);
           if constexpr (TF32) {
-            // 3xTF32: A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (the lo.lo term is below fp32 rounding)
+            // 3xTF32: A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (the lo.lo term is below fp32 rounding);
+            // the first sweep of a two-sweep row: A_hi.B_hi only (pass A, margin d)
             const uint32_t b1 = b0 + p.n_tile * kRowBytes;
+            const bool one = WIDE && g < p.n_chunks;
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint32_t acc = (kb | kk) != 0;
               tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, acc);
-              tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b1 + kk * 32), idesc, 1);
-              tc_mma_tf32_ts(d, tmem + alo_col + kb * BK + kk * 8, sw128_desc(b0 + kk * 32), idesc, 1);
+              if (!one) {
+                tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b1 + kk * 32), idesc, 1);
+                tc_mma_tf32_ts(d, tmem + alo_col + kb * BK + kk * 8, sw128_desc(b0 + kk * 32), idesc, 1);
+              }
             }
           } else {
 #pragma unroll
@@ -240,12 +251,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sh = ew >> 2;            // column share of this thread: 0 or 1
     const int row = q * 32 + lane;     // query row within the tile
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    // TF32 two-sweep rows: margin d = 2^-8 ||q_row|| max_i ||k_i|| on the
+    // 1xTF32 first sweep (see the header); ||q|| from the split below, shared
+    // through the end of the (not yet used) candidate area
+    float* qn = reinterpret_cast<float*>(cand + kCap * kCStride) - 128;
+    float kmax = 0.f;
+    if constexpr (TF32 && WIDE) {
+      for (int i = threadIdx.x - 32 * kEpiWarp0; i < p.n_sub; i += 32 * kEpiWarps)
+        kmax = fmaxf(kmax, p.knorm[(int64_t)hh * p.n_sub + i]);
+      kmax = warp_max(kmax);
+      if (lane == 0) cnts[ew] = __float_as_int(kmax);
+      epi_bar();
+      kmax = 0.f;
+#pragma unroll
+      for (int i = 0; i < kEpiWarps; ++i) kmax = fmaxf(kmax, __int_as_float(cnts[i]));
+    }
     if constexpr (TF32) {
       if (sh == 0) {
         // split this row of the resident query tile: hi (TF32-exact) back into
         // shared memory in place, lo = x - hi into TMEM columns [alo_col, +d_h)
         mbar_wait(a_full, 0);
         const int sw = row & 7;
+        float qq = 0.f;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           float* arow = reinterpret_cast<float*>(sA + kb * 16384 + row * kRowBytes);
           uint32_t lo[32];
@@ -253,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ch = 0; ch < 8; ++ch) {
             float4* pc = reinterpret_cast<float4*>(arow) + (ch ^ sw);  // logical chunk ch
             float4 x = *pc;
+            qq = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, qq))));
             float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
             *pc = h;
             lo[ch * 4 + 0] = __float_as_uint(x.x - h.x);
@@ -262,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_st32(lane_base + alo_col + kb * BK, lo);
         }
+        if (WIDE) qn[row] = qq;
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
@@ -353,6 +382,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     float tau = INFINITY;
 #pragma unroll
     for (int i = 0; i < KT; ++i) tau = fminf(tau, fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]));
+    if constexpr (TF32 && WIDE) {
+      // ||q||^2 summed in fp32 (relative error < 2^-17 for d_h <= 128): x 1.001
+      // makes sqrt an upper bound; the margin itself has 2x slack (2^-8 vs 2^-9)
+      const float d = 0x1p-8f * __fsqrt_ru(qn[row] * 1.001f) * kmax;
+      tau = __fsub_rd(tau, d);
+    }
     epi_bar();  // exchange read everywhere before the candidate area is written
     SEL_TS(3);
 
@@ -523,16 +558,27 @@ size_t smem_bytes(const Shape& s) {
          (size_t)kCap * kCStride * 8 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
 }
 
-// K -> (K_hi, K_lo) for the 3xTF32 B operand.
+// K -> (K_hi, K_lo) for the 3xTF32 B operand, and ||k_i|| per sub-key row
+// (fp32 sum of squares, x 1.001 before a rounded-up sqrt: an upper bound),
+// one warp per row.
 __global__ void split_tf32_kernel(const float* __restrict__ k, float* __restrict__ hi,
-                                  float* __restrict__ lo, int64_t n) {
+                                  float* __restrict__ lo, float* __restrict__ knorm, int64_t rows,
+                                  int d) {
   pdl_enter();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float x = k[i];
-  const float h = tf32_hi(x);
-  hi[i] = h;
-  lo[i] = x - h;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  float ss = 0.f;
+  for (int e = lane; e < d; e += 32) {
+    const int64_t i = r * d + e;
+    const float x = k[i];
+    const float h = tf32_hi(x);
+    hi[i] = h;
+    lo[i] = x - h;
+    ss = fmaf(x, x, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) knorm[r] = __fsqrt_ru(ss * 1.001f);
 }
 
 template <int KT, bool TF32, bool WIDE>
@@ -573,7 +619,8 @@ extern "C" int msn_select_ts_dump(unsigned long long* host, int n) {
 }
 
 size_t select_tc_workspace_bytes(const Shape& s) {
-  return is_tf32(s) ? 2 * sizeof(float) * (size_t)s.H * 2 * s.n_sub * s.d_h : 0;
+  return is_tf32(s) ? 2 * sizeof(float) * (size_t)s.H * 2 * s.n_sub * s.d_h +
+                          sizeof(float) * (size_t)s.H * 2 * s.n_sub : 0;
 }
 
 bool select_tc_supported(const Shape& s) {
@@ -612,10 +659,14 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
   const int64_t kel = (int64_t)s.H * 2 * s.n_sub * s.d_h;
   const void* kb_hi = K;
   const void* kb_lo = K;
+  float* knorm = nullptr;
   if (tf) {
     float* hi = (float*)ws;
     float* lo = hi + kel;
-    launch_pdl(split_tf32_kernel, (unsigned)((kel + 255) / 256), 256, 0, st, (const float*)K, hi, lo, kel);
+    knorm = lo + kel;
+    const int64_t krows = (int64_t)s.H * 2 * s.n_sub;
+    launch_pdl(split_tf32_kernel, (unsigned)((krows + 7) / 8), 256, 0, st, (const float*)K, hi, lo, knorm,
+               krows, s.d_h);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ++*launches;
@@ -635,7 +686,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
   if (!kmap(&mk, kb_hi) || !kmap(&mklo, kb_lo)) return cudaErrorInvalidValue;
   const int n_chunks = s.n_sub / nt;
   TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, n_chunks, s.d_h / bk, n_chunks <= 2 ? 1 : 2,
-             cd.vc, cd.n, cd.rq};
+             cd.vc, cd.n, cd.rq, knorm};
   cudaError_t e;
   if (tf) {
     if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);
