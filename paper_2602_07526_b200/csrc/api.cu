@@ -274,7 +274,8 @@ static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* q
   cudaStream_t cs = (cudaStream_t)stream;
   // fused Cartesian + gather when there are enough queries to fill the GPU
   // with warps (one warp per query); small batches keep one warp per lookup
-  if (h->cfg.heads * h->cfg.k <= 256 && B >= 8192) {
+  static const int64_t fuse_min_b = getenv("MSN_FUSE_MIN_B") ? atoll(getenv("MSN_FUSE_MIN_B")) : 8192;
+  if (h->cfg.heads * h->cfg.k <= 256 && B >= fuse_min_b) {
     return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
                      &h->last_launches, values, out, gate);
   }
