@@ -39,6 +39,9 @@ template <int KMAX, int MAXC>
 struct CartSmem {
   float sv2[KMAX];
   int32_t si2[KMAX];
+  float sva[KMAX];     // the row half's sorted scores / indices / candidate offsets
+  int32_t sia[KMAX];
+  int32_t soff[KMAX];
   uint64_t cand[MAXC];
   uint64_t res[KMAX];
 };
@@ -78,6 +81,10 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
         const int a = lane + 32 * u;
         va[u] = a < k ? v[u] : -INFINITY;
         ia[u] = a < k ? ix[u] : 0;
+        if (a < k) {
+          sm.sva[a] = v[u];
+          sm.sia[a] = ix[u];
+        }
       }
     } else {
 #pragma unroll
@@ -102,35 +109,59 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     }
   }
   tau = warp_max(tau);
-  // prefix lengths p_a
+  // prefix lengths p_a = #{b < k/(a+1) : c(a, b) >= tau}: c(a, b) is
+  // non-increasing in b (sorted halves, monotone rounding), so a binary search
   int p[APL];
   int mine = 0;
 #pragma unroll
   for (int u = 0; u < APL; ++u) {
     const int a = lane + 32 * u;
-    p[u] = 0;
+    int lo = 0;
     if (a < k) {
-      const int lim = k / (a + 1);
-      while (p[u] < lim && va[u] + sm.sv2[p[u]] >= tau) ++p[u];
+      int len = k / (a + 1);
+      while (len > 0) {
+        const int h = len >> 1;
+        if (va[u] + sm.sv2[lo + h] >= tau) {
+          lo += h + 1;
+          len -= h + 1;
+        } else {
+          len = h;
+        }
+      }
     }
-    mine += p[u];
+    p[u] = lo;
+    mine += lo;
   }
-  // exclusive prefix over lanes
-  int incl = mine;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int o = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += o;
-  }
-  const int m = __shfl_sync(0xffffffffu, incl, 31);
-  int off = incl - mine;
+  // exclusive prefix in row order (rows 0..31 on the lanes, then 32..63)
+  int m = 0;
 #pragma unroll
   for (int u = 0; u < APL; ++u) {
-    for (int q = 0; q < p[u]; ++q) {
-      const float c = va[u] + sm.sv2[q];
-      const uint32_t flat = (uint32_t)ia[u] * (uint32_t)n_sub + (uint32_t)sm.si2[q];
-      sm.cand[off++] = sel_key(c, flat);
+    int incl = p[u];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
     }
+    const int a = lane + 32 * u;
+    if (a < k) sm.soff[a] = m + incl - p[u];
+    m += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  (void)mine;
+  __syncwarp();
+  // candidate x (lane-parallel): row a = the last row with soff[a] <= x (p_a is
+  // non-increasing in a, so every row before the empty tail is non-empty),
+  // column b = x - soff[a]
+  for (int x = lane; x < m; x += 32) {
+    int a = 0, len = k;
+    while (len > 1) {
+      const int h = len >> 1;
+      if (sm.soff[a + h] <= x) a += h;
+      len -= h;
+    }
+    const int b = x - sm.soff[a];
+    const float c = sm.sva[a] + sm.sv2[b];
+    const uint32_t flat = (uint32_t)sm.sia[a] * (uint32_t)n_sub + (uint32_t)sm.si2[b];
+    sm.cand[x] = sel_key(c, flat);
   }
   __syncwarp();
   // exact rank by composite key; keys are distinct (flat ids are distinct)
