@@ -66,15 +66,22 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     float v[2];
     int32_t ix[2];
     const int n = cand_n[row];
+    {
+      // sort by the composite key (score desc, index asc) as one u64
+      uint64_t key[2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int e = r * 32 + lane;
-      const bool ok = e < n;
-      const uint2 c = ok ? cand[row * kCandCap + e] : make_uint2(__float_as_uint(-INFINITY), 0x7fffffffu);
-      v[r] = __uint_as_float(c.x);
-      ix[r] = (int32_t)c.y;
+      for (int r = 0; r < 2; ++r) {
+        const int e = r * 32 + lane;
+        const uint2 c = e < n ? cand[row * kCandCap + e] : make_uint2(0u, 0u);
+        key[r] = e < n ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
+      }
+      warp_sort64_u64(key);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        v[r] = key[r] ? sel_key_score(key[r]) : -INFINITY;
+        ix[r] = key[r] ? (int32_t)sel_key_index(key[r]) : 0x7fffffff;
+      }
     }
-    warp_sort64(v, ix);
     if (half == 0) {
 #pragma unroll
       for (int u = 0; u < APL; ++u) {

@@ -42,6 +42,33 @@ __device__ __forceinline__ void warp_sort64(float (&v)[2], int32_t (&ix)[2]) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) bitonic_step64(v, ix, size, stride);
 }
 
+// The same network over composite u64 keys (larger = better, sel_key):
+// one 64-bit comparison per exchange.
+__device__ __forceinline__ void warp_sort64_u64(uint64_t (&x)[2]) {
+  const int lane = threadIdx.x % 32;
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride == 32) {
+        const uint64_t a = x[0] > x[1] ? x[0] : x[1], b = x[0] > x[1] ? x[1] : x[0];
+        x[0] = a;
+        x[1] = b;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int e = r * 32 + lane;
+          const uint64_t o = shfl_xor_u64(x[r], stride);
+          const bool lower = (e & stride) == 0;
+          const bool desc = (e & size) == 0;
+          // keep the better of the pair when (lower == desc), else the worse
+          x[r] = (lower == desc) == (o > x[r]) ? o : x[r];
+        }
+      }
+    }
+  }
+}
+
 // Exact per-half top list of lookup l when the scorer's candidate list
 // overflowed (cand_n > kCandCap): rescore all n_sub sub-keys of this
 // (head, half) and keep the best 64 under (score desc, index asc).  32
