@@ -832,10 +832,11 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
 // get the sentinel key.
 // DENSE: instead of records, the dS of the lookup-half is written as one
 // dense bf16 row dSd[b, h*2 + half, 0:n_sub] (zeros elsewhere) for the
-// tensor-core dQ and dK (dk_tc.cu), and dQ is not computed here;
-// n_sub <= kDenseMax.
+// tensor-core dK (dk_tc.cu) and, unless DQ, the tensor-core dQ;
+// n_sub <= kDenseMax.  DQ: dQ by the warp here (the m distinct K rows of the
+// lookup-half from L2) -- cheaper than the dense GEMM when n_sub is large.
 constexpr int kDenseMax = 2048;
-template <typename QT, int KPL, int EPL, bool DENSE>
+template <typename QT, int KPL, int EPL, bool DENSE, bool DQ>
 __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     const int32_t* __restrict__ idx,
                                                     const float* __restrict__ w,
@@ -936,7 +937,7 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       uint4* g4 = reinterpret_cast<uint4*>(dSd + (l * 2 + half) * (int64_t)n_sub);
       for (int c = lane; c < n16; c += 32) g4[c] = row4[c];
     }
-    if constexpr (DENSE) {
+    if constexpr (DENSE && !DQ) {
       __syncwarp();
       continue;  // dQ = dSd . K runs on the tensor cores (dk_tc.cu)
     }
@@ -1139,18 +1140,23 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   const unsigned blocks = (unsigned)((L + 7) / 8);
   const int E = epl_of(s.d_h);
   const bool dense = dk_tc_supported(s);
+  const bool dq_tc = dense && dq_tc_wanted(s);
   const GrpScratch g = grp_scratch(ws);
   if (!dense) {
     cudaError_t e0 = grp_begin(g, nrows, st);
     if (e0 != cudaSuccess) return e0;
   }
 #define DSDQ(QT, KPL, E_)                                                                      \
-  if (dense)                                                                                   \
-    launch_pdl(ds_dq_kernel<QT, KPL, E_, true>, blocks, 256, 0, st,                                    \
+  if (dense && dq_tc)                                                                          \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, true, false>, blocks, 256, 0, st,                             \
+        (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride);                 \
+  else if (dense)                                                                              \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, true, true>, blocks, 256, 0, st,                              \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride);                 \
   else                                                                                         \
-    launch_pdl(ds_dq_kernel<QT, KPL, E_, false>, blocks, 256, 0, st,                                   \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, false, true>, blocks, 256, 0, st,                             \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride)
 #define DSDQ_E(QT, KPL)                                                                        \
@@ -1167,7 +1173,7 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
-  if (dense) return launch_dk_tc(s, Q, K, dQ, dK, ws.dk_ws, st, launches);
+  if (dense) return launch_dk_tc(s, Q, K, dQ, dK, ws.dk_ws, st, launches, dq_tc);
   const int64_t n = 2 * L * s.k;
   if (s.qk_dt == F32)
     return grp_finish<MODE_DK, float, float>(g, n, nrows, ws.dsS, Q, nullptr, nullptr, dK, s.H,

@@ -371,8 +371,14 @@ size_t dk_tc_workspace_bytes(const Shape& s) {
   return dense_ds_bytes(s) + part;
 }
 
+bool dq_tc_wanted(const Shape& s) {
+  // MSN_DQ_TC=0/1 forces the choice (A/B measurements only)
+  static const int f = env_int("MSN_DQ_TC", -1);
+  return f >= 0 ? f != 0 : s.n_sub < 1024;
+}
+
 cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* dQ, float* dK,
-                         void* ws, cudaStream_t st, int* launches) {
+                         void* ws, cudaStream_t st, int* launches, bool with_dq) {
   if (!dk_tc_supported(s)) return cudaErrorNotSupported;
   const uint16_t* dSd = (const uint16_t*)ws;
   float* part = (float*)((char*)ws + dense_ds_bytes(s));
@@ -403,7 +409,7 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
       return cudaErrorInvalidValue;
   }
   // dQ = dSd . K per (head, half) on the tensor cores
-  {
+  if (with_dq) {
     CUtensorMap ma, mk;
     // dSd [B, HH, n_sub] as the K-major A operand: dims (n_sub, HH, B), box (64, 1, 128)
     cuuint64_t dims[3] = {(cuuint64_t)s.n_sub, (cuuint64_t)HH, (cuuint64_t)s.B};

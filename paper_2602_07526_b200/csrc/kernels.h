@@ -101,7 +101,10 @@ size_t dk_tc_workspace_bytes(const Shape& s);
 // that ds_dq_kernel writes (dense mode).
 // Also writes dQ = dSd . K (=) on the tensor cores.
 cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* K, float* dQ, float* dK,
-                         void* ws, cudaStream_t st, int* launches);
+                         void* ws, cudaStream_t st, int* launches, bool with_dq = true);
+// dQ on the tensor cores too (dense dS . K), or by ds_dq_kernel from the m
+// distinct K rows of each lookup-half: the dense GEMM's work grows with n_sub.
+bool dq_tc_wanted(const Shape& s);
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 
