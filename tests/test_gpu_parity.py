@@ -560,3 +560,21 @@ def test_fused_forward_matches_phases(name, B, groups):
     torch.cuda.synchronize()
     assert torch.equal(idx, i2) and torch.equal(w, w2)
     assert torch.equal(out, o2)
+
+
+def test_step_host_pipelined_matches_device():
+    """PKMLookup.step_host (host buffers, 4 slices with copies overlapping the
+    kernels): out and d_query are per-query results, bitwise equal to the
+    device-resident forward/backward; d_values / d_subkeys receive the slices'
+    sums one after another (equal up to fp32 reassociation)."""
+    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=4096 + 200)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, _ = lk.backward(dOut, Q, K, V, idx, w)
+    dK2 = torch.zeros_like(dK)
+    dV2 = torch.zeros_like(dV)
+    out_h, dq_h = lk.step_host(Q.cpu().pin_memory(), dOut.cpu().pin_memory(), K, V, dK2, dV2)
+    assert torch.equal(out_h, out.cpu()) and torch.equal(dq_h, dq.cpu())
+    torch.testing.assert_close(dV2, dV, rtol=1e-5, atol=1e-7)
+    torch.testing.assert_close(dK2, dK, rtol=1e-4, atol=1e-6)
