@@ -881,16 +881,37 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
     bool first[KPL];
 #pragma unroll
     for (int u = 0; u < KPL; ++u) { dS[u] = 0.f; first[u] = true; }
-    for (int v = 0; v < k; ++v) {
-      const bool lo = KPL == 1 || v < 32;
-      const int rv = __shfl_sync(0xffffffffu, lo ? r[0] : r[KPL - 1], v % 32);
-      const float dsv = __shfl_sync(0xffffffffu, lo ? ds[0] : ds[KPL - 1], v % 32);
+    if constexpr (KPL == 1) {
+      // the lanes holding the same sub-key index r (one group per distinct r)
+      // sum their ds in ascending lane (= t) order: the same additions as the
+      // all-pairs loop below, in max(group size) steps instead of k
+      const bool valid = lane < k;
+      unsigned grp = __match_any_sync(0xffffffffu, valid ? r[0] : -1 - lane);
+      first[0] = (grp & ((1u << lane) - 1u)) == 0u;
+      int steps = __popc(grp);
 #pragma unroll
-      for (int u = 0; u < KPL; ++u) {
-        const int t = lane + 32 * u;
-        if (rv == r[u]) {
-          dS[u] += dsv;
-          if (v < t) first[u] = false;
+      for (int o = 16; o > 0; o >>= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+      for (int j = 0; j < steps; ++j) {
+        const int src = grp ? __ffs(grp) - 1 : lane;
+        const float v = __shfl_sync(0xffffffffu, ds[0], src);
+        if (grp) {
+          dS[0] += v;
+          grp &= grp - 1u;
+        }
+      }
+      if (!valid) dS[0] = 0.f;
+    } else {
+      for (int v = 0; v < k; ++v) {
+        const bool lo = KPL == 1 || v < 32;
+        const int rv = __shfl_sync(0xffffffffu, lo ? r[0] : r[KPL - 1], v % 32);
+        const float dsv = __shfl_sync(0xffffffffu, lo ? ds[0] : ds[KPL - 1], v % 32);
+#pragma unroll
+        for (int u = 0; u < KPL; ++u) {
+          const int t = lane + 32 * u;
+          if (rv == r[u]) {
+            dS[u] += dsv;
+            if (v < t) first[u] = false;
+          }
         }
       }
     }
