@@ -542,7 +542,8 @@ def run_sharded(args, rank, world, local_rank):
     Q, K, V, dOut = wl.make_all(cfg, dev)  # every rank draws the same seeded tensors
     B_l = cfg.batch // world
     sp = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l,
-                    qk_dtype=cfg.qk_dtype, value_dtype=cfg.value_dtype, device=dev)
+                    qk_dtype=cfg.qk_dtype, value_dtype=cfg.value_dtype, device=dev,
+                    transport=args.transport)
     q_l = Q[rank * B_l:(rank + 1) * B_l].contiguous()
     d_l = dOut[rank * B_l:(rank + 1) * B_l].contiguous()
     Vs = sp.value_shard(V)
@@ -586,7 +587,11 @@ def run_sharded(args, rank, world, local_rank):
             "config": {"workload": cfg.name, "batch_total": cfg.batch, "batch_per_rank": B_l,
                        "heads": cfg.heads, "n_sub": cfg.n_sub, "n_slots": cfg.n_slots,
                        "rows_per_rank": sp.rows, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
-                       "parallelism": f"row-sharded table x{world} (all-gather idx/w, reduce-scatter partials)",
+                       "parallelism": (f"row-sharded table x{world} (all-gather idx/w, reduce-scatter partials)"
+                                       if args.transport == "nccl" else
+                                       f"row-sharded table x{world} (all-gather idx/w, gather fused with the "
+                                       "reduce-scatter: partials pushed to the home rank over peer memory)"),
+                       "transport": args.transport,
                        "l2": "flushed before every step (512 MiB write, outside the timed events)"},
             "clocks": clocks.summary()}
 
@@ -675,6 +680,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="C4 through the row-sharded path even at N=1")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="row-sharded forward: NCCL reduce-scatter, or the gather pushing partials to peers")
     ap.add_argument("--prologue", action="store_true",
                     help="include LayerNorm(q), K~ = Theta LayerNorm(k) and their backward (SURVEY 8(f) f2)")
     ap.add_argument("--update", choices=["none", "sgd", "adagrad"], default="none",

@@ -226,6 +226,30 @@ msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B,
                           const int32_t* idx, const float* weights, const void* values,
                           float* out);
 
+/* a5 over the local rows FUSED WITH THE REDUCE-SCATTER (peer-memory push,
+ * NVLink): B = world * local_batch queries in rank-major order (the
+ * all-gathered idx / weights); the partial row of query b -- the same sum
+ * msn_pkm_gather computes -- is stored into its home rank's receive buffer
+ *   peer_recv[p][((rank * local_batch + b % local_batch) * G + g) * d_value + e],
+ *   p = b / local_batch, G = head_groups,
+ * where peer_recv is a DEVICE array of world pointers to [world, local_batch,
+ * G, d_value] fp32 receive buffers mapped into this process (CUDA IPC /
+ * symmetric memory; plain local buffers when ranks are emulated on one GPU).
+ * Every receive slot is written by exactly one rank.  The caller orders the
+ * pushes of all ranks before msn_pkm_reduce_partials (a cross-rank barrier).
+ * MSN_ERR_UNSUPPORTED if heads * k > 512. */
+msn_status msn_pkm_gather_push(msn_pkm_t h, void* stream, int64_t B,
+                               const int32_t* idx, const float* weights, const void* values,
+                               float* const* peer_recv, int32_t world, int32_t rank,
+                               int64_t local_batch);
+
+/* out[b] = sum_{p = 0 .. world-1} recv[p][b]  in rank order (written, =):
+ * the home rank's half of the fused reduce-scatter.  recv [world,
+ * local_batch, G, d_value] fp32 (this rank's receive buffer), out
+ * [local_batch, G, d_value] fp32; deterministic, independent of arrival order. */
+msn_status msn_pkm_reduce_partials(msn_pkm_t h, void* stream, int64_t local_batch, int32_t world,
+                                   const float* recv, float* out);
+
 /* a6 over the local rows: d_values += w * d_out[b] and dw = <values[idx], d_out[b]>
  * for local slots (dw = 0 for slots held by other ranks). */
 msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B,

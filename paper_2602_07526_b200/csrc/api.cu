@@ -251,6 +251,49 @@ msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B, const int32_t* i
   return MSN_OK;
 }
 
+msn_status msn_pkm_gather_push(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                               const float* weights, const void* values, float* const* peer_recv,
+                               int32_t world, int32_t rank, int64_t local_batch) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(MSN_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
+  if (local_batch < 1 || B != (int64_t)world * local_batch)
+    return fail(MSN_ERR_INVALID_ARG, "B = %lld must equal world * local_batch = %d * %lld", (long long)B,
+                world, (long long)local_batch);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(values);
+  if (!peer_recv) return fail(MSN_ERR_INVALID_ARG, "peer_recv is NULL");
+  const Shape s = shape_of(h->cfg, B);
+  Push push;
+  push.peers = peer_recv;
+  push.rank = rank;
+  push.lb = local_batch;
+  cudaError_t e = launch_gather_push(s, idx, weights, values, push, (cudaStream_t)stream, &h->last_launches);
+  if (e == cudaErrorNotSupported) return fail(MSN_ERR_UNSUPPORTED, "gather_push: heads * k > 512");
+  if (e != cudaSuccess) return cuda_fail(e, "gather_push");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_reduce_partials(msn_pkm_t h, void* stream, int64_t local_batch, int32_t world,
+                                   const float* recv, float* out) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (local_batch < 0 || world < 1) return fail(MSN_ERR_INVALID_ARG, "local_batch / world");
+  if (local_batch == 0) return MSN_OK;
+  REQUIRE_PTR(recv);
+  REQUIRE_PTR(out);
+  const Shape s = shape_of(h->cfg, local_batch);
+  cudaError_t e = launch_reduce_partials(recv, world, local_batch, s.og, s.d_v, out, (cudaStream_t)stream,
+                                         &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_partials");
+  return MSN_OK;
+}
+
 static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* query,
                              const void* subkeys, const void* values, float* out, int32_t* idx,
                              float* weights, void* workspace, size_t workspace_bytes,

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
                                                      const VT* __restrict__ V,
                                                      float* __restrict__ out, int64_t B, int H, int k,
                                                      int d_v, int64_t row_begin,
-                                                     int64_t row_end, Gate gate, int og) {
+                                                     int64_t row_end, Gate gate, int og, Push push) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;  // lanes per row
@@ -50,7 +50,13 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
     gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * hpg * k, (grp + 1) * hpg * k, V, d_v, tot);
     if (g == 0) {
       const int64_t orow = b * og + grp;
-      float* o = out + orow * d_v;
+      float* o;
+      if (push.peers) {  // fused reduce-scatter: the home rank's receive slot
+        const int64_t home = b / push.lb, bl = b - home * push.lb;
+        o = push.peers[home] + (((int64_t)push.rank * push.lb + bl) * og + grp) * d_v;
+      } else {
+        o = out + orow * d_v;
+      }
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int vec = gl * VPL + v;
@@ -68,12 +74,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
 
 template <typename VT>
 cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const VT* V, float* out,
-                     cudaStream_t st, const Gate& gate) {
+                     cudaStream_t st, const Gate& gate, const Push& push) {
   const int R = s.d_v * (int)sizeof(VT) / 16;
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);
 #define GATHER(VPL, G, U)                                                                      \
   launch_pdl(gather_kernel<VT, VPL, G, U>, blocks, 256, 0, st, idx, w, V, out, s.B, s.H, s.k, s.d_v, \
-             s.row_begin, s.row_end, gate, s.og)
+             s.row_begin, s.row_end, gate, s.og, push)
   MSN_GATHER_DISPATCH(R, GATHER);
 #undef GATHER
   return cudaGetLastError();
@@ -84,8 +90,46 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
                           float* out, cudaStream_t st, int* launches, const Gate& gate) {
   if (s.H * s.k > kMaxHK) return cudaErrorNotSupported;
-  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, out, st, gate)
-                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, out, st, gate);
+  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, out, st, gate, Push{})
+                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, out, st, gate, Push{});
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+cudaError_t launch_gather_push(const Shape& s, const int32_t* idx, const float* w, const void* V,
+                               const Push& push, cudaStream_t st, int* launches) {
+  if (s.H * s.k > kMaxHK || !push.peers || push.lb <= 0) return cudaErrorNotSupported;
+  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, nullptr, st, Gate{}, push)
+                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, nullptr, st,
+                                                          Gate{}, push);
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+namespace {
+// out = recv[0] + recv[1] + ... in rank order, float4 per thread
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float4* __restrict__ recv, int world,
+                                                              int64_t n4, float4* __restrict__ out) {
+  pdl_enter();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  float4 a = recv[i];
+  for (int p = 1; p < world; ++p) {
+    const float4 v = recv[(int64_t)p * n4 + i];
+    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+  }
+  out[i] = a;
+}
+}  // namespace
+
+cudaError_t launch_reduce_partials(const float* recv, int world, int64_t lb, int og, int d_v,
+                                   float* out, cudaStream_t st, int* launches) {
+  if (d_v % 4) return cudaErrorNotSupported;
+  const int64_t n4 = lb * og * d_v / 4;
+  if (n4 == 0) return cudaSuccess;
+  launch_pdl(reduce_partials_kernel, (unsigned)((n4 + 255) / 256), 256, 0, st, (const float4*)recv, world,
+             n4, (float4*)out);
+  cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++*launches;
   return e;
 }

@@ -75,6 +75,20 @@ cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* id
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
                           float* out, cudaStream_t st, int* launches, const Gate& gate = Gate{});
 
+// a5 fused with the reduce-scatter of the row-sharded table: query b's
+// partial row is stored straight into its home rank's receive buffer
+// peers[b / lb][(rank * lb + b % lb) * og + g] (peer memory over NVLink).
+struct Push {
+  float* const* peers = nullptr;  // device array [world] of receive buffers
+  int rank = 0;
+  int64_t lb = 0;                 // queries per rank
+};
+cudaError_t launch_gather_push(const Shape& s, const int32_t* idx, const float* w, const void* V,
+                               const Push& push, cudaStream_t st, int* launches);
+// out[b, g] = sum_p recv[p][b][g] in rank order (=).
+cudaError_t launch_reduce_partials(const float* recv, int world, int64_t lb, int og, int d_v,
+                                   float* out, cudaStream_t st, int* launches);
+
 // f1 backward: dx = dxt (.) g(v_o) (=), dvo = dxt (.) x (.) g'(v_o) (=).
 cudaError_t launch_gate_backward(int64_t B, int d_v, int kind, const float* x, const float* vo,
                                  const float* dxt, float* dx, float* dvo, cudaStream_t st,

@@ -14,7 +14,12 @@ the sub-keys are replicated (they are small).  One step:
 
 The collectives are torch.distributed calls (NCCL over NVLink/NVSwitch on the
 GPU box): fixed-size, graph-capturable, no host synchronisation, NVLS-capable
-(reduce-scatter).  The data-path kernels are the C ABI's phase entry points
+(reduce-scatter).  transport="p2p" fuses the forward's gather with its
+reduce-scatter instead: msn_pkm_gather_push stores every query's partial row
+straight into the home rank's receive buffer (torch symmetric memory, NVLink
+peer stores issued by the gather kernel as the rows are summed), a device-side
+barrier orders the pushes, and msn_pkm_reduce_partials adds the world partials
+in rank order (deterministic).  The data-path kernels are the C ABI's phase entry points
 (msn_pkm_select / _gather / _scatter / _backward_keys).  dK is this rank's
 contribution; summing it across ranks is the caller's data-parallel job
 (like any replicated parameter).
@@ -30,7 +35,11 @@ import torch.distributed as dist
 class ShardedPKM:
     def __init__(self, heads: int, n_sub: int, d_half: int, d_value: int, k: int,
                  local_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
-                 group=None, phases=None, device=None):
+                 group=None, phases=None, device=None, transport: str = "nccl"):
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport {transport!r}: 'nccl' or 'p2p'")
+        self.transport = transport
+        self._symm = None
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -63,13 +72,35 @@ class ShardedPKM:
         dist.reduce_scatter_tensor(out, x.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
         return out
 
+    def _p2p_buffers(self, B_l: int, device):
+        """This rank's receive buffer [world, B_l, d_v] in symmetric memory and
+        the device array of every rank's buffer address (peer-mapped)."""
+        if self._symm is None or self._symm[0].shape[1] != B_l:
+            try:
+                import torch.distributed._symmetric_memory as symm
+            except ImportError as e:  # pragma: no cover - depends on the torch build
+                raise RuntimeError("transport='p2p' needs torch symmetric memory") from e
+            buf = symm.empty((self.world, B_l, self.d_value), dtype=torch.float32, device=device)
+            group = self.group if self.group is not None else dist.group.WORLD
+            hdl = symm.rendezvous(buf, group)
+            ptrs = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device=device)
+            self._symm = (buf, hdl, ptrs)
+        return self._symm
+
     def forward(self, query: torch.Tensor, subkeys: torch.Tensor, value_shard: torch.Tensor):
         """Returns (out [B_l,d_v], tape) for the local queries."""
         idx, w = self.ph.select(query, subkeys)
         idx_all = self._all_gather(idx)
         w_all = self._all_gather(w)
-        part = self.ph.gather(idx_all, w_all, value_shard)
-        out = self._reduce_scatter(part)
+        if self.transport == "p2p":
+            buf, hdl, ptrs = self._p2p_buffers(query.shape[0], query.device)
+            hdl.barrier(channel=0)  # every rank is done reading its previous step's partials
+            self.ph.gather_push(idx_all, w_all, value_shard, ptrs, self.world, self.rank)
+            hdl.barrier(channel=0)  # every push has landed
+            out = self.ph.reduce_partials(buf, self.world)
+        else:
+            part = self.ph.gather(idx_all, w_all, value_shard)
+            out = self._reduce_scatter(part)
         return out, (idx, w, idx_all, w_all)
 
     def backward(self, d_out: torch.Tensor, query: torch.Tensor, subkeys: torch.Tensor,

@@ -212,6 +212,24 @@ class PKMLookup:
         _lib.check(self.lib.msn_pkm_gather(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(V), _ptr(out)))
         return out
 
+    def gather_push(self, idx: torch.Tensor, w: torch.Tensor, values: torch.Tensor,
+                    peer_ptrs: torch.Tensor, world: int, rank: int) -> None:
+        """a5 over this process's rows, each query's partial pushed into its home
+        rank's receive buffer (peer_ptrs: int64 device tensor of `world` buffer
+        addresses; see msn_pkm_gather_push)."""
+        idx, w, V = self._dev(idx), self._dev(w), self._dev(values)
+        B = idx.shape[0]
+        _lib.check(self.lib.msn_pkm_gather_push(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(V),
+                                                ctypes.c_void_p(peer_ptrs.data_ptr()), world, rank, B // world))
+
+    def reduce_partials(self, recv: torch.Tensor, world: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """out = recv[0] + ... + recv[world-1] (rank order); recv [world, B_l, ...]."""
+        lb = recv.shape[1]
+        if out is None:
+            out = torch.empty(self._out_shape(lb), dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.msn_pkm_reduce_partials(self._h, _stream(), lb, world, _ptr(recv), _ptr(out)))
+        return out
+
     # ----------------------------------------------------------- backward
     def backward(self, d_out, query, subkeys, values, idx, w,
                  d_subkeys: Optional[torch.Tensor] = None, d_values: Optional[torch.Tensor] = None):

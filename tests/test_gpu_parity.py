@@ -578,3 +578,35 @@ def test_step_host_pipelined_matches_device():
     assert torch.equal(out_h, out.cpu()) and torch.equal(dq_h, dq.cpu())
     torch.testing.assert_close(dV2, dV, rtol=1e-5, atol=1e-7)
     torch.testing.assert_close(dK2, dK, rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_gather_push_matches_sharded_gather(P):
+    """The gather fused with the reduce-scatter (msn_pkm_gather_push +
+    msn_pkm_reduce_partials), P ranks emulated on one GPU (their receive
+    buffers are local tensors; each emulated rank's kernel runs to completion
+    before the reductions): every home rank's output equals the rank-order sum
+    of the P shard gathers bitwise, and the unsharded forward up to fp32
+    reassociation."""
+    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=256 * P)
+    Q, K, V, _ = wl.make_all(cfg, DEV)
+    full = lookup_for(cfg)
+    out_full, idx, w = full.forward(Q, K, V)
+    n, B_l = cfg.n_slots, cfg.batch // P
+    recv = [torch.full((P, B_l, cfg.d_value), float("nan"), device=DEV) for _ in range(P)]
+    ptrs = torch.tensor([r.data_ptr() for r in recv], dtype=torch.int64, device=DEV)
+    parts = []
+    for r in range(P):
+        r0, r1 = r * n // P, (r + 1) * n // P
+        lk = lookup_for(cfg, row_begin=r0, row_end=r1)
+        Vs = V[r0:r1].contiguous()
+        parts.append(lk.gather(idx, w, Vs))
+        lk.gather_push(idx, w, Vs, ptrs, P, r)
+    torch.cuda.synchronize()
+    for home in range(P):
+        out = full.reduce_partials(recv[home], P)
+        ref = parts[0][home * B_l:(home + 1) * B_l].clone()
+        for r in range(1, P):
+            ref += parts[r][home * B_l:(home + 1) * B_l]
+        assert torch.equal(out, ref)
+        torch.testing.assert_close(out, out_full[home * B_l:(home + 1) * B_l], rtol=1e-5, atol=1e-6)
