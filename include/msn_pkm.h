@@ -257,6 +257,26 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B,
                            const void* values, float* d_values, float* dw,
                            void* workspace, size_t workspace_bytes);
 
+/* a6 over the local rows for the row-sharded table OVER PEER MEMORY (no
+ * all-gather of d_out, no reduce-scatter of dw): B = world * local_batch
+ * queries in rank-major order (the all-gathered idx / weights); the d_out
+ * row of query b is read from its home rank's buffer
+ *   peer_d_out[p][(b % local_batch) * G * d_value ...],  p = b / local_batch,
+ * and dw of its slot (b, h, t) held by this rank is stored into
+ *   peer_dw[p][((b % local_batch) * heads + h) * k + t]
+ * (every element has exactly one owner rank, so the home buffers need no
+ * zeroing or summation).  peer_d_out / peer_dw: DEVICE arrays of world
+ * pointers to [local_batch, G, d_value] fp32 / [local_batch, heads, k] fp32
+ * buffers mapped into this process.  d_values += as msn_pkm_scatter.  The
+ * caller orders the d_out writes of all ranks before, and every rank's call
+ * before the dw reads (cross-rank barriers).  Deterministic grouped path
+ * only (MSN_ERR_UNSUPPORTED with MSN_FLAG_ATOMIC_BWD). */
+msn_status msn_pkm_scatter_p2p(msn_pkm_t h, void* stream, int64_t B,
+                               const int32_t* idx, const float* weights,
+                               const float* const* peer_d_out, const void* values,
+                               float* d_values, float* const* peer_dw, int32_t world,
+                               int64_t local_batch, void* workspace, size_t workspace_bytes);
+
 /* a7-a8 given the full dw: d_query (=) and d_subkeys (+=). */
 msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B,
                                  const void* query, const void* subkeys,

@@ -59,6 +59,7 @@ SIGNATURES = {
     "msn_pkm_gather": [_P, _P, _I64, _P, _P, _P, _P],
     "msn_pkm_gather_push": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _I64],
     "msn_pkm_reduce_partials": [_P, _P, _I64, ctypes.c_int32, _P, _P],
+    "msn_pkm_scatter_p2p": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int32, _I64, _P, _SZ],
     "msn_pkm_scatter": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_backward_keys": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_last_launch_count": [_P],

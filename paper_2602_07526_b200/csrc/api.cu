@@ -411,6 +411,41 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* 
   return MSN_OK;
 }
 
+msn_status msn_pkm_scatter_p2p(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                               const float* weights, const float* const* peer_d_out, const void* values,
+                               float* d_values, float* const* peer_dw, int32_t world,
+                               int64_t local_batch, void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
+  if (world < 1 || local_batch < 1 || B != (int64_t)world * local_batch)
+    return fail(MSN_ERR_INVALID_ARG, "B = %lld must equal world * local_batch = %d * %lld", (long long)B,
+                world, (long long)local_batch);
+  if (h->cfg.flags & MSN_FLAG_ATOMIC_BWD)
+    return fail(MSN_ERR_UNSUPPORTED, "scatter_p2p runs the deterministic grouped backward only");
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(d_values);
+  REQUIRE_PTR(workspace);
+  if (!peer_d_out || !peer_dw) return fail(MSN_ERR_INVALID_ARG, "peer_d_out / peer_dw is NULL");
+  const Shape s = shape_of(h->cfg, B);
+  const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
+  if (workspace_bytes < need)
+    return fail(MSN_ERR_WORKSPACE, "scatter workspace %zu < %zu bytes", workspace_bytes, need);
+  const BwdWorkspace ws = carve_bwd_workspace(shape_of(h->cfg, 0), B, workspace);
+  ScatterPeers peers;
+  peers.d_out = peer_d_out;
+  peers.dw = peer_dw;
+  peers.local_batch = local_batch;
+  cudaError_t e = launch_scatter_sorted(s, idx, weights, nullptr, values, d_values, nullptr, ws,
+                                        (cudaStream_t)stream, &h->last_launches,
+                                        TraceEvents{h->trace, h->ntrace}, 0, 0.f, 0.f, nullptr, &peers);
+  if (e != cudaSuccess) return cuda_fail(e, "scatter_p2p (dV, dw)");
+  return MSN_OK;
+}
+
 msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
                                   const float* weights, const float* d_out, void* values,
                                   int32_t update, float lr, float eps, float* state, float* dw,

@@ -208,6 +208,13 @@ struct GrpArgs {
   float lr = 0.f, eps = 0.f;
   float* state = nullptr;  // Adagrad accumulator [rows, D]
   void* Vw = nullptr;      // the value table, written in place
+  // row-sharded backward over peer memory (MODE_DV): x row r of the global
+  // batch lives on rank r / xl (px[rank] + (r % xl) D) and dw[rec] goes to
+  // rank rec / dl (pd[rank] + rec % dl); null: the local X / dots arrays
+  const float* const* px = nullptr;
+  float* const* pd = nullptr;
+  uint32_t xl = 0, dl = 0;
+  FastDiv div_xl, div_dl;
 };
 
 // Applies the fused update to VW consecutive elements at element offset off
@@ -352,8 +359,15 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
         rec[u] = src(j, w_);
         wt[u] = w_;
         const int64_t xr = grp_xrow<MODE>(a, rec[u]);
+        const XT* xrow;
+        if (MODE == MODE_DV && a.px) {  // the home rank's d_out row (peer memory)
+          const uint32_t home = a.div_xl.div((uint32_t)xr);
+          xrow = reinterpret_cast<const XT*>(a.px[home]) + lane * VW + (int64_t)(xr - (int64_t)home * a.xl) * D;
+        } else {
+          xrow = X + xr * D;
+        }
 #pragma unroll
-        for (int i = 0; i < NVEC; ++i) ldg_vec<XT, VW>(X + xr * D + i * 32 * VW, x[u] + i * VW);
+        for (int i = 0; i < NVEC; ++i) ldg_vec<XT, VW>(xrow + i * 32 * VW, x[u] + i * VW);
       } else {
         rec[u] = 0xffffffffu;
         wt[u] = 0.f;
@@ -378,7 +392,14 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
         const int u = lane / (32 / U);
 #pragma unroll
         for (int uu = 0; uu < U; ++uu)
-          if (uu == u && rec[uu] != 0xffffffffu) a.dots[rec[uu]] = r;
+          if (uu == u && rec[uu] != 0xffffffffu) {
+            if (a.pd) {  // dw straight into the home rank's buffer (one owner per element)
+              const uint32_t home = a.div_dl.div(rec[uu]);
+              a.pd[home][rec[uu] - home * a.dl] = r;
+            } else {
+              a.dots[rec[uu]] = r;
+            }
+          }
       }
     }
   }
@@ -773,7 +794,8 @@ template <int MODE, typename XT, typename YT>
 cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const float* wts,
                        const void* X, const void* Y, float* dots, float* G, int H, int k, int D,
                        cudaStream_t st, int* launches, const TraceEvents& tr = TraceEvents{},
-                       const UpdateArgs& up = UpdateArgs{}, int og = 1) {
+                       const UpdateArgs& up = UpdateArgs{}, int og = 1,
+                       const ScatterPeers* peers = nullptr) {
   if (n == 0 || nrows == 0) return cudaSuccess;
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 2) rb = (int64_t)num_sms() * 2;
@@ -795,6 +817,14 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   a.eps = up.eps;
   a.state = up.state;
   a.Vw = const_cast<void*>(Y);
+  if (peers) {
+    a.px = peers->d_out;
+    a.pd = peers->dw;
+    a.xl = (uint32_t)(peers->local_batch * og);
+    a.dl = (uint32_t)(peers->local_batch * H * k);
+    a.div_xl = FastDiv(a.xl);
+    a.div_dl = FastDiv(a.dl);
+  }
   switch (D / 32) {
     case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches, tr);
     case 2: return grp_reduce_t<MODE, XT, YT, 2>(a, n, nrows, st, launches, tr);
@@ -812,7 +842,7 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
 __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64_t row_begin,
                                int64_t row_end, uint32_t sentinel, uint32_t* __restrict__ keys,
                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ rank,
-                               float* __restrict__ dw) {
+                               float* __restrict__ dw) {  // dw null: non-local slots are other ranks'
   pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -821,7 +851,7 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
   const uint32_t key = local ? (uint32_t)(f - row_begin) : sentinel;
   keys[p] = key;
   if (local) rank[p] = atomicAdd(&cnt[key], 1u);
-  else dw[p] = 0.f;
+  else if (dw) dw[p] = 0.f;
 }
 
 // ----------------------------------------------- ds, dQ and dK records ----
@@ -1104,7 +1134,7 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
                                   const float* dOut, const void* V, float* dV, float* dw,
                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
                                   const TraceEvents& tr, int upd, float lr, float eps,
-                                  float* state) {
+                                  float* state, const ScatterPeers* peers) {
   if (!epl_ok(s.d_v)) return cudaErrorNotSupported;
   const int64_t n = s.B * s.H * s.k;  // s.B is the gather batch here
   if (n == 0) return cudaSuccess;
@@ -1113,16 +1143,16 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
   cudaError_t e = grp_begin(g, nrows, st);
   if (e != cudaSuccess) return e;
   launch_pdl(dv_keys_kernel, (unsigned)((n + 255) / 256), 256, 0, st, idx, n, s.row_begin, s.row_end,
-                                                              nrows, g.keys, g.cnt, g.rank, dw);
+                                                              nrows, g.keys, g.cnt, g.rank, peers ? nullptr : dw);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
   if (s.v_dt == F32)
     return grp_finish<MODE_DV, float, float>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k, s.d_v, st,
-                                             launches, tr, UpdateArgs{upd, lr, eps, state}, s.og);
+                                             launches, tr, UpdateArgs{upd, lr, eps, state}, s.og, peers);
   return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k,
                                                    s.d_v, st, launches, tr, UpdateArgs{upd, lr, eps, state},
-                                                   s.og);
+                                                   s.og, peers);
 }
 
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,

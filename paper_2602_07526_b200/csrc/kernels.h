@@ -128,6 +128,16 @@ struct TraceEvents {
   int n = 0;
 };
 
+// Row-sharded backward over peer memory: the d_out rows of query b are read
+// from rank b / local_batch's buffer d_out[rank] ([local_batch, og, d_v]) and
+// dw of record (b, h, t) is written into rank b / local_batch's dw[rank]
+// ([local_batch, H, k]); each dw element has exactly one owner rank.
+struct ScatterPeers {
+  const float* const* d_out = nullptr;  // device array [world]
+  float* const* dw = nullptr;           // device array [world]
+  int64_t local_batch = 0;
+};
+
 // a6 deterministic: group (idx -> cid) by row, then fused row-major dV += / dw.
 // tr: events around the short-run reducer (profiling only).
 // upd: 0 -> dV += g; 1 -> SGD, 2 -> Adagrad applied to V in
@@ -136,7 +146,8 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
                                   const float* dOut, const void* V, float* dV, float* dw,
                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
                                   const TraceEvents& tr = TraceEvents{}, int upd = 0,
-                                  float lr = 0.f, float eps = 0.f, float* state = nullptr);
+                                  float lr = 0.f, float eps = 0.f, float* state = nullptr,
+                                  const ScatterPeers* peers = nullptr);
 // a6 atomic: query-major re-gather + red.global.add.v4.f32.
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,

@@ -19,7 +19,10 @@ reduce-scatter instead: msn_pkm_gather_push stores every query's partial row
 straight into the home rank's receive buffer (torch symmetric memory, NVLink
 peer stores issued by the gather kernel as the rows are summed), a device-side
 barrier orders the pushes, and msn_pkm_reduce_partials adds the world partials
-in rank order (deterministic).  The data-path kernels are the C ABI's phase entry points
+in rank order (deterministic).  Its backward reads every d_out row from the
+home rank's buffer inside the dV reducer and stores every dw element into the
+home rank's buffer (msn_pkm_scatter_p2p): no all-gather of d_out, no
+reduce-scatter of dw.  The data-path kernels are the C ABI's phase entry points
 (msn_pkm_select / _gather / _scatter / _backward_keys).  dK is this rank's
 contribution; summing it across ranks is the caller's data-parallel job
 (like any replicated parameter).
@@ -111,8 +114,32 @@ class ShardedPKM:
         dev = d_out.device
         if d_value_shard is None:
             d_value_shard = torch.zeros((self.rows, self.d_value), dtype=torch.float32, device=dev)
-        d_all = self._all_gather(d_out.float())
-        dw_part = self.ph.scatter(idx_all, w_all, d_all, value_shard, d_value_shard)
-        dw = self._reduce_scatter(dw_part)
+        if self.transport == "p2p":
+            dbuf, dwbuf, dh, dptrs, wptrs = self._p2p_bwd_buffers(d_out.shape[0], dev)
+            dh.barrier(channel=0)  # every rank is done with the previous step's buffers
+            dbuf.copy_(d_out.float())
+            dh.barrier(channel=0)  # every rank's d_out is in place
+            self.ph.scatter_p2p(idx_all, w_all, value_shard, d_value_shard, dptrs, wptrs, self.world)
+            dh.barrier(channel=0)  # every owner's dw has landed
+            dw = dwbuf.clone()
+        else:
+            d_all = self._all_gather(d_out.float())
+            dw_part = self.ph.scatter(idx_all, w_all, d_all, value_shard, d_value_shard)
+            dw = self._reduce_scatter(dw_part)
         dq, d_subkeys = self.ph.backward_keys(query, subkeys, idx, w, dw, d_subkeys)
         return dq, d_subkeys, d_value_shard, dw
+
+    def _p2p_bwd_buffers(self, B_l: int, device):
+        """Symmetric d_out [B_l, d_v] and dw [B_l, H, k] buffers of this rank and
+        the device arrays of every rank's addresses."""
+        if getattr(self, "_symm_bwd", None) is None or self._symm_bwd[0].shape[0] != B_l:
+            import torch.distributed._symmetric_memory as symm
+            group = self.group if self.group is not None else dist.group.WORLD
+            dbuf = symm.empty((B_l, self.d_value), dtype=torch.float32, device=device)
+            dh = symm.rendezvous(dbuf, group)
+            wbuf = symm.empty((B_l, self.heads, self.k), dtype=torch.float32, device=device)
+            wh = symm.rendezvous(wbuf, group)
+            dptrs = torch.tensor([int(p) for p in dh.buffer_ptrs], dtype=torch.int64, device=device)
+            wptrs = torch.tensor([int(p) for p in wh.buffer_ptrs], dtype=torch.int64, device=device)
+            self._symm_bwd = (dbuf, wbuf, dh, dptrs, wptrs)
+        return self._symm_bwd

@@ -268,6 +268,21 @@ class PKMLookup:
                                             _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
         return dw
 
+    def scatter_p2p(self, idx, w, values, d_values, dout_ptrs: torch.Tensor, dw_ptrs: torch.Tensor, world: int):
+        """a6 over this process's rows, d_out rows read from and dw written to the
+        home ranks' buffers (int64 device tensors of `world` addresses; see
+        msn_pkm_scatter_p2p)."""
+        idx, w, V = self._dev(idx), self._dev(w), self._dev(values)
+        B = idx.shape[0]
+        f, b = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(self.lib.msn_pkm_workspace_size(self._h, 0, B, ctypes.byref(f), ctypes.byref(b)))
+        ws = torch.empty(b.value, dtype=torch.uint8, device=self.device) \
+            if self._ws is None or self._ws.numel() < b.value else self._ws
+        _lib.check(self.lib.msn_pkm_scatter_p2p(self._h, _stream(), B, _ptr(idx), _ptr(w),
+                                                ctypes.c_void_p(dout_ptrs.data_ptr()), _ptr(V), _ptr(d_values),
+                                                ctypes.c_void_p(dw_ptrs.data_ptr()), world, B // world,
+                                                _ptr(ws), ws.numel()))
+
     def scatter_update(self, idx, w, d_out, values, update: str = "sgd", lr: float = 1e-3,
                        eps: float = 1e-10, state: Optional[torch.Tensor] = None):
         """a6 with the optimiser step fused: values is updated
