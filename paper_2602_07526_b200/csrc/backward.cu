@@ -339,7 +339,7 @@ __device__ __forceinline__ uint32_t grp_xrow(const GrpArgs& a, uint32_t rec) {
 
 // Sums the entries src(j), j in [j0, j1), of one row into acc (in j order),
 // U x rows in flight at a time; MODE_DV also writes dw[rec] = <y, x>.
-template <int MODE, typename XT, int EPL, int U, typename Src>
+template <int MODE, typename XT, int EPL, int U, bool P2P, typename Src>
 __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1, Src src,
                                                const float* y, float* acc) {
   constexpr int VW = EPL < 4 ? EPL : 4;
@@ -360,7 +360,7 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
         wt[u] = w_;
         const int64_t xr = grp_xrow<MODE>(a, rec[u]);
         const XT* xrow;
-        if (MODE == MODE_DV && a.px) {  // the home rank's d_out row (peer memory)
+        if (P2P) {  // the home rank's d_out row (peer memory)
           const uint32_t home = a.div_xl.div((uint32_t)xr);
           xrow = reinterpret_cast<const XT*>(a.px[home]) + lane * VW + (int64_t)(xr - (int64_t)home * a.xl) * D;
         } else {
@@ -393,7 +393,7 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 #pragma unroll
         for (int uu = 0; uu < U; ++uu)
           if (uu == u && rec[uu] != 0xffffffffu) {
-            if (a.pd) {  // dw straight into the home rank's buffer (one owner per element)
+            if (P2P) {  // dw straight into the home rank's buffer (one owner per element)
               const uint32_t home = a.div_dl.div(rec[uu]);
               a.pd[home][rec[uu] - home * a.dl] = r;
             } else {
@@ -413,7 +413,7 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // after that two ahead), so a run costs about one memory round trip.  The
 // row sum is added to G by one vector reduction per lane (red.global.add,
 // performed in L2): the row's only update, so G = G + sum bitwise.
-template <int MODE, typename XT, typename YT, int EPL, bool UPD>
+template <int MODE, typename XT, typename YT, int EPL, bool UPD, bool P2P>
 __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4))) grp_reduce_short_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BP
     if (lane >= len) rk = 0xffffffffu;
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
-    grp_accumulate<MODE, XT, EPL, U>(
+    grp_accumulate<MODE, XT, EPL, U, P2P>(
         a, 0, len,
         [&](int j, float& w_) {
           const int s = __ffs(__ballot_sync(0xffffffffu, rk == (uint32_t)j)) - 1;
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
 // pieces in flight); warp w sums the w-th 32-entry slice in order, the CTA
 // adds the 8 slice sums in warp order.  A run of one piece adds its sum to G
 // directly (its only update); longer runs leave the piece sum for step 3.
-template <int MODE, typename XT, typename YT, int EPL>
+template <int MODE, typename XT, typename YT, int EPL, bool P2P>
 __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
     // the slice's ids, one per lane, then consumed in order
     const uint32_t myid = j0 + lane < j1 ? a.ent[run.x + j0 + lane] : 0u;
     const float myw = j0 + lane < j1 ? a.wts[myid] : 0.f;
-    grp_accumulate<MODE, XT, EPL, U>(
+    grp_accumulate<MODE, XT, EPL, U, P2P>(
         a, j0, j1,
         [&](int j, float& w_) {
           w_ = __shfl_sync(0xffffffffu, myw, (j - j0) & 31);
@@ -755,9 +755,11 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   if (sb < 1) sb = 1;
   if (tr.n > 0) cudaEventRecord(tr.ev[0], st);  // profiling: the short-run reducer alone
   if (MODE == MODE_DV && a.upd)
-    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, true>, (unsigned)sb, 256, 0, st, a);
+    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, true, false>, (unsigned)sb, 256, 0, st, a);
+  else if (MODE == MODE_DV && a.px)
+    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false, MODE == MODE_DV>, (unsigned)sb, 256, 0, st, a);
   else
-    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false>, (unsigned)sb, 256, 0, st, a);
+    launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false, false>, (unsigned)sb, 256, 0, st, a);
   if (tr.n > 1) cudaEventRecord(tr.ev[1], st);
   // long runs: sort, pieces, combine
   static bool attr = false;
@@ -774,7 +776,10 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   int64_t pb = (int64_t)sms * 8;
   const int64_t pneed = grp_pieces_max(n);
   if (pb > pneed) pb = pneed;
-  launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL>, (unsigned)pb, 256, 0, st, a);
+  if (MODE == MODE_DV && a.px)
+    launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL, MODE == MODE_DV>, (unsigned)pb, 256, 0, st, a);
+  else
+    launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL, false>, (unsigned)pb, 256, 0, st, a);
   int64_t cb = (lneed + 7) / 8;
   if (cb > (int64_t)sms * 4) cb = (int64_t)sms * 4;
   launch_pdl(grp_combine_long_kernel<YT, EPL>, (unsigned)cb, 256, 0, st, a);

@@ -171,12 +171,27 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     sm.cand[x] = sel_key(c, flat);
   }
   __syncwarp();
-  // exact rank by composite key; keys are distinct (flat ids are distinct)
-  for (int x = lane; x < m; x += 32) {
-    const uint64_t kx = sm.cand[x];
-    int r = 0;
-    for (int y = 0; y < m; ++y) r += sm.cand[y] > kx;
-    if (r < k) sm.res[r] = kx;
+  // exact rank by composite key; keys are distinct (flat ids are distinct).
+  // Up to 64 candidates (the common case): each lane ranks its two in one
+  // pass over the list (one shared load per two comparisons).
+  if (m <= 64) {
+    const uint64_t k0 = lane < m ? sm.cand[lane] : ~0ull;
+    const uint64_t k1 = lane + 32 < m ? sm.cand[lane + 32] : ~0ull;
+    int r0 = 0, r1 = 0;
+    for (int y = 0; y < m; ++y) {
+      const uint64_t ky = sm.cand[y];
+      r0 += ky > k0;
+      r1 += ky > k1;
+    }
+    if (lane < m && r0 < k) sm.res[r0] = k0;
+    if (lane + 32 < m && r1 < k) sm.res[r1] = k1;
+  } else {
+    for (int x = lane; x < m; x += 32) {
+      const uint64_t kx = sm.cand[x];
+      int r = 0;
+      for (int y = 0; y < m; ++y) r += sm.cand[y] > kx;
+      if (r < k) sm.res[r] = kx;
+    }
   }
   __syncwarp();
   // softmax over the k selected scores, max = the first (reading R1)
