@@ -90,12 +90,17 @@ def test_integer_data_bit_exact_selection(B, H, n_sub, d_h, k):
         parity.row_close(out.cpu().numpy(), o["out"], 1e-4, what="out")
 
 
-@pytest.mark.parametrize("d_h,n_sub", [(32, 64), (64, 64), (128, 1024)])
-def test_zero_query_closed_form(d_h, n_sub):
-    """q = 0: all scores tie at 0 -> idx = 0..k-1 (massive-tie path)."""
-    cfg = wl.tiny_config(16, 2, d_h, n_sub, 64, 8, torch.bfloat16, torch.bfloat16)
+@pytest.mark.parametrize("d_h,n_sub,dt", [(32, 64, torch.bfloat16), (64, 64, torch.bfloat16),
+                                          (128, 1024, torch.bfloat16), (128, 1024, torch.float32),
+                                          (64, 256, torch.float32)])
+def test_zero_query_closed_form(d_h, n_sub, dt):
+    """q = 0: all scores tie at 0 -> idx = 0..k-1.  On the tcgen05 scorer every
+    row lets all its columns through the bound (resident and two-sweep rows,
+    bf16 and 3xTF32 with the 1xTF32 first sweep), so every row takes the
+    exact rescoring path."""
+    cfg = wl.tiny_config(16, 2, d_h, n_sub, 64, 8, dt, torch.bfloat16)
     _, K, V, _ = wl.make_all(cfg, DEV)
-    Q = torch.zeros((16, 2, 2, d_h), dtype=torch.bfloat16, device=DEV)
+    Q = torch.zeros((16, 2, 2, d_h), dtype=dt, device=DEV)
     out, idx, w = lookup_for(cfg).forward(Q, K, V)
     assert torch.equal(idx.cpu(), torch.arange(8, dtype=torch.int32).expand(16, 2, 8))
     assert torch.allclose(w, torch.full_like(w, 1 / 8), rtol=1e-6)
