@@ -361,9 +361,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     const bool resident = p.passes == 1;  // whole row in the two TMEM buffers
     if (resident) {
-      wait_chunks(0, p.n_chunks);
-      SEL_TS(1);
-      pass_a(0, p.n_sub);
+      // chunk by chunk, so that pass A over chunk 0 runs under the MMA of chunk 1
+      // (both stay resident for pass B)
+      for (int c = 0; c < p.n_chunks; ++c) {
+        wait_chunks(c, 1);
+        if (c == 0) SEL_TS(1);
+        pass_a(c, p.n_tile);
+      }
     } else {
       for (int c = 0; c < p.n_chunks; ++c) {
         wait_chunks(c, 1);
