@@ -18,6 +18,8 @@
 // split S ways for parallelism and the S partials are added into dK in split
 // order: bitwise deterministic.  Rounding dS to bf16 (2^-9 relative) is
 // within the bf16-config tolerance; fp32 configs keep the sort-based path.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -28,6 +30,7 @@ using namespace tc;
 
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 TMEM alloc + epilogue (tile (w-2)/4)
 constexpr int kCtasPerSm = 1;
+constexpr int kDqStages = 4;
 // MT 128-row tiles per CTA share every B stage (M = 128 MT): stages of
 // (16 MT + 32) KB at d_h = 256, up to ~192 KB of ring
 __host__ __device__ constexpr int stages_for(int MT) { return MT == 1 ? 4 : 3; }
@@ -194,29 +197,32 @@ struct DqParams {
   float* dQ;  // [B, H*2, d_h]
 };
 
-template <int MT>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+// Persistent: one CTA per SM walks the (query tile, head.half) tiles in
+// hh-major order (the K block of an hh stays hot in L2); two TMEM
+// accumulators, so the MMA of tile i+1 runs while the epilogue drains tile i,
+// and the TMA ring streams the k-blocks of successive tiles without a break.
+__global__ void __launch_bounds__(kThreads, 1)
     dq_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                   const __grid_constant__ CUtensorMap tmap_k, const DqParams p) {
+                   const __grid_constant__ CUtensorMap tmap_k, const DqParams p, int mtiles) {
   pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   const int nb = p.d_h / 64;                      // B atoms per stage
   constexpr int kABytes = 128 * 128;              // 128 queries x 64 sub-keys bf16
-  constexpr int kStg = stages_for(MT);
-  uint8_t* sA = smem_raw + pad;                   // kStg x MT x 16 KB
-  uint8_t* sB = sA + kStg * MT * kABytes;         // kStg x nb atoms
+  constexpr int kStg = kDqStages;
+  uint8_t* sA = smem_raw + pad;                   // kStg x 16 KB
+  uint8_t* sB = sA + kStg * kABytes;              // kStg x nb atoms
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStg * nb * kAtom);
   uint64_t* full = bars;
   uint64_t* empty = full + kStg;
-  uint64_t* tdone = empty + kStg;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
-  const uint32_t tcols = tmem_cols(MT * p.d_h);
+  uint64_t* tfull = empty + kStg;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t tcols = tmem_cols(2 * p.d_h);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * 128 * MT;
-  const int hh = blockIdx.y;
   const int nkb = p.n_sub / 64;
+  const int ntiles = mtiles * 2 * p.H;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap_a);
@@ -225,7 +231,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tdone, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -241,56 +250,73 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(MT * kABytes) + (uint32_t)nb * kAtom;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStg;
-        mbar_wait(&empty[s], ((kb / kStg) & 1) ^ 1);
-        mbar_expect_tx(&full[s], bytes);
-        // queries >= B (ragged last tile) are zero-filled by TMA
-#pragma unroll
-        for (int t = 0; t < MT; ++t)
-          tma_load_3d(sA + (s * MT + t) * kABytes, &tmap_a, &full[s], kb * 64, hh, m0 + 128 * t);
-        for (int j = 0; j < nb; ++j)
-          tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_k, &full[s], 64 * j, kb * 64, hh);
+      const uint32_t bytes = (uint32_t)kABytes + (uint32_t)nb * kAtom;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int hh = t / mtiles, m0 = (t - hh * mtiles) * 128;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStg;
+          mbar_wait(&empty[s], ((it / kStg) & 1) ^ 1);
+          mbar_expect_tx(&full[s], bytes);
+          // queries >= B (ragged last tile) are zero-filled by TMA
+          tma_load_3d(sA + s * kABytes, &tmap_a, &full[s], kb * 64, hh, m0);
+          for (int j = 0; j < nb; ++j)
+            tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_k, &full[s], 64 * j, kb * 64, hh);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(128, p.d_h) | (1u << 16);  // B MN-major
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStg;
-        mbar_wait(&full[s], (kb / kStg) & 1);
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const int buf = lt & 1;
+        mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t b0 = smem_u32(sB + s * nb * kAtom);
+        const uint32_t d = tmem + buf * p.d_h;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStg;
+          mbar_wait(&full[s], (it / kStg) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * kABytes);
+          const uint32_t b0 = smem_u32(sB + s * nb * kAtom);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // 16 sub-keys: +32 B in the A row, +2 KB in B
-#pragma unroll
-          for (int t = 0; t < MT; ++t)  // the MT query tiles share the K block
-            tc_mma(tmem + t * p.d_h, sw128_desc(smem_u32(sA + (s * MT + t) * kABytes) + kk * 32),
-                   sw128_mn_desc(b0 + kk * 2048), idesc, (kb | kk) != 0);
-        tc_commit(&empty[s]);
+          for (int kk = 0; kk < 4; ++kk)  // 16 sub-keys: +32 B in the A row, +2 KB in B
+            tc_mma(d, sw128_desc(a0 + kk * 32), sw128_mn_desc(b0 + kk * 2048), idesc, (kb | kk) != 0);
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[buf]);
       }
-      tc_commit(tdone);
     }
-  } else if ((warp - 2) / 4 < MT) {
+  } else {
+    // epilogue: warps 2..9, TMEM lane quarter warp % 4, column half (warp - 2) / 4
     const int q = warp & 3;
-    const int t = (warp - 2) / 4;
+    const int ch = (warp - 2) / 4;
+    const int cw = p.d_h / 2;
     const int row = q * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + t * p.d_h;
-    const int64_t b = (int64_t)m0 + t * 128 + row;
-    float* dst = p.dQ + (b * (2 * p.H) + hh) * (int64_t)p.d_h;
-    mbar_wait(tdone, 0);
-    tc_fence_after();
-    for (int c0 = 0; c0 < p.d_h; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(lane_base + c0, r);
-      if (b < p.B) {
-        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+    int lt = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int hh = t / mtiles, m0 = (t - hh * mtiles) * 128;
+      const int buf = lt & 1;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + buf * p.d_h;
+      const int64_t b = (int64_t)m0 + row;
+      float* dst = p.dQ + (b * (2 * p.H) + hh) * (int64_t)p.d_h;
+      for (int c0 = ch * cw; c0 < (ch + 1) * cw; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_base + c0, r);
+        if (b < p.B) {
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                              __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          for (int j = 0; j < 8; ++j)
+            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
   tc_fence_before();
@@ -306,10 +332,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // dK gains on long codebooks (C4, n_sub 2048: -21 us) and loses on short ones
 // (C2, n_sub 512: +7.5 us, too few k-blocks per split).
 int env_int(const char* n, int d) { const char* v = getenv(n); return v ? atoi(v) : d; }
-int dq_mt(const Shape& s) {
-  static const int f = env_int("MSN_DQ_MT", 1);
-  return (f >= 2 && s.B > 128) ? 2 : 1;
+int num_sms_dk() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
+int dq_mt(const Shape&) { return 1; }
 int dk_mt(const Shape& s) {
   static const int f = env_int("MSN_DK_MT", 0);
   const bool want = f == 0 ? s.n_sub >= 1024 : f >= 2;
@@ -317,8 +350,8 @@ int dk_mt(const Shape& s) {
 }
 
 size_t dq_smem_bytes(const Shape& s, int MT) {
-  const int st = stages_for(MT);
-  return 1024 + (size_t)st * (MT * 128 * 128 + (s.d_h / 64) * kAtom) + 8 * (2 * st + 1) + 16;
+  (void)MT;
+  return 1024 + (size_t)kDqStages * (128 * 128 + (s.d_h / 64) * kAtom) + 8 * (2 * kDqStages + 4) + 16;
 }
 
 // dK += sum_s part[s] (fixed split order)
@@ -431,16 +464,17 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
     DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ};
-    const int mtq = dq_mt(s);
-    auto dqk = mtq == 2 ? dq_gemm_kernel<2> : dq_gemm_kernel<1>;
-    static bool qattr[2] = {false, false};
-    if (!qattr[mtq - 1]) {
-      cudaError_t e0 = cudaFuncSetAttribute(dqk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static bool qattr = false;
+    if (!qattr) {
+      cudaError_t e0 = cudaFuncSetAttribute(dq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            227 * 1024);
       if (e0 != cudaSuccess) return e0;
-      qattr[mtq - 1] = true;
+      qattr = true;
     }
-    dim3 qgrid((unsigned)((s.B + 128 * mtq - 1) / (128 * mtq)), HH);
-    launch_pdl(dqk, qgrid, kThreads, dq_smem_bytes(s, mtq), st, ma, mk, qp);
+    const int mtiles = (int)((s.B + 127) / 128);
+    const int ntiles = mtiles * HH;
+    launch_pdl(dq_gemm_kernel, (unsigned)std::min(ntiles, num_sms_dk()), kThreads, dq_smem_bytes(s, 1), st,
+               ma, mk, qp, mtiles);
     cudaError_t e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return e1;
     ++*launches;
