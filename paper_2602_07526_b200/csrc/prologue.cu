@@ -87,7 +87,11 @@ __global__ void __launch_bounds__(256) ln_backward_kernel(const T* __restrict__ 
 }
 
 // C[b] (= or +=) A[b] B[b]: A(i,k) = A[b*a_bs + i*a_rs + k*a_cs], likewise B;
-// C row-major with row stride c_rs.  64 x 64 tile per CTA, k-steps of 16.
+// C row-major with row stride c_rs.  64 x 64 tile per CTA, k-steps of 16;
+// the operand loads run kPf steps ahead of the math (a register ring), so a
+// k-step costs its arithmetic rather than a global-load round trip.  The k
+// order of the accumulation is unchanged (ascending).
+constexpr int kPf = 4;
 template <typename TA, typename TB, typename TC>
 __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const TA* __restrict__ A,
                                                    int64_t a_rs, int64_t a_cs, int64_t a_bs,
@@ -107,39 +111,54 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const TA
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  for (int k0 = 0; k0 < K; k0 += 16) {
-    // 16 x 64 elements per operand tile, 4 per thread; consecutive threads
-    // walk the operand's contiguous dimension (coalesced loads)
+  const bool a_k = a_cs == 1;  // A contiguous along k
+  const bool b_k = b_rs == 1;  // B contiguous along k
+  // 16 x 64 elements per operand tile, 4 per thread; consecutive threads walk
+  // the operand's contiguous dimension (coalesced loads)
+  auto load = [&](int k0, float (&va)[4], float (&vb)[4]) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = tid + u * 256;
-      const bool a_k = a_cs == 1;  // A contiguous along k
       const int kk = a_k ? e % 16 : e / 64, ii = a_k ? e / 16 : e % 64;
       const int gk = k0 + kk;
-      As[kk][ii] = (m0 + ii < M && gk < K) ? ld_f(A + (int64_t)(m0 + ii) * a_rs + (int64_t)gk * a_cs) : 0.f;
+      va[u] = (m0 + ii < M && gk < K) ? ld_f(A + (int64_t)(m0 + ii) * a_rs + (int64_t)gk * a_cs) : 0.f;
+      const int kb = b_k ? e % 16 : e / 64, jj = b_k ? e / 16 : e % 64;
+      const int gb = k0 + kb;
+      vb[u] = (n0 + jj < N && gb < K) ? ld_f(B + (int64_t)gb * b_rs + (int64_t)(n0 + jj) * b_cs) : 0.f;
     }
+  };
+  float ra[kPf][4], rb[kPf][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * 256;
-      const bool b_k = b_rs == 1;  // B contiguous along k
-      const int kk = b_k ? e % 16 : e / 64, jj = b_k ? e / 16 : e % 64;
-      const int gk = k0 + kk;
-      Bs[kk][jj] = (n0 + jj < N && gk < K) ? ld_f(B + (int64_t)gk * b_rs + (int64_t)(n0 + jj) * b_cs) : 0.f;
+  for (int d = 0; d < kPf; ++d) load(d * 16, ra[d], rb[d]);
+  for (int k0 = 0; k0 < K; k0 += 16 * kPf) {
+#pragma unroll
+    for (int d = 0; d < kPf; ++d) {
+      const int kc = k0 + d * 16;
+      if (kc >= K) break;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = tid + u * 256;
+        const int kk = a_k ? e % 16 : e / 64, ii = a_k ? e / 16 : e % 64;
+        As[kk][ii] = ra[d][u];
+        const int kb = b_k ? e % 16 : e / 64, jj = b_k ? e / 16 : e % 64;
+        Bs[kb][jj] = rb[d][u];
+      }
+      __syncthreads();
+      load(kc + 16 * kPf, ra[d], rb[d]);  // kPf steps ahead (zeros past K)
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
