@@ -57,6 +57,9 @@ SWEEP = [
     # tensor-core dK: d_h 64, split-K with a ragged last split
     (1000, 2, 256, 64, 64, 16, torch.bfloat16, torch.bfloat16),
     (70, 2, 128, 64, 64, 16, torch.bfloat16, torch.bfloat16),
+    # two-sweep scorer rows (n_sub > 512) with KT = 8: bf16, and fp32 (1xTF32 first sweep)
+    (50, 2, 1024, 64, 64, 8, torch.bfloat16, torch.bfloat16),
+    (40, 1, 1024, 32, 64, 5, torch.float32, torch.float32),
 ]
 
 
