@@ -647,3 +647,33 @@ def test_scatter_p2p_matches_sharded_scatter(P):
         torch.cuda.synchronize()
         assert torch.equal(dv, dv_ref)
     assert torch.equal(torch.cat(dws), dw_sum)
+
+
+def _random_shapes(n, seed=2602):
+    """Seeded random shapes across the library's supported ranges: B ragged,
+    H up to 8, n_sub from 16 to 1024 (tcgen05 resident and two-sweep rows,
+    SIMT fallback shapes), d_h / d_v of every per-lane width the kernels
+    template on, k from 1 to 64, fp32 / bf16 keys and values."""
+    import random
+    rnd = random.Random(seed)
+    dts = [torch.float32, torch.bfloat16]
+    out = []
+    while len(out) < n:
+        n_sub = rnd.choice([16, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 1024])
+        k = rnd.randint(1, min(64, n_sub))
+        H = rnd.choice([1, 2, 3, 4, 8])
+        if H * k > 512:
+            continue
+        out.append((rnd.randint(1, 400), H, n_sub, rnd.choice([32, 64, 128, 256]),
+                    rnd.choice([32, 64, 128, 256, 512]), k, rnd.choice(dts), rnd.choice(dts)))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes(24),
+                         ids=lambda s: "x".join(str(v) for v in s[:6]) + f"-{str(s[6])[6:]}-{str(s[7])[6:]}")
+def test_random_shapes_fwd_bwd(shape):
+    B, H, n_sub, d_h, d_v, k, qdt, vdt = shape
+    cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, qdt, vdt, index=500 + n_sub + k + H)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    res = run_fwd_bwd(cfg, Q, K, V, dOut)
+    check_all(cfg, Q, K, V, dOut, res)
