@@ -273,15 +273,19 @@ def test_fused_update(update, name, B):
 
 # ------------------------------------------ head groups / tokens (f4) ----
 @pytest.mark.parametrize("tables", [False, True])
-@pytest.mark.parametrize("B,dt,G,H", [(300, torch.float32, 4, 8), (2048, torch.bfloat16, 16, 16),
-                                      (9000, torch.float32, 2, 4)])
-def test_head_groups(B, dt, G, H, tables):
+@pytest.mark.parametrize("B,dt,G,H,n_sub,d_h", [(300, torch.float32, 4, 8, 64, 32),
+                                                (2048, torch.bfloat16, 16, 16, 64, 32),
+                                                (9000, torch.float32, 2, 4, 64, 32),
+                                                # tcgen05 scorer: resident rows, two-sweep rows
+                                                (700, torch.bfloat16, 4, 8, 256, 64),
+                                                (300, torch.bfloat16, 2, 4, 1024, 64)])
+def test_head_groups(B, dt, G, H, tables, n_sub, d_h):
     """Token-specific codebooks: G groups of H/G heads with a
     shared table (or one table per group), out [B, G, d_v].  The reference is
     G independent fp64 oracle lookups -- group g's heads, its table -- and the
     backward the same with d_out[:, g]; dV rows, dK and dQ compared per group."""
     from oracle import oracle as orc
-    n_sub, d_h, d_v, k = 64, 32, 64, 8
+    d_v, k = 64, 8
     cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, dt, dt, index=14)
     Q, K, V1, _ = wl.make_all(cfg, DEV)
     n = n_sub * n_sub
