@@ -347,17 +347,22 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         Qh = Q.cpu().pin_memory()
         dOh = dOut.cpu().pin_memory()
+        # the user-facing handle returns d_query in the query's own dtype
+        # (bf16 for bf16 configs, MSN_FLAG_DQ_QK_DTYPE): half the D2H bytes
+        lk_e = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, cfg.batch,
+                         cfg.qk_dtype, cfg.value_dtype, atomic_bwd=args.atomic, device=dev,
+                         head_groups=cfg.head_groups, group_tables=cfg.group_tables, dq_in_qk_dtype=True)
         out_h = torch.empty((B,) + tuple(cfg.out_shape_tail), dtype=torch.float32).pin_memory()
-        dq_h = torch.empty((B, cfg.heads, 2, cfg.d_half), dtype=torch.float32).pin_memory()
+        dq_h = torch.empty((B, cfg.heads, 2, cfg.d_half), dtype=lk_e.dq_dtype).pin_memory()
         n_e2e = max(3, min(args.steps, 20))
         for _ in range(3):
-            lk.step_host(Qh, dOh, K, V, dK, dV, out_h, dq_h)
+            lk_e.step_host(Qh, dOh, K, V, dK, dV, out_h, dq_h)
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
         for i in range(n_e2e):
             flush.zero_()
             ev[i][0].record(stream)
-            lk.step_host(Qh, dOh, K, V, dK, dV, out_h, dq_h)   # H2D q, dOut; D2H out, dQ
+            lk_e.step_host(Qh, dOh, K, V, dK, dV, out_h, dq_h)   # H2D q, dOut; D2H out, dQ
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         e2e_ms = sum(a.elapsed_time(b) for a, b in ev) / n_e2e
@@ -365,11 +370,11 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         h2d = Qh.numel() * Qh.element_size() + dOh.numel() * dOh.element_size()
-        d2h = out_h.numel() * 4 + dq_h.numel() * 4
+        d2h = out_h.numel() * out_h.element_size() + dq_h.numel() * dq_h.element_size()
         e2e = {"value": lookups / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.item()),
-               "note": "PKMLookup.step_host: pinned host query + d_out in, out + d_query back to pinned host (4 slices, copies on their own streams overlapping the kernels), "
+               "note": "PKMLookup.step_host: pinned host query + d_out in, out + d_query (in the query dtype) back to pinned host (4 slices, copies on their own streams overlapping the kernels), "
                        "forward+backward through msn_pkm_forward/msn_pkm_backward, one sync"}
 
     if rank != 0:

@@ -28,7 +28,8 @@
  *   idx      [B, H, k]   int32      global flat slot ids i*n_sub + j
  *   weights  [B, H, k]   fp32       softmax weights, same order as idx
  *   d_out    [B, d_value] fp32
- *   d_query  [B, H, 2, d_half] fp32            written (=)
+ *   d_query  [B, H, 2, d_half] fp32            written (=)  (qk_dtype with
+ *            MSN_FLAG_DQ_QK_DTYPE)
  *   d_subkeys[H, 2, n_sub, d_half] fp32        accumulated (+=)
  *   d_values [row_end-row_begin, d_value] fp32 accumulated (+=)
  *   dw       [B, H, k] fp32   d loss / d weights (local rows only when sharded)
@@ -88,6 +89,10 @@ typedef enum { MSN_UPDATE_SGD = 1, MSN_UPDATE_ADAGRAD = 2 } msn_update;
                                       values hold G * n_sub^2 rows, group g's
                                       slots at rows g*n_sub^2 + i*n_sub + j, and
                                       idx reports those global rows */
+#define MSN_FLAG_DQ_QK_DTYPE 0x4u /* d_query written in qk_dtype (bf16 for bf16
+                                     configs, rounded once, RNE) instead of fp32:
+                                     the gradient in the query's own dtype, half
+                                     the bytes (e.g. for a host copy) */
 
 typedef struct msn_pkm* msn_pkm_t;
 

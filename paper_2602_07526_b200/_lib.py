@@ -16,6 +16,7 @@ ABI_VERSION = 1
 MSN_F32, MSN_BF16 = 0, 1
 FLAG_ATOMIC_BWD = 0x1
 FLAG_GROUP_TABLES = 0x2
+FLAG_DQ_QK_DTYPE = 0x4
 GATES = {"tanh": 1, "sigmoid": 2, "identity": 3}  # msn_gate (include/msn_pkm.h)
 UPDATES = {"sgd": 1, "adagrad": 2}                # msn_update
 

@@ -56,6 +56,7 @@ Shape shape_of(const msn_pkm_config& c, int64_t B) {
   s.row_end = c.row_end;
   s.og = c.head_groups > 1 ? c.head_groups : 1;
   s.tab_stride = (c.flags & MSN_FLAG_GROUP_TABLES) ? (int64_t)c.n_sub * c.n_sub : 0;
+  s.dq_bf16 = (c.flags & MSN_FLAG_DQ_QK_DTYPE) && c.qk_dtype == MSN_BF16;
   return s;
 }
 
@@ -165,7 +166,7 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
   if (c->d_value < 1 || (c->d_value * vsz) % 16)
     return fail(MSN_ERR_INVALID_ARG, "d_value * sizeof(value) must be a multiple of 16 bytes");
   if (c->max_batch < 0) return fail(MSN_ERR_INVALID_ARG, "max_batch < 0");
-  if (c->flags & ~(MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES))
+  if (c->flags & ~(MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES | MSN_FLAG_DQ_QK_DTYPE))
     return fail(MSN_ERR_INVALID_ARG, "unknown flags");
   const int G = c->head_groups > 1 ? c->head_groups : 1;
   if (c->head_groups < 0 || c->heads % G)

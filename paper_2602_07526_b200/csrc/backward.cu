@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     uint32_t* __restrict__ cnt,
                                                     uint32_t* __restrict__ rank,
                                                     uint16_t* __restrict__ dSd, int hg,
-                                                    int32_t tab_stride) {
+                                                    int32_t tab_stride, bool dq_bf16) {
   pdl_enter();
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   __shared__ int32_t s_r[8][64];
@@ -1015,9 +1015,15 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
         }
     }
     __syncwarp();
-    float* o = dQ + (l * 2 + half) * d_h + lane * EPL;
+    if (dq_bf16) {  // MSN_FLAG_DQ_QK_DTYPE: one RNE rounding
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dQ) + (l * 2 + half) * d_h + lane * EPL;
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) o[i] = acc[i];
+      for (int i = 0; i < EPL; ++i) o[i] = __float2bfloat16_rn(acc[i]);
+    } else {
+      float* o = dQ + (l * 2 + half) * d_h + lane * EPL;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) o[i] = acc[i];
+    }
   }
 }
 
@@ -1206,15 +1212,15 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   if (dense && dq_tc)                                                                          \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, true, false>, blocks, 256, 0, st,                             \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride);                 \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16);                 \
   else if (dense)                                                                              \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, true, true>, blocks, 256, 0, st,                              \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride);                 \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16);                 \
   else                                                                                         \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, false, true>, blocks, 256, 0, st,                             \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride)
+        g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16)
 #define DSDQ_E(QT, KPL)                                                                        \
   switch (E) { case 1: DSDQ(QT, KPL, 1); break; case 2: DSDQ(QT, KPL, 2); break;              \
     case 4: DSDQ(QT, KPL, 4); break; case 8: DSDQ(QT, KPL, 8); break;                          \

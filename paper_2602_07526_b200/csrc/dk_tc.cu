@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 struct DqParams {
   int64_t B;
   int H, n_sub, d_h;
-  float* dQ;  // [B, H*2, d_h]
+  float* dQ;  // [B, H*2, d_h] (bf16 when bf16_out)
+  int bf16_out = 0;
 };
 
 // Persistent: one CTA per SM walks the (query tile, head.half) tiles in
@@ -302,16 +303,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + buf * p.d_h;
       const int64_t b = (int64_t)m0 + row;
-      float* dst = p.dQ + (b * (2 * p.H) + hh) * (int64_t)p.d_h;
+      const int64_t qoff = (b * (2 * p.H) + hh) * (int64_t)p.d_h;
       for (int c0 = ch * cw; c0 < (ch + 1) * cw; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(lane_base + c0, r);
         if (b < p.B) {
-          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+          if (p.bf16_out) {  // MSN_FLAG_DQ_QK_DTYPE: one RNE rounding, 16 B stores
+            uint4* d8 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.dQ) + qoff + c0);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            for (int j = 0; j < 4; ++j) {
+              uint32_t w[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 2 * t]),
+                                                               __uint_as_float(r[8 * j + 2 * t + 1]));
+                w[t] = *reinterpret_cast<const uint32_t*>(&v);
+              }
+              d8[j] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            float4* d4 = reinterpret_cast<float4*>(p.dQ + qoff + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          }
         }
       }
       tc_fence_before();
@@ -463,7 +479,7 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-    DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ};
+    DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ, s.dq_bf16 ? 1 : 0};
     static bool qattr = false;
     if (!qattr) {
       cudaError_t e0 = cudaFuncSetAttribute(dq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

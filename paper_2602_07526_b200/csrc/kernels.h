@@ -16,6 +16,7 @@ struct Shape {
   int64_t row_begin, row_end;  // local value rows
   int og = 1;                  // output head groups: out [B, og, d_v]
   int64_t tab_stride = 0;      // per-group tables: group g's rows start at g * tab_stride
+  bool dq_bf16 = false;        // d_query written in bf16 (MSN_FLAG_DQ_QK_DTYPE, bf16 configs)
 };
 
 // Per-half candidate lists, the hand-off between a1+a2 and a3: for every

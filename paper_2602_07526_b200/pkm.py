@@ -40,10 +40,13 @@ class PKMLookup:
     def __init__(self, heads: int, n_sub: int, d_half: int, d_value: int, k: int,
                  max_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
                  atomic_bwd: bool = False, row_begin: int = 0, row_end: Optional[int] = None,
-                 device=None, head_groups: int = 1, group_tables: bool = False):
+                 device=None, head_groups: int = 1, group_tables: bool = False,
+                 dq_in_qk_dtype: bool = False):
         """head_groups G > 1: consecutive blocks of heads/G
         heads form a group (a token with its own codebooks); out is [B, G, d_v].
-        group_tables: every group has its own table (values [G*n_sub^2, d_v])."""
+        group_tables: every group has its own table (values [G*n_sub^2, d_v]).
+        dq_in_qk_dtype: d_query comes back in the query dtype (bf16 for bf16
+        configs; MSN_FLAG_DQ_QK_DTYPE) instead of fp32."""
         self.lib = _lib.load()
         self.heads, self.n_sub, self.d_half, self.d_value, self.k = heads, n_sub, d_half, d_value, k
         self.max_batch = max_batch
@@ -53,7 +56,9 @@ class PKMLookup:
         self.row_begin = row_begin
         self.row_end = self.table_rows if row_end is None else row_end
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        flags = (_lib.FLAG_ATOMIC_BWD if atomic_bwd else 0) | (_lib.FLAG_GROUP_TABLES if group_tables else 0)
+        flags = (_lib.FLAG_ATOMIC_BWD if atomic_bwd else 0) | (_lib.FLAG_GROUP_TABLES if group_tables else 0) \
+            | (_lib.FLAG_DQ_QK_DTYPE if dq_in_qk_dtype else 0)
+        self.dq_dtype = qk_dtype if (dq_in_qk_dtype and qk_dtype == torch.bfloat16) else torch.float32
         cfg = _lib.Config(_lib.ABI_VERSION, heads, n_sub, d_half, d_value, k, max_batch,
                           _DT[qk_dtype], _DT[value_dtype], flags, self.head_groups,
                           self.row_begin, self.row_end)
@@ -244,7 +249,7 @@ class PKMLookup:
             d_subkeys = torch.zeros((self.heads, 2, self.n_sub, self.d_half), dtype=torch.float32, device=self.device)
         if d_values is None:
             d_values = torch.zeros((self.row_end - self.row_begin, self.d_value), dtype=torch.float32, device=self.device)
-        d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=self.device)
+        d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=self.dq_dtype, device=self.device)
         dw = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
         ws = self.workspace(B)
         _lib.check(self.lib.msn_pkm_backward(self._h, _stream(), B, _ptr(d), _ptr(q), _ptr(K), _ptr(V),
@@ -306,7 +311,7 @@ class PKMLookup:
         B = q.shape[0]
         if d_subkeys is None:
             d_subkeys = torch.zeros((self.heads, 2, self.n_sub, self.d_half), dtype=torch.float32, device=self.device)
-        d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=self.device)
+        d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=self.dq_dtype, device=self.device)
         ws = self.workspace(B)
         _lib.check(self.lib.msn_pkm_backward_keys(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(idx), _ptr(w),
                                                   _ptr(dw), _ptr(d_query), _ptr(d_subkeys), _ptr(ws), ws.numel()))
@@ -330,7 +335,7 @@ class PKMLookup:
         if out_h is None:
             out_h = torch.empty(self._out_shape(B), dtype=torch.float32).pin_memory()
         if d_query_h is None:
-            d_query_h = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32).pin_memory()
+            d_query_h = torch.empty((B, self.heads, 2, self.d_half), dtype=self.dq_dtype).pin_memory()
         if chunks is None:
             # measured on the B200 (C2): 4 slices 1.03 ms, 8: 1.16 ms, 16: 2.18 ms
             # (host launch cost per slice); MSN_HOST_CHUNKS overrides
@@ -343,7 +348,7 @@ class PKMLookup:
         out = torch.empty(self._out_shape(B), dtype=torch.float32, device=dev)
         idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=dev)
         w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=dev)
-        dq = torch.empty((B, self.heads, 2, self.d_half), dtype=torch.float32, device=dev)
+        dq = torch.empty((B, self.heads, 2, self.d_half), dtype=self.dq_dtype, device=dev)
         dw = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=dev)
         step = (B + chunks - 1) // chunks
         ws = self.workspace(min(B, step))

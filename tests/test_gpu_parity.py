@@ -681,3 +681,21 @@ def test_random_shapes_fwd_bwd(shape):
     Q, K, V, dOut = wl.make_all(cfg, DEV)
     res = run_fwd_bwd(cfg, Q, K, V, dOut)
     check_all(cfg, Q, K, V, dOut, res)
+
+
+@pytest.mark.parametrize("name", ["c2_mid_bf16", "c4_large_sharded_bf16"])
+def test_dq_in_query_dtype(name):
+    """MSN_FLAG_DQ_QK_DTYPE: d_query comes back in bf16, the fp32 result rounded
+    once (RNE) -- on the tensor-core dQ path (C2) and the per-lookup dQ of
+    long codebooks (C4)."""
+    cfg = wl.CONFIGS[name].scaled(batch=300)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    lk16 = lookup_for(cfg, dq_in_qk_dtype=True)
+    out, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, dw = lk.backward(dOut, Q, K, V, idx, w)
+    dq16, dK16, dV16, dw16 = lk16.backward(dOut, Q, K, V, idx, w)
+    torch.cuda.synchronize()
+    assert dq16.dtype == torch.bfloat16
+    assert torch.equal(dq16, dq.to(torch.bfloat16))
+    assert torch.equal(dK16, dK) and torch.equal(dV16, dV) and torch.equal(dw16, dw)
