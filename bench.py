@@ -374,7 +374,7 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": lookups / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.item()),
-               "note": "PKMLookup.step_host: pinned host query + d_out in, out + d_query (in the query dtype) back to pinned host (4 slices, copies on their own streams overlapping the kernels), "
+               "note": "PKMLookup.step_host: pinned host query + d_out in, out + d_query (in the query dtype) back to pinned host (2 slices, copies on their own streams overlapping the kernels), "
                        "forward+backward through msn_pkm_forward/msn_pkm_backward, one sync"}
 
     if rank != 0:

@@ -324,7 +324,7 @@ class PKMLookup:
         and the upstream gradient (pinned host tensors), a1-a8 on the device
         (d_subkeys/d_values device buffers accumulated), D2H copies of out and
         d_query into pinned host tensors, one synchronisation at the end.
-        The batch runs as `chunks` consecutive slices (default: 4 when every
+        The batch runs as `chunks` consecutive slices (default: 2 when every
         slice keeps >= 1024 queries) so that the copies overlap the kernels:
         H2D of slice c+1 and D2H of slice c-1 on their own streams while the
         compute stream runs slice c.  The library calls stay in one fixed
@@ -337,9 +337,10 @@ class PKMLookup:
         if d_query_h is None:
             d_query_h = torch.empty((B, self.heads, 2, self.d_half), dtype=self.dq_dtype).pin_memory()
         if chunks is None:
-            # measured on the B200 (C2): 4 slices 1.03 ms, 8: 1.16 ms, 16: 2.18 ms
-            # (host launch cost per slice); MSN_HOST_CHUNKS overrides
-            chunks = int(os.environ.get("MSN_HOST_CHUNKS", "0")) or (4 if B >= 4 * 1024 else 1)
+            # measured on the B200 (C2, bf16 d_query): 2 slices 0.78 ms, 3: 0.82,
+            # 4: 0.84, 6: 1.00 (a slice of B/n queries costs more than 1/n of the
+            # whole batch's kernels); MSN_HOST_CHUNKS overrides
+            chunks = int(os.environ.get("MSN_HOST_CHUNKS", "0")) or (2 if B >= 2 * 1024 else 1)
         chunks = max(1, min(chunks, B)) if B > 0 else 1
         dev = self.device
         q = torch.empty(query_h.shape, dtype=query_h.dtype, device=dev)

@@ -586,7 +586,7 @@ def test_step_host_pipelined_matches_device():
     dq, dK, dV, _ = lk.backward(dOut, Q, K, V, idx, w)
     dK2 = torch.zeros_like(dK)
     dV2 = torch.zeros_like(dV)
-    out_h, dq_h = lk.step_host(Q.cpu().pin_memory(), dOut.cpu().pin_memory(), K, V, dK2, dV2)
+    out_h, dq_h = lk.step_host(Q.cpu().pin_memory(), dOut.cpu().pin_memory(), K, V, dK2, dV2, chunks=4)
     assert torch.equal(out_h, out.cpu()) and torch.equal(dq_h, dq.cpu())
     torch.testing.assert_close(dV2, dV, rtol=1e-5, atol=1e-7)
     torch.testing.assert_close(dK2, dK, rtol=1e-4, atol=1e-6)
