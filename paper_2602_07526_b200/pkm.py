@@ -361,22 +361,26 @@ class PKMLookup:
             st.wait_stream(main)
         sc = ctypes.c_void_p(s_comp.cuda_stream)
         spans = [(c0, min(B, c0 + step)) for c0 in range(0, B, step)] if B > 0 else []
-        ev_in = []
+        ev_q, ev_d = [], []
         with torch.cuda.stream(s_in):
-            for c0, c1 in spans:
+            for c0, c1 in spans:  # the slice's query first (its forward needs only that)
                 q[c0:c1].copy_(query_h[c0:c1], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_in)
+                ev_q.append(e)
                 d[c0:c1].copy_(d_out_h[c0:c1], non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(s_in)
-                ev_in.append(e)
-        for (c0, c1), e in zip(spans, ev_in):
+                ev_d.append(e)
+        for (c0, c1), eq, ed in zip(spans, ev_q, ev_d):
             n = c1 - c0
-            s_comp.wait_event(e)
+            s_comp.wait_event(eq)
             _lib.check(self.lib.msn_pkm_forward(self._h, sc, n, _ptr(q[c0:c1]), _ptr(subkeys), _ptr(values),
                                                 _ptr(out[c0:c1]), _ptr(idx[c0:c1]), _ptr(w[c0:c1]),
                                                 _ptr(ws), ws.numel()))
             e_f = torch.cuda.Event()
             e_f.record(s_comp)
+            s_comp.wait_event(ed)
             _lib.check(self.lib.msn_pkm_backward(self._h, sc, n, _ptr(d[c0:c1]), _ptr(q[c0:c1]), _ptr(subkeys),
                                                  _ptr(values), _ptr(idx[c0:c1]), _ptr(w[c0:c1]), _ptr(dq[c0:c1]),
                                                  _ptr(d_subkeys), _ptr(d_values), _ptr(dw[c0:c1]),
