@@ -94,18 +94,21 @@ __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
 // MSN_SELECT_TS builds (profiling only): globaltimer stamps per CTA at the
 // epilogue's phase boundaries (warp 4, lane 0), summarised by tools/select_ts.py.
 #ifdef MSN_SELECT_TS
-__device__ unsigned long long g_sel_ts[65536 * 8];
+__device__ unsigned long long g_sel_ts[65536 * 16];
+#define SEL_TS_ANY(i)                                                               \
+  do {                                                                              \
+    unsigned long long t_;                                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+    const int c_ = blockIdx.y * gridDim.x + blockIdx.x;                             \
+    if (c_ < 65536) g_sel_ts[c_ * 16 + (i)] = t_;                                   \
+  } while (0)
 #define SEL_TS(i)                                                                   \
   do {                                                                              \
-    if (threadIdx.x == 32 * kEpiWarp0) {                                            \
-      unsigned long long t_;                                                        \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
-      const int c_ = blockIdx.y * gridDim.x + blockIdx.x;                           \
-      if (c_ < 65536) g_sel_ts[c_ * 8 + (i)] = t_;                                  \
-    }                                                                               \
+    if (threadIdx.x == 32 * kEpiWarp0) SEL_TS_ANY(i);                               \
   } while (0)
 #else
 #define SEL_TS(i) do {} while (0)
+#define SEL_TS_ANY(i) do {} while (0)
 #endif
 
 struct TcParams {
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpiWarps);
     }
-    mbar_init(a_ready, 4);
+    mbar_init(a_ready, kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -206,7 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = TF32 ? idesc_tf32(128, p.n_tile) : idesc_bf16(128, p.n_tile);
       mbar_wait(a_full, 0);
+      SEL_TS_ANY(14);
       if (TF32) mbar_wait(a_ready, 0);
+      SEL_TS_ANY(15);
       tc_fence_after();
       int it = 0;
       for (int g = 0; g < total_chunks; ++g) {
@@ -254,26 +259,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TF32 two-sweep rows: margin d = 2^-8 ||q_row|| max_i ||k_i|| on the
     // 1xTF32 first sweep (see the header); ||q|| from the split below, shared
     // through the end of the (not yet used) candidate area
-    float* qn = reinterpret_cast<float*>(cand + kCap * kCStride) - 128;
-    float kmax = 0.f;
-    if constexpr (TF32 && WIDE) {
-      for (int i = threadIdx.x - 32 * kEpiWarp0; i < p.n_sub; i += 32 * kEpiWarps)
-        kmax = fmaxf(kmax, p.knorm[(int64_t)hh * p.n_sub + i]);
-      kmax = warp_max(kmax);
-      if (lane == 0) cnts[ew] = __float_as_int(kmax);
-      epi_bar();
-      kmax = 0.f;
-#pragma unroll
-      for (int i = 0; i < kEpiWarps; ++i) kmax = fmaxf(kmax, __int_as_float(cnts[i]));
-    }
+    float* qn = reinterpret_cast<float*>(cand + kCap * kCStride) - 256;  // [2][128]
     if constexpr (TF32) {
-      if (sh == 0) {
+      {
         // split this row of the resident query tile: hi (TF32-exact) back into
-        // shared memory in place, lo = x - hi into TMEM columns [alo_col, +d_h)
+        // shared memory in place, lo = x - hi into TMEM columns [alo_col, +d_h);
+        // the two warps of a lane quarter take alternate k-blocks
         mbar_wait(a_full, 0);
         const int sw = row & 7;
         float qq = 0.f;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = sh; kb < p.k_blocks; kb += 2) {
           float* arow = reinterpret_cast<float*>(sA + kb * 16384 + row * kRowBytes);
           uint32_t lo[32];
 #pragma unroll
@@ -290,13 +285,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_st32(lane_base + alo_col + kb * BK, lo);
         }
-        if (WIDE) qn[row] = qq;
+        if (WIDE) qn[sh * 128 + row] = qq;  // the two halves of ||q||^2, added at tau
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_ready);
       }
+    }
+    float kmax = 0.f;
+    if constexpr (TF32 && WIDE) {
+      for (int i = threadIdx.x - 32 * kEpiWarp0; i < p.n_sub; i += 32 * kEpiWarps)
+        kmax = fmaxf(kmax, p.knorm[(int64_t)hh * p.n_sub + i]);
+      kmax = warp_max(kmax);
+      if (lane == 0) cnts[ew] = __float_as_int(kmax);
+      epi_bar();
+      kmax = 0.f;
+#pragma unroll
+      for (int i = 0; i < kEpiWarps; ++i) kmax = fmaxf(kmax, __int_as_float(cnts[i]));
     }
     // A segment = nseg consecutive chunks starting at global chunk g0, resident
     // in the TMEM buffers (g0 + u) & 1.  This thread owns the 32-column pieces
@@ -371,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       for (int c = 0; c < p.n_chunks; ++c) {
         wait_chunks(c, 1);
+        if (c < 7) SEL_TS(7 + c);
         pass_a(c, p.n_tile);
         release_chunks(c, 1);
       }
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (TF32 && WIDE) {
       // ||q||^2 summed in fp32 (relative error < 2^-17 for d_h <= 128): x 1.001
       // makes sqrt an upper bound; the margin itself has 2x slack (2^-8 vs 2^-9)
-      const float d = 0x1p-8f * __fsqrt_ru(qn[row] * 1.001f) * kmax;
+      const float d = 0x1p-8f * __fsqrt_ru((qn[row] + qn[128 + row]) * 1.001f) * kmax;
       tau = __fsub_rd(tau, d);
     }
     epi_bar();  // exchange read everywhere before the candidate area is written
@@ -611,11 +618,11 @@ cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& 
 
 }  // namespace
 
-// Profiling builds only: copies the per-CTA stamps (8 per CTA) to host.
+// Profiling builds only: copies the per-CTA stamps (16 per CTA) to host.
 extern "C" int msn_select_ts_dump(unsigned long long* host, int n) {
 #ifdef MSN_SELECT_TS
   cudaDeviceSynchronize();
-  return cudaMemcpyFromSymbol(host, g_sel_ts, sizeof(unsigned long long) * (size_t)n * 8) == cudaSuccess ? n : -1;
+  return cudaMemcpyFromSymbol(host, g_sel_ts, sizeof(unsigned long long) * (size_t)n * 16) == cudaSuccess ? n : -1;
 #else
   (void)host; (void)n;
   return -1;
