@@ -72,10 +72,83 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
   }  // output groups
 }
 
+// Rows of R >= 64 16-byte vectors (e.g. d_v = 512 bf16): WPQ = R / 32 warps
+// per query, each lane one 16-byte vector of every row.  Every output element
+// is still one FMA chain over the query's rows in ascending order, the same
+// additions as gather_kernel's VPL = R / 32 lanes (G = 1) and the fused
+// kernel's: bitwise identical, with WPQ times the warps (small batches,
+// e.g. C5, otherwise leave most SMs idle).
+template <typename VT, int U>
+__global__ void __launch_bounds__(256) gather_wide_kernel(const int32_t* __restrict__ idx,
+                                                          const float* __restrict__ w,
+                                                          const VT* __restrict__ V,
+                                                          float* __restrict__ out, int64_t B, int HK,
+                                                          int d_v, int wpq, int og, Gate gate) {
+  pdl_enter();
+  constexpr int PER = elem<VT>::per16;
+  __shared__ int32_t s_idx[kWarps][kMaxHK];
+  __shared__ float s_w[kWarps][kMaxHK];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qpb = kWarps / wpq;
+  const int64_t b = (int64_t)blockIdx.x * qpb + wid / wpq;
+  if (b >= B) return;
+  const int vec = (wid % wpq) * 32 + lane;  // this lane's 16-byte vector of the row
+  for (int r = lane; r < HK; r += 32) {
+    s_idx[wid][r] = idx[b * HK + r];
+    s_w[wid][r] = w[b * HK + r];
+  }
+  __syncwarp();
+  const int E = HK / og;
+  for (int grp = 0; grp < og; ++grp) {
+    float acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    for (int base = grp * E; base < (grp + 1) * E; base += U) {
+      uint4 x[U];
+      float wt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = base + u;
+        const int f = r < (grp + 1) * E ? s_idx[wid][r] : -1;
+        wt[u] = f >= 0 ? s_w[wid][r] : 0.f;
+        x[u] = f >= 0 ? ldg_nc_v4(V + (int64_t)f * d_v + vec * PER) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float f[PER];
+        unpack16<VT>(x[u], f);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[e] = fmaf(wt[u], f[e], acc[e]);
+      }
+    }
+    const int64_t orow = b * og + grp;
+    float* o = out + orow * d_v + vec * PER;
+#pragma unroll
+    for (int e = 0; e < PER; e += 4) *reinterpret_cast<float4*>(o + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+    if (gate.kind) {
+#pragma unroll
+      for (int e = 0; e < PER; e += 4) {
+        const int64_t off = orow * d_v + vec * PER + e;
+        const float4 xx = *reinterpret_cast<const float4*>(gate.x + off);
+        *reinterpret_cast<float4*>(gate.xt + off) =
+            make_float4(xx.x * gate_g(acc[e], gate.kind), xx.y * gate_g(acc[e + 1], gate.kind),
+                        xx.z * gate_g(acc[e + 2], gate.kind), xx.w * gate_g(acc[e + 3], gate.kind));
+      }
+    }
+  }
+}
+
 template <typename VT>
 cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const VT* V, float* out,
                      cudaStream_t st, const Gate& gate, const Push& push) {
   const int R = s.d_v * (int)sizeof(VT) / 16;
+  if (R >= 64 && R % 32 == 0 && R <= 128 && !push.peers && s.row_begin == 0 &&
+      s.row_end >= (int64_t)s.n_sub * s.n_sub * (s.tab_stride ? s.og : 1)) {
+    const int wpq = R / 32, qpb = kWarps / wpq;
+    launch_pdl(gather_wide_kernel<VT, 16>, (unsigned)((s.B + qpb - 1) / qpb), 256, 0, st, idx, w, V, out, s.B,
+               s.H * s.k, s.d_v, wpq, s.og, gate);
+    return cudaGetLastError();
+  }
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);
 #define GATHER(VPL, G, U)                                                                      \
   launch_pdl(gather_kernel<VT, VPL, G, U>, blocks, 256, 0, st, idx, w, V, out, s.B, s.H, s.k, s.d_v, \

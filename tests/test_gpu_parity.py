@@ -558,7 +558,7 @@ def test_invalid_arguments_raise():
 
 
 @pytest.mark.parametrize("name,B,groups", [("c2_mid_bf16", 8192 + 37, 1), ("c3_train_fp32_zipf", 8192 + 5, 1),
-                                           ("f4_tokens_bf16", 40, 16)])
+                                           ("f4_tokens_bf16", 40, 16), ("c5_latency_bf16", 8192 + 3, 1)])
 def test_fused_forward_matches_phases(name, B, groups):
     """msn_pkm_forward (fused Cartesian + gather for B >= 8192) and the phase
     calls select + gather add in the same order (gather_rows.cuh): bitwise
