@@ -153,8 +153,14 @@ def algorithmic_bytes(cfg, idx=None, update="none"):
     gather = contrib * cfg.d_value * esz + contrib * 8 + out_elems * 4
     out = {"gather": gather}
     if idx is not None:
-        uniq = int(torch.unique(idx).numel())
+        rows, hits = torch.unique(idx, return_counts=True)
+        uniq = int(rows.numel())
         out["unique_rows"] = uniq
+        # SURVEY 8(d) "C3 skew": the workload describes itself
+        top = torch.topk(hits, min(1000, uniq)).values
+        out["skew"] = {"contributions": contrib, "unique_frac": uniq / max(contrib, 1),
+                       "max_hits_one_row": int(hits.max()) if uniq else 0,
+                       "top1000_rows_hit_share": float(top.sum()) / max(contrib, 1)}
         # V rows read once, dV read+written once (fp32), idx/w/dw, dOut once
         out["scatter"] = uniq * cfg.d_value * (esz + 8) + contrib * 12 + out_elems * 4
         if update != "none":  # V read + V written (+ Adagrad state read + written), no dV
@@ -426,6 +432,7 @@ def run_ours(args, rank, world, local_rank):
     kernels["scatter"]["GBps"] = ab["scatter"] / (s_ms / 1e3) / 1e9
     kernels["scatter"]["algorithmic_bytes"] = ab["scatter"]
     kernels["scatter"]["unique_rows"] = ab["unique_rows"]
+    kernels["scatter"]["skew"] = ab["skew"]
     kernels["select"]["TFLOPs"] = ab["select_flops"] / (sel_ms / 1e3) / 1e12
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -447,6 +454,7 @@ def run_ours(args, rank, world, local_rank):
                    "gate": args.gate,
                    "prologue": bool(args.prologue),
                    "update": args.update,
+                   "slot_hits": ab["skew"],
                    "l2": "flushed before every step (512 MiB write, outside the timed events)"},
         "roofline": roof,
         "kernels": kernels,

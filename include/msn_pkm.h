@@ -93,6 +93,13 @@ typedef enum { MSN_UPDATE_SGD = 1, MSN_UPDATE_ADAGRAD = 2 } msn_update;
                                      configs, rounded once, RNE) instead of fp32:
                                      the gradient in the query's own dtype, half
                                      the bytes (e.g. for a host copy) */
+#define MSN_FLAG_VALIDATE 0x8u /* SURVEY 8(b) MSN_VALIDATE: every call that
+                                  consumes a tape (idx, weights) first checks
+                                  it as msn_pkm_validate_tape does, SYNCHRONISES
+                                  the stream, and returns MSN_ERR_INVALID_ARG
+                                  (nothing launched) if any slot is invalid.
+                                  A debugging mode: not graph-capturable; the
+                                  handle then owns a 4-byte device word. */
 
 typedef struct msn_pkm* msn_pkm_t;
 
@@ -288,6 +295,17 @@ msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B,
                                  const int32_t* idx, const float* weights, const float* dw,
                                  float* d_query, float* d_subkeys,
                                  void* workspace, size_t workspace_bytes);
+
+/* Tape check (SURVEY 8(b) "Errors"): *bad (DEVICE int32, written =, zeroed
+ * on the stream first) = the number of slots (b, h, t) of idx / weights
+ * [B, H, k] that are not what a4 produces: idx outside the
+ * lookup's table ([0, n_sub^2), or [g n_sub^2, (g+1) n_sub^2) for head group g
+ * under MSN_FLAG_GROUP_TABLES), an id repeated within one lookup (each copy
+ * counts), or a weight that is not in [0, 1] (NaN included).  Asynchronous,
+ * no host sync, graph-capturable.  The softmax normalisation itself is not
+ * checked. */
+msn_status msn_pkm_validate_tape(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                                 const float* weights, int32_t* bad);
 
 /* Number of kernel launches the last forward/backward/phase call enqueued
  * (for the bench's gpu_launches count). */

@@ -17,6 +17,7 @@ MSN_F32, MSN_BF16 = 0, 1
 FLAG_ATOMIC_BWD = 0x1
 FLAG_GROUP_TABLES = 0x2
 FLAG_DQ_QK_DTYPE = 0x4
+FLAG_VALIDATE = 0x8
 GATES = {"tanh": 1, "sigmoid": 2, "identity": 3}  # msn_gate (include/msn_pkm.h)
 UPDATES = {"sgd": 1, "adagrad": 2}                # msn_update
 
@@ -61,6 +62,7 @@ SIGNATURES = {
     "msn_pkm_gather_push": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _I64],
     "msn_pkm_reduce_partials": [_P, _P, _I64, ctypes.c_int32, _P, _P],
     "msn_pkm_scatter_p2p": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int32, _I64, _P, _SZ],
+    "msn_pkm_validate_tape": [_P, _P, _I64, _P, _P, _P],
     "msn_pkm_scatter": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_backward_keys": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_last_launch_count": [_P],

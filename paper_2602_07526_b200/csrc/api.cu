@@ -1,6 +1,7 @@
 // api.cu -- the C ABI declared in include/msn_pkm.h: validation, workspace
 // carving and launch orchestration on the caller's stream.  No device
-// allocation, no host synchronisation.
+// allocation, no host synchronisation (except under MSN_FLAG_VALIDATE: one
+// 4-byte flag word per handle, and a stream sync per tape check).
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -16,6 +17,8 @@ struct msn_pkm {
   int last_launches;
   cudaEvent_t trace[4];  // optional stage-boundary events (msn_pkm_set_trace_events)
   int ntrace;
+  int32_t* d_bad;  // MSN_FLAG_VALIDATE only: device word + pinned host copy
+  int32_t* h_bad;
 };
 
 namespace {
@@ -87,6 +90,21 @@ msn_status check_batch(msn_pkm_t h, int64_t B) {
     if (!(p)) return fail(MSN_ERR_INVALID_ARG, "%s is NULL", #p);                            \
     if (!aligned16(p)) return fail(MSN_ERR_INVALID_ARG, "%s is not 16-byte aligned", #p);   \
   } while (0)
+
+// MSN_FLAG_VALIDATE: check the tape, synchronise, refuse an invalid one.
+msn_status check_tape(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx, const float* w) {
+  if (!(h->cfg.flags & MSN_FLAG_VALIDATE) || B == 0) return MSN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_validate_tape(shape_of(h->cfg, B), idx, w, h->d_bad, st, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->h_bad, h->d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "tape validation");
+  if (*h->h_bad)
+    return fail(MSN_ERR_INVALID_ARG,
+                "tape: %d invalid slots (idx outside the table, repeated in a lookup, or weight not in [0, 1])",
+                *h->h_bad);
+  return MSN_OK;
+}
 
 // a1 + a2 into per-half candidate lists; then either the Cartesian stage
 // alone (select) or fused with the gather (forward: values != NULL).
@@ -166,7 +184,8 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
   if (c->d_value < 1 || (c->d_value * vsz) % 16)
     return fail(MSN_ERR_INVALID_ARG, "d_value * sizeof(value) must be a multiple of 16 bytes");
   if (c->max_batch < 0) return fail(MSN_ERR_INVALID_ARG, "max_batch < 0");
-  if (c->flags & ~(MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES | MSN_FLAG_DQ_QK_DTYPE))
+  if (c->flags &
+      ~(MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES | MSN_FLAG_DQ_QK_DTYPE | MSN_FLAG_VALIDATE))
     return fail(MSN_ERR_INVALID_ARG, "unknown flags");
   const int G = c->head_groups > 1 ? c->head_groups : 1;
   if (c->head_groups < 0 || c->heads % G)
@@ -185,11 +204,23 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
   h->cfg = *c;
   h->last_launches = 0;
   h->ntrace = 0;
+  h->d_bad = nullptr;
+  h->h_bad = nullptr;
+  if (c->flags & MSN_FLAG_VALIDATE) {
+    cudaError_t e = cudaMalloc(&h->d_bad, sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMallocHost(&h->h_bad, sizeof(int32_t));
+    if (e != cudaSuccess) {
+      msn_pkm_destroy(h);
+      return cuda_fail(e, "MSN_FLAG_VALIDATE flag word");
+    }
+  }
   *out = h;
   return MSN_OK;
 }
 
 msn_status msn_pkm_destroy(msn_pkm_t h) {
+  if (h && h->d_bad) cudaFree(h->d_bad);
+  if (h && h->h_bad) cudaFreeHost(h->h_bad);
   delete h;
   return MSN_OK;
 }
@@ -245,6 +276,7 @@ msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B, const int32_t* i
   REQUIRE_PTR(weights);
   REQUIRE_PTR(values);
   REQUIRE_PTR(out);
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   cudaError_t e = launch_gather(s, idx, weights, values, out, (cudaStream_t)stream,
                                 &h->last_launches);
@@ -268,6 +300,7 @@ msn_status msn_pkm_gather_push(msn_pkm_t h, void* stream, int64_t B, const int32
   REQUIRE_PTR(weights);
   REQUIRE_PTR(values);
   if (!peer_recv) return fail(MSN_ERR_INVALID_ARG, "peer_recv is NULL");
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   Push push;
   push.peers = peer_recv;
@@ -292,6 +325,23 @@ msn_status msn_pkm_reduce_partials(msn_pkm_t h, void* stream, int64_t local_batc
   cudaError_t e = launch_reduce_partials(recv, world, local_batch, s.og, s.d_v, out, (cudaStream_t)stream,
                                          &h->last_launches);
   if (e != cudaSuccess) return cuda_fail(e, "reduce_partials");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_validate_tape(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
+                                 const float* weights, int32_t* bad) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
+  if (!bad) return fail(MSN_ERR_INVALID_ARG, "bad is NULL");
+  if (B > 0) {
+    REQUIRE_PTR(idx);
+    REQUIRE_PTR(weights);
+  }
+  cudaError_t e = launch_validate_tape(shape_of(h->cfg, B), idx, weights, bad, (cudaStream_t)stream,
+                                       &h->last_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "validate_tape");
   return MSN_OK;
 }
 
@@ -393,6 +443,7 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* 
   REQUIRE_PTR(values);
   REQUIRE_PTR(d_values);
   REQUIRE_PTR(dw);
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   cudaStream_t cs = (cudaStream_t)stream;
   cudaError_t e;
@@ -431,6 +482,7 @@ msn_status msn_pkm_scatter_p2p(msn_pkm_t h, void* stream, int64_t B, const int32
   REQUIRE_PTR(d_values);
   REQUIRE_PTR(workspace);
   if (!peer_d_out || !peer_dw) return fail(MSN_ERR_INVALID_ARG, "peer_d_out / peer_dw is NULL");
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
   if (workspace_bytes < need)
@@ -468,6 +520,7 @@ msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const in
   REQUIRE_PTR(dw);
   REQUIRE_PTR(workspace);
   if (update == MSN_UPDATE_ADAGRAD) REQUIRE_PTR(state);
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
   if (workspace_bytes < need)
@@ -498,6 +551,7 @@ msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B, const voi
   REQUIRE_PTR(d_query);
   REQUIRE_PTR(d_subkeys);
   REQUIRE_PTR(workspace);
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(s, B);
   if (workspace_bytes < need)
@@ -533,6 +587,7 @@ msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B, const float* d
   REQUIRE_PTR(d_subkeys);
   REQUIRE_PTR(d_values);
   REQUIRE_PTR(workspace);
+  if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(s, B);
   if (workspace_bytes < need)

@@ -91,6 +91,10 @@ cudaError_t launch_reduce_partials(const float* recv, int world, int64_t lb, int
                                    float* out, cudaStream_t st, int* launches);
 
 // f1 backward: dx = dxt (.) g(v_o) (=), dvo = dxt (.) x (.) g'(v_o) (=).
+// validate.cu: *bad = number of invalid tape slots (range, duplicates, weight
+// not in [0, 1]); zeroes *bad first.
+cudaError_t launch_validate_tape(const Shape& s, const int32_t* idx, const float* w, int32_t* bad,
+                                 cudaStream_t st, int* launches);
 cudaError_t launch_gate_backward(int64_t B, int d_v, int kind, const float* x, const float* vo,
                                  const float* dxt, float* dx, float* dvo, cudaStream_t st,
                                  int* launches);

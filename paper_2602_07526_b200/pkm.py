@@ -41,12 +41,14 @@ class PKMLookup:
                  max_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
                  atomic_bwd: bool = False, row_begin: int = 0, row_end: Optional[int] = None,
                  device=None, head_groups: int = 1, group_tables: bool = False,
-                 dq_in_qk_dtype: bool = False):
+                 dq_in_qk_dtype: bool = False, validate: bool = False):
         """head_groups G > 1: consecutive blocks of heads/G
         heads form a group (a token with its own codebooks); out is [B, G, d_v].
         group_tables: every group has its own table (values [G*n_sub^2, d_v]).
         dq_in_qk_dtype: d_query comes back in the query dtype (bf16 for bf16
-        configs; MSN_FLAG_DQ_QK_DTYPE) instead of fp32."""
+        configs; MSN_FLAG_DQ_QK_DTYPE) instead of fp32.
+        validate: every call that consumes a tape checks it first and raises
+        on an invalid one (MSN_FLAG_VALIDATE; synchronises the stream)."""
         self.lib = _lib.load()
         self.heads, self.n_sub, self.d_half, self.d_value, self.k = heads, n_sub, d_half, d_value, k
         self.max_batch = max_batch
@@ -57,7 +59,7 @@ class PKMLookup:
         self.row_end = self.table_rows if row_end is None else row_end
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         flags = (_lib.FLAG_ATOMIC_BWD if atomic_bwd else 0) | (_lib.FLAG_GROUP_TABLES if group_tables else 0) \
-            | (_lib.FLAG_DQ_QK_DTYPE if dq_in_qk_dtype else 0)
+            | (_lib.FLAG_DQ_QK_DTYPE if dq_in_qk_dtype else 0) | (_lib.FLAG_VALIDATE if validate else 0)
         self.dq_dtype = qk_dtype if (dq_in_qk_dtype and qk_dtype == torch.bfloat16) else torch.float32
         cfg = _lib.Config(_lib.ABI_VERSION, heads, n_sub, d_half, d_value, k, max_batch,
                           _DT[qk_dtype], _DT[value_dtype], flags, self.head_groups,
@@ -208,6 +210,15 @@ class PKMLookup:
         _lib.check(self.lib.msn_pkm_select(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(idx),
                                            _ptr(w), _ptr(ws), ws.numel()))
         return idx, w
+
+    def validate_tape(self, idx: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        """Number of invalid slots of the tape (idx outside the lookup's table,
+        repeated within a lookup, weight not in [0, 1]) as a device int32 tensor."""
+        idx, w = self._dev(idx), self._dev(w)
+        bad = torch.empty(1, dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.msn_pkm_validate_tape(self._h, _stream(), idx.shape[0], _ptr(idx), _ptr(w),
+                                                  _ptr(bad)))
+        return bad
 
     def gather(self, idx: torch.Tensor, w: torch.Tensor, values: torch.Tensor) -> torch.Tensor:
         """a5 over this process's rows (rows of other shards contribute 0)."""

@@ -557,6 +557,44 @@ def test_invalid_arguments_raise():
         lk.forward(big, K, V)
 
 
+@pytest.mark.parametrize("name,groups,tables", [("c2_mid_bf16", 1, False), ("f4_tokens_pertable_bf16", 16, True)])
+def test_validate_tape(name, groups, tables):
+    """msn_pkm_validate_tape counts exactly the corrupted slots (SURVEY 8(b)
+    "Errors"); with MSN_FLAG_VALIDATE a consumer of a bad tape raises before
+    launching, and a good tape gives the unvalidated results bitwise."""
+    from paper_2602_07526_b200._lib import MsnError
+    cfg = wl.CONFIGS[name].scaled(batch=300)
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    kw = dict(head_groups=groups, group_tables=tables)
+    lk = lookup_for(cfg, **kw)
+    lv = lookup_for(cfg, validate=True, **kw)
+    out, idx, w = lk.forward(Q, K, V)
+    assert int(lk.validate_tape(idx, w).item()) == 0
+    n2 = cfg.n_sub * cfg.n_sub
+    bad_i, bad_w = idx.clone(), w.clone()
+    bad_i[0, 0, 0] = -1                    # below the table
+    bad_i[1, 1, 3] = n2 * groups           # past the last table row
+    bad_i[2, 0, 5] = bad_i[2, 0, 4]        # repeated id: both copies count
+    bad_w[3, 0, 0] = float("nan")
+    bad_w[4, 1, 2] = -0.25
+    expect = 1 + 1 + 2 + 1 + 1
+    if tables:                             # head 0 (group 0) pointing into group 1's table
+        bad_i[5, 0, 1] = bad_i[5, 0, 1] % n2 + n2
+        expect += 1
+    assert int(lk.validate_tape(bad_i, bad_w).item()) == expect
+    assert int(lk.validate_tape(idx, bad_w).item()) == 2
+    with pytest.raises(MsnError, match="INVALID_ARG"):
+        lv.backward(dOut, Q, K, V, bad_i, w)
+    with pytest.raises(MsnError, match="INVALID_ARG"):
+        lv.gather(idx, bad_w, V)
+    r0 = lk.backward(dOut, Q, K, V, idx, w)
+    r1 = lv.backward(dOut, Q, K, V, idx, w)
+    torch.cuda.synchronize()
+    for a, b in zip(r0, r1):
+        assert torch.equal(a, b)
+    assert torch.equal(lv.gather(idx, w, V), lk.gather(idx, w, V))
+
+
 @pytest.mark.parametrize("name,B,groups", [("c2_mid_bf16", 8192 + 37, 1), ("c3_train_fp32_zipf", 8192 + 5, 1),
                                            ("f4_tokens_bf16", 40, 16), ("c5_latency_bf16", 8192 + 3, 1)])
 def test_fused_forward_matches_phases(name, B, groups):
