@@ -176,6 +176,57 @@ def test_full_size_invariants(name):
                      parity.rtol_for(cfg.value_dtype), (~aff).reshape(-1), "dw (sampled)")
 
 
+@pytest.mark.parametrize("name", ["f4_tokens_bf16", "f4_tokens_pertable_bf16"])
+def test_f4_full_size(name):
+    """SURVEY 8(f) f4 at its bench size (2048 queries x 16 tokens, n = 256^2,
+    d_v = 512; shared table or 16 per-token tables): invariants over every
+    lookup, plus sampled queries recomputed per token by the fp64 oracle."""
+    from oracle import oracle as orc
+    cfg = wl.CONFIGS[name]
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    G, n = cfg.head_groups, cfg.n_sub * cfg.n_sub
+    lk = lookup_for(cfg, head_groups=G, group_tables=cfg.group_tables)
+    out, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, dw = lk.backward(dOut, Q, K, V, idx, w)
+    torch.cuda.synchronize()
+    assert tuple(out.shape) == (cfg.batch, G, cfg.d_value)
+    assert torch.allclose(w.double().sum(-1), torch.ones(1, dtype=torch.float64, device=DEV), atol=1e-6)
+    assert (w[..., 1:] <= w[..., :-1] + 1e-7).all()
+    s = torch.sort(idx, dim=-1).values
+    assert (s[..., 1:] != s[..., :-1]).all()
+    hg = cfg.heads // G
+    grp = (torch.arange(cfg.heads, device=DEV) // hg).view(1, -1, 1)
+    lo = grp * n if cfg.group_tables else torch.zeros_like(grp)
+    assert (idx >= lo).all() and (idx < lo + n).all()
+    # sum over rows of dV = (H/G) * sum over b, g of dOut[b, g]  (sum_t w = 1)
+    lhs = dV.double().sum(0)
+    rhs = hg * dOut.double().sum((0, 1))
+    assert torch.allclose(lhs, rhs, rtol=1e-4, atol=1e-3 * float(rhs.abs().max()))
+    touched = torch.zeros(cfg.n_slots, dtype=torch.bool, device=DEV)
+    touched[idx.reshape(-1).long()] = True
+    assert (dV[~touched] == 0).all()
+    sel = torch.arange(0, cfg.batch, cfg.batch // 16, device=DEV)[:16]
+    rt = parity.rtol_for(cfg.value_dtype)
+    Qs, Kc, Vc, Ds = Q[sel].cpu(), K.cpu(), V.cpu(), dOut[sel].cpu()
+    for g in range(G):
+        hs = slice(g * hg, (g + 1) * hg)
+        Vg = Vc[g * n:(g + 1) * n] if cfg.group_tables else Vc
+        off = g * n if cfg.group_tables else 0
+        o = orc.forward(Qs[:, hs].contiguous(), Kc[hs].contiguous(), Vg, cfg.k)
+        ig = idx[sel][:, hs].cpu().numpy().astype(np.int64) - off
+        aff, _ = parity.compare_selection(Qs[:, hs].contiguous(), Kc[hs].contiguous(), ig, o, cfg.n_sub)
+        ok = ~aff.any(axis=1)
+        parity.row_close(out[sel][:, g].cpu().numpy(), o["out"], rt, ok, f"out token {g} (sampled)")
+        bw = orc.backward(Qs[:, hs].contiguous(), Kc[hs].contiguous(), Vg, o["idx"], Ds[:, g].contiguous(),
+                          want_dense_dv=False)
+        parity.row_close(dw[sel][:, hs].cpu().numpy().reshape(-1, cfg.k), bw["dw"].reshape(-1, cfg.k), rt,
+                         np.repeat(ok, hg), f"dw token {g} (sampled)")
+        absq, _ = parity.grad_key_magnitudes(Qs[:, hs].contiguous(), Kc[hs].contiguous(), o, bw, cfg.n_sub)
+        parity.row_close(dq[sel][:, hs].cpu().numpy().reshape(-1, cfg.d_half), bw["dQ"].reshape(-1, cfg.d_half),
+                         rt, np.repeat(np.repeat(ok, hg), 2), f"dQ token {g} (sampled)",
+                         absmag=absq.reshape(-1, cfg.d_half))
+
+
 # ------------------------------------------- memory-gated fusion (f1) ----
 @pytest.mark.parametrize("gate", ["tanh", "sigmoid", "identity"])
 @pytest.mark.parametrize("name,B", [("tiny_fp32", 300), ("c2_mid_bf16", 512), ("c3_train_fp32_zipf", 8192)])
