@@ -35,6 +35,12 @@ namespace msn {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+#ifndef MSN_CART_TAU_STEPS
+#define MSN_CART_TAU_STEPS 3  // counted interpolation steps on tau (see the header)
+#endif
+// ... in the standalone Cartesian kernel only: in the fused Cartesian +
+// gather kernel the steps lengthen every query warp's serial prologue before
+// its row stream (measured: C3 +88 us, C4 +57 us per step), so it keeps tau0
 constexpr int kMaxHK = 256;  // H*k staged per warp in the fused kernel
 
 // Per-warp scratch of one lookup's Cartesian stage.
@@ -51,7 +57,7 @@ struct CartSmem {
 
 // One warp computes lookup l: writes idx/w[l*k + t] to global and, when
 // s_idx/s_w are given, to shared memory too (for a fused gather).
-template <int KMAX, int MAXC>
+template <int KMAX, int MAXC, int TAU_STEPS>
 __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64_t l,
                                                  const uint2* __restrict__ cand,
                                                  const int32_t* __restrict__ cand_n, int n_sub,
@@ -126,7 +132,7 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
   {
     float hi = __shfl_sync(0xffffffffu, va[0], 0) + sm.sv2[0];
 #pragma unroll 1
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < TAU_STEPS; ++it) {
       const float x = tau + 0.35f * (hi - tau);
       if (!(x > tau)) break;  // warp-uniform
       int cnt = 0;
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const uint2* __restrict_
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
-  cartesian_lookup<KMAX, MAXC>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, nullptr, nullptr,
+  cartesian_lookup<KMAX, MAXC, MSN_CART_TAU_STEPS>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, nullptr, nullptr,
                                (int32_t)((l % H) / hg) * tab_stride);
 }
 
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (b >= B) return;
   for (int h = 0; h < H; ++h)
-    cartesian_lookup<KMAX, MAXC>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
+    cartesian_lookup<KMAX, MAXC, 0>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
                                  (int32_t)(h / (H / og)) * tab_stride);
   const int HK = H * k;
