@@ -119,11 +119,12 @@ def _worker(rank, world, port, result_q):
         dist.destroy_process_group()
 
 
-def test_sharded_step_matches_unsharded_oracle_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_step_matches_unsharded_oracle(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
