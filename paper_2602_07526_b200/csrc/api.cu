@@ -65,7 +65,7 @@ Shape shape_of(const msn_pkm_config& c, int64_t B) {
 
 // forward workspace layout: [cand (score, index) | cand_n | scores (SIMT scorer only)]
 size_t fwd_bytes(const Shape& s) {
-  const int64_t rows = s.B * s.H * 2;
+  const int64_t rows = s.B * s.H * 2 * select_segments(s, true);  // (row, column segment) lists
   size_t b = align256(sizeof(uint2) * rows * kCandCap) + align256(sizeof(int32_t) * rows);
   if (!select_tc_supported(s)) b += align256(sizeof(float) * rows * s.n_sub);
   else b += align256(select_tc_workspace_bytes(s));
@@ -115,9 +115,11 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   const Shape s = shape_of(h->cfg, B);
   if (ws_bytes < fwd_bytes(s))
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
-  const int64_t rows = B * s.H * 2;
-  char* p = (char*)ws;
   Cands cd;
+  cd.SC = select_segments(s, true);
+  cd.S = select_segments(s, false);
+  const int64_t rows = B * s.H * 2 * cd.SC;
+  char* p = (char*)ws;
   cd.vc = (uint2*)p;
   p += align256(sizeof(uint2) * rows * kCandCap);
   cd.n = (int32_t*)p;

@@ -63,7 +63,7 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
                                                  const int32_t* __restrict__ cand_n, int n_sub,
                                                  int k, int32_t* __restrict__ idx,
                                                  float* __restrict__ w, int32_t* s_idx,
-                                                 float* s_w, int32_t tab_off) {
+                                                 float* s_w, int32_t tab_off, int SC, int S) {
   constexpr int APL = KMAX / 32;  // rows a per lane
   const int lane = threadIdx.x % 32;
 
@@ -74,17 +74,43 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     const int64_t row = l * 2 + half;
     float v[2];
     int32_t ix[2];
-    const int n = cand_n[row];
+    const int n = cand_n[row * SC];
     {
       // sort by the composite key (score desc, index asc) as one u64
       uint64_t key[2];
+      const uint2* rc = cand + row * SC * kCandCap;
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int e = r * 32 + lane;
-        const uint2 c = e < n ? cand[row * kCandCap + e] : make_uint2(0u, 0u);
+        const uint2 c = e < n ? rc[e] : make_uint2(0u, 0u);
         key[r] = e < n ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
       }
       warp_sort64_u64(key);
+      if (KMAX == 32 && S == 2) {
+        // the row's second column segment (its own list, see select_tc.cu):
+        // sorted likewise, then the best 32 of both lists by the half-cleaner
+        // max(A_i, B_31-i) and a 5-step bitonic merge (k <= 32 here)
+        const int n1 = cand_n[row * SC + 1];
+        uint64_t k1[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int e = r * 32 + lane;
+          const uint2 c = e < n1 ? rc[kCandCap + e] : make_uint2(0u, 0u);
+          k1[r] = e < n1 ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
+        }
+        warp_sort64_u64(k1);
+        const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)k1[0], 31 - lane);
+        const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(k1[0] >> 32), 31 - lane);
+        const uint64_t bk = ((uint64_t)bhi << 32) | blo;
+        uint64_t c = key[0] > bk ? key[0] : bk;
+#pragma unroll
+        for (int stride = 16; stride > 0; stride >>= 1) {
+          const uint64_t o = shfl_xor_u64(c, stride);
+          c = ((lane & stride) == 0) == (o > c) ? o : c;
+        }
+        key[0] = c;
+        key[1] = 0ull;
+      }
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         v[r] = key[r] ? sel_key_score(key[r]) : -INFINITY;
@@ -271,14 +297,14 @@ __global__ void __launch_bounds__(256) cartesian_kernel(const uint2* __restrict_
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w, int H, int hg,
-                                                        int32_t tab_stride) {
+                                                        int32_t tab_stride, int SC, int S) {
   pdl_enter();
   __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
   cartesian_lookup<KMAX, MAXC, MSN_CART_TAU_STEPS>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, nullptr, nullptr,
-                               (int32_t)((l % H) / hg) * tab_stride);
+                               (int32_t)((l % H) / hg) * tab_stride, SC, S);
 }
 
 // a3 + a4 + a5 fused: one warp per query runs the Cartesian stage of its H
@@ -290,7 +316,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
     const uint2* __restrict__ cand,
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
-    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride) {
+    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride, int SC, int S) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;
@@ -303,7 +329,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   for (int h = 0; h < H; ++h)
     cartesian_lookup<KMAX, MAXC, 0>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
-                                 (int32_t)(h / (H / og)) * tab_stride);
+                                 (int32_t)(h / (H / og)) * tab_stride, SC, S);
   const int HK = H * k;
   const int g = lane / LG, gl = lane % LG;
   const int E = HK / og;  // entries per output group
@@ -336,7 +362,7 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
   launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
-      cd.vc, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride)
+      cd.vc, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride, cd.SC, cd.S)
   MSN_GATHER_DISPATCH(R, FUSED);
 #undef FUSED
   return cudaGetLastError();
@@ -366,10 +392,10 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (s.k <= 32)
     launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride);
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC, cd.S);
   else if (s.k <= 64)
     launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride);
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC, cd.S);
   else
     return cudaErrorNotSupported;
   cudaError_t e = cudaGetLastError();

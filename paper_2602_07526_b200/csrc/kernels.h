@@ -34,9 +34,12 @@ struct Rescore {
   int qk_dt = 0;
 };
 struct Cands {
-  uint2* vc;     // [B*H*2, kCandCap] (float bits of the score, sub-key index)
-  int32_t* n;    // [B*H*2]
+  uint2* vc;     // [B*H*2, SC*kCandCap] (float bits of the score, sub-key index)
+  int32_t* n;    // [B*H*2, SC]: entries of each column segment's list
   Rescore rq;    // inputs, for rescoring overflowed rows
+  int SC = 1;    // segment slots per row in the buffers (workspace layout)
+  int S = 1;     // column segments in use (<= SC): the tcgen05 scorer splits a
+                 // row over S CTAs, each writing the list of its columns
 };
 
 // a1+a2 (SIMT scorer, fp32 configs): exact per-half top-k (n = k entries).
@@ -48,6 +51,11 @@ cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, flo
 // Returns cudaErrorNotSupported when the shape is not handled.
 // fp32 inputs run 3xTF32 (kind::tf32); ws holds the split sub-keys
 // (select_tc_workspace_bytes).
+// Column segments of a scorer row: 2 when a bf16 row of 512 < n_sub <= 1024
+// would otherwise need two MMA sweeps and the grid is small (<= 74 CTAs:
+// latency regime, e.g. C5), else 1.  for_workspace: the layout's SC, which
+// does not depend on B.
+int select_segments(const Shape& s, bool for_workspace);
 cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
                              void* ws, cudaStream_t st, int* launches);
 bool select_tc_supported(const Shape& s);

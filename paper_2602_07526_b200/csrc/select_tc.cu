@@ -35,6 +35,10 @@
 // is rescored exactly by its write-out warp (warp_sort.cuh, exact_half_topk)
 // -- correctness never depends on the bound being tight.
 //
+// Small grids of bf16 rows with 512 < n_sub <= 1024 (C5: 32 CTAs) split every
+// row over S = 2 CTAs (blockIdx.z = column segment of n_sub / 2 columns, each
+// resident and scored once); each CTA writes the list of its own columns
+// (a superset of that segment's top-KT), the Cartesian stage merges the two.
 // Rows that fit TMEM (n_sub <= 512, two buffers) are scored once; longer rows
 // are scored twice (the MMA pass is cheap next to the epilogue): the first
 // pass feeds pass A, the second pass B, so tau is the whole row's bound.
@@ -119,6 +123,8 @@ struct TcParams {
   int32_t* cn;
   Rescore rq;
   const float* knorm;  // TF32, two sweeps: ||k_i|| (rounded up) per sub-key row [H*2*n_sub]  // overflowed rows are rescored exactly from these
+  int seg_cols;        // columns per CTA: n_sub / S (blockIdx.z = column segment)
+  int SC;              // segment slots per row in vc / cn
 };
 
 template <int KT, bool TF32, bool WIDE>
@@ -153,6 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int hh = blockIdx.x;  // h*2 + half
   const int64_t m0 = (int64_t)blockIdx.y * 128;
+  const int seg = blockIdx.z;  // column segment [col_seg, col_seg + seg_cols)
+  const int col_seg = seg * p.seg_cols;
   const int total_chunks = p.passes * p.n_chunks;
 
   if (threadIdx.x == 0) {
@@ -197,10 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           mbar_expect_tx(&full[s], lo ? stage_bytes : p.n_tile * kRowBytes);
-          tma_load_2d(sB + s * stage_bytes, &tmap_k, &full[s], kb * BK, hh * p.n_sub + c * p.n_tile);
+          tma_load_2d(sB + s * stage_bytes, &tmap_k, &full[s], kb * BK, hh * p.n_sub + col_seg + c * p.n_tile);
           if (lo)
             tma_load_2d(sB + s * stage_bytes + p.n_tile * kRowBytes, &tmap_klo, &full[s], kb * BK,
-                        hh * p.n_sub + c * p.n_tile);
+                        hh * p.n_sub + col_seg + c * p.n_tile);
         }
       }
     }
@@ -485,13 +493,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     if (resident) {
-      pass_b(0, p.n_sub, 0);
+      pass_b(0, p.seg_cols, col_seg);
       release_chunks(0, p.n_chunks);
     } else {
       for (int c = 0; c < p.n_chunks; ++c) {
         const int g = p.n_chunks + c;
         wait_chunks(g, 1);
-        pass_b(g, p.n_tile, c * p.n_tile);
+        pass_b(g, p.n_tile, col_seg + c * p.n_tile);
         release_chunks(g, 1);
       }
     }
@@ -514,13 +522,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (b >= p.B) continue;
       if (n > kCap) { any_ovf = true; continue; }
       const int64_t grow = b * p.H * 2 + hh;
-      if (lane == 0) p.cn[grow] = n;
+      if (lane == 0) p.cn[grow * p.SC + seg] = n;
+      uint2* dst = p.vc + (grow * p.SC + seg) * kCandCap;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int i = hf * 32 + lane;
         if (i < n) {
           const int slot = i < n0 ? i : kCap - 1 - (i - n0);
-          p.vc[grow * kCandCap + i] = cand[slot * kCStride + trow];
+          dst[i] = cand[slot * kCStride + trow];
         }
       }
     }
@@ -532,11 +541,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = __shfl_sync(0xffffffffu, cn_l, rr) + __shfl_sync(0xffffffffu, cn_l, 16 + rr);
         if (b >= p.B || n <= kCap) continue;
         const int64_t grow = b * p.H * 2 + hh;
+        uint2* dst = p.vc + (grow * p.SC + seg) * kCandCap;
         const int nn = p.rq.qk_dt == F32
-            ? exact_half_topk<float>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub, p.vc + grow * kCandCap)
-            : exact_half_topk<__nv_bfloat16>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub,
-                                             p.vc + grow * kCandCap);
-        if (lane == 0) p.cn[grow] = nn;
+            ? exact_half_topk<float>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub, dst, col_seg,
+                                     p.seg_cols)
+            : exact_half_topk<__nv_bfloat16>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub, dst,
+                                             col_seg, p.seg_cols);
+        if (lane == 0) p.cn[grow * p.SC + seg] = nn;
       }
     }
   }
@@ -605,7 +616,7 @@ cudaError_t launch_ktw(const Shape& s, const CUtensorMap& mq, const CUtensorMap&
   }
   // x = head/half (fastest): concurrently resident CTAs spread over all 2H
   // sub-key codebooks instead of hammering one codebook's lines in L2
-  dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128));
+  dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128), (unsigned)(s.n_sub / p.seg_cols));
   launch_pdl(select_tc_kernel<KT, TF32, WIDE>, grid, kThreads, sm, st, mq, mk, mklo, p);
   return cudaGetLastError();
 }
@@ -627,6 +638,17 @@ extern "C" int msn_select_ts_dump(unsigned long long* host, int n) {
   (void)host; (void)n;
   return -1;
 #endif
+}
+
+int select_segments(const Shape& s, bool for_workspace) {
+  if (is_tf32(s) || !select_tc_supported(s) || s.k > 32) return 1;
+  const int nt = n_tile_for(s);
+  if (s.n_sub <= 512 || s.n_sub > 1024 || (s.n_sub / 2) % nt != 0) return 1;
+  if (for_workspace) return 2;
+  static const int mode = getenv("MSN_SELECT_SPLIT") ? atoi(getenv("MSN_SELECT_SPLIT")) : -1;
+  if (mode >= 0) return mode ? 2 : 1;
+  const int64_t ctas = (s.B + 127) / 128 * s.H * 2;
+  return ctas <= 74 ? 2 : 1;
 }
 
 size_t select_tc_workspace_bytes(const Shape& s) {
@@ -695,9 +717,10 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   if (!kmap(&mk, kb_hi) || !kmap(&mklo, kb_lo)) return cudaErrorInvalidValue;
-  const int n_chunks = s.n_sub / nt;
+  const int seg_cols = s.n_sub / cd.S;
+  const int n_chunks = seg_cols / nt;
   TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, n_chunks, s.d_h / bk, n_chunks <= 2 ? 1 : 2,
-             cd.vc, cd.n, cd.rq, knorm};
+             cd.vc, cd.n, cd.rq, knorm, seg_cols, cd.SC};
   cudaError_t e;
   if (tf) {
     if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);

@@ -93,7 +93,9 @@ __device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, flo
 }
 template <typename T>
 __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int half, int H, int n_sub,
-                                            uint2* vc) {
+                                            uint2* vc, int col0 = 0, int ncols = -1) {
+  // columns [col0, col0 + ncols) of the row (a column segment; default all)
+  if (ncols < 0) ncols = n_sub;
   const int lane = threadIdx.x % 32;
   float v[2];
   int32_t ix[2];
@@ -101,7 +103,7 @@ __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int 
   const int d = rq.d_h;
   const bool mine = lane * 8 < d;
   const T* q = (const T*)rq.Q + (l * 2 + half) * (int64_t)d;
-  const T* kb = (const T*)rq.K + ((int64_t)(h * 2 + half) * n_sub) * d + lane * 8;
+  const T* kb = (const T*)rq.K + ((int64_t)(h * 2 + half) * n_sub + col0) * d + lane * 8;
   float qs[8];
   if (mine) load8<T>(q + lane * 8, qs);
   else
@@ -109,12 +111,12 @@ __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int 
     for (int e = 0; e < 8; ++e) qs[e] = 0.f;
   v[0] = v[1] = -INFINITY;
   ix[0] = ix[1] = 0x7fffffff;
-  for (int base = 0; base < n_sub; base += 32) {
+  for (int base = 0; base < ncols; base += 32) {
     float part[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
       float acc = 0.f;
-      if (mine && base + r < n_sub) {
+      if (mine && base + r < ncols) {
         float x[8];
         load8<T>(kb + (int64_t)(base + r) * d, x);
 #pragma unroll
@@ -133,8 +135,8 @@ __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int 
       }
     }
     const int i = base + lane;
-    float nv[2] = {i < n_sub ? part[0] + 0.0f : -INFINITY, -INFINITY};
-    int32_t ni[2] = {i < n_sub ? i : 0x7fffffff, 0x7fffffff};
+    float nv[2] = {i < ncols ? part[0] + 0.0f : -INFINITY, -INFINITY};
+    int32_t ni[2] = {i < ncols ? col0 + i : 0x7fffffff, 0x7fffffff};
     const float wv = __shfl_sync(0xffffffffu, v[1], 31);  // current 64th
     const int32_t wi = __shfl_sync(0xffffffffu, ix[1], 31);
     if (!__any_sync(0xffffffffu, before(nv[0], ni[0], wv, wi))) continue;
@@ -148,8 +150,8 @@ __device__ __forceinline__ int exact_half_topk(const Rescore rq, int64_t l, int 
 #pragma unroll
     for (int stride = 32; stride > 0; stride >>= 1) bitonic_step64(v, ix, 64, stride);
   }
-  // the row's new candidate list: its best min(64, n_sub) sub-keys
-  const int n = n_sub < 64 ? n_sub : 64;
+  // the row's new candidate list: its best min(64, ncols) sub-keys
+  const int n = ncols < 64 ? ncols : 64;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int e = r * 32 + lane;
