@@ -137,10 +137,18 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
     if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half top-k)");
   }
   if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);  // stage boundary: scoring done
-  if (values) {
+  if (values && cd.S == 1) {
     if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);  // (fused: no separate Cartesian stage)
     e = launch_cartesian_gather(s, cd, idx, weights, values, out, st, launches, gate);
     if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax + gather");
+    return MSN_OK;
+  }
+  if (values) {  // column-segmented scorer rows: Cartesian stage, then the gather
+    e = launch_cartesian(s, cd, idx, weights, st, launches);
+    if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax");
+    if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);
+    e = launch_gather(s, idx, weights, values, out, st, launches, gate);
+    if (e != cudaSuccess) return cuda_fail(e, "gather");
     return MSN_OK;
   }
   e = launch_cartesian(s, cd, idx, weights, st, launches);

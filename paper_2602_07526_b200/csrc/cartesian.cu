@@ -57,13 +57,13 @@ struct CartSmem {
 
 // One warp computes lookup l: writes idx/w[l*k + t] to global and, when
 // s_idx/s_w are given, to shared memory too (for a fused gather).
-template <int KMAX, int MAXC, int TAU_STEPS>
+template <int KMAX, int MAXC, int TAU_STEPS, int SEG>
 __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64_t l,
                                                  const uint2* __restrict__ cand,
                                                  const int32_t* __restrict__ cand_n, int n_sub,
                                                  int k, int32_t* __restrict__ idx,
                                                  float* __restrict__ w, int32_t* s_idx,
-                                                 float* s_w, int32_t tab_off, int SC, int S) {
+                                                 float* s_w, int32_t tab_off, int SC) {
   constexpr int APL = KMAX / 32;  // rows a per lane
   const int lane = threadIdx.x % 32;
 
@@ -86,7 +86,7 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
         key[r] = e < n ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
       }
       warp_sort64_u64(key);
-      if (KMAX == 32 && S == 2) {
+      if constexpr (KMAX == 32 && SEG == 2) {
         // the row's second column segment (its own list, see select_tc.cu):
         // sorted likewise, then the best 32 of both lists by the half-cleaner
         // max(A_i, B_31-i) and a 5-step bitonic merge (k <= 32 here)
@@ -291,20 +291,20 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
   __syncwarp();
 }
 
-template <int KMAX, int MAXC>
+template <int KMAX, int MAXC, int SEG>
 __global__ void __launch_bounds__(256) cartesian_kernel(const uint2* __restrict__ cand,
                                                         const int32_t* __restrict__ cand_n,
                                                         int64_t L, int n_sub, int k,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w, int H, int hg,
-                                                        int32_t tab_stride, int SC, int S) {
+                                                        int32_t tab_stride, int SC) {
   pdl_enter();
   __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
   const int wid = threadIdx.x / 32;
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (l >= L) return;
-  cartesian_lookup<KMAX, MAXC, MSN_CART_TAU_STEPS>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, nullptr, nullptr,
-                               (int32_t)((l % H) / hg) * tab_stride, SC, S);
+  cartesian_lookup<KMAX, MAXC, MSN_CART_TAU_STEPS, SEG>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, nullptr,
+                                                        nullptr, (int32_t)((l % H) / hg) * tab_stride, SC);
 }
 
 // a3 + a4 + a5 fused: one warp per query runs the Cartesian stage of its H
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
     const uint2* __restrict__ cand,
     const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
     int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V,
-    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride, int SC, int S) {
+    float* __restrict__ out, int d_v, Gate gate, int og, int32_t tab_stride, int SC) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;
@@ -327,9 +327,9 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (b >= B) return;
   for (int h = 0; h < H; ++h)
-    cartesian_lookup<KMAX, MAXC, 0>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
+    cartesian_lookup<KMAX, MAXC, 0, 1>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
-                                 (int32_t)(h / (H / og)) * tab_stride, SC, S);
+                                 (int32_t)(h / (H / og)) * tab_stride, SC);
   const int HK = H * k;
   const int g = lane / LG, gl = lane % LG;
   const int E = HK / og;  // entries per output group
@@ -362,7 +362,7 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
   const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
 #define FUSED(VPL, G, U)                                                                      \
   launch_pdl(cartesian_gather_kernel<KMAX, MAXC, VT, VPL, G, U>, blocks, 256, 0, st,                   \
-      cd.vc, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride, cd.SC, cd.S)
+      cd.vc, cd.n, s.B, s.H, s.n_sub, s.k, idx, w, V, out, s.d_v, gate, s.og, (int32_t)s.tab_stride, cd.SC)
   MSN_GATHER_DISPATCH(R, FUSED);
 #undef FUSED
   return cudaGetLastError();
@@ -373,7 +373,7 @@ cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float*
 cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* idx, float* w,
                                     const void* V, float* out, cudaStream_t st, int* launches,
                                     const Gate& gate) {
-  if (s.H * s.k > kMaxHK || s.row_begin != 0) return cudaErrorNotSupported;
+  if (s.H * s.k > kMaxHK || s.row_begin != 0 || cd.S != 1) return cudaErrorNotSupported;
   cudaError_t e;
   if (s.k <= 32) {
     e = s.v_dt == F32 ? dispatch_fused<32, 119, float>(s, cd, idx, w, (const float*)V, out, st, gate)
@@ -390,12 +390,17 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
                              cudaStream_t st, int* launches) {
   const int64_t L = s.B * s.H;
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  if (s.k <= 32)
-    launch_pdl(cartesian_kernel<32, 119>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC, cd.S);
+  if (s.k <= 32 && cd.S == 2)
+    launch_pdl(cartesian_kernel<32, 119, 2>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC);
+  else if (cd.S != 1)
+    return cudaErrorNotSupported;
+  else if (s.k <= 32)
+    launch_pdl(cartesian_kernel<32, 119, 1>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC);
   else if (s.k <= 64)
-    launch_pdl(cartesian_kernel<64, 280>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
-               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC, cd.S);
+    launch_pdl(cartesian_kernel<64, 280, 1>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
+               s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC);
   else
     return cudaErrorNotSupported;
   cudaError_t e = cudaGetLastError();

@@ -127,7 +127,7 @@ struct TcParams {
   int SC;              // segment slots per row in vc / cn
 };
 
-template <int KT, bool TF32, bool WIDE>
+template <int KT, bool TF32, bool WIDE, bool SEG>
 __global__ void __launch_bounds__(kThreads, 1)
     select_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                      const __grid_constant__ CUtensorMap tmap_k,
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int hh = blockIdx.x;  // h*2 + half
   const int64_t m0 = (int64_t)blockIdx.y * 128;
-  const int seg = blockIdx.z;  // column segment [col_seg, col_seg + seg_cols)
-  const int col_seg = seg * p.seg_cols;
+  const int seg = SEG ? (int)blockIdx.z : 0;  // column segment [col_seg, col_seg + seg_cols)
+  const int col_seg = SEG ? seg * p.seg_cols : 0;
   const int total_chunks = p.passes * p.n_chunks;
 
   if (threadIdx.x == 0) {
@@ -603,13 +603,13 @@ __global__ void split_tf32_kernel(const float* __restrict__ k, float* __restrict
   if (lane == 0) knorm[r] = __fsqrt_ru(ss * 1.001f);
 }
 
-template <int KT, bool TF32, bool WIDE>
-cudaError_t launch_ktw(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+template <int KT, bool TF32, bool WIDE, bool SEG>
+cudaError_t launch_ktws(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
                        const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
   const size_t sm = smem_bytes(s);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT, TF32, WIDE>,
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT, TF32, WIDE, SEG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -617,8 +617,14 @@ cudaError_t launch_ktw(const Shape& s, const CUtensorMap& mq, const CUtensorMap&
   // x = head/half (fastest): concurrently resident CTAs spread over all 2H
   // sub-key codebooks instead of hammering one codebook's lines in L2
   dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128), (unsigned)(s.n_sub / p.seg_cols));
-  launch_pdl(select_tc_kernel<KT, TF32, WIDE>, grid, kThreads, sm, st, mq, mk, mklo, p);
+  launch_pdl(select_tc_kernel<KT, TF32, WIDE, SEG>, grid, kThreads, sm, st, mq, mk, mklo, p);
   return cudaGetLastError();
+}
+template <int KT, bool TF32, bool WIDE>
+cudaError_t launch_ktw(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+                       const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
+  if (!TF32 && !WIDE && p.seg_cols < p.n_sub) return launch_ktws<KT, TF32, WIDE, true>(s, mq, mk, mklo, p, st);
+  return launch_ktws<KT, TF32, WIDE, false>(s, mq, mk, mklo, p, st);
 }
 template <int KT, bool TF32>
 cudaError_t launch_kt(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
