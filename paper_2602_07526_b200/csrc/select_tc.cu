@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     if (resident) {
-      pass_b(0, p.seg_cols, col_seg);
+      pass_b(0, SEG ? p.seg_cols : p.n_sub, col_seg);
       release_chunks(0, p.n_chunks);
     } else {
       for (int c = 0; c < p.n_chunks; ++c) {
@@ -544,9 +544,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint2* dst = p.vc + (grow * p.SC + seg) * kCandCap;
         const int nn = p.rq.qk_dt == F32
             ? exact_half_topk<float>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub, dst, col_seg,
-                                     p.seg_cols)
+                                     SEG ? p.seg_cols : -1)
             : exact_half_topk<__nv_bfloat16>(p.rq, b * p.H + (hh >> 1), hh & 1, p.H, p.n_sub, dst,
-                                             col_seg, p.seg_cols);
+                                             col_seg, SEG ? p.seg_cols : -1);
         if (lane == 0) p.cn[grow * p.SC + seg] = nn;
       }
     }
