@@ -1,6 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
 the same seeded inputs, element by element, under the north_star bar
 (tests/parity.py).  Needs a B200."""
+import os
 import numpy as np
 import pytest
 import torch
@@ -644,6 +645,39 @@ def test_validate_tape(name, groups, tables):
     for a, b in zip(r0, r1):
         assert torch.equal(a, b)
     assert torch.equal(lv.gather(idx, w, V), lk.gather(idx, w, V))
+
+
+_SPLIT_SCRIPT = """
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2602_07526_b200 import workloads as wl
+from paper_2602_07526_b200.pkm import PKMLookup
+cfg = wl.CONFIGS[sys.argv[2]].scaled(batch=int(sys.argv[3]))
+Q, K, V, _ = wl.make_all(cfg, "cuda")
+lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, cfg.batch, cfg.qk_dtype, cfg.value_dtype)
+out, idx, w = lk.forward(Q, K, V)
+torch.save({"out": out.cpu(), "idx": idx.cpu(), "w": w.cpu()}, sys.argv[4])
+"""
+
+
+@pytest.mark.parametrize("name,B", [("c5_latency_bf16", 512), ("c5_latency_bf16", 130)])
+def test_select_column_split_matches_unsplit(name, B, tmp_path):
+    """Scorer rows split over two CTAs (MSN_SELECT_SPLIT=1, the default for
+    small grids) and scored by one CTA in two sweeps (=0) select the same
+    slots: idx, w and out bitwise equal (separate processes: the switch is
+    read once per process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"r{mode}.pt")
+        env = dict(os.environ, MSN_SELECT_SPLIT=mode)
+        subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT, root, name, str(B), f], env=env, check=True,
+                       timeout=600)
+        res[mode] = torch.load(f)
+    for key in ("idx", "w", "out"):
+        assert torch.equal(res["0"][key], res["1"][key]), key
 
 
 @pytest.mark.parametrize("name,B,groups", [("c2_mid_bf16", 8192 + 37, 1), ("c3_train_fp32_zipf", 8192 + 5, 1),
