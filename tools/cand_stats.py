@@ -1,6 +1,7 @@
 """Per-half candidate-list statistics of the tcgen05 scorer (profiling aid):
 runs msn_pkm_select on a workload and reads cand_n back from the forward
-workspace (layout in api.cu: cand (score, index) | cand_n, 256-B aligned).
+workspace (layout in api.cu: cand (score, index) | cand_n, 256-B aligned;
+SC segment slots per row, SC = 2 for bf16 rows of 512 < n_sub <= 1024).
 
     python tools/cand_stats.py c4_large_sharded_bf16 [B]
 """
@@ -27,8 +28,11 @@ B = Q.shape[0]
 lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B, cfg.qk_dtype, cfg.value_dtype)
 lk.select(Q, K)
 torch.cuda.synchronize()
-rows = B * cfg.heads * 2
+SC = 2 if (cfg.qk_dtype == torch.bfloat16 and 512 < cfg.n_sub <= 1024 and cfg.k <= 32) else 1
+rows = B * cfg.heads * 2 * SC
 off = a256(8 * rows * 64)
 n = lk._ws[off: off + 4 * rows].view(torch.int32).cpu()
+if SC == 2:  # unused second segment counts are stale when the row was not split
+    print("(rows with two column segments: counts per segment)")
 print(name, "rows", rows, "mean", n.float().mean().item(), "max", n.max().item(),
       "overflow(>64)", int((n > 64).sum()), "p99", n.float().quantile(0.99).item())
