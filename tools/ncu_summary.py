@@ -43,7 +43,7 @@ def main():
             v = num(r[i]) if i is not None else None
             if v is not None and m == "gpu__time_duration.sum":
                 u = units[i]
-                v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                v = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
                 sc = 1
             elif v is not None and units[i].endswith("byte"):
                 # normalise to bytes, then the column scale (1e-6 -> MB)
