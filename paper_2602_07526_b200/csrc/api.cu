@@ -72,6 +72,13 @@ size_t fwd_bytes(const Shape& s) {
   return b;
 }
 
+msn_status check_bwd_shape(msn_pkm_t h, bool values, bool keys) {
+  if (backward_supported(shape_of(h->cfg, 0), values, keys)) return MSN_OK;
+  return fail(MSN_ERR_UNSUPPORTED,
+              "backward needs d_value (%d) and d_half (%d) in 32 * {1, 2, 4, 8, 16} and k <= 64; "
+              "nothing was launched", h->cfg.d_value, h->cfg.d_half);
+}
+
 msn_status check_handle(msn_pkm_t h) {
   if (!h) return fail(MSN_ERR_INVALID_ARG, "null handle");
   return MSN_OK;
@@ -453,6 +460,7 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* 
   REQUIRE_PTR(values);
   REQUIRE_PTR(d_values);
   REQUIRE_PTR(dw);
+  if ((st = check_bwd_shape(h, true, false))) return st;
   if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   cudaStream_t cs = (cudaStream_t)stream;
@@ -492,6 +500,7 @@ msn_status msn_pkm_scatter_p2p(msn_pkm_t h, void* stream, int64_t B, const int32
   REQUIRE_PTR(d_values);
   REQUIRE_PTR(workspace);
   if (!peer_d_out || !peer_dw) return fail(MSN_ERR_INVALID_ARG, "peer_d_out / peer_dw is NULL");
+  if ((st = check_bwd_shape(h, true, false))) return st;
   if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
@@ -530,6 +539,7 @@ msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const in
   REQUIRE_PTR(dw);
   REQUIRE_PTR(workspace);
   if (update == MSN_UPDATE_ADAGRAD) REQUIRE_PTR(state);
+  if ((st = check_bwd_shape(h, true, false))) return st;
   if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
@@ -561,6 +571,7 @@ msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B, const voi
   REQUIRE_PTR(d_query);
   REQUIRE_PTR(d_subkeys);
   REQUIRE_PTR(workspace);
+  if ((st = check_bwd_shape(h, false, true))) return st;
   if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(s, B);
@@ -597,6 +608,7 @@ msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B, const float* d
   REQUIRE_PTR(d_subkeys);
   REQUIRE_PTR(d_values);
   REQUIRE_PTR(workspace);
+  if ((st = check_bwd_shape(h, true, true))) return st;
   if ((st = check_tape(h, stream, B, idx, weights))) return st;
   const Shape s = shape_of(h->cfg, B);
   const size_t need = bwd_workspace_bytes(s, B);

@@ -700,16 +700,7 @@ __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
   }
 }
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+int num_sms() { return device_sms(); }
 
 // scratch of the grouping (carved by carve_bwd_workspace)
 struct GrpScratch {
@@ -762,12 +753,10 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
     launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false, false>, (unsigned)sb, 256, 0, st, a);
   if (tr.n > 1) cudaEventRecord(tr.ev[1], st);
   // long runs: sort, pieces, combine
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grp_sort_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GRP_SORT_SMEM * 4);
+  static std::atomic<uint64_t> attr{0};
+  {
+    cudaError_t e = smem_attr_once(attr, grp_sort_long_kernel, GRP_SORT_SMEM * 4);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int64_t lneed = n / (GRP_SHORT + 1) + 1;
   int64_t lb = (lneed + 7) / 8;
@@ -1075,6 +1064,12 @@ bool epl_ok(int D) {
 }
 
 }  // namespace
+
+bool backward_supported(const Shape& s, bool values, bool keys) {
+  if (values && !epl_ok(s.d_v)) return false;
+  if (keys && (!epl_ok(s.d_h) || s.k > 64)) return false;
+  return true;
+}
 
 // ---------------------------------------------------------- workspace ------
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 #ifndef __CUDACC__
 #error "CUDA only"
 #endif
@@ -42,6 +44,37 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   static const bool off = getenv("MSN_NO_PDL") != nullptr;  // A/B measurements only
   cfg.numAttrs = off ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
+// Host side: per-device state.  The current device's SM count (cached per
+// device), and a one-time-per-device cudaFuncSetAttribute(max dynamic shared
+// memory) for a kernel: `done` is that call site's bitmask of devices
+// already set (atomic: several host threads may launch concurrently).
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+inline int device_sms() {
+  static std::atomic<int> cache[64];
+  const int d = current_device();
+  if (d < 0 || d >= 64) return 148;
+  int n = cache[d].load(std::memory_order_relaxed);
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+    cache[d].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+template <typename... KArgs>
+inline cudaError_t smem_attr_once(std::atomic<uint64_t>& done, void (*kernel)(KArgs...), int bytes) {
+  const int d = current_device();
+  const uint64_t bit = (d >= 0 && d < 64) ? (uint64_t(1) << d) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 // Order-preserving map fp32 -> uint32 (larger float -> larger uint).  -0 is

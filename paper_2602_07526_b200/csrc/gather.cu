@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) gather_wide_kernel(const int32_t* __restr
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qpb = kWarps / wpq;
   const int64_t b = (int64_t)blockIdx.x * qpb + wid / wpq;
-  if (b >= B) return;
+  if (wid >= qpb * wpq || b >= B) return;  // (wpq divides kWarps for the R the launcher allows)
   const int vec = (wid % wpq) * 32 + lane;  // this lane's 16-byte vector of the row
   for (int r = lane; r < HK; r += 32) {
     s_idx[wid][r] = idx[b * HK + r];
@@ -142,7 +142,7 @@ template <typename VT>
 cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const VT* V, float* out,
                      cudaStream_t st, const Gate& gate, const Push& push) {
   const int R = s.d_v * (int)sizeof(VT) / 16;
-  if (R >= 64 && R % 32 == 0 && R <= 128 && !push.peers && s.row_begin == 0 &&
+  if ((R == 64 || R == 128) && !push.peers && s.row_begin == 0 &&
       s.row_end >= (int64_t)s.n_sub * s.n_sub * (s.tab_stride ? s.og : 1)) {
     const int wpq = R / 32, qpb = kWarps / wpq;
     launch_pdl(gather_wide_kernel<VT, 16>, (unsigned)((s.B + qpb - 1) / qpb), 256, 0, st, idx, w, V, out, s.B,

@@ -121,6 +121,11 @@ struct BwdWorkspace {
   void* dk_ws;                    // tensor-core dQ/dK scratch (bf16 configs)
 };
 
+// Host-side shape check of the backward, made before anything is launched:
+// the value reducers need d_v (values), the key path d_h (keys), each in
+// 32 * {1, 2, 4, 8, 16}, and k <= 64.
+bool backward_supported(const Shape& s, bool values, bool keys);
+
 // a7 dQ + a8 dK on the tensor cores (bf16 q/K): dQ = dS . K, dK += dS^T . Q per (head, half).
 bool dk_tc_supported(const Shape& s);
 size_t dk_tc_workspace_bytes(const Shape& s);

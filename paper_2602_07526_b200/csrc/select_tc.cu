@@ -607,12 +607,10 @@ template <int KT, bool TF32, bool WIDE, bool SEG>
 cudaError_t launch_ktws(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
                        const CUtensorMap& mklo, TcParams p, cudaStream_t st) {
   const size_t sm = smem_bytes(s);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel<KT, TF32, WIDE, SEG>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static std::atomic<uint64_t> attr_done{0};
+  {
+    cudaError_t e = smem_attr_once(attr_done, select_tc_kernel<KT, TF32, WIDE, SEG>, 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   // x = head/half (fastest): concurrently resident CTAs spread over all 2H
   // sub-key codebooks instead of hammering one codebook's lines in L2

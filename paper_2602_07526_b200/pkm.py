@@ -266,8 +266,8 @@ class PKMLookup:
         _lib.check(self.lib.msn_pkm_backward(self._h, _stream(), B, _ptr(d), _ptr(q), _ptr(K), _ptr(V),
                                              _ptr(idx), _ptr(w), _ptr(d_query), _ptr(d_subkeys),
                                              _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
-        if host:
-            return d_query.cpu(), d_subkeys, d_values, dw
+        if host:  # every result back on the caller's (host) device
+            return d_query.cpu(), d_subkeys.cpu(), d_values.cpu(), dw.cpu()
         return d_query, d_subkeys, d_values, dw
 
     def scatter(self, idx, w, d_out, values, d_values, gather_batch: Optional[int] = None):
@@ -304,6 +304,16 @@ class PKMLookup:
         """a6 with the optimiser step fused: values is updated
         IN PLACE (SGD / Adagrad on the touched rows, state += g^2 for Adagrad);
         returns dw (computed from the values before the update)."""
+        rows = self.row_end - self.row_begin
+        if values.device.type != "cuda" or tuple(values.shape) != (rows, self.d_value) \
+                or values.dtype != self.value_dtype or not values.is_contiguous():
+            raise ValueError(f"values must be a contiguous CUDA tensor [{rows},{self.d_value}] {self.value_dtype} "
+                             "(updated in place)")
+        if update == "adagrad" and (state is None or state.device.type != "cuda" or state.dtype != torch.float32
+                                    or tuple(state.shape) != (rows, self.d_value) or not state.is_contiguous()):
+            raise ValueError(f"Adagrad needs state: a contiguous CUDA fp32 tensor [{rows},{self.d_value}]")
+        if update not in _lib.UPDATES:
+            raise ValueError(f"update {update!r}: 'sgd' or 'adagrad'")
         idx, w, d = self._dev(idx), self._dev(w), self._dev(d_out)
         Bg = idx.shape[0]
         dw = torch.empty((Bg, self.heads, self.k), dtype=torch.float32, device=self.device)
@@ -427,7 +437,7 @@ class PKMFunction(torch.autograd.Function):
     def backward(ctx, d_out):
         q, K, V, idx, w = ctx.saved_tensors
         dq, dK, dV, _ = ctx.lookup.backward(d_out.contiguous().float(), q, K, V, idx, w)
-        return None, dq.to(q.dtype), dK.to(K.dtype), dV.to(V.dtype)
+        return (None, dq.to(q.device, q.dtype), dK.to(K.device, K.dtype), dV.to(V.device, V.dtype))
 
 
 def pkm(lookup: PKMLookup, query, subkeys, values):

@@ -95,6 +95,19 @@ def row_close(gpu: np.ndarray, ref: np.ndarray, rtol: float, row_mask=None, what
     return worst
 
 
+def plain_row_err(gpu: np.ndarray, ref: np.ndarray, row_mask=None) -> float:
+    """SURVEY.md 8(c)'s plain metric: per row  max_e |g - o| / max(max_e |o_row|,
+    1e-6 max |o|), worst row (reported next to the condition-aware one)."""
+    g = np.asarray(gpu, dtype=np.float64).reshape(gpu.shape[0], -1)
+    r = np.asarray(ref, dtype=np.float64).reshape(ref.shape[0], -1)
+    floor = 1e-6 * np.abs(r).max() + 1e-300
+    if row_mask is not None:
+        g, r = g[row_mask], r[row_mask]
+    if g.size == 0:
+        return 0.0
+    return float((np.abs(g - r).max(axis=1) / np.maximum(np.abs(r).max(axis=1), floor)).max())
+
+
 def grad_key_magnitudes(Q, K, o, bw, n_sub):
     """Sum of |terms| behind each element of dQ and dK.  ds_t = w_t dw_t -
     w_t sum_u w_u dw_u has magnitude A_t = w_t (|dw_t| + sum_u w_u |dw_u|);
@@ -137,23 +150,28 @@ def check_forward(Q, K, V, k, out, idx, w, max_affected_frac=0.01):
     return o, affected, rep
 
 
-def check_backward(Q, K, V, k, dOut, o, affected, dQ, dK, dV, dw=None, gpu_idx=None):
-    """Backward parity at the oracle's own selection, masking tie-affected lookups."""
+def check_backward(Q, K, V, k, dOut, o, affected, dQ, dK, dV, dw=None, gpu_idx=None, assert_plain=False):
+    """Backward parity at the oracle's own selection, masking tie-affected lookups.
+    out, w, dw and dV are always held to the plain row-max metric; dQ and dK to
+    the condition-aware one (R14), with the plain one reported and, with
+    assert_plain, asserted too."""
     n_sub = K.shape[2]
     B, H = affected.shape
     bw = orc.backward(Q, K, V, o["idx"], dOut, want_dense_dv=False)
     rtol = rtol_for(V.dtype)
-    # dQ and dK come from the query / sub-key operands (and, on the bf16
-    # tensor-core path, a bf16-rounded dS: reading R12), so their tolerance
-    # follows the q/K dtype; out, dw and dV follow the value dtype (R14)
-    rtol_qk = max(rtol, rtol_for(K.dtype))
+    # every output and gradient is held to the value dtype's tolerance
+    # (north_star: "1e-4 relative for fp32 and 2e-2 relative for bf16 values")
+    rtol_qk = rtol
     rep = {}
     absq, absk = grad_key_magnitudes(Q, K, o, bw, n_sub)
     # dQ rows: per (b,h,half)
     mask_q = np.repeat((~affected).reshape(-1), 2)
-    rep["dQ_err"] = row_close(dQ.detach().cpu().numpy().reshape(B * H * 2, -1),
-                              bw["dQ"].reshape(B * H * 2, -1), rtol_qk, mask_q, "dQ",
+    dq_g = dQ.detach().cpu().numpy().reshape(B * H * 2, -1)
+    rep["dQ_err"] = row_close(dq_g, bw["dQ"].reshape(B * H * 2, -1), rtol_qk, mask_q, "dQ",
                               absmag=absq.reshape(B * H * 2, -1))
+    rep["dQ_err_plain"] = plain_row_err(dq_g, bw["dQ"].reshape(B * H * 2, -1), mask_q)
+    if assert_plain:
+        assert rep["dQ_err_plain"] <= rtol, f"dQ: plain row-max error {rep['dQ_err_plain']:.3g} > {rtol}"
     if dw is not None:
         rep["dw_err"] = row_close(dw.detach().cpu().numpy().reshape(B * H, -1),
                                   bw["dw"].reshape(B * H, -1), rtol, (~affected).reshape(-1), "dw")
@@ -179,6 +197,9 @@ def check_backward(Q, K, V, k, dOut, o, affected, dQ, dK, dV, dw=None, gpu_idx=N
     keys = [(h, half, i) for h in range(H) for half in range(2) for i in range(n_sub)]
     mask_k = np.array([kk not in bad_keys for kk in keys], bool)
     rep["dK_err"] = row_close(dk_g, dk_o, rtol_qk, mask_k, "dK", absmag=absk.reshape(dk_o.shape))
+    rep["dK_err_plain"] = plain_row_err(dk_g, dk_o, mask_k)
+    if assert_plain:
+        assert rep["dK_err_plain"] <= rtol, f"dK: plain row-max error {rep['dK_err_plain']:.3g} > {rtol}"
     zero_o = np.all(dk_o == 0, axis=1) & mask_k
     assert np.all(dk_g[zero_o] == 0), "never-selected sub-keys must get exactly 0 gradient"
     return bw, rep

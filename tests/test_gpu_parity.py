@@ -571,8 +571,13 @@ def test_backward_unsupported_width_is_reported():
     Q, K, V, dOut = wl.make_all(cfg, DEV)
     lk = lookup_for(cfg)
     out, idx, w = lk.forward(Q, K, V)          # forward supports d_half % 16 == 0
+    dV = torch.full((cfg.n_slots, cfg.d_value), 0.25, dtype=torch.float32, device=DEV)
+    dK = torch.full((cfg.heads, 2, cfg.n_sub, cfg.d_half), 0.5, dtype=torch.float32, device=DEV)
     with pytest.raises(MsnError, match="UNSUPPORTED"):
-        lk.backward(dOut, Q, K, V, idx, w)      # backward needs d_half % 32 == 0
+        lk.backward(dOut, Q, K, V, idx, w, d_subkeys=dK, d_values=dV)  # backward needs d_half % 32 == 0
+    torch.cuda.synchronize()
+    # checked on the host before any launch: the accumulators are untouched
+    assert torch.all(dV == 0.25) and torch.all(dK == 0.5)
 
 
 def test_autograd_function():
@@ -595,6 +600,25 @@ def test_host_tensors_end_to_end():
     out_h, idx_h, w_h = lk.forward(Q.pin_memory(), K.to(DEV), V.to(DEV))
     out_d, idx_d, w_d = lk.forward(Q.to(DEV), K.to(DEV), V.to(DEV))
     assert out_h.device.type == "cpu" and torch.equal(out_h, out_d.cpu())
+
+
+def test_host_tensors_backward_and_autograd():
+    """Host inputs: every backward result comes back on the host, and autograd
+    over CPU-resident parameters gets CPU gradients (equal to the device run)."""
+    from paper_2602_07526_b200.pkm import pkm
+    cfg = wl.tiny_config(16, 2, 32, 64, 64, 8, torch.float32, torch.float32)
+    Q, K, V, dOut = wl.make_all(cfg, "cpu")
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)
+    res_h = lk.backward(dOut, Q, K, V, idx, w)
+    assert all(t.device.type == "cpu" for t in res_h)
+    res_d = lk.backward(dOut.to(DEV), Q.to(DEV), K.to(DEV), V.to(DEV), idx.to(DEV), w.to(DEV))
+    for a, b in zip(res_h, res_d):
+        assert torch.equal(a, b.cpu())
+    q, k_, v = (t.clone().requires_grad_(True) for t in (Q, K, V))
+    (pkm(lk, q, k_, v) * dOut).sum().backward()
+    assert q.grad.device.type == k_.grad.device.type == v.grad.device.type == "cpu"
+    assert torch.equal(k_.grad, res_h[1]) and torch.equal(v.grad, res_h[2])
 
 
 def test_invalid_arguments_raise():

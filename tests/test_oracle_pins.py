@@ -86,6 +86,13 @@ def test_golden_n4_forward_backward():
     np.testing.assert_allclose(r["out"][0], g["expect_out"], rtol=1e-15)
     d = np.array([g["dOut"]])
     bw = orc.backward(Q, K, V, r["idx"], d)
+    # dw_t = <V[f_t], dOut> = [<(1,2),(1,0)>, <(3,4),(1,0)>]
+    np.testing.assert_array_equal(bw["dw"][0, 0], g["expect_dw"])
+    # ds_t = w_t (dw_t - sum_u w_u dw_u) = -/+ 2 w0 w1 (softmax Jacobian); the dS of
+    # each half is recovered from dQ_col = ds0 K_col[0] + ds1 K_col[1] with K_col = I
+    w0, w1 = g["expect_w"]
+    np.testing.assert_allclose(g["expect_ds"], [-2 * w0 * w1, 2 * w0 * w1], rtol=1e-15)
+    np.testing.assert_allclose(bw["dQ"][0, 0, 1], g["expect_ds"], rtol=1e-14)
     np.testing.assert_allclose(bw["dQ"][0, 0, 0], g["expect_dq_row"], atol=1e-15)
     np.testing.assert_allclose(bw["dQ"][0, 0, 1], g["expect_dq_col"], rtol=1e-14)
     for row, val in g["expect_dV_rows"].items():
