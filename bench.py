@@ -1,17 +1,21 @@
-"""bench.py -- PKM lookup forward+backward throughput on B200 (the driver's
+"""bench.py -- PKM lookups/sec forward+backward on B200 (the driver's
 contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2_mid_bf16]
+                    [--workload c4_large_sharded_bf16] [--transport peer|nccl]
 
-A step is one pass of the whole hot path over one batch of synthetic input:
-select (scoring + per-half top-k + Cartesian top-k + softmax) -> gather ->
-scatter (dV, dw) -> backward_keys (ds, dQ, dK), through the C ABI.  With N>1
-(torchrun) every rank runs an independent replica of the workload (values
-replicated per GPU: "replicas only", no data-path collective; scaling
-"weak").  Timing: CUDA events on the launching stream around every phase of
-every timed step; L2 is flushed (a 512 MiB write) before every step, outside
-the events; barrier + synchronize on both sides; max over ranks.
+Default workload: BASELINE.json configs[3] (C4), the configuration the metric
+("... at 1/2/4/8 B200") is quoted on: the row-sharded 2 GiB table through the
+library's record exchange at ANY N (N = 1 runs the same code path with one
+shard).  --gpus N > 1 without torchrun re-launches itself under torchrun (one
+process per GPU, NCCL process group, rank p owns rows [p n/P, (p+1) n/P)).
+A step = msn_pkm_forward_sharded (select a1-a4, route, gather a5, combine) +
+msn_pkm_backward_sharded (scatter a6, collect, backward_keys a7-a8) over the
+whole batch of 32,768 queries (strong scaling).  Timing: the step captured
+into a CUDA graph, replayed K times with CUDA events around each replay on the
+launching stream; L2 flushed (a 512 MiB write) before every replay, outside
+the events; barrier + synchronize on both sides; max over ranks.  Other
+workloads (C2, C3, C5, f4) run the unsharded path (replicas at N > 1).
 """
 from __future__ import annotations
 
@@ -539,74 +543,278 @@ def run_latency(args, rank, world, local_rank):
 
 
 def run_sharded(args, rank, world, local_rank):
-    """C4 (configs[3]): the row-sharded table, strong scaling (fixed total
-    batch B = 32,768 split over the ranks).  Phases timed with CUDA events;
-    value = total lookups / max-over-ranks step time."""
+    """C4 (configs[3], the metric's config): the row-sharded table through the
+    library's record exchange (a9) at ANY world size -- N = 1 runs the same
+    code path (one shard, the exchange to itself).  Strong scaling: the total
+    batch B = 32,768 is split over the ranks, rank p owns rows [p n/P,
+    (p+1) n/P).  A step = msn_pkm_forward_sharded + msn_pkm_backward_sharded
+    (peer transport: select, route, barrier, gather, barrier, combine;
+    d_out, barrier, scatter, barrier, collect, backward_keys), captured once
+    into a CUDA graph and replayed; value = total lookups / max-over-ranks
+    step time."""
     import torch.distributed as dist
     from paper_2602_07526_b200 import workloads as wl
     from paper_2602_07526_b200.distributed import ShardedPKM
+    from paper_2602_07526_b200.pkm import _ptr
+    from paper_2602_07526_b200._lib import check
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    if not dist.is_initialized():
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29612")
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     cfg = wl.CONFIGS[args.workload]
-    Q, K, V, dOut = wl.make_all(cfg, dev)  # every rank draws the same seeded tensors
     B_l = cfg.batch // world
+    Q, K, V, dOut = wl.make_all(cfg, dev)  # every rank draws the same seeded tensors
     sp = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l,
                     qk_dtype=cfg.qk_dtype, value_dtype=cfg.value_dtype, device=dev,
                     transport=args.transport)
     q_l = Q[rank * B_l:(rank + 1) * B_l].contiguous()
     d_l = dOut[rank * B_l:(rank + 1) * B_l].contiguous()
     Vs = sp.value_shard(V)
+    q_cpu_sample = Q[:512].cpu() if (rank == 0 and world == 1) else None
     del V, Q, dOut
+    torch.cuda.empty_cache()
+    lk, x = sp.ph, sp.xb.x
     dVs = torch.zeros((sp.rows, cfg.d_value), dtype=torch.float32, device=dev)
     dK = torch.zeros((cfg.heads, 2, cfg.n_sub, cfg.d_half), dtype=torch.float32, device=dev)
+    out = torch.empty((B_l, cfg.d_value), dtype=torch.float32, device=dev)
+    idx = torch.empty((B_l, cfg.heads, cfg.k), dtype=torch.int32, device=dev)
+    w = torch.empty((B_l, cfg.heads, cfg.k), dtype=torch.float32, device=dev)
+    dq = torch.empty((B_l, cfg.heads, 2, cfg.d_half), dtype=torch.float32, device=dev)
+    dw = torch.empty_like(w)
+    ws = sp.ws
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    launches = [0]
+    peer = args.transport == "peer"
 
-    def step():
-        out, tape = sp.forward(q_l, K, Vs)
-        sp.backward(d_l, q_l, K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
-        return out
+    def step(sp_=None):
+        if peer:
+            sptr = ctypes.c_void_p((sp_ or stream).cuda_stream)
+            check(lk.lib.msn_pkm_forward_sharded(lk._h, sptr, B_l, _ptr(q_l), _ptr(K), _ptr(Vs), ctypes.byref(x),
+                                                 _ptr(out), _ptr(idx), _ptr(w), _ptr(ws), ws.numel()))
+            n = lk.last_launch_count()
+            check(lk.lib.msn_pkm_backward_sharded(lk._h, sptr, B_l, _ptr(d_l), _ptr(q_l), _ptr(K), _ptr(Vs),
+                                                  _ptr(idx), _ptr(w), ctypes.byref(x), _ptr(dq), _ptr(dK),
+                                                  _ptr(dVs), _ptr(dw), _ptr(ws), ws.numel()))
+            launches[0] = n + lk.last_launch_count()
+        else:
+            o, tape = sp.forward(q_l, K, Vs)
+            sp.backward(d_l, q_l, K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
 
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # (1) per-phase breakdown (peer transport): the same kernels through the
+    # phase calls, CUDA events between them (eager; launch gaps included)
+    per, reduce_ms = {}, 0.0
+    phases = ["select", "cartesian", "route", "gather", "combine", "scatter", "backward_keys"]
+    if peer:
+        per = {p: 0.0 for p in phases}
+        nb = max(2, min(args.steps, 10))
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(nb)]
+        for e in evs:
+            for j in range(10):
+                e[j].record(stream)
+        torch.cuda.synchronize()
+        sptr = ctypes.c_void_p(stream.cuda_stream)
+        for e in evs:
+            flush.zero_()
+            e[0].record(stream)
+            arr = (ctypes.c_void_p * 2)(e[1].cuda_event, e[2].cuda_event)
+            check(lk.lib.msn_pkm_set_trace_events(lk._h, arr, 2))
+            check(lk.lib.msn_pkm_select(lk._h, sptr, B_l, _ptr(q_l), _ptr(K), _ptr(idx), _ptr(w), _ptr(ws),
+                                        ws.numel()))
+            check(lk.lib.msn_pkm_set_trace_events(lk._h, None, 0))
+            lk.exchange_route(idx, w, x)
+            lk.exchange_barrier(x)
+            e[3].record(stream)
+            lk.exchange_gather(Vs, x)
+            lk.exchange_barrier(x)
+            e[4].record(stream)
+            lk.exchange_combine(x, out)
+            e[5].record(stream)
+            sp.xb.region("DOUT", B_l, cfg.d_value).copy_(d_l)
+            lk.exchange_barrier(x)
+            arr = (ctypes.c_void_p * 2)(e[8].cuda_event, e[9].cuda_event)
+            check(lk.lib.msn_pkm_set_trace_events(lk._h, arr, 2))
+            lk.exchange_scatter(Vs, dVs, x, ws)
+            check(lk.lib.msn_pkm_set_trace_events(lk._h, None, 0))
+            lk.exchange_barrier(x)
+            e[6].record(stream)
+            lk.exchange_collect(idx, x, dw)
+            check(lk.lib.msn_pkm_backward_keys(lk._h, sptr, B_l, _ptr(q_l), _ptr(K), _ptr(idx), _ptr(w), _ptr(dw),
+                                               _ptr(dq), _ptr(dK), _ptr(ws), ws.numel()))
+            e[7].record(stream)
+        torch.cuda.synchronize()
+        order = [(0, 1, "select"), (1, 2, "cartesian"), (2, 3, "route"), (3, 4, "gather"), (4, 5, "combine"),
+                 (5, 6, "scatter"), (6, 7, "backward_keys")]
+        for e in evs:
+            for a, b, name in order:
+                per[name] += e[a].elapsed_time(e[b]) / nb
+        reduce_ms = sum(e[8].elapsed_time(e[9]) for e in evs) / nb
+    # (2) the timed region: the step captured into a CUDA graph, replayed K
+    # times, CUDA events around each replay, L2 flushed before each outside
+    graph = None
+    if peer:
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            step(cap)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            flush.zero_()
+            graph.replay()
+    gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     clocks = ClockSampler(dev.index or 0)
+    t_wall = time.perf_counter()
     with clocks:
         for i in range(args.steps):
             flush.zero_()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
+            gev[i][0].record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
+            gev[i][1].record(stream)
         torch.cuda.synchronize()
-    dist.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in gev) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    ctl = sp.xb.region("CTL", 64)
+    timeouts = int(ctl[17].item())
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        sp_e = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l, qk_dtype=cfg.qk_dtype,
+                          value_dtype=cfg.value_dtype, device=dev, transport=args.transport, dq_in_qk_dtype=True)
+        qh, dh = q_l.cpu().pin_memory(), d_l.cpu().pin_memory()
+        out_h = torch.empty((B_l, cfg.d_value), dtype=torch.float32).pin_memory()
+        dq_h = torch.empty((B_l, cfg.heads, 2, cfg.d_half), dtype=sp_e.ph.dq_dtype).pin_memory()
+        qd, dd = torch.empty_like(q_l), torch.empty_like(d_l)
+
+        def e2e_step():
+            qd.copy_(qh, non_blocking=True)
+            dd.copy_(dh, non_blocking=True)
+            o, tape = sp_e.forward(qd, K, Vs)
+            dq_e, _, _, _ = sp_e.backward(dd, qd, K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
+            out_h.copy_(o, non_blocking=True)
+            dq_h.copy_(dq_e, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(3, min(args.steps, 20))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
+        for i in range(n_e2e):
+            flush.zero_()
+            ev[i][0].record(stream)
+            e2e_step()
+            ev[i][1].record(stream)
+            torch.cuda.current_stream(dev).synchronize()  # the result is on the host
+        e2e_ms = sum(a.elapsed_time(b) for a, b in ev) / n_e2e
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = qh.numel() * qh.element_size() + dh.numel() * dh.element_size()
+        d2h = out_h.numel() * out_h.element_size() + dq_h.numel() * dq_h.element_size()
+        e2e = {"value": cfg.batch * cfg.heads / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": float(te.item()),
+               "note": "ShardedPKM forward+backward (msn_pkm_forward_sharded / msn_pkm_backward_sharded) fed from "
+                       "pinned host memory: H2D of the rank's queries and d_out, D2H of out (fp32) and d_query "
+                       "(bf16), one synchronisation per step; per-rank bytes"}
+        del sp_e
+
+    # slot-hit statistics (the workload describes itself) from this rank's tape
+    ab = algorithmic_bytes(cfg.scaled(batch=B_l), idx, "none")
+    uniq_local = None
+    if rank == 0:
+        loc = idx[(idx >= sp.row_begin) & (idx < sp.row_end)]
+        uniq_local = int(torch.unique(loc).numel())
     if rank != 0:
         return None
-    lookups = cfg.batch * cfg.heads
-    return {"metric": METRIC, "value": lookups / (ms / 1e3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": _dtype_name(cfg.value_dtype),
-            "data": "synthetic (seeded, BASELINE.json configs[3] recipe)",
-            "config": {"workload": cfg.name, "batch_total": cfg.batch, "batch_per_rank": B_l,
-                       "heads": cfg.heads, "n_sub": cfg.n_sub, "n_slots": cfg.n_slots,
-                       "rows_per_rank": sp.rows, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
-                       "parallelism": (f"row-sharded table x{world} (all-gather idx/w, reduce-scatter partials)"
-                                       if args.transport == "nccl" else
-                                       f"row-sharded table x{world} (all-gather idx/w, gather fused with the "
-                                       "reduce-scatter: partials pushed to the home rank over peer memory)"),
-                       "transport": args.transport,
-                       "l2": "flushed before every step (512 MiB write, outside the timed events)"},
-            "clocks": clocks.summary()}
+    peaks, peaks_kind = load_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    bf16_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+    esz = 2 if cfg.value_dtype == torch.bfloat16 else 4
+    HK = cfg.heads * cfg.k
+    contrib_l = B_l * HK
+    # algorithmic bytes per launch (DESIGN.md section 6): gather of the records:
+    # records (12 B) + value rows + the partial rows written; dV reducer: every
+    # touched row's V read once, dV read + written once (fp32), 12 B per record
+    # (row, w, query) + 4 B dw, + the d_out rows read once per (source, query)
+    rec_l = contrib_l  # records this rank receives (= sends, in expectation, uniform slots)
+    gather_b = rec_l * (12 + cfg.d_value * esz) + world * B_l * cfg.d_value * 4
+    scatter_b = (uniq_local or 0) * cfg.d_value * (esz + 8) + rec_l * 16 + world * B_l * cfg.d_value * 4
+    select_f = 4 * B_l * cfg.heads * cfg.n_sub * cfg.d_half
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload + "_xchg", {})
+    cands = {}
+    if peer:
+        cands = {
+            "gather": {"kernel": "gather_records_kernel (a5 over the received records, partials to the home)",
+                       "bound": "hbm", "ms": per["gather"], "work": gather_b, "peak": hbm, "unit": "GB/s",
+                       "traffic": traffic.get("gather")},
+            "dv_reduce": {"kernel": "grp_reduce_short_kernel (a6 over the received records: dV +=, dw)",
+                          "bound": "hbm", "ms": reduce_ms, "work": scatter_b, "peak": hbm, "unit": "GB/s",
+                          "traffic": traffic.get("dv_reduce")},
+            "select": {"kernel": "select_tc_kernel (a1+a2, tcgen05 bf16)", "bound": "tensor", "ms": per["select"],
+                       "work": select_f, "peak": bf16_peak, "unit": "TFLOP/s", "traffic": None},
+        }
+    rl = {}
+    for name, c in cands.items():
+        if c["ms"] <= 0:
+            continue
+        scale = 1e9 if c["unit"] == "GB/s" else 1e12
+        ach = c["work"] / (c["ms"] / 1e3) / scale
+        rl[name] = {"kernel": c["kernel"], "bound": c["bound"], "achieved": ach, "peak": c["peak"],
+                    "unit": c["unit"], "frac": ach / c["peak"], "traffic": c["traffic"], "ms": c["ms"],
+                    "algorithmic": c["work"], "peak_kind": peaks_kind}
+    roof = None
+    if rl:
+        dom = max(rl, key=lambda n_: rl[n_]["ms"])
+        roof = dict(rl[dom])
+        roof["dominant_of"] = sorted(rl)
+    total = sum(per.values()) or 1.0
+    kernels = {p: {"ms": per[p], "share": per[p] / total} for p in per}
+    kernels["rooflines"] = rl
+    kernels["dv_reduce_ms"] = reduce_ms
+    res = {"metric": METRIC, "value": cfg.batch * cfg.heads / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": _dtype_name(cfg.value_dtype),
+           "data": "synthetic (seeded, BASELINE.json configs[3] recipe, DESIGN.md Inputs)",
+           "timing": ("timed region: the sharded step (msn_pkm_forward_sharded + msn_pkm_backward_sharded, every "
+                      "kernel and barrier) replayed from a CUDA graph, CUDA events around each replay, max over "
+                      "ranks; kernels{} = an eager pass through the phase calls with events between them"
+                      if peer else "eager steps (NCCL transport: one host read of the record counts per step)"),
+           "config": {"workload": cfg.name, "batch_total": cfg.batch, "batch_per_rank": B_l,
+                      "heads": cfg.heads, "n_sub": cfg.n_sub, "n_slots": cfg.n_slots,
+                      "rows_per_rank": sp.rows, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k,
+                      "parallelism": f"row-sharded table x{world}: records all-to-all, partials returned "
+                                     f"({'peer memory, fused into the route/gather/scatter kernels' if peer else 'NCCL'})",
+                      "transport": args.transport,
+                      "slot_hits_rank0": ab.get("skew"), "unique_local_rows_rank0": uniq_local,
+                      "l2": "flushed before every step (512 MiB write, outside the timed events)"},
+           "roofline": roof, "kernels": kernels, "gpu_launches": launches[0] * args.steps,
+           "clocks": clocks.summary(), "e2e": e2e, "wall_s_timed_region": t_wall,
+           "barrier_timeouts": timeouts}
+    if world == 1 and not args.no_cpu_baseline:
+        from paper_2602_07526_b200 import workloads as wl2
+        Kc = K.cpu()
+        Vc = wl2.make_values(cfg, "cpu")
+        dc = wl2.make_dout(cfg, "cpu", batch=512)
+        res["cpu_baseline"] = cpu_baseline(cfg, q_cpu_sample, Kc, Vc, dc, queries=512)
+    return res
 
 
 def cpu_baseline(cfg, Q, K, V, dOut, queries=None):
@@ -688,13 +896,16 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="c2_mid_bf16")
+    ap.add_argument("--workload", default="c4_large_sharded_bf16",
+                    help="BASELINE.json configs: c4_large_sharded_bf16 (default: the metric's config, the "
+                         "row-sharded table at any N), c2_mid_bf16, c3_train_fp32_zipf, c5_latency_bf16, f4_*")
     ap.add_argument("--atomic", action="store_true", help="atomic (non-deterministic) dV scatter")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sharded", action="store_true", help="C4 through the row-sharded path even at N=1")
-    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
-                    help="row-sharded forward: NCCL reduce-scatter, or the gather pushing partials to peers")
+    ap.add_argument("--unsharded", action="store_true",
+                    help="C4 through the unsharded single-GPU path (msn_pkm_forward/backward) instead")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="row-sharded exchange: peer memory inside the library's kernels (default), or NCCL")
     ap.add_argument("--prologue", action="store_true",
                     help="include LayerNorm(q), K~ = Theta LayerNorm(k) and their backward (SURVEY 8(f) f2)")
     ap.add_argument("--update", choices=["none", "sgd", "adagrad"], default="none",
@@ -704,10 +915,21 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
+        # the fp64 oracle on the host cores, rank 0 only (other ranks: no work)
         res = run_reference(args, rank, world)
         if res is not None:
             print(json.dumps(res), flush=True)
@@ -718,7 +940,7 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.workload.startswith("c5"):
         res = run_latency(args, rank, world, local_rank)
-    elif args.workload.startswith("c4") and (world > 1 or args.sharded):
+    elif args.workload.startswith("c4") and not args.unsharded:
         res = run_sharded(args, rank, world, local_rank)
     else:
         res = run_ours(args, rank, world, local_rank)

@@ -58,7 +58,8 @@
 extern "C" {
 #endif
 
-#define MSN_PKM_ABI_VERSION 1
+#define MSN_PKM_ABI_VERSION 2
+#define MSN_MAX_WORLD 8 /* ranks of one NVLink/NVSwitch node (8 x B200) */
 
 typedef enum {
   MSN_OK = 0,
@@ -123,6 +124,14 @@ typedef struct {
                           and the deterministic backward. */
   int64_t row_begin;   /* this process holds value rows [row_begin, row_end) */
   int64_t row_end;     /* (row-sharded table); 0 and n_sub^2 when unsharded */
+  int32_t world_size;  /* P: 0 or 1 = no record exchange (the rows are row_begin..row_end);
+                          2 <= P <= MSN_MAX_WORLD = the row-sharded table with the
+                          library's record exchange (BASELINE.json
+                          configs[3]): this rank holds rows [rank n/P, (rank+1) n/P),
+                          n % P == 0, and row_begin/row_end must be 0/0 or exactly that
+                          range.  A P = 1 exchange (the same sharded code path on one
+                          GPU) is world_size = 1 with the msn_pkm_exchange calls. */
+  int32_t rank;        /* 0 <= rank < max(world_size, 1) */
 } msn_pkm_config;
 
 /* Create / destroy a handle.  create validates the config. */
@@ -220,12 +229,10 @@ msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B,
                             float* d_query, float* d_subkeys, float* d_values, float* dw,
                             void* workspace, size_t workspace_bytes);
 
-/* ---- phase entry points (the row-sharded table, BASELINE.json configs[3]).
- * A sharded step is: select (local queries) -> all-gather idx/weights ->
- * gather (all queries, local rows) -> reduce-scatter of the partial outputs;
- * backward: all-gather d_out -> scatter (all queries, local rows) ->
- * reduce-scatter of dw -> backward_keys (local queries).  The collectives are
- * the caller's (torch.distributed over NCCL). */
+/* ---- phase entry points: the steps of forward / backward one at a time
+ * (select = a1-a4, gather = a5, scatter = a6, backward_keys = a7-a8), over
+ * the handle's rows [row_begin, row_end); slots outside them contribute 0.
+ * The row-sharded table's exchange has its own calls (msn_pkm_exchange_*). */
 
 /* a1-a4: idx, weights for B queries. */
 msn_status msn_pkm_select(msn_pkm_t h, void* stream, int64_t B,
@@ -238,30 +245,6 @@ msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B,
                           const int32_t* idx, const float* weights, const void* values,
                           float* out);
 
-/* a5 over the local rows FUSED WITH THE REDUCE-SCATTER (peer-memory push,
- * NVLink): B = world * local_batch queries in rank-major order (the
- * all-gathered idx / weights); the partial row of query b -- the same sum
- * msn_pkm_gather computes -- is stored into its home rank's receive buffer
- *   peer_recv[p][((rank * local_batch + b % local_batch) * G + g) * d_value + e],
- *   p = b / local_batch, G = head_groups,
- * where peer_recv is a DEVICE array of world pointers to [world, local_batch,
- * G, d_value] fp32 receive buffers mapped into this process (CUDA IPC /
- * symmetric memory; plain local buffers when ranks are emulated on one GPU).
- * Every receive slot is written by exactly one rank.  The caller orders the
- * pushes of all ranks before msn_pkm_reduce_partials (a cross-rank barrier).
- * MSN_ERR_UNSUPPORTED if heads * k > 512. */
-msn_status msn_pkm_gather_push(msn_pkm_t h, void* stream, int64_t B,
-                               const int32_t* idx, const float* weights, const void* values,
-                               float* const* peer_recv, int32_t world, int32_t rank,
-                               int64_t local_batch);
-
-/* out[b] = sum_{p = 0 .. world-1} recv[p][b]  in rank order (written, =):
- * the home rank's half of the fused reduce-scatter.  recv [world,
- * local_batch, G, d_value] fp32 (this rank's receive buffer), out
- * [local_batch, G, d_value] fp32; deterministic, independent of arrival order. */
-msn_status msn_pkm_reduce_partials(msn_pkm_t h, void* stream, int64_t local_batch, int32_t world,
-                                   const float* recv, float* out);
-
 /* a6 over the local rows: d_values += w * d_out[b] and dw = <values[idx], d_out[b]>
  * for local slots (dw = 0 for slots held by other ranks). */
 msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B,
@@ -269,32 +252,131 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B,
                            const void* values, float* d_values, float* dw,
                            void* workspace, size_t workspace_bytes);
 
-/* a6 over the local rows for the row-sharded table OVER PEER MEMORY (no
- * all-gather of d_out, no reduce-scatter of dw): B = world * local_batch
- * queries in rank-major order (the all-gathered idx / weights); the d_out
- * row of query b is read from its home rank's buffer
- *   peer_d_out[p][(b % local_batch) * G * d_value ...],  p = b / local_batch,
- * and dw of its slot (b, h, t) held by this rank is stored into
- *   peer_dw[p][((b % local_batch) * heads + h) * k + t]
- * (every element has exactly one owner rank, so the home buffers need no
- * zeroing or summation).  peer_d_out / peer_dw: DEVICE arrays of world
- * pointers to [local_batch, G, d_value] fp32 / [local_batch, heads, k] fp32
- * buffers mapped into this process.  d_values += as msn_pkm_scatter.  The
- * caller orders the d_out writes of all ranks before, and every rank's call
- * before the dw reads (cross-rank barriers).  Deterministic grouped path
- * only (MSN_ERR_UNSUPPORTED with MSN_FLAG_ATOMIC_BWD). */
-msn_status msn_pkm_scatter_p2p(msn_pkm_t h, void* stream, int64_t B,
-                               const int32_t* idx, const float* weights,
-                               const float* const* peer_d_out, const void* values,
-                               float* d_values, float* const* peer_dw, int32_t world,
-                               int64_t local_batch, void* workspace, size_t workspace_bytes);
-
 /* a7-a8 given the full dw: d_query (=) and d_subkeys (+=). */
 msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B,
                                  const void* query, const void* subkeys,
                                  const int32_t* idx, const float* weights, const float* dw,
                                  float* d_query, float* d_subkeys,
                                  void* workspace, size_t workspace_bytes);
+
+/* ---- the row-sharded table with the library's record exchange (a9;
+ * SURVEY.md 8(e); north_star: "row-sharded across the 8xB200 box, with ...
+ * index all-to-all and partial-sum return"; BASELINE.json configs[3]).
+ *
+ * Rank p is home to its local_batch = B_l queries and owns value rows
+ * [p n/P, (p+1) n/P) (owner(f) = f / (n/P)); the sub-keys are replicated.
+ *   forward   select (a1-a4, local queries) -> ROUTE: every (b, h, t) slot becomes
+ *             a record {local row, w, b} sent to its owner (all-to-all of records,
+ *             12 B each, grouped by query) -> GATHER: every owner sums w V[row]
+ *             over the records of each (source, query) into a partial row and
+ *             returns it to the source (all-to-all of partials) -> COMBINE: the
+ *             home adds the P partials in owner order.
+ *   backward  every owner reads the d_out rows its records need (from the home's
+ *             DOUT region), SCATTERs (dV shard +=, dw per record, the same grouped
+ *             deterministic reduction as msn_pkm_scatter, records summed in global
+ *             contribution order -> dV shards bitwise equal to the unsharded dV)
+ *             and returns dw per record -> COLLECT: the home puts dw back in
+ *             (b, h, t) order -> backward_keys (a7-a8) on the local queries.
+ * Every rank has one exchange buffer of msn_pkm_exchange_layout() bytes (the
+ * caller allocates it; zero-filled once before first use).  Two transports:
+ *   MSN_XCHG_PEER   base[p] is rank p's buffer mapped into this process (torch
+ *                   symmetric memory / CUDA IPC, NVLink peer memory): ROUTE,
+ *                   GATHER and SCATTER store straight into the peers' IN regions
+ *                   (the transfer is issued by the compute kernel, row by row),
+ *                   msn_pkm_exchange_barrier orders the ranks (device-side flags,
+ *                   no host sync: graph-capturable).  msn_pkm_forward_sharded /
+ *                   msn_pkm_backward_sharded run the whole step.
+ *   MSN_XCHG_STAGED only base[rank] is used: outgoing data is staged in the OUT
+ *                   regions (segment p for rank p) and the caller moves them
+ *                   with its collectives (NCCL all-to-all(v) over NVLink):
+ *                   OUT_ROW/OUT_W/OUT_Q segment p (CTL counts[p] records) ->
+ *                   rank p's IN_* segment [rank]; OUT_OFF -> IN_OFF; PART_OUT ->
+ *                   PART_IN; DW_OUT segment p (the IN counts) -> DW_IN; the
+ *                   caller all-gathers the homes' d_out into DOUT_ALL.
+ * Region layout of one exchange buffer (cap = B_l * heads * k records per
+ * (source, owner) pair; offsets from msn_pkm_exchange_layout, 256-B aligned): */
+enum {
+  MSN_XREG_IN_ROW = 0,  /* int32 [P][cap]  local row of the records source s sent here */
+  MSN_XREG_IN_W,        /* fp32  [P][cap]  their weights */
+  MSN_XREG_IN_Q,        /* int32 [P][cap]  their query (index in the source's batch) */
+  MSN_XREG_IN_OFF,      /* int32 [P][B_l+1] per-query record offsets of segment s ([B_l] = count) */
+  MSN_XREG_PART_IN,     /* fp32  [P][B_l][d_value] partial sums returned by owner o */
+  MSN_XREG_DOUT,        /* fp32  [B_l][d_value] this home's d_out (read by the owners) */
+  MSN_XREG_DW_IN,       /* fp32  [P][cap]  dw returned by owner o, in this home's record order */
+  MSN_XREG_POS,         /* int32 [B_l*H*k] slot (b,h,t) -> its record's position in owner's segment */
+  MSN_XREG_CTL,         /* uint32 [64]: [0,P) barrier flags, [16] epoch, [17] barrier timeout,
+                           [32, 32+P) records this rank sent to owner p (counts) */
+  MSN_XREG_SCRATCH,     /* int32 [2][P][B_l+1] route scratch (local) */
+  MSN_XREG_OUT_ROW,     /* STAGED only: int32 [P][cap] records for owner p */
+  MSN_XREG_OUT_W,       /*   fp32  [P][cap] */
+  MSN_XREG_OUT_Q,       /*   int32 [P][cap] */
+  MSN_XREG_OUT_OFF,     /*   int32 [P][B_l+1] */
+  MSN_XREG_PART_OUT,    /*   fp32  [P][B_l][d_value] partials for home s */
+  MSN_XREG_DOUT_ALL,    /*   fp32  [P][B_l][d_value] every home's d_out (all-gathered) */
+  MSN_XREG_DW_OUT,      /*   fp32  [P][cap] dw for home s, in s's record order */
+  MSN_XREG_COUNT
+};
+typedef enum { MSN_XCHG_PEER = 0, MSN_XCHG_STAGED = 1 } msn_exchange_transport;
+typedef struct {
+  int32_t transport;    /* msn_exchange_transport */
+  int32_t world;        /* P = max(config world_size, 1) */
+  int32_t rank;         /* = config rank */
+  int64_t local_batch;  /* B_l, the same on every rank */
+  void* base[MSN_MAX_WORLD]; /* DEVICE pointers: base[p] = rank p's exchange buffer
+                                (PEER: all P mapped here; STAGED: base[rank] only) */
+} msn_pkm_exchange;
+
+/* Byte offsets of the regions (offsets[MSN_XREG_COUNT], may be NULL) and the
+ * total size of one exchange buffer for this handle and local_batch (STAGED
+ * regions included when staged != 0). */
+msn_status msn_pkm_exchange_layout(msn_pkm_t h, int64_t local_batch, int32_t staged,
+                                   int64_t* offsets, size_t* bytes);
+
+/* The whole sharded forward (PEER transport): select a1-a4 on the B_l local
+ * queries, ROUTE, barrier, GATHER, barrier, COMBINE.  values = this rank's
+ * rows [n/P, d_value]; out [B_l, d_value] fp32 (=); idx / weights [B_l,H,k]
+ * (the tape, global slot ids).  Every rank calls it with the same B_l. */
+msn_status msn_pkm_forward_sharded(msn_pkm_t h, void* stream, int64_t local_batch, const void* query,
+                                   const void* subkeys, const void* values, const msn_pkm_exchange* x,
+                                   float* out, int32_t* idx, float* weights, void* workspace,
+                                   size_t workspace_bytes);
+/* The whole sharded backward (PEER transport): d_out -> DOUT, barrier,
+ * SCATTER (d_values += for this rank's rows), barrier, COLLECT (dw [B_l,H,k],
+ * may be NULL), backward_keys (d_query =, d_subkeys += for the local
+ * queries).  Workspace: msn_pkm_workspace_size(h, B_l, P * B_l). */
+msn_status msn_pkm_backward_sharded(msn_pkm_t h, void* stream, int64_t local_batch, const float* d_out,
+                                    const void* query, const void* subkeys, const void* values,
+                                    const int32_t* idx, const float* weights, const msn_pkm_exchange* x,
+                                    float* d_query, float* d_subkeys, float* d_values, float* dw,
+                                    void* workspace, size_t workspace_bytes);
+
+/* The phases (both transports; the STAGED caller moves the data in between;
+ * ranks emulated on one GPU call them rank by rank, no barrier needed). */
+/* ROUTE: idx/weights [B_l,H,k] of this rank's queries -> records into every
+ * owner's IN segment [rank] (PEER) or OUT segment [owner] (STAGED), per-query
+ * offsets likewise, POS, and CTL counts. */
+msn_status msn_pkm_exchange_route(msn_pkm_t h, void* stream, const int32_t* idx, const float* weights,
+                                  const msn_pkm_exchange* x);
+/* GATHER: for every source s and query b, the partial sum of w V[row] over the
+ * records in IN segment s -> PART_IN[rank][b] of rank s (PEER) or PART_OUT[s][b]
+ * (STAGED); zeros for a query without records here. */
+msn_status msn_pkm_exchange_gather(msn_pkm_t h, void* stream, const void* values, const msn_pkm_exchange* x);
+/* COMBINE: out[b] = sum_o PART_IN[o][b], o ascending (=). */
+msn_status msn_pkm_exchange_combine(msn_pkm_t h, void* stream, const msn_pkm_exchange* x, float* out);
+/* SCATTER: dV shard (+=) and dw of every record in the IN segments, d_out rows
+ * from the homes' DOUT (PEER) or DOUT_ALL (STAGED); dw -> DW_IN[rank] of the
+ * home (PEER) or DW_OUT[s] (STAGED).  Workspace as msn_pkm_backward_sharded. */
+msn_status msn_pkm_exchange_scatter(msn_pkm_t h, void* stream, const void* values, float* d_values,
+                                    const msn_pkm_exchange* x, void* workspace, size_t workspace_bytes);
+/* COLLECT: dw[b,h,t] = DW_IN[owner][POS[b,h,t]] (=). */
+msn_status msn_pkm_exchange_collect(msn_pkm_t h, void* stream, const int32_t* idx,
+                                    const msn_pkm_exchange* x, float* dw);
+/* Device-side barrier over the P ranks (PEER): release-store of an epoch into
+ * every rank's CTL flag [rank], then acquire-spin until all P flags of this
+ * rank reach it.  Bounded: a rank that waits more than 10 s (a peer that
+ * never arrives) sets CTL[17] = 1 and returns instead of hanging the GPU;
+ * the results of that step are then invalid (the caller may check CTL[17]). */
+msn_status msn_pkm_exchange_barrier(msn_pkm_t h, void* stream, const msn_pkm_exchange* x);
 
 /* Tape check (SURVEY 8(b) "Errors"): *bad (DEVICE int32, written =, zeroed
  * on the stream first) = the number of slots (b, h, t) of idx / weights

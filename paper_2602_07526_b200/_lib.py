@@ -12,7 +12,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MSN_LIB: an alternative build of the same library (A/B measurements only)
 LIB_PATH = os.environ.get("MSN_LIB", os.path.join(_HERE, "libmsn_pkm.so"))
 
-ABI_VERSION = 1
+ABI_VERSION = 2
+MAX_WORLD = 8
 MSN_F32, MSN_BF16 = 0, 1
 FLAG_ATOMIC_BWD = 0x1
 FLAG_GROUP_TABLES = 0x2
@@ -38,7 +39,18 @@ class Config(ctypes.Structure):
                 ("max_batch", ctypes.c_int64), ("qk_dtype", ctypes.c_int32),
                 ("value_dtype", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("head_groups", ctypes.c_int32), ("row_begin", ctypes.c_int64),
-                ("row_end", ctypes.c_int64)]
+                ("row_end", ctypes.c_int64), ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+# msn_pkm_exchange (a9, the row-sharded table's record exchange)
+XCHG_PEER, XCHG_STAGED = 0, 1
+XREG = ["IN_ROW", "IN_W", "IN_Q", "IN_OFF", "PART_IN", "DOUT", "DW_IN", "POS", "CTL", "SCRATCH",
+        "OUT_ROW", "OUT_W", "OUT_Q", "OUT_OFF", "PART_OUT", "DOUT_ALL", "DW_OUT"]
+
+
+class Exchange(ctypes.Structure):
+    _fields_ = [("transport", ctypes.c_int32), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("local_batch", ctypes.c_int64), ("base", ctypes.c_void_p * MAX_WORLD)]
 
 
 # name -> argtypes (all return msn_status except where noted)
@@ -59,9 +71,16 @@ SIGNATURES = {
     "msn_pkm_backward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_select": [_P, _P, _I64, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_gather": [_P, _P, _I64, _P, _P, _P, _P],
-    "msn_pkm_gather_push": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _I64],
-    "msn_pkm_reduce_partials": [_P, _P, _I64, ctypes.c_int32, _P, _P],
-    "msn_pkm_scatter_p2p": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int32, _I64, _P, _SZ],
+    "msn_pkm_exchange_layout": [_P, _I64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_SZ)],
+    "msn_pkm_forward_sharded": [_P, _P, _I64, _P, _P, _P, ctypes.POINTER(Exchange), _P, _P, _P, _P, _SZ],
+    "msn_pkm_backward_sharded": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Exchange), _P, _P, _P,
+                                 _P, _P, _SZ],
+    "msn_pkm_exchange_route": [_P, _P, _P, _P, ctypes.POINTER(Exchange)],
+    "msn_pkm_exchange_gather": [_P, _P, _P, ctypes.POINTER(Exchange)],
+    "msn_pkm_exchange_combine": [_P, _P, ctypes.POINTER(Exchange), _P],
+    "msn_pkm_exchange_scatter": [_P, _P, _P, _P, ctypes.POINTER(Exchange), _P, _SZ],
+    "msn_pkm_exchange_collect": [_P, _P, _P, ctypes.POINTER(Exchange), _P],
+    "msn_pkm_exchange_barrier": [_P, _P, ctypes.POINTER(Exchange)],
     "msn_pkm_validate_tape": [_P, _P, _I64, _P, _P, _P],
     "msn_pkm_scatter": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_backward_keys": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],

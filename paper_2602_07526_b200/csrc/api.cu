@@ -209,6 +209,25 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
     return fail(MSN_ERR_INVALID_ARG, "head_groups must be >= 0 and divide heads");
   const int64_t n = (int64_t)c->n_sub * c->n_sub * ((c->flags & MSN_FLAG_GROUP_TABLES) ? G : 1);
   if (n >= (int64_t(1) << 31)) return fail(MSN_ERR_INVALID_ARG, "table rows must be < 2^31");
+  if (c->world_size < 0 || c->world_size > MSN_MAX_WORLD)
+    return fail(MSN_ERR_INVALID_ARG, "world_size %d not in [0, %d]", c->world_size, MSN_MAX_WORLD);
+  if (c->rank < 0 || c->rank >= (c->world_size > 1 ? c->world_size : 1))
+    return fail(MSN_ERR_INVALID_ARG, "rank %d outside [0, world_size)", c->rank);
+  msn_pkm_config cc = *c;
+  if (c->world_size > 1) {  // the row-sharded table: rank r owns rows [r n/P, (r+1) n/P)
+    if (n % c->world_size)
+      return fail(MSN_ERR_INVALID_ARG, "table rows %lld not divisible by world_size %d", (long long)n,
+                  c->world_size);
+    if (G > 1) return fail(MSN_ERR_UNSUPPORTED, "head groups need the unsharded table");
+    const int64_t rpr = n / c->world_size;
+    if (!(c->row_begin == 0 && c->row_end == 0) &&
+        !(c->row_begin == c->rank * rpr && c->row_end == (c->rank + 1) * rpr))
+      return fail(MSN_ERR_INVALID_ARG, "row_begin/row_end must be 0/0 or rank's rows [%lld, %lld)",
+                  (long long)(c->rank * rpr), (long long)((c->rank + 1) * rpr));
+    cc.row_begin = c->rank * rpr;
+    cc.row_end = (c->rank + 1) * rpr;
+  }
+  c = &cc;
   if (c->row_begin < 0 || c->row_end > n || c->row_begin >= c->row_end)
     return fail(MSN_ERR_INVALID_ARG, "need 0 <= row_begin < row_end <= table rows");
   if (G > 1 && (c->row_begin != 0 || c->row_end != n))
@@ -298,50 +317,6 @@ msn_status msn_pkm_gather(msn_pkm_t h, void* stream, int64_t B, const int32_t* i
   cudaError_t e = launch_gather(s, idx, weights, values, out, (cudaStream_t)stream,
                                 &h->last_launches);
   if (e != cudaSuccess) return cuda_fail(e, "gather");
-  return MSN_OK;
-}
-
-msn_status msn_pkm_gather_push(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
-                               const float* weights, const void* values, float* const* peer_recv,
-                               int32_t world, int32_t rank, int64_t local_batch) {
-  msn_status st = check_handle(h);
-  if (st) return st;
-  h->last_launches = 0;
-  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
-  if (world < 1 || rank < 0 || rank >= world)
-    return fail(MSN_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
-  if (local_batch < 1 || B != (int64_t)world * local_batch)
-    return fail(MSN_ERR_INVALID_ARG, "B = %lld must equal world * local_batch = %d * %lld", (long long)B,
-                world, (long long)local_batch);
-  REQUIRE_PTR(idx);
-  REQUIRE_PTR(weights);
-  REQUIRE_PTR(values);
-  if (!peer_recv) return fail(MSN_ERR_INVALID_ARG, "peer_recv is NULL");
-  if ((st = check_tape(h, stream, B, idx, weights))) return st;
-  const Shape s = shape_of(h->cfg, B);
-  Push push;
-  push.peers = peer_recv;
-  push.rank = rank;
-  push.lb = local_batch;
-  cudaError_t e = launch_gather_push(s, idx, weights, values, push, (cudaStream_t)stream, &h->last_launches);
-  if (e == cudaErrorNotSupported) return fail(MSN_ERR_UNSUPPORTED, "gather_push: heads * k > 512");
-  if (e != cudaSuccess) return cuda_fail(e, "gather_push");
-  return MSN_OK;
-}
-
-msn_status msn_pkm_reduce_partials(msn_pkm_t h, void* stream, int64_t local_batch, int32_t world,
-                                   const float* recv, float* out) {
-  msn_status st = check_handle(h);
-  if (st) return st;
-  h->last_launches = 0;
-  if (local_batch < 0 || world < 1) return fail(MSN_ERR_INVALID_ARG, "local_batch / world");
-  if (local_batch == 0) return MSN_OK;
-  REQUIRE_PTR(recv);
-  REQUIRE_PTR(out);
-  const Shape s = shape_of(h->cfg, local_batch);
-  cudaError_t e = launch_reduce_partials(recv, world, local_batch, s.og, s.d_v, out, (cudaStream_t)stream,
-                                         &h->last_launches);
-  if (e != cudaSuccess) return cuda_fail(e, "reduce_partials");
   return MSN_OK;
 }
 
@@ -481,43 +456,6 @@ msn_status msn_pkm_scatter(msn_pkm_t h, void* stream, int64_t B, const int32_t* 
   return MSN_OK;
 }
 
-msn_status msn_pkm_scatter_p2p(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
-                               const float* weights, const float* const* peer_d_out, const void* values,
-                               float* d_values, float* const* peer_dw, int32_t world,
-                               int64_t local_batch, void* workspace, size_t workspace_bytes) {
-  msn_status st = check_handle(h);
-  if (st) return st;
-  h->last_launches = 0;
-  if (B < 0) return fail(MSN_ERR_INVALID_ARG, "B < 0");
-  if (world < 1 || local_batch < 1 || B != (int64_t)world * local_batch)
-    return fail(MSN_ERR_INVALID_ARG, "B = %lld must equal world * local_batch = %d * %lld", (long long)B,
-                world, (long long)local_batch);
-  if (h->cfg.flags & MSN_FLAG_ATOMIC_BWD)
-    return fail(MSN_ERR_UNSUPPORTED, "scatter_p2p runs the deterministic grouped backward only");
-  REQUIRE_PTR(idx);
-  REQUIRE_PTR(weights);
-  REQUIRE_PTR(values);
-  REQUIRE_PTR(d_values);
-  REQUIRE_PTR(workspace);
-  if (!peer_d_out || !peer_dw) return fail(MSN_ERR_INVALID_ARG, "peer_d_out / peer_dw is NULL");
-  if ((st = check_bwd_shape(h, true, false))) return st;
-  if ((st = check_tape(h, stream, B, idx, weights))) return st;
-  const Shape s = shape_of(h->cfg, B);
-  const size_t need = bwd_workspace_bytes(shape_of(h->cfg, 0), B);
-  if (workspace_bytes < need)
-    return fail(MSN_ERR_WORKSPACE, "scatter workspace %zu < %zu bytes", workspace_bytes, need);
-  const BwdWorkspace ws = carve_bwd_workspace(shape_of(h->cfg, 0), B, workspace);
-  ScatterPeers peers;
-  peers.d_out = peer_d_out;
-  peers.dw = peer_dw;
-  peers.local_batch = local_batch;
-  cudaError_t e = launch_scatter_sorted(s, idx, weights, nullptr, values, d_values, nullptr, ws,
-                                        (cudaStream_t)stream, &h->last_launches,
-                                        TraceEvents{h->trace, h->ntrace}, 0, 0.f, 0.f, nullptr, &peers);
-  if (e != cudaSuccess) return cuda_fail(e, "scatter_p2p (dV, dw)");
-  return MSN_OK;
-}
-
 msn_status msn_pkm_scatter_update(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx,
                                   const float* weights, const float* d_out, void* values,
                                   int32_t update, float lr, float eps, float* state, float* dw,
@@ -629,6 +567,364 @@ msn_status msn_pkm_backward(msn_pkm_t h, void* stream, int64_t B, const float* d
   return MSN_OK;
 }
 
+
+// ------------------------------------------- a9 record exchange (sharded) --
+}  // extern "C"
+namespace {
+
+struct XLayout {
+  int64_t off[MSN_XREG_COUNT + 1];  // byte offsets; off[COUNT] = total
+};
+
+XLayout xlayout(const msn_pkm_config& c, int P, int64_t lb, bool staged) {
+  const int64_t cap = lb * c.heads * c.k, dv = c.d_value;
+  int64_t sz[MSN_XREG_COUNT] = {};
+  sz[MSN_XREG_IN_ROW] = sz[MSN_XREG_IN_W] = sz[MSN_XREG_IN_Q] = sz[MSN_XREG_DW_IN] = 4 * P * cap;
+  sz[MSN_XREG_IN_OFF] = 4 * P * (lb + 1);
+  sz[MSN_XREG_PART_IN] = 4 * P * lb * dv;
+  sz[MSN_XREG_DOUT] = 4 * lb * dv;
+  sz[MSN_XREG_POS] = 4 * cap;
+  sz[MSN_XREG_CTL] = 4 * 64;
+  sz[MSN_XREG_SCRATCH] = 4 * 2 * P * (lb + 1);
+  if (staged) {
+    sz[MSN_XREG_OUT_ROW] = sz[MSN_XREG_OUT_W] = sz[MSN_XREG_OUT_Q] = sz[MSN_XREG_DW_OUT] = 4 * P * cap;
+    sz[MSN_XREG_OUT_OFF] = 4 * P * (lb + 1);
+    sz[MSN_XREG_PART_OUT] = sz[MSN_XREG_DOUT_ALL] = 4 * P * lb * dv;
+  }
+  XLayout L;
+  int64_t o = 0;
+  for (int r = 0; r < MSN_XREG_COUNT; ++r) {
+    L.off[r] = o;
+    o += (int64_t)align256((size_t)sz[r]);
+  }
+  L.off[MSN_XREG_COUNT] = o;
+  return L;
+}
+
+// The per-call view of the exchange: sizes and every pointer a phase needs.
+struct XView {
+  int P, rank;
+  bool staged;
+  int64_t lb, cap, rpr;
+  XLayout L;
+  const msn_pkm_exchange* x;
+  template <typename T>
+  T* reg(int p, int r) const { return (T*)((char*)x->base[p] + L.off[r]); }
+  template <typename T>
+  T* own(int r) const { return reg<T>(rank, r); }
+  RecordsIn records_in() const {
+    RecordsIn ri;
+    ri.P = P;
+    ri.lb = lb;
+    ri.cap = cap;
+    ri.row = own<int32_t>(MSN_XREG_IN_ROW);
+    ri.q = own<int32_t>(MSN_XREG_IN_Q);
+    ri.off = own<int32_t>(MSN_XREG_IN_OFF);
+    ri.w = own<float>(MSN_XREG_IN_W);
+    return ri;
+  }
+};
+
+msn_status make_view(msn_pkm_t h, const msn_pkm_exchange* x, XView& v) {
+  if (!x) return fail(MSN_ERR_INVALID_ARG, "exchange is NULL");
+  const msn_pkm_config& c = h->cfg;
+  const int P = c.world_size > 1 ? c.world_size : 1;
+  if (x->world != P || x->rank != c.rank)
+    return fail(MSN_ERR_INVALID_ARG, "exchange world/rank %d/%d != config %d/%d", x->world, x->rank, P, c.rank);
+  if (x->transport != MSN_XCHG_PEER && x->transport != MSN_XCHG_STAGED)
+    return fail(MSN_ERR_INVALID_ARG, "exchange transport %d", x->transport);
+  if (x->local_batch < 0 || x->local_batch > c.max_batch)
+    return fail(MSN_ERR_INVALID_ARG, "local_batch %lld outside [0, max_batch]", (long long)x->local_batch);
+  if (c.head_groups > 1) return fail(MSN_ERR_UNSUPPORTED, "the exchange needs head_groups <= 1");
+  if (c.heads * c.k > 512) return fail(MSN_ERR_UNSUPPORTED, "the exchange needs heads * k <= 512");
+  if (c.flags & (MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES))
+    return fail(MSN_ERR_UNSUPPORTED, "the exchange runs the deterministic backward over one table");
+  const int64_t n = (int64_t)c.n_sub * c.n_sub;
+  if (c.row_begin != (int64_t)c.rank * (n / P) || c.row_end != (int64_t)(c.rank + 1) * (n / P))
+    return fail(MSN_ERR_INVALID_ARG, "the exchange needs the rank's rows [rank n/P, (rank+1) n/P)");
+  const bool staged = x->transport == MSN_XCHG_STAGED;
+  for (int p = 0; p < P; ++p) {
+    if (staged && p != c.rank) continue;
+    if (!x->base[p] || ((uintptr_t)x->base[p] & 255u))
+      return fail(MSN_ERR_INVALID_ARG, "exchange base[%d] is NULL or not 256-byte aligned", p);
+  }
+  v.P = P;
+  v.rank = c.rank;
+  v.staged = staged;
+  v.lb = x->local_batch;
+  v.cap = v.lb * c.heads * c.k;
+  v.rpr = n / P;
+  v.L = xlayout(c, P, v.lb, staged);
+  v.x = x;
+  return MSN_OK;
+}
+
+cudaError_t x_route(msn_pkm_t h, const XView& v, const int32_t* idx, const float* w, cudaStream_t st, int* L) {
+  RouteArgs a;
+  a.P = v.P;
+  a.lb = v.lb;
+  a.rpr = v.rpr;
+  for (int o = 0; o < kMaxWorld; ++o) {
+    a.row.p[o] = a.q.p[o] = a.off.p[o] = nullptr;
+    a.w.p[o] = nullptr;
+  }
+  for (int o = 0; o < v.P; ++o) {
+    if (v.staged) {  // OUT segment [o] of this rank
+      a.row.p[o] = v.own<int32_t>(MSN_XREG_OUT_ROW) + o * v.cap;
+      a.w.p[o] = v.own<float>(MSN_XREG_OUT_W) + o * v.cap;
+      a.q.p[o] = v.own<int32_t>(MSN_XREG_OUT_Q) + o * v.cap;
+      a.off.p[o] = v.own<int32_t>(MSN_XREG_OUT_OFF) + o * (v.lb + 1);
+    } else {  // owner o's IN segment [rank], over NVLink
+      a.row.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_ROW) + v.rank * v.cap;
+      a.w.p[o] = v.reg<float>(o, MSN_XREG_IN_W) + v.rank * v.cap;
+      a.q.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_Q) + v.rank * v.cap;
+      a.off.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_OFF) + v.rank * (v.lb + 1);
+    }
+  }
+  a.pos = v.own<int32_t>(MSN_XREG_POS);
+  a.counts = v.own<int32_t>(MSN_XREG_CTL) + 32;
+  a.cnt = v.own<int32_t>(MSN_XREG_SCRATCH);
+  a.qoff = a.cnt + v.P * (v.lb + 1);
+  return launch_route(shape_of(h->cfg, v.lb), idx, w, a, st, L);
+}
+
+cudaError_t x_gather(msn_pkm_t h, const XView& v, const void* values, cudaStream_t st, int* L) {
+  PerRank<float> dst;
+  for (int p = 0; p < kMaxWorld; ++p) dst.p[p] = nullptr;
+  const int64_t dv = h->cfg.d_value;
+  for (int p = 0; p < v.P; ++p)
+    dst.p[p] = v.staged ? v.own<float>(MSN_XREG_PART_OUT) + p * v.lb * dv
+                        : v.reg<float>(p, MSN_XREG_PART_IN) + v.rank * v.lb * dv;
+  return launch_gather_records(shape_of(h->cfg, v.lb), v.records_in(), values, dst, st, L);
+}
+
+cudaError_t x_combine(msn_pkm_t h, const XView& v, float* out, cudaStream_t st, int* L) {
+  return launch_reduce_partials(v.own<float>(MSN_XREG_PART_IN), v.P, v.lb, 1, h->cfg.d_value, out, st, L);
+}
+
+cudaError_t x_scatter(msn_pkm_t h, const XView& v, const void* values, float* d_values, void* ws,
+                      cudaStream_t st, int* L) {
+  PerRank<const float> xs;
+  PerRank<float> dd;
+  for (int p = 0; p < kMaxWorld; ++p) {
+    xs.p[p] = nullptr;
+    dd.p[p] = nullptr;
+  }
+  const int64_t dv = h->cfg.d_value;
+  for (int p = 0; p < v.P; ++p) {
+    xs.p[p] = v.staged ? v.own<float>(MSN_XREG_DOUT_ALL) + p * v.lb * dv : v.reg<float>(p, MSN_XREG_DOUT);
+    dd.p[p] = v.staged ? v.own<float>(MSN_XREG_DW_OUT) + p * v.cap
+                       : v.reg<float>(p, MSN_XREG_DW_IN) + v.rank * v.cap;
+  }
+  const Shape s = shape_of(h->cfg, v.lb);
+  const BwdWorkspace bw = carve_bwd_workspace(s, v.P * v.lb, ws);
+  return launch_scatter_records(s, v.records_in(), xs, values, d_values, dd, bw, st, L,
+                                TraceEvents{h->trace, h->ntrace});
+}
+
+cudaError_t x_collect(msn_pkm_t h, const XView& v, const int32_t* idx, float* dw, cudaStream_t st, int* L) {
+  return launch_collect_dw(shape_of(h->cfg, v.lb), idx, v.own<int32_t>(MSN_XREG_POS), v.own<float>(MSN_XREG_DW_IN),
+                           v.cap, v.rpr, dw, st, L);
+}
+
+cudaError_t x_barrier(const XView& v, cudaStream_t st, int* L) {
+  if (v.staged) return cudaSuccess;  // (the caller's collectives order the staged transport)
+  PerRank<uint32_t> f;
+  for (int p = 0; p < kMaxWorld; ++p) f.p[p] = nullptr;
+  for (int p = 0; p < v.P; ++p) f.p[p] = v.reg<uint32_t>(p, MSN_XREG_CTL);
+  return launch_exchange_barrier(v.P, v.rank, f, v.own<uint32_t>(MSN_XREG_CTL), st, L);
+}
+
+size_t x_ws_bytes(msn_pkm_t h, const XView& v) {
+  const Shape s = shape_of(h->cfg, v.lb);
+  const size_t a = fwd_bytes(s), b = bwd_workspace_bytes(s, v.P * v.lb);
+  return a > b ? a : b;
+}
+
+}  // namespace
+extern "C" {
+
+msn_status msn_pkm_exchange_layout(msn_pkm_t h, int64_t local_batch, int32_t staged, int64_t* offsets,
+                                   size_t* bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, local_batch))) return st;
+  const int P = h->cfg.world_size > 1 ? h->cfg.world_size : 1;
+  const XLayout L = xlayout(h->cfg, P, local_batch, staged != 0);
+  if (offsets)
+    for (int r = 0; r < MSN_XREG_COUNT; ++r) offsets[r] = L.off[r];
+  if (bytes) *bytes = (size_t)L.off[MSN_XREG_COUNT];
+  return MSN_OK;
+}
+
+#define XCALL(expr, what)                                      \
+  do {                                                         \
+    cudaError_t e_ = (expr);                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);         \
+  } while (0)
+
+msn_status msn_pkm_exchange_route(msn_pkm_t h, void* stream, const int32_t* idx, const float* weights,
+                                  const msn_pkm_exchange* x) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb == 0) return MSN_OK;
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  if ((st = check_tape(h, stream, v.lb, idx, weights))) return st;
+  XCALL(x_route(h, v, idx, weights, (cudaStream_t)stream, &h->last_launches), "exchange route");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_exchange_gather(msn_pkm_t h, void* stream, const void* values, const msn_pkm_exchange* x) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb == 0) return MSN_OK;
+  REQUIRE_PTR(values);
+  XCALL(x_gather(h, v, values, (cudaStream_t)stream, &h->last_launches), "exchange gather");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_exchange_combine(msn_pkm_t h, void* stream, const msn_pkm_exchange* x, float* out) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb == 0) return MSN_OK;
+  REQUIRE_PTR(out);
+  XCALL(x_combine(h, v, out, (cudaStream_t)stream, &h->last_launches), "exchange combine");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_exchange_scatter(msn_pkm_t h, void* stream, const void* values, float* d_values,
+                                    const msn_pkm_exchange* x, void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb == 0) return MSN_OK;
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(d_values);
+  REQUIRE_PTR(workspace);
+  if ((st = check_bwd_shape(h, true, false))) return st;
+  const size_t need = bwd_workspace_bytes(shape_of(h->cfg, v.lb), v.P * v.lb);
+  if (workspace_bytes < need)
+    return fail(MSN_ERR_WORKSPACE, "exchange scatter workspace %zu < %zu bytes", workspace_bytes, need);
+  XCALL(x_scatter(h, v, values, d_values, workspace, (cudaStream_t)stream, &h->last_launches), "exchange scatter");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_exchange_collect(msn_pkm_t h, void* stream, const int32_t* idx, const msn_pkm_exchange* x,
+                                    float* dw) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb == 0) return MSN_OK;
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(dw);
+  XCALL(x_collect(h, v, idx, dw, (cudaStream_t)stream, &h->last_launches), "exchange collect");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_exchange_barrier(msn_pkm_t h, void* stream, const msn_pkm_exchange* x) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  XCALL(x_barrier(v, (cudaStream_t)stream, &h->last_launches), "exchange barrier");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_forward_sharded(msn_pkm_t h, void* stream, int64_t local_batch, const void* query,
+                                   const void* subkeys, const void* values, const msn_pkm_exchange* x,
+                                   float* out, int32_t* idx, float* weights, void* workspace,
+                                   size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, local_batch))) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb != local_batch) return fail(MSN_ERR_INVALID_ARG, "local_batch != exchange local_batch");
+  if (v.staged) return fail(MSN_ERR_INVALID_ARG, "forward_sharded runs the PEER transport; STAGED: use the phases");
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(out);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(workspace);
+  if (workspace_bytes < x_ws_bytes(h, v))
+    return fail(MSN_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, x_ws_bytes(h, v));
+  cudaStream_t cs = (cudaStream_t)stream;
+  int* L = &h->last_launches;
+  // every rank takes part in every barrier, also with no local queries
+  if (v.lb > 0 && (st = do_select(h, cs, v.lb, query, subkeys, idx, weights, workspace, workspace_bytes, L)))
+    return st;
+  if (v.lb > 0) XCALL(x_route(h, v, idx, weights, cs, L), "exchange route");
+  XCALL(x_barrier(v, cs, L), "exchange barrier");
+  if (v.lb > 0) XCALL(x_gather(h, v, values, cs, L), "exchange gather");
+  XCALL(x_barrier(v, cs, L), "exchange barrier");
+  if (v.lb > 0) XCALL(x_combine(h, v, out, cs, L), "exchange combine");
+  return MSN_OK;
+}
+
+msn_status msn_pkm_backward_sharded(msn_pkm_t h, void* stream, int64_t local_batch, const float* d_out,
+                                    const void* query, const void* subkeys, const void* values,
+                                    const int32_t* idx, const float* weights, const msn_pkm_exchange* x,
+                                    float* d_query, float* d_subkeys, float* d_values, float* dw,
+                                    void* workspace, size_t workspace_bytes) {
+  msn_status st = check_handle(h);
+  if (st) return st;
+  if ((st = check_batch(h, local_batch))) return st;
+  h->last_launches = 0;
+  XView v;
+  if ((st = make_view(h, x, v))) return st;
+  if (v.lb != local_batch) return fail(MSN_ERR_INVALID_ARG, "local_batch != exchange local_batch");
+  if (v.staged) return fail(MSN_ERR_INVALID_ARG, "backward_sharded runs the PEER transport; STAGED: use the phases");
+  REQUIRE_PTR(d_out);
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(values);
+  REQUIRE_PTR(idx);
+  REQUIRE_PTR(weights);
+  REQUIRE_PTR(d_query);
+  REQUIRE_PTR(d_subkeys);
+  REQUIRE_PTR(d_values);
+  REQUIRE_PTR(workspace);
+  if (dw && !aligned16(dw)) return fail(MSN_ERR_INVALID_ARG, "dw is not 16-byte aligned");
+  if ((st = check_bwd_shape(h, true, true))) return st;
+  if (workspace_bytes < x_ws_bytes(h, v))
+    return fail(MSN_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, x_ws_bytes(h, v));
+  if ((st = check_tape(h, stream, v.lb, idx, weights))) return st;
+  cudaStream_t cs = (cudaStream_t)stream;
+  int* L = &h->last_launches;
+  const Shape s = shape_of(h->cfg, v.lb);
+  const BwdWorkspace bw = carve_bwd_workspace(s, v.P * v.lb, workspace);
+  float* dwp = dw ? dw : bw.dw;
+  if (v.lb > 0)
+    XCALL(cudaMemcpyAsync(v.own<float>(MSN_XREG_DOUT), d_out, sizeof(float) * v.lb * h->cfg.d_value,
+                          cudaMemcpyDeviceToDevice, cs), "d_out -> exchange");
+  XCALL(x_barrier(v, cs, L), "exchange barrier");
+  XCALL(x_scatter(h, v, values, d_values, workspace, cs, L), "exchange scatter");
+  XCALL(x_barrier(v, cs, L), "exchange barrier");
+  if (v.lb > 0) {
+    XCALL(x_collect(h, v, idx, dwp, cs, L), "exchange collect");
+    XCALL(launch_backward_keys(s, query, subkeys, idx, weights, dwp, d_query, d_subkeys, bw, cs, L),
+          "backward (ds, dQ, dK)");
+  }
+  return MSN_OK;
+}
 
 // ------------------------------------------------ prologue --
 msn_status msn_pkm_layernorm(msn_pkm_t h, void* stream, int64_t rows, const void* x, void* y) {

@@ -208,13 +208,19 @@ struct GrpArgs {
   float lr = 0.f, eps = 0.f;
   float* state = nullptr;  // Adagrad accumulator [rows, D]
   void* Vw = nullptr;      // the value table, written in place
-  // row-sharded backward over peer memory (MODE_DV): x row r of the global
-  // batch lives on rank r / xl (px[rank] + (r % xl) D) and dw[rec] goes to
-  // rank rec / dl (pd[rank] + rec % dl); null: the local X / dots arrays
-  const float* const* px = nullptr;
-  float* const* pd = nullptr;
+  // row-sharded backward over peer memory (MODE_DV, P2P kernels): x row r of
+  // the global batch lives on rank r / xl (px[rank] + (r % xl) D) and dw[rec]
+  // goes to rank rec / dl (pd[rank] + rec % dl)
+  PerRank<const float> px{};
+  PerRank<float> pd{};
   uint32_t xl = 0, dl = 0;
   FastDiv div_xl, div_dl;
+  // exchanged records (a9, MODE_DV): record j = s * cap + i of source s; its
+  // x row is s * xq_lb + xq[j] (the query in the source's batch); null: the
+  // record id encodes the query (cid = (b H + h) k + t)
+  const int32_t* xq = nullptr;
+  uint32_t xq_lb = 0;
+  FastDiv div_cap;
 };
 
 // Applies the fused update to VW consecutive elements at element offset off
@@ -328,6 +334,7 @@ __device__ __forceinline__ void stg_vec(float* p, const float* v) {
 template <int MODE>
 __device__ __forceinline__ uint32_t grp_xrow(const GrpArgs& a, uint32_t rec) {
   if constexpr (MODE == MODE_DV) {
+    if (a.xq) return a.div_cap.div(rec) * a.xq_lb + (uint32_t)a.xq[rec];
     if (a.og == 1) return a.div_hk.div(rec);
     const uint32_t bh = a.div_k.div(rec);  // b * H + h
     const uint32_t b = a.div_h.div(bh);
@@ -362,7 +369,11 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
         const XT* xrow;
         if (P2P) {  // the home rank's d_out row (peer memory)
           const uint32_t home = a.div_xl.div((uint32_t)xr);
-          xrow = reinterpret_cast<const XT*>(a.px[home]) + lane * VW + (int64_t)(xr - (int64_t)home * a.xl) * D;
+          const float* hb = nullptr;
+#pragma unroll
+          for (int q = 0; q < kMaxWorld; ++q)
+            if (q == (int)home) hb = a.px.p[q];
+          xrow = reinterpret_cast<const XT*>(hb) + lane * VW + (int64_t)(xr - (int64_t)home * a.xl) * D;
         } else {
           xrow = X + xr * D;
         }
@@ -395,7 +406,11 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
           if (uu == u && rec[uu] != 0xffffffffu) {
             if (P2P) {  // dw straight into the home rank's buffer (one owner per element)
               const uint32_t home = a.div_dl.div(rec[uu]);
-              a.pd[home][rec[uu] - home * a.dl] = r;
+              float* hd = nullptr;
+#pragma unroll
+              for (int q = 0; q < kMaxWorld; ++q)
+                if (q == (int)home) hd = a.pd.p[q];
+              hd[rec[uu] - home * a.dl] = r;
             } else {
               a.dots[rec[uu]] = r;
             }
@@ -747,7 +762,7 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   if (tr.n > 0) cudaEventRecord(tr.ev[0], st);  // profiling: the short-run reducer alone
   if (MODE == MODE_DV && a.upd)
     launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, true, false>, (unsigned)sb, 256, 0, st, a);
-  else if (MODE == MODE_DV && a.px)
+  else if (MODE == MODE_DV && a.xl)
     launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false, MODE == MODE_DV>, (unsigned)sb, 256, 0, st, a);
   else
     launch_pdl(grp_reduce_short_kernel<MODE, XT, YT, EPL, false, false>, (unsigned)sb, 256, 0, st, a);
@@ -765,7 +780,7 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   int64_t pb = (int64_t)sms * 8;
   const int64_t pneed = grp_pieces_max(n);
   if (pb > pneed) pb = pneed;
-  if (MODE == MODE_DV && a.px)
+  if (MODE == MODE_DV && a.xl)
     launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL, MODE == MODE_DV>, (unsigned)pb, 256, 0, st, a);
   else
     launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL, false>, (unsigned)pb, 256, 0, st, a);
@@ -815,9 +830,15 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
     a.px = peers->d_out;
     a.pd = peers->dw;
     a.xl = (uint32_t)(peers->local_batch * og);
-    a.dl = (uint32_t)(peers->local_batch * H * k);
+    a.dl = (uint32_t)(peers->cap ? peers->cap : peers->local_batch * H * k);
     a.div_xl = FastDiv(a.xl);
     a.div_dl = FastDiv(a.dl);
+    if (!peers->p2p) a.xl = 0;  // (staged records: local X / dots)
+  }
+  if (peers && peers->xq) {
+    a.xq = peers->xq;
+    a.xq_lb = (uint32_t)peers->local_batch;
+    a.div_cap = FastDiv((uint32_t)peers->cap);
   }
   switch (D / 32) {
     case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches, tr);
@@ -1159,6 +1180,58 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
   return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, w, dOut, V, dw, dV, s.H, s.k,
                                                    s.d_v, st, launches, tr, UpdateArgs{upd, lr, eps, state},
                                                    s.og, peers);
+}
+
+namespace {
+// Keys of exchanged records (a9): record j = s * cap + i of source s is valid
+// iff i < off[s][lb] (the segment's count); key = its local row.
+__global__ void rec_keys_kernel(const int32_t* __restrict__ row, const int32_t* __restrict__ off, int64_t lb,
+                                FastDiv div_cap, uint32_t cap, int64_t n, uint32_t sentinel,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ cnt,
+                                uint32_t* __restrict__ rank) {
+  pdl_enter();
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t sr = div_cap.div((uint32_t)p);
+  const uint32_t i = (uint32_t)p - sr * cap;
+  const bool valid = (int64_t)i < (int64_t)off[(int64_t)sr * (lb + 1) + lb];
+  const uint32_t key = valid ? (uint32_t)row[p] : sentinel;
+  keys[p] = key;
+  if (valid) rank[p] = atomicAdd(&cnt[key], 1u);
+}
+}  // namespace
+
+cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const PerRank<const float>& x_src,
+                                   const void* V, float* dV, const PerRank<float>& dw_dst,
+                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
+                                   const TraceEvents& tr) {
+  if (!epl_ok(s.d_v) || s.og != 1) return cudaErrorNotSupported;
+  const int64_t n = (int64_t)r.P * r.cap;
+  if (n == 0) return cudaSuccess;
+  if (n >= (int64_t(1) << 32)) return cudaErrorNotSupported;
+  const uint32_t nrows = (uint32_t)(s.row_end - s.row_begin);
+  const GrpScratch g = grp_scratch(ws);
+  cudaError_t e = grp_begin(g, nrows, st);
+  if (e != cudaSuccess) return e;
+  launch_pdl(rec_keys_kernel, (unsigned)((n + 255) / 256), 256, 0, st, r.row, r.off, r.lb,
+             FastDiv((uint32_t)r.cap), (uint32_t)r.cap, n, nrows, g.keys, g.cnt, g.rank);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  // the records' x rows and dw destinations are per source rank (peer memory,
+  // or the staged local regions): the P2P reducers with record -> query map
+  ScatterPeers peers;
+  peers.d_out = x_src;
+  peers.dw = dw_dst;
+  peers.local_batch = r.lb;
+  peers.p2p = true;
+  peers.xq = r.q;
+  peers.cap = r.cap;
+  if (s.v_dt == F32)
+    return grp_finish<MODE_DV, float, float>(g, n, nrows, r.w, nullptr, V, nullptr, dV, s.H, s.k, s.d_v, st,
+                                             launches, tr, UpdateArgs{}, 1, &peers);
+  return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, r.w, nullptr, V, nullptr, dV, s.H, s.k,
+                                                   s.d_v, st, launches, tr, UpdateArgs{}, 1, &peers);
 }
 
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
                                                      const VT* __restrict__ V,
                                                      float* __restrict__ out, int64_t B, int H, int k,
                                                      int d_v, int64_t row_begin,
-                                                     int64_t row_end, Gate gate, int og, Push push) {
+                                                     int64_t row_end, Gate gate, int og) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   constexpr int LG = 32 / G;  // lanes per row
@@ -50,13 +50,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
     gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * hpg * k, (grp + 1) * hpg * k, V, d_v, tot);
     if (g == 0) {
       const int64_t orow = b * og + grp;
-      float* o;
-      if (push.peers) {  // fused reduce-scatter: the home rank's receive slot
-        const int64_t home = b / push.lb, bl = b - home * push.lb;
-        o = push.peers[home] + (((int64_t)push.rank * push.lb + bl) * og + grp) * d_v;
-      } else {
-        o = out + orow * d_v;
-      }
+      float* o = out + orow * d_v;
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int vec = gl * VPL + v;
@@ -140,9 +134,9 @@ __global__ void __launch_bounds__(256) gather_wide_kernel(const int32_t* __restr
 
 template <typename VT>
 cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const VT* V, float* out,
-                     cudaStream_t st, const Gate& gate, const Push& push) {
+                     cudaStream_t st, const Gate& gate) {
   const int R = s.d_v * (int)sizeof(VT) / 16;
-  if ((R == 64 || R == 128) && !push.peers && s.row_begin == 0 &&
+  if ((R == 64 || R == 128) && s.row_begin == 0 &&
       s.row_end >= (int64_t)s.n_sub * s.n_sub * (s.tab_stride ? s.og : 1)) {
     const int wpq = R / 32, qpb = kWarps / wpq;
     launch_pdl(gather_wide_kernel<VT, 16>, (unsigned)((s.B + qpb - 1) / qpb), 256, 0, st, idx, w, V, out, s.B,
@@ -152,7 +146,7 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);
 #define GATHER(VPL, G, U)                                                                      \
   launch_pdl(gather_kernel<VT, VPL, G, U>, blocks, 256, 0, st, idx, w, V, out, s.B, s.H, s.k, s.d_v, \
-             s.row_begin, s.row_end, gate, s.og, push)
+             s.row_begin, s.row_end, gate, s.og)
   MSN_GATHER_DISPATCH(R, GATHER);
 #undef GATHER
   return cudaGetLastError();
@@ -163,18 +157,8 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
                           float* out, cudaStream_t st, int* launches, const Gate& gate) {
   if (s.H * s.k > kMaxHK) return cudaErrorNotSupported;
-  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, out, st, gate, Push{})
-                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, out, st, gate, Push{});
-  if (e == cudaSuccess) ++*launches;
-  return e;
-}
-
-cudaError_t launch_gather_push(const Shape& s, const int32_t* idx, const float* w, const void* V,
-                               const Push& push, cudaStream_t st, int* launches) {
-  if (s.H * s.k > kMaxHK || !push.peers || push.lb <= 0) return cudaErrorNotSupported;
-  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, nullptr, st, Gate{}, push)
-                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, nullptr, st,
-                                                          Gate{}, push);
+  cudaError_t e = s.v_dt == F32 ? dispatch<float>(s, idx, w, (const float*)V, out, st, gate)
+                                : dispatch<__nv_bfloat16>(s, idx, w, (const __nv_bfloat16*)V, out, st, gate);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

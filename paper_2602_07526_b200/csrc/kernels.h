@@ -9,6 +9,14 @@ namespace msn {
 
 enum Dt { F32 = 0, BF16 = 1 };
 
+// Per-rank pointers of the row-sharded exchange (a9), passed by value in the
+// kernel parameters (graph-capturable, no device pointer arrays).
+constexpr int kMaxWorld = 8;
+template <typename T>
+struct PerRank {
+  T* p[kMaxWorld];
+};
+
 struct Shape {
   int64_t B;       // queries in this call
   int H, n_sub, d_h, d_v, k;
@@ -84,16 +92,6 @@ cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* id
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
                           float* out, cudaStream_t st, int* launches, const Gate& gate = Gate{});
 
-// a5 fused with the reduce-scatter of the row-sharded table: query b's
-// partial row is stored straight into its home rank's receive buffer
-// peers[b / lb][(rank * lb + b % lb) * og + g] (peer memory over NVLink).
-struct Push {
-  float* const* peers = nullptr;  // device array [world] of receive buffers
-  int rank = 0;
-  int64_t lb = 0;                 // queries per rank
-};
-cudaError_t launch_gather_push(const Shape& s, const int32_t* idx, const float* w, const void* V,
-                               const Push& push, cudaStream_t st, int* launches);
 // out[b, g] = sum_p recv[p][b][g] in rank order (=).
 cudaError_t launch_reduce_partials(const float* recv, int world, int64_t lb, int og, int d_v,
                                    float* out, cudaStream_t st, int* launches);
@@ -151,9 +149,13 @@ struct TraceEvents {
 // dw of record (b, h, t) is written into rank b / local_batch's dw[rank]
 // ([local_batch, H, k]); each dw element has exactly one owner rank.
 struct ScatterPeers {
-  const float* const* d_out = nullptr;  // device array [world]
-  float* const* dw = nullptr;           // device array [world]
+  PerRank<const float> d_out{};  // rank p's [local_batch, og, d_v] rows
+  PerRank<float> dw{};           // rank p's dw destination (pre-offset)
   int64_t local_batch = 0;
+  bool p2p = true;               // false: x rows / dw in the local X / dots arrays
+  // exchanged records (a9): record j = s * cap + i, query xq[j] of source s
+  const int32_t* xq = nullptr;
+  int64_t cap = 0;
 };
 
 // a6 deterministic: group (idx -> cid) by row, then fused row-major dV += / dw.
@@ -175,6 +177,43 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
                                  const int32_t* idx, const float* w, const float* dw, float* dQ,
                                  float* dK, const BwdWorkspace& ws, cudaStream_t st,
                                  int* launches);
+
+// ---- a9 record exchange of the row-sharded table (exchange.cu) ----
+struct RouteArgs {
+  int P;                    // world
+  int64_t lb;               // local batch B_l
+  int64_t rpr;              // value rows per rank (n / P)
+  PerRank<int32_t> row, q;  // destination of owner o's records (pre-offset: segment start)
+  PerRank<float> w;
+  PerRank<int32_t> off;     // destination of owner o's per-query offsets [B_l + 1]
+  int32_t* pos;             // [B_l * H * k]
+  int32_t* counts;          // [P] records for owner o
+  int32_t* cnt;             // scratch [P][B_l + 1]
+  int32_t* qoff;            // scratch [P][B_l + 1]
+};
+cudaError_t launch_route(const Shape& s, const int32_t* idx, const float* w, const RouteArgs& a,
+                         cudaStream_t st, int* launches);
+struct RecordsIn {
+  int P;
+  int64_t lb, cap;
+  const int32_t *row, *q, *off;  // [P][cap], [P][cap], [P][B_l + 1]
+  const float* w;                // [P][cap]
+};
+// partial of source s's query b -> dst.p[s] + b * d_v (pre-offset per source)
+cudaError_t launch_gather_records(const Shape& s, const RecordsIn& r, const void* V,
+                                  const PerRank<float>& dst, cudaStream_t st, int* launches);
+// dV (+=) and dw of the records; d_out row of (s, b) at x_src.p[s] + b * d_v,
+// dw of record (s, i) -> dw_dst.p[s] + i.
+cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const PerRank<const float>& x_src,
+                                   const void* V, float* dV, const PerRank<float>& dw_dst,
+                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
+                                   const TraceEvents& tr);
+// dw[b,h,t] = dw_in[owner * cap + pos[b,h,t]]
+cudaError_t launch_collect_dw(const Shape& s, const int32_t* idx, const int32_t* pos, const float* dw_in,
+                              int64_t cap, int64_t rpr, float* dw, cudaStream_t st, int* launches);
+// device barrier: flags.p[o] = rank o's CTL flag array, ctl = own CTL words
+cudaError_t launch_exchange_barrier(int P, int rank, const PerRank<uint32_t>& flags, uint32_t* ctl,
+                                    cudaStream_t st, int* launches);
 
 // ---- prologue (prologue.cu) ----
 bool prologue_supported(const Shape& s);

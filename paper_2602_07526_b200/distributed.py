@@ -1,31 +1,36 @@
-"""Row-sharded value table across GPUs (BASELINE.json configs[3]).
+"""Row-sharded value table across GPUs (BASELINE.json configs[3]; SURVEY.md
+8(e)): the plumbing around the library's record
+exchange (msn_pkm_exchange_* / msn_pkm_forward_sharded, include/msn_pkm.h).
 
-Rank p of P holds value rows [p*n/P, (p+1)*n/P) and its own B_local queries;
-the sub-keys are replicated (they are small).  One step:
+Rank p of P holds value rows [p n/P, (p+1) n/P) and its own B_l queries; the
+sub-keys are replicated (they are small).  One step:
 
-  forward   select (a1-a4, local queries)             -> idx, w      [B_l,H,k]
-            all-gather idx, w (8 B per contribution)   -> [P*B_l,H,k]
-            gather over the local rows, all queries    -> partial [P*B_l,d_v]
-            reduce-scatter(sum) of the partials        -> out [B_l,d_v]
-  backward  all-gather d_out                           -> [P*B_l,d_v]
-            scatter over the local rows: dV_shard +=, dw for local slots (0 else)
-            reduce-scatter(sum) of dw  (one owner per element: the sum is exact)
-            backward_keys on the local queries         -> dQ (=), dK (+=)
+  forward   select (a1-a4, local queries)                 -> idx, w [B_l,H,k]
+            ROUTE: one 12-B record {row, w, b} per slot to its owner
+            GATHER: per (source, query) partial sums       -> back to the home
+            COMBINE: the P partials added in owner order   -> out [B_l, d_v]
+  backward  owners read the d_out rows of their records, SCATTER (dV shard +=,
+            dw per record, deterministic grouped reduction), return dw;
+            COLLECT puts dw in (b,h,t) order; backward_keys on the local
+            queries -> dQ (=), dK (+=, this rank's queries: summing it across
+            ranks is the caller's data-parallel job, like any replicated
+            parameter).
 
-The collectives are torch.distributed calls (NCCL over NVLink/NVSwitch on the
-GPU box): fixed-size, graph-capturable, no host synchronisation, NVLS-capable
-(reduce-scatter).  transport="p2p" fuses the forward's gather with its
-reduce-scatter instead: msn_pkm_gather_push stores every query's partial row
-straight into the home rank's receive buffer (torch symmetric memory, NVLink
-peer stores issued by the gather kernel as the rows are summed), a device-side
-barrier orders the pushes, and msn_pkm_reduce_partials adds the world partials
-in rank order (deterministic).  Its backward reads every d_out row from the
-home rank's buffer inside the dV reducer and stores every dw element into the
-home rank's buffer (msn_pkm_scatter_p2p): no all-gather of d_out, no
-reduce-scatter of dw.  The data-path kernels are the C ABI's phase entry points
-(msn_pkm_select / _gather / _scatter / _backward_keys).  dK is this rank's
-contribution; summing it across ranks is the caller's data-parallel job
-(like any replicated parameter).
+transport="peer" (default): every rank's exchange buffer lives in torch
+symmetric memory and is mapped into every peer (NVLink); the library's
+kernels store records, partials and dw straight into the peers' buffers and
+order the ranks with a device-side barrier: msn_pkm_forward_sharded /
+msn_pkm_backward_sharded run the whole step, no host synchronisation, CUDA
+graph capturable.  With world size 1 the buffer is a plain device tensor (the
+same code path, nothing leaves the GPU).
+
+transport="nccl": the same kernels with the STAGED layout; the data moves
+with torch.distributed collectives (NCCL over NVLink on the GPU box): the
+record counts by all_to_all_single (one host read of P counts: the sizes of
+the variable all-to-all), the records and the returned dw by batched
+send/recv of exactly the counted records, the per-query offsets and the
+partials by all_to_all_single, d_out by all_gather.  This is the baseline the
+peer transport is measured against (and the host logic the gloo tests cover).
 """
 from __future__ import annotations
 
@@ -34,18 +39,82 @@ from typing import Optional
 import torch
 import torch.distributed as dist
 
+from . import _lib
+
+_DT = {"IN_ROW": torch.int32, "IN_W": torch.float32, "IN_Q": torch.int32, "IN_OFF": torch.int32,
+       "PART_IN": torch.float32, "DOUT": torch.float32, "DW_IN": torch.float32, "POS": torch.int32,
+       "CTL": torch.int32, "SCRATCH": torch.int32, "OUT_ROW": torch.int32, "OUT_W": torch.float32,
+       "OUT_Q": torch.int32, "OUT_OFF": torch.int32, "PART_OUT": torch.float32, "DOUT_ALL": torch.float32,
+       "DW_OUT": torch.float32}
+
+
+class ExchangeBuffer:
+    """One rank's exchange buffer and typed views of its regions (the layout
+    msn_pkm_exchange_layout reports)."""
+
+    def __init__(self, lk, local_batch: int, world: int, rank: int, transport: str, group=None,
+                 device=None, buf: Optional[torch.Tensor] = None, bases=None):
+        self.world, self.rank, self.lb = world, rank, local_batch
+        self.cap = local_batch * lk.heads * lk.k
+        self.d_value = lk.d_value
+        staged = transport == "nccl"
+        self.offsets, nbytes = lk.exchange_layout(local_batch, staged)
+        self.nbytes = nbytes
+        self._hdl = None
+        if buf is None:
+            if transport == "peer" and world > 1:
+                try:
+                    import torch.distributed._symmetric_memory as symm
+                except ImportError as e:  # pragma: no cover - depends on the torch build
+                    raise RuntimeError("transport='peer' needs torch symmetric memory") from e
+                buf = symm.empty(nbytes, dtype=torch.uint8, device=device)
+                buf.zero_()
+                self._hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+                bases = [int(p) for p in self._hdl.buffer_ptrs]
+                torch.cuda.synchronize(device)
+                self._hdl.barrier(channel=0)  # every buffer zeroed before any peer writes
+            else:
+                buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        self.buf = buf
+        if bases is None:
+            bases = [0] * world
+            bases[rank] = buf.data_ptr()
+        self.x = _lib.Exchange()
+        self.x.transport = _lib.XCHG_STAGED if staged else _lib.XCHG_PEER
+        self.x.world, self.x.rank, self.x.local_batch = world, rank, local_batch
+        for p in range(_lib.MAX_WORLD):
+            self.x.base[p] = bases[p] if p < world else None
+
+    def region(self, name: str, *shape) -> torch.Tensor:
+        dt = _DT[name]
+        n = 1
+        for s in shape:
+            n *= s
+        o = self.offsets[name]
+        return self.buf[o:o + n * torch.tensor([], dtype=dt).element_size()].view(dt).view(*shape)
+
+    # typed views
+    def records(self, out: bool):
+        P, cap = self.world, self.cap
+        pre = "OUT_" if out else "IN_"
+        return (self.region(pre + "ROW", P, cap), self.region(pre + "W", P, cap), self.region(pre + "Q", P, cap),
+                self.region(pre + "OFF", P, self.lb + 1))
+
+    def counts(self) -> torch.Tensor:
+        return self.region("CTL", 64)[32:32 + self.world]
+
 
 class ShardedPKM:
     def __init__(self, heads: int, n_sub: int, d_half: int, d_value: int, k: int,
                  local_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
-                 group=None, phases=None, device=None, transport: str = "nccl"):
-        if transport not in ("nccl", "p2p"):
-            raise ValueError(f"transport {transport!r}: 'nccl' or 'p2p'")
+                 group=None, phases=None, device=None, transport: str = "peer",
+                 dq_in_qk_dtype: bool = False):
+        if transport not in ("peer", "nccl"):
+            raise ValueError(f"transport {transport!r}: 'peer' or 'nccl'")
         self.transport = transport
-        self._symm = None
         self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         n = n_sub * n_sub
         if n % self.world:
             raise ValueError(f"n_sub^2 = {n} is not divisible by the world size {self.world}")
@@ -56,90 +125,111 @@ class ShardedPKM:
         self.local_batch = local_batch
         if phases is None:
             from .pkm import PKMLookup
-            phases = PKMLookup(heads, n_sub, d_half, d_value, k, max_batch=local_batch * self.world,
-                               qk_dtype=qk_dtype, value_dtype=value_dtype,
-                               row_begin=self.row_begin, row_end=self.row_end, device=device)
+            phases = PKMLookup(heads, n_sub, d_half, d_value, k, max_batch=local_batch,
+                               qk_dtype=qk_dtype, value_dtype=value_dtype, device=device,
+                               world_size=self.world, rank=self.rank, dq_in_qk_dtype=dq_in_qk_dtype)
         self.ph = phases
+        self.xb = ExchangeBuffer(phases, local_batch, self.world, self.rank, transport, group, device)
+        self.ws = phases.workspace(local_batch, self.world * local_batch)
+
+    @property
+    def exchange(self):
+        return self.xb.x
 
     def value_shard(self, full_values: torch.Tensor) -> torch.Tensor:
         """This rank's rows of a full table (every rank generates the same seeded table)."""
         return full_values[self.row_begin:self.row_end].contiguous()
 
-    def _all_gather(self, x: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-        dist.all_gather_into_tensor(out, x.contiguous(), group=self.group)
-        return out
-
-    def _reduce_scatter(self, x: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((x.shape[0] // self.world,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-        dist.reduce_scatter_tensor(out, x.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
-        return out
-
-    def _p2p_buffers(self, B_l: int, device):
-        """This rank's receive buffer [world, B_l, d_v] in symmetric memory and
-        the device array of every rank's buffer address (peer-mapped)."""
-        if self._symm is None or self._symm[0].shape[1] != B_l:
-            try:
-                import torch.distributed._symmetric_memory as symm
-            except ImportError as e:  # pragma: no cover - depends on the torch build
-                raise RuntimeError("transport='p2p' needs torch symmetric memory") from e
-            buf = symm.empty((self.world, B_l, self.d_value), dtype=torch.float32, device=device)
-            group = self.group if self.group is not None else dist.group.WORLD
-            hdl = symm.rendezvous(buf, group)
-            ptrs = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device=device)
-            self._symm = (buf, hdl, ptrs)
-        return self._symm
-
-    def forward(self, query: torch.Tensor, subkeys: torch.Tensor, value_shard: torch.Tensor):
-        """Returns (out [B_l,d_v], tape) for the local queries."""
+    # ------------------------------------------------------------ forward
+    def forward(self, query: torch.Tensor, subkeys: torch.Tensor, value_shard: torch.Tensor,
+                out: Optional[torch.Tensor] = None):
+        """Returns (out [B_l, d_v], tape (idx, w)) for the local queries."""
+        x = self.xb.x
+        if self.transport == "peer":
+            out, idx, w = self.ph.forward_sharded(query, subkeys, value_shard, x, out=out, ws=self.ws)
+            return out, (idx, w)
         idx, w = self.ph.select(query, subkeys)
-        idx_all = self._all_gather(idx)
-        w_all = self._all_gather(w)
-        if self.transport == "p2p":
-            buf, hdl, ptrs = self._p2p_buffers(query.shape[0], query.device)
-            hdl.barrier(channel=0)  # every rank is done reading its previous step's partials
-            self.ph.gather_push(idx_all, w_all, value_shard, ptrs, self.world, self.rank)
-            hdl.barrier(channel=0)  # every push has landed
-            out = self.ph.reduce_partials(buf, self.world)
-        else:
-            part = self.ph.gather(idx_all, w_all, value_shard)
-            out = self._reduce_scatter(part)
-        return out, (idx, w, idx_all, w_all)
+        self.ph.exchange_route(idx, w, x)
+        sc, rc = self._counts()
+        self._move_records(sc, rc)
+        self.ph.exchange_gather(value_shard, x)
+        P, lb, dv = self.world, self.local_batch, self.d_value
+        self._a2a_fixed(self.xb.region("PART_IN", P * lb * dv), self.xb.region("PART_OUT", P * lb * dv))
+        out = self.ph.exchange_combine(x, out)
+        self._rc, self._sc = rc, sc
+        return out, (idx, w)
 
+    # ----------------------------------------------------------- backward
     def backward(self, d_out: torch.Tensor, query: torch.Tensor, subkeys: torch.Tensor,
                  value_shard: torch.Tensor, tape, d_subkeys: Optional[torch.Tensor] = None,
                  d_value_shard: Optional[torch.Tensor] = None):
         """Returns (d_query, d_subkeys (this rank's part, +=), d_value_shard (+=), dw)."""
-        idx, w, idx_all, w_all = tape
+        idx, w = tape
         dev = d_out.device
         if d_value_shard is None:
             d_value_shard = torch.zeros((self.rows, self.d_value), dtype=torch.float32, device=dev)
-        if self.transport == "p2p":
-            dbuf, dwbuf, dh, dptrs, wptrs = self._p2p_bwd_buffers(d_out.shape[0], dev)
-            dh.barrier(channel=0)  # every rank is done with the previous step's buffers
-            dbuf.copy_(d_out.float())
-            dh.barrier(channel=0)  # every rank's d_out is in place
-            self.ph.scatter_p2p(idx_all, w_all, value_shard, d_value_shard, dptrs, wptrs, self.world)
-            dh.barrier(channel=0)  # every owner's dw has landed
-            dw = dwbuf.clone()
+        if d_subkeys is None:
+            d_subkeys = torch.zeros((self.heads, 2, self.n_sub, self.d_half), dtype=torch.float32, device=dev)
+        x = self.xb.x
+        if self.transport == "peer":
+            dq, dK, dV, dw = self.ph.backward_sharded(d_out.float().contiguous(), query, subkeys, value_shard,
+                                                      idx, w, x, d_subkeys, d_value_shard, ws=self.ws)
+            return dq, dK, dV, dw
+        P, lb, dv = self.world, self.local_batch, self.d_value
+        dall = self.xb.region("DOUT_ALL", P * lb, dv)
+        if P > 1:
+            dist.all_gather_into_tensor(dall, d_out.float().contiguous(), group=self.group)
         else:
-            d_all = self._all_gather(d_out.float())
-            dw_part = self.ph.scatter(idx_all, w_all, d_all, value_shard, d_value_shard)
-            dw = self._reduce_scatter(dw_part)
+            dall.copy_(d_out)
+        self.ph.exchange_scatter(value_shard, d_value_shard, x, ws=self.ws)
+        self._move_dw(self._sc, self._rc)
+        dw = self.ph.exchange_collect(idx, x)
         dq, d_subkeys = self.ph.backward_keys(query, subkeys, idx, w, dw, d_subkeys)
         return dq, d_subkeys, d_value_shard, dw
 
-    def _p2p_bwd_buffers(self, B_l: int, device):
-        """Symmetric d_out [B_l, d_v] and dw [B_l, H, k] buffers of this rank and
-        the device arrays of every rank's addresses."""
-        if getattr(self, "_symm_bwd", None) is None or self._symm_bwd[0].shape[0] != B_l:
-            import torch.distributed._symmetric_memory as symm
-            group = self.group if self.group is not None else dist.group.WORLD
-            dbuf = symm.empty((B_l, self.d_value), dtype=torch.float32, device=device)
-            dh = symm.rendezvous(dbuf, group)
-            wbuf = symm.empty((B_l, self.heads, self.k), dtype=torch.float32, device=device)
-            wh = symm.rendezvous(wbuf, group)
-            dptrs = torch.tensor([int(p) for p in dh.buffer_ptrs], dtype=torch.int64, device=device)
-            wptrs = torch.tensor([int(p) for p in wh.buffer_ptrs], dtype=torch.int64, device=device)
-            self._symm_bwd = (dbuf, wbuf, dh, dptrs, wptrs)
-        return self._symm_bwd
+    # ------------------------------------------- the NCCL (staged) moves
+    def _counts(self):
+        """Records this rank sends to each owner (sc) and receives from each
+        source (rc): one all_to_all_single of P counts and ONE host read."""
+        sc_d = self.xb.counts().clone()
+        rc_d = torch.empty_like(sc_d)
+        if self.world > 1:
+            dist.all_to_all_single(rc_d, sc_d, group=self.group)
+        else:
+            rc_d.copy_(sc_d)
+        both = torch.cat([sc_d, rc_d]).cpu().tolist()  # the documented host sync of this transport
+        return both[:self.world], both[self.world:]
+
+    def _a2a_fixed(self, out: torch.Tensor, inp: torch.Tensor):
+        if self.world > 1:
+            dist.all_to_all_single(out, inp, group=self.group)
+        else:
+            out.copy_(inp)
+
+    def _sendrecv(self, sends, recvs):
+        """sends[p] / recvs[p]: contiguous tensors to / from rank p (self: a copy)."""
+        ops = []
+        for p in range(self.world):
+            if p == self.rank:
+                recvs[p].copy_(sends[p])
+                continue
+            if sends[p].numel():
+                ops.append(dist.P2POp(dist.isend, sends[p], p, self.group))
+            if recvs[p].numel():
+                ops.append(dist.P2POp(dist.irecv, recvs[p], p, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def _move_records(self, sc, rc):
+        o_row, o_w, o_q, o_off = self.xb.records(out=True)
+        i_row, i_w, i_q, i_off = self.xb.records(out=False)
+        for o, i in ((o_row, i_row), (o_w, i_w), (o_q, i_q)):
+            self._sendrecv([o[p, :sc[p]] for p in range(self.world)], [i[p, :rc[p]] for p in range(self.world)])
+        self._a2a_fixed(i_off.view(-1), o_off.view(-1))
+
+    def _move_dw(self, sc, rc):
+        P, cap = self.world, self.xb.cap
+        d_out = self.xb.region("DW_OUT", P, cap)   # owner side: dw for home s, rc[s] records
+        d_in = self.xb.region("DW_IN", P, cap)     # home side: dw from owner o, sc[o] records
+        self._sendrecv([d_out[p, :rc[p]] for p in range(P)], [d_in[p, :sc[p]] for p in range(P)])

@@ -41,20 +41,27 @@ class PKMLookup:
                  max_batch: int, qk_dtype=torch.bfloat16, value_dtype=torch.bfloat16,
                  atomic_bwd: bool = False, row_begin: int = 0, row_end: Optional[int] = None,
                  device=None, head_groups: int = 1, group_tables: bool = False,
-                 dq_in_qk_dtype: bool = False, validate: bool = False):
+                 dq_in_qk_dtype: bool = False, validate: bool = False, world_size: int = 0,
+                 rank: int = 0):
         """head_groups G > 1: consecutive blocks of heads/G
         heads form a group (a token with its own codebooks); out is [B, G, d_v].
         group_tables: every group has its own table (values [G*n_sub^2, d_v]).
         dq_in_qk_dtype: d_query comes back in the query dtype (bf16 for bf16
         configs; MSN_FLAG_DQ_QK_DTYPE) instead of fp32.
         validate: every call that consumes a tape checks it first and raises
-        on an invalid one (MSN_FLAG_VALIDATE; synchronises the stream)."""
+        on an invalid one (MSN_FLAG_VALIDATE; synchronises the stream).
+        world_size P > 1, rank: the row-sharded table with the library's
+        record exchange (a9): this handle holds rows [rank n/P, (rank+1) n/P)."""
         self.lib = _lib.load()
         self.heads, self.n_sub, self.d_half, self.d_value, self.k = heads, n_sub, d_half, d_value, k
         self.max_batch = max_batch
         self.qk_dtype, self.value_dtype = qk_dtype, value_dtype
         self.head_groups, self.group_tables = max(1, head_groups), group_tables
         self.table_rows = n_sub * n_sub * (self.head_groups if group_tables else 1)
+        self.world_size, self.rank = world_size, rank
+        if world_size > 1:
+            rpr = self.table_rows // world_size
+            row_begin, row_end = rank * rpr, (rank + 1) * rpr
         self.row_begin = row_begin
         self.row_end = self.table_rows if row_end is None else row_end
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -63,7 +70,7 @@ class PKMLookup:
         self.dq_dtype = qk_dtype if (dq_in_qk_dtype and qk_dtype == torch.bfloat16) else torch.float32
         cfg = _lib.Config(_lib.ABI_VERSION, heads, n_sub, d_half, d_value, k, max_batch,
                           _DT[qk_dtype], _DT[value_dtype], flags, self.head_groups,
-                          self.row_begin, self.row_end)
+                          self.row_begin, self.row_end, world_size, rank)
         h = ctypes.c_void_p()
         _lib.check(self.lib.msn_pkm_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
@@ -228,24 +235,6 @@ class PKMLookup:
         _lib.check(self.lib.msn_pkm_gather(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(V), _ptr(out)))
         return out
 
-    def gather_push(self, idx: torch.Tensor, w: torch.Tensor, values: torch.Tensor,
-                    peer_ptrs: torch.Tensor, world: int, rank: int) -> None:
-        """a5 over this process's rows, each query's partial pushed into its home
-        rank's receive buffer (peer_ptrs: int64 device tensor of `world` buffer
-        addresses; see msn_pkm_gather_push)."""
-        idx, w, V = self._dev(idx), self._dev(w), self._dev(values)
-        B = idx.shape[0]
-        _lib.check(self.lib.msn_pkm_gather_push(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(V),
-                                                ctypes.c_void_p(peer_ptrs.data_ptr()), world, rank, B // world))
-
-    def reduce_partials(self, recv: torch.Tensor, world: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """out = recv[0] + ... + recv[world-1] (rank order); recv [world, B_l, ...]."""
-        lb = recv.shape[1]
-        if out is None:
-            out = torch.empty(self._out_shape(lb), dtype=torch.float32, device=self.device)
-        _lib.check(self.lib.msn_pkm_reduce_partials(self._h, _stream(), lb, world, _ptr(recv), _ptr(out)))
-        return out
-
     # ----------------------------------------------------------- backward
     def backward(self, d_out, query, subkeys, values, idx, w,
                  d_subkeys: Optional[torch.Tensor] = None, d_values: Optional[torch.Tensor] = None):
@@ -283,21 +272,6 @@ class PKMLookup:
         _lib.check(self.lib.msn_pkm_scatter(self._h, _stream(), B, _ptr(idx), _ptr(w), _ptr(d), _ptr(V),
                                             _ptr(d_values), _ptr(dw), _ptr(ws), ws.numel()))
         return dw
-
-    def scatter_p2p(self, idx, w, values, d_values, dout_ptrs: torch.Tensor, dw_ptrs: torch.Tensor, world: int):
-        """a6 over this process's rows, d_out rows read from and dw written to the
-        home ranks' buffers (int64 device tensors of `world` addresses; see
-        msn_pkm_scatter_p2p)."""
-        idx, w, V = self._dev(idx), self._dev(w), self._dev(values)
-        B = idx.shape[0]
-        f, b = ctypes.c_size_t(), ctypes.c_size_t()
-        _lib.check(self.lib.msn_pkm_workspace_size(self._h, 0, B, ctypes.byref(f), ctypes.byref(b)))
-        ws = torch.empty(b.value, dtype=torch.uint8, device=self.device) \
-            if self._ws is None or self._ws.numel() < b.value else self._ws
-        _lib.check(self.lib.msn_pkm_scatter_p2p(self._h, _stream(), B, _ptr(idx), _ptr(w),
-                                                ctypes.c_void_p(dout_ptrs.data_ptr()), _ptr(V), _ptr(d_values),
-                                                ctypes.c_void_p(dw_ptrs.data_ptr()), world, B // world,
-                                                _ptr(ws), ws.numel()))
 
     def scatter_update(self, idx, w, d_out, values, update: str = "sgd", lr: float = 1e-3,
                        eps: float = 1e-10, state: Optional[torch.Tensor] = None):
@@ -338,6 +312,73 @@ class PKMLookup:
                                                   _ptr(dw), _ptr(d_query), _ptr(d_subkeys), _ptr(ws), ws.numel()))
         return d_query, d_subkeys
 
+
+    # ------------------------------------- a9 record exchange (sharded table)
+    def exchange_layout(self, local_batch: int, staged: bool):
+        """{region name: byte offset} and the total bytes of one exchange buffer."""
+        offs = (ctypes.c_int64 * len(_lib.XREG))()
+        nb = ctypes.c_size_t()
+        _lib.check(self.lib.msn_pkm_exchange_layout(self._h, local_batch, int(staged), offs, ctypes.byref(nb)))
+        return dict(zip(_lib.XREG, list(offs))), nb.value
+
+    def forward_sharded(self, query, subkeys, values, xchg, out=None, idx=None, w=None, ws=None):
+        """a1-a5 + a9 over peer memory (msn_pkm_forward_sharded): out [B_l, d_v]."""
+        B = query.shape[0]
+        if out is None:
+            out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        if idx is None:
+            idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        if w is None:
+            w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        if ws is None:
+            ws = self.workspace(B, xchg.world * B)
+        _lib.check(self.lib.msn_pkm_forward_sharded(self._h, _stream(), B, _ptr(query), _ptr(subkeys), _ptr(values),
+                                                    ctypes.byref(xchg), _ptr(out), _ptr(idx), _ptr(w),
+                                                    _ptr(ws), ws.numel()))
+        return out, idx, w
+
+    def backward_sharded(self, d_out, query, subkeys, values, idx, w, xchg, d_subkeys, d_values,
+                         d_query=None, dw=None, ws=None):
+        """a6-a8 + a9 over peer memory (msn_pkm_backward_sharded)."""
+        B = query.shape[0]
+        if d_query is None:
+            d_query = torch.empty((B, self.heads, 2, self.d_half), dtype=self.dq_dtype, device=self.device)
+        if dw is None:
+            dw = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        if ws is None:
+            ws = self.workspace(B, xchg.world * B)
+        _lib.check(self.lib.msn_pkm_backward_sharded(self._h, _stream(), B, _ptr(d_out), _ptr(query), _ptr(subkeys),
+                                                     _ptr(values), _ptr(idx), _ptr(w), ctypes.byref(xchg),
+                                                     _ptr(d_query), _ptr(d_subkeys), _ptr(d_values), _ptr(dw),
+                                                     _ptr(ws), ws.numel()))
+        return d_query, d_subkeys, d_values, dw
+
+    def exchange_route(self, idx, w, xchg):
+        _lib.check(self.lib.msn_pkm_exchange_route(self._h, _stream(), _ptr(idx), _ptr(w), ctypes.byref(xchg)))
+
+    def exchange_gather(self, values, xchg):
+        _lib.check(self.lib.msn_pkm_exchange_gather(self._h, _stream(), _ptr(values), ctypes.byref(xchg)))
+
+    def exchange_combine(self, xchg, out=None):
+        if out is None:
+            out = torch.empty((xchg.local_batch, self.d_value), dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.msn_pkm_exchange_combine(self._h, _stream(), ctypes.byref(xchg), _ptr(out)))
+        return out
+
+    def exchange_scatter(self, values, d_values, xchg, ws=None):
+        if ws is None:
+            ws = self.workspace(xchg.local_batch, xchg.world * xchg.local_batch)
+        _lib.check(self.lib.msn_pkm_exchange_scatter(self._h, _stream(), _ptr(values), _ptr(d_values),
+                                                     ctypes.byref(xchg), _ptr(ws), ws.numel()))
+
+    def exchange_collect(self, idx, xchg, dw=None):
+        if dw is None:
+            dw = torch.empty(tuple(idx.shape), dtype=torch.float32, device=self.device)
+        _lib.check(self.lib.msn_pkm_exchange_collect(self._h, _stream(), _ptr(idx), ctypes.byref(xchg), _ptr(dw)))
+        return dw
+
+    def exchange_barrier(self, xchg):
+        _lib.check(self.lib.msn_pkm_exchange_barrier(self._h, _stream(), ctypes.byref(xchg)))
 
     def step_host(self, query_h, d_out_h, subkeys, values, d_subkeys, d_values,
                   out_h=None, d_query_h=None, chunks: Optional[int] = None):

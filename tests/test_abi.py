@@ -45,14 +45,15 @@ def test_library_has_no_host_fallback_symbols(lib):
 
 def _cfg(**kw):
     from paper_2602_07526_b200 import _lib
-    base = dict(abi_version=1, heads=2, n_sub=64, d_half=32, d_value=64, k=8, max_batch=16,
+    base = dict(abi_version=2, heads=2, n_sub=64, d_half=32, d_value=64, k=8, max_batch=16,
                 qk_dtype=0, value_dtype=0, flags=0, reserved=0, row_begin=0, row_end=64 * 64)
     base.update(kw)
     return _lib.Config(**base)
 
 
 @pytest.mark.parametrize("bad,status", [
-    (dict(abi_version=2), 1), (dict(heads=0), 1), (dict(k=0), 1), (dict(k=65, n_sub=128, row_end=128 * 128), 2),
+    (dict(abi_version=1), 1), (dict(world_size=9), 1), (dict(world_size=2, rank=2), 1),
+    (dict(world_size=3), 1), (dict(world_size=2, row_begin=0, row_end=100), 1), (dict(heads=0), 1), (dict(k=0), 1), (dict(k=65, n_sub=128, row_end=128 * 128), 2),
     (dict(k=70), 1), (dict(d_half=24), 1), (dict(d_value=2, value_dtype=0), 1),
     (dict(row_begin=10, row_end=5), 1), (dict(flags=0x80), 1), (dict(qk_dtype=7), 1),
     (dict(n_sub=4096, row_end=4096 * 4096), 2),
@@ -88,5 +89,44 @@ def test_sharded_handle_rejects_full_forward(lib):
     h = ctypes.c_void_p()
     assert lib.msn_pkm_create(ctypes.byref(_cfg(row_begin=0, row_end=2048)), ctypes.byref(h)) == 0
     p = ctypes.c_void_p(0x1000)
+    assert lib.msn_pkm_forward(h, None, 4, p, p, p, p, p, p, p, 1 << 30) == 1
+    lib.msn_pkm_destroy(h)
+
+
+def _x(lib_mod, world, rank, lb, transport=0, bases=None):
+    x = lib_mod.Exchange()
+    x.transport, x.world, x.rank, x.local_batch = transport, world, rank, lb
+    for i, b in enumerate(bases or []):
+        x.base[i] = b
+    return x
+
+
+def test_sharded_config_and_exchange_checks(lib):
+    """world_size > 1 derives the rank's rows [r n/P, (r+1) n/P); the exchange
+    calls validate world/rank/transport/bases on the host before any launch."""
+    from paper_2602_07526_b200 import _lib
+    h = ctypes.c_void_p()
+    assert lib.msn_pkm_create(ctypes.byref(_cfg(world_size=4, rank=1, row_begin=0, row_end=0)), ctypes.byref(h)) == 0
+    offs = (ctypes.c_int64 * len(_lib.XREG))()
+    nb = ctypes.c_size_t()
+    assert lib.msn_pkm_exchange_layout(h, 16, 1, offs, ctypes.byref(nb)) == 0
+    assert list(offs) == sorted(offs) and all(o % 256 == 0 for o in offs) and nb.value >= offs[-1]
+    peer = ctypes.c_size_t()
+    assert lib.msn_pkm_exchange_layout(h, 16, 0, None, ctypes.byref(peer)) == 0 and peer.value < nb.value
+    # IN_ROW holds P * cap int32 records, cap = B_l * H * k
+    assert offs[1] - offs[0] >= 4 * 4 * 16 * 2 * 8
+    p = ctypes.c_void_p(0x100000)
+    good = _x(_lib, 4, 1, 16, 0, [0x100000, 0x200000, 0x300000, 0x400000])
+    assert lib.msn_pkm_exchange_route(h, None, None, None, ctypes.byref(good)) == 1     # null idx
+    for bad in (_x(_lib, 2, 1, 16, 0, [0x100000] * 2), _x(_lib, 4, 0, 16, 0, [0x100000] * 4),
+                _x(_lib, 4, 1, 17, 0, [0x100000] * 4), _x(_lib, 4, 1, 16, 5, [0x100000] * 4),
+                _x(_lib, 4, 1, 16, 0, [0x100000, 0x100010, 0x100000, 0x100000]),
+                _x(_lib, 4, 1, 16, 0, [0x100000, 0, 0x100000, 0x100000])):
+        assert lib.msn_pkm_exchange_route(h, None, p, p, ctypes.byref(bad)) == 1, lib.msn_pkm_last_error()
+    # staged: only base[rank] is needed; forward_sharded needs the peer transport
+    st = _x(_lib, 4, 1, 16, 1, [0, 0x100000, 0, 0])
+    assert lib.msn_pkm_forward_sharded(h, None, 16, p, p, p, ctypes.byref(st), p, p, p, p, 1 << 30) == 1
+    assert b"PEER" in lib.msn_pkm_last_error()
+    # the whole-table forward is refused on a shard
     assert lib.msn_pkm_forward(h, None, 4, p, p, p, p, p, p, p, 1 << 30) == 1
     lib.msn_pkm_destroy(h)

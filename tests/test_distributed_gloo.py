@@ -1,9 +1,15 @@
-"""World-size-2 gloo tests (CPU) of the row-sharded table's host plumbing
-(paper_2602_07526_b200/distributed.py): all-gathers, reduce-scatters, shard
-ranges and the dw exactness argument.  The four data-path phases are stood in
-for by a CPU implementation built on the fp64 oracle (test-only; the product
-path has no CPU fallback), so what is checked here is the collective algebra:
-the sharded step must reproduce the unsharded oracle result."""
+"""World-size-2/4 gloo tests (CPU) of the row-sharded table's host plumbing
+(paper_2602_07526_b200/distributed.py, transport "nccl"): the counts
+exchange, the counted send/recv of the records and of the returned dw, the
+fixed-size all-to-alls of the per-query offsets and the partials, the
+all-gather of d_out, shard ranges.  The exchange buffer and its region layout
+are the library's (msn_pkm_exchange_layout, a host function); the data-path
+kernels are stood in for by a CPU implementation of the phases' documented
+semantics (include/msn_pkm.h, "the row-sharded table with the library's record
+exchange") built on the fp64 oracle -- test infrastructure only (the product
+path has no CPU fallback).  The sharded step must reproduce the unsharded
+oracle result.  The kernels themselves are checked against the oracle with
+emulated ranks on the GPU (tests/test_gpu_sharded.py)."""
 import os
 import socket
 
@@ -17,37 +23,81 @@ from oracle import oracle as orc
 
 
 class OraclePhases:
-    """CPU stand-in for the four C-ABI phase calls (test infrastructure)."""
+    """CPU stand-in for the C-ABI phase calls of the STAGED exchange (test
+    infrastructure): reads and writes the exchange buffer's regions exactly as
+    include/msn_pkm.h documents them."""
 
-    def __init__(self, n_sub, k, row_begin, row_end):
-        self.n_sub, self.k, self.r0, self.r1 = n_sub, k, row_begin, row_end
+    def __init__(self, cfg, world, rank, B_l):
+        from paper_2602_07526_b200.pkm import PKMLookup
+        self.real = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, max_batch=B_l,
+                              qk_dtype=cfg.qk_dtype, value_dtype=cfg.value_dtype, device="cpu",
+                              world_size=world if world > 1 else 0, rank=rank)
+        self.heads, self.k, self.d_value, self.n_sub = cfg.heads, cfg.k, cfg.d_value, cfg.n_sub
+        self.P, self.rank, self.lb = world, rank, B_l
+        self.rpr = cfg.n_slots // world
+        self.xb = None  # set after ShardedPKM builds the buffer
+
+    def exchange_layout(self, lb, staged):
+        return self.real.exchange_layout(lb, staged)
+
+    def workspace(self, B, gb=None):
+        return torch.empty(1, dtype=torch.uint8)
 
     def select(self, q, K):
         o = orc.forward(q, K, np.zeros((self.n_sub * self.n_sub, 4), np.float32), self.k)
         return torch.from_numpy(o["idx"].astype(np.int32)), torch.from_numpy(o["w"]).float()
 
-    def gather(self, idx, w, Vs):
-        B, H, k = idx.shape
-        out = torch.zeros((B, Vs.shape[1]), dtype=torch.float64)
-        for b in range(B):
-            for h in range(H):
-                for t in range(k):
-                    f = int(idx[b, h, t])
-                    if self.r0 <= f < self.r1:
-                        out[b] += float(w[b, h, t]) * Vs[f - self.r0].double()
-        return out.float()
+    def exchange_route(self, idx, w, x):
+        P, lb, cap = self.P, self.lb, self.xb.cap
+        o_row, o_w, o_q, o_off = self.xb.records(out=True)
+        pos = self.xb.region("POS", cap)
+        cnt = [0] * P
+        HK = self.heads * self.k
+        for o in range(P):
+            o_off[o, 0] = 0
+        for b in range(lb):
+            for r in range(HK):
+                f = int(idx.view(lb, HK)[b, r])
+                o, row = f // self.rpr, f % self.rpr
+                o_row[o, cnt[o]], o_w[o, cnt[o]], o_q[o, cnt[o]] = row, w.view(lb, HK)[b, r], b
+                pos[b * HK + r] = cnt[o]
+                cnt[o] += 1
+            for o in range(P):
+                o_off[o, b + 1] = cnt[o]
+        self.xb.counts()[:] = torch.tensor(cnt, dtype=torch.int32)
 
-    def scatter(self, idx, w, d, Vs, dVs):
-        B, H, k = idx.shape
-        dw = torch.zeros((B, H, k))
-        for b in range(B):
-            for h in range(H):
-                for t in range(k):
-                    f = int(idx[b, h, t])
-                    if self.r0 <= f < self.r1:
-                        dw[b, h, t] = float((Vs[f - self.r0].double() * d[b].double()).sum())
-                        dVs[f - self.r0] += float(w[b, h, t]) * d[b]
-        return dw
+    def exchange_gather(self, Vs, x):
+        P, lb = self.P, self.lb
+        i_row, i_w, i_q, i_off = self.xb.records(out=False)
+        part = self.xb.region("PART_OUT", P, lb, self.d_value)
+        for s in range(P):
+            for b in range(lb):
+                acc = torch.zeros(self.d_value, dtype=torch.float64)
+                for j in range(int(i_off[s, b]), int(i_off[s, b + 1])):
+                    assert int(i_q[s, j]) == b
+                    acc += float(i_w[s, j]) * Vs[int(i_row[s, j])].double()
+                part[s, b] = acc.float()
+
+    def exchange_combine(self, x, out=None):
+        part = self.xb.region("PART_IN", self.P, self.lb, self.d_value)
+        return part.double().sum(0).float()
+
+    def exchange_scatter(self, Vs, dVs, x, ws=None):
+        P, lb = self.P, self.lb
+        i_row, i_w, i_q, i_off = self.xb.records(out=False)
+        dall = self.xb.region("DOUT_ALL", P, lb, self.d_value)
+        dw_out = self.xb.region("DW_OUT", P, self.xb.cap)
+        for s in range(P):
+            for j in range(int(i_off[s, lb])):
+                row, d = int(i_row[s, j]), dall[s, int(i_q[s, j])]
+                dw_out[s, j] = float((Vs[row].double() * d.double()).sum())
+                dVs[row] += float(i_w[s, j]) * d
+
+    def exchange_collect(self, idx, x, dw=None):
+        dw_in = self.xb.region("DW_IN", self.P, self.xb.cap)
+        pos = self.xb.region("POS", self.xb.cap)
+        f = idx.reshape(-1).long()
+        return dw_in[f // self.rpr, pos.long()].view(idx.shape).clone()
 
     def backward_keys(self, q, K, idx, w, dw, dK):
         B, H, k = idx.shape
@@ -84,13 +134,15 @@ def _worker(rank, world, port, result_q):
     try:
         from paper_2602_07526_b200.distributed import ShardedPKM
         from paper_2602_07526_b200 import workloads as wl
-        cfg = wl.tiny_config(6 * world, 2, 8, 8, 8, 3, torch.float32, torch.float32, index=77)
+        cfg = wl.tiny_config(6 * world, 2, 16, 8, 8, 3, torch.float32, torch.float32, index=77)
         Q, K, V, dOut = wl.make_all(cfg)
         B_l = cfg.batch // world
         n = cfg.n_slots
         r0, r1 = rank * n // world, (rank + 1) * n // world
-        sp = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l,
-                        phases=OraclePhases(cfg.n_sub, cfg.k, r0, r1))
+        ph = OraclePhases(cfg, world, rank, B_l)
+        sp = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l, cfg.qk_dtype,
+                        cfg.value_dtype, phases=ph, device="cpu", transport="nccl")
+        ph.xb = sp.xb
         assert (sp.row_begin, sp.row_end) == (r0, r1)
         q_l = Q[rank * B_l:(rank + 1) * B_l].contiguous()
         d_l = dOut[rank * B_l:(rank + 1) * B_l].contiguous()
@@ -142,7 +194,7 @@ def _bad_worker(rank, world, port, result_q):
     try:
         from paper_2602_07526_b200.distributed import ShardedPKM
         try:
-            ShardedPKM(1, 5, 16, 16, 2, 4, phases=object())  # 25 rows over 2 ranks
+            ShardedPKM(1, 5, 16, 16, 2, 4, phases=object(), transport="nccl")  # 25 rows over 2 ranks
             result_q.put("no error")
         except ValueError:
             result_q.put("ok")

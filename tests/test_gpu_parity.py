@@ -739,67 +739,6 @@ def test_step_host_pipelined_matches_device():
     torch.testing.assert_close(dK2, dK, rtol=1e-4, atol=1e-6)
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_gather_push_matches_sharded_gather(P):
-    """The gather fused with the reduce-scatter (msn_pkm_gather_push +
-    msn_pkm_reduce_partials), P ranks emulated on one GPU (their receive
-    buffers are local tensors; each emulated rank's kernel runs to completion
-    before the reductions): every home rank's output equals the rank-order sum
-    of the P shard gathers bitwise, and the unsharded forward up to fp32
-    reassociation."""
-    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=256 * P)
-    Q, K, V, _ = wl.make_all(cfg, DEV)
-    full = lookup_for(cfg)
-    out_full, idx, w = full.forward(Q, K, V)
-    n, B_l = cfg.n_slots, cfg.batch // P
-    recv = [torch.full((P, B_l, cfg.d_value), float("nan"), device=DEV) for _ in range(P)]
-    ptrs = torch.tensor([r.data_ptr() for r in recv], dtype=torch.int64, device=DEV)
-    parts = []
-    for r in range(P):
-        r0, r1 = r * n // P, (r + 1) * n // P
-        lk = lookup_for(cfg, row_begin=r0, row_end=r1)
-        Vs = V[r0:r1].contiguous()
-        parts.append(lk.gather(idx, w, Vs))
-        lk.gather_push(idx, w, Vs, ptrs, P, r)
-    torch.cuda.synchronize()
-    for home in range(P):
-        out = full.reduce_partials(recv[home], P)
-        ref = parts[0][home * B_l:(home + 1) * B_l].clone()
-        for r in range(1, P):
-            ref += parts[r][home * B_l:(home + 1) * B_l]
-        assert torch.equal(out, ref)
-        torch.testing.assert_close(out, out_full[home * B_l:(home + 1) * B_l], rtol=1e-5, atol=1e-6)
-
-
-@pytest.mark.parametrize("P", [2, 4])
-def test_scatter_p2p_matches_sharded_scatter(P):
-    """The row-sharded backward over peer memory (msn_pkm_scatter_p2p), P ranks
-    emulated on one GPU: every rank's dV shard is bitwise the one the
-    all-gather path (msn_pkm_scatter on the gathered d_out) produces, and every
-    home rank's dw equals the reduce-scattered dw (one owner per element)."""
-    cfg = wl.CONFIGS["c2_mid_bf16"].scaled(batch=256 * P)
-    Q, K, V, dOut = wl.make_all(cfg, DEV)
-    full = lookup_for(cfg)
-    _, idx, w = full.forward(Q, K, V)
-    n, B_l = cfg.n_slots, cfg.batch // P
-    douts = [dOut[p * B_l:(p + 1) * B_l].contiguous() for p in range(P)]
-    dws = [torch.full((B_l, cfg.heads, cfg.k), float("nan"), device=DEV) for _ in range(P)]
-    dptrs = torch.tensor([t.data_ptr() for t in douts], dtype=torch.int64, device=DEV)
-    wptrs = torch.tensor([t.data_ptr() for t in dws], dtype=torch.int64, device=DEV)
-    dw_sum = torch.zeros((cfg.batch, cfg.heads, cfg.k), device=DEV)
-    for r in range(P):
-        r0, r1 = r * n // P, (r + 1) * n // P
-        lk = lookup_for(cfg, row_begin=r0, row_end=r1)
-        Vs = V[r0:r1].contiguous()
-        dv_ref = torch.zeros((r1 - r0, cfg.d_value), device=DEV)
-        dw_sum += lk.scatter(idx, w, dOut, Vs, dv_ref)
-        dv = torch.zeros_like(dv_ref)
-        lk.scatter_p2p(idx, w, Vs, dv, dptrs, wptrs, P)
-        torch.cuda.synchronize()
-        assert torch.equal(dv, dv_ref)
-    assert torch.equal(torch.cat(dws), dw_sum)
-
-
 def _random_shapes(n, seed=2602):
     """Seeded random shapes across the library's supported ranges: B ragged,
     H up to 8, n_sub from 16 to 1024 (tcgen05 resident and two-sweep rows,
