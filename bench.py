@@ -606,7 +606,7 @@ def run_sharded(args, rank, world, local_rank):
     # (1) per-phase breakdown (peer transport): the same kernels through the
     # phase calls, CUDA events between them (eager; launch gaps included)
     per, reduce_ms = {}, 0.0
-    phases = ["select", "cartesian", "route", "gather", "combine", "scatter", "backward_keys"]
+    phases = ["select", "cartesian_route", "gather", "combine", "scatter", "backward_keys"]
     if peer:
         per = {p: 0.0 for p in phases}
         nb = max(2, min(args.steps, 10))
@@ -621,10 +621,9 @@ def run_sharded(args, rank, world, local_rank):
             e[0].record(stream)
             arr = (ctypes.c_void_p * 2)(e[1].cuda_event, e[2].cuda_event)
             check(lk.lib.msn_pkm_set_trace_events(lk._h, arr, 2))
-            check(lk.lib.msn_pkm_select(lk._h, sptr, B_l, _ptr(q_l), _ptr(K), _ptr(idx), _ptr(w), _ptr(ws),
-                                        ws.numel()))
+            check(lk.lib.msn_pkm_exchange_select(lk._h, sptr, _ptr(q_l), _ptr(K), _ptr(Vs), ctypes.byref(x),
+                                                 _ptr(idx), _ptr(w), _ptr(out), _ptr(ws), ws.numel()))
             check(lk.lib.msn_pkm_set_trace_events(lk._h, None, 0))
-            lk.exchange_route(idx, w, x)
             lk.exchange_barrier(x)
             e[3].record(stream)
             lk.exchange_gather(Vs, x)
@@ -645,7 +644,10 @@ def run_sharded(args, rank, world, local_rank):
                                                _ptr(dq), _ptr(dK), _ptr(ws), ws.numel()))
             e[7].record(stream)
         torch.cuda.synchronize()
-        order = [(0, 1, "select"), (1, 2, "cartesian"), (2, 3, "route"), (3, 4, "gather"), (4, 5, "combine"),
+        # select = the tcgen05 scorer; cartesian_route = the fused Cartesian top-k +
+        # softmax + route + local-shard gather (+ barrier); gather = the remote
+        # windows (+ barrier); scatter includes the d_out hand-over and barriers
+        order = [(0, 1, "select"), (1, 3, "cartesian_route"), (3, 4, "gather"), (4, 5, "combine"),
                  (5, 6, "scatter"), (6, 7, "backward_keys")]
         for e in evs:
             for a, b, name in order:
@@ -747,13 +749,14 @@ def run_sharded(args, rank, world, local_rank):
     esz = 2 if cfg.value_dtype == torch.bfloat16 else 4
     HK = cfg.heads * cfg.k
     contrib_l = B_l * HK
-    # algorithmic bytes per launch: gather of the records:
-    # records (12 B) + value rows + the partial rows written; dV reducer: every
-    # touched row's V read once, dV read + written once (fp32), 12 B per record
-    # (row, w, query) + 4 B dw, + the d_out rows read once per (source, query)
+    # algorithmic bytes per step and rank: the forward's
+    # value rows + records written and read (8 B each) + idx/w (8 B per slot)
+    # + the partial rows; the dV reducer: every touched row's V read once, dV
+    # read + written once (fp32), 12 B per record (row, w, dw) + the d_out rows
+    # read once per (source, query)
     rec_l = contrib_l  # records this rank receives (= sends, in expectation, uniform slots)
-    gather_b = rec_l * (12 + cfg.d_value * esz) + world * B_l * cfg.d_value * 4
-    scatter_b = (uniq_local or 0) * cfg.d_value * (esz + 8) + rec_l * 16 + world * B_l * cfg.d_value * 4
+    gather_b = rec_l * (cfg.d_value * esz + 8 + 8) + contrib_l * 8 + world * B_l * cfg.d_value * 4
+    scatter_b = (uniq_local or 0) * cfg.d_value * (esz + 8) + rec_l * 12 + world * B_l * cfg.d_value * 4
     select_f = 4 * B_l * cfg.heads * cfg.n_sub * cfg.d_half
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -762,9 +765,10 @@ def run_sharded(args, rank, world, local_rank):
     cands = {}
     if peer:
         cands = {
-            "gather": {"kernel": "gather_records_kernel (a5 over the received records, partials to the home)",
-                       "bound": "hbm", "ms": per["gather"], "work": gather_b, "peak": hbm, "unit": "GB/s",
-                       "traffic": traffic.get("gather")},
+            "gather": {"kernel": ("cartesian_route_kernel (a3+a4 + route + the local shard's a5, fused)" if world == 1
+                                  else "gather_records_kernel + the local shard in cartesian_route_kernel (a5)"),
+                       "bound": "hbm", "ms": per["cartesian_route"] + per["gather"], "work": gather_b, "peak": hbm,
+                       "unit": "GB/s", "traffic": traffic.get("gather")},
             "dv_reduce": {"kernel": "grp_reduce_short_kernel (a6 over the received records: dV +=, dw)",
                           "bound": "hbm", "ms": reduce_ms, "work": scatter_b, "peak": hbm, "unit": "GB/s",
                           "traffic": traffic.get("dv_reduce")},

@@ -265,55 +265,57 @@ msn_status msn_pkm_backward_keys(msn_pkm_t h, void* stream, int64_t B,
  *
  * Rank p is home to its local_batch = B_l queries and owns value rows
  * [p n/P, (p+1) n/P) (owner(f) = f / (n/P)); the sub-keys are replicated.
- *   forward   select (a1-a4, local queries) -> ROUTE: every (b, h, t) slot becomes
- *             a record {local row, w, b} sent to its owner (all-to-all of records,
- *             12 B each, grouped by query) -> GATHER: every owner sums w V[row]
- *             over the records of each (source, query) into a partial row and
- *             returns it to the source (all-to-all of partials) -> COMBINE: the
- *             home adds the P partials in owner order.
- *   backward  every owner reads the d_out rows its records need (from the home's
- *             DOUT region), SCATTERs (dV shard +=, dw per record, the same grouped
- *             deterministic reduction as msn_pkm_scatter, records summed in global
- *             contribution order -> dV shards bitwise equal to the unsharded dV)
- *             and returns dw per record -> COLLECT: the home puts dw back in
- *             (b, h, t) order -> backward_keys (a7-a8) on the local queries.
+ *   forward   SELECT: scoring a1-a2 and the Cartesian top-k + softmax a3-a4 of
+ *             the local queries, fused with the ROUTE: every slot (b, h, t)
+ *             becomes an 8-byte record {local row, w} in its owner's window for
+ *             (this source, b) -- H*k slots per (source, query), records in
+ *             (h, t) order, count in IN_CNT -- and the rows this rank owns are
+ *             gathered right there into its own partial (a5, local shard);
+ *             GATHER: every owner sums w V[row] over the records of each
+ *             (remote source, query) and returns the partial row to the source;
+ *             COMBINE: the home adds the P partials in owner order.
+ *   backward  every owner reads the d_out rows its records need (from the
+ *             home's DOUT), SCATTERs (dV shard +=, dw per record: the grouped
+ *             deterministic reduction of msn_pkm_scatter, records summed in
+ *             global contribution order -> dV shards bitwise equal to the
+ *             unsharded dV) and returns dw per record -> COLLECT: the home puts
+ *             dw back in (b, h, t) order -> backward_keys (a7-a8) locally.
  * Every rank has one exchange buffer of msn_pkm_exchange_layout() bytes (the
  * caller allocates it; zero-filled once before first use).  Two transports:
  *   MSN_XCHG_PEER   base[p] is rank p's buffer mapped into this process (torch
- *                   symmetric memory / CUDA IPC, NVLink peer memory): ROUTE,
+ *                   symmetric memory / CUDA IPC, NVLink peer memory): SELECT,
  *                   GATHER and SCATTER store straight into the peers' IN regions
- *                   (the transfer is issued by the compute kernel, row by row),
- *                   msn_pkm_exchange_barrier orders the ranks (device-side flags,
- *                   no host sync: graph-capturable).  msn_pkm_forward_sharded /
- *                   msn_pkm_backward_sharded run the whole step.
+ *                   (the all-to-all is issued by the compute kernels, record by
+ *                   record and row by row: only the actual records and partials
+ *                   cross NVLink); msn_pkm_exchange_barrier orders the ranks
+ *                   (device-side flags, no host sync: graph-capturable).
+ *                   msn_pkm_forward_sharded / msn_pkm_backward_sharded run the
+ *                   whole step.
  *   MSN_XCHG_STAGED only base[rank] is used: outgoing data is staged in the OUT
  *                   regions (segment p for rank p) and the caller moves them
- *                   with its collectives (NCCL all-to-all(v) over NVLink):
- *                   OUT_ROW/OUT_W/OUT_Q segment p (CTL counts[p] records) ->
- *                   rank p's IN_* segment [rank]; OUT_OFF -> IN_OFF; PART_OUT ->
- *                   PART_IN; DW_OUT segment p (the IN counts) -> DW_IN; the
- *                   caller all-gathers the homes' d_out into DOUT_ALL.
- * Region layout of one exchange buffer (cap = B_l * heads * k records per
- * (source, owner) pair; offsets from msn_pkm_exchange_layout, 256-B aligned): */
+ *                   with fixed-size collectives (NCCL over NVLink, no host sync):
+ *                   all-to-all OUT_ROW/OUT_W/OUT_CNT -> IN_ROW/IN_W/IN_CNT,
+ *                   PART_OUT -> PART_IN, DW_OUT -> DW_IN, and an all-gather of
+ *                   the homes' d_out into DOUT_ALL.  Whole windows move (P x
+ *                   B_l*H*k records per rank): the baseline the peer transport
+ *                   is measured against.
+ * Region layout of one exchange buffer (cap = B_l*H*k: one window of H*k
+ * records per query; offsets from msn_pkm_exchange_layout, 256-B aligned): */
 enum {
-  MSN_XREG_IN_ROW = 0,  /* int32 [P][cap]  local row of the records source s sent here */
-  MSN_XREG_IN_W,        /* fp32  [P][cap]  their weights */
-  MSN_XREG_IN_Q,        /* int32 [P][cap]  their query (index in the source's batch) */
-  MSN_XREG_IN_OFF,      /* int32 [P][B_l+1] per-query record offsets of segment s ([B_l] = count) */
-  MSN_XREG_PART_IN,     /* fp32  [P][B_l][d_value] partial sums returned by owner o */
+  MSN_XREG_IN_ROW = 0,  /* int32 [P][B_l][H*k] local rows of the records source s sent here */
+  MSN_XREG_IN_W,        /* fp32  [P][B_l][H*k] their weights */
+  MSN_XREG_IN_CNT,      /* int32 [P][B_l]      records in window (s, b) */
+  MSN_XREG_PART_IN,     /* fp32  [P][B_l][d_value] partial sums from owner o ([rank]: the local shard) */
   MSN_XREG_DOUT,        /* fp32  [B_l][d_value] this home's d_out (read by the owners) */
-  MSN_XREG_DW_IN,       /* fp32  [P][cap]  dw returned by owner o, in this home's record order */
-  MSN_XREG_POS,         /* int32 [B_l*H*k] slot (b,h,t) -> its record's position in owner's segment */
-  MSN_XREG_CTL,         /* uint32 [64]: [0,P) barrier flags, [16] epoch, [17] barrier timeout,
-                           [32, 32+P) records this rank sent to owner p (counts) */
-  MSN_XREG_SCRATCH,     /* int32 [2][P][B_l+1] route scratch (local) */
-  MSN_XREG_OUT_ROW,     /* STAGED only: int32 [P][cap] records for owner p */
-  MSN_XREG_OUT_W,       /*   fp32  [P][cap] */
-  MSN_XREG_OUT_Q,       /*   int32 [P][cap] */
-  MSN_XREG_OUT_OFF,     /*   int32 [P][B_l+1] */
+  MSN_XREG_DW_IN,       /* fp32  [P][B_l][H*k] dw returned by owner o, in o's window order */
+  MSN_XREG_POS,         /* int32 [B_l*H*k] slot (b,h,t) -> its record's position in the window */
+  MSN_XREG_CTL,         /* uint32 [64]: [0,P) barrier flags, [16] epoch, [17] barrier timeout */
+  MSN_XREG_OUT_ROW,     /* STAGED only: int32 [P][B_l][H*k] records for owner p */
+  MSN_XREG_OUT_W,       /*   fp32  [P][B_l][H*k] */
+  MSN_XREG_OUT_CNT,     /*   int32 [P][B_l] */
   MSN_XREG_PART_OUT,    /*   fp32  [P][B_l][d_value] partials for home s */
   MSN_XREG_DOUT_ALL,    /*   fp32  [P][B_l][d_value] every home's d_out (all-gathered) */
-  MSN_XREG_DW_OUT,      /*   fp32  [P][cap] dw for home s, in s's record order */
+  MSN_XREG_DW_OUT,      /*   fp32  [P][B_l][H*k] dw for home s, in this owner's window order */
   MSN_XREG_COUNT
 };
 typedef enum { MSN_XCHG_PEER = 0, MSN_XCHG_STAGED = 1 } msn_exchange_transport;
@@ -332,8 +334,8 @@ typedef struct {
 msn_status msn_pkm_exchange_layout(msn_pkm_t h, int64_t local_batch, int32_t staged,
                                    int64_t* offsets, size_t* bytes);
 
-/* The whole sharded forward (PEER transport): select a1-a4 on the B_l local
- * queries, ROUTE, barrier, GATHER, barrier, COMBINE.  values = this rank's
+/* The whole sharded forward (PEER transport): SELECT (a1-a4 + route + the
+ * local shard's gather), barrier, GATHER, barrier, COMBINE.  values = this rank's
  * rows [n/P, d_value]; out [B_l, d_value] fp32 (=); idx / weights [B_l,H,k]
  * (the tape, global slot ids).  Every rank calls it with the same B_l. */
 msn_status msn_pkm_forward_sharded(msn_pkm_t h, void* stream, int64_t local_batch, const void* query,
@@ -352,23 +354,28 @@ msn_status msn_pkm_backward_sharded(msn_pkm_t h, void* stream, int64_t local_bat
 
 /* The phases (both transports; the STAGED caller moves the data in between;
  * ranks emulated on one GPU call them rank by rank, no barrier needed). */
-/* ROUTE: idx/weights [B_l,H,k] of this rank's queries -> records into every
- * owner's IN segment [rank] (PEER) or OUT segment [owner] (STAGED), per-query
- * offsets likewise, POS, and CTL counts. */
-msn_status msn_pkm_exchange_route(msn_pkm_t h, void* stream, const int32_t* idx, const float* weights,
-                                  const msn_pkm_exchange* x);
-/* GATHER: for every source s and query b, the partial sum of w V[row] over the
- * records in IN segment s -> PART_IN[rank][b] of rank s (PEER) or PART_OUT[s][b]
- * (STAGED); zeros for a query without records here. */
+/* SELECT: a1-a4 of the B_l local queries (idx / weights [B_l,H,k], the tape)
+ * fused with the ROUTE into the owners' windows (+ POS, IN_CNT) and the gather
+ * of the local shard's rows into PART_IN[rank] (PEER; PART_OUT[rank] when
+ * STAGED; with P = 1 straight into out, which COMBINE then leaves as it is).
+ * Workspace: msn_pkm_workspace_size(h, B_l, ...) forward bytes. */
+msn_status msn_pkm_exchange_select(msn_pkm_t h, void* stream, const void* query, const void* subkeys,
+                                   const void* values, const msn_pkm_exchange* x, int32_t* idx,
+                                   float* weights, float* out, void* workspace, size_t workspace_bytes);
+/* GATHER: for every REMOTE source s and query b, the partial sum of w V[row]
+ * over the records of window (s, b) -> PART_IN[rank][b] of rank s (PEER) or
+ * PART_OUT[s][b] (STAGED); zeros for an empty window. */
 msn_status msn_pkm_exchange_gather(msn_pkm_t h, void* stream, const void* values, const msn_pkm_exchange* x);
-/* COMBINE: out[b] = sum_o PART_IN[o][b], o ascending (=). */
+/* COMBINE: out[b] = sum_o PART_IN[o][b], o ascending (=); P = 1: nothing to
+ * add (SELECT wrote out). */
 msn_status msn_pkm_exchange_combine(msn_pkm_t h, void* stream, const msn_pkm_exchange* x, float* out);
-/* SCATTER: dV shard (+=) and dw of every record in the IN segments, d_out rows
+/* SCATTER: dV shard (+=) and dw of every record in the IN windows, d_out rows
  * from the homes' DOUT (PEER) or DOUT_ALL (STAGED); dw -> DW_IN[rank] of the
- * home (PEER) or DW_OUT[s] (STAGED).  Workspace as msn_pkm_backward_sharded. */
+ * home (PEER) or DW_OUT[s] (STAGED), in window order.  Workspace as
+ * msn_pkm_backward_sharded. */
 msn_status msn_pkm_exchange_scatter(msn_pkm_t h, void* stream, const void* values, float* d_values,
                                     const msn_pkm_exchange* x, void* workspace, size_t workspace_bytes);
-/* COLLECT: dw[b,h,t] = DW_IN[owner][POS[b,h,t]] (=). */
+/* COLLECT: dw[b,h,t] = DW_IN[owner][b][POS[b,h,t]] (=). */
 msn_status msn_pkm_exchange_collect(msn_pkm_t h, void* stream, const int32_t* idx,
                                     const msn_pkm_exchange* x, float* dw);
 /* Device-side barrier over the P ranks (PEER): release-store of an epoch into

@@ -44,8 +44,8 @@ class Config(ctypes.Structure):
 
 # msn_pkm_exchange (a9, the row-sharded table's record exchange)
 XCHG_PEER, XCHG_STAGED = 0, 1
-XREG = ["IN_ROW", "IN_W", "IN_Q", "IN_OFF", "PART_IN", "DOUT", "DW_IN", "POS", "CTL", "SCRATCH",
-        "OUT_ROW", "OUT_W", "OUT_Q", "OUT_OFF", "PART_OUT", "DOUT_ALL", "DW_OUT"]
+XREG = ["IN_ROW", "IN_W", "IN_CNT", "PART_IN", "DOUT", "DW_IN", "POS", "CTL",
+        "OUT_ROW", "OUT_W", "OUT_CNT", "PART_OUT", "DOUT_ALL", "DW_OUT"]
 
 
 class Exchange(ctypes.Structure):
@@ -75,7 +75,7 @@ SIGNATURES = {
     "msn_pkm_forward_sharded": [_P, _P, _I64, _P, _P, _P, ctypes.POINTER(Exchange), _P, _P, _P, _P, _SZ],
     "msn_pkm_backward_sharded": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Exchange), _P, _P, _P,
                                  _P, _P, _SZ],
-    "msn_pkm_exchange_route": [_P, _P, _P, _P, ctypes.POINTER(Exchange)],
+    "msn_pkm_exchange_select": [_P, _P, _P, _P, _P, ctypes.POINTER(Exchange), _P, _P, _P, _P, _SZ],
     "msn_pkm_exchange_gather": [_P, _P, _P, ctypes.POINTER(Exchange)],
     "msn_pkm_exchange_combine": [_P, _P, ctypes.POINTER(Exchange), _P],
     "msn_pkm_exchange_scatter": [_P, _P, _P, _P, ctypes.POINTER(Exchange), _P, _SZ],

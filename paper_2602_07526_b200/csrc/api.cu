@@ -72,6 +72,19 @@ size_t fwd_bytes(const Shape& s) {
   return b;
 }
 
+// the candidate lists at the start of the forward workspace; returns the rest
+char* carve_cands(const Shape& s, void* ws, Cands& cd) {
+  cd.SC = select_segments(s, true);
+  cd.S = select_segments(s, false);
+  const int64_t rows = s.B * s.H * 2 * cd.SC;
+  char* p = (char*)ws;
+  cd.vc = (uint2*)p;
+  p += align256(sizeof(uint2) * rows * kCandCap);
+  cd.n = (int32_t*)p;
+  p += align256(sizeof(int32_t) * rows);
+  return p;
+}
+
 msn_status check_bwd_shape(msn_pkm_t h, bool values, bool keys) {
   if (backward_supported(shape_of(h->cfg, 0), values, keys)) return MSN_OK;
   return fail(MSN_ERR_UNSUPPORTED,
@@ -123,14 +136,7 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   if (ws_bytes < fwd_bytes(s))
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
   Cands cd;
-  cd.SC = select_segments(s, true);
-  cd.S = select_segments(s, false);
-  const int64_t rows = B * s.H * 2 * cd.SC;
-  char* p = (char*)ws;
-  cd.vc = (uint2*)p;
-  p += align256(sizeof(uint2) * rows * kCandCap);
-  cd.n = (int32_t*)p;
-  p += align256(sizeof(int32_t) * rows);
+  char* p = carve_cands(s, ws, cd);
   cd.rq.Q = query;
   cd.rq.K = subkeys;
   cd.rq.d_h = s.d_h;
@@ -579,16 +585,15 @@ struct XLayout {
 XLayout xlayout(const msn_pkm_config& c, int P, int64_t lb, bool staged) {
   const int64_t cap = lb * c.heads * c.k, dv = c.d_value;
   int64_t sz[MSN_XREG_COUNT] = {};
-  sz[MSN_XREG_IN_ROW] = sz[MSN_XREG_IN_W] = sz[MSN_XREG_IN_Q] = sz[MSN_XREG_DW_IN] = 4 * P * cap;
-  sz[MSN_XREG_IN_OFF] = 4 * P * (lb + 1);
+  sz[MSN_XREG_IN_ROW] = sz[MSN_XREG_IN_W] = sz[MSN_XREG_DW_IN] = 4 * P * cap;
+  sz[MSN_XREG_IN_CNT] = 4 * P * lb;
   sz[MSN_XREG_PART_IN] = 4 * P * lb * dv;
   sz[MSN_XREG_DOUT] = 4 * lb * dv;
   sz[MSN_XREG_POS] = 4 * cap;
   sz[MSN_XREG_CTL] = 4 * 64;
-  sz[MSN_XREG_SCRATCH] = 4 * 2 * P * (lb + 1);
   if (staged) {
-    sz[MSN_XREG_OUT_ROW] = sz[MSN_XREG_OUT_W] = sz[MSN_XREG_OUT_Q] = sz[MSN_XREG_DW_OUT] = 4 * P * cap;
-    sz[MSN_XREG_OUT_OFF] = 4 * P * (lb + 1);
+    sz[MSN_XREG_OUT_ROW] = sz[MSN_XREG_OUT_W] = sz[MSN_XREG_DW_OUT] = 4 * P * cap;
+    sz[MSN_XREG_OUT_CNT] = 4 * P * lb;
     sz[MSN_XREG_PART_OUT] = sz[MSN_XREG_DOUT_ALL] = 4 * P * lb * dv;
   }
   XLayout L;
@@ -603,7 +608,7 @@ XLayout xlayout(const msn_pkm_config& c, int P, int64_t lb, bool staged) {
 
 // The per-call view of the exchange: sizes and every pointer a phase needs.
 struct XView {
-  int P, rank;
+  int P, rank, HK;
   bool staged;
   int64_t lb, cap, rpr;
   XLayout L;
@@ -615,11 +620,12 @@ struct XView {
   RecordsIn records_in() const {
     RecordsIn ri;
     ri.P = P;
+    ri.rank = rank;
     ri.lb = lb;
     ri.cap = cap;
+    ri.HK = HK;
     ri.row = own<int32_t>(MSN_XREG_IN_ROW);
-    ri.q = own<int32_t>(MSN_XREG_IN_Q);
-    ri.off = own<int32_t>(MSN_XREG_IN_OFF);
+    ri.cnt = own<int32_t>(MSN_XREG_IN_CNT);
     ri.w = own<float>(MSN_XREG_IN_W);
     return ri;
   }
@@ -636,7 +642,7 @@ msn_status make_view(msn_pkm_t h, const msn_pkm_exchange* x, XView& v) {
   if (x->local_batch < 0 || x->local_batch > c.max_batch)
     return fail(MSN_ERR_INVALID_ARG, "local_batch %lld outside [0, max_batch]", (long long)x->local_batch);
   if (c.head_groups > 1) return fail(MSN_ERR_UNSUPPORTED, "the exchange needs head_groups <= 1");
-  if (c.heads * c.k > 512) return fail(MSN_ERR_UNSUPPORTED, "the exchange needs heads * k <= 512");
+  if (c.heads * c.k > 256) return fail(MSN_ERR_UNSUPPORTED, "the exchange needs heads * k <= 256");
   if (c.flags & (MSN_FLAG_ATOMIC_BWD | MSN_FLAG_GROUP_TABLES))
     return fail(MSN_ERR_UNSUPPORTED, "the exchange runs the deterministic backward over one table");
   const int64_t n = (int64_t)c.n_sub * c.n_sub;
@@ -652,40 +658,53 @@ msn_status make_view(msn_pkm_t h, const msn_pkm_exchange* x, XView& v) {
   v.rank = c.rank;
   v.staged = staged;
   v.lb = x->local_batch;
-  v.cap = v.lb * c.heads * c.k;
+  v.HK = c.heads * c.k;
+  v.cap = v.lb * v.HK;
   v.rpr = n / P;
   v.L = xlayout(c, P, v.lb, staged);
   v.x = x;
   return MSN_OK;
 }
 
-cudaError_t x_route(msn_pkm_t h, const XView& v, const int32_t* idx, const float* w, cudaStream_t st, int* L) {
-  RouteArgs a;
-  a.P = v.P;
-  a.lb = v.lb;
-  a.rpr = v.rpr;
-  for (int o = 0; o < kMaxWorld; ++o) {
-    a.row.p[o] = a.q.p[o] = a.off.p[o] = nullptr;
-    a.w.p[o] = nullptr;
-  }
+// SELECT: the scorer (a1-a2), then the fused Cartesian + route + local gather.
+msn_status x_select(msn_pkm_t h, const XView& v, const void* query, const void* subkeys, const void* values,
+                    int32_t* idx, float* w, float* out, void* ws, size_t ws_bytes, cudaStream_t st, int* L) {
+  const Shape s = shape_of(h->cfg, v.lb);
+  if (ws_bytes < fwd_bytes(s))
+    return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
+  Cands cd;
+  char* p = carve_cands(s, ws, cd);
+  cd.rq.Q = query;
+  cd.rq.K = subkeys;
+  cd.rq.d_h = s.d_h;
+  cd.rq.qk_dt = s.qk_dt;
+  cudaError_t e = select_tc_supported(s) ? launch_select_tc(s, query, subkeys, cd, p, st, L)
+                                         : launch_select_simt(s, query, subkeys, (float*)p, cd, st, L);
+  if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half candidates)");
+  if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);
+  RouteArgs ra;
+  ra.P = v.P;
+  ra.rank = v.rank;
+  ra.rpr = v.rpr;
   for (int o = 0; o < v.P; ++o) {
     if (v.staged) {  // OUT segment [o] of this rank
-      a.row.p[o] = v.own<int32_t>(MSN_XREG_OUT_ROW) + o * v.cap;
-      a.w.p[o] = v.own<float>(MSN_XREG_OUT_W) + o * v.cap;
-      a.q.p[o] = v.own<int32_t>(MSN_XREG_OUT_Q) + o * v.cap;
-      a.off.p[o] = v.own<int32_t>(MSN_XREG_OUT_OFF) + o * (v.lb + 1);
+      ra.row.p[o] = v.own<int32_t>(MSN_XREG_OUT_ROW) + o * v.cap;
+      ra.w.p[o] = v.own<float>(MSN_XREG_OUT_W) + o * v.cap;
+      ra.cnt.p[o] = v.own<int32_t>(MSN_XREG_OUT_CNT) + o * v.lb;
     } else {  // owner o's IN segment [rank], over NVLink
-      a.row.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_ROW) + v.rank * v.cap;
-      a.w.p[o] = v.reg<float>(o, MSN_XREG_IN_W) + v.rank * v.cap;
-      a.q.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_Q) + v.rank * v.cap;
-      a.off.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_OFF) + v.rank * (v.lb + 1);
+      ra.row.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_ROW) + v.rank * v.cap;
+      ra.w.p[o] = v.reg<float>(o, MSN_XREG_IN_W) + v.rank * v.cap;
+      ra.cnt.p[o] = v.reg<int32_t>(o, MSN_XREG_IN_CNT) + v.rank * v.lb;
     }
   }
-  a.pos = v.own<int32_t>(MSN_XREG_POS);
-  a.counts = v.own<int32_t>(MSN_XREG_CTL) + 32;
-  a.cnt = v.own<int32_t>(MSN_XREG_SCRATCH);
-  a.qoff = a.cnt + v.P * (v.lb + 1);
-  return launch_route(shape_of(h->cfg, v.lb), idx, w, a, st, L);
+  ra.pos = v.own<int32_t>(MSN_XREG_POS);
+  const int64_t dv = h->cfg.d_value;
+  ra.part = v.P == 1 ? out  // nothing to combine
+                     : v.own<float>(v.staged ? MSN_XREG_PART_OUT : MSN_XREG_PART_IN) + v.rank * v.lb * dv;
+  e = launch_cartesian_route(s, cd, idx, w, values, ra, st, L);
+  if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax + route + local gather");
+  if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);
+  return MSN_OK;
 }
 
 cudaError_t x_gather(msn_pkm_t h, const XView& v, const void* values, cudaStream_t st, int* L) {
@@ -699,6 +718,7 @@ cudaError_t x_gather(msn_pkm_t h, const XView& v, const void* values, cudaStream
 }
 
 cudaError_t x_combine(msn_pkm_t h, const XView& v, float* out, cudaStream_t st, int* L) {
+  if (v.P == 1) return cudaSuccess;  // SELECT wrote out
   return launch_reduce_partials(v.own<float>(MSN_XREG_PART_IN), v.P, v.lb, 1, h->cfg.d_value, out, st, L);
 }
 
@@ -714,7 +734,7 @@ cudaError_t x_scatter(msn_pkm_t h, const XView& v, const void* values, float* d_
   for (int p = 0; p < v.P; ++p) {
     xs.p[p] = v.staged ? v.own<float>(MSN_XREG_DOUT_ALL) + p * v.lb * dv : v.reg<float>(p, MSN_XREG_DOUT);
     dd.p[p] = v.staged ? v.own<float>(MSN_XREG_DW_OUT) + p * v.cap
-                       : v.reg<float>(p, MSN_XREG_DW_IN) + v.rank * v.cap;
+                       : v.reg<float>(p, MSN_XREG_DW_IN) + v.rank * v.cap;  // window order
   }
   const Shape s = shape_of(h->cfg, v.lb);
   const BwdWorkspace bw = carve_bwd_workspace(s, v.P * v.lb, ws);
@@ -763,19 +783,24 @@ msn_status msn_pkm_exchange_layout(msn_pkm_t h, int64_t local_batch, int32_t sta
     if (e_ != cudaSuccess) return cuda_fail(e_, what);         \
   } while (0)
 
-msn_status msn_pkm_exchange_route(msn_pkm_t h, void* stream, const int32_t* idx, const float* weights,
-                                  const msn_pkm_exchange* x) {
+msn_status msn_pkm_exchange_select(msn_pkm_t h, void* stream, const void* query, const void* subkeys,
+                                   const void* values, const msn_pkm_exchange* x, int32_t* idx, float* weights,
+                                   float* out, void* workspace, size_t workspace_bytes) {
   msn_status st = check_handle(h);
   if (st) return st;
   h->last_launches = 0;
   XView v;
   if ((st = make_view(h, x, v))) return st;
   if (v.lb == 0) return MSN_OK;
+  REQUIRE_PTR(query);
+  REQUIRE_PTR(subkeys);
+  REQUIRE_PTR(values);
   REQUIRE_PTR(idx);
   REQUIRE_PTR(weights);
-  if ((st = check_tape(h, stream, v.lb, idx, weights))) return st;
-  XCALL(x_route(h, v, idx, weights, (cudaStream_t)stream, &h->last_launches), "exchange route");
-  return MSN_OK;
+  REQUIRE_PTR(workspace);
+  if (v.P == 1) REQUIRE_PTR(out);
+  return x_select(h, v, query, subkeys, values, idx, weights, out, workspace, workspace_bytes,
+                  (cudaStream_t)stream, &h->last_launches);
 }
 
 msn_status msn_pkm_exchange_gather(msn_pkm_t h, void* stream, const void* values, const msn_pkm_exchange* x) {
@@ -869,9 +894,9 @@ msn_status msn_pkm_forward_sharded(msn_pkm_t h, void* stream, int64_t local_batc
   cudaStream_t cs = (cudaStream_t)stream;
   int* L = &h->last_launches;
   // every rank takes part in every barrier, also with no local queries
-  if (v.lb > 0 && (st = do_select(h, cs, v.lb, query, subkeys, idx, weights, workspace, workspace_bytes, L)))
+  if (v.lb > 0 &&
+      (st = x_select(h, v, query, subkeys, values, idx, weights, out, workspace, workspace_bytes, cs, L)))
     return st;
-  if (v.lb > 0) XCALL(x_route(h, v, idx, weights, cs, L), "exchange route");
   XCALL(x_barrier(v, cs, L), "exchange barrier");
   if (v.lb > 0) XCALL(x_gather(h, v, values, cs, L), "exchange gather");
   XCALL(x_barrier(v, cs, L), "exchange barrier");

@@ -215,12 +215,6 @@ struct GrpArgs {
   PerRank<float> pd{};
   uint32_t xl = 0, dl = 0;
   FastDiv div_xl, div_dl;
-  // exchanged records (a9, MODE_DV): record j = s * cap + i of source s; its
-  // x row is s * xq_lb + xq[j] (the query in the source's batch); null: the
-  // record id encodes the query (cid = (b H + h) k + t)
-  const int32_t* xq = nullptr;
-  uint32_t xq_lb = 0;
-  FastDiv div_cap;
 };
 
 // Applies the fused update to VW consecutive elements at element offset off
@@ -334,7 +328,6 @@ __device__ __forceinline__ void stg_vec(float* p, const float* v) {
 template <int MODE>
 __device__ __forceinline__ uint32_t grp_xrow(const GrpArgs& a, uint32_t rec) {
   if constexpr (MODE == MODE_DV) {
-    if (a.xq) return a.div_cap.div(rec) * a.xq_lb + (uint32_t)a.xq[rec];
     if (a.og == 1) return a.div_hk.div(rec);
     const uint32_t bh = a.div_k.div(rec);  // b * H + h
     const uint32_t b = a.div_h.div(bh);
@@ -835,11 +828,7 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
     a.div_dl = FastDiv(a.dl);
     if (!peers->p2p) a.xl = 0;  // (staged records: local X / dots)
   }
-  if (peers && peers->xq) {
-    a.xq = peers->xq;
-    a.xq_lb = (uint32_t)peers->local_batch;
-    a.div_cap = FastDiv((uint32_t)peers->cap);
-  }
+
   switch (D / 32) {
     case 1: return grp_reduce_t<MODE, XT, YT, 1>(a, n, nrows, st, launches, tr);
     case 2: return grp_reduce_t<MODE, XT, YT, 2>(a, n, nrows, st, launches, tr);
@@ -1183,21 +1172,22 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
 }
 
 namespace {
-// Keys of exchanged records (a9): record j = s * cap + i of source s is valid
-// iff i < off[s][lb] (the segment's count); key = its local row.
-__global__ void rec_keys_kernel(const int32_t* __restrict__ row, const int32_t* __restrict__ off, int64_t lb,
-                                FastDiv div_cap, uint32_t cap, int64_t n, uint32_t sentinel,
-                                uint32_t* __restrict__ keys, uint32_t* __restrict__ cnt,
-                                uint32_t* __restrict__ rank) {
+// Keys of exchanged records (a9): record j = s * cap + b * HK + i (window
+// (s, b), cap = lb * HK) is valid iff i < cnt[s * lb + b]; key = its local
+// row.  The record id orders the contributions globally: source s's query b
+// is the global query s * lb + b, so j / HK is the d_out row (as the cid of
+// the unsharded path) and ascending j is ascending (query, h, t).
+__global__ void rec_keys_kernel(const int32_t* __restrict__ row, const int32_t* __restrict__ cnt, FastDiv div_hk,
+                                uint32_t HK, int64_t n, uint32_t sentinel, uint32_t* __restrict__ keys,
+                                uint32_t* __restrict__ gcnt, uint32_t* __restrict__ rank) {
   pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const uint32_t sr = div_cap.div((uint32_t)p);
-  const uint32_t i = (uint32_t)p - sr * cap;
-  const bool valid = (int64_t)i < (int64_t)off[(int64_t)sr * (lb + 1) + lb];
+  const uint32_t win = div_hk.div((uint32_t)p);  // s * lb + b
+  const bool valid = (uint32_t)p - win * HK < (uint32_t)cnt[win];
   const uint32_t key = valid ? (uint32_t)row[p] : sentinel;
   keys[p] = key;
-  if (valid) rank[p] = atomicAdd(&cnt[key], 1u);
+  if (valid) rank[p] = atomicAdd(&gcnt[key], 1u);
 }
 }  // namespace
 
@@ -1213,8 +1203,8 @@ cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const Per
   const GrpScratch g = grp_scratch(ws);
   cudaError_t e = grp_begin(g, nrows, st);
   if (e != cudaSuccess) return e;
-  launch_pdl(rec_keys_kernel, (unsigned)((n + 255) / 256), 256, 0, st, r.row, r.off, r.lb,
-             FastDiv((uint32_t)r.cap), (uint32_t)r.cap, n, nrows, g.keys, g.cnt, g.rank);
+  launch_pdl(rec_keys_kernel, (unsigned)((n + 255) / 256), 256, 0, st, r.row, r.cnt, FastDiv((uint32_t)r.HK),
+             (uint32_t)r.HK, n, nrows, g.keys, g.cnt, g.rank);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
@@ -1225,7 +1215,6 @@ cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const Per
   peers.dw = dw_dst;
   peers.local_batch = r.lb;
   peers.p2p = true;
-  peers.xq = r.q;
   peers.cap = r.cap;
   if (s.v_dt == F32)
     return grp_finish<MODE_DV, float, float>(g, n, nrows, r.w, nullptr, V, nullptr, dV, s.H, s.k, s.d_v, st,

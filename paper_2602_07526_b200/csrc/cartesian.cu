@@ -355,6 +355,121 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   }  // output groups
 }
 
+// a3 + a4 + ROUTE + the local shard's a5 (the row-sharded table, a9): one
+// warp per local query runs the Cartesian stage of its H lookups (the tape
+// idx / w), then turns its H k slots into records {local row, w} in their
+// owners' windows for this query (in (h, t) order: the position of slot r is
+// the number of earlier slots with the same owner), writes the per-owner
+// counts and every slot's position, and gathers the slots this rank owns
+// into its own partial row -- the same rows, order and arithmetic as the
+// owner-side gather of a remote window.  With peer memory the record stores
+// cross NVLink as they are issued.
+struct OwnerDiv {
+  FastDiv div;
+  uint32_t rpr;
+};
+template <int KMAX, int MAXC, int SEG, typename VT, int VPL, int G, int U>
+__global__ void __launch_bounds__(256) cartesian_route_kernel(
+    const uint2* __restrict__ cand, const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
+    int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V, int d_v, int SC, RouteArgs ra,
+    OwnerDiv od) {
+  pdl_enter();
+  constexpr int PER = elem<VT>::per16;
+  constexpr int LG = 32 / G;
+  __shared__ CartSmem<KMAX, MAXC> sm[kWarpsPerBlock];
+  __shared__ int32_t s_idx[kWarpsPerBlock][kMaxHK];
+  __shared__ float s_w[kWarpsPerBlock][kMaxHK];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
+  if (b >= B) return;
+  for (int h = 0; h < H; ++h)
+    cartesian_lookup<KMAX, MAXC, 0, SEG>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w, &s_idx[wid][h * k],
+                                         &s_w[wid][h * k], 0, SC);
+  const int HK = H * k;
+  const int P = ra.P;
+  int base = 0;  // lane o < P: the records of owner o so far in this query's window
+  for (int r0 = 0; r0 < HK; r0 += 32) {
+    const int r = r0 + lane;
+    int o = -1;
+    int32_t row = 0;
+    float wt = 0.f;
+    if (r < HK) {
+      const uint32_t f = (uint32_t)s_idx[wid][r];
+      const uint32_t q = od.div.div(f);
+      o = (int)q;
+      row = (int32_t)(f - q * od.rpr);
+      wt = s_w[wid][r];
+    }
+    int my = 0, add = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q) {
+      if (q < P) {
+        const unsigned m = __ballot_sync(0xffffffffu, o == q);
+        const int bq = __shfl_sync(0xffffffffu, base, q);
+        if (o == q) my = bq + __popc(m & ((1u << lane) - 1u));
+        if (lane == q) add = __popc(m);
+      }
+    }
+    base += add;
+    if (r < HK) {
+      int32_t* prow = nullptr;
+      float* pw = nullptr;
+#pragma unroll
+      for (int q = 0; q < kMaxWorld; ++q)
+        if (q == o) {
+          prow = ra.row.p[q];
+          pw = ra.w.p[q];
+        }
+      prow[b * HK + my] = row;
+      pw[b * HK + my] = wt;
+      ra.pos[b * HK + r] = my;
+      s_idx[wid][r] = o == ra.rank ? row : -1;  // the local shard's rows, in place
+    }
+  }
+  if (lane < P) {
+    int32_t* pc = nullptr;
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q)
+      if (q == lane) pc = ra.cnt.p[q];
+    pc[b] = base;
+  }
+  __syncwarp();
+  // the local shard's rows: masked slots (-1) load nothing and add 0
+  float acc[VPL][PER];
+  gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], 0, HK, V, d_v, acc);
+  const int g = lane / LG, gl = lane % LG;
+  if (g == 0) {
+    float* o = ra.part + b * d_v;
+    const int row_vecs = d_v / PER;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int vec = gl * VPL + v;
+      if (vec < row_vecs) {
+#pragma unroll
+        for (int e = 0; e < PER; e += 4)
+          *reinterpret_cast<float4*>(o + vec * PER + e) =
+              make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
+      }
+    }
+  }
+}
+
+template <int KMAX, int MAXC, int SEG, typename VT>
+cudaError_t dispatch_route(const Shape& s, const Cands& cd, int32_t* idx, float* w, const VT* V,
+                           const RouteArgs& ra, cudaStream_t st) {
+  const int R = s.d_v * (int)sizeof(VT) / 16;
+  const unsigned blocks = (unsigned)((s.B + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  OwnerDiv od;
+  od.div = FastDiv((uint32_t)ra.rpr);
+  od.rpr = (uint32_t)ra.rpr;
+#define ROUTE(VPL, G, U)                                                                             \
+  launch_pdl(cartesian_route_kernel<KMAX, MAXC, SEG, VT, VPL, G, U>, blocks, 256, 0, st, cd.vc, cd.n, s.B, s.H, \
+             s.n_sub, s.k, idx, w, V, s.d_v, cd.SC, ra, od)
+  MSN_GATHER_DISPATCH(R, ROUTE);
+#undef ROUTE
+  return cudaGetLastError();
+}
+
 template <int KMAX, int MAXC, typename VT>
 cudaError_t dispatch_fused(const Shape& s, const Cands& cd, int32_t* idx, float* w, const VT* V,
                            float* out, cudaStream_t st, const Gate& gate) {
@@ -382,6 +497,27 @@ cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* id
     e = s.v_dt == F32 ? dispatch_fused<64, 280, float>(s, cd, idx, w, (const float*)V, out, st, gate)
                       : dispatch_fused<64, 280, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st, gate);
   }
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+cudaError_t launch_cartesian_route(const Shape& s, const Cands& cd, int32_t* idx, float* w, const void* V,
+                                   const RouteArgs& ra, cudaStream_t st, int* launches) {
+  if (s.H * s.k > kMaxHK || s.og != 1 || s.tab_stride || ra.P < 1 || ra.P > kMaxWorld) return cudaErrorNotSupported;
+  if (s.B == 0) return cudaSuccess;
+  const bool bf = s.v_dt != F32;
+  cudaError_t e;
+  if (s.k <= 32 && cd.S == 2)
+    e = bf ? dispatch_route<32, 119, 2, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, ra, st)
+           : dispatch_route<32, 119, 2, float>(s, cd, idx, w, (const float*)V, ra, st);
+  else if (cd.S != 1)
+    return cudaErrorNotSupported;
+  else if (s.k <= 32)
+    e = bf ? dispatch_route<32, 119, 1, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, ra, st)
+           : dispatch_route<32, 119, 1, float>(s, cd, idx, w, (const float*)V, ra, st);
+  else
+    e = bf ? dispatch_route<64, 280, 1, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, ra, st)
+           : dispatch_route<64, 280, 1, float>(s, cd, idx, w, (const float*)V, ra, st);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

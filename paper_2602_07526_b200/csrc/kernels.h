@@ -153,9 +153,7 @@ struct ScatterPeers {
   PerRank<float> dw{};           // rank p's dw destination (pre-offset)
   int64_t local_batch = 0;
   bool p2p = true;               // false: x rows / dw in the local X / dots arrays
-  // exchanged records (a9): record j = s * cap + i, query xq[j] of source s
-  const int32_t* xq = nullptr;
-  int64_t cap = 0;
+  int64_t cap = 0;               // dw destination segment per rank (0: local_batch H k)
 };
 
 // a6 deterministic: group (idx -> cid) by row, then fused row-major dV += / dw.
@@ -179,36 +177,41 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
                                  int* launches);
 
 // ---- a9 record exchange of the row-sharded table (exchange.cu) ----
+// a2-a4 + ROUTE + the local shard's a5, fused (cartesian.cu): one warp per
+// local query runs the Cartesian stage of its H lookups (idx / w, the tape),
+// writes every slot as a record {local row, w} into its owner's window
+// row.p[o] / w.p[o] + b H k (in (h, t) order; cnt.p[o][b] = the count,
+// pos[b H k + r] = the slot's place in the window) and gathers the slots this
+// rank owns into part + b d_v.
 struct RouteArgs {
-  int P;                    // world
-  int64_t lb;               // local batch B_l
-  int64_t rpr;              // value rows per rank (n / P)
-  PerRank<int32_t> row, q;  // destination of owner o's records (pre-offset: segment start)
-  PerRank<float> w;
-  PerRank<int32_t> off;     // destination of owner o's per-query offsets [B_l + 1]
-  int32_t* pos;             // [B_l * H * k]
-  int32_t* counts;          // [P] records for owner o
-  int32_t* cnt;             // scratch [P][B_l + 1]
-  int32_t* qoff;            // scratch [P][B_l + 1]
+  int P = 1, rank = 0;
+  int64_t rpr = 0;          // value rows per rank (n / P)
+  PerRank<int32_t> row{}, cnt{};
+  PerRank<float> w{};
+  int32_t* pos = nullptr;   // [B_l * H * k]
+  float* part = nullptr;    // [B_l, d_v] the local shard's partial sums
 };
-cudaError_t launch_route(const Shape& s, const int32_t* idx, const float* w, const RouteArgs& a,
-                         cudaStream_t st, int* launches);
+cudaError_t launch_cartesian_route(const Shape& s, const Cands& cd, int32_t* idx, float* w, const void* V,
+                                   const RouteArgs& r, cudaStream_t st, int* launches);
+// The owner's view of the records it received: window (s, b) holds
+// cnt[s * lb + b] records at s * cap + b * HK (cap = lb * HK).
 struct RecordsIn {
-  int P;
-  int64_t lb, cap;
-  const int32_t *row, *q, *off;  // [P][cap], [P][cap], [P][B_l + 1]
-  const float* w;                // [P][cap]
+  int P = 1, rank = 0;
+  int64_t lb = 0, cap = 0;
+  int HK = 0;
+  const int32_t *row = nullptr, *cnt = nullptr;
+  const float* w = nullptr;
 };
-// partial of source s's query b -> dst.p[s] + b * d_v (pre-offset per source)
+// partial of remote source s's query b -> dst.p[s] + b * d_v (pre-offset per source)
 cudaError_t launch_gather_records(const Shape& s, const RecordsIn& r, const void* V,
                                   const PerRank<float>& dst, cudaStream_t st, int* launches);
 // dV (+=) and dw of the records; d_out row of (s, b) at x_src.p[s] + b * d_v,
-// dw of record (s, i) -> dw_dst.p[s] + i.
+// dw of the record at window position i of source s -> dw_dst.p[s] + i.
 cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const PerRank<const float>& x_src,
                                    const void* V, float* dV, const PerRank<float>& dw_dst,
                                    const BwdWorkspace& ws, cudaStream_t st, int* launches,
                                    const TraceEvents& tr);
-// dw[b,h,t] = dw_in[owner * cap + pos[b,h,t]]
+// dw[b,h,t] = dw_in[owner * cap + b * H * k + pos[b,h,t]]
 cudaError_t launch_collect_dw(const Shape& s, const int32_t* idx, const int32_t* pos, const float* dw_in,
                               int64_t cap, int64_t rpr, float* dw, cudaStream_t st, int* launches);
 // device barrier: flags.p[o] = rank o's CTL flag array, ctl = own CTL words

@@ -5,10 +5,11 @@ exchange (msn_pkm_exchange_* / msn_pkm_forward_sharded, include/msn_pkm.h).
 Rank p of P holds value rows [p n/P, (p+1) n/P) and its own B_l queries; the
 sub-keys are replicated (they are small).  One step:
 
-  forward   select (a1-a4, local queries)                 -> idx, w [B_l,H,k]
-            ROUTE: one 12-B record {row, w, b} per slot to its owner
-            GATHER: per (source, query) partial sums       -> back to the home
-            COMBINE: the P partials added in owner order   -> out [B_l, d_v]
+  forward   SELECT: a1-a4 of the local queries (idx, w [B_l,H,k]) fused with
+            the ROUTE (one 8-B record {row, w} per slot into its owner's
+            window for this query) and the local shard's gather
+            GATHER: per (remote source, query) partial sums -> back to the home
+            COMBINE: the P partials added in owner order    -> out [B_l, d_v]
   backward  owners read the d_out rows of their records, SCATTER (dV shard +=,
             dw per record, deterministic grouped reduction), return dw;
             COLLECT puts dw in (b,h,t) order; backward_keys on the local
@@ -25,12 +26,11 @@ graph capturable.  With world size 1 the buffer is a plain device tensor (the
 same code path, nothing leaves the GPU).
 
 transport="nccl": the same kernels with the STAGED layout; the data moves
-with torch.distributed collectives (NCCL over NVLink on the GPU box): the
-record counts by all_to_all_single (one host read of P counts: the sizes of
-the variable all-to-all), the records and the returned dw by batched
-send/recv of exactly the counted records, the per-query offsets and the
-partials by all_to_all_single, d_out by all_gather.  This is the baseline the
-peer transport is measured against (and the host logic the gloo tests cover).
+with fixed-size torch.distributed collectives (NCCL over NVLink on the GPU
+box; no host synchronisation): all_to_all_single of the record windows,
+counts, partials and returned dw, all_gather of d_out.  Whole windows move
+(P x B_l H k records per rank): the baseline the peer transport is measured
+against (and the host logic the gloo tests cover).
 """
 from __future__ import annotations
 
@@ -41,11 +41,10 @@ import torch.distributed as dist
 
 from . import _lib
 
-_DT = {"IN_ROW": torch.int32, "IN_W": torch.float32, "IN_Q": torch.int32, "IN_OFF": torch.int32,
-       "PART_IN": torch.float32, "DOUT": torch.float32, "DW_IN": torch.float32, "POS": torch.int32,
-       "CTL": torch.int32, "SCRATCH": torch.int32, "OUT_ROW": torch.int32, "OUT_W": torch.float32,
-       "OUT_Q": torch.int32, "OUT_OFF": torch.int32, "PART_OUT": torch.float32, "DOUT_ALL": torch.float32,
-       "DW_OUT": torch.float32}
+_DT = {"IN_ROW": torch.int32, "IN_W": torch.float32, "IN_CNT": torch.int32, "PART_IN": torch.float32,
+       "DOUT": torch.float32, "DW_IN": torch.float32, "POS": torch.int32, "CTL": torch.int32,
+       "OUT_ROW": torch.int32, "OUT_W": torch.float32, "OUT_CNT": torch.int32, "PART_OUT": torch.float32,
+       "DOUT_ALL": torch.float32, "DW_OUT": torch.float32}
 
 
 class ExchangeBuffer:
@@ -95,13 +94,10 @@ class ExchangeBuffer:
 
     # typed views
     def records(self, out: bool):
+        """(row, w, cnt) views: [P, B_l * H * k] windows and [P, B_l] counts."""
         P, cap = self.world, self.cap
         pre = "OUT_" if out else "IN_"
-        return (self.region(pre + "ROW", P, cap), self.region(pre + "W", P, cap), self.region(pre + "Q", P, cap),
-                self.region(pre + "OFF", P, self.lb + 1))
-
-    def counts(self) -> torch.Tensor:
-        return self.region("CTL", 64)[32:32 + self.world]
+        return (self.region(pre + "ROW", P, cap), self.region(pre + "W", P, cap), self.region(pre + "CNT", P, self.lb))
 
 
 class ShardedPKM:
@@ -148,15 +144,12 @@ class ShardedPKM:
         if self.transport == "peer":
             out, idx, w = self.ph.forward_sharded(query, subkeys, value_shard, x, out=out, ws=self.ws)
             return out, (idx, w)
-        idx, w = self.ph.select(query, subkeys)
-        self.ph.exchange_route(idx, w, x)
-        sc, rc = self._counts()
-        self._move_records(sc, rc)
+        idx, w, out = self.ph.exchange_select(query, subkeys, value_shard, x, out=out, ws=self.ws)
+        self._move_records()
         self.ph.exchange_gather(value_shard, x)
         P, lb, dv = self.world, self.local_batch, self.d_value
-        self._a2a_fixed(self.xb.region("PART_IN", P * lb * dv), self.xb.region("PART_OUT", P * lb * dv))
+        self._a2a(self.xb.region("PART_IN", P * lb * dv), self.xb.region("PART_OUT", P * lb * dv))
         out = self.ph.exchange_combine(x, out)
-        self._rc, self._sc = rc, sc
         return out, (idx, w)
 
     # ----------------------------------------------------------- backward
@@ -182,54 +175,22 @@ class ShardedPKM:
         else:
             dall.copy_(d_out)
         self.ph.exchange_scatter(value_shard, d_value_shard, x, ws=self.ws)
-        self._move_dw(self._sc, self._rc)
+        P, cap = self.world, self.xb.cap
+        self._a2a(self.xb.region("DW_IN", P * cap), self.xb.region("DW_OUT", P * cap))
         dw = self.ph.exchange_collect(idx, x)
         dq, d_subkeys = self.ph.backward_keys(query, subkeys, idx, w, dw, d_subkeys)
         return dq, d_subkeys, d_value_shard, dw
 
     # ------------------------------------------- the NCCL (staged) moves
-    def _counts(self):
-        """Records this rank sends to each owner (sc) and receives from each
-        source (rc): one all_to_all_single of P counts and ONE host read."""
-        sc_d = self.xb.counts().clone()
-        rc_d = torch.empty_like(sc_d)
-        if self.world > 1:
-            dist.all_to_all_single(rc_d, sc_d, group=self.group)
-        else:
-            rc_d.copy_(sc_d)
-        both = torch.cat([sc_d, rc_d]).cpu().tolist()  # the documented host sync of this transport
-        return both[:self.world], both[self.world:]
-
-    def _a2a_fixed(self, out: torch.Tensor, inp: torch.Tensor):
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
+        """Fixed-size all-to-all: chunk p of inp -> rank p's chunk [rank] of out."""
         if self.world > 1:
             dist.all_to_all_single(out, inp, group=self.group)
         else:
             out.copy_(inp)
 
-    def _sendrecv(self, sends, recvs):
-        """sends[p] / recvs[p]: contiguous tensors to / from rank p (self: a copy)."""
-        ops = []
-        for p in range(self.world):
-            if p == self.rank:
-                recvs[p].copy_(sends[p])
-                continue
-            if sends[p].numel():
-                ops.append(dist.P2POp(dist.isend, sends[p], p, self.group))
-            if recvs[p].numel():
-                ops.append(dist.P2POp(dist.irecv, recvs[p], p, self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-
-    def _move_records(self, sc, rc):
-        o_row, o_w, o_q, o_off = self.xb.records(out=True)
-        i_row, i_w, i_q, i_off = self.xb.records(out=False)
-        for o, i in ((o_row, i_row), (o_w, i_w), (o_q, i_q)):
-            self._sendrecv([o[p, :sc[p]] for p in range(self.world)], [i[p, :rc[p]] for p in range(self.world)])
-        self._a2a_fixed(i_off.view(-1), o_off.view(-1))
-
-    def _move_dw(self, sc, rc):
-        P, cap = self.world, self.xb.cap
-        d_out = self.xb.region("DW_OUT", P, cap)   # owner side: dw for home s, rc[s] records
-        d_in = self.xb.region("DW_IN", P, cap)     # home side: dw from owner o, sc[o] records
-        self._sendrecv([d_out[p, :rc[p]] for p in range(P)], [d_in[p, :sc[p]] for p in range(P)])
+    def _move_records(self):
+        o_row, o_w, o_cnt = self.xb.records(out=True)
+        i_row, i_w, i_cnt = self.xb.records(out=False)
+        for o, i in ((o_row, i_row), (o_w, i_w), (o_cnt, i_cnt)):
+            self._a2a(i.view(-1), o.view(-1))

@@ -353,13 +353,26 @@ class PKMLookup:
                                                      _ptr(ws), ws.numel()))
         return d_query, d_subkeys, d_values, dw
 
-    def exchange_route(self, idx, w, xchg):
-        _lib.check(self.lib.msn_pkm_exchange_route(self._h, _stream(), _ptr(idx), _ptr(w), ctypes.byref(xchg)))
+    def exchange_select(self, query, subkeys, values, xchg, out=None, ws=None):
+        """a1-a4 fused with the route and the local shard's gather: (idx, w) and,
+        with P = 1, out."""
+        B = query.shape[0]
+        idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        if out is None and xchg.world == 1:
+            out = torch.empty((B, self.d_value), dtype=torch.float32, device=self.device)
+        if ws is None:
+            ws = self.workspace(B, xchg.world * B)
+        _lib.check(self.lib.msn_pkm_exchange_select(self._h, _stream(), _ptr(query), _ptr(subkeys), _ptr(values),
+                                                    ctypes.byref(xchg), _ptr(idx), _ptr(w), _ptr(out),
+                                                    _ptr(ws), ws.numel()))
+        return idx, w, out
 
     def exchange_gather(self, values, xchg):
         _lib.check(self.lib.msn_pkm_exchange_gather(self._h, _stream(), _ptr(values), ctypes.byref(xchg)))
 
     def exchange_combine(self, xchg, out=None):
+        """out = sum of the P partials (P = 1: out is what exchange_select wrote)."""
         if out is None:
             out = torch.empty((xchg.local_batch, self.d_value), dtype=torch.float32, device=self.device)
         _lib.check(self.lib.msn_pkm_exchange_combine(self._h, _stream(), ctypes.byref(xchg), _ptr(out)))

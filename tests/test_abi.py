@@ -113,16 +113,18 @@ def test_sharded_config_and_exchange_checks(lib):
     assert list(offs) == sorted(offs) and all(o % 256 == 0 for o in offs) and nb.value >= offs[-1]
     peer = ctypes.c_size_t()
     assert lib.msn_pkm_exchange_layout(h, 16, 0, None, ctypes.byref(peer)) == 0 and peer.value < nb.value
-    # IN_ROW holds P * cap int32 records, cap = B_l * H * k
+    # IN_ROW holds P * cap int32 records, cap = B_l * H * k (one window of H * k per query)
     assert offs[1] - offs[0] >= 4 * 4 * 16 * 2 * 8
     p = ctypes.c_void_p(0x100000)
     good = _x(_lib, 4, 1, 16, 0, [0x100000, 0x200000, 0x300000, 0x400000])
-    assert lib.msn_pkm_exchange_route(h, None, None, None, ctypes.byref(good)) == 1     # null idx
+    assert lib.msn_pkm_exchange_select(h, None, None, None, None, ctypes.byref(good), None, None, None,
+                                       None, 0) == 1     # null query
     for bad in (_x(_lib, 2, 1, 16, 0, [0x100000] * 2), _x(_lib, 4, 0, 16, 0, [0x100000] * 4),
                 _x(_lib, 4, 1, 17, 0, [0x100000] * 4), _x(_lib, 4, 1, 16, 5, [0x100000] * 4),
                 _x(_lib, 4, 1, 16, 0, [0x100000, 0x100010, 0x100000, 0x100000]),
                 _x(_lib, 4, 1, 16, 0, [0x100000, 0, 0x100000, 0x100000])):
-        assert lib.msn_pkm_exchange_route(h, None, p, p, ctypes.byref(bad)) == 1, lib.msn_pkm_last_error()
+        assert lib.msn_pkm_exchange_select(h, None, p, p, p, ctypes.byref(bad), p, p, p, p,
+                                           1 << 30) == 1, lib.msn_pkm_last_error()
     # staged: only base[rank] is needed; forward_sharded needs the peer transport
     st = _x(_lib, 4, 1, 16, 1, [0, 0x100000, 0, 0])
     assert lib.msn_pkm_forward_sharded(h, None, 16, p, p, p, ctypes.byref(st), p, p, p, p, 1 << 30) == 1

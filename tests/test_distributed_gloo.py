@@ -1,8 +1,7 @@
 """World-size-2/4 gloo tests (CPU) of the row-sharded table's host plumbing
-(paper_2602_07526_b200/distributed.py, transport "nccl"): the counts
-exchange, the counted send/recv of the records and of the returned dw, the
-fixed-size all-to-alls of the per-query offsets and the partials, the
-all-gather of d_out, shard ranges.  The exchange buffer and its region layout
+(paper_2602_07526_b200/distributed.py, transport "nccl"): the fixed-size
+all-to-alls of the record windows and counts, of the partials and of the
+returned dw, the all-gather of d_out, shard ranges.  The exchange buffer and its region layout
 are the library's (msn_pkm_exchange_layout, a host function); the data-path
 kernels are stood in for by a CPU implementation of the phases' documented
 semantics (include/msn_pkm.h, "the row-sharded table with the library's record
@@ -43,61 +42,69 @@ class OraclePhases:
     def workspace(self, B, gb=None):
         return torch.empty(1, dtype=torch.uint8)
 
-    def select(self, q, K):
+    def exchange_select(self, q, K, Vs, x, out=None, ws=None):
+        """a1-a4 (oracle), then the route into the OUT windows (records of query b
+        for owner o at [b H k, b H k + cnt) in (h, t) order) and the local
+        shard's partial into PART_OUT[rank]."""
         o = orc.forward(q, K, np.zeros((self.n_sub * self.n_sub, 4), np.float32), self.k)
-        return torch.from_numpy(o["idx"].astype(np.int32)), torch.from_numpy(o["w"]).float()
-
-    def exchange_route(self, idx, w, x):
-        P, lb, cap = self.P, self.lb, self.xb.cap
-        o_row, o_w, o_q, o_off = self.xb.records(out=True)
-        pos = self.xb.region("POS", cap)
-        cnt = [0] * P
-        HK = self.heads * self.k
-        for o in range(P):
-            o_off[o, 0] = 0
+        idx = torch.from_numpy(o["idx"].astype(np.int32))
+        w = torch.from_numpy(o["w"]).float()
+        P, lb, HK = self.P, self.lb, self.heads * self.k
+        o_row, o_w, o_cnt = self.xb.records(out=True)
+        pos = self.xb.region("POS", self.xb.cap)
+        part = self.xb.region("PART_OUT", P, lb, self.d_value)
         for b in range(lb):
+            cnt = [0] * P
+            acc = torch.zeros(self.d_value, dtype=torch.float64)
             for r in range(HK):
                 f = int(idx.view(lb, HK)[b, r])
-                o, row = f // self.rpr, f % self.rpr
-                o_row[o, cnt[o]], o_w[o, cnt[o]], o_q[o, cnt[o]] = row, w.view(lb, HK)[b, r], b
-                pos[b * HK + r] = cnt[o]
-                cnt[o] += 1
-            for o in range(P):
-                o_off[o, b + 1] = cnt[o]
-        self.xb.counts()[:] = torch.tensor(cnt, dtype=torch.int32)
+                ow, row = f // self.rpr, f % self.rpr
+                wt = w.view(lb, HK)[b, r]
+                o_row[ow, b * HK + cnt[ow]], o_w[ow, b * HK + cnt[ow]] = row, wt
+                pos[b * HK + r] = cnt[ow]
+                cnt[ow] += 1
+                if ow == self.rank:
+                    acc += float(wt) * Vs[row].double()
+            o_cnt[:, b] = torch.tensor(cnt, dtype=torch.int32)
+            part[self.rank, b] = acc.float()
+        return idx, w, (part[self.rank].clone() if P == 1 else None)
 
     def exchange_gather(self, Vs, x):
-        P, lb = self.P, self.lb
-        i_row, i_w, i_q, i_off = self.xb.records(out=False)
+        P, lb, HK = self.P, self.lb, self.heads * self.k
+        i_row, i_w, i_cnt = self.xb.records(out=False)
         part = self.xb.region("PART_OUT", P, lb, self.d_value)
         for s in range(P):
+            if s == self.rank:
+                continue
             for b in range(lb):
                 acc = torch.zeros(self.d_value, dtype=torch.float64)
-                for j in range(int(i_off[s, b]), int(i_off[s, b + 1])):
-                    assert int(i_q[s, j]) == b
-                    acc += float(i_w[s, j]) * Vs[int(i_row[s, j])].double()
+                for j in range(int(i_cnt[s, b])):
+                    acc += float(i_w[s, b * HK + j]) * Vs[int(i_row[s, b * HK + j])].double()
                 part[s, b] = acc.float()
 
     def exchange_combine(self, x, out=None):
         part = self.xb.region("PART_IN", self.P, self.lb, self.d_value)
-        return part.double().sum(0).float()
+        return part.double().sum(0).float() if self.P > 1 else out
 
     def exchange_scatter(self, Vs, dVs, x, ws=None):
-        P, lb = self.P, self.lb
-        i_row, i_w, i_q, i_off = self.xb.records(out=False)
+        P, lb, HK = self.P, self.lb, self.heads * self.k
+        i_row, i_w, i_cnt = self.xb.records(out=False)
         dall = self.xb.region("DOUT_ALL", P, lb, self.d_value)
         dw_out = self.xb.region("DW_OUT", P, self.xb.cap)
         for s in range(P):
-            for j in range(int(i_off[s, lb])):
-                row, d = int(i_row[s, j]), dall[s, int(i_q[s, j])]
-                dw_out[s, j] = float((Vs[row].double() * d.double()).sum())
-                dVs[row] += float(i_w[s, j]) * d
+            for b in range(lb):
+                for j in range(int(i_cnt[s, b])):
+                    row, d = int(i_row[s, b * HK + j]), dall[s, b]
+                    dw_out[s, b * HK + j] = float((Vs[row].double() * d.double()).sum())
+                    dVs[row] += float(i_w[s, b * HK + j]) * d
 
     def exchange_collect(self, idx, x, dw=None):
+        HK = self.heads * self.k
         dw_in = self.xb.region("DW_IN", self.P, self.xb.cap)
-        pos = self.xb.region("POS", self.xb.cap)
+        pos = self.xb.region("POS", self.xb.cap).long()
         f = idx.reshape(-1).long()
-        return dw_in[f // self.rpr, pos.long()].view(idx.shape).clone()
+        win = torch.arange(f.numel()) // HK * HK
+        return dw_in[f // self.rpr, win + pos].view(idx.shape).clone()
 
     def backward_keys(self, q, K, idx, w, dw, dK):
         B, H, k = idx.shape
