@@ -864,13 +864,18 @@ __global__ void dv_keys_kernel(const int32_t* __restrict__ idx, int64_t n, int64
 // t with r_t = r in t order; dQ[b,h,half] = sum_r dS_r K[h,half,r]; one dK
 // record per distinct r (first occurrence, counted for the grouping), others
 // get the sentinel key.
-// DENSE: instead of records, the dS of the lookup-half is written as one
-// dense bf16 row dSd[b, h*2 + half, 0:n_sub] (zeros elsewhere) for the
-// tensor-core dK (dk_tc.cu) and, unless DQ, the tensor-core dQ;
-// n_sub <= kDenseMax.  DQ: dQ by the warp here (the m distinct K rows of the
-// lookup-half from L2) -- cheaper than the dense GEMM when n_sub is large.
+// OUT = OUT_DENSE: instead of grouping records, the dS of the lookup-half is
+// written as one dense bf16 row dSd[b, h*2 + half, 0:n_sub] (zeros elsewhere)
+// for the tensor-core dK (dk_tc.cu) and, unless DQ, the tensor-core dQ;
+// n_sub <= kDenseMax.  OUT = OUT_COMPACT: the m distinct (sub-key, dS) pairs
+// of the lookup-half as k uint2 slots {index, dS bits} (index 0xffffffff past
+// m) from which the tensor-core dK builds its operand tiles in shared memory
+// (no dense matrix in HBM).  DQ: dQ by the warp here (the m distinct K rows
+// of the lookup-half from L2) -- cheaper than the dense GEMM when n_sub is
+// large.
 constexpr int kDenseMax = 2048;
-template <typename QT, int KPL, int EPL, bool DENSE, bool DQ>
+enum { OUT_GROUP = 0, OUT_DENSE = 1, OUT_COMPACT = 2 };
+template <typename QT, int KPL, int EPL, int OUT, bool DQ>
 __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     const int32_t* __restrict__ idx,
                                                     const float* __restrict__ w,
@@ -885,6 +890,7 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     int32_t tab_stride, bool dq_bf16) {
   pdl_enter();
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
+  constexpr bool DENSE = OUT == OUT_DENSE;
   __shared__ int32_t s_r[8][64];
   __shared__ float s_d[8][64];
   __shared__ __align__(16) uint16_t s_row[DENSE ? 8 : 1][DENSE ? kDenseMax : 8];
@@ -950,7 +956,7 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       }
     }
     // records
-    if constexpr (!DENSE) {
+    if constexpr (OUT == OUT_GROUP) {
 #pragma unroll
       for (int u = 0; u < KPL; ++u) {
         const int t = lane + 32 * u;
@@ -991,6 +997,11 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       __syncwarp();
       uint4* g4 = reinterpret_cast<uint4*>(dSd + (l * 2 + half) * (int64_t)n_sub);
       for (int c = lane; c < n16; c += 32) g4[c] = row4[c];
+    }
+    if constexpr (OUT == OUT_COMPACT) {
+      uint2* rec = reinterpret_cast<uint2*>(dSd) + (l * 2 + half) * (int64_t)k;
+      for (int c = lane; c < k; c += 32)
+        rec[c] = c < m ? make_uint2((uint32_t)s_r[wid][c], __float_as_uint(s_d[wid][c])) : make_uint2(0xffffffffu, 0u);
     }
     if constexpr (DENSE && !DQ) {
       __syncwarp();
@@ -1216,11 +1227,16 @@ cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const Per
   peers.local_batch = r.lb;
   peers.p2p = true;
   peers.cap = r.cap;
+  // one rank: the only source is this one -- the plain local reducers (x rows
+  // and dw in single arrays), the same kernels as the unsharded backward
+  const ScatterPeers* pp = r.P > 1 ? &peers : nullptr;
+  const float* X = r.P > 1 ? nullptr : x_src.p[0];
+  float* dots = r.P > 1 ? nullptr : dw_dst.p[0];
   if (s.v_dt == F32)
-    return grp_finish<MODE_DV, float, float>(g, n, nrows, r.w, nullptr, V, nullptr, dV, s.H, s.k, s.d_v, st,
-                                             launches, tr, UpdateArgs{}, 1, &peers);
-  return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, r.w, nullptr, V, nullptr, dV, s.H, s.k,
-                                                   s.d_v, st, launches, tr, UpdateArgs{}, 1, &peers);
+    return grp_finish<MODE_DV, float, float>(g, n, nrows, r.w, X, V, dots, dV, s.H, s.k, s.d_v, st,
+                                             launches, tr, UpdateArgs{}, 1, pp);
+  return grp_finish<MODE_DV, float, __nv_bfloat16>(g, n, nrows, r.w, X, V, dots, dV, s.H, s.k,
+                                                   s.d_v, st, launches, tr, UpdateArgs{}, 1, pp);
 }
 
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
@@ -1267,15 +1283,15 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   }
 #define DSDQ(QT, KPL, E_)                                                                      \
   if (dense && dq_tc)                                                                          \
-    launch_pdl(ds_dq_kernel<QT, KPL, E_, true, false>, blocks, 256, 0, st,                             \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_DENSE, false>, blocks, 256, 0, st,                        \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16);                 \
   else if (dense)                                                                              \
-    launch_pdl(ds_dq_kernel<QT, KPL, E_, true, true>, blocks, 256, 0, st,                              \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_COMPACT, true>, blocks, 256, 0, st,                       \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16);                 \
   else                                                                                         \
-    launch_pdl(ds_dq_kernel<QT, KPL, E_, false, true>, blocks, 256, 0, st,                             \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_GROUP, true>, blocks, 256, 0, st,                         \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16)
 #define DSDQ_E(QT, KPL)                                                                        \

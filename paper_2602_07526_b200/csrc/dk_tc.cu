@@ -49,6 +49,8 @@ struct DkParams {
   int64_t q_per_split;  // queries per split (multiple of kBK)
   float* out;           // partials [S][H*2][n_sub][d_h] (or dK itself when S == 1)
   int accumulate;       // 1: out += acc (S == 1, out = dK); 0: out = acc
+  const uint2* rec;     // REC: compact records [B][H*2][k] {sub-key, dS bits}
+  int k;
 };
 
 // MN-major, 128-byte-swizzled operand: atoms of 64 (M or N) elements x 8
@@ -63,7 +65,14 @@ constexpr uint32_t idesc_bf16_mn(int M, int N) {
   return idesc_bf16(M, N) | (1u << 15) | (1u << 16);
 }
 
-template <int MT>
+// REC: the A tiles (dS^T of the k-block's 64 queries over the CTA's MT x 128
+// sub-keys) are built in shared memory from the compact records of
+// ds_dq_kernel (p.rec: k slots {sub-key, dS} per (query, head, half)) by the
+// epilogue warps, which are idle until the last k-block: zero the stage,
+// named barrier, one bf16 store per record in range at its 128-byte-swizzle
+// position (the layout TMA would produce), fence.proxy.async, arrive.  No
+// dense dS matrix in HBM; TMA then loads only the Q tiles.
+template <int MT, bool REC>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     dk_gemm_kernel(const __grid_constant__ CUtensorMap tmap_ds,
                    const __grid_constant__ CUtensorMap tmap_q, const DkParams p) {
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     prefetch_tmap(&tmap_ds);
     prefetch_tmap(&tmap_q);
     for (int s = 0; s < kStg; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], REC ? 1 + 8 : 1);  // (REC: + one arrive per builder warp)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tdone, 1);
@@ -112,16 +121,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(2 * MT + nb) * kAtom;
+      const uint32_t bytes = (uint32_t)((REC ? 0 : 2 * MT) + nb) * kAtom;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % kStg;
         mbar_wait(&empty[s], ((kb / kStg) & 1) ^ 1);
         mbar_expect_tx(&full[s], bytes);
         const int b0 = (int)(q0 + (int64_t)kb * kBK);
         // queries >= B (ragged last block) are zero-filled by TMA
+        if constexpr (!REC) {
 #pragma unroll
-        for (int t = 0; t < 2 * MT; ++t)
-          tma_load_3d(sA + (s * MT * 2 + t) * kAtom, &tmap_ds, &full[s], i0 + 64 * t, hh, b0);
+          for (int t = 0; t < 2 * MT; ++t)
+            tma_load_3d(sA + (s * MT * 2 + t) * kAtom, &tmap_ds, &full[s], i0 + 64 * t, hh, b0);
+        }
         for (int j = 0; j < nb; ++j)
           tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_q, &full[s], 64 * j, hh, b0);
       }
@@ -144,7 +155,53 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
       tc_commit(tdone);
     }
-  } else if ((warp - 2) / 4 < MT) {
+  } else {
+    if constexpr (REC) {
+      // ----- A-tile builders (warps 2..9, 256 threads): thread u handles the
+      // k-block's query u / 4 and every 4th of its k record slots
+      const int u = threadIdx.x - 64;
+      const int ql = u >> 2, part = u & 3;
+      const int HH = 2 * p.H;
+      constexpr int kRecMax = 16;  // k <= 64 slots per query over 4 threads
+      const int per = (p.k + 3) / 4;
+      uint2 nxt[kRecMax];
+      auto load_kb = [&](int kb) {
+        const int64_t b = q0 + (int64_t)kb * kBK + ql;
+        const uint2* r = p.rec + (b * HH + hh) * (int64_t)p.k;
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c) {
+          const int slot = part + 4 * c;
+          nxt[c] = (c < per && slot < p.k && b < q1) ? r[slot] : make_uint2(0xffffffffu, 0u);
+        }
+      };
+      if (nkb > 0) load_kb(0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kStg;
+        uint2 cur[kRecMax];
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c) cur[c] = nxt[c];
+        if (kb + 1 < nkb) load_kb(kb + 1);  // in flight while this stage is built
+        mbar_wait(&empty[s], ((kb / kStg) & 1) ^ 1);
+        uint8_t* a = sA + s * MT * 2 * kAtom;
+        uint4* a4 = reinterpret_cast<uint4*>(a);
+        for (int i = u; i < MT * 2 * kAtom / 16; i += 256) a4[i] = make_uint4(0, 0, 0, 0);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c) {
+          const uint32_t il = cur[c].x - (uint32_t)i0;  // (sentinel and out-of-range wrap high)
+          if (il < (uint32_t)(kBM * MT)) {
+            const uint32_t e = il & 63u;
+            const uint32_t off = (il >> 6) * kAtom + ql * 128 + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) + (e & 7u) * 2;
+            const __nv_bfloat16 v = __float2bfloat16_rn(__uint_as_float(cur[c].y));
+            *reinterpret_cast<__nv_bfloat16*>(a + off) = v;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+      }
+    }
+    if ((warp - 2) / 4 < MT) {
     // ----- epilogue (warps 2..: TMEM lane quarter warp % 4, tile (warp - 2) / 4): row i0 + 128 t + row
     const int q = warp & 3;
     const int t = (warp - 2) / 4;
@@ -176,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         d4[j] = v;
       }
     }
+    }  // epilogue warps
   }
   tc_fence_before();
   __syncthreads();
@@ -390,7 +448,10 @@ size_t dk_smem_bytes(const Shape& s, int MT) {
   return 1024 + (size_t)st * (2 * MT + s.d_h / 64) * kAtom + 8 * (2 * st + 1) + 16;
 }
 
+bool dq_tc_wanted_(const Shape& s);
+// the dense bf16 dS matrix (tensor-core dQ wanted), else the compact records
 size_t dense_ds_bytes(const Shape& s) {
+  if (!dq_tc_wanted_(s)) return ((size_t)s.B * s.H * 2 * s.k * 8 + 255) & ~(size_t)255;
   return ((size_t)s.B * s.H * 2 * s.n_sub * 2 + 255) & ~(size_t)255;
 }
 
@@ -413,11 +474,14 @@ size_t dk_tc_workspace_bytes(const Shape& s) {
   return dense_ds_bytes(s) + part;
 }
 
-bool dq_tc_wanted(const Shape& s) {
+namespace {
+bool dq_tc_wanted_(const Shape& s) {
   // MSN_DQ_TC=0/1 forces the choice (A/B measurements only)
   static const int f = env_int("MSN_DQ_TC", -1);
   return f >= 0 ? f != 0 : s.n_sub < 1024;
 }
+}  // namespace
+bool dq_tc_wanted(const Shape& s) { return dq_tc_wanted_(s); }
 
 cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* dQ, float* dK,
                          void* ws, cudaStream_t st, int* launches, bool with_dq) {
@@ -487,11 +551,14 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
   const int S = splits_for(s);
   const int64_t kblocks = (s.B + kBK - 1) / kBK;
   const int64_t qps = ((kblocks + S - 1) / S) * kBK;
-  DkParams p{s.B, s.H, s.n_sub, s.d_h, qps, S > 1 ? part : dK, S > 1 ? 0 : 1};
+  DkParams p{s.B, s.H, s.n_sub, s.d_h, qps, S > 1 ? part : dK, S > 1 ? 0 : 1,
+             reinterpret_cast<const uint2*>(ws), s.k};
   const int mtk = dk_mt(s);
-  auto dkk = mtk == 2 ? dk_gemm_kernel<2> : dk_gemm_kernel<1>;
-  static std::atomic<uint64_t> attr[2];
-  cudaError_t e = smem_attr_once(attr[mtk - 1], dkk, 227 * 1024);
+  const bool rec = !with_dq;  // ds_dq_kernel wrote compact records (dQ done there)
+  auto dkk = rec ? (mtk == 2 ? dk_gemm_kernel<2, true> : dk_gemm_kernel<1, true>)
+                 : (mtk == 2 ? dk_gemm_kernel<2, false> : dk_gemm_kernel<1, false>);
+  static std::atomic<uint64_t> attr[4];
+  cudaError_t e = smem_attr_once(attr[(mtk - 1) * 2 + (rec ? 1 : 0)], dkk, 227 * 1024);
   if (e != cudaSuccess) return e;
   dim3 grid(s.n_sub / (kBM * mtk), HH, S);
   launch_pdl(dkk, grid, kThreads, dk_smem_bytes(s, mtk), st, mds, mq, p);
