@@ -422,7 +422,7 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // row sum is added to G by one vector reduction per lane (red.global.add,
 // performed in L2): the row's only update, so G = G + sum bitwise.
 template <int MODE, typename XT, typename YT, int EPL, bool UPD, bool P2P>
-__global__ void __launch_bounds__(256, (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4))) grp_reduce_short_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4)))) grp_reduce_short_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
@@ -748,7 +748,7 @@ template <int MODE, typename XT, typename YT, int EPL>
 cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream_t st,
                          int* launches, const TraceEvents& tr) {
   const int sms = num_sms();
-  int64_t sb = (int64_t)sms * (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4));
+  int64_t sb = (int64_t)sms * (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4)));
   const int64_t sneed = ((n < (int64_t)nrows ? n : (int64_t)nrows) + 7) / 8;
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
@@ -835,6 +835,9 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
     case 4: return grp_reduce_t<MODE, XT, YT, 4>(a, n, nrows, st, launches, tr);
     case 8: return grp_reduce_t<MODE, XT, YT, 8>(a, n, nrows, st, launches, tr);
     case 16: return grp_reduce_t<MODE, XT, YT, 16>(a, n, nrows, st, launches, tr);
+    case 32:  // value rows of 1024 (the paper's inferred width)
+      if constexpr (MODE == MODE_DV) return grp_reduce_t<MODE, XT, YT, 32>(a, n, nrows, st, launches, tr);
+      else return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
 }
@@ -1083,11 +1086,13 @@ bool epl_ok(int D) {
   const int e = D / 32;
   return D % 32 == 0 && (e == 1 || e == 2 || e == 4 || e == 8 || e == 16);
 }
+// value rows: also 1024 wide (EPL 32) in the value reducers
+bool epl_ok_v(int D) { return epl_ok(D) || D == 1024; }
 
 }  // namespace
 
 bool backward_supported(const Shape& s, bool values, bool keys) {
-  if (values && !epl_ok(s.d_v)) return false;
+  if (values && !epl_ok_v(s.d_v)) return false;
   if (keys && (!epl_ok(s.d_h) || s.k > 64)) return false;
   return true;
 }
@@ -1162,7 +1167,7 @@ cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const floa
                                   const BwdWorkspace& ws, cudaStream_t st, int* launches,
                                   const TraceEvents& tr, int upd, float lr, float eps,
                                   float* state, const ScatterPeers* peers) {
-  if (!epl_ok(s.d_v)) return cudaErrorNotSupported;
+  if (!epl_ok_v(s.d_v)) return cudaErrorNotSupported;
   const int64_t n = s.B * s.H * s.k;  // s.B is the gather batch here
   if (n == 0) return cudaSuccess;
   const uint32_t nrows = (uint32_t)(s.row_end - s.row_begin);
@@ -1206,7 +1211,7 @@ cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const Per
                                    const void* V, float* dV, const PerRank<float>& dw_dst,
                                    const BwdWorkspace& ws, cudaStream_t st, int* launches,
                                    const TraceEvents& tr) {
-  if (!epl_ok(s.d_v) || s.og != 1) return cudaErrorNotSupported;
+  if (!epl_ok_v(s.d_v) || s.og != 1) return cudaErrorNotSupported;
   const int64_t n = (int64_t)r.P * r.cap;
   if (n == 0) return cudaSuccess;
   if (n >= (int64_t(1) << 32)) return cudaErrorNotSupported;
@@ -1242,7 +1247,7 @@ cudaError_t launch_scatter_records(const Shape& s, const RecordsIn& r, const Per
 cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const float* w,
                                   const float* dOut, const void* V, float* dV, float* dw,
                                   cudaStream_t st, int* launches) {
-  if (!epl_ok(s.d_v)) return cudaErrorNotSupported;
+  if (!epl_ok_v(s.d_v)) return cudaErrorNotSupported;
   const unsigned blocks = (unsigned)((s.B + 7) / 8);
   const int HK = s.H * s.k;
 #define ATOMIC(VT, E)                                                                          \
@@ -1252,11 +1257,11 @@ cudaError_t launch_scatter_atomic(const Shape& s, const int32_t* idx, const floa
   if (s.v_dt == F32) {
     switch (E) { case 1: ATOMIC(float, 1); break; case 2: ATOMIC(float, 2); break;
       case 4: ATOMIC(float, 4); break; case 8: ATOMIC(float, 8); break;
-      default: ATOMIC(float, 16); }
+      case 16: ATOMIC(float, 16); break; default: ATOMIC(float, 32); }
   } else {
     switch (E) { case 1: ATOMIC(__nv_bfloat16, 1); break; case 2: ATOMIC(__nv_bfloat16, 2); break;
       case 4: ATOMIC(__nv_bfloat16, 4); break; case 8: ATOMIC(__nv_bfloat16, 8); break;
-      default: ATOMIC(__nv_bfloat16, 16); }
+      case 16: ATOMIC(__nv_bfloat16, 16); break; default: ATOMIC(__nv_bfloat16, 32); }
   }
 #undef ATOMIC
   cudaError_t e = cudaGetLastError();

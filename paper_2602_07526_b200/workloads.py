@@ -85,14 +85,14 @@ CONFIGS = {
     # the paper's deployed design -- token-specific query
     # networks and sub-keys, one value table shared by the layer's tokens
     # (hybrid allocation), n = 256^2, k = 32, a
-    # batch of 2048 x 16 tokens.  d_v = 512 (the
-    # paper's width is not stated; SURVEY E8 infers ~1024, above this build's
-    # 512-wide reducer), d_h = 128.  One head per token: 16 groups.
-    "f4_tokens_bf16": PKMConfig("f4_tokens_bf16", 5, 2048, 16, 128, 256, 512, 32,
+    # batch of 2048 x 16 tokens.  d_v = 1024 (the
+    # paper's width is not stated; SURVEY E8 infers ~1024), d_h = 128.  One
+    # head per token: 16 groups.
+    "f4_tokens_bf16": PKMConfig("f4_tokens_bf16", 5, 2048, 16, 128, 256, 1024, 32,
                                 torch.bfloat16, torch.bfloat16, key_std=1.0, head_groups=16),
     # ... and the per-token value tables of the paper's "per-token V" ablation
     # (PAPER.md:446): 16 tables of 256^2 rows.
-    "f4_tokens_pertable_bf16": PKMConfig("f4_tokens_pertable_bf16", 6, 2048, 16, 128, 256, 512, 32,
+    "f4_tokens_pertable_bf16": PKMConfig("f4_tokens_pertable_bf16", 6, 2048, 16, 128, 256, 1024, 32,
                                          torch.bfloat16, torch.bfloat16, key_std=1.0, head_groups=16,
                                          group_tables=True),
 }

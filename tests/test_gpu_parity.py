@@ -61,6 +61,8 @@ SWEEP = [
     # two-sweep scorer rows (n_sub > 512) with KT = 8: bf16, and fp32 (1xTF32 first sweep)
     (50, 2, 1024, 64, 64, 8, torch.bfloat16, torch.bfloat16),
     (40, 1, 1024, 32, 64, 5, torch.float32, torch.float32),
+    # value rows of 1024 (the paper's inferred width), bf16
+    (70, 2, 128, 64, 1024, 16, torch.bfloat16, torch.bfloat16),
 ]
 
 
