@@ -722,8 +722,10 @@ cudaError_t x_combine(msn_pkm_t h, const XView& v, float* out, cudaStream_t st, 
   return launch_reduce_partials(v.own<float>(MSN_XREG_PART_IN), v.P, v.lb, 1, h->cfg.d_value, out, st, L);
 }
 
+// dw_direct (P = 1 only, may be NULL): write dw straight into the caller's
+// [B_l, H, k] array (one rank's windows are the slots in (b, h, t) order)
 cudaError_t x_scatter(msn_pkm_t h, const XView& v, const void* values, float* d_values, void* ws,
-                      cudaStream_t st, int* L) {
+                      cudaStream_t st, int* L, float* dw_direct = nullptr, const float* dout_direct = nullptr) {
   PerRank<const float> xs;
   PerRank<float> dd;
   for (int p = 0; p < kMaxWorld; ++p) {
@@ -736,6 +738,8 @@ cudaError_t x_scatter(msn_pkm_t h, const XView& v, const void* values, float* d_
     dd.p[p] = v.staged ? v.own<float>(MSN_XREG_DW_OUT) + p * v.cap
                        : v.reg<float>(p, MSN_XREG_DW_IN) + v.rank * v.cap;  // window order
   }
+  if (v.P == 1 && dw_direct) dd.p[0] = dw_direct;
+  if (v.P == 1 && dout_direct && !v.staged) xs.p[0] = dout_direct;
   const Shape s = shape_of(h->cfg, v.lb);
   const BwdWorkspace bw = carve_bwd_workspace(s, v.P * v.lb, ws);
   return launch_scatter_records(s, v.records_in(), xs, values, d_values, dd, bw, st, L,
@@ -747,8 +751,10 @@ cudaError_t x_collect(msn_pkm_t h, const XView& v, const int32_t* idx, float* dw
                            v.cap, v.rpr, dw, st, L);
 }
 
-cudaError_t x_barrier(const XView& v, cudaStream_t st, int* L) {
-  if (v.staged) return cudaSuccess;  // (the caller's collectives order the staged transport)
+cudaError_t x_barrier(const XView& v, cudaStream_t st, int* L, bool always = false) {
+  // (the caller's collectives order the staged transport; one rank in the
+  // composite calls: stream order)
+  if (v.staged || (v.P == 1 && !always)) return cudaSuccess;
   PerRank<uint32_t> f;
   for (int p = 0; p < kMaxWorld; ++p) f.p[p] = nullptr;
   for (int p = 0; p < v.P; ++p) f.p[p] = v.reg<uint32_t>(p, MSN_XREG_CTL);
@@ -866,7 +872,7 @@ msn_status msn_pkm_exchange_barrier(msn_pkm_t h, void* stream, const msn_pkm_exc
   h->last_launches = 0;
   XView v;
   if ((st = make_view(h, x, v))) return st;
-  XCALL(x_barrier(v, (cudaStream_t)stream, &h->last_launches), "exchange barrier");
+  XCALL(x_barrier(v, (cudaStream_t)stream, &h->last_launches, true), "exchange barrier");
   return MSN_OK;
 }
 
@@ -937,14 +943,15 @@ msn_status msn_pkm_backward_sharded(msn_pkm_t h, void* stream, int64_t local_bat
   const Shape s = shape_of(h->cfg, v.lb);
   const BwdWorkspace bw = carve_bwd_workspace(s, v.P * v.lb, workspace);
   float* dwp = dw ? dw : bw.dw;
-  if (v.lb > 0)
+  if (v.lb > 0 && v.P > 1)  // (one rank: the scatter reads the caller's d_out)
     XCALL(cudaMemcpyAsync(v.own<float>(MSN_XREG_DOUT), d_out, sizeof(float) * v.lb * h->cfg.d_value,
                           cudaMemcpyDeviceToDevice, cs), "d_out -> exchange");
   XCALL(x_barrier(v, cs, L), "exchange barrier");
-  XCALL(x_scatter(h, v, values, d_values, workspace, cs, L), "exchange scatter");
+  // one rank: the scatter's dw is already in (b, h, t) order, no collect
+  XCALL(x_scatter(h, v, values, d_values, workspace, cs, L, v.P == 1 ? dwp : nullptr, d_out), "exchange scatter");
   XCALL(x_barrier(v, cs, L), "exchange barrier");
   if (v.lb > 0) {
-    XCALL(x_collect(h, v, idx, dwp, cs, L), "exchange collect");
+    if (v.P > 1) XCALL(x_collect(h, v, idx, dwp, cs, L), "exchange collect");
     XCALL(launch_backward_keys(s, query, subkeys, idx, weights, dwp, d_query, d_subkeys, bw, cs, L),
           "backward (ds, dQ, dK)");
   }

@@ -894,12 +894,13 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
   pdl_enter();
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   constexpr bool DENSE = OUT == OUT_DENSE;
-  __shared__ int32_t s_r[8][64];
-  __shared__ float s_d[8][64];
+  __shared__ int32_t s_r[8][2][64];
+  __shared__ float s_d[8][2][64];
   __shared__ __align__(16) uint16_t s_row[DENSE ? 8 : 1][DENSE ? kDenseMax : 8];
   const int lane = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (l >= L) return;
+  int mh[2] = {0, 0};  // distinct sub-keys per half
   const int h = (int)(l % H);
   float wt[KPL], g[KPL], ds[KPL];
   int32_t f[KPL];
@@ -972,9 +973,8 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
         }
       }
     }
-    // dQ: lanes over d_h.  The distinct sub-keys of this half are compacted
-    // into shared memory (first-occurrence order) and their K rows are
-    // loaded DQ_U at a time, all loads of a group in flight together.
+    // the distinct sub-keys of this half, compacted into shared memory in
+    // first-occurrence order (dQ below, the dense / compact dS outputs)
     int m = 0;
 #pragma unroll
     for (int u = 0; u < KPL; ++u) {
@@ -983,11 +983,12 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       const unsigned bm = __ballot_sync(0xffffffffu, fl);
       if (fl) {
         const int pos = m + __popc(bm & ((1u << lane) - 1u));
-        s_r[wid][pos] = r[u];
-        s_d[wid][pos] = dS[u];
+        s_r[wid][half][pos] = r[u];
+        s_d[wid][half][pos] = dS[u];
       }
       m += __popc(bm);
     }
+    mh[half] = m;
     __syncwarp();
     if constexpr (DENSE) {
       // dense row: zero, place the m distinct values, copy out (16 B per lane)
@@ -996,46 +997,57 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       for (int c = lane; c < n16; c += 32) row4[c] = make_uint4(0, 0, 0, 0);
       __syncwarp();
       for (int c = lane; c < m; c += 32)
-        s_row[wid][s_r[wid][c]] = __bfloat16_as_ushort(__float2bfloat16_rn(s_d[wid][c]));
+        s_row[wid][s_r[wid][half][c]] = __bfloat16_as_ushort(__float2bfloat16_rn(s_d[wid][half][c]));
       __syncwarp();
       uint4* g4 = reinterpret_cast<uint4*>(dSd + (l * 2 + half) * (int64_t)n_sub);
       for (int c = lane; c < n16; c += 32) g4[c] = row4[c];
+      __syncwarp();
     }
     if constexpr (OUT == OUT_COMPACT) {
       uint2* rec = reinterpret_cast<uint2*>(dSd) + (l * 2 + half) * (int64_t)k;
       for (int c = lane; c < k; c += 32)
-        rec[c] = c < m ? make_uint2((uint32_t)s_r[wid][c], __float_as_uint(s_d[wid][c])) : make_uint2(0xffffffffu, 0u);
+        rec[c] = c < m ? make_uint2((uint32_t)s_r[wid][half][c], __float_as_uint(s_d[wid][half][c]))
+                       : make_uint2(0xffffffffu, 0u);
     }
-    if constexpr (DENSE && !DQ) {
-      __syncwarp();
-      continue;  // dQ = dSd . K runs on the tensor cores (dk_tc.cu)
-    }
-    float acc[EPL];
+  }
+  if constexpr (!DQ) return;  // dQ = dSd . K runs on the tensor cores (dk_tc.cu)
+  // dQ[b,h,half] = sum_r dS_r K[h,half,r], lanes over d_h, both halves
+  // together: DQ_U rows of each half in flight per step (the m distinct K
+  // rows of a lookup-half come from L2), each half's sum in first-occurrence
+  // order (the same additions as one half at a time)
+  float acc[2][EPL];
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
-    const QT* Kh = K + (int64_t)(h * 2 + half) * n_sub * d_h + lane * EPL;
-    for (int b0 = 0; b0 < m; b0 += DQ_U) {
-      float kr[DQ_U][EPL];
+  for (int i = 0; i < EPL; ++i) acc[0][i] = acc[1][i] = 0.f;
+  const QT* Kh0 = K + (int64_t)(h * 2) * n_sub * d_h + lane * EPL;
+  const QT* Kh1 = Kh0 + (int64_t)n_sub * d_h;
+  const int mm = mh[0] > mh[1] ? mh[0] : mh[1];
+  for (int b0 = 0; b0 < mm; b0 += DQ_U) {
+    float kr[2][DQ_U][EPL];
+#pragma unroll
+    for (int u = 0; u < DQ_U; ++u) {
+      if (b0 + u < mh[0]) load_slice<QT, EPL>(Kh0 + (int64_t)s_r[wid][0][b0 + u] * d_h, kr[0][u]);
+      if (b0 + u < mh[1]) load_slice<QT, EPL>(Kh1 + (int64_t)s_r[wid][1][b0 + u] * d_h, kr[1][u]);
+    }
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
       for (int u = 0; u < DQ_U; ++u)
-        if (b0 + u < m) load_slice<QT, EPL>(Kh + (int64_t)s_r[wid][b0 + u] * d_h, kr[u]);
+        if (b0 + u < mh[hf]) {
+          const float dSv = s_d[wid][hf][b0 + u];
 #pragma unroll
-      for (int u = 0; u < DQ_U; ++u)
-        if (b0 + u < m) {
-          const float dSv = s_d[wid][b0 + u];
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] = fmaf(dSv, kr[u][i], acc[i]);
+          for (int i = 0; i < EPL; ++i) acc[hf][i] = fmaf(dSv, kr[hf][u][i], acc[hf][i]);
         }
-    }
-    __syncwarp();
+  }
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
     if (dq_bf16) {  // MSN_FLAG_DQ_QK_DTYPE: one RNE rounding
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dQ) + (l * 2 + half) * d_h + lane * EPL;
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dQ) + (l * 2 + hf) * d_h + lane * EPL;
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) o[i] = __float2bfloat16_rn(acc[i]);
+      for (int i = 0; i < EPL; ++i) o[i] = __float2bfloat16_rn(acc[hf][i]);
     } else {
-      float* o = dQ + (l * 2 + half) * d_h + lane * EPL;
+      float* o = dQ + (l * 2 + hf) * d_h + lane * EPL;
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) o[i] = acc[i];
+      for (int i = 0; i < EPL; ++i) o[i] = acc[hf][i];
     }
   }
 }

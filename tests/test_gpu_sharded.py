@@ -168,7 +168,13 @@ def test_forward_backward_sharded_p1_vs_phases_and_oracle(B):
         dq, _, _, dw = sp.backward(dOut, Q, K, V, tape, d_subkeys=dK, d_value_shard=dV)
     torch.cuda.synchronize()
     ctl = sp.xb.region("CTL", 64).cpu()
-    assert ctl[16].item() == 8 and ctl[17].item() == 0  # 4 barriers per step, no timeout
+    assert ctl[17].item() == 0  # no barrier timeout (one rank: the composite needs none)
+    # the barrier phase itself: epochs advance, own flag set, no timeout
+    for _ in range(3):
+        sp.ph.exchange_barrier(sp.xb.x)
+    torch.cuda.synchronize()
+    ctl = sp.xb.region("CTL", 64).cpu()
+    assert ctl[16].item() == ctl[0].item() == 3 and ctl[17].item() == 0
     ref = run_emulated(cfg, Q, K, V, dOut, 1, "peer")
     assert torch.equal(out, ref["out"]) and torch.equal(tape[0], ref["idx"]) and torch.equal(dw, ref["dw"])
     assert torch.equal(dq, ref["dQ"])
