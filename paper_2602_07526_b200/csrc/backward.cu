@@ -1022,21 +1022,25 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
   const QT* Kh1 = Kh0 + (int64_t)n_sub * d_h;
   const int mm = mh[0] > mh[1] ? mh[0] : mh[1];
   for (int b0 = 0; b0 < mm; b0 += DQ_U) {
+    // unconditional loads (a row past m repeats row 0 and is added with 0): no
+    // branches between them, so all 2 DQ_U rows are in flight together
     float kr[2][DQ_U][EPL];
+    float dv[2][DQ_U];
 #pragma unroll
-    for (int u = 0; u < DQ_U; ++u) {
-      if (b0 + u < mh[0]) load_slice<QT, EPL>(Kh0 + (int64_t)s_r[wid][0][b0 + u] * d_h, kr[0][u]);
-      if (b0 + u < mh[1]) load_slice<QT, EPL>(Kh1 + (int64_t)s_r[wid][1][b0 + u] * d_h, kr[1][u]);
-    }
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int u = 0; u < DQ_U; ++u) {
+        const bool in = b0 + u < mh[hf];
+        const int j = in ? b0 + u : 0;
+        dv[hf][u] = in ? s_d[wid][hf][j] : 0.f;
+        load_slice<QT, EPL>((hf ? Kh1 : Kh0) + (int64_t)s_r[wid][hf][j] * d_h, kr[hf][u]);
+      }
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
       for (int u = 0; u < DQ_U; ++u)
-        if (b0 + u < mh[hf]) {
-          const float dSv = s_d[wid][hf][b0 + u];
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[hf][i] = fmaf(dSv, kr[hf][u][i], acc[hf][i]);
-        }
+        for (int i = 0; i < EPL; ++i) acc[hf][i] = fmaf(dv[hf][u], kr[hf][u][i], acc[hf][i]);
   }
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {

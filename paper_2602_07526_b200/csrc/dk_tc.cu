@@ -165,40 +165,67 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       constexpr int kRecMax = 16;  // k <= 64 slots per query over 4 threads
       const int per = (p.k + 3) / 4;
       uint2 nxt[kRecMax];
+      auto rec_ptr = [&](int kb) -> const uint2* {
+        const int64_t b = q0 + (int64_t)kb * kBK + ql;
+        return p.rec + (b * HH + hh) * (int64_t)p.k;
+      };
       auto load_kb = [&](int kb) {
         const int64_t b = q0 + (int64_t)kb * kBK + ql;
-        const uint2* r = p.rec + (b * HH + hh) * (int64_t)p.k;
+        const uint2* r = rec_ptr(kb);
 #pragma unroll
         for (int c = 0; c < kRecMax; ++c) {
           const int slot = part + 4 * c;
           nxt[c] = (c < per && slot < p.k && b < q1) ? r[slot] : make_uint2(0xffffffffu, 0u);
         }
       };
+      // the records of k-block kb + kPre are pulled into L2 now, so that the
+      // register load one k-block ahead hits L2 (the k-block budget is one
+      // MMA of ~0.7 us; an HBM miss would not fit in it)
+      constexpr int kPre = 3;
+      auto prefetch_kb = [&](int kb) {
+        if (kb < nkb && (part & 1) == 0 && q0 + (int64_t)kb * kBK + ql < q1) {
+          const char* a = reinterpret_cast<const char*>(rec_ptr(kb)) + (part >> 1) * 128;
+          if ((part >> 1) * 128 < p.k * 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        }
+      };
+      for (int i = 0; i < kPre && i < nkb; ++i) prefetch_kb(i);
       if (nkb > 0) load_kb(0);
+      int s = 0;
+      uint32_t ph = 0;
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStg;
         uint2 cur[kRecMax];
 #pragma unroll
         for (int c = 0; c < kRecMax; ++c) cur[c] = nxt[c];
+        prefetch_kb(kb + kPre);
         if (kb + 1 < nkb) load_kb(kb + 1);  // in flight while this stage is built
-        mbar_wait(&empty[s], ((kb / kStg) & 1) ^ 1);
+        mbar_wait(&empty[s], ph ^ 1);
         uint8_t* a = sA + s * MT * 2 * kAtom;
         uint4* a4 = reinterpret_cast<uint4*>(a);
-        for (int i = u; i < MT * 2 * kAtom / 16; i += 256) a4[i] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < MT * 2 * kAtom / 16 / 256; ++i) a4[u + 256 * i] = make_uint4(0, 0, 0, 0);
         asm volatile("bar.sync 1, 256;" ::: "memory");
+        const uint32_t abase = smem_u32(a) + (uint32_t)ql * 128;
 #pragma unroll
         for (int c = 0; c < kRecMax; ++c) {
-          const uint32_t il = cur[c].x - (uint32_t)i0;  // (sentinel and out-of-range wrap high)
-          if (il < (uint32_t)(kBM * MT)) {
+          if (c < per) {
+            const uint32_t il = cur[c].x - (uint32_t)i0;  // (sentinel and out-of-range wrap high)
             const uint32_t e = il & 63u;
-            const uint32_t off = (il >> 6) * kAtom + ql * 128 + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) + (e & 7u) * 2;
+            const uint32_t off = (il >> 6) * kAtom + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) + (e & 7u) * 2;
             const __nv_bfloat16 v = __float2bfloat16_rn(__uint_as_float(cur[c].y));
-            *reinterpret_cast<__nv_bfloat16*>(a + off) = v;
+            const uint32_t inr = il < (uint32_t)(kBM * MT) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n@p st.shared.b16 [%0], %1;\n}\n" ::"r"(abase + off),
+                "h"(__bfloat16_as_ushort(v)), "r"(inr)
+                : "memory");
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[s]);
+        if (++s == kStg) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     if ((warp - 2) / 4 < MT) {
