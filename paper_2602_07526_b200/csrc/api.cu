@@ -63,12 +63,11 @@ Shape shape_of(const msn_pkm_config& c, int64_t B) {
   return s;
 }
 
-// forward workspace layout: [cand (score, index) | cand_n | scores (SIMT scorer only)]
+// forward workspace layout: [cand (score, index) | cand_n | split sub-keys (3xTF32)]
 size_t fwd_bytes(const Shape& s) {
   const int64_t rows = s.B * s.H * 2 * select_segments(s, true);  // (row, column segment) lists
-  size_t b = align256(sizeof(uint2) * rows * kCandCap) + align256(sizeof(int32_t) * rows);
-  if (!select_tc_supported(s)) b += align256(sizeof(float) * rows * s.n_sub);
-  else b += align256(select_tc_workspace_bytes(s));
+  size_t b = align256(sizeof(uint2) * rows * select_cap(s)) + align256(sizeof(int32_t) * rows);
+  b += align256(select_tc_workspace_bytes(s));
   return b;
 }
 
@@ -76,13 +75,24 @@ size_t fwd_bytes(const Shape& s) {
 char* carve_cands(const Shape& s, void* ws, Cands& cd) {
   cd.SC = select_segments(s, true);
   cd.S = select_segments(s, false);
+  cd.cap = select_cap(s);
   const int64_t rows = s.B * s.H * 2 * cd.SC;
   char* p = (char*)ws;
   cd.vc = (uint2*)p;
-  p += align256(sizeof(uint2) * rows * kCandCap);
+  p += align256(sizeof(uint2) * rows * cd.cap);
   cd.n = (int32_t*)p;
   p += align256(sizeof(int32_t) * rows);
   return p;
+}
+
+// The scorer (a1-a2) is the tcgen05 kernel only: other shapes are refused on
+// the host before anything is launched.
+msn_status check_select_shape(const Shape& s) {
+  if (select_tc_supported(s)) return MSN_OK;
+  return fail(MSN_ERR_UNSUPPORTED,
+              "the tcgen05 scorer needs n_sub %% 32 == 0, d_half %% 64 == 0 and <= 256 (bf16) or "
+              "%% 32 == 0 and <= 128 (fp32), k <= 64 (n_sub %d, d_half %d, k %d); nothing was launched",
+              s.n_sub, s.d_h, s.k);
 }
 
 msn_status check_bwd_shape(msn_pkm_t h, bool values, bool keys) {
@@ -133,6 +143,8 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
                      int* launches, const void* values = nullptr, float* out = nullptr,
                      const Gate& gate = Gate{}) {
   const Shape s = shape_of(h->cfg, B);
+  msn_status st0 = check_select_shape(s);
+  if (st0) return st0;
   if (ws_bytes < fwd_bytes(s))
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
   Cands cd;
@@ -141,14 +153,8 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   cd.rq.K = subkeys;
   cd.rq.d_h = s.d_h;
   cd.rq.qk_dt = s.qk_dt;
-  cudaError_t e;
-  if (select_tc_supported(s)) {
-    e = launch_select_tc(s, query, subkeys, cd, p, st, launches);
-    if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half candidates)");
-  } else {
-    e = launch_select_simt(s, query, subkeys, (float*)p, cd, st, launches);
-    if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half top-k)");
-  }
+  cudaError_t e = launch_select_tc(s, query, subkeys, cd, p, st, launches);
+  if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half candidates)");
   if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);  // stage boundary: scoring done
   if (values && cd.S == 1) {
     if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);  // (fused: no separate Cartesian stage)
@@ -241,6 +247,7 @@ msn_status msn_pkm_create(const msn_pkm_config* c, msn_pkm_t* out) {
   if (G > 1 && (c->flags & MSN_FLAG_ATOMIC_BWD))
     return fail(MSN_ERR_UNSUPPORTED, "head groups need the deterministic backward");
   if (c->n_sub > 2048) return fail(MSN_ERR_UNSUPPORTED, "n_sub > 2048 is not supported");
+
   msn_pkm* h = new (std::nothrow) msn_pkm;
   if (!h) return fail(MSN_ERR_INTERNAL, "out of host memory");
   h->cfg = *c;
@@ -670,6 +677,8 @@ msn_status make_view(msn_pkm_t h, const msn_pkm_exchange* x, XView& v) {
 msn_status x_select(msn_pkm_t h, const XView& v, const void* query, const void* subkeys, const void* values,
                     int32_t* idx, float* w, float* out, void* ws, size_t ws_bytes, cudaStream_t st, int* L) {
   const Shape s = shape_of(h->cfg, v.lb);
+  msn_status st0 = check_select_shape(s);
+  if (st0) return st0;
   if (ws_bytes < fwd_bytes(s))
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
   Cands cd;
@@ -678,8 +687,7 @@ msn_status x_select(msn_pkm_t h, const XView& v, const void* query, const void* 
   cd.rq.K = subkeys;
   cd.rq.d_h = s.d_h;
   cd.rq.qk_dt = s.qk_dt;
-  cudaError_t e = select_tc_supported(s) ? launch_select_tc(s, query, subkeys, cd, p, st, L)
-                                         : launch_select_simt(s, query, subkeys, (float*)p, cd, st, L);
+  cudaError_t e = launch_select_tc(s, query, subkeys, cd, p, st, L);
   if (e != cudaSuccess) return cuda_fail(e, "select (scoring + per-half candidates)");
   if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);
   RouteArgs ra;

@@ -3,8 +3,8 @@
 // per lookup, all in registers and shared memory.
 //
 // Per-half order (a2).  Each half arrives as an unordered candidate list
-// (<= kCandCap entries containing its top-k, see kernels.h); the warp sorts
-// it with a 64-element bitonic network across lanes (shuffles; element
+// (a superset of its top-k, up to 64 entries, 128 for k > 32, see kernels.h);
+// the warp sorts it with a bitonic network across lanes (shuffles; element
 // e = r*32 + lane, composite order (score desc, index asc) -- reading R5)
 // and keeps the first k: I (row half) and J (column half).
 //
@@ -74,31 +74,38 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     const int64_t row = l * 2 + half;
     float v[2];
     int32_t ix[2];
-    const int n = cand_n[row * SC];
+    // the list: [0, n0) u [CAP - n1, CAP) (the scorer's two appending ends)
+    constexpr int CAP = cand_cap(KMAX);
+    constexpr int R = CAP / 32;
+    uint64_t key[R];
     {
       // sort by the composite key (score desc, index asc) as one u64
-      uint64_t key[2];
-      const uint2* rc = cand + row * SC * kCandCap;
+      const uint32_t nn = (uint32_t)cand_n[row * SC];
+      const int n0 = (int)(nn & 0xffffu), n1 = (int)(nn >> 16);
+      const uint2* rc = cand + row * SC * CAP;
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < R; ++r) {
         const int e = r * 32 + lane;
-        const uint2 c = e < n ? rc[e] : make_uint2(0u, 0u);
-        key[r] = e < n ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
+        const bool in = e < n0 || e >= CAP - n1;
+        const uint2 c = in ? rc[e] : make_uint2(0u, 0u);
+        key[r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
       }
-      warp_sort64_u64(key);
+      warp_sort_u64<R>(key);
       if constexpr (KMAX == 32 && SEG == 2) {
         // the row's second column segment (its own list, see select_tc.cu):
         // sorted likewise, then the best 32 of both lists by the half-cleaner
         // max(A_i, B_31-i) and a 5-step bitonic merge (k <= 32 here)
-        const int n1 = cand_n[row * SC + 1];
+        const uint32_t nb = (uint32_t)cand_n[row * SC + 1];
+        const int m0 = (int)(nb & 0xffffu), m1 = (int)(nb >> 16);
         uint64_t k1[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int e = r * 32 + lane;
-          const uint2 c = e < n1 ? rc[kCandCap + e] : make_uint2(0u, 0u);
-          k1[r] = e < n1 ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
+          const bool in = e < m0 || e >= CAP - m1;
+          const uint2 c = in ? rc[CAP + e] : make_uint2(0u, 0u);
+          k1[r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
         }
-        warp_sort64_u64(k1);
+        warp_sort_u64<2>(k1);
         const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)k1[0], 31 - lane);
         const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(k1[0] >> 32), 31 - lane);
         const uint64_t bk = ((uint64_t)bhi << 32) | blo;

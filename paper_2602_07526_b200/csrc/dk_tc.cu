@@ -72,7 +72,7 @@ constexpr uint32_t idesc_bf16_mn(int M, int N) {
 // named barrier, one bf16 store per record in range at its 128-byte-swizzle
 // position (the layout TMA would produce), fence.proxy.async, arrive.  No
 // dense dS matrix in HBM; TMA then loads only the Q tiles.
-template <int MT, bool REC>
+template <int MT, bool REC, int RP = 8>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     dk_gemm_kernel(const __grid_constant__ CUtensorMap tmap_ds,
                    const __grid_constant__ CUtensorMap tmap_q, const DkParams p) {
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const int u = threadIdx.x - 64;
       const int ql = u >> 2, part = u & 3;
       const int HH = 2 * p.H;
-      constexpr int kRecMax = 16;  // k <= 64 slots per query over 4 threads
+      constexpr int kRecMax = RP;  // record slots per thread: k <= 4 RP
       const int per = (p.k + 3) / 4;
       uint2 nxt[kRecMax];
       auto rec_ptr = [&](int kb) -> const uint2* {
@@ -188,6 +188,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           if ((part >> 1) * 128 < p.k * 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
         }
       };
+      // every stage starts zeroed; afterwards a thread only clears the
+      // entries it wrote into that stage kStg k-blocks earlier.  The position
+      // (query ql, sub-key) of an entry is written only by the 4 threads of
+      // query ql -- lanes of one warp -- so a __syncwarp between the clears
+      // and the new stores orders them (no CTA barrier, no full zeroing).
+      for (int i = u; i < kStg * MT * 2 * kAtom / 16; i += 256)
+        reinterpret_cast<uint4*>(sA)[i] = make_uint4(0, 0, 0, 0);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      uint32_t old[kStg][kRecMax];
+#pragma unroll
+      for (int t = 0; t < kStg; ++t)
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c) old[t][c] = 0xffffffffu;
       for (int i = 0; i < kPre && i < nkb; ++i) prefetch_kb(i);
       if (nkb > 0) load_kb(0);
       int s = 0;
@@ -199,26 +212,47 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         prefetch_kb(kb + kPre);
         if (kb + 1 < nkb) load_kb(kb + 1);  // in flight while this stage is built
         mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* a = sA + s * MT * 2 * kAtom;
-        uint4* a4 = reinterpret_cast<uint4*>(a);
-#pragma unroll
-        for (int i = 0; i < MT * 2 * kAtom / 16 / 256; ++i) a4[u + 256 * i] = make_uint4(0, 0, 0, 0);
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const uint32_t abase = smem_u32(a) + (uint32_t)ql * 128;
+        const uint32_t abase = smem_u32(sA + s * MT * 2 * kAtom);
+        // the stage index is a runtime value: select this stage's old list
+        // with constant indices (registers, no local memory)
+        uint32_t prev[kRecMax];
 #pragma unroll
         for (int c = 0; c < kRecMax; ++c) {
+          prev[c] = old[0][c];
+#pragma unroll
+          for (int t = 1; t < kStg; ++t)
+            if (s == t) prev[c] = old[t][c];
+        }
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c)
+          if (c < per)
+            asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %1, -1;\n@p st.shared.b16 [%0], 0;\n}\n" ::"r"(abase + prev[c]),
+                         "r"(prev[c])
+                         : "memory");
+        __syncwarp();
+        uint32_t now[kRecMax];
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c) {
+          now[c] = 0xffffffffu;
           if (c < per) {
             const uint32_t il = cur[c].x - (uint32_t)i0;  // (sentinel and out-of-range wrap high)
             const uint32_t e = il & 63u;
-            const uint32_t off = (il >> 6) * kAtom + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) + (e & 7u) * 2;
+            const uint32_t off = (il >> 6) * kAtom + (uint32_t)ql * 128 + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) +
+                                 (e & 7u) * 2;
             const __nv_bfloat16 v = __float2bfloat16_rn(__uint_as_float(cur[c].y));
-            const uint32_t inr = il < (uint32_t)(kBM * MT) ? 1u : 0u;
+            const bool inr = il < (uint32_t)(kBM * MT);
+            if (inr) now[c] = off;
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n@p st.shared.b16 [%0], %1;\n}\n" ::"r"(abase + off),
-                "h"(__bfloat16_as_ushort(v)), "r"(inr)
+                "h"(__bfloat16_as_ushort(v)), "r"(inr ? 1u : 0u)
                 : "memory");
           }
         }
+#pragma unroll
+        for (int c = 0; c < kRecMax; ++c)
+#pragma unroll
+          for (int t = 0; t < kStg; ++t)
+            if (s == t) old[t][c] = now[c];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[s]);
@@ -582,10 +616,12 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
              reinterpret_cast<const uint2*>(ws), s.k};
   const int mtk = dk_mt(s);
   const bool rec = !with_dq;  // ds_dq_kernel wrote compact records (dQ done there)
-  auto dkk = rec ? (mtk == 2 ? dk_gemm_kernel<2, true> : dk_gemm_kernel<1, true>)
+  const bool rp16 = s.k > 32;  // record slots per builder thread: k <= 32 -> 8, else 16
+  auto dkk = rec ? (mtk == 2 ? (rp16 ? dk_gemm_kernel<2, true, 16> : dk_gemm_kernel<2, true, 8>)
+                             : (rp16 ? dk_gemm_kernel<1, true, 16> : dk_gemm_kernel<1, true, 8>))
                  : (mtk == 2 ? dk_gemm_kernel<2, false> : dk_gemm_kernel<1, false>);
-  static std::atomic<uint64_t> attr[4];
-  cudaError_t e = smem_attr_once(attr[(mtk - 1) * 2 + (rec ? 1 : 0)], dkk, 227 * 1024);
+  static std::atomic<uint64_t> attr[8];
+  cudaError_t e = smem_attr_once(attr[(mtk - 1) * 4 + (rec ? 2 : 0) + (rp16 ? 1 : 0)], dkk, 227 * 1024);
   if (e != cudaSuccess) return e;
   dim3 grid(s.n_sub / (kBM * mtk), HH, S);
   launch_pdl(dkk, grid, kThreads, dk_smem_bytes(s, mtk), st, mds, mq, p);

@@ -28,13 +28,14 @@ struct Shape {
 };
 
 // Per-half candidate lists, the hand-off between a1+a2 and a3: for every
-// (b, h, half) row r, entries i < cand_n[r] of vc[r*kCandCap + i] are
-// (score bits, sub-key index) pairs in no particular order that are
-// guaranteed to contain the row's top-k under (score desc, index asc).
-// cand_n[r] <= kCandCap always: a tcgen05 scorer row whose bound let more
-// than kCandCap columns through (massive exact ties) is rescored exactly from
-// the query and sub-keys in `rq` before it is written.
-constexpr int kCandCap = 64;
+// (b, h, half) row r and column segment g, the list vc[(r*SC + g)*cap ...] of
+// cap = cand_cap(KT) (score bits, sub-key index) pairs holds, in no particular
+// order, a superset of the segment's top-k under (score desc, index asc):
+// entries [0, n0) and [cap - n1, cap) with n[r*SC + g] = n0 | n1 << 16 (the
+// two scorer threads of a row append from both ends).  n0 + n1 <= cap always:
+// a row whose bound let more columns through (massive exact ties) is rescored
+// exactly from the query and sub-keys in `rq` into [0, nn), n1 = 0.
+__host__ __device__ constexpr int cand_cap(int kt) { return kt > 32 ? 128 : 64; }
 struct Rescore {
   const void* Q = nullptr;  // [B, H, 2, d_h] qk dtype
   const void* K = nullptr;  // [H, 2, n_sub, d_h] qk dtype
@@ -42,21 +43,17 @@ struct Rescore {
   int qk_dt = 0;
 };
 struct Cands {
-  uint2* vc;     // [B*H*2, SC*kCandCap] (float bits of the score, sub-key index)
-  int32_t* n;    // [B*H*2, SC]: entries of each column segment's list
+  uint2* vc;     // [B*H*2, SC, cap] (float bits of the score, sub-key index)
+  int32_t* n;    // [B*H*2, SC]: n0 | n1 << 16 per column segment's list
   Rescore rq;    // inputs, for rescoring overflowed rows
   int SC = 1;    // segment slots per row in the buffers (workspace layout)
   int S = 1;     // column segments in use (<= SC): the tcgen05 scorer splits a
                  // row over S CTAs, each writing the list of its columns
+  int cap = 64;  // list capacity, cand_cap(KT)
 };
 
-// a1+a2 (SIMT scorer, fp32 configs): exact per-half top-k (n = k entries).
-// scores_ws: [B,H,2,n_sub] fp32 scratch.
-cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, float* scores_ws,
-                               const Cands& cd, cudaStream_t st, int* launches);
-
-// a1+a2 on tcgen05 (bf16 configs): fused scoring GEMM + candidate selection.
-// Returns cudaErrorNotSupported when the shape is not handled.
+// a1+a2 on tcgen05: fused scoring GEMM + candidate selection (the only
+// scorer).  Returns cudaErrorNotSupported when the shape is not handled.
 // fp32 inputs run 3xTF32 (kind::tf32); ws holds the split sub-keys
 // (select_tc_workspace_bytes).
 // Column segments of a scorer row: 2 when a bf16 row of 512 < n_sub <= 1024
@@ -64,9 +61,10 @@ cudaError_t launch_select_simt(const Shape& s, const void* Q, const void* K, flo
 // latency regime, e.g. C5), else 1.  for_workspace: the layout's SC, which
 // does not depend on B.
 int select_segments(const Shape& s, bool for_workspace);
+int select_cap(const Shape& s);  // candidate list capacity (64, or 128 for k > 32)
 cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
                              void* ws, cudaStream_t st, int* launches);
-bool select_tc_supported(const Shape& s);
+bool select_tc_supported(const Shape& s);  // shape check only (no driver call)
 size_t select_tc_workspace_bytes(const Shape& s);
 
 // Memory-gated fusion: x~ = x (.) g(v_o), applied in the

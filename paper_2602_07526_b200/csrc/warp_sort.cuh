@@ -69,8 +69,43 @@ __device__ __forceinline__ void warp_sort64_u64(uint64_t (&x)[2]) {
   }
 }
 
+// Descending sort of 32 R composite keys (element e = r*32 + lane), R a power
+// of 2: strides >= 32 exchange registers of a lane, smaller ones lanes.
+template <int R>
+__device__ __forceinline__ void warp_sort_u64(uint64_t (&x)[R]) {
+  const int lane = threadIdx.x % 32;
+#pragma unroll
+  for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int r2 = r ^ (stride / 32);
+          if (r2 > r) {
+            const bool desc = ((r * 32 + lane) & size) == 0;
+            const uint64_t a = x[r], b = x[r2];
+            const bool sw = desc ? (b > a) : (a > b);
+            x[r] = sw ? b : a;
+            x[r2] = sw ? a : b;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = r * 32 + lane;
+          const uint64_t o = shfl_xor_u64(x[r], stride);
+          const bool lower = (e & stride) == 0;
+          const bool desc = (e & size) == 0;
+          x[r] = (lower == desc) == (o > x[r]) ? o : x[r];
+        }
+      }
+    }
+  }
+}
+
 // Exact per-half top list of lookup l when the scorer's candidate list
-// overflowed (cand_n > kCandCap): rescore all n_sub sub-keys of this
+// overflowed (its two ends met): rescore all n_sub sub-keys of this
 // (head, half) and keep the best 64 under (score desc, index asc).  32
 // sub-keys per step: lane e holds elements [8e, 8e+8) of q and of each K row
 // (coalesced 16-B loads), the 32 partial dots are summed across lanes by a

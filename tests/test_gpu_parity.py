@@ -47,7 +47,7 @@ def check_all(cfg, Q, K, V, dOut, res, backward=True):
 SWEEP = [
     # (B, H, n_sub, d_h, d_v, k, qk dtype, v dtype)
     (1, 1, 16, 32, 32, 1, torch.float32, torch.float32),
-    (7, 3, 40, 32, 64, 5, torch.float32, torch.float32),
+    (7, 3, 32, 32, 64, 5, torch.float32, torch.float32),
     (33, 2, 128, 64, 64, 8, torch.float32, torch.float32),
     (130, 4, 64, 32, 128, 17, torch.float32, torch.float32),
     (65, 2, 96, 64, 256, 32, torch.bfloat16, torch.bfloat16),
@@ -80,13 +80,15 @@ def test_small_shapes_fwd_bwd(shape):
 def test_integer_data_bit_exact_selection(B, H, n_sub, d_h, k):
     """Integer-valued queries/keys: every score is exact in fp32 and fp64, so
     the selection (including the tie rule R5, with many exact ties) must be
-    bit-identical -- on the SIMT path (d_h=32) and the tcgen05 path (bf16)."""
+    bit-identical -- 3xTF32 (fp32) and kind::f16 (bf16) tcgen05 scoring."""
     g = torch.Generator(device="cpu").manual_seed(5 + n_sub)
     d_v = 64
     Q = torch.randint(-2, 3, (B, H, 2, d_h), generator=g).float()
     K = torch.randint(-1, 2, (H, 2, n_sub, d_h), generator=g).float()
     V = torch.randn((n_sub * n_sub, d_v), generator=g) * 0.02
     for dt in (torch.float32, torch.bfloat16):
+        if dt == torch.bfloat16 and d_h % 64:
+            continue  # (the bf16 scorer takes d_half in multiples of 64)
         cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, dt, torch.float32)
         lk = lookup_for(cfg)
         out, idx, w = lk.forward(Q.to(dt).to(DEV), K.to(dt).to(DEV), V.to(DEV))
@@ -96,7 +98,7 @@ def test_integer_data_bit_exact_selection(B, H, n_sub, d_h, k):
         parity.row_close(out.cpu().numpy(), o["out"], 1e-4, what="out")
 
 
-@pytest.mark.parametrize("d_h,n_sub,dt", [(32, 64, torch.bfloat16), (64, 64, torch.bfloat16),
+@pytest.mark.parametrize("d_h,n_sub,dt", [(32, 64, torch.float32), (64, 64, torch.bfloat16),
                                           (128, 1024, torch.bfloat16), (128, 1024, torch.float32),
                                           (64, 256, torch.float32)])
 def test_zero_query_closed_form(d_h, n_sub, dt):
@@ -328,7 +330,7 @@ def test_fused_update(update, name, B):
 # ------------------------------------------ head groups / tokens (f4) ----
 @pytest.mark.parametrize("tables", [False, True])
 @pytest.mark.parametrize("B,dt,G,H,n_sub,d_h", [(300, torch.float32, 4, 8, 64, 32),
-                                                (2048, torch.bfloat16, 16, 16, 64, 32),
+                                                (2048, torch.bfloat16, 16, 16, 64, 64),
                                                 (9000, torch.float32, 2, 4, 64, 32),
                                                 # tcgen05 scorer: resident rows, two-sweep rows
                                                 (700, torch.bfloat16, 4, 8, 256, 64),
@@ -741,11 +743,22 @@ def test_step_host_pipelined_matches_device():
     torch.testing.assert_close(dK2, dK, rtol=1e-4, atol=1e-6)
 
 
-def _random_shapes(n, seed=2602):
-    """Seeded random shapes across the library's supported ranges: B ragged,
-    H up to 8, n_sub from 16 to 1024 (tcgen05 resident and two-sweep rows,
-    SIMT fallback shapes), d_h / d_v of every per-lane width the kernels
-    template on, k from 1 to 64, fp32 / bf16 keys and values."""
+def scorer_supports(n_sub, d_h, k, qdt):
+    """The tcgen05 scorer's shape rule (the library's only scorer; anything
+    else is refused with MSN_ERR_UNSUPPORTED before a launch)."""
+    if qdt == torch.bfloat16:
+        ok_d = d_h % 64 == 0 and d_h <= 256
+    else:
+        ok_d = d_h % 32 == 0 and d_h <= 128
+    return ok_d and n_sub % 32 == 0 and k <= 64
+
+
+def _random_shapes(n, seed=2602, supported=True):
+    """Seeded random shapes across the library's ranges: B ragged, H up to 8,
+    n_sub from 16 to 1024 (tcgen05 resident and two-sweep rows), d_h / d_v of
+    every per-lane width the kernels template on, k from 1 to 64, fp32 / bf16
+    keys and values -- the ones the scorer takes (supported=True) or the ones
+    it refuses."""
     import random
     rnd = random.Random(seed)
     dts = [torch.float32, torch.bfloat16]
@@ -756,9 +769,25 @@ def _random_shapes(n, seed=2602):
         H = rnd.choice([1, 2, 3, 4, 8])
         if H * k > 512:
             continue
-        out.append((rnd.randint(1, 400), H, n_sub, rnd.choice([32, 64, 128, 256]),
-                    rnd.choice([32, 64, 128, 256, 512]), k, rnd.choice(dts), rnd.choice(dts)))
+        shp = (rnd.randint(1, 400), H, n_sub, rnd.choice([32, 64, 128, 256]),
+               rnd.choice([32, 64, 128, 256, 512]), k, rnd.choice(dts), rnd.choice(dts))
+        if scorer_supports(shp[2], shp[3], shp[5], shp[6]) == supported:
+            out.append(shp)
     return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes(6, seed=77, supported=False),
+                         ids=lambda s: "x".join(str(v) for v in s[:6]) + f"-{str(s[6])[6:]}")
+def test_unsupported_shapes_refused(shape):
+    """Shapes outside the tcgen05 scorer's rule: forward returns
+    MSN_ERR_UNSUPPORTED before any launch (there is no second scorer)."""
+    from paper_2602_07526_b200._lib import MsnError
+    B, H, n_sub, d_h, d_v, k, qdt, vdt = shape
+    cfg = wl.tiny_config(B, H, d_h, n_sub, d_v, k, qdt, vdt, index=300 + n_sub + k)
+    Q, K, V, _ = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    with pytest.raises(MsnError, match="UNSUPPORTED"):
+        lk.forward(Q, K, V)
 
 
 @pytest.mark.parametrize("shape", _random_shapes(24),
