@@ -5,13 +5,15 @@
 //   and its gradients dTheta = sum_i dk~_i k_i^T, dk_i = Theta^T dk~_i
 //   (PAPER.md:296-302).
 // LN: one warp per row (the row lives in the lane registers), fp32 math,
-// output rounded once to the storage type.  The Theta products are batched
-// over the 2H codebooks as a 64x64-tiled fp32 SIMT GEMM (shared-memory
-// staging, 4x4 outputs per thread): at n_sub x d x d per codebook this is a
-// few hundred MFLOP per step, and fp32 keeps the fp32 configs exact enough
-// for their 1e-4 tolerance.
+// output rounded once to the storage type.  The Theta products (three per
+// step: K~ = K^ Theta^T, dK^ = dK~ Theta, dTheta += dK~^T K^) run on the
+// tensor cores as 3xTF32 tcgen05 GEMMs (pgemm_kernel: hi.hi + hi.lo + lo.hi,
+// fp32-accurate for the fp32 configs' 1e-4), batched over the 2H codebooks.
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
+
+#include <type_traits>
 
 namespace msn {
 namespace {
@@ -86,102 +88,156 @@ __global__ void __launch_bounds__(256) ln_backward_kernel(const T* __restrict__ 
   for (int i = 0; i < EPL; ++i) dx[r * D + i * 32 + lane] = rs * (g[i] - mg - v[i] * mgx);
 }
 
-// C[b] (= or +=) A[b] B[b]: A(i,k) = A[b*a_bs + i*a_rs + k*a_cs], likewise B;
-// C row-major with row stride c_rs.  64 x 64 tile per CTA, k-steps of 16;
-// the operand loads run kPf steps ahead of the math (a register ring), so a
-// k-step costs its arithmetic rather than a global-load round trip.  The k
-// order of the accumulation is unchanged (ascending).
-constexpr int kPf = 4;
+// ---- 3xTF32 tcgen05 GEMM for the Theta products ---------------------------
+// C[m][n] (=, or += with accumulate) = sum_k A(m, k) B(n, k) per batch z, with
+// A(m, k) = A[z a_bs + m a_rs + k a_cs] and B(n, k) = B[z b_bs + k b_rs + n b_cs]
+// (any layout: the operands are staged by the threads, which walk the source's
+// contiguous dimension), C[z c_bs + m c_rs + n].  One CTA per (128-row tile,
+// batch); N (<= 256, % 16) in one TMEM accumulator; K in blocks of 32: every
+// element is split x = hi + lo (hi = the TF32 value, lo exact in fp32) into
+// two 128-byte-swizzled K-major tiles of each operand, and one elected thread
+// issues D += Ahi.Bhi + Ahi.Blo + Alo.Bhi per 8-element step (the lo.lo term
+// is below fp32 rounding).  Two stages: the threads stage k-block kb + 1
+// while the tensor cores run kb (tcgen05.commit frees a stage).
+constexpr int kPgThreads = 256;
+constexpr int kPgM = 128;
+struct PgArgs {
+  int M, N, K;
+  const void* A;
+  int64_t a_rs, a_cs, a_bs;
+  const void* B;
+  int64_t b_rs, b_cs, b_bs;
+  void* C;
+  int64_t c_rs, c_bs;
+  int accumulate;
+};
+__device__ __forceinline__ uint32_t sw128_off(int r, int kk) {  // fp32 element (row r, k kk < 32)
+  return (uint32_t)r * 128u + ((((uint32_t)kk >> 2) ^ ((uint32_t)r & 7u)) << 4) + ((uint32_t)kk & 3u) * 4u;
+}
 template <typename TA, typename TB, typename TC>
-__global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const TA* __restrict__ A,
-                                                   int64_t a_rs, int64_t a_cs, int64_t a_bs,
-                                                   const TB* __restrict__ B, int64_t b_rs,
-                                                   int64_t b_cs, int64_t b_bs, TC* __restrict__ C,
-                                                   int64_t c_rs, int64_t c_bs, int accumulate) {
+__global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
+  using namespace tc;
   pdl_enter();
-  __shared__ float As[16][64 + 4], Bs[16][64 + 4];
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  const int64_t bi = blockIdx.z;
-  A += bi * a_bs;
-  B += bi * b_bs;
-  C += bi * c_bs;
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  const bool a_k = a_cs == 1;  // A contiguous along k
-  const bool b_k = b_rs == 1;  // B contiguous along k
-  // 16 x 64 elements per operand tile, 4 per thread; consecutive threads walk
-  // the operand's contiguous dimension (coalesced loads)
-  auto load = [&](int k0, float (&va)[4], float (&vb)[4]) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * 256;
-      const int kk = a_k ? e % 16 : e / 64, ii = a_k ? e / 16 : e % 64;
-      const int gk = k0 + kk;
-      va[u] = (m0 + ii < M && gk < K) ? ld_f(A + (int64_t)(m0 + ii) * a_rs + (int64_t)gk * a_cs) : 0.f;
-      const int kb = b_k ? e % 16 : e / 64, jj = b_k ? e / 16 : e % 64;
-      const int gb = k0 + kb;
-      vb[u] = (n0 + jj < N && gb < K) ? ld_f(B + (int64_t)gb * b_rs + (int64_t)(n0 + jj) * b_cs) : 0.f;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* base = smem_raw + pad;
+  const int NP = (g.N + 7) & ~7;                 // B rows staged (multiple of 8: whole swizzle atoms)
+  const int a_bytes = kPgM * 128, b_bytes = NP * 128;
+  const int stage = 2 * a_bytes + 2 * b_bytes;   // A_hi, A_lo, B_hi, B_lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * stage);
+  uint64_t* empty = bars;                        // [2]
+  uint64_t* done = bars + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
+  uint32_t tcols = 32;
+  while ((int)tcols < g.N) tcols <<= 1;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int m0 = blockIdx.x * kPgM;
+  const int64_t z = blockIdx.y;
+  const TA* A = reinterpret_cast<const TA*>(g.A) + z * g.a_bs;
+  const TB* B = reinterpret_cast<const TB*>(g.B) + z * g.b_bs;
+  if (tid == 0) {
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t idesc = idesc_tf32(kPgM, NP < 16 ? 16 : NP);
+  const int nkb = (g.K + 31) / 32;
+  // staging: element e of a [rows x 32] tile; the source's contiguous
+  // dimension is the fastest over consecutive threads
+  auto stage_tile = [&](auto* src, int64_t rs, int64_t cs, int rows, int row0, int rmax, int k0, uint8_t* hi,
+                        uint8_t* lo) {
+    const bool kfast = cs == 1;
+    for (int e = tid; e < rows * 32; e += kPgThreads) {
+      const int r = kfast ? e / 32 : e % rows;
+      const int kk = kfast ? e % 32 : e / rows;
+      const int gr = row0 + r, gk = k0 + kk;
+      float x = 0.f;
+      if (gr < rmax && gk < g.K) x = elem<std::remove_cv_t<std::remove_pointer_t<decltype(src)>>>::to_f(
+                                         src[(int64_t)gr * rs + (int64_t)gk * cs]);
+      const float h = tf32_hi(x);
+      const uint32_t o = sw128_off(r, kk);
+      *reinterpret_cast<float*>(hi + o) = h;
+      *reinterpret_cast<float*>(lo + o) = x - h;
     }
   };
-  float ra[kPf][4], rb[kPf][4];
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int s = kb & 1;
+    if (kb >= 2) mbar_wait(&empty[s], ((kb - 2) >> 1) & 1);
+    uint8_t* st = base + s * stage;
+    stage_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, kb * 32, st, st + a_bytes);
+    stage_tile(B, g.b_cs, g.b_rs, NP, 0, g.N, kb * 32, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t ah = smem_u32(st), al = ah + a_bytes, bh = al + a_bytes, bl = bh + b_bytes;
 #pragma unroll
-  for (int d = 0; d < kPf; ++d) load(d * 16, ra[d], rb[d]);
-  for (int k0 = 0; k0 < K; k0 += 16 * kPf) {
-#pragma unroll
-    for (int d = 0; d < kPf; ++d) {
-      const int kc = k0 + d * 16;
-      if (kc >= K) break;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = tid + u * 256;
-        const int kk = a_k ? e % 16 : e / 64, ii = a_k ? e / 16 : e % 64;
-        As[kk][ii] = ra[d][u];
-        const int kb = b_k ? e % 16 : e / 64, jj = b_k ? e / 16 : e % 64;
-        Bs[kb][jj] = rb[d][u];
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t acc = (kb | kk) != 0;
+        tc_mma_tf32(tmem, sw128_desc(ah + kk * 32), sw128_desc(bh + kk * 32), idesc, acc);
+        tc_mma_tf32(tmem, sw128_desc(ah + kk * 32), sw128_desc(bl + kk * 32), idesc, 1);
+        tc_mma_tf32(tmem, sw128_desc(al + kk * 32), sw128_desc(bh + kk * 32), idesc, 1);
       }
-      __syncthreads();
-      load(kc + 16 * kPf, ra[d], rb[d]);  // kPf steps ahead (zeros past K)
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        float a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-      }
-      __syncthreads();
+      tc_commit(&empty[s]);
+      if (kb == nkb - 1) tc_commit(done);
     }
   }
+  if (nkb > 0) mbar_wait(done, 0);
+  tc_fence_after();
+  // epilogue: warp w reads TMEM lane quarter w % 4 (rows), column half w / 4
+  {
+    const int q = warp & 3, ch = warp >> 2;
+    const int row = m0 + q * 32 + lane;
+    const int half = ((g.N + 63) / 64) * 32;  // columns per warp group, multiple of 32
+    TC* C = reinterpret_cast<TC*>(g.C) + z * g.c_bs + (int64_t)row * g.c_rs;
+    for (int c0 = ch * half; c0 < g.N && c0 < (ch + 1) * half; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+      if (row < g.M) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
-    if (m >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tx * 4 + j;
-      if (n >= N) continue;
-      TC* p = C + (int64_t)m * c_rs + n;
-      const float v = accumulate ? ld_f(p) + acc[i][j] : acc[i][j];
-      st_f(p, v);
+        for (int j = 0; j < 32; ++j) {
+          if (c0 + j >= g.N) break;
+          float v = nkb > 0 ? __uint_as_float(r[j]) : 0.f;
+          if (g.accumulate) v += ld_f(C + c0 + j);
+          st_f(C + c0 + j, v);
+        }
+      }
     }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
   }
 }
 
+size_t pgemm_smem(int N) {
+  const int NP = (N + 7) & ~7;
+  return 1024 + 2 * (2 * kPgM * 128 + 2 * NP * 128) + 64;
+}
+
 template <typename TA, typename TB, typename TC>
-cudaError_t gemm(int batch, int M, int N, int K, const TA* A, int64_t a_rs, int64_t a_cs,
-                 int64_t a_bs, const TB* B, int64_t b_rs, int64_t b_cs, int64_t b_bs, TC* C,
-                 int64_t c_rs, int64_t c_bs, int accumulate, cudaStream_t st) {
-  dim3 grid((N + 63) / 64, (M + 63) / 64, batch);
-  return launch_pdl(gemm_kernel<TA, TB, TC>, grid, 256, 0, st, M, N, K, A, a_rs, a_cs, a_bs, B,
-                    b_rs, b_cs, b_bs, C, c_rs, c_bs, accumulate);
+cudaError_t pgemm(int batch, int M, int N, int K, const TA* A, int64_t a_rs, int64_t a_cs, int64_t a_bs,
+                  const TB* B, int64_t b_rs, int64_t b_cs, int64_t b_bs, TC* C, int64_t c_rs, int64_t c_bs,
+                  int accumulate, cudaStream_t st) {
+  if (N > 256 || N % 16) return cudaErrorNotSupported;
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t e = smem_attr_once(attr, pgemm_kernel<TA, TB, TC>, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  PgArgs g{M, N, K, A, a_rs, a_cs, a_bs, B, b_rs, b_cs, b_bs, C, c_rs, c_bs, accumulate};
+  dim3 grid((M + kPgM - 1) / kPgM, batch);
+  return launch_pdl(pgemm_kernel<TA, TB, TC>, grid, kPgThreads, pgemm_smem(N), st, g);
 }
 
 template <typename T>
@@ -221,13 +277,13 @@ cudaError_t launch_layernorm(const Shape& s, int64_t rows, const void* x, void* 
 cudaError_t launch_key_transform(const Shape& s, const void* khat, const float* theta, void* keff,
                                  cudaStream_t st, int* launches) {
   const int d = s.d_h, n = s.n_sub, HH = 2 * s.H;
-  // K~ [n x d] = K^ [n x d] Theta^T:  B(k, j) = Theta[j][k]
+  // K~ [n x d] = K^ [n x d] Theta^T:  A(i, k) = K^[i][k], B(j, k) = Theta[j][k]
   cudaError_t e = s.qk_dt == F32
-      ? gemm<float, float, float>(HH, n, d, d, (const float*)khat, d, 1, (int64_t)n * d, theta, 1, d,
-                                  (int64_t)d * d, (float*)keff, d, (int64_t)n * d, 0, st)
-      : gemm<__nv_bfloat16, float, __nv_bfloat16>(HH, n, d, d, (const __nv_bfloat16*)khat, d, 1,
-                                                  (int64_t)n * d, theta, 1, d, (int64_t)d * d,
-                                                  (__nv_bfloat16*)keff, d, (int64_t)n * d, 0, st);
+      ? pgemm<float, float, float>(HH, n, d, d, (const float*)khat, d, 1, (int64_t)n * d, theta, 1, d,
+                                   (int64_t)d * d, (float*)keff, d, (int64_t)n * d, 0, st)
+      : pgemm<__nv_bfloat16, float, __nv_bfloat16>(HH, n, d, d, (const __nv_bfloat16*)khat, d, 1,
+                                                   (int64_t)n * d, theta, 1, d, (int64_t)d * d,
+                                                   (__nv_bfloat16*)keff, d, (int64_t)n * d, 0, st);
   if (e == cudaSuccess) ++*launches;
   return e;
 }
@@ -236,17 +292,17 @@ cudaError_t launch_key_transform_backward(const Shape& s, const void* khat, cons
                                           const float* dkeff, float* dkhat, float* dtheta,
                                           cudaStream_t st, int* launches) {
   const int d = s.d_h, n = s.n_sub, HH = 2 * s.H;
-  // dK^ [n x d] = dK~ [n x d] Theta [d x d]   (=)
-  cudaError_t e = gemm<float, float, float>(HH, n, d, d, dkeff, d, 1, (int64_t)n * d, theta, d, 1,
-                                            (int64_t)d * d, dkhat, d, (int64_t)n * d, 0, st);
+  // dK^ [n x d] = dK~ [n x d] Theta [d x d] (=):  A(i, r) = dK~[i][r], B(c, r) = Theta[r][c]
+  cudaError_t e = pgemm<float, float, float>(HH, n, d, d, dkeff, d, 1, (int64_t)n * d, theta, d, 1,
+                                             (int64_t)d * d, dkhat, d, (int64_t)n * d, 0, st);
   if (e != cudaSuccess) return e;
-  // dTheta [d x d] += dK~^T [d x n] K^ [n x d]:  A(i, k) = dK~[k][i]
+  // dTheta [d x d] += dK~^T K^:  A(r, i) = dK~[i][r], B(c, i) = K^[i][c]
   e = s.qk_dt == F32
-      ? gemm<float, float, float>(HH, d, d, n, dkeff, 1, d, (int64_t)n * d, (const float*)khat, d, 1,
-                                  (int64_t)n * d, dtheta, d, (int64_t)d * d, 1, st)
-      : gemm<float, __nv_bfloat16, float>(HH, d, d, n, dkeff, 1, d, (int64_t)n * d,
-                                          (const __nv_bfloat16*)khat, d, 1, (int64_t)n * d, dtheta, d,
-                                          (int64_t)d * d, 1, st);
+      ? pgemm<float, float, float>(HH, d, d, n, dkeff, 1, d, (int64_t)n * d, (const float*)khat, d, 1,
+                                   (int64_t)n * d, dtheta, d, (int64_t)d * d, 1, st)
+      : pgemm<float, __nv_bfloat16, float>(HH, d, d, n, dkeff, 1, d, (int64_t)n * d,
+                                           (const __nv_bfloat16*)khat, d, 1, (int64_t)n * d, dtheta, d,
+                                           (int64_t)d * d, 1, st);
   if (e == cudaSuccess) *launches += 2;
   return e;
 }

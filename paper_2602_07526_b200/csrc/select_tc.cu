@@ -540,22 +540,26 @@ bool is_tf32(const Shape& s) { return s.qk_dt == F32; }
 
 // Largest N tile (<= 256, multiple of 32, dividing n_sub); TF32 also keeps
 // 2 accumulators + the A_lo operand (d_h columns) within 512 TMEM columns.
-int n_tile_for(const Shape& s) {
-  const int cap = is_tf32(s) ? (512 - s.d_h) / 2 : kMaxNTile;
-  for (int nt = cap - cap % 32; nt >= 32; nt -= 32)
-    if (s.n_sub % nt == 0) return nt;
-  return 0;
-}
-
 int kt_of(int k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 64; }
 
-size_t smem_bytes(const Shape& s) {
-  const int nt = n_tile_for(s);
+size_t smem_for_tile(const Shape& s, int nt) {
   const int bk = is_tf32(s) ? 32 : 64;
   const int parts = is_tf32(s) ? 2 : 1;
   return 1024 + (size_t)(s.d_h / bk) * 16384 + (size_t)kStages * parts * nt * kRowBytes +
          (size_t)kt_of(s.k) * 256 * 4 + 256 * 4 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
 }
+
+// Largest N tile (<= 256, multiple of 32, dividing n_sub) whose stages fit
+// shared memory; TF32 also keeps 2 accumulators + the A_lo operand (d_h
+// columns) within 512 TMEM columns.
+int n_tile_for(const Shape& s) {
+  const int cap = is_tf32(s) ? (512 - s.d_h) / 2 : kMaxNTile;
+  for (int nt = cap - cap % 32; nt >= 32; nt -= 32)
+    if (s.n_sub % nt == 0 && smem_for_tile(s, nt) <= 227 * 1024) return nt;
+  return 0;
+}
+
+size_t smem_bytes(const Shape& s) { return smem_for_tile(s, n_tile_for(s)); }
 
 // K -> (K_hi, K_lo) for the 3xTF32 B operand, and ||k_i|| per sub-key row
 // (fp32 sum of squares, x 1.001 before a rounded-up sqrt: an upper bound),

@@ -46,7 +46,7 @@ def check_all(cfg, Q, K, V, dOut, res, backward=True):
 # ------------------------------------------------------------ small sweep --
 SWEEP = [
     # (B, H, n_sub, d_h, d_v, k, qk dtype, v dtype)
-    (1, 1, 16, 32, 32, 1, torch.float32, torch.float32),
+    (1, 1, 32, 32, 32, 1, torch.float32, torch.float32),
     (7, 3, 32, 32, 64, 5, torch.float32, torch.float32),
     (33, 2, 128, 64, 64, 8, torch.float32, torch.float32),
     (130, 4, 64, 32, 128, 17, torch.float32, torch.float32),
@@ -179,6 +179,54 @@ def test_full_size_invariants(name):
                      absmag=absq.reshape(-1, cfg.d_half))
     parity.row_close(dw[sel].cpu().numpy().reshape(-1, cfg.k), bw["dw"].reshape(-1, cfg.k),
                      parity.rtol_for(cfg.value_dtype), (~aff).reshape(-1), "dw (sampled)")
+
+
+def test_c3_full_size_vs_oracle_hot_rows():
+    """Full C3 (16,384 Zipf-clustered queries x 8 heads, the deterministic
+    fp32 backward) against the fp64 oracle run on the whole batch: selection,
+    out, dw, dQ, every dK row, and the dV rows of the 1,000 hottest slots
+    (up to thousands of contributions each: the long-run reducers) -- element
+    by element, none of them masked."""
+    from oracle import oracle as orc
+    cfg = wl.CONFIGS["c3_train_fp32_zipf"]
+    Q, K, V, dOut = wl.make_all(cfg, DEV)
+    lk = lookup_for(cfg)
+    out, idx, w = lk.forward(Q, K, V)
+    dq, dK, dV, dw = lk.backward(dOut, Q, K, V, idx, w)
+    torch.cuda.synchronize()
+    Qc, Kc, Vc = Q.cpu(), K.cpu(), V.cpu()
+    o = orc.forward(Qc, Kc, Vc, cfg.k)
+    aff, rep = parity.compare_selection(Qc, Kc, idx.cpu().numpy(), o, cfg.n_sub)
+    assert aff.sum() <= max(2, 0.01 * aff.size), rep
+    rows, hits = np.unique(o["idx"], return_counts=True)
+    hot = rows[np.argsort(-hits, kind="stable")[:1000]]
+    assert hits.max() > 500, "the Zipf workload is expected to have hot rows"
+    # hot rows touched by a tie-affected lookup (either selection) are skipped
+    bad = set()
+    for b, h in zip(*np.nonzero(aff)):
+        bad.update(o["idx"][b, h].tolist())
+        bad.update(idx[b, h].cpu().tolist())
+    hot = np.array([r for r in hot.tolist() if r not in bad], dtype=np.int64)
+    assert hot.size >= 990
+    bw = orc.backward(Qc, Kc, Vc, o["idx"], dOut.cpu(), rows=np.sort(hot))
+    rt = parity.rtol_for(cfg.value_dtype)
+    err_v = parity.row_close(dV[torch.from_numpy(np.sort(hot)).to(DEV)].cpu().numpy(), bw["dV"], rt,
+                             what="dV (1000 hottest rows)")
+    absq, absk = parity.grad_key_magnitudes(Qc, Kc, o, bw, cfg.n_sub)
+    ok = (~aff).reshape(-1)
+    err_q = parity.row_close(dq.cpu().numpy().reshape(-1, cfg.d_half), bw["dQ"].reshape(-1, cfg.d_half), rt,
+                             np.repeat(ok, 2), "dQ", absmag=absq.reshape(-1, cfg.d_half))
+    mask_k = np.ones(cfg.heads * 2 * cfg.n_sub, bool)
+    for b, h in zip(*np.nonzero(aff)):
+        for f in o["idx"][b, h].tolist() + idx[b, h].cpu().tolist():
+            mask_k[(h * 2) * cfg.n_sub + f // cfg.n_sub] = False
+            mask_k[(h * 2 + 1) * cfg.n_sub + f % cfg.n_sub] = False
+    err_k = parity.row_close(dK.cpu().numpy().reshape(-1, cfg.d_half), bw["dK"].reshape(-1, cfg.d_half), rt,
+                             mask_k, "dK", absmag=absk.reshape(-1, cfg.d_half))
+    err_w = parity.row_close(dw.cpu().numpy().reshape(-1, cfg.k), bw["dw"].reshape(-1, cfg.k), rt, ok, "dw")
+    err_o = parity.row_close(out.cpu().numpy(), o["out"], rt, ~aff.any(axis=1), "out")
+    print("C3 full:", rep, {"max_hits": int(hits.max()), "dV_hot": err_v, "dQ": err_q, "dK": err_k,
+                            "dw": err_w, "out": err_o})
 
 
 @pytest.mark.parametrize("name", ["f4_tokens_bf16", "f4_tokens_pertable_bf16"])
@@ -571,14 +619,14 @@ def test_sharded_phases_match_full():
 
 def test_backward_unsupported_width_is_reported():
     from paper_2602_07526_b200._lib import MsnError
-    cfg = wl.tiny_config(4, 1, 16, 16, 32, 2, torch.float32, torch.float32)
+    cfg = wl.tiny_config(4, 1, 32, 32, 48, 2, torch.float32, torch.float32)
     Q, K, V, dOut = wl.make_all(cfg, DEV)
     lk = lookup_for(cfg)
-    out, idx, w = lk.forward(Q, K, V)          # forward supports d_half % 16 == 0
+    out, idx, w = lk.forward(Q, K, V)          # the forward takes d_value * 4 % 16 == 0
     dV = torch.full((cfg.n_slots, cfg.d_value), 0.25, dtype=torch.float32, device=DEV)
     dK = torch.full((cfg.heads, 2, cfg.n_sub, cfg.d_half), 0.5, dtype=torch.float32, device=DEV)
     with pytest.raises(MsnError, match="UNSUPPORTED"):
-        lk.backward(dOut, Q, K, V, idx, w, d_subkeys=dK, d_values=dV)  # backward needs d_half % 32 == 0
+        lk.backward(dOut, Q, K, V, idx, w, d_subkeys=dK, d_values=dV)  # the reducers take 32 * 2^j
     torch.cuda.synchronize()
     # checked on the host before any launch: the accumulators are untouched
     assert torch.all(dV == 0.25) and torch.all(dK == 0.5)
