@@ -32,9 +32,9 @@ struct Shape {
 // cap = cand_cap(KT) (score bits, sub-key index) pairs holds, in no particular
 // order, a superset of the segment's top-k under (score desc, index asc):
 // entries [0, n0) and [cap - n1, cap) with n[r*SC + g] = n0 | n1 << 16 (the
-// two scorer threads of a row append from both ends).  n0 + n1 <= cap always:
-// a row whose bound let more columns through (massive exact ties) is rescored
-// exactly from the query and sub-keys in `rq` into [0, nn), n1 = 0.
+// tcgen05 scorer writes compact lists, n1 = 0).  n0 + n1 <= cap always: a row
+// whose bound let more columns through (massive exact ties) is rescored
+// exactly from the query and sub-keys in `rq` into [0, nn).
 __host__ __device__ constexpr int cand_cap(int kt) { return kt > 32 ? 128 : 64; }
 struct Rescore {
   const void* Q = nullptr;  // [B, H, 2, d_h] qk dtype

@@ -153,29 +153,43 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
   const uint32_t idesc = idesc_tf32(kPgM, NP < 16 ? 16 : NP);
   const int nkb = (g.K + 31) / 32;
   // staging: element e of a [rows x 32] tile; the source's contiguous
-  // dimension is the fastest over consecutive threads
+  // dimension is the fastest over consecutive threads.  All of a thread's
+  // loads are issued first (registers), then split and stored.
   auto stage_tile = [&](auto* src, int64_t rs, int64_t cs, int rows, int row0, int rmax, int k0, uint8_t* hi,
-                        uint8_t* lo) {
+                        uint8_t* lo, auto cnt) {
+    constexpr int NE = decltype(cnt)::value;  // elements per thread (rows * 32 / kPgThreads, max)
     const bool kfast = cs == 1;
-    for (int e = tid; e < rows * 32; e += kPgThreads) {
+    float x[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = tid + i * kPgThreads;
       const int r = kfast ? e / 32 : e % rows;
       const int kk = kfast ? e % 32 : e / rows;
       const int gr = row0 + r, gk = k0 + kk;
-      float x = 0.f;
-      if (gr < rmax && gk < g.K) x = elem<std::remove_cv_t<std::remove_pointer_t<decltype(src)>>>::to_f(
-                                         src[(int64_t)gr * rs + (int64_t)gk * cs]);
-      const float h = tf32_hi(x);
+      x[i] = 0.f;
+      if (e < rows * 32 && gr < rmax && gk < g.K)
+        x[i] = elem<std::remove_cv_t<std::remove_pointer_t<decltype(src)>>>::to_f(src[(int64_t)gr * rs + (int64_t)gk * cs]);
+    }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = tid + i * kPgThreads;
+      if (e >= rows * 32) break;
+      const int r = kfast ? e / 32 : e % rows;
+      const int kk = kfast ? e % 32 : e / rows;
+      const float h = tf32_hi(x[i]);
       const uint32_t o = sw128_off(r, kk);
       *reinterpret_cast<float*>(hi + o) = h;
-      *reinterpret_cast<float*>(lo + o) = x - h;
+      *reinterpret_cast<float*>(lo + o) = x[i] - h;
     }
   };
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;
     if (kb >= 2) mbar_wait(&empty[s], ((kb - 2) >> 1) & 1);
     uint8_t* st = base + s * stage;
-    stage_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, kb * 32, st, st + a_bytes);
-    stage_tile(B, g.b_cs, g.b_rs, NP, 0, g.N, kb * 32, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes);
+    stage_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, kb * 32, st, st + a_bytes,
+               std::integral_constant<int, kPgM * 32 / kPgThreads>{});
+    stage_tile(B, g.b_cs, g.b_rs, NP, 0, g.N, kb * 32, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes,
+               std::integral_constant<int, 256 * 32 / kPgThreads>{});
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {

@@ -30,7 +30,7 @@
 //           thread 1 from the top (no atomics).  The row's top-KT under
 //           (score desc, index asc) has scores >= tau, so the list contains
 //           it (ties with tau are kept).
-// For random scores ~1.3 KT columns pass.  A row with more than kCandCap = 64
+// For random scores ~1.3 KT columns pass.  A row with more than CAP (64; 128 for KT = 64)
 // passing columns (massive exact ties, adversarial data) is written with
 // is rescored exactly by its write-out warp (warp_sort.cuh, exact_half_topk)
 // -- correctness never depends on the bound being tight.
@@ -67,6 +67,7 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 constexpr int kStages = 3;
 constexpr int kMaxNTile = 256;
 // candidate slots per row list: cand_cap(KT) (kernels.h)
+constexpr int kCStride = 129;      // buffer entry (slot, row) at slot*129 + row: bank rotation
 constexpr int kRowBytes = 128;     // one 128-byte swizzle row per k-block (64 bf16 / 32 fp32)
 
 // In-register bitonic sort of N values, descending.
@@ -138,16 +139,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t alo_col = 2u * (uint32_t)p.n_tile;     // TF32: A_lo columns [2 n_tile, +d_h)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr int CAP = cand_cap(KT);
-  // carve: A (k_blocks x 16 KB) | B ring | tau exchange [KT][2][128] | ||q||^2
-  //        halves [2][128] | per-thread counts [2][128] | bars.  Pass B appends
-  //        the candidates straight to the row's list in global memory.
+  // carve: A (k_blocks x 16 KB) | B ring | candidates [CAP][129] (score bits,
+  //        column) | ||q||^2 halves [2][128] | per-thread counts [2][128] |
+  //        bars.  The tau exchange [KT][2][128] reuses the candidate area.
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
   const int stage_bytes = B_PARTS * p.n_tile * kRowBytes;
-  float* xch = reinterpret_cast<float*>(sB + kStages * stage_bytes);  // [KT][2][128] sorted group maxima
-  float* qn = xch + KT * 256;                                         // [2][128]
-  int* cnts = reinterpret_cast<int*>(qn + 256);                       // [2][128]
+  uint2* cand = reinterpret_cast<uint2*>(sB + kStages * stage_bytes);
+  float* xch = reinterpret_cast<float*>(cand);            // [KT][2][128] sorted group maxima
+  float* qn = reinterpret_cast<float*>(cand + CAP * kCStride);  // [2][128]
+  int* cnts = reinterpret_cast<int*>(qn + 256);                 // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(cnts + 256);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
@@ -409,29 +411,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     epi_bar();  // exchange read everywhere before the candidate area is written
     SEL_TS(3);
 
-    // ---- pass B: append every column >= tau to the row's list in global
-    // memory: thread 0 at slots 0, 1, ... ; thread 1 at slots CAP-1, CAP-2, ...
-    // (no atomics; the two meet only when the row overflows, and an
-    // overflowed row is rescored below).  Rows past B store nothing.
-    const int64_t my_b = m0 + row;
-    const int64_t my_grow = my_b * p.H * 2 + hh;
-    uint2* my_list = p.vc + (my_grow * p.SC + seg) * CAP;
-    const bool live = my_b < p.B;
-    uint64_t caddr = reinterpret_cast<uint64_t>(my_list + (sh == 0 ? 0 : CAP - 1));
-    const uint64_t step = sh == 0 ? 8ull : (uint64_t)(-8ll);
+    // ---- pass B: append every column >= tau to the row's buffer
+    // thread 0: slots 0, 1, ... ; thread 1: slots CAP-1, CAP-2, ...  (entry = slot*129 + row)
+    const uint32_t cbase = smem_u32(cand) + (uint32_t)row * 8u;
+    const uint32_t step = sh == 0 ? (uint32_t)(kCStride * 8) : (uint32_t)(-(kCStride * 8));
+    uint32_t caddr = cbase + (sh == 0 ? 0u : (uint32_t)((CAP - 1) * kCStride * 8));
     int cnt = 0;  // this thread's appended columns (may exceed its room: row overflow)
     auto filter32 = [&](const uint32_t (&r)[32], uint32_t col0) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) m |= (__uint_as_float(r[jj]) >= tau ? 1u : 0u) << jj;
-      if (!live) m = 0;
-      if (__any_sync(0xffffffffu, cnt + __popc(m) > CAP)) {
+      if (__any_sync(0xffffffffu, cnt > CAP - 32)) {
         // near the end of this thread's room: bounded stores, exact count
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
-          if ((m >> jj) & 1u) {
+          if (__uint_as_float(r[jj]) >= tau) {
             if (cnt < CAP) {
-              asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(caddr), "r"(r[jj]), "r"(col0 + jj)
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(caddr), "r"(r[jj]), "r"(col0 + jj)
                            : "memory");
               caddr += step;
             }
@@ -440,15 +433,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return;
       }
-      if (m == 0) return;
-      // four independent store chains (columns g*8 .. g*8+7), each starting at
-      // its prefix of the mask: no serial dependency across the 32 columns
-      uint64_t ca[4];
+#ifndef MSN_PASSB_CHAIN
+      // hit mask, then four independent store chains (columns g*8 .. g*8+7),
+      // each starting at its prefix of the mask: no serial dependency across
+      // the 32 columns
+      uint32_t m = 0;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) m |= (__uint_as_float(r[jj]) >= tau ? 1u : 0u) << jj;
+      uint32_t ca[4];
       ca[0] = caddr;
-      ca[1] = ca[0] + (uint64_t)__popc(m & 0xffu) * step;
-      ca[2] = ca[1] + (uint64_t)__popc(m & 0xff00u) * step;
-      ca[3] = ca[2] + (uint64_t)__popc(m & 0xff0000u) * step;
-      caddr = ca[3] + (uint64_t)__popc(m >> 24) * step;
+      ca[1] = ca[0] + (uint32_t)__popc(m & 0xffu) * step;
+      ca[2] = ca[1] + (uint32_t)__popc(m & 0xff00u) * step;
+      ca[3] = ca[2] + (uint32_t)__popc(m & 0xff0000u) * step;
+      caddr = ca[3] + (uint32_t)__popc(m >> 24) * step;
       cnt += __popc(m);
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj)
@@ -459,12 +456,28 @@ __global__ void __launch_bounds__(kThreads, 1)
               "{\n.reg .pred p;\n.reg .b32 t;\n"
               "and.b32 t, %1, %5;\n"
               "setp.ne.b32 p, t, 0;\n"
-              "@p st.global.v2.u32 [%0], {%2, %3};\n"
-              "@p add.u64 %0, %0, %4;\n}\n"
-              : "+l"(ca[g])
-              : "r"(m), "r"(r[col]), "r"(col0 + col), "l"(step), "r"(1u << col)
+              "@p st.shared.v2.u32 [%0], {%2, %3};\n"
+              "@p add.u32 %0, %0, %4;\n}\n"
+              : "+r"(ca[g])
+              : "r"(m), "r"(r[col]), "r"(col0 + col), "r"(step), "r"(1u << col)
               : "memory");
         }
+#else
+      const uint32_t a0 = caddr;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "setp.ge.f32 p, %1, %2;\n"
+            "@p st.shared.v2.u32 [%0], {%3, %4};\n"
+            "@p add.u32 %0, %0, %5;\n}\n"
+            : "+r"(caddr)
+            : "f"(__uint_as_float(r[jj])), "f"(tau), "r"(r[jj]), "r"(col0 + jj), "r"(step)
+            : "memory");
+      // appended = |caddr - a0| / (129*8)
+      const uint32_t moved = sh == 0 ? caddr - a0 : a0 - caddr;
+      cnt += (int)(moved / (uint32_t)(kCStride * 8));
+#endif
     };
     auto pass_b = [&](int g0, int seg_cols, int col_base) {
       for (int j0 = 64 * sh; j0 < seg_cols; j0 += 128) {
@@ -496,25 +509,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     epi_bar();
     SEL_TS(5);
 
-    // ---- counts: warp ew takes rows 16 ew .. 16 ew + 15 (lane rr and
-    // 16 + rr hold the two threads' counts of row rr); the list of a row is
-    // [0, n0) u [CAP - n1, CAP), packed as n0 | n1 << 16 into cn.  A row with
-    // n0 + n1 > CAP (massive exact ties: the two ends met) is rescored
-    // exactly by the warp into a fresh list [0, nn).
+    // ---- write-out: warp ew writes rows 16 ew .. 16 ew + 15, lane = slot;
+    // the 16 rows' counts come in with one shared load per lane
     const int r0 = ew * 16;
     const int cn_l = cnts[(lane >> 4) * 128 + r0 + (lane & 15)];
-    const int n0_l = __shfl_sync(0xffffffffu, cn_l, lane & 15);
-    const int n1_l = __shfl_sync(0xffffffffu, cn_l, 16 + (lane & 15));
-    {
-      const int64_t b = m0 + r0 + lane;
-      if (lane < 16 && b < p.B && n0_l + n1_l <= CAP)
-        p.cn[(b * p.H * 2 + hh) * p.SC + seg] = n0_l | (n1_l << 16);
+    bool any_ovf = false;
+#pragma unroll 4
+    for (int rr = 0; rr < 16; ++rr) {
+      const int trow = r0 + rr;
+      const int64_t b = m0 + trow;
+      const int n0 = __shfl_sync(0xffffffffu, cn_l, rr);
+      const int n = n0 + __shfl_sync(0xffffffffu, cn_l, 16 + rr);
+      if (b >= p.B) continue;
+      if (n > CAP) { any_ovf = true; continue; }
+      const int64_t grow = b * p.H * 2 + hh;
+      if (lane == 0) p.cn[grow * p.SC + seg] = n;
+      uint2* dst = p.vc + (grow * p.SC + seg) * CAP;
+#pragma unroll
+      for (int hf = 0; hf < CAP / 32; ++hf) {
+        const int i = hf * 32 + lane;
+        if (i < n) {
+          const int slot = i < n0 ? i : CAP - 1 - (i - n0);
+          dst[i] = cand[slot * kCStride + trow];
+        }
+      }
     }
-    const unsigned ovf = __ballot_sync(0xffffffffu, lane < 16 && m0 + r0 + lane < p.B && n0_l + n1_l > CAP);
-    if (ovf) {
+    if (any_ovf) {
+      // more than CAP columns passed tau (massive exact ties): exact
+      // rescoring of those rows by the warp, their best min(64, n_sub) sub-keys
       for (int rr = 0; rr < 16; ++rr) {
-        if (!((ovf >> rr) & 1u)) continue;
         const int64_t b = m0 + r0 + rr;
+        const int n = __shfl_sync(0xffffffffu, cn_l, rr) + __shfl_sync(0xffffffffu, cn_l, 16 + rr);
+        if (b >= p.B || n <= CAP) continue;
         const int64_t grow = b * p.H * 2 + hh;
         uint2* dst = p.vc + (grow * p.SC + seg) * CAP;
         const int nn = p.rq.qk_dt == F32
@@ -546,7 +572,7 @@ size_t smem_for_tile(const Shape& s, int nt) {
   const int bk = is_tf32(s) ? 32 : 64;
   const int parts = is_tf32(s) ? 2 : 1;
   return 1024 + (size_t)(s.d_h / bk) * 16384 + (size_t)kStages * parts * nt * kRowBytes +
-         (size_t)kt_of(s.k) * 256 * 4 + 256 * 4 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
+         (size_t)cand_cap(kt_of(s.k)) * kCStride * 8 + 256 * 4 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
 }
 
 // Largest N tile (<= 256, multiple of 32, dividing n_sub) whose stages fit
