@@ -141,7 +141,7 @@ msn_status check_tape(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx, 
 msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
                      const void* subkeys, int32_t* idx, float* weights, void* ws, size_t ws_bytes,
                      int* launches, const void* values = nullptr, float* out = nullptr,
-                     const Gate& gate = Gate{}) {
+                     const Gate& gate = Gate{}, bool per_lookup = false) {
   const Shape s = shape_of(h->cfg, B);
   msn_status st0 = check_select_shape(s);
   if (st0) return st0;
@@ -156,6 +156,12 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
   cudaError_t e = launch_select_tc(s, query, subkeys, cd, p, st, launches);
   if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half candidates)");
   if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);  // stage boundary: scoring done
+  if (values && per_lookup) {  // small batches: Cartesian + gather fused per lookup
+    if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);
+    e = launch_cartesian_gather_lookup(s, cd, idx, weights, values, out, st, launches);
+    if (e != cudaSuccess) return cuda_fail(e, "cartesian top-k + softmax + gather (per lookup)");
+    return MSN_OK;
+  }
   if (values && cd.S == 1) {
     if (h->ntrace > 1) cudaEventRecord(h->trace[1], st);  // (fused: no separate Cartesian stage)
     e = launch_cartesian_gather(s, cd, idx, weights, values, out, st, launches, gate);
@@ -378,6 +384,11 @@ static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* q
     return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
                      &h->last_launches, values, out, gate);
   }
+  // smaller batches: Cartesian + gather fused per lookup (8x the warps of
+  // the per-query kernel), unless a gate or head groups ask for the phases
+  if (!gate.kind && cartesian_gather_lookup_ok(shape_of(h->cfg, B)))
+    return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes, &h->last_launches,
+                     values, out, gate, true);
   if ((st = do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
                       &h->last_launches)))
     return st;

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   const int row_vecs = d_v / PER;
   for (int grp = 0; grp < og; ++grp) {
     float acc[VPL][PER];
-    gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * E, (grp + 1) * E, V, d_v, acc);
+    gather_rows_heads<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * (E / k), (grp + 1) * (E / k), k, V, d_v, acc);
     if (g == 0) {
       const int64_t orow = b * og + grp;
       float* o = out + orow * d_v;
@@ -360,6 +360,75 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
       if (gate.kind) store_gated<VPL, PER>(gate, orow, d_v, gl, row_vecs, acc);
     }
   }  // output groups
+}
+
+// a3 + a4 + a5 fused per LOOKUP (small batches, the latency regime): warp w
+// of a block runs the Cartesian stage of lookup l = 8 blockIdx + w, then
+// gathers its k value rows into a partial row (gather_rows); the block holds
+// 8 / H whole queries, whose H partials are added in head order -- the order
+// of gather_rows_heads, so the result is bitwise that of the phase calls.
+// Eight times the warps of the per-query kernel for the same batch (C5: 2048
+// instead of 512), so a small batch fills the GPU.  k <= 32, d_v <= 512,
+// H | 8, one output group, no gate.
+constexpr int kLkMaxDv = 512;
+template <int MAXC, int SEG, typename VT, int VPL, int G, int U>
+__global__ void __launch_bounds__(256) cartesian_gather_lookup_kernel(
+    const uint2* __restrict__ cand, const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
+    int32_t* __restrict__ idx, float* __restrict__ w, const VT* __restrict__ V, float* __restrict__ out, int d_v,
+    int SC) {
+  pdl_enter();
+  constexpr int PER = elem<VT>::per16;
+  constexpr int LG = 32 / G;
+  __shared__ CartSmem<32, MAXC> sm[kWarpsPerBlock];
+  __shared__ int32_t s_idx[kWarpsPerBlock][32];
+  __shared__ float s_w[kWarpsPerBlock][32];
+  __shared__ __align__(16) float part[kWarpsPerBlock][kLkMaxDv];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
+  const int64_t L = B * H;
+  if (l < L) {
+    cartesian_lookup<32, MAXC, 0, SEG>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, s_idx[wid], s_w[wid], 0, SC);
+    float p[VPL][PER];
+    gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], 0, k, V, d_v, p);
+    const int g = lane / LG, gl = lane % LG;
+    const int row_vecs = d_v / PER;
+    if (g == 0) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int vec = gl * VPL + v;
+        if (vec < row_vecs) {
+#pragma unroll
+          for (int e = 0; e < PER; e += 4)
+            *reinterpret_cast<float4*>(&part[wid][vec * PER + e]) = make_float4(p[v][e], p[v][e + 1], p[v][e + 2], p[v][e + 3]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // the block's queries: out[b] = ((0 + p_0) + p_1) + ... (head order)
+  const int qpb = kWarpsPerBlock / H;
+  const int64_t b0 = (int64_t)blockIdx.x * qpb;
+  for (int i = threadIdx.x; i < qpb * d_v; i += blockDim.x) {
+    const int q = i / d_v, e = i - q * d_v;
+    if (b0 + q >= B) break;
+    float t = 0.f;
+    for (int h = 0; h < H; ++h) t += part[q * H + h][e];
+    out[(b0 + q) * d_v + e] = t;
+  }
+}
+
+template <int SEG, typename VT>
+cudaError_t dispatch_lookup(const Shape& s, const Cands& cd, int32_t* idx, float* w, const VT* V, float* out,
+                            cudaStream_t st) {
+  const int R = s.d_v * (int)sizeof(VT) / 16;
+  const int64_t L = s.B * s.H;
+  const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
+#define LK(VPL, G, U)                                                                                        \
+  launch_pdl(cartesian_gather_lookup_kernel<119, SEG, VT, VPL, G, U>, blocks, 256, 0, st, cd.vc, cd.n, s.B, s.H, \
+             s.n_sub, s.k, idx, w, V, out, s.d_v, cd.SC)
+  MSN_GATHER_DISPATCH(R, LK);
+#undef LK
+  return cudaGetLastError();
 }
 
 // a3 + a4 + ROUTE + the local shard's a5 (the row-sharded table, a9): one
@@ -504,6 +573,27 @@ cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* id
     e = s.v_dt == F32 ? dispatch_fused<64, 280, float>(s, cd, idx, w, (const float*)V, out, st, gate)
                       : dispatch_fused<64, 280, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st, gate);
   }
+  if (e == cudaSuccess) ++*launches;
+  return e;
+}
+
+bool cartesian_gather_lookup_ok(const Shape& s) {
+  return s.k <= 32 && s.d_v <= kLkMaxDv && s.H <= kWarpsPerBlock && kWarpsPerBlock % s.H == 0 && s.og == 1 &&
+         s.tab_stride == 0 && s.row_begin == 0;
+}
+
+cudaError_t launch_cartesian_gather_lookup(const Shape& s, const Cands& cd, int32_t* idx, float* w, const void* V,
+                                          float* out, cudaStream_t st, int* launches) {
+  if (!cartesian_gather_lookup_ok(s) || cd.S > 2) return cudaErrorNotSupported;
+  if (s.B == 0) return cudaSuccess;
+  const bool bf = s.v_dt != F32;
+  cudaError_t e;
+  if (cd.S == 2)
+    e = bf ? dispatch_lookup<2, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st)
+           : dispatch_lookup<2, float>(s, cd, idx, w, (const float*)V, out, st);
+  else
+    e = bf ? dispatch_lookup<1, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st)
+           : dispatch_lookup<1, float>(s, cd, idx, w, (const float*)V, out, st);
   if (e == cudaSuccess) ++*launches;
   return e;
 }

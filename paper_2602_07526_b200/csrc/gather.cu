@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const int32_t* __restrict__
   const int hpg = H / og;  // heads per output group (og = 1: all)
   for (int grp = 0; grp < og; ++grp) {
     float tot[VPL][PER];
-    gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * hpg * k, (grp + 1) * hpg * k, V, d_v, tot);
+    gather_rows_heads<VT, VPL, G, U>(s_idx[wid], s_w[wid], grp * hpg, (grp + 1) * hpg, k, V, d_v, tot);
     if (g == 0) {
       const int64_t orow = b * og + grp;
       float* o = out + orow * d_v;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) gather_wide_kernel(const int32_t* __restr
                                                           const float* __restrict__ w,
                                                           const VT* __restrict__ V,
                                                           float* __restrict__ out, int64_t B, int HK,
-                                                          int d_v, int wpq, int og, Gate gate) {
+                                                          int d_v, int wpq, int og, Gate gate, int k) {
   pdl_enter();
   constexpr int PER = elem<VT>::per16;
   __shared__ int32_t s_idx[kWarps][kMaxHK];
@@ -97,23 +97,32 @@ __global__ void __launch_bounds__(256) gather_wide_kernel(const int32_t* __restr
     float acc[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-    for (int base = grp * E; base < (grp + 1) * E; base += U) {
-      uint4 x[U];
-      float wt[U];
+    // per head: the k rows into a partial, partials added in head order
+    // (gather_rows_heads' order, gather_rows.cuh)
+    for (int h0 = grp * E; h0 < (grp + 1) * E; h0 += k) {
+      float part[PER];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int r = base + u;
-        const int f = r < (grp + 1) * E ? s_idx[wid][r] : -1;
-        wt[u] = f >= 0 ? s_w[wid][r] : 0.f;
-        x[u] = f >= 0 ? ldg_nc_v4(V + (int64_t)f * d_v + vec * PER) : make_uint4(0, 0, 0, 0);
+      for (int e = 0; e < PER; ++e) part[e] = 0.f;
+      for (int base = h0; base < h0 + k; base += U) {
+        uint4 x[U];
+        float wt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = base + u;
+          const int f = r < h0 + k ? s_idx[wid][r] : -1;
+          wt[u] = f >= 0 ? s_w[wid][r] : 0.f;
+          x[u] = f >= 0 ? ldg_nc_v4(V + (int64_t)f * d_v + vec * PER) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float f[PER];
+          unpack16<VT>(x[u], f);
+#pragma unroll
+          for (int e = 0; e < PER; ++e) part[e] = fmaf(wt[u], f[e], part[e]);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        float f[PER];
-        unpack16<VT>(x[u], f);
-#pragma unroll
-        for (int e = 0; e < PER; ++e) acc[e] = fmaf(wt[u], f[e], acc[e]);
-      }
+      for (int e = 0; e < PER; ++e) acc[e] += part[e];
     }
     const int64_t orow = b * og + grp;
     float* o = out + orow * d_v + vec * PER;
@@ -140,7 +149,7 @@ cudaError_t dispatch(const Shape& s, const int32_t* idx, const float* w, const V
       s.row_end >= (int64_t)s.n_sub * s.n_sub * (s.tab_stride ? s.og : 1)) {
     const int wpq = R / 32, qpb = kWarps / wpq;
     launch_pdl(gather_wide_kernel<VT, 16>, (unsigned)((s.B + qpb - 1) / qpb), 256, 0, st, idx, w, V, out, s.B,
-               s.H * s.k, s.d_v, wpq, s.og, gate);
+               s.H * s.k, s.d_v, wpq, s.og, gate, s.k);
     return cudaGetLastError();
   }
   const unsigned blocks = (unsigned)((s.B + kWarps - 1) / kWarps);

@@ -2,9 +2,8 @@
 // PAPER.md:226-229) in a fixed order (reading R18): lane group g (of G) takes
 // rows r0+g, r0+g+G, ... in ascending order, U rows in flight, an fp32 FMA
 // chain per group, then the G group sums are combined by an xor tree.
-// gather_kernel runs it over all H*k rows of a query (output group); the
-// fused Cartesian + gather kernel over one head's k rows, the per-head
-// partials then added in head order.
+// gather_rows_heads runs it over each head's k rows and adds the per-head
+// partials in head order.
 #pragma once
 #include "common.cuh"
 
@@ -58,6 +57,30 @@ __device__ __forceinline__ void gather_rows(const int32_t* s_idx, const float* s
     for (int v = 0; v < VPL; ++v)
 #pragma unroll
       for (int e = 0; e < PER; ++e) acc[v][e] += __shfl_xor_sync(0xffffffffu, acc[v][e], m);
+}
+
+// The same sum organised by head (reading R18): the k rows of each head h in
+// [h0, h1) into a partial, the partials added in ascending head order.  Every
+// gather of the unsharded path uses this order -- per query (gather_kernel,
+// gather_wide_kernel, cartesian_gather_kernel) or per lookup and then per
+// query (cartesian_gather_lookup_kernel) -- so they agree bitwise.
+template <typename VT, int VPL, int G, int U>
+__device__ __forceinline__ void gather_rows_heads(const int32_t* s_idx, const float* s_w, int h0, int h1, int k,
+                                                  const VT* __restrict__ V, int d_v,
+                                                  float (&acc)[VPL][elem<VT>::per16]) {
+  constexpr int PER = elem<VT>::per16;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v)
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[v][e] = 0.f;
+  for (int h = h0; h < h1; ++h) {
+    float p[VPL][PER];
+    gather_rows<VT, VPL, G, U>(s_idx, s_w, h * k, (h + 1) * k, V, d_v, p);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[v][e] += p[v][e];
+  }
 }
 
 // (VPL, G, U) per row width R = d_v * sizeof(V) / 16 vectors (R <= 128).

@@ -86,6 +86,12 @@ cudaError_t launch_cartesian_gather(const Shape& s, const Cands& cd, int32_t* id
                                     const void* V, float* out, cudaStream_t st, int* launches,
                                     const Gate& gate = Gate{});
 
+// a2 (ordering) + a3 + a4 + a5 fused per lookup (small batches): one warp per
+// lookup, the block's H partials added per query in head order.
+bool cartesian_gather_lookup_ok(const Shape& s);
+cudaError_t launch_cartesian_gather_lookup(const Shape& s, const Cands& cd, int32_t* idx, float* w, const void* V,
+                                          float* out, cudaStream_t st, int* launches);
+
 // a5: out[b] = sum over local rows of w * V[idx - row_begin] (=).
 cudaError_t launch_gather(const Shape& s, const int32_t* idx, const float* w, const void* V,
                           float* out, cudaStream_t st, int* launches, const Gate& gate = Gate{});

@@ -140,16 +140,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr int CAP = cand_cap(KT);
   // carve: A (k_blocks x 16 KB) | B ring | candidates [CAP][129] (score bits,
-  //        column) | ||q||^2 halves [2][128] | per-thread counts [2][128] |
-  //        bars.  The tau exchange [KT][2][128] reuses the candidate area.
+  //        column) | per-thread counts [2][128] | bars.  The tau exchange
+  //        [KT][2][128] and ||q||^2 reuse the candidate area.
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* sA = smem_raw + pad;
   uint8_t* sB = sA + p.k_blocks * 16384;
   const int stage_bytes = B_PARTS * p.n_tile * kRowBytes;
   uint2* cand = reinterpret_cast<uint2*>(sB + kStages * stage_bytes);
   float* xch = reinterpret_cast<float*>(cand);            // [KT][2][128] sorted group maxima
-  float* qn = reinterpret_cast<float*>(cand + CAP * kCStride);  // [2][128]
-  int* cnts = reinterpret_cast<int*>(qn + 256);                 // [2][128]
+  // ||q||^2 halves: the last 1 KB of the candidate area (written before pass A,
+  // read at tau, before pass B fills the buffer; the tau exchange at its start
+  // is at most KT KB < the area - 1 KB)
+  float* qn = reinterpret_cast<float*>(cand + CAP * kCStride) - 256;  // [2][128]
+  int* cnts = reinterpret_cast<int*>(cand + CAP * kCStride);          // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(cnts + 256);
   uint64_t* a_full = bars;
   uint64_t* full = bars + 1;
@@ -572,7 +575,7 @@ size_t smem_for_tile(const Shape& s, int nt) {
   const int bk = is_tf32(s) ? 32 : 64;
   const int parts = is_tf32(s) ? 2 : 1;
   return 1024 + (size_t)(s.d_h / bk) * 16384 + (size_t)kStages * parts * nt * kRowBytes +
-         (size_t)cand_cap(kt_of(s.k)) * kCStride * 8 + 256 * 4 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
+         (size_t)cand_cap(kt_of(s.k)) * kCStride * 8 + 256 * 4 + 8 * (1 + 2 * kStages + 5) + 16;
 }
 
 // Largest N tile (<= 256, multiple of 32, dividing n_sub) whose stages fit

@@ -199,15 +199,16 @@ def test_c3_full_size_vs_oracle_hot_rows():
     aff, rep = parity.compare_selection(Qc, Kc, idx.cpu().numpy(), o, cfg.n_sub)
     assert aff.sum() <= max(2, 0.01 * aff.size), rep
     rows, hits = np.unique(o["idx"], return_counts=True)
-    hot = rows[np.argsort(-hits, kind="stable")[:1000]]
-    assert hits.max() > 500, "the Zipf workload is expected to have hot rows"
-    # hot rows touched by a tie-affected lookup (either selection) are skipped
+    order = np.argsort(-hits, kind="stable")
+    # the 1,000 hottest rows no tie-affected lookup touches (either selection:
+    # their expected values would need the CUDA path's selection)
     bad = set()
     for b, h in zip(*np.nonzero(aff)):
         bad.update(o["idx"][b, h].tolist())
         bad.update(idx[b, h].cpu().tolist())
-    hot = np.array([r for r in hot.tolist() if r not in bad], dtype=np.int64)
-    assert hot.size >= 990
+    hot_i = [i for i in order.tolist() if int(rows[i]) not in bad][:1000]
+    hot = rows[hot_i].astype(np.int64)
+    assert hits[hot_i[0]] > 500 and hits[hot_i[-1]] >= 20, "the Zipf workload is expected to have hot rows"
     bw = orc.backward(Qc, Kc, Vc, o["idx"], dOut.cpu(), rows=np.sort(hot))
     rt = parity.rtol_for(cfg.value_dtype)
     err_v = parity.row_close(dV[torch.from_numpy(np.sort(hot)).to(DEV)].cpu().numpy(), bw["dV"], rt,
@@ -225,7 +226,7 @@ def test_c3_full_size_vs_oracle_hot_rows():
                              mask_k, "dK", absmag=absk.reshape(-1, cfg.d_half))
     err_w = parity.row_close(dw.cpu().numpy().reshape(-1, cfg.k), bw["dw"].reshape(-1, cfg.k), rt, ok, "dw")
     err_o = parity.row_close(out.cpu().numpy(), o["out"], rt, ~aff.any(axis=1), "out")
-    print("C3 full:", rep, {"max_hits": int(hits.max()), "dV_hot": err_v, "dQ": err_q, "dK": err_k,
+    print("C3 full:", rep, {"max_hits": int(hits.max()), "hot_hits_min": int(hits[hot_i[-1]]), "dV_hot": err_v, "dQ": err_q, "dK": err_k,
                             "dw": err_w, "out": err_o})
 
 
