@@ -209,9 +209,12 @@ def test_c3_full_size_vs_oracle_hot_rows():
     hot_i = [i for i in order.tolist() if int(rows[i]) not in bad][:1000]
     hot = rows[hot_i].astype(np.int64)
     assert hits[hot_i[0]] > 500 and hits[hot_i[-1]] >= 20, "the Zipf workload is expected to have hot rows"
-    bw = orc.backward(Qc, Kc, Vc, o["idx"], dOut.cpu(), rows=np.sort(hot))
+    bw = orc.backward(Qc, Kc, Vc, o["idx"], dOut.cpu(), want_dense_dv=False)  # dV over the touched rows
     rt = parity.rtol_for(cfg.value_dtype)
-    err_v = parity.row_close(dV[torch.from_numpy(np.sort(hot)).to(DEV)].cpu().numpy(), bw["dV"], rt,
+    hs = np.sort(hot)
+    pos = np.searchsorted(bw["rows"], hs)
+    assert np.array_equal(bw["rows"][pos], hs)
+    err_v = parity.row_close(dV[torch.from_numpy(hs).to(DEV)].cpu().numpy(), bw["dV"][pos], rt,
                              what="dV (1000 hottest rows)")
     absq, absk = parity.grad_key_magnitudes(Qc, Kc, o, bw, cfg.n_sub)
     ok = (~aff).reshape(-1)
