@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) ln_backward_kernel(const T* __restrict__ 
 // A(m, k) = A[z a_bs + m a_rs + k a_cs] and B(n, k) = B[z b_bs + k b_rs + n b_cs]
 // (any layout: the operands are staged by the threads, which walk the source's
 // contiguous dimension), C[z c_bs + m c_rs + n].  One CTA per (128-row tile,
-// batch); N (<= 256, % 16) in one TMEM accumulator; K in blocks of 32: every
+// 64-column tile, batch), the tile in one TMEM accumulator; K in blocks of 32: every
 // element is split x = hi + lo (hi = the TF32 value, lo exact in fp32) into
 // two 128-byte-swizzled K-major tiles of each operand, and one elected thread
 // issues D += Ahi.Bhi + Ahi.Blo + Alo.Bhi per 8-element step (the lo.lo term
@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(256) ln_backward_kernel(const T* __restrict__ 
 // while the tensor cores run kb (tcgen05.commit frees a stage).
 constexpr int kPgThreads = 256;
 constexpr int kPgM = 128;
+constexpr int kPgN = 64;  // columns per CTA (C tiles of 128 x 64: 4x the CTAs of whole rows)
 struct PgArgs {
   int M, N, K;
   const void* A;
@@ -121,18 +122,19 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* base = smem_raw + pad;
-  const int NP = (g.N + 7) & ~7;                 // B rows staged (multiple of 8: whole swizzle atoms)
+  const int n0 = blockIdx.y * kPgN;
+  const int NT = g.N - n0 < kPgN ? g.N - n0 : kPgN;  // this CTA's columns (multiple of 16)
+  const int NP = kPgN;                           // B rows staged (whole swizzle atoms; zeros past N)
   const int a_bytes = kPgM * 128, b_bytes = NP * 128;
   const int stage = 2 * a_bytes + 2 * b_bytes;   // A_hi, A_lo, B_hi, B_lo
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * stage);
   uint64_t* empty = bars;                        // [2]
   uint64_t* done = bars + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
-  uint32_t tcols = 32;
-  while ((int)tcols < g.N) tcols <<= 1;
+  const uint32_t tcols = kPgN;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int m0 = blockIdx.x * kPgM;
-  const int64_t z = blockIdx.y;
+  const int64_t z = blockIdx.z;
   const TA* A = reinterpret_cast<const TA*>(g.A) + z * g.a_bs;
   const TB* B = reinterpret_cast<const TB*>(g.B) + z * g.b_bs;
   if (tid == 0) {
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t idesc = idesc_tf32(kPgM, NP < 16 ? 16 : NP);
+  const uint32_t idesc = idesc_tf32(kPgM, NP);
   const int nkb = (g.K + 31) / 32;
   // staging: element e of a [rows x 32] tile; the source's contiguous
   // dimension is the fastest over consecutive threads.  All of a thread's
@@ -188,8 +190,8 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
     uint8_t* st = base + s * stage;
     stage_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, kb * 32, st, st + a_bytes,
                std::integral_constant<int, kPgM * 32 / kPgThreads>{});
-    stage_tile(B, g.b_cs, g.b_rs, NP, 0, g.N, kb * 32, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes,
-               std::integral_constant<int, 256 * 32 / kPgThreads>{});
+    stage_tile(B, g.b_cs, g.b_rs, NP, n0, g.N, kb * 32, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes,
+               std::integral_constant<int, kPgN * 32 / kPgThreads>{});
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
@@ -209,21 +211,33 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
   if (nkb > 0) mbar_wait(done, 0);
   tc_fence_after();
   // epilogue: warp w reads TMEM lane quarter w % 4 (rows), column half w / 4
+  // (32 columns each); 4 consecutive columns per vector access
   {
     const int q = warp & 3, ch = warp >> 2;
     const int row = m0 + q * 32 + lane;
-    const int half = ((g.N + 63) / 64) * 32;  // columns per warp group, multiple of 32
-    TC* C = reinterpret_cast<TC*>(g.C) + z * g.c_bs + (int64_t)row * g.c_rs;
-    for (int c0 = ch * half; c0 < g.N && c0 < (ch + 1) * half; c0 += 32) {
+    const int c0 = ch * 32;
+    if (c0 < NT) {
       uint32_t r[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
       if (row < g.M) {
+        TC* C = reinterpret_cast<TC*>(g.C) + z * g.c_bs + (int64_t)row * g.c_rs + n0 + c0;
+        const int nc = NT - c0 < 32 ? NT - c0 : 32;  // 16 or 32
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (c0 + j >= g.N) break;
-          float v = nkb > 0 ? __uint_as_float(r[j]) : 0.f;
-          if (g.accumulate) v += ld_f(C + c0 + j);
-          st_f(C + c0 + j, v);
+        for (int j = 0; j < 32; j += 4) {
+          if (j >= nc) break;
+          float v[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            v[t] = nkb > 0 ? __uint_as_float(r[j + t]) : 0.f;
+            if (g.accumulate) v[t] += ld_f(C + j + t);
+          }
+          if constexpr (sizeof(TC) == 4) {
+            *reinterpret_cast<float4*>(C + j) = make_float4(v[0], v[1], v[2], v[3]);
+          } else {
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+            *reinterpret_cast<uint2*>(C + j) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+          }
         }
       }
     }
@@ -236,22 +250,19 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
   }
 }
 
-size_t pgemm_smem(int N) {
-  const int NP = (N + 7) & ~7;
-  return 1024 + 2 * (2 * kPgM * 128 + 2 * NP * 128) + 64;
-}
+size_t pgemm_smem() { return 1024 + 2 * (2 * kPgM * 128 + 2 * kPgN * 128) + 64; }
 
 template <typename TA, typename TB, typename TC>
 cudaError_t pgemm(int batch, int M, int N, int K, const TA* A, int64_t a_rs, int64_t a_cs, int64_t a_bs,
                   const TB* B, int64_t b_rs, int64_t b_cs, int64_t b_bs, TC* C, int64_t c_rs, int64_t c_bs,
                   int accumulate, cudaStream_t st) {
-  if (N > 256 || N % 16) return cudaErrorNotSupported;
+  if (N % 32 || (N > kPgN && N % kPgN)) return cudaErrorNotSupported;
   static std::atomic<uint64_t> attr{0};
   cudaError_t e = smem_attr_once(attr, pgemm_kernel<TA, TB, TC>, 227 * 1024);
   if (e != cudaSuccess) return e;
   PgArgs g{M, N, K, A, a_rs, a_cs, a_bs, B, b_rs, b_cs, b_bs, C, c_rs, c_bs, accumulate};
-  dim3 grid((M + kPgM - 1) / kPgM, batch);
-  return launch_pdl(pgemm_kernel<TA, TB, TC>, grid, kPgThreads, pgemm_smem(N), st, g);
+  dim3 grid((M + kPgM - 1) / kPgM, (N + kPgN - 1) / kPgN, batch);
+  return launch_pdl(pgemm_kernel<TA, TB, TC>, grid, kPgThreads, pgemm_smem(), st, g);
 }
 
 template <typename T>

@@ -15,7 +15,12 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "rege
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(r for r in rows if r and r[0] == "Address")
 ai, si, ni = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
-body = [r for r in rows[rows.index(hdr) + 1:] if len(r) == len(hdr)]
+body = []  # the first matching kernel's instructions (up to the next kernel's header)
+for r in rows[rows.index(hdr) + 1:]:
+    if r and r[0] in ("Address", "Kernel Name"):
+        break
+    if len(r) == len(hdr):
+        body.append(r)
 tot = sum(int(r[ni]) for r in body)
 print(f"{len(body)} instructions, {tot} samples")
 ranked = sorted(enumerate(body), key=lambda x: -int(x[1][ni]))[:top]
