@@ -155,13 +155,13 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
   const uint32_t idesc = idesc_tf32(kPgM, NP);
   const int nkb = (g.K + 31) / 32;
   // staging: element e of a [rows x 32] tile; the source's contiguous
-  // dimension is the fastest over consecutive threads.  All of a thread's
-  // loads are issued first (registers), then split and stored.
-  auto stage_tile = [&](auto* src, int64_t rs, int64_t cs, int rows, int row0, int rmax, int k0, uint8_t* hi,
-                        uint8_t* lo, auto cnt) {
-    constexpr int NE = decltype(cnt)::value;  // elements per thread (rows * 32 / kPgThreads, max)
+  // dimension is the fastest over consecutive threads.  The global loads of
+  // k-block kb + 1 are issued (into registers) right after k-block kb is
+  // stored, so they overlap kb's barrier, MMA and the wait for a free stage.
+  constexpr int NA = kPgM * 32 / kPgThreads, NB = kPgN * 32 / kPgThreads;
+  auto load_tile = [&](auto* src, int64_t rs, int64_t cs, int rows, int row0, int rmax, int k0, auto& x) {
+    constexpr int NE = sizeof(x) / sizeof(float);
     const bool kfast = cs == 1;
-    float x[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       const int e = tid + i * kPgThreads;
@@ -169,13 +169,16 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
       const int kk = kfast ? e % 32 : e / rows;
       const int gr = row0 + r, gk = k0 + kk;
       x[i] = 0.f;
-      if (e < rows * 32 && gr < rmax && gk < g.K)
+      if (gr < rmax && gk < g.K)
         x[i] = elem<std::remove_cv_t<std::remove_pointer_t<decltype(src)>>>::to_f(src[(int64_t)gr * rs + (int64_t)gk * cs]);
     }
+  };
+  auto store_tile = [&](int64_t cs, int rows, uint8_t* hi, uint8_t* lo, const auto& x) {
+    constexpr int NE = sizeof(x) / sizeof(float);
+    const bool kfast = cs == 1;
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       const int e = tid + i * kPgThreads;
-      if (e >= rows * 32) break;
       const int r = kfast ? e / 32 : e % rows;
       const int kk = kfast ? e % 32 : e / rows;
       const float h = tf32_hi(x[i]);
@@ -184,14 +187,21 @@ __global__ void __launch_bounds__(kPgThreads, 1) pgemm_kernel(PgArgs g) {
       *reinterpret_cast<float*>(lo + o) = x[i] - h;
     }
   };
+  float xa[NA], xb[NB];
+  if (nkb > 0) {
+    load_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, 0, xa);
+    load_tile(B, g.b_cs, g.b_rs, NP, n0, g.N, 0, xb);
+  }
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;
     if (kb >= 2) mbar_wait(&empty[s], ((kb - 2) >> 1) & 1);
     uint8_t* st = base + s * stage;
-    stage_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, kb * 32, st, st + a_bytes,
-               std::integral_constant<int, kPgM * 32 / kPgThreads>{});
-    stage_tile(B, g.b_cs, g.b_rs, NP, n0, g.N, kb * 32, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes,
-               std::integral_constant<int, kPgN * 32 / kPgThreads>{});
+    store_tile(g.a_cs, kPgM, st, st + a_bytes, xa);
+    store_tile(g.b_rs, NP, st + 2 * a_bytes, st + 2 * a_bytes + b_bytes, xb);
+    if (kb + 1 < nkb) {
+      load_tile(A, g.a_rs, g.a_cs, kPgM, m0, g.M, (kb + 1) * 32, xa);
+      load_tile(B, g.b_cs, g.b_rs, NP, n0, g.N, (kb + 1) * 32, xb);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
