@@ -890,7 +890,8 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
                                                     uint32_t* __restrict__ cnt,
                                                     uint32_t* __restrict__ rank,
                                                     uint16_t* __restrict__ dSd, int hg,
-                                                    int32_t tab_stride, bool dq_bf16) {
+                                                    int32_t tab_stride, bool dq_bf16, int tile_rows = 0,
+                                                    int ntiles = 0) {
   pdl_enter();
   constexpr int DQ_U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
   constexpr bool DENSE = OUT == OUT_DENSE;
@@ -1004,10 +1005,32 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
       __syncwarp();
     }
     if constexpr (OUT == OUT_COMPACT) {
+      // the m records sorted by sub-key (rank = number of smaller indices;
+      // the indices are distinct), and per dK tile of tile_rows sub-keys the
+      // offset of its first record: tile t's records are [off[t], off[t+1]),
+      // so the dK tile builder reads only its own (dk_tc.cu)
       uint2* rec = reinterpret_cast<uint2*>(dSd) + (l * 2 + half) * (int64_t)k;
-      for (int c = lane; c < k; c += 32)
-        rec[c] = c < m ? make_uint2((uint32_t)s_r[wid][half][c], __float_as_uint(s_d[wid][half][c]))
-                       : make_uint2(0xffffffffu, 0u);
+      uint8_t* off = reinterpret_cast<uint8_t*>(reinterpret_cast<uint2*>(dSd) + (int64_t)L * 2 * k) +
+                     (l * 2 + half) * 32;
+      for (int c = lane; c < k; c += 32) {
+        if (c < m) {
+          const int32_t r = s_r[wid][half][c];
+          int rk = 0;
+          for (int j = 0; j < m; ++j) rk += s_r[wid][half][j] < r;
+          rec[rk] = make_uint2((uint32_t)r, __float_as_uint(s_d[wid][half][c]));
+        } else {
+          rec[c] = make_uint2(0xffffffffu, 0u);
+        }
+      }
+      int below = 0;  // lane t: records with sub-key < t tile_rows
+      for (int c = 0; c < m; c += 32) {
+        const int idx0 = c + lane < m ? s_r[wid][half][c + lane] : 0x7fffffff;
+        for (int t = 0; t <= ntiles; ++t) {
+          const int n = __popc(__ballot_sync(0xffffffffu, idx0 < t * tile_rows));
+          if (lane == t) below += n;
+        }
+      }
+      if (lane <= ntiles) off[lane] = (uint8_t)below;
     }
   }
   if constexpr (!DQ) return;  // dQ = dSd . K runs on the tensor cores (dk_tc.cu)
@@ -1306,15 +1329,16 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   if (dense && dq_tc)                                                                          \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_DENSE, false>, blocks, 256, 0, st,                        \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16);                 \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16, 0, 0);           \
   else if (dense)                                                                              \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_COMPACT, true>, blocks, 256, 0, st,                       \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16);                 \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16,        \
+        dk_tile_rows(s), s.n_sub / dk_tile_rows(s));                                             \
   else                                                                                         \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_GROUP, true>, blocks, 256, 0, st,                         \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
-        g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16)
+        g.cnt, g.rank, nullptr, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16, 0, 0)
 #define DSDQ_E(QT, KPL)                                                                        \
   switch (E) { case 1: DSDQ(QT, KPL, 1); break; case 2: DSDQ(QT, KPL, 2); break;              \
     case 4: DSDQ(QT, KPL, 4); break; case 8: DSDQ(QT, KPL, 8); break;                          \

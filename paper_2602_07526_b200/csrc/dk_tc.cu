@@ -67,12 +67,14 @@ constexpr uint32_t idesc_bf16_mn(int M, int N) {
 
 // REC: the A tiles (dS^T of the k-block's 64 queries over the CTA's MT x 128
 // sub-keys) are built in shared memory from the compact records of
-// ds_dq_kernel (p.rec: k slots {sub-key, dS} per (query, head, half)) by the
-// epilogue warps, which are idle until the last k-block: zero the stage,
-// named barrier, one bf16 store per record in range at its 128-byte-swizzle
-// position (the layout TMA would produce), fence.proxy.async, arrive.  No
-// dense dS matrix in HBM; TMA then loads only the Q tiles.
-template <int MT, bool REC, int RP = 8>
+// ds_dq_kernel (p.rec: per (query, head, half) the records {sub-key, dS}
+// sorted by sub-key, and per tile the offset of its first record) by the
+// epilogue warps, which are idle until the last k-block: each query's row is
+// cleared by its 4 threads, then its records in this tile are stored (one
+// bf16 each) at their 128-byte-swizzle positions (the layout TMA would
+// produce), fence.proxy.async, arrive.  No dense dS matrix in HBM; TMA loads
+// only the Q tiles.
+template <int MT, bool REC>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     dk_gemm_kernel(const __grid_constant__ CUtensorMap tmap_ds,
                    const __grid_constant__ CUtensorMap tmap_q, const DkParams p) {
@@ -162,97 +164,81 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const int u = threadIdx.x - 64;
       const int ql = u >> 2, part = u & 3;
       const int HH = 2 * p.H;
-      constexpr int kRecMax = RP;  // record slots per thread: k <= 4 RP
-      const int per = (p.k + 3) / 4;
-      uint2 nxt[kRecMax];
-      auto rec_ptr = [&](int kb) -> const uint2* {
-        const int64_t b = q0 + (int64_t)kb * kBK + ql;
-        return p.rec + (b * HH + hh) * (int64_t)p.k;
-      };
-      auto load_kb = [&](int kb) {
-        const int64_t b = q0 + (int64_t)kb * kBK + ql;
-        const uint2* r = rec_ptr(kb);
-#pragma unroll
-        for (int c = 0; c < kRecMax; ++c) {
-          const int slot = part + 4 * c;
-          nxt[c] = (c < per && slot < p.k && b < q1) ? r[slot] : make_uint2(0xffffffffu, 0u);
+      constexpr int kNr = 4;  // records per thread held one k-block ahead (more: loaded when used)
+      const int64_t nlh = p.B * HH;  // lookup-halves (the per-tile offsets follow the records)
+      const uint8_t* offs = reinterpret_cast<const uint8_t*>(p.rec + nlh * p.k);
+      const int tile = blockIdx.x;   // this CTA's sub-key tile (kBM * MT rows)
+      auto lh_of = [&](int kb) -> int64_t { return (q0 + (int64_t)kb * kBK + ql) * HH + hh; };
+      // the records of query ql in this tile are [lo, hi) of its sorted list
+      // (per-tile offsets written by ds_dq_kernel); the 4 threads of the query
+      // take every 4th.  Offsets run two k-blocks ahead, records one.
+      auto load_off = [&](int kb, int& lo, int& hi) {
+        lo = hi = 0;
+        if (kb < nkb && q0 + (int64_t)kb * kBK + ql < q1) {
+          const uint16_t two = *reinterpret_cast<const uint16_t*>(offs + lh_of(kb) * 32 + (tile & ~1));
+          lo = (tile & 1) ? two >> 8 : two & 0xff;
+          hi = (tile & 1) ? offs[lh_of(kb) * 32 + tile + 1] : two >> 8;
         }
       };
-      // the records of k-block kb + kPre are pulled into L2 now, so that the
-      // register load one k-block ahead hits L2 (the k-block budget is one
-      // MMA of ~0.7 us; an HBM miss would not fit in it)
-      constexpr int kPre = 3;
+      auto load_rec = [&](int kb, int lo, int hi, uint2 (&x)[kNr]) {
+        const uint2* r = p.rec + lh_of(kb < nkb ? kb : 0) * p.k;
+#pragma unroll
+        for (int c = 0; c < kNr; ++c) {
+          const int j = lo + part + 4 * c;
+          x[c] = j < hi ? r[j] : make_uint2(0xffffffffu, 0u);
+        }
+      };
+      // offsets and records of k-block kb + kPre into L2 now
+      constexpr int kPre = 4;
       auto prefetch_kb = [&](int kb) {
-        if (kb < nkb && (part & 1) == 0 && q0 + (int64_t)kb * kBK + ql < q1) {
-          const char* a = reinterpret_cast<const char*>(rec_ptr(kb)) + (part >> 1) * 128;
-          if ((part >> 1) * 128 < p.k * 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        if (kb < nkb && part < 2 && q0 + (int64_t)kb * kBK + ql < q1) {
+          const char* a = part == 0 ? reinterpret_cast<const char*>(offs + lh_of(kb) * 32)
+                                    : reinterpret_cast<const char*>(p.rec + lh_of(kb) * p.k);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
         }
       };
-      // every stage starts zeroed; afterwards a thread only clears the
-      // entries it wrote into that stage kStg k-blocks earlier.  The position
-      // (query ql, sub-key) of an entry is written only by the 4 threads of
-      // query ql -- lanes of one warp -- so a __syncwarp between the clears
-      // and the new stores orders them (no CTA barrier, no full zeroing).
-      for (int i = u; i < kStg * MT * 2 * kAtom / 16; i += 256)
-        reinterpret_cast<uint4*>(sA)[i] = make_uint4(0, 0, 0, 0);
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      uint32_t old[kStg][kRecMax];
-#pragma unroll
-      for (int t = 0; t < kStg; ++t)
-#pragma unroll
-        for (int c = 0; c < kRecMax; ++c) old[t][c] = 0xffffffffu;
+      // a stage's A tile must start zeroed: every query row is cleared by its
+      // own 4 threads (lanes of one warp) before they write it, so a
+      // __syncwarp orders clear and writes (no CTA barrier)
       for (int i = 0; i < kPre && i < nkb; ++i) prefetch_kb(i);
-      if (nkb > 0) load_kb(0);
+      int lo0, hi0, lo1, hi1;
+      load_off(0, lo0, hi0);
+      load_off(1, lo1, hi1);
+      uint2 cur[kNr], nr[kNr];
+      load_rec(0, lo0, hi0, cur);
       int s = 0;
       uint32_t ph = 0;
       for (int kb = 0; kb < nkb; ++kb) {
-        uint2 cur[kRecMax];
-#pragma unroll
-        for (int c = 0; c < kRecMax; ++c) cur[c] = nxt[c];
         prefetch_kb(kb + kPre);
-        if (kb + 1 < nkb) load_kb(kb + 1);  // in flight while this stage is built
+        int lo2, hi2;
+        load_off(kb + 2, lo2, hi2);
+        load_rec(kb + 1, lo1, hi1, nr);
         mbar_wait(&empty[s], ph ^ 1);
-        const uint32_t abase = smem_u32(sA + s * MT * 2 * kAtom);
-        // the stage index is a runtime value: select this stage's old list
-        // with constant indices (registers, no local memory)
-        uint32_t prev[kRecMax];
+        uint8_t* a = sA + s * MT * 2 * kAtom;
+        const uint32_t abase = smem_u32(a) + (uint32_t)ql * 128;
+        // this query's row: MT * 2 atoms x 128 B, 4 threads x (MT * 2 * 8 / 4) x 16 B
 #pragma unroll
-        for (int c = 0; c < kRecMax; ++c) {
-          prev[c] = old[0][c];
-#pragma unroll
-          for (int t = 1; t < kStg; ++t)
-            if (s == t) prev[c] = old[t][c];
+        for (int i = 0; i < MT * 2 * 8 / 4; ++i) {
+          const int c16 = part + 4 * i;  // 16-byte chunk of the query's row (8 per atom)
+          *reinterpret_cast<uint4*>(a + (c16 >> 3) * kAtom + ql * 128 + (c16 & 7) * 16) = make_uint4(0, 0, 0, 0);
         }
-#pragma unroll
-        for (int c = 0; c < kRecMax; ++c)
-          if (c < per)
-            asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %1, -1;\n@p st.shared.b16 [%0], 0;\n}\n" ::"r"(abase + prev[c]),
-                         "r"(prev[c])
-                         : "memory");
         __syncwarp();
-        uint32_t now[kRecMax];
-#pragma unroll
-        for (int c = 0; c < kRecMax; ++c) {
-          now[c] = 0xffffffffu;
-          if (c < per) {
-            const uint32_t il = cur[c].x - (uint32_t)i0;  // (sentinel and out-of-range wrap high)
+        auto put = [&](uint2 r) {
+          const uint32_t il = r.x - (uint32_t)i0;
+          if (il < (uint32_t)(kBM * MT)) {
             const uint32_t e = il & 63u;
-            const uint32_t off = (il >> 6) * kAtom + (uint32_t)ql * 128 + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) +
-                                 (e & 7u) * 2;
-            const __nv_bfloat16 v = __float2bfloat16_rn(__uint_as_float(cur[c].y));
-            const bool inr = il < (uint32_t)(kBM * MT);
-            if (inr) now[c] = off;
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n@p st.shared.b16 [%0], %1;\n}\n" ::"r"(abase + off),
-                "h"(__bfloat16_as_ushort(v)), "r"(inr ? 1u : 0u)
-                : "memory");
+            const uint32_t off = (il >> 6) * kAtom + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) + (e & 7u) * 2;
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(abase + off),
+                         "h"(__bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r.y))))
+                         : "memory");
           }
+        };
+#pragma unroll
+        for (int c = 0; c < kNr; ++c) put(cur[c]);
+        {  // (rare) more than 4 kNr records of this query in the tile
+          const uint2* r = p.rec + lh_of(kb) * p.k;
+          for (int j = lo0 + part + 4 * kNr; j < hi0; j += 4) put(r[j]);
         }
-#pragma unroll
-        for (int c = 0; c < kRecMax; ++c)
-#pragma unroll
-          for (int t = 0; t < kStg; ++t)
-            if (s == t) old[t][c] = now[c];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[s]);
@@ -260,6 +246,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           s = 0;
           ph ^= 1;
         }
+#pragma unroll
+        for (int c = 0; c < kNr; ++c) cur[c] = nr[c];
+        lo0 = lo1;
+        hi0 = hi1;
+        lo1 = lo2;
+        hi1 = hi2;
       }
     }
     if ((warp - 2) / 4 < MT) {
@@ -511,12 +503,15 @@ size_t dk_smem_bytes(const Shape& s, int MT) {
 
 bool dq_tc_wanted_(const Shape& s);
 // the dense bf16 dS matrix (tensor-core dQ wanted), else the compact records
+// (k slots of 8 B) and their per-tile offsets (32 B) per (query, head, half)
 size_t dense_ds_bytes(const Shape& s) {
-  if (!dq_tc_wanted_(s)) return ((size_t)s.B * s.H * 2 * s.k * 8 + 255) & ~(size_t)255;
+  if (!dq_tc_wanted_(s)) return ((size_t)s.B * s.H * 2 * (s.k * 8 + 32) + 255) & ~(size_t)255;
   return ((size_t)s.B * s.H * 2 * s.n_sub * 2 + 255) & ~(size_t)255;
 }
 
 }  // namespace
+
+int dk_tile_rows(const Shape& s) { return kBM * dk_mt(s); }
 
 bool dk_tc_supported(const Shape& s) {
   // The tensor-core path rounds dS to bf16 (2^-9 relative): only where the
@@ -616,12 +611,10 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
              reinterpret_cast<const uint2*>(ws), s.k};
   const int mtk = dk_mt(s);
   const bool rec = !with_dq;  // ds_dq_kernel wrote compact records (dQ done there)
-  const bool rp16 = s.k > 32;  // record slots per builder thread: k <= 32 -> 8, else 16
-  auto dkk = rec ? (mtk == 2 ? (rp16 ? dk_gemm_kernel<2, true, 16> : dk_gemm_kernel<2, true, 8>)
-                             : (rp16 ? dk_gemm_kernel<1, true, 16> : dk_gemm_kernel<1, true, 8>))
+  auto dkk = rec ? (mtk == 2 ? dk_gemm_kernel<2, true> : dk_gemm_kernel<1, true>)
                  : (mtk == 2 ? dk_gemm_kernel<2, false> : dk_gemm_kernel<1, false>);
-  static std::atomic<uint64_t> attr[8];
-  cudaError_t e = smem_attr_once(attr[(mtk - 1) * 4 + (rec ? 2 : 0) + (rp16 ? 1 : 0)], dkk, 227 * 1024);
+  static std::atomic<uint64_t> attr[4];
+  cudaError_t e = smem_attr_once(attr[(mtk - 1) * 2 + (rec ? 1 : 0)], dkk, 227 * 1024);
   if (e != cudaSuccess) return e;
   dim3 grid(s.n_sub / (kBM * mtk), HH, S);
   launch_pdl(dkk, grid, kThreads, dk_smem_bytes(s, mtk), st, mds, mq, p);

@@ -130,6 +130,9 @@ bool backward_supported(const Shape& s, bool values, bool keys);
 
 // a7 dQ + a8 dK on the tensor cores (bf16 q/K): dQ = dS . K, dK += dS^T . Q per (head, half).
 bool dk_tc_supported(const Shape& s);
+// sub-key rows per dK CTA tile (128 x tiles per CTA); the compact dS records
+// carry per-tile offsets for it
+int dk_tile_rows(const Shape& s);
 size_t dk_tc_workspace_bytes(const Shape& s);
 // ws starts with the dense bf16 score-gradient matrix dSd [B, H*2, n_sub]
 // that ds_dq_kernel writes (dense mode).
