@@ -443,7 +443,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t m = 0;
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) m |= (__uint_as_float(r[jj]) >= tau ? 1u : 0u) << jj;
-      if (m == 0) return;  // most pieces of a long row pass nothing: skip the store chains
       uint32_t ca[4];
       ca[0] = caddr;
       ca[1] = ca[0] + (uint32_t)__popc(m & 0xffu) * step;
