@@ -1330,6 +1330,10 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_DENSE, false>, blocks, 256, 0, st,                        \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16, 0, 0);           \
+  else if (dense && !dk_compact(s))                                                            \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_DENSE, true>, blocks, 256, 0, st,                         \
+        (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16, 0, 0);           \
   else if (dense)                                                                              \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_COMPACT, true>, blocks, 256, 0, st,                       \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \

@@ -172,13 +172,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       // the records of query ql in this tile are [lo, hi) of its sorted list
       // (per-tile offsets written by ds_dq_kernel); the 4 threads of the query
       // take every 4th.  Offsets run two k-blocks ahead, records one.
+      // (two byte loads whose values are only used a k-block later: no stall here)
       auto load_off = [&](int kb, int& lo, int& hi) {
-        lo = hi = 0;
-        if (kb < nkb && q0 + (int64_t)kb * kBK + ql < q1) {
-          const uint16_t two = *reinterpret_cast<const uint16_t*>(offs + lh_of(kb) * 32 + (tile & ~1));
-          lo = (tile & 1) ? two >> 8 : two & 0xff;
-          hi = (tile & 1) ? offs[lh_of(kb) * 32 + tile + 1] : two >> 8;
-        }
+        const bool ok = kb < nkb && q0 + (int64_t)kb * kBK + ql < q1;
+        const uint8_t* o = offs + lh_of(ok ? kb : 0) * 32 + tile;
+        lo = ok ? (int)o[0] : 0;
+        hi = ok ? (int)o[1] : 0;
       };
       auto load_rec = [&](int kb, int lo, int hi, uint2 (&x)[kNr]) {
         const uint2* r = p.rec + lh_of(kb < nkb ? kb : 0) * p.k;
@@ -504,8 +503,9 @@ size_t dk_smem_bytes(const Shape& s, int MT) {
 bool dq_tc_wanted_(const Shape& s);
 // the dense bf16 dS matrix (tensor-core dQ wanted), else the compact records
 // (k slots of 8 B) and their per-tile offsets (32 B) per (query, head, half)
+bool dk_compact_(const Shape& s);
 size_t dense_ds_bytes(const Shape& s) {
-  if (!dq_tc_wanted_(s)) return ((size_t)s.B * s.H * 2 * (s.k * 8 + 32) + 255) & ~(size_t)255;
+  if (dk_compact_(s)) return ((size_t)s.B * s.H * 2 * (s.k * 8 + 32) + 255) & ~(size_t)255;
   return ((size_t)s.B * s.H * 2 * s.n_sub * 2 + 255) & ~(size_t)255;
 }
 
@@ -537,7 +537,17 @@ bool dq_tc_wanted_(const Shape& s) {
   return f >= 0 ? f != 0 : s.n_sub < 1024;
 }
 }  // namespace
+// the dK operand from compact records (no dense dS) whenever dQ is not on the
+// tensor cores; MSN_DK_DENSE=1 keeps the dense matrix (A/B measurements only)
+bool dk_compact_(const Shape& s) {
+  static const int f = env_int("MSN_DK_DENSE", 0);
+  return !dq_tc_wanted_(s) && !f;
+}
+}  // namespace
 bool dq_tc_wanted(const Shape& s) { return dq_tc_wanted_(s); }
+bool dk_compact(const Shape& s) { return dk_compact_(s); }
+namespace {
+}  // namespace
 
 cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* dQ, float* dK,
                          void* ws, cudaStream_t st, int* launches, bool with_dq) {
@@ -610,7 +620,7 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
   DkParams p{s.B, s.H, s.n_sub, s.d_h, qps, S > 1 ? part : dK, S > 1 ? 0 : 1,
              reinterpret_cast<const uint2*>(ws), s.k};
   const int mtk = dk_mt(s);
-  const bool rec = !with_dq;  // ds_dq_kernel wrote compact records (dQ done there)
+  const bool rec = dk_compact(s);  // ds_dq_kernel wrote compact records (dQ done there)
   auto dkk = rec ? (mtk == 2 ? dk_gemm_kernel<2, true> : dk_gemm_kernel<1, true>)
                  : (mtk == 2 ? dk_gemm_kernel<2, false> : dk_gemm_kernel<1, false>);
   static std::atomic<uint64_t> attr[4];

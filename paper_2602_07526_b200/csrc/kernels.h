@@ -142,6 +142,8 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* K, float* dQ
 // dQ on the tensor cores too (dense dS . K), or by ds_dq_kernel from the m
 // distinct K rows of each lookup-half: the dense GEMM's work grows with n_sub.
 bool dq_tc_wanted(const Shape& s);
+// dK from the compact records (else from the dense bf16 dS matrix)
+bool dk_compact(const Shape& s);
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 
