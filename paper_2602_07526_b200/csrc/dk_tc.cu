@@ -536,7 +536,6 @@ bool dq_tc_wanted_(const Shape& s) {
   static const int f = env_int("MSN_DQ_TC", -1);
   return f >= 0 ? f != 0 : s.n_sub < 1024;
 }
-}  // namespace
 // the dK operand from compact records (no dense dS) whenever dQ is not on the
 // tensor cores; MSN_DK_DENSE=1 keeps the dense matrix (A/B measurements only)
 bool dk_compact_(const Shape& s) {
@@ -546,8 +545,6 @@ bool dk_compact_(const Shape& s) {
 }  // namespace
 bool dq_tc_wanted(const Shape& s) { return dq_tc_wanted_(s); }
 bool dk_compact(const Shape& s) { return dk_compact_(s); }
-namespace {
-}  // namespace
 
 cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* dQ, float* dK,
                          void* ws, cudaStream_t st, int* launches, bool with_dq) {
