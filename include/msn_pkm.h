@@ -165,6 +165,17 @@ msn_status msn_pkm_forward_gated(msn_pkm_t h, void* stream, int64_t B,
                                  int32_t* idx, float* weights,
                                  void* workspace, size_t workspace_bytes);
 
+/* Forward with the query LayerNorm folded into the scorer's operand load
+ * (reading R23: LN over each d_half-wide query
+ * half, no affine, eps = 1e-5): everything msn_pkm_forward does on
+ * q^ = LN(query), and q^ [B, H, 2, d_half] (qk_dtype, rounded once) is
+ * written to q_hat -- the backward's query (msn_pkm_backward(..., q_hat, ...)
+ * gives d q^; msn_pkm_layernorm_backward(query, d q^) the gradient w.r.t. the
+ * raw query).  Same errors as msn_pkm_forward; q_hat 16-byte aligned. */
+msn_status msn_pkm_forward_qln(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                               const void* subkeys, const void* values, float* out, int32_t* idx,
+                               float* weights, void* q_hat, void* workspace, size_t workspace_bytes);
+
 /* Step a6 with the optimiser step fused into the row reduction (SURVEY 8(f)
  * f3): the value gradient g_r of every touched row r (this handle's rows) is
  * applied to the table in place instead of being accumulated into a

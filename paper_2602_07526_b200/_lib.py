@@ -60,6 +60,7 @@ SIGNATURES = {
     "msn_pkm_destroy": [_P],
     "msn_pkm_workspace_size": [_P, _I64, _I64, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)],
     "msn_pkm_forward": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ],
+    "msn_pkm_forward_qln": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_forward_gated": [_P, _P, _I64, _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P, _P, _P, _SZ],
     "msn_pkm_gate_backward": [_P, _P, _I64, ctypes.c_int32, _P, _P, _P, _P, _P],
     "msn_pkm_layernorm": [_P, _P, _I64, _P, _P],

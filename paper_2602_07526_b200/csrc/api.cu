@@ -141,7 +141,7 @@ msn_status check_tape(msn_pkm_t h, void* stream, int64_t B, const int32_t* idx, 
 msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
                      const void* subkeys, int32_t* idx, float* weights, void* ws, size_t ws_bytes,
                      int* launches, const void* values = nullptr, float* out = nullptr,
-                     const Gate& gate = Gate{}, bool per_lookup = false) {
+                     const Gate& gate = Gate{}, bool per_lookup = false, void* qhat = nullptr) {
   const Shape s = shape_of(h->cfg, B);
   msn_status st0 = check_select_shape(s);
   if (st0) return st0;
@@ -149,11 +149,11 @@ msn_status do_select(msn_pkm_t h, cudaStream_t st, int64_t B, const void* query,
     return fail(MSN_ERR_WORKSPACE, "forward workspace %zu < %zu bytes", ws_bytes, fwd_bytes(s));
   Cands cd;
   char* p = carve_cands(s, ws, cd);
-  cd.rq.Q = query;
+  cd.rq.Q = qhat ? qhat : query;  // (the exact rescoring scores the normalised query)
   cd.rq.K = subkeys;
   cd.rq.d_h = s.d_h;
   cd.rq.qk_dt = s.qk_dt;
-  cudaError_t e = launch_select_tc(s, query, subkeys, cd, p, st, launches);
+  cudaError_t e = launch_select_tc(s, query, subkeys, cd, p, st, launches, qhat);
   if (e != cudaSuccess) return cuda_fail(e, "select (tcgen05 scoring + per-half candidates)");
   if (h->ntrace > 0) cudaEventRecord(h->trace[0], st);  // stage boundary: scoring done
   if (values && per_lookup) {  // small batches: Cartesian + gather fused per lookup
@@ -359,7 +359,7 @@ msn_status msn_pkm_validate_tape(msn_pkm_t h, void* stream, int64_t B, const int
 static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* query,
                              const void* subkeys, const void* values, float* out, int32_t* idx,
                              float* weights, void* workspace, size_t workspace_bytes,
-                             const Gate& gate) {
+                             const Gate& gate, void* qhat = nullptr) {
   msn_status st = check_handle(h);
   if (st) return st;
   if ((st = check_batch(h, B))) return st;
@@ -382,15 +382,15 @@ static msn_status do_forward(msn_pkm_t h, void* stream, int64_t B, const void* q
   static const int64_t fuse_min_b = getenv("MSN_FUSE_MIN_B") ? atoll(getenv("MSN_FUSE_MIN_B")) : 8192;
   if (h->cfg.heads * h->cfg.k <= 256 && B >= fuse_min_b) {
     return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
-                     &h->last_launches, values, out, gate);
+                     &h->last_launches, values, out, gate, false, qhat);
   }
   // smaller batches: Cartesian + gather fused per lookup (8x the warps of
   // the per-query kernel), unless a gate or head groups ask for the phases
   if (!gate.kind && cartesian_gather_lookup_ok(shape_of(h->cfg, B)))
     return do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes, &h->last_launches,
-                     values, out, gate, true);
+                     values, out, gate, true, qhat);
   if ((st = do_select(h, cs, B, query, subkeys, idx, weights, workspace, workspace_bytes,
-                      &h->last_launches)))
+                      &h->last_launches, nullptr, nullptr, Gate{}, false, qhat)))
     return st;
   cudaError_t e = launch_gather(shape_of(h->cfg, B), idx, weights, values, out, cs,
                                 &h->last_launches, gate);
@@ -403,6 +403,14 @@ msn_status msn_pkm_forward(msn_pkm_t h, void* stream, int64_t B, const void* que
                            float* weights, void* workspace, size_t workspace_bytes) {
   return do_forward(h, stream, B, query, subkeys, values, out, idx, weights, workspace,
                     workspace_bytes, Gate{});
+}
+
+msn_status msn_pkm_forward_qln(msn_pkm_t h, void* stream, int64_t B, const void* query,
+                               const void* subkeys, const void* values, float* out, int32_t* idx,
+                               float* weights, void* q_hat, void* workspace, size_t workspace_bytes) {
+  if (B > 0) REQUIRE_PTR(q_hat);
+  return do_forward(h, stream, B, query, subkeys, values, out, idx, weights, workspace, workspace_bytes,
+                    Gate{}, q_hat);
 }
 
 msn_status msn_pkm_forward_gated(msn_pkm_t h, void* stream, int64_t B, const void* query,

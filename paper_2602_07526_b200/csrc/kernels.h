@@ -62,8 +62,11 @@ struct Cands {
 // does not depend on B.
 int select_segments(const Shape& s, bool for_workspace);
 int select_cap(const Shape& s);  // candidate list capacity (64, or 128 for k > 32)
+// qhat (f2, may be null): LayerNorm each query half-vector on load (no affine,
+// eps 1e-5) and write q^ [B, H, 2, d_h] (query dtype) there; the exact
+// rescoring of overflowed rows then reads cd.rq.Q = qhat.
 cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
-                             void* ws, cudaStream_t st, int* launches);
+                             void* ws, cudaStream_t st, int* launches, void* qhat = nullptr);
 bool select_tc_supported(const Shape& s);  // shape check only (no driver call)
 size_t select_tc_workspace_bytes(const Shape& s);
 

@@ -49,6 +49,7 @@
 // and tau - d (rounded down) bounds the 3xTF32 KT-th score from below.
 #include <cuda.h>
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -125,6 +126,7 @@ struct TcParams {
   const float* knorm;  // TF32, two sweeps: ||k_i|| (rounded up) per sub-key row [H*2*n_sub]  // overflowed rows are rescored exactly from these
   int seg_cols;        // columns per CTA: n_sub / S (blockIdx.z = column segment)
   int SC;              // segment slots per row in vc / cn
+  void* qhat = nullptr;  // f2: LayerNorm the query tile on load, q^ written here (nullptr: off)
 };
 
 template <int KT, bool TF32, bool WIDE, bool SEG>
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = TF32 ? idesc_tf32(128, p.n_tile) : idesc_bf16(128, p.n_tile);
       mbar_wait(a_full, 0);
       SEL_TS_ANY(14);
-      if (TF32) mbar_wait(a_ready, 0);
+      if (TF32 || p.qhat) mbar_wait(a_ready, 0);
       SEL_TS_ANY(15);
       tc_fence_after();
       int it = 0;
@@ -270,6 +272,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sh = ew >> 2;            // column share of this thread: 0 or 1
     const int row = q * 32 + lane;     // query row within the tile
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    // f2: LayerNorm of the query row folded into the operand
+    // load (reading R23: no affine, eps = 1e-5): the resident
+    // query tile is normalised in place in shared memory before any MMA reads
+    // it (two passes over the row: mean, then variance; the two threads of a
+    // row exchange their halves' sums), and q^ is written out for the
+    // backward (q_hat [B, H, 2, d_h], rounded once to the query dtype).
+    if (p.qhat) {
+      using QT = typename std::conditional<TF32, float, __nv_bfloat16>::type;
+      constexpr int EPC = 16 / (int)sizeof(QT);  // elements per 16-byte chunk
+      mbar_wait(a_full, 0);
+      float* lnx = reinterpret_cast<float*>(cnts);  // [2][128] (the counts come much later)
+      const int sw = row & 7;
+      const int64_t b = m0 + row;
+      auto chunk = [&](int kb, int ch) -> uint4* {
+        return reinterpret_cast<uint4*>(sA + kb * 16384 + row * kRowBytes) + (ch ^ sw);
+      };
+      float sum = 0.f;
+      for (int kb = sh; kb < p.k_blocks; kb += 2)
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          float f[EPC];
+          unpack16<QT>(*chunk(kb, ch), f);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) sum += f[e];
+        }
+      lnx[sh * 128 + row] = sum;
+      epi_bar();
+      const float mu = (lnx[row] + lnx[128 + row]) / (float)p.d_h;
+      epi_bar();
+      float ss = 0.f;
+      for (int kb = sh; kb < p.k_blocks; kb += 2)
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          float f[EPC];
+          unpack16<QT>(*chunk(kb, ch), f);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) ss += (f[e] - mu) * (f[e] - mu);
+        }
+      lnx[sh * 128 + row] = ss;
+      epi_bar();
+      const float rs = rsqrtf((lnx[row] + lnx[128 + row]) / (float)p.d_h + 1e-5f);
+      QT* qh = reinterpret_cast<QT*>(p.qhat) + (b * p.H * 2 + hh) * (int64_t)p.d_h;
+      for (int kb = sh; kb < p.k_blocks; kb += 2)
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4* c = chunk(kb, ch);
+          float f[EPC];
+          unpack16<QT>(*c, f);
+          uint4 o;
+          if constexpr (TF32) {
+            o = make_uint4(__float_as_uint((f[0] - mu) * rs), __float_as_uint((f[1] - mu) * rs),
+                           __float_as_uint((f[2] - mu) * rs), __float_as_uint((f[3] - mu) * rs));
+          } else {
+            uint32_t w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const __nv_bfloat162 v = __floats2bfloat162_rn((f[2 * t] - mu) * rs, (f[2 * t + 1] - mu) * rs);
+              w[t] = *reinterpret_cast<const uint32_t*>(&v);
+            }
+            o = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          *c = o;
+          if (b < p.B) *reinterpret_cast<uint4*>(qh + kb * (kRowBytes / (int)sizeof(QT)) + ch * EPC) = o;
+        }
+      epi_bar();  // (the exchange slots are reused below)
+      if constexpr (!TF32) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_ready);
+      }
+    }
     // TF32 two-sweep rows: margin d = 2^-8 ||q_row|| max_i ||k_i|| on the
     // 1xTF32 first sweep (see the header); ||q|| from the split below (qn)
     if constexpr (TF32) {
@@ -684,7 +757,7 @@ bool select_tc_supported(const Shape& s) {
 }
 
 cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const Cands& cd,
-                             void* ws, cudaStream_t st, int* launches) {
+                             void* ws, cudaStream_t st, int* launches, void* qhat) {
   if (!select_tc_supported(s) || get_encode() == nullptr || cd.cap != select_cap(s)) return cudaErrorNotSupported;
   const bool tf = is_tf32(s);
   const int bk = tf ? 32 : 64;
@@ -735,7 +808,7 @@ cudaError_t launch_select_tc(const Shape& s, const void* Q, const void* K, const
   const int seg_cols = s.n_sub / cd.S;
   const int n_chunks = seg_cols / nt;
   TcParams p{s.B, s.H, s.n_sub, s.d_h, s.k, nt, n_chunks, s.d_h / bk, n_chunks <= 2 ? 1 : 2,
-             cd.vc, cd.n, cd.rq, knorm, seg_cols, cd.SC};
+             cd.vc, cd.n, cd.rq, knorm, seg_cols, cd.SC, qhat};
   cudaError_t e;
   if (tf) {
     if (s.k <= 8) e = launch_kt<8, true>(s, mq, mk, mklo, p, st);

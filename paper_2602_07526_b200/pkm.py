@@ -141,6 +141,21 @@ class PKMLookup:
             return out.cpu(), idx.cpu(), w.cpu()
         return out, idx, w
 
+    def forward_qln(self, query: torch.Tensor, subkeys: torch.Tensor, values: torch.Tensor):
+        """a1-a5 on q^ = LN(query), the LayerNorm folded into the scorer's
+        operand load.  Returns (out, idx, w, q_hat)."""
+        self._check_inputs(query, subkeys, values)
+        q, K, V = self._dev(query), self._dev(subkeys), self._dev(values)
+        B = q.shape[0]
+        out = torch.empty(self._out_shape(B), dtype=torch.float32, device=self.device)
+        idx = torch.empty((B, self.heads, self.k), dtype=torch.int32, device=self.device)
+        w = torch.empty((B, self.heads, self.k), dtype=torch.float32, device=self.device)
+        q_hat = torch.empty_like(q)
+        ws = self.workspace(B)
+        _lib.check(self.lib.msn_pkm_forward_qln(self._h, _stream(), B, _ptr(q), _ptr(K), _ptr(V), _ptr(out),
+                                                _ptr(idx), _ptr(w), _ptr(q_hat), _ptr(ws), ws.numel()))
+        return out, idx, w, q_hat
+
     def forward_gated(self, query: torch.Tensor, subkeys: torch.Tensor, values: torch.Tensor,
                       x_in: torch.Tensor, gate: str = "tanh"):
         """a1-a5 plus the memory-gated fusion x~ = x_in * g(v_o) (SURVEY 8(f)

@@ -474,9 +474,11 @@ def test_prologue_stages(dt, d_h):
     parity.row_close((dth - d0).cpu().reshape(-1, d_h).numpy(), rth.reshape(-1, d_h), 1e-4, what="dTheta")
 
 
-def test_prologue_chain_fp32():
+@pytest.mark.parametrize("fused_ln", [False, True])
+def test_prologue_chain_fp32(fused_ln):
     """q^ = LN(q), K~ = Theta LN(k), lookup, backward, back through the
-    prologue -- the whole chain on the GPU against the fp64 oracle chain."""
+    prologue -- the whole chain on the GPU against the fp64 oracle chain.
+    fused_ln: LN(q) folded into the scorer's operand load (msn_pkm_forward_qln)."""
     from oracle import oracle as orc
     from oracle import prologue as op
     B, H, n_sub, d_h, d_v, k = 500, 2, 128, 64, 64, 8
@@ -485,10 +487,13 @@ def test_prologue_chain_fp32():
     g = torch.Generator(device="cpu").manual_seed(22)
     theta = (torch.eye(d_h) + 0.1 * torch.randn((H, 2, d_h, d_h), generator=g)).to(DEV)
     lk = lookup_for(cfg, B)
-    qh = lk.layernorm(Q)
     kh = lk.layernorm(K)
     ke = lk.key_transform(kh, theta)
-    out, idx, w = lk.forward(qh, ke, V)
+    if fused_ln:
+        out, idx, w, qh = lk.forward_qln(Q, ke, V)
+    else:
+        qh = lk.layernorm(Q)
+        out, idx, w = lk.forward(qh, ke, V)
     dqh, dke, dV, dw = lk.backward(dOut, qh, ke, V, idx, w)
     dq = lk.layernorm_backward(Q, dqh)
     dkh, dth = lk.key_transform_backward(kh, theta, dke)
@@ -528,6 +533,31 @@ def test_prologue_chain_fp32():
                      absmag=mag_dth.reshape(-1, d_h))
     parity.row_close(dk.cpu().reshape(-1, d_h).numpy(), dk_o.reshape(-1, d_h), 1e-4, what="dk",
                      absmag=ln_mag(K, mag_dkh).reshape(-1, d_h))
+
+
+@pytest.mark.parametrize("name,B", [("c2_mid_bf16", 777), ("c5_latency_bf16", 300), ("c4_large_sharded_bf16", 200)])
+def test_forward_qln_matches_layernorm_then_forward(name, B):
+    """bf16: the LayerNorm folded into the scorer's operand load gives q^ within
+    one bf16 rounding of msn_pkm_layernorm's (its sums run in another order),
+    the same selection except at near-ties, and the same out within the bf16
+    tolerance; q^ against the fp64 LN oracle too."""
+    from oracle import prologue as op
+    cfg = wl.CONFIGS[name].scaled(batch=B)
+    Q, K, V, _ = wl.make_all(cfg, DEV)
+    Q = (3.0 * Q.float() + 0.5).to(cfg.qk_dtype)  # a non-trivial mean and scale
+    lk = lookup_for(cfg, B)
+    out_f, idx_f, w_f, qh_f = lk.forward_qln(Q, K, V)
+    qh = lk.layernorm(Q)
+    out, idx, w = lk.forward(qh, K, V)
+    torch.cuda.synchronize()
+    d = (qh_f.float() - qh.float()).abs()
+    assert float(d.max()) <= 2 * float(2.0 ** -8 * qh.float().abs().max())
+    parity.row_close(qh_f.cpu().float().reshape(-1, cfg.d_half).numpy(),
+                     op.layernorm(Q.cpu()).reshape(-1, cfg.d_half), 2e-2, what="q^ vs oracle LN")
+    same = (idx_f == idx).all(-1).all(-1)
+    assert float(same.float().mean()) > 0.98
+    sel = same.cpu().numpy()
+    parity.row_close(out_f.cpu().numpy(), out.cpu().numpy(), 2e-2, sel, "out")
 
 
 # --------------------------------------------------- hot rows (grouping) --
