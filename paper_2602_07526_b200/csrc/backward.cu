@@ -383,8 +383,13 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       d[u] = 0.f;
+      if constexpr (EPL % 2 == 0) {
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] = fmaf(wt[u], x[u][i], acc[i]);
+        for (int i = 0; i < EPL; i += 2) ffma2(acc[i], acc[i + 1], x[u][i], x[u][i + 1], wt[u]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) acc[i] = fmaf(wt[u], x[u][i], acc[i]);
+      }
       if constexpr (MODE == MODE_DV) {
 #pragma unroll
         for (int i = 0; i < EPL; ++i) d[u] = fmaf(y[i], x[u][i], d[u]);
@@ -1064,9 +1069,15 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-      for (int u = 0; u < DQ_U; ++u)
+      for (int u = 0; u < DQ_U; ++u) {
+        if constexpr (EPL % 2 == 0) {
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) acc[hf][i] = fmaf(dv[hf][u], kr[hf][u][i], acc[hf][i]);
+          for (int i = 0; i < EPL; i += 2) ffma2(acc[hf][i], acc[hf][i + 1], kr[hf][u][i], kr[hf][u][i + 1], dv[hf][u]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[hf][i] = fmaf(dv[hf][u], kr[hf][u][i], acc[hf][i]);
+        }
+      }
   }
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {

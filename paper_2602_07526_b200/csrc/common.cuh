@@ -214,6 +214,20 @@ __device__ __forceinline__ float gate_dg(float v, int kind) {
   return 1.0f;
 }
 
+// Two independent fp32 FMAs in one instruction (FFMA2, sm_100):
+// a0 = fma(x0, s, a0), a1 = fma(x1, s, a1) -- each exactly the scalar fmaf,
+// so replacing a pair of fmaf by it changes no result bit.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float s) {
+  asm("{\n.reg .b64 A, X, S;\n"
+      "mov.b64 A, {%0, %1};\n"
+      "mov.b64 X, {%2, %3};\n"
+      "mov.b64 S, {%4, %4};\n"
+      "fma.rn.f32x2 A, X, S, A;\n"
+      "mov.b64 {%0, %1}, A;\n}\n"
+      : "+f"(a0), "+f"(a1)
+      : "f"(x0), "f"(x1), "f"(s));
+}
+
 // fire-and-forget vector fp32 add into global memory (sm_90+).
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),

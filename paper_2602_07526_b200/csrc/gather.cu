@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256) gather_wide_kernel(const int32_t* __restr
           float f[PER];
           unpack16<VT>(x[u], f);
 #pragma unroll
-          for (int e = 0; e < PER; ++e) part[e] = fmaf(wt[u], f[e], part[e]);
+          for (int e = 0; e < PER; e += 2) ffma2(part[e], part[e + 1], f[e], f[e + 1], wt[u]);
         }
       }
 #pragma unroll

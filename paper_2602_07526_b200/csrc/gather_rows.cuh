@@ -48,7 +48,7 @@ __device__ __forceinline__ void gather_rows(const int32_t* s_idx, const float* s
         float f[PER];
         unpack16<VT>(x[u][v], f);
 #pragma unroll
-        for (int e = 0; e < PER; ++e) acc[v][e] = fmaf(wt[u], f[e], acc[v][e]);
+        for (int e = 0; e < PER; e += 2) ffma2(acc[v][e], acc[v][e + 1], f[e], f[e + 1], wt[u]);
       }
   }
 #pragma unroll
