@@ -7,8 +7,9 @@
 //   1. group the contributions by destination row (key = slot row, record
 //      = contribution id cid = (b*H + h)*k + t): atomic counts, one
 //      contiguous segment per touched row, placement (see "grouping");
-//   2. row-major reduce: one warp per row with <= 32 contributions, one CTA
-//      per longer row; each row's record ids are sorted first, so the sum
+//   2. row-major reduce: one warp per row with <= 32 contributions; longer
+//      rows in fixed 32-entry slices (one warp each, then the slice sums in
+//      slice order); each row's record ids are sorted first, so the sum
 //      order is fixed (bitwise repeatable), and the row is read and written
 //      once (G = G + sum).  For dV the same pass computes
 //      dw[cid] = <V[row], dOut[b]>, reading each touched value row ONCE.
@@ -61,14 +62,19 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 #define MSN_SHORT_BPS 4  // resident blocks per SM of the short-run reducer (8 values/lane)
 #endif
 constexpr int GRP_SHORT = 32;     // runs up to this length: one warp, one entry per lane
-constexpr int GRP_PIECE = 256;       // long runs are reduced in pieces of this many entries
-constexpr int GRP_SORT_SMEM = 16384;  // long runs sorted in shared memory up to this length
-enum { CTL_TOTAL = 0, CTL_NSHORT = 1, CTL_NLONG = 2, CTL_NPIECES = 3, CTL_WORDS = 8 };
+constexpr int GRP_SLICE = 32;     // long runs are reduced in slices of this many entries (one warp each)
+constexpr int GRP_WARP_SORT = 1024;   // long runs sorted by one warp in registers up to this length
+constexpr int GRP_SORT_SMEM = 16384;  // longer runs: one CTA, in shared memory up to this length
+enum { CTL_TOTAL = 0, CTL_NSHORT = 1, CTL_NLONG = 2, CTL_NPIECES = 3, CTL_NHUGE = 4, CTL_SORTQ = 5,
+       CTL_WORDS = 8 };
 __host__ __device__ __forceinline__ uint32_t grp_npieces(uint32_t c) {
-  return c > GRP_SHORT ? (c + GRP_PIECE - 1) / GRP_PIECE : 0u;
+  return c > GRP_SHORT ? (c + GRP_SLICE - 1) / GRP_SLICE : 0u;
 }
-// sum of grp_npieces over runs of total length n: <= n / 33 + 1 pieces
-inline int64_t grp_pieces_max(int64_t n) { return n / (GRP_SHORT + 1) + 1; }
+// sum of grp_npieces over runs of total length n (every run > 32 entries):
+// <= n / 32 + (number of runs) <= n / 32 + n / 33
+inline int64_t grp_pieces_max(int64_t n) { return n / GRP_SLICE + n / (GRP_SHORT + 1) + 2; }
+// runs longer than GRP_WARP_SORT: <= n / 1025
+inline int64_t grp_huge_max(int64_t n) { return n / (GRP_WARP_SORT + 1) + 1; }
 
 // Each block owns a contiguous range of rows: pass 1 counts its entries,
 // short and long runs and long-run pieces; one atomic per counter per block
@@ -80,6 +86,7 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
                                                        uint4* __restrict__ runs_short,
                                                        uint4* __restrict__ runs_long,
                                                        uint2* __restrict__ pieces,
+                                                       uint32_t* __restrict__ huge,
                                                        uint32_t* __restrict__ ctl) {
   pdl_enter();
   __shared__ uint32_t sh[4][8];
@@ -152,6 +159,7 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
         const uint32_t li = lb + (es >> 16);
         runs_long[li] = make_uint4(ec, c, (uint32_t)r, ep);
         for (uint32_t j = 0; j < np; ++j) pieces[ep + j] = make_uint2(li, j);
+        if (c > (uint32_t)GRP_WARP_SORT) huge[atomicAdd(&ctl[CTL_NHUGE], 1u)] = li;  // (any order)
       }
     }
     base += tot[0];
@@ -189,8 +197,8 @@ struct GrpArgs {
   const float* wts;       // weight by record id
   const uint4* runs_short;
   const uint4* runs_long;
-  const uint2* pieces;    // long-run pieces {long run, j}
-  float* part;            // per-piece partial rows (runs with >= 2 pieces)
+  const uint2* pieces;    // long-run slices {long run, j} (GRP_SLICE entries each)
+  float* part;            // per-slice partial rows
   const uint32_t* ctl;
   const void* X;          // x rows (dOut fp32 or Q)
   const void* Y;          // V (MODE_DV dot)
@@ -215,6 +223,8 @@ struct GrpArgs {
   PerRank<float> pd{};
   uint32_t xl = 0, dl = 0;
   FastDiv div_xl, div_dl;
+  const uint32_t* huge = nullptr;  // long runs > GRP_WARP_SORT entries (indices into runs_long)
+  uint32_t* ctl_rw = nullptr;      // = ctl (the sort's work queue counter)
 };
 
 // Applies the fused update to VW consecutive elements at element offset off
@@ -575,28 +585,20 @@ __device__ __forceinline__ void warp_sort_run(uint32_t* g, int L) {
 }
 
 // Long runs (> 32 entries), step 1: every run's record ids are sorted
-// ascending in place, fixing its summation order.  Runs of <= 1024 entries:
-// one warp each, in registers; longer runs (then): one CTA each, in shared
-// memory up to GRP_SORT_SMEM entries, else in place in global memory.
+// ascending in place, fixing its summation order.  Runs of more than
+// GRP_WARP_SORT entries (the `huge` list, few) go first, one CTA each, in
+// shared memory up to GRP_SORT_SMEM entries, else in place in global memory;
+// then every warp takes the other runs from a work queue (one atomic per
+// run), sorting each in registers -- so a CTA held up by a huge run does not
+// hold up a static share of the short ones.
 __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
   pdl_enter();
   extern __shared__ __align__(16) uint32_t s_sort[];  // [GRP_SORT_SMEM]
   const int64_t nruns = a.ctl[CTL_NLONG];
-  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < nruns; r += nw) {
-    const uint4 run = a.runs_long[r];
+  const int64_t nhuge = a.ctl[CTL_NHUGE];
+  for (int64_t h = blockIdx.x; h < nhuge; h += gridDim.x) {
+    const uint4 run = a.runs_long[a.huge[h]];
     const int L = (int)run.y;
-    uint32_t* g = a.ent_rw + run.x;
-    if (L <= 64) warp_sort_run<2>(g, L);
-    else if (L <= 128) warp_sort_run<4>(g, L);
-    else if (L <= 256) warp_sort_run<8>(g, L);
-    else if (L <= 512) warp_sort_run<16>(g, L);
-    else if (L <= 1024) warp_sort_run<32>(g, L);
-  }
-  for (int64_t r = blockIdx.x; r < nruns; r += gridDim.x) {
-    const uint4 run = a.runs_long[r];
-    const int L = (int)run.y;
-    if (L <= 1024) continue;
     int P = 1;
     while (P < L) P <<= 1;
     uint32_t* g = a.ent_rw + run.x;
@@ -610,30 +612,44 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
       block_bitonic(g, L, P);
     }
   }
+  const int lane = threadIdx.x % 32;
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(a.ctl_rw + CTL_SORTQ, 1u);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if ((int64_t)r >= nruns) break;
+    const uint4 run = a.runs_long[r];
+    const int L = (int)run.y;
+    uint32_t* g = a.ent_rw + run.x;
+    if (L <= 64) warp_sort_run<2>(g, L);
+    else if (L <= 128) warp_sort_run<4>(g, L);
+    else if (L <= 256) warp_sort_run<8>(g, L);
+    else if (L <= 512) warp_sort_run<16>(g, L);
+    else if (L <= GRP_WARP_SORT) warp_sort_run<32>(g, L);
+  }
 }
 
-// Step 2: one CTA per piece of GRP_PIECE consecutive sorted entries (many
-// pieces in flight); warp w sums the w-th 32-entry slice in order, the CTA
-// adds the 8 slice sums in warp order.  A run of one piece adds its sum to G
-// directly (its only update); longer runs leave the piece sum for step 3.
+// Step 2: one warp per slice of GRP_SLICE consecutive sorted entries of a
+// long run (a flat list over all runs: every warp has a full slice's work,
+// many slices in flight); the slice sum, in entry order, goes to part[slice].
 template <int MODE, typename XT, typename YT, int EPL, bool P2P>
-__global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256) grp_reduce_slice_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
   constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
-  __shared__ __align__(16) float s_part[8 * D];
-  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int lane = threadIdx.x % 32;
   const int64_t np = a.ctl[CTL_NPIECES];
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
   const YT* __restrict__ Y = reinterpret_cast<const YT*>(a.Y) + lane * VW;
-  for (int64_t pc = blockIdx.x; pc < np; pc += gridDim.x) {
+  for (int64_t pc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; pc < np; pc += nw) {
     const uint2 piece = a.pieces[pc];
     const uint4 run = a.runs_long[piece.x];
     const int L = (int)run.y;
     const uint32_t key = run.z;
-    const int j0 = (int)piece.y * GRP_PIECE + wid * 32;
-    const int j1 = min(j0 + 32, min(L, ((int)piece.y + 1) * GRP_PIECE));
+    const int j0 = (int)piece.y * GRP_SLICE;
+    const int j1 = min(j0 + GRP_SLICE, L);
     float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
@@ -652,29 +668,13 @@ __global__ void __launch_bounds__(256) grp_reduce_piece_kernel(GrpArgs a) {
         },
         y, acc);
 #pragma unroll
-    for (int i = 0; i < NVEC; ++i) stg_vec<VW>(s_part + wid * D + lane * VW + i * 32 * VW, acc + i * VW);
-    __syncthreads();
-    const bool single = L <= GRP_PIECE;
-    for (int e = threadIdx.x; e < D; e += blockDim.x) {
-      float t = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += s_part[w * D + e];
-      if (!single) {
-        a.part[pc * D + e] = t;
-      } else if (MODE == MODE_DV && a.upd) {
-        const int64_t off = (int64_t)key * D + e;
-        const float yv = elem<YT>::to_f(reinterpret_cast<const YT*>(a.Vw)[off]);
-        update_vec<YT, 1>(a, off, &yv, &t);
-      } else {
-        atomicAdd(a.G + (int64_t)key * D + e, t);  // the row's only update
-      }
-    }
-    __syncthreads();
+    for (int i = 0; i < NVEC; ++i) stg_vec<VW>(a.part + pc * D + lane * VW + i * 32 * VW, acc + i * VW);
   }
 }
 
-// Step 3: one warp per long run of >= 2 pieces: G += the piece sums, added
-// in piece order (one update per element).
+// Step 3: one warp per long run (>= 2 slices): G += the slice sums, added in
+// slice order (one update per element); the slice sums are requested CB at a
+// time, so a run of many slices costs few memory round trips.
 template <typename YT, int EPL>
 __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
   pdl_enter();
@@ -687,16 +687,25 @@ __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < nruns; r += nw) {
     const uint4 run = a.runs_long[r];
     const int npc = (int)grp_npieces(run.y);
-    if (npc < 2) continue;
-    float acc[EPL], v[EPL];
+    constexpr int CB = EPL >= 16 ? 2 : (EPL >= 8 ? 4 : 8);
+    float acc[EPL];
 #pragma unroll
     for (int i = 0; i < NVEC; ++i) ldg_vec<float, VW>(a.part + (int64_t)run.w * D + lane * VW + i * 32 * VW, acc + i * VW);
-    for (int j = 1; j < npc; ++j) {
+    for (int j0 = 1; j0 < npc; j0 += CB) {
+      float v[CB][EPL];
 #pragma unroll
-      for (int i = 0; i < NVEC; ++i)
-        ldg_vec<float, VW>(a.part + (int64_t)(run.w + j) * D + lane * VW + i * 32 * VW, v + i * VW);
+      for (int c = 0; c < CB; ++c)
+        if (j0 + c < npc) {
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] += v[i];
+          for (int i = 0; i < NVEC; ++i)
+            ldg_vec<float, VW>(a.part + (int64_t)(run.w + j0 + c) * D + lane * VW + i * 32 * VW, v[c] + i * VW);
+        }
+#pragma unroll
+      for (int c = 0; c < CB; ++c)
+        if (j0 + c < npc) {
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] += v[c][i];
+        }
     }
     if (a.upd) {
 #pragma unroll
@@ -728,6 +737,7 @@ struct GrpScratch {
   uint2* pieces;    // [grp_pieces_max(n)]
   float* part;      // [grp_pieces_max(n) * D]
   uint32_t* ctl;    // CTL_WORDS
+  uint32_t* huge;   // [grp_huge_max(n)]
 };
 
 // zero the row counters and the control words (the counts are accumulated by
@@ -776,12 +786,12 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   if (lb > (int64_t)sms * 3) lb = (int64_t)sms * 3;
   launch_pdl(grp_sort_long_kernel, (unsigned)lb, 256, GRP_SORT_SMEM * 4, st, a);
   int64_t pb = (int64_t)sms * 8;
-  const int64_t pneed = grp_pieces_max(n);
+  const int64_t pneed = (grp_pieces_max(n) + 7) / 8;
   if (pb > pneed) pb = pneed;
   if (MODE == MODE_DV && a.xl)
-    launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL, MODE == MODE_DV>, (unsigned)pb, 256, 0, st, a);
+    launch_pdl(grp_reduce_slice_kernel<MODE, XT, YT, EPL, MODE == MODE_DV>, (unsigned)pb, 256, 0, st, a);
   else
-    launch_pdl(grp_reduce_piece_kernel<MODE, XT, YT, EPL, false>, (unsigned)pb, 256, 0, st, a);
+    launch_pdl(grp_reduce_slice_kernel<MODE, XT, YT, EPL, false>, (unsigned)pb, 256, 0, st, a);
   int64_t cb = (lneed + 7) / 8;
   if (cb > (int64_t)sms * 4) cb = (int64_t)sms * 4;
   launch_pdl(grp_combine_long_kernel<YT, EPL>, (unsigned)cb, 256, 0, st, a);
@@ -810,7 +820,7 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   int64_t rb = ((int64_t)nrows + 1023) / 1024;
   if (rb > (int64_t)num_sms() * 8) rb = (int64_t)num_sms() * 8;
   launch_pdl(grp_runs_kernel, (unsigned)rb, 256, 0, st, g.cnt, nrows, g.off, g.runs_short, g.runs_long,
-                                                g.pieces, g.ctl);
+                                                g.pieces, g.huge, g.ctl);
   launch_pdl(grp_place_kernel, (unsigned)((n + 255) / 256), 256, 0, st, g.keys, g.rank, g.off, wts, n, nrows,
                                                                 g.ent, g.went);
   cudaError_t e = cudaGetLastError();
@@ -818,6 +828,8 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   *launches += 2;
   GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
+  a.huge = g.huge;
+  a.ctl_rw = g.ctl;
   a.og = og;
   a.H = H;
   a.div_h = FastDiv((uint32_t)H);
@@ -1179,6 +1191,7 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   b += align256(sizeof(uint2) * grp_pieces_max(pl.n));             // pieces
   b += align256(sizeof(float) * grp_pieces_max(pl.n) * pl.D);      // piece partials
   b += align256(sizeof(uint32_t) * CTL_WORDS);
+  b += align256(sizeof(uint32_t) * grp_huge_max(pl.n));     // huge runs
   b += align256(sizeof(float) * n_dk);                      // dsS
   b += align256(sizeof(float) * n_dv);                      // dw
   b += align256(dk_tc_workspace_bytes(s));
@@ -1203,6 +1216,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.pieces = (uint2*)p; p += align256(sizeof(uint2) * grp_pieces_max(pl.n));
   w.part = (float*)p; p += align256(sizeof(float) * grp_pieces_max(pl.n) * pl.D);
   w.ctl = (uint32_t*)p; p += align256(sizeof(uint32_t) * CTL_WORDS);
+  w.huge = (uint32_t*)p; p += align256(sizeof(uint32_t) * grp_huge_max(pl.n));
   w.dsS = (float*)p; p += align256(sizeof(float) * n_dk);
   w.dw = (float*)p; p += align256(sizeof(float) * n_dv);
   w.dk_ws = (void*)p; p += align256(dk_tc_workspace_bytes(s));
@@ -1212,7 +1226,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
 // ------------------------------------------------------------ launchers ---
 static GrpScratch grp_scratch(const BwdWorkspace& ws) {
   return GrpScratch{ws.cnt, ws.off, ws.rank, ws.keys, ws.ent, ws.went, ws.runs_short, ws.runs_long,
-                    ws.pieces, ws.part, ws.ctl};
+                    ws.pieces, ws.part, ws.ctl, ws.huge};
 }
 
 cudaError_t launch_scatter_sorted(const Shape& s, const int32_t* idx, const float* w,

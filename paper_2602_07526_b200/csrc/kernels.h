@@ -121,6 +121,7 @@ struct BwdWorkspace {
   uint2* pieces;                  // long-run pieces {long run, j}
   float* part;                    // piece partial rows
   uint32_t* ctl;                  // grouping counters
+  uint32_t* huge;                 // long runs sorted by a CTA
   float* dsS;                     // 2*B*H*k aggregated score grads
   float* dw;                      // B*H*k (when the caller gives none)
   void* dk_ws;                    // tensor-core dQ/dK scratch (bf16 configs)

@@ -36,6 +36,8 @@ sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 def step():
     check(lib.msn_pkm_forward(h, sp, B, _ptr(Q), _ptr(K), _ptr(V), _ptr(out), _ptr(idx), _ptr(w),
                               _ptr(ws), ws.numel()))
+    if not cfg.backward:  # (forward-only configs: C1, C5)
+        return
     check(lib.msn_pkm_scatter(h, sp, B, _ptr(idx), _ptr(w), _ptr(dOut), _ptr(V), _ptr(dV), _ptr(dw),
                               _ptr(ws), ws.numel()))
     check(lib.msn_pkm_backward_keys(h, sp, B, _ptr(Q), _ptr(K), _ptr(idx), _ptr(w), _ptr(dw),
