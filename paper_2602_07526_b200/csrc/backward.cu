@@ -64,7 +64,6 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 constexpr int GRP_SHORT = 32;     // runs up to this length: one warp, one entry per lane
 constexpr int GRP_SLICE = 32;     // long runs are reduced in slices of this many entries (one warp each)
 constexpr int GRP_WARP_SORT = 1024;   // long runs sorted by one warp in registers up to this length
-constexpr int GRP_SORT_SMEM = 16384;  // longer runs: one CTA, in shared memory up to this length
 enum { CTL_TOTAL = 0, CTL_NSHORT = 1, CTL_NLONG = 2, CTL_NPIECES = 3, CTL_NHUGE = 4, CTL_SORTQ = 5,
        CTL_WORDS = 8 };
 __host__ __device__ __forceinline__ uint32_t grp_npieces(uint32_t c) {
@@ -85,7 +84,7 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
                                                        uint32_t nrows, uint32_t* __restrict__ off,
                                                        uint4* __restrict__ runs_short,
                                                        uint4* __restrict__ runs_long,
-                                                       uint2* __restrict__ pieces,
+                                                       uint4* __restrict__ pieces,
                                                        uint32_t* __restrict__ huge,
                                                        uint32_t* __restrict__ ctl) {
   pdl_enter();
@@ -158,7 +157,9 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
       } else {
         const uint32_t li = lb + (es >> 16);
         runs_long[li] = make_uint4(ec, c, (uint32_t)r, ep);
-        for (uint32_t j = 0; j < np; ++j) pieces[ep + j] = make_uint2(li, j);
+        // slice j: {first entry, entries (<= GRP_SLICE), row, long run}
+        for (uint32_t j = 0; j < np; ++j)
+          pieces[ep + j] = make_uint4(ec + j * GRP_SLICE, min((uint32_t)GRP_SLICE, c - j * GRP_SLICE), (uint32_t)r, li);
         if (c > (uint32_t)GRP_WARP_SORT) huge[atomicAdd(&ctl[CTL_NHUGE], 1u)] = li;  // (any order)
       }
     }
@@ -197,7 +198,7 @@ struct GrpArgs {
   const float* wts;       // weight by record id
   const uint4* runs_short;
   const uint4* runs_long;
-  const uint2* pieces;    // long-run slices {long run, j} (GRP_SLICE entries each)
+  const uint4* pieces;    // long-run slices {first entry, entries, row, long run}
   float* part;            // per-slice partial rows
   const uint32_t* ctl;
   const void* X;          // x rows (dOut fp32 or Q)
@@ -225,6 +226,8 @@ struct GrpArgs {
   FastDiv div_xl, div_dl;
   const uint32_t* huge = nullptr;  // long runs > GRP_WARP_SORT entries (indices into runs_long)
   uint32_t* ctl_rw = nullptr;      // = ctl (the sort's work queue counter)
+  float* went_rw = nullptr;        // = went (long runs: rewritten in sorted order by the sort)
+  uint32_t id_shift = 0;           // record id >> id_shift < 256 (the huge runs' bucket)
 };
 
 // Applies the fused update to VW consecutive elements at element offset off
@@ -585,34 +588,124 @@ __device__ __forceinline__ void warp_sort_run(uint32_t* g, int L) {
 }
 
 // Long runs (> 32 entries), step 1: every run's record ids are sorted
-// ascending in place, fixing its summation order.  Runs of more than
-// GRP_WARP_SORT entries (the `huge` list, few) go first, one CTA each, in
-// shared memory up to GRP_SORT_SMEM entries, else in place in global memory;
-// then every warp takes the other runs from a work queue (one atomic per
-// run), sorting each in registers -- so a CTA held up by a huge run does not
-// hold up a static share of the short ones.
+// ascending in place, fixing its summation order, and its weights are
+// rewritten in that order (went[e] = wts[ent[e]]).  Runs of more than
+// GRP_WARP_SORT entries (the `huge` list, few) go first, one CTA each: a
+// two-level sort in shared memory -- bucket by the id's top 8 bits (a
+// counting pass), then every bucket sorted by a warp in registers (a bucket
+// of more than GRP_WARP_SORT entries by the CTA) -- the ascending order of the
+// run either way.  Then every warp takes the other runs from a work queue
+// (one atomic per run), sorting each in registers -- so a CTA held up by a
+// huge run does not hold up a static share of the short ones.
+template <int R>
+__device__ __forceinline__ void warp_sort_run_w(const GrpArgs& a, uint32_t* g, float* gw, int L) {
+  const int lane = threadIdx.x % 32;
+  uint32_t x[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) x[r] = r * 32 + lane < L ? g[r * 32 + lane] : 0xffffffffu;
+  warp_sort_asc<R>(x);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r * 32 + lane < L) {
+      g[r * 32 + lane] = x[r];
+      gw[r * 32 + lane] = a.wts[x[r]];
+    }
+}
+// a warp sorts g[0, L) (L <= GRP_WARP_SORT; gw: the weights in that order, or nullptr)
+__device__ __forceinline__ void warp_sort_any(const GrpArgs& a, uint32_t* g, float* gw, int L) {
+  if (gw) {
+    if (L <= 32) warp_sort_run_w<1>(a, g, gw, L);
+    else if (L <= 64) warp_sort_run_w<2>(a, g, gw, L);
+    else if (L <= 128) warp_sort_run_w<4>(a, g, gw, L);
+    else if (L <= 256) warp_sort_run_w<8>(a, g, gw, L);
+    else if (L <= 512) warp_sort_run_w<16>(a, g, gw, L);
+    else warp_sort_run_w<32>(a, g, gw, L);
+  } else {
+    if (L <= 1) return;
+    if (L <= 32) warp_sort_run<1>(g, L);
+    else if (L <= 64) warp_sort_run<2>(g, L);
+    else if (L <= 128) warp_sort_run<4>(g, L);
+    else if (L <= 256) warp_sort_run<8>(g, L);
+    else if (L <= 512) warp_sort_run<16>(g, L);
+    else warp_sort_run<32>(g, L);
+  }
+}
+constexpr int GRP_BUCKET_SMEM = 8192;  // huge runs bucket-sorted in shared memory up to this length
+constexpr int GRP_SORT_SMEM_BYTES = (2 * GRP_BUCKET_SMEM + 2 * 256 + 8) * 4;
+
 __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
   pdl_enter();
-  extern __shared__ __align__(16) uint32_t s_sort[];  // [GRP_SORT_SMEM]
+  extern __shared__ __align__(16) uint32_t s_sort[];  // [2 * GRP_BUCKET_SMEM + 2 * 256 + 8]
+  const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
   const int64_t nruns = a.ctl[CTL_NLONG];
   const int64_t nhuge = a.ctl[CTL_NHUGE];
   for (int64_t h = blockIdx.x; h < nhuge; h += gridDim.x) {
     const uint4 run = a.runs_long[a.huge[h]];
     const int L = (int)run.y;
-    int P = 1;
-    while (P < L) P <<= 1;
     uint32_t* g = a.ent_rw + run.x;
-    if (P <= GRP_SORT_SMEM) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) s_sort[i] = i < L ? g[i] : 0xffffffffu;
-      __syncthreads();
-      block_bitonic(s_sort, P, P);
-      for (int i = threadIdx.x; i < L; i += blockDim.x) g[i] = s_sort[i];
-      __syncthreads();
-    } else {
+    float* gw = a.went_rw + run.x;
+    if (L > GRP_BUCKET_SMEM) {  // (very long: in place in global memory)
+      int P = 1;
+      while (P < L) P <<= 1;
       block_bitonic(g, L, P);
+      for (int i = tid; i < L; i += blockDim.x) gw[i] = a.wts[g[i]];
+      __syncthreads();
+      continue;
     }
+    uint32_t* sa = s_sort;
+    uint32_t* sb = sa + GRP_BUCKET_SMEM;
+    uint32_t* cnt = sb + GRP_BUCKET_SMEM;  // [256] counts, then the scatter cursors
+    uint32_t* off = cnt + 256;             // [256] bucket offsets
+    uint32_t* wsum = off + 256;            // [8]
+    cnt[tid] = 0u;
+    __syncthreads();
+    for (int i = tid; i < L; i += blockDim.x) {
+      const uint32_t v = g[i];
+      sa[i] = v;
+      atomicAdd(&cnt[v >> a.id_shift], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 256 bucket counts
+    const uint32_t c = cnt[tid];
+    uint32_t x = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += o;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < wid; ++w) pre += wsum[w];
+    off[tid] = pre + x - c;
+    cnt[tid] = pre + x - c;  // cursor
+    __syncthreads();
+    for (int i = tid; i < L; i += blockDim.x) {
+      const uint32_t v = sa[i];
+      sb[atomicAdd(&cnt[v >> a.id_shift], 1u)] = v;  // (any order inside the bucket)
+    }
+    __syncthreads();
+    // cnt[b] is now the end of bucket b
+    for (int b = wid; b < 256; b += 8) {
+      const int o = (int)off[b], n = (int)cnt[b] - o;
+      if (n <= GRP_WARP_SORT) warp_sort_any(a, sb + o, nullptr, n);
+    }
+    __syncthreads();
+    for (int b = 0; b < 256; ++b) {  // (a bucket of more than GRP_WARP_SORT entries: the CTA)
+      const int o = (int)off[b], n = (int)cnt[b] - o;
+      if (n > GRP_WARP_SORT) {
+        int P = 1;
+        while (P < n) P <<= 1;
+        block_bitonic(sb + o, n, P);
+      }
+    }
+    for (int i = tid; i < L; i += blockDim.x) {
+      const uint32_t v = sb[i];
+      g[i] = v;
+      gw[i] = a.wts[v];
+    }
+    __syncthreads();
   }
-  const int lane = threadIdx.x % 32;
   for (;;) {
     uint32_t r = 0;
     if (lane == 0) r = atomicAdd(a.ctl_rw + CTL_SORTQ, 1u);
@@ -620,20 +713,17 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
     if ((int64_t)r >= nruns) break;
     const uint4 run = a.runs_long[r];
     const int L = (int)run.y;
-    uint32_t* g = a.ent_rw + run.x;
-    if (L <= 64) warp_sort_run<2>(g, L);
-    else if (L <= 128) warp_sort_run<4>(g, L);
-    else if (L <= 256) warp_sort_run<8>(g, L);
-    else if (L <= 512) warp_sort_run<16>(g, L);
-    else if (L <= GRP_WARP_SORT) warp_sort_run<32>(g, L);
+    if (L <= GRP_WARP_SORT) warp_sort_any(a, a.ent_rw + run.x, a.went_rw + run.x, L);
   }
 }
 
 // Step 2: one warp per slice of GRP_SLICE consecutive sorted entries of a
 // long run (a flat list over all runs: every warp has a full slice's work,
 // many slices in flight); the slice sum, in entry order, goes to part[slice].
+// The next slice's record is loaded one iteration ahead, so a slice costs
+// two dependent round trips (its ids and weights, then the x rows).
 template <int MODE, typename XT, typename YT, int EPL, bool P2P>
-__global__ void __launch_bounds__(256) grp_reduce_slice_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256, 4) grp_reduce_slice_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
@@ -643,32 +733,30 @@ __global__ void __launch_bounds__(256) grp_reduce_slice_kernel(GrpArgs a) {
   const int64_t np = a.ctl[CTL_NPIECES];
   const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
   const YT* __restrict__ Y = reinterpret_cast<const YT*>(a.Y) + lane * VW;
-  for (int64_t pc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; pc < np; pc += nw) {
-    const uint2 piece = a.pieces[pc];
-    const uint4 run = a.runs_long[piece.x];
-    const int L = (int)run.y;
-    const uint32_t key = run.z;
-    const int j0 = (int)piece.y * GRP_SLICE;
-    const int j1 = min(j0 + GRP_SLICE, L);
+  int64_t pc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  uint4 cur = pc < np ? a.pieces[pc] : make_uint4(0, 0, 0, 0);
+  for (; pc < np; pc += nw) {
+    const uint4 nxt = pc + nw < np ? a.pieces[pc + nw] : make_uint4(0, 0, 0, 0);
+    const int n = (int)cur.y;
+    const uint32_t myid = lane < n ? a.ent[cur.x + lane] : 0u;
+    const float myw = lane < n ? a.went[cur.x + lane] : 0.f;
     float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
-      for (int i = 0; i < NVEC; ++i) ldg_vec<YT, VW>(Y + (int64_t)key * D + i * 32 * VW, y + i * VW);
+      for (int i = 0; i < NVEC; ++i) ldg_vec<YT, VW>(Y + (int64_t)cur.z * D + i * 32 * VW, y + i * VW);
     }
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
-    // the slice's ids, one per lane, then consumed in order
-    const uint32_t myid = j0 + lane < j1 ? a.ent[run.x + j0 + lane] : 0u;
-    const float myw = j0 + lane < j1 ? a.wts[myid] : 0.f;
     grp_accumulate<MODE, XT, EPL, U, P2P>(
-        a, j0, j1,
+        a, 0, n,
         [&](int j, float& w_) {
-          w_ = __shfl_sync(0xffffffffu, myw, (j - j0) & 31);
-          return __shfl_sync(0xffffffffu, myid, (j - j0) & 31);
+          w_ = __shfl_sync(0xffffffffu, myw, j);
+          return __shfl_sync(0xffffffffu, myid, j);
         },
         y, acc);
 #pragma unroll
     for (int i = 0; i < NVEC; ++i) stg_vec<VW>(a.part + pc * D + lane * VW + i * 32 * VW, acc + i * VW);
+    cur = nxt;
   }
 }
 
@@ -734,7 +822,7 @@ struct GrpScratch {
   float* went;      // [n]
   uint4* runs_short;  // [min(n, rows)]
   uint4* runs_long;   // [n / 33 + 1]
-  uint2* pieces;    // [grp_pieces_max(n)]
+  uint4* pieces;    // [grp_pieces_max(n)]
   float* part;      // [grp_pieces_max(n) * D]
   uint32_t* ctl;    // CTL_WORDS
   uint32_t* huge;   // [grp_huge_max(n)]
@@ -778,13 +866,13 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   // long runs: sort, pieces, combine
   static std::atomic<uint64_t> attr{0};
   {
-    cudaError_t e = smem_attr_once(attr, grp_sort_long_kernel, GRP_SORT_SMEM * 4);
+    cudaError_t e = smem_attr_once(attr, grp_sort_long_kernel, GRP_SORT_SMEM_BYTES);
     if (e != cudaSuccess) return e;
   }
   const int64_t lneed = n / (GRP_SHORT + 1) + 1;
   int64_t lb = (lneed + 7) / 8;
   if (lb > (int64_t)sms * 3) lb = (int64_t)sms * 3;
-  launch_pdl(grp_sort_long_kernel, (unsigned)lb, 256, GRP_SORT_SMEM * 4, st, a);
+  launch_pdl(grp_sort_long_kernel, (unsigned)lb, 256, GRP_SORT_SMEM_BYTES, st, a);
   int64_t pb = (int64_t)sms * 8;
   const int64_t pneed = (grp_pieces_max(n) + 7) / 8;
   if (pb > pneed) pb = pneed;
@@ -830,6 +918,12 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
   a.huge = g.huge;
   a.ctl_rw = g.ctl;
+  a.went_rw = g.went;
+  {
+    uint32_t bits = 0;
+    while (bits < 32 && (uint64_t(1) << bits) < (uint64_t)n) ++bits;
+    a.id_shift = bits > 8 ? bits - 8 : 0;
+  }
   a.og = og;
   a.H = H;
   a.div_h = FastDiv((uint32_t)H);
@@ -1188,7 +1282,7 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   b += 4 * align256(sizeof(uint32_t) * pl.n);               // rank, keys, ent, went
   b += align256(sizeof(uint4) * nshort);                    // runs_short
   b += align256(sizeof(uint4) * (pl.n / (GRP_SHORT + 1) + 1));  // runs_long
-  b += align256(sizeof(uint2) * grp_pieces_max(pl.n));             // pieces
+  b += align256(sizeof(uint4) * grp_pieces_max(pl.n));             // slices
   b += align256(sizeof(float) * grp_pieces_max(pl.n) * pl.D);      // piece partials
   b += align256(sizeof(uint32_t) * CTL_WORDS);
   b += align256(sizeof(uint32_t) * grp_huge_max(pl.n));     // huge runs
@@ -1213,7 +1307,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.went = (float*)p; p += align256(sizeof(uint32_t) * pl.n);
   w.runs_short = (uint4*)p; p += align256(sizeof(uint4) * nshort);
   w.runs_long = (uint4*)p; p += align256(sizeof(uint4) * (pl.n / (GRP_SHORT + 1) + 1));
-  w.pieces = (uint2*)p; p += align256(sizeof(uint2) * grp_pieces_max(pl.n));
+  w.pieces = (uint4*)p; p += align256(sizeof(uint4) * grp_pieces_max(pl.n));
   w.part = (float*)p; p += align256(sizeof(float) * grp_pieces_max(pl.n) * pl.D);
   w.ctl = (uint32_t*)p; p += align256(sizeof(uint32_t) * CTL_WORDS);
   w.huge = (uint32_t*)p; p += align256(sizeof(uint32_t) * grp_huge_max(pl.n));

@@ -118,7 +118,7 @@ struct BwdWorkspace {
   uint32_t *rank, *keys, *ent;    // per-contribution rank, row key, grouped record ids
   float* went;                    // grouped weights
   uint4 *runs_short, *runs_long;  // run records {offset, length, row, first piece}
-  uint2* pieces;                  // long-run pieces {long run, j}
+  uint4* pieces;                  // long-run slices {first entry, entries, row, long run}
   float* part;                    // piece partial rows
   uint32_t* ctl;                  // grouping counters
   uint32_t* huge;                 // long runs sorted by a CTA
