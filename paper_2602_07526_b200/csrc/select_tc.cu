@@ -208,15 +208,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       for (int g = 0; g < total_chunks; ++g) {
         const int c = g % p.n_chunks;
-        const bool lo = TF32 && !(WIDE && g < p.n_chunks);  // 1xTF32 first sweep: K_hi only
-        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        const bool one = TF32 && WIDE && g < p.n_chunks;  // 1xTF32 first sweep: K_hi only ...
+        const int kstep = one ? 2 : 1;                     // ... two k-blocks per stage (both halves)
+        const int krow = hh * p.n_sub + col_seg + c * p.n_tile;
+        for (int kb = 0; kb < p.k_blocks; kb += kstep, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], lo ? stage_bytes : p.n_tile * kRowBytes);
-          tma_load_2d(sB + s * stage_bytes, &tmap_k, &full[s], kb * BK, hh * p.n_sub + col_seg + c * p.n_tile);
-          if (lo)
-            tma_load_2d(sB + s * stage_bytes + p.n_tile * kRowBytes, &tmap_klo, &full[s], kb * BK,
-                        hh * p.n_sub + col_seg + c * p.n_tile);
+          const bool second = TF32 && (!one || kb + 1 < p.k_blocks);
+          mbar_expect_tx(&full[s], second ? stage_bytes : p.n_tile * kRowBytes);
+          tma_load_2d(sB + s * stage_bytes, &tmap_k, &full[s], kb * BK, krow);
+          if (second)
+            tma_load_2d(sB + s * stage_bytes + p.n_tile * kRowBytes, one ? &tmap_k : &tmap_klo, &full[s],
+                        (one ? kb + 1 : kb) * BK, krow);
         }
       }
     }
@@ -235,7 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[buf], ((g >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + buf * acc_stride;
-        for (int kb = 0; kb < p.k_blocks; ++kb, ++it) {
+        const bool one = TF32 && WIDE && g < p.n_chunks;
+        const int kstep = one ? 2 : 1;
+        for (int kb = 0; kb < p.k_blocks; kb += kstep, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
           tc_fence_after();
@@ -243,14 +248,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = smem_u32(sB + s * stage_bytes);
           if constexpr (TF32) {
             // 3xTF32: A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (the lo.lo term is below fp32 rounding);
-            // the first sweep of a two-sweep row: A_hi.B_hi only (pass A, margin d)
+            // the first sweep of a two-sweep row: A_hi.B_hi only (pass A, margin d), the
+            // stage holding k-blocks kb and kb + 1
             const uint32_t b1 = b0 + p.n_tile * kRowBytes;
-            const bool one = WIDE && g < p.n_chunks;
+            if (one) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint32_t acc = (kb | kk) != 0;
-              tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, acc);
-              if (!one) {
+              for (int kk = 0; kk < BK / 8; ++kk)
+                tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+              if (kb + 1 < p.k_blocks) {
+                const uint32_t a1 = a0 + 16384;
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk)
+                  tc_mma_tf32(d, sw128_desc(a1 + kk * 32), sw128_desc(b1 + kk * 32), idesc, 1);
+              }
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint32_t acc = (kb | kk) != 0;
+                tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, acc);
                 tc_mma_tf32(d, sw128_desc(a0 + kk * 32), sw128_desc(b1 + kk * 32), idesc, 1);
                 tc_mma_tf32_ts(d, tmem + alo_col + kb * BK + kk * 8, sw128_desc(b0 + kk * 32), idesc, 1);
               }
