@@ -331,6 +331,26 @@ __device__ __forceinline__ void red_vec(float* p, const float* v) {
     for (int i = 0; i < VW; ++i) atomicAdd(p + i, v[i]);
   }
 }
+// the same with an L2 eviction-priority policy (common.cuh)
+template <typename T, int VW>
+__device__ __forceinline__ void ldg_vec_pol(const T* p, float* f, uint64_t pol) {
+  if constexpr (sizeof(T) == 4 && VW == 4) {
+    const uint4 v = ldg_v4_pol(p, pol);
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  } else if constexpr (sizeof(T) == 2 && VW == 4) {
+    const uint2 v = ldg_v2_pol(p, pol);
+    f[0] = __uint_as_float(v.x << 16); f[1] = __uint_as_float(v.x & 0xffff0000u);
+    f[2] = __uint_as_float(v.y << 16); f[3] = __uint_as_float(v.y & 0xffff0000u);
+  } else {
+    ldg_vec<T, VW>(p, f);
+  }
+}
+template <int VW>
+__device__ __forceinline__ void red_vec_pol(float* p, const float* v, uint64_t pol) {
+  if constexpr (VW == 4) red_add_v4_pol(p, v[0], v[1], v[2], v[3], pol);
+  else red_vec<VW>(p, v);
+}
 template <int VW>
 __device__ __forceinline__ void stg_vec(float* p, const float* v) {
   if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
@@ -354,7 +374,7 @@ __device__ __forceinline__ uint32_t grp_xrow(const GrpArgs& a, uint32_t rec) {
 // U x rows in flight at a time; MODE_DV also writes dw[rec] = <y, x>.
 template <int MODE, typename XT, int EPL, int U, bool P2P, typename Src>
 __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1, Src src,
-                                               const float* y, float* acc) {
+                                               const float* y, float* acc, uint64_t xpol) {
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
@@ -384,7 +404,11 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
           xrow = X + xr * D;
         }
 #pragma unroll
-        for (int i = 0; i < NVEC; ++i) ldg_vec<XT, VW>(xrow + i * 32 * VW, x[u] + i * VW);
+        for (int i = 0; i < NVEC; ++i) {
+          // d_out rows (MODE_DV) are re-read by ~H k records each: kept in L2
+          if constexpr (MODE == MODE_DV) ldg_vec_pol<XT, VW>(xrow + i * 32 * VW, x[u] + i * VW, xpol);
+          else ldg_vec<XT, VW>(xrow + i * 32 * VW, x[u] + i * VW);
+        }
       } else {
         rec[u] = 0xffffffffu;
         wt[u] = 0.f;
@@ -452,6 +476,7 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
   const int64_t nruns = a.ctl[CTL_NSHORT];
   const YT* __restrict__ Y = reinterpret_cast<const YT*>(a.Y) + lane * VW;
   float* __restrict__ Gl = a.G + lane * VW;
+  const uint64_t pol_once = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
   uint4 cur = c < nruns ? a.runs_short[c] : make_uint4(0, 0, 0, 0);
   uint4 nxt = c + nw < nruns ? a.runs_short[c + nw] : make_uint4(0, 0, 0, 0);
   uint32_t me = 0xffffffffu;
@@ -468,7 +493,7 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
     float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
-      for (int i = 0; i < NVEC; ++i) ldg_vec<YT, VW>(Y + (int64_t)key * D + i * 32 * VW, y + i * VW);
+      for (int i = 0; i < NVEC; ++i) ldg_vec_pol<YT, VW>(Y + (int64_t)key * D + i * 32 * VW, y + i * VW, pol_once);
     }
     // next run's entries and the record after it; that run's value row is
     // pulled into L2 now (two iterations ahead of its use, no registers held)
@@ -504,14 +529,14 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
           w_ = __shfl_sync(0xffffffffu, cw, s);
           return __shfl_sync(0xffffffffu, ce, s);
         },
-        y, acc);
+        y, acc, pol_keep);
     if constexpr (MODE == MODE_DV && UPD) {
 #pragma unroll
       for (int i = 0; i < NVEC; ++i)
         update_vec<YT, VW>(a, (int64_t)key * D + (i * 32 + lane) * VW, y + i * VW, acc + i * VW);
     } else {
 #pragma unroll
-      for (int i = 0; i < NVEC; ++i) red_vec<VW>(Gl + (int64_t)key * D + i * 32 * VW, acc + i * VW);
+      for (int i = 0; i < NVEC; ++i) red_vec_pol<VW>(Gl + (int64_t)key * D + i * 32 * VW, acc + i * VW, pol_once);
     }
     cur = nxt;
     nxt = nn;
@@ -735,6 +760,7 @@ __global__ void __launch_bounds__(256, 4) grp_reduce_slice_kernel(GrpArgs a) {
   const YT* __restrict__ Y = reinterpret_cast<const YT*>(a.Y) + lane * VW;
   int64_t pc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   uint4 cur = pc < np ? a.pieces[pc] : make_uint4(0, 0, 0, 0);
+  const uint64_t pol_once = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
   for (; pc < np; pc += nw) {
     const uint4 nxt = pc + nw < np ? a.pieces[pc + nw] : make_uint4(0, 0, 0, 0);
     const int n = (int)cur.y;
@@ -743,7 +769,7 @@ __global__ void __launch_bounds__(256, 4) grp_reduce_slice_kernel(GrpArgs a) {
     float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
-      for (int i = 0; i < NVEC; ++i) ldg_vec<YT, VW>(Y + (int64_t)cur.z * D + i * 32 * VW, y + i * VW);
+      for (int i = 0; i < NVEC; ++i) ldg_vec_pol<YT, VW>(Y + (int64_t)cur.z * D + i * 32 * VW, y + i * VW, pol_once);
     }
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
@@ -753,7 +779,7 @@ __global__ void __launch_bounds__(256, 4) grp_reduce_slice_kernel(GrpArgs a) {
           w_ = __shfl_sync(0xffffffffu, myw, j);
           return __shfl_sync(0xffffffffu, myid, j);
         },
-        y, acc);
+        y, acc, pol_keep);
 #pragma unroll
     for (int i = 0; i < NVEC; ++i) stg_vec<VW>(a.part + pc * D + lane * VW + i * 32 * VW, acc + i * VW);
     cur = nxt;
@@ -805,7 +831,8 @@ __global__ void __launch_bounds__(256) grp_combine_long_kernel(GrpArgs a) {
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < NVEC; ++i) red_vec<VW>(a.G + (int64_t)run.z * D + lane * VW + i * 32 * VW, acc + i * VW);
+      for (int i = 0; i < NVEC; ++i)
+        red_vec_pol<VW>(a.G + (int64_t)run.z * D + lane * VW + i * 32 * VW, acc + i * VW, l2_policy_evict_first());
     }
   }
 }

@@ -170,6 +170,38 @@ __device__ __forceinline__ uint4 ldg_v4(const void* p) {
   return r;
 }
 
+// L2 eviction-priority policies (createpolicy) and loads / reductions
+// carrying them: rows streamed once (value rows, gradient rows) are marked
+// evict_first, rows re-read from L2 many times (d_out) evict_last, so the
+// stream does not push the reused rows out of the 126 MB L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_v4_pol(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_v2_pol(const void* p, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void red_add_v4_pol(float* p, float a, float b, float c, float d, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d), "l"(pol)
+               : "memory");
+}
+
 // unpack a 16-byte vector of T into fp32
 template <typename T>
 __device__ __forceinline__ void unpack16(const uint4& v, float* f);

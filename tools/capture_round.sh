@@ -18,7 +18,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/ref.json 
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --nvtx --nvtx-include "prof/" --csv --log-file $O/c4_launches.csv python tools/prof_sharded.py > /dev/null 2>&1
 echo "c4 launches rc=$?"
-for w in c2_mid_bf16 c3_train_fp32_zipf; do
+for w in c2_mid_bf16 c3_train_fp32_zipf c5_latency_bf16; do
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
       --nvtx --nvtx-include "prof/" --csv --log-file $O/${w}_launches.csv python tools/prof_step.py $w > /dev/null 2>&1
   echo "$w launches rc=$?"
@@ -29,3 +29,7 @@ ncu -i $O/c4_full.ncu-rep --page raw --csv > $O/c4_full_raw.csv 2>/dev/null
 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "prof/" -o $O/c2_full \
     python tools/prof_step.py c2_mid_bf16 > $O/ncu_full_c2.log 2>&1; echo "c2 full rc=$?"
 ncu -i $O/c2_full.ncu-rep --page raw --csv > $O/c2_full_raw.csv 2>/dev/null
+# the roofline kernels' DRAM traffic -> profiles/traffic.json (run here; copy back)
+python tools/traffic_json.py $T c4_large_sharded_bf16_xchg=$O/c4_full_raw.csv c2_mid_bf16=$O/c2_full_raw.csv > $O/traffic.log 2>&1
+cp profiles/traffic.json $O/traffic.json
+rm -f $O/*.ncu-rep
