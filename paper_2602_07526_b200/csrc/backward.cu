@@ -897,10 +897,12 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
     if (e != cudaSuccess) return e;
   }
   const int64_t lneed = n / (GRP_SHORT + 1) + 1;
+  // (all three grids one wave of grid-stride / work-queue CTAs: with no long
+  // run -- uniform traffic -- each launch reads its counter and exits)
   int64_t lb = (lneed + 7) / 8;
-  if (lb > (int64_t)sms * 3) lb = (int64_t)sms * 3;
+  if (lb > (int64_t)sms * 2) lb = (int64_t)sms * 2;
   launch_pdl(grp_sort_long_kernel, (unsigned)lb, 256, GRP_SORT_SMEM_BYTES, st, a);
-  int64_t pb = (int64_t)sms * 8;
+  int64_t pb = (int64_t)sms * 4;
   const int64_t pneed = (grp_pieces_max(n) + 7) / 8;
   if (pb > pneed) pb = pneed;
   if (MODE == MODE_DV && a.xl)
@@ -908,7 +910,7 @@ cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream
   else
     launch_pdl(grp_reduce_slice_kernel<MODE, XT, YT, EPL, false>, (unsigned)pb, 256, 0, st, a);
   int64_t cb = (lneed + 7) / 8;
-  if (cb > (int64_t)sms * 4) cb = (int64_t)sms * 4;
+  if (cb > (int64_t)sms * 2) cb = (int64_t)sms * 2;
   launch_pdl(grp_combine_long_kernel<YT, EPL>, (unsigned)cb, 256, 0, st, a);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) *launches += 4;
