@@ -58,6 +58,11 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 #ifndef MSN_SHORT_U
 #define MSN_SHORT_U 2  // x rows in flight per warp in the short-run reducer (8 values/lane)
 #endif
+#ifndef MSN_G_PREFETCH
+#define MSN_G_PREFETCH 0  // L2 prefetch of the gradient row two runs ahead of its reduction (off: the
+                          // red.add is fire-and-forget; a prefetched line evicted before it is read
+                          // twice -- C4 DRAM reads 4.77 -> 4.54 GB, reducer 1252 -> 1225 us)
+#endif
 #ifndef MSN_SHORT_BPS
 #define MSN_SHORT_BPS 4  // resident blocks per SM of the short-run reducer (8 values/lane)
 #endif
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
     }
     {  // ... and its gradient row, which the row's single reduction updates in L2
       constexpr int GLINES = (D * 4 + 127) / 128;
-      if (!UPD && lane >= 32 - GLINES && c + 2 * nw < nruns)
+      if (MSN_G_PREFETCH && !UPD && lane >= 32 - GLINES && c + 2 * nw < nruns)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.G) +
                                                        (int64_t)nn.z * D * 4 + (31 - lane) * 128));
     }
