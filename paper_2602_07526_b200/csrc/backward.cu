@@ -58,6 +58,9 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 #ifndef MSN_SHORT_U
 #define MSN_SHORT_U 2  // x rows in flight per warp in the short-run reducer (8 values/lane)
 #endif
+#ifndef MSN_V_PREFETCH
+#define MSN_V_PREFETCH 1  // L2 prefetch of the value row two runs ahead of its load
+#endif
 #ifndef MSN_G_PREFETCH
 #define MSN_G_PREFETCH 0  // L2 prefetch of the gradient row two runs ahead of its reduction (off: the
                           // red.add is fire-and-forget; a prefetched line evicted before it is read
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
     const uint4 nn = c + 2 * nw < nruns ? a.runs_short[c + 2 * nw] : make_uint4(0, 0, 0, 0);
     if constexpr (MODE == MODE_DV) {
       constexpr int LINES = (D * (int)sizeof(YT) + 127) / 128;
-      if (lane < LINES && c + 2 * nw < nruns)
+      if (MSN_V_PREFETCH && lane < LINES && c + 2 * nw < nruns)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.Y) +
                                                        (int64_t)nn.z * D * (int)sizeof(YT) + lane * 128));
     }
