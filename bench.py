@@ -598,8 +598,10 @@ def run_sharded(args, rank, world, local_rank):
                                                   _ptr(dVs), _ptr(dw), _ptr(ws), ws.numel()))
             launches[0] = n + lk.last_launch_count()
         else:
+            c0 = sp.launch_count
             o, tape = sp.forward(q_l, K, Vs)
             sp.backward(d_l, q_l, K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
+            launches[0] = sp.launch_count - c0
 
     for _ in range(args.warmup):
         flush.zero_()

@@ -127,6 +127,11 @@ class ShardedPKM:
         self.ph = phases
         self.xb = ExchangeBuffer(phases, local_batch, self.world, self.rank, transport, group, device)
         self.ws = phases.workspace(local_batch, self.world * local_batch)
+        self.launch_count = 0  # library kernel launches issued by this object (all calls)
+
+    def _counted(self, r):
+        self.launch_count += self.ph.last_launch_count()
+        return r
 
     @property
     def exchange(self):
@@ -142,14 +147,14 @@ class ShardedPKM:
         """Returns (out [B_l, d_v], tape (idx, w)) for the local queries."""
         x = self.xb.x
         if self.transport == "peer":
-            out, idx, w = self.ph.forward_sharded(query, subkeys, value_shard, x, out=out, ws=self.ws)
+            out, idx, w = self._counted(self.ph.forward_sharded(query, subkeys, value_shard, x, out=out, ws=self.ws))
             return out, (idx, w)
-        idx, w, out = self.ph.exchange_select(query, subkeys, value_shard, x, out=out, ws=self.ws)
+        idx, w, out = self._counted(self.ph.exchange_select(query, subkeys, value_shard, x, out=out, ws=self.ws))
         self._move_records()
-        self.ph.exchange_gather(value_shard, x)
+        self._counted(self.ph.exchange_gather(value_shard, x))
         P, lb, dv = self.world, self.local_batch, self.d_value
         self._a2a(self.xb.region("PART_IN", P * lb * dv), self.xb.region("PART_OUT", P * lb * dv))
-        out = self.ph.exchange_combine(x, out)
+        out = self._counted(self.ph.exchange_combine(x, out))
         return out, (idx, w)
 
     # ----------------------------------------------------------- backward
@@ -165,8 +170,9 @@ class ShardedPKM:
             d_subkeys = torch.zeros((self.heads, 2, self.n_sub, self.d_half), dtype=torch.float32, device=dev)
         x = self.xb.x
         if self.transport == "peer":
-            dq, dK, dV, dw = self.ph.backward_sharded(d_out.float().contiguous(), query, subkeys, value_shard,
-                                                      idx, w, x, d_subkeys, d_value_shard, ws=self.ws)
+            dq, dK, dV, dw = self._counted(self.ph.backward_sharded(d_out.float().contiguous(), query, subkeys,
+                                                                    value_shard, idx, w, x, d_subkeys,
+                                                                    d_value_shard, ws=self.ws))
             return dq, dK, dV, dw
         P, lb, dv = self.world, self.local_batch, self.d_value
         dall = self.xb.region("DOUT_ALL", P * lb, dv)
@@ -174,11 +180,11 @@ class ShardedPKM:
             dist.all_gather_into_tensor(dall, d_out.float().contiguous(), group=self.group)
         else:
             dall.copy_(d_out)
-        self.ph.exchange_scatter(value_shard, d_value_shard, x, ws=self.ws)
+        self._counted(self.ph.exchange_scatter(value_shard, d_value_shard, x, ws=self.ws))
         P, cap = self.world, self.xb.cap
         self._a2a(self.xb.region("DW_IN", P * cap), self.xb.region("DW_OUT", P * cap))
-        dw = self.ph.exchange_collect(idx, x)
-        dq, d_subkeys = self.ph.backward_keys(query, subkeys, idx, w, dw, d_subkeys)
+        dw = self._counted(self.ph.exchange_collect(idx, x))
+        dq, d_subkeys = self._counted(self.ph.backward_keys(query, subkeys, idx, w, dw, d_subkeys))
         return dq, d_subkeys, d_value_shard, dw
 
     # ------------------------------------------- the NCCL (staged) moves

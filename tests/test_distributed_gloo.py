@@ -42,6 +42,9 @@ class OraclePhases:
     def workspace(self, B, gb=None):
         return torch.empty(1, dtype=torch.uint8)
 
+    def last_launch_count(self):
+        return 0  # (no GPU kernels here)
+
     def exchange_select(self, q, K, Vs, x, out=None, ws=None):
         """a1-a4 (oracle), then the route into the OUT windows (records of query b
         for owner o at [b H k, b H k + cnt) in (h, t) order) and the local
