@@ -1157,31 +1157,34 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
     }
     if constexpr (OUT == OUT_COMPACT) {
       // the m records sorted by sub-key (rank = number of smaller indices;
-      // the indices are distinct), and per dK tile of tile_rows sub-keys the
-      // offset of its first record: tile t's records are [off[t], off[t+1]),
-      // so the dK tile builder reads only its own (dk_tc.cu)
-      uint2* rec = reinterpret_cast<uint2*>(dSd) + (l * 2 + half) * (int64_t)k;
-      uint8_t* off = reinterpret_cast<uint8_t*>(reinterpret_cast<uint2*>(dSd) + (int64_t)L * 2 * k) +
+      // the indices are distinct), and per block of tile_rows sub-keys
+      // the end of its records: block t's records are [t ? off[t-1] : 0,
+      // off[t]) (blocks of one dK tile, tile_rows sub-keys), so the dK tile
+      // builder reads only its own (dk_tc.cu)
+      // a record = bf16(dS) << 16 | sub-key (n_sub <= 2048; both consumers
+      // multiply by the bf16-rounded dS), 0xffffffff past m
+      uint32_t* rec = reinterpret_cast<uint32_t*>(dSd) + (l * 2 + half) * (int64_t)k;
+      uint8_t* off = reinterpret_cast<uint8_t*>(reinterpret_cast<uint32_t*>(dSd) + (int64_t)L * 2 * k) +
                      (l * 2 + half) * 32;
       for (int c = lane; c < k; c += 32) {
         if (c < m) {
           const int32_t r = s_r[wid][half][c];
           int rk = 0;
           for (int j = 0; j < m; ++j) rk += s_r[wid][half][j] < r;
-          rec[rk] = make_uint2((uint32_t)r, __float_as_uint(s_d[wid][half][c]));
+          rec[rk] = ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(s_d[wid][half][c])) << 16) | (uint32_t)r;
         } else {
-          rec[c] = make_uint2(0xffffffffu, 0u);
+          rec[c] = 0xffffffffu;
         }
       }
-      int below = 0;  // lane t: records with sub-key < t tile_rows
+      int below = 0;  // lane t: records with sub-key < (t + 1) tile_rows
       for (int c = 0; c < m; c += 32) {
         const int idx0 = c + lane < m ? s_r[wid][half][c + lane] : 0x7fffffff;
-        for (int t = 0; t <= ntiles; ++t) {
-          const int n = __popc(__ballot_sync(0xffffffffu, idx0 < t * tile_rows));
+        for (int t = 0; t < ntiles; ++t) {
+          const int n = __popc(__ballot_sync(0xffffffffu, idx0 < (t + 1) * tile_rows));
           if (lane == t) below += n;
         }
       }
-      if (lane <= ntiles) off[lane] = (uint8_t)below;
+      if (lane < ntiles) off[lane] = (uint8_t)below;
     }
   }
   if constexpr (!DQ) return;  // dQ = dSd . K runs on the tensor cores (dk_tc.cu)
@@ -1479,6 +1482,7 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   const int E = epl_of(s.d_h);
   const bool dense = dk_tc_supported(s);
   const bool dq_tc = dense && dq_tc_wanted(s);
+  const bool dq_rec = dense && !dq_tc && dk_compact(s) && dq_rec_wanted(s);  // dQ on the tensor cores from the records
   const GrpScratch g = grp_scratch(ws);
   if (!dense) {
     cudaError_t e0 = grp_begin(g, nrows, st);
@@ -1493,6 +1497,11 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_DENSE, true>, blocks, 256, 0, st,                         \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
         g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16, 0, 0);           \
+  else if (dense && dq_rec)                                                                    \
+    launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_COMPACT, false>, blocks, 256, 0, st,                      \
+        (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
+        g.cnt, g.rank, (uint16_t*)ws.dk_ws, s.H / s.og, (int32_t)s.tab_stride, s.dq_bf16,        \
+        dk_tile_rows(s), s.n_sub / dk_tile_rows(s));                                             \
   else if (dense)                                                                              \
     launch_pdl(ds_dq_kernel<QT, KPL, E_, OUT_COMPACT, true>, blocks, 256, 0, st,                       \
         (const QT*)K, idx, w, dw, L, s.H, s.n_sub, s.d_h, s.k, dQ, g.keys, ws.dsS, nrows,       \
@@ -1516,7 +1525,7 @@ cudaError_t launch_backward_keys(const Shape& s, const void* Q, const void* K,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ++*launches;
-  if (dense) return launch_dk_tc(s, Q, K, dQ, dK, ws.dk_ws, st, launches, dq_tc);
+  if (dense) return launch_dk_tc(s, Q, K, dQ, dK, ws.dk_ws, st, launches, dq_tc || dq_rec);
   const int64_t n = 2 * L * s.k;
   if (s.qk_dt == F32)
     return grp_finish<MODE_DK, float, float>(g, n, nrows, ws.dsS, Q, nullptr, nullptr, dK, s.H,

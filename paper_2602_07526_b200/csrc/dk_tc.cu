@@ -31,6 +31,8 @@ using namespace tc;
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 TMEM alloc + epilogue (tile (w-2)/4)
 constexpr int kCtasPerSm = 1;
 constexpr int kDqStages = 4;
+constexpr int kDqStagesRec = 4;   // REC: + the staged records (2 x 128 queries x k <= 32 records of 4 B)
+constexpr int kDqRecBytes = 2 * 128 * 32 * 4;
 // MT 128-row tiles per CTA share every B stage (M = 128 MT): stages of
 // (16 MT + 32) KB at d_h = 256, up to ~192 KB of ring
 __host__ __device__ constexpr int stages_for(int MT) { return MT == 1 ? 4 : 3; }
@@ -49,7 +51,7 @@ struct DkParams {
   int64_t q_per_split;  // queries per split (multiple of kBK)
   float* out;           // partials [S][H*2][n_sub][d_h] (or dK itself when S == 1)
   int accumulate;       // 1: out += acc (S == 1, out = dK); 0: out = acc
-  const uint2* rec;     // REC: compact records [B][H*2][k] {sub-key, dS bits}
+  const uint32_t* rec;  // REC: compact records [B][H*2][k] bf16(dS) << 16 | sub-key
   int k;
 };
 
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const int ql = u >> 2, part = u & 3;
       const int HH = 2 * p.H;
       constexpr int kNr = 4;  // records per thread held one k-block ahead (more: loaded when used)
+      constexpr uint32_t kNone = 0xffffffffu;
       const int64_t nlh = p.B * HH;  // lookup-halves (the per-tile offsets follow the records)
       const uint8_t* offs = reinterpret_cast<const uint8_t*>(p.rec + nlh * p.k);
       const int tile = blockIdx.x;   // this CTA's sub-key tile (kBM * MT rows)
@@ -173,18 +176,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       // (per-tile offsets written by ds_dq_kernel); the 4 threads of the query
       // take every 4th.  Offsets run two k-blocks ahead, records one.
       // (two byte loads whose values are only used a k-block later: no stall here)
+      // (offsets per tile: tile t's records end at o[t])
       auto load_off = [&](int kb, int& lo, int& hi) {
         const bool ok = kb < nkb && q0 + (int64_t)kb * kBK + ql < q1;
-        const uint8_t* o = offs + lh_of(ok ? kb : 0) * 32 + tile;
-        lo = ok ? (int)o[0] : 0;
-        hi = ok ? (int)o[1] : 0;
+        const uint8_t* o = offs + lh_of(ok ? kb : 0) * 32;
+        lo = ok && tile ? (int)o[tile - 1] : 0;
+        hi = ok ? (int)o[tile] : 0;
       };
-      auto load_rec = [&](int kb, int lo, int hi, uint2 (&x)[kNr]) {
-        const uint2* r = p.rec + lh_of(kb < nkb ? kb : 0) * p.k;
+      auto load_rec = [&](int kb, int lo, int hi, uint32_t (&x)[kNr]) {
+        const uint32_t* r = p.rec + lh_of(kb < nkb ? kb : 0) * p.k;
 #pragma unroll
         for (int c = 0; c < kNr; ++c) {
           const int j = lo + part + 4 * c;
-          x[c] = j < hi ? r[j] : make_uint2(0xffffffffu, 0u);
+          x[c] = j < hi ? r[j] : kNone;
         }
       };
       // offsets and records of k-block kb + kPre into L2 now
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       int lo0, hi0, lo1, hi1;
       load_off(0, lo0, hi0);
       load_off(1, lo1, hi1);
-      uint2 cur[kNr], nr[kNr];
+      uint32_t cur[kNr], nr[kNr];
       load_rec(0, lo0, hi0, cur);
       int s = 0;
       uint32_t ph = 0;
@@ -222,20 +226,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           *reinterpret_cast<uint4*>(a + (c16 >> 3) * kAtom + ql * 128 + (c16 & 7) * 16) = make_uint4(0, 0, 0, 0);
         }
         __syncwarp();
-        auto put = [&](uint2 r) {
-          const uint32_t il = r.x - (uint32_t)i0;
+        auto put = [&](uint32_t r) {
+          const uint32_t il = (r & 0xffffu) - (uint32_t)i0;  // (the sentinel's 0xffff is past every tile)
           if (il < (uint32_t)(kBM * MT)) {
             const uint32_t e = il & 63u;
             const uint32_t off = (il >> 6) * kAtom + ((((e >> 3) ^ (uint32_t)(ql & 7))) << 4) + (e & 7u) * 2;
-            asm volatile("st.shared.b16 [%0], %1;" ::"r"(abase + off),
-                         "h"(__bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r.y))))
-                         : "memory");
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(abase + off), "h"((unsigned short)(r >> 16)) : "memory");
           }
         };
 #pragma unroll
         for (int c = 0; c < kNr; ++c) put(cur[c]);
         {  // (rare) more than 4 kNr records of this query in the tile
-          const uint2* r = p.rec + lh_of(kb) * p.k;
+          const uint32_t* r = p.rec + lh_of(kb) * p.k;
           for (int j = lo0 + part + 4 * kNr; j < hi0; j += 4) put(r[j]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -306,13 +308,25 @@ struct DqParams {
   int H, n_sub, d_h;
   float* dQ;  // [B, H*2, d_h] (bf16 when bf16_out)
   int bf16_out = 0;
+  const uint32_t* rec = nullptr;  // REC: compact records [B][H*2][k] (bf16(dS) << 16 | sub-key) + block offsets
+  int k = 0;
 };
+// REC: 4 more warps (10..13) build the A tiles from the records
+__host__ __device__ constexpr int dq_threads(bool rec) { return rec ? kThreads + 128 : kThreads; }
 
 // Persistent: one CTA per SM walks the (query tile, head.half) tiles in
 // hh-major order (the K block of an hh stays hot in L2); two TMEM
 // accumulators, so the MMA of tile i+1 runs while the epilogue drains tile i,
 // and the TMA ring streams the k-blocks of successive tiles without a break.
-__global__ void __launch_bounds__(kThreads, 1)
+//
+// REC (n_sub >= 1024: no dense dS in HBM): warps 10..13 build each stage's A
+// tile -- dS of the tile's 128 queries over the k-block's 64 sub-keys, K-major
+// in the 128-byte swizzle TMA would produce -- from the compact records of
+// ds_dq_kernel: thread r walks query r's records (sorted by sub-key; the
+// sentinel 0xffffffff past its m) block by block, clears its 128-byte row and
+// stores each record of the block as one bf16, fence.proxy.async, arrive.
+template <bool REC>
+__global__ void __launch_bounds__(dq_threads(REC), 1)
     dq_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_k, const DqParams p, int mtiles) {
   pdl_enter();
@@ -320,10 +334,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   const int nb = p.d_h / 64;                      // B atoms per stage
   constexpr int kABytes = 128 * 128;              // 128 queries x 64 sub-keys bf16
-  constexpr int kStg = kDqStages;
+  constexpr int kStg = REC ? kDqStagesRec : kDqStages;
   uint8_t* sA = smem_raw + pad;                   // kStg x 16 KB
   uint8_t* sB = sA + kStg * kABytes;              // kStg x nb atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStg * nb * kAtom);
+  uint32_t* sRec = reinterpret_cast<uint32_t*>(sB + kStg * nb * kAtom);  // REC: [2][128][32] records
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sRec) + (REC ? kDqRecBytes : 0));
   uint64_t* full = bars;
   uint64_t* empty = full + kStg;
   uint64_t* tfull = empty + kStg;
@@ -339,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_k);
     for (int s = 0; s < kStg; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], REC ? 1 + 4 : 1);  // (REC: + one arrive per builder warp)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -361,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)kABytes + (uint32_t)nb * kAtom;
+      const uint32_t bytes = (REC ? 0u : (uint32_t)kABytes) + (uint32_t)nb * kAtom;
       int it = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int hh = t / mtiles, m0 = (t - hh * mtiles) * 128;
@@ -370,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ((it / kStg) & 1) ^ 1);
           mbar_expect_tx(&full[s], bytes);
           // queries >= B (ragged last tile) are zero-filled by TMA
-          tma_load_3d(sA + s * kABytes, &tmap_a, &full[s], kb * 64, hh, m0);
+          if constexpr (!REC) tma_load_3d(sA + s * kABytes, &tmap_a, &full[s], kb * 64, hh, m0);
           for (int j = 0; j < nb; ++j)
             tma_load_3d(sB + (s * nb + j) * kAtom, &tmap_k, &full[s], 64 * j, kb * 64, hh);
         }
@@ -399,6 +414,60 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit(&tfull[buf]);
       }
     }
+  } else if (REC && warp >= 10) {
+    // ----- A-tile builders (warps 10..13): thread r = query row r of the tile.
+    // The tile's records (k <= 32 per query) are staged in shared memory by
+    // cp.async one tile ahead (each thread copies and reads only its own
+    // query's, so its cp.async.wait_group is the only ordering needed); per
+    // k-block the four warps zero the stage's A tile (contiguous 16-byte
+    // stores: no bank conflicts), meet at a named barrier, and each thread
+    // stores its query's records of the block.
+    const int r = (warp - 10) * 32 + lane;
+    const int bt = threadIdx.x - 10 * 32;  // 0..127
+    const int HH = 2 * p.H;
+    auto stage_recs = [&](int t, int buf) {
+      const int hh = t / mtiles, m0 = (t - hh * mtiles) * 128;
+      const int64_t b = (int64_t)m0 + r;
+      if (t < ntiles && b < p.B) {
+        const char* src = reinterpret_cast<const char*>(p.rec + (b * HH + hh) * p.k);
+        const uint32_t dst = smem_u32(sRec + (buf * 128 + r) * 32);
+        for (int c = 0; c < p.k / 4; ++c)  // (k % 4 == 0: 16 B = four records)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 16)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int it = 0, lt = 0;
+    stage_recs(blockIdx.x, 0);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int hh = t / mtiles, m0 = (t - hh * mtiles) * 128;
+      const bool valid = (int64_t)m0 + r < p.B;
+      stage_recs(t + gridDim.x, (lt + 1) & 1);  // the next tile's records
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's have landed
+      const uint32_t* my = sRec + ((lt & 1) * 128 + r) * 32;
+      int j = 0;
+      uint32_t x0 = valid ? my[0] : 0xffffffffu;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % kStg;
+        mbar_wait(&empty[s], ((it / kStg) & 1) ^ 1);
+        uint4* az = reinterpret_cast<uint4*>(sA + s * kABytes);
+#pragma unroll
+        for (int c = 0; c < kABytes / 16 / 128; ++c) az[c * 128 + bt] = make_uint4(0, 0, 0, 0);
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // the 4 builder warps: tile zeroed
+        const uint32_t abase = smem_u32(sA + s * kABytes + r * 128);
+        while (((x0 & 0xffffu) >> 6) == (uint32_t)kb) {  // (the sentinel's block 1023 is never reached)
+          const uint32_t e = x0 & 63u;
+          const uint32_t off = ((((e >> 3) ^ (uint32_t)(r & 7))) << 4) + (e & 7u) * 2;
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(abase + off), "h"((unsigned short)(x0 >> 16)) : "memory");
+          ++j;
+          x0 = j < p.k ? my[j] : 0xffffffffu;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
     // epilogue: warps 2..9, TMEM lane quarter warp % 4, column half (warp - 2) / 4
     const int q = warp & 3;
@@ -470,6 +539,10 @@ size_t dq_smem_bytes(const Shape& s, int MT) {
   (void)MT;
   return 1024 + (size_t)kDqStages * (128 * 128 + (s.d_h / 64) * kAtom) + 8 * (2 * kDqStages + 4) + 16;
 }
+size_t dq_rec_smem_bytes(const Shape& s) {
+  return 1024 + (size_t)kDqStagesRec * (128 * 128 + (s.d_h / 64) * kAtom) + kDqRecBytes +
+         8 * (2 * kDqStagesRec + 4) + 16;
+}
 
 // dK += sum_s part[s] (fixed split order)
 __global__ void dk_reduce_kernel(const float4* __restrict__ part, float4* __restrict__ dK,
@@ -505,7 +578,7 @@ bool dq_tc_wanted_(const Shape& s);
 // (k slots of 8 B) and their per-tile offsets (32 B) per (query, head, half)
 bool dk_compact_(const Shape& s);
 size_t dense_ds_bytes(const Shape& s) {
-  if (dk_compact_(s)) return ((size_t)s.B * s.H * 2 * (s.k * 8 + 32) + 255) & ~(size_t)255;
+  if (dk_compact_(s)) return ((size_t)s.B * s.H * 2 * (s.k * 4 + 32) + 255) & ~(size_t)255;
   return ((size_t)s.B * s.H * 2 * s.n_sub * 2 + 255) & ~(size_t)255;
 }
 
@@ -544,6 +617,15 @@ bool dk_compact_(const Shape& s) {
 }
 }  // namespace
 bool dq_tc_wanted(const Shape& s) { return dq_tc_wanted_(s); }
+// compact records: dQ on the tensor cores with the A tiles built from them
+// (MSN_DQ_REC=1 turns it on, else the SIMT dQ of ds_dq_kernel; A/B measurements only)
+bool dq_rec_wanted(const Shape& s) {
+  // default off: measured on C4, dq_gemm with built A tiles takes 316 us against
+  // the ~240 us the SIMT dQ adds to ds_dq (builder-bound: 43 % tensor-pipe activity)
+  static const int f = env_int("MSN_DQ_REC", 0);
+  // (the records staged in shared memory: k <= 32, pairs of 16 bytes)
+  return f != 0 && s.k <= 32 && s.k % 4 == 0 && dq_rec_smem_bytes(s) <= 227 * 1024;
+}
 bool dk_compact(const Shape& s) { return dk_compact_(s); }
 
 cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* dQ, float* dK,
@@ -577,8 +659,33 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  // dQ = dSd . K per (head, half) on the tensor cores
-  if (with_dq) {
+  // dQ = dS . K per (head, half) on the tensor cores: from the dense dS
+  // matrix by TMA, or (compact records) with the A tiles built in shared memory
+  if (with_dq && dk_compact(s)) {
+    CUtensorMap mk;
+    cuuint64_t kdims[3] = {(cuuint64_t)s.d_h, (cuuint64_t)s.n_sub, (cuuint64_t)HH};
+    cuuint64_t kstrides[2] = {(cuuint64_t)s.d_h * 2, (cuuint64_t)s.n_sub * s.d_h * 2};
+    cuuint32_t kbox[3] = {64, 64, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (get_encode()(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(Kp), kdims,
+                     kstrides, kbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ, s.dq_bf16 ? 1 : 0};
+    qp.rec = reinterpret_cast<const uint32_t*>(ws);
+    qp.k = s.k;
+    static std::atomic<uint64_t> qattr{0};
+    cudaError_t e0 = smem_attr_once(qattr, dq_gemm_kernel<true>, 227 * 1024);
+    if (e0 != cudaSuccess) return e0;
+    const int mtiles = (int)((s.B + 127) / 128);
+    const int ntiles = mtiles * HH;
+    launch_pdl(dq_gemm_kernel<true>, (unsigned)std::min(ntiles, num_sms_dk()), dq_threads(true),
+               dq_rec_smem_bytes(s), st, mk, mk, qp, mtiles);
+    cudaError_t e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) return e1;
+    ++*launches;
+  } else if (with_dq) {
     CUtensorMap ma, mk;
     // dSd [B, HH, n_sub] as the K-major A operand: dims (n_sub, HH, B), box (64, 1, 128)
     cuuint64_t dims[3] = {(cuuint64_t)s.n_sub, (cuuint64_t)HH, (cuuint64_t)s.B};
@@ -601,12 +708,12 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
       return cudaErrorInvalidValue;
     DqParams qp{s.B, s.H, s.n_sub, s.d_h, dQ, s.dq_bf16 ? 1 : 0};
     static std::atomic<uint64_t> qattr{0};
-    cudaError_t e0 = smem_attr_once(qattr, dq_gemm_kernel, 227 * 1024);
+    cudaError_t e0 = smem_attr_once(qattr, dq_gemm_kernel<false>, 227 * 1024);
     if (e0 != cudaSuccess) return e0;
     const int mtiles = (int)((s.B + 127) / 128);
     const int ntiles = mtiles * HH;
-    launch_pdl(dq_gemm_kernel, (unsigned)std::min(ntiles, num_sms_dk()), kThreads, dq_smem_bytes(s, 1), st,
-               ma, mk, qp, mtiles);
+    launch_pdl(dq_gemm_kernel<false>, (unsigned)std::min(ntiles, num_sms_dk()), dq_threads(false),
+               dq_smem_bytes(s, 1), st, ma, mk, qp, mtiles);
     cudaError_t e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return e1;
     ++*launches;
@@ -615,7 +722,7 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* Kp, float* d
   const int64_t kblocks = (s.B + kBK - 1) / kBK;
   const int64_t qps = ((kblocks + S - 1) / S) * kBK;
   DkParams p{s.B, s.H, s.n_sub, s.d_h, qps, S > 1 ? part : dK, S > 1 ? 0 : 1,
-             reinterpret_cast<const uint2*>(ws), s.k};
+             reinterpret_cast<const uint32_t*>(ws), s.k};
   const int mtk = dk_mt(s);
   const bool rec = dk_compact(s);  // ds_dq_kernel wrote compact records (dQ done there)
   auto dkk = rec ? (mtk == 2 ? dk_gemm_kernel<2, true> : dk_gemm_kernel<1, true>)

@@ -148,6 +148,9 @@ cudaError_t launch_dk_tc(const Shape& s, const void* Q, const void* K, float* dQ
 bool dq_tc_wanted(const Shape& s);
 // dK from the compact records (else from the dense bf16 dS matrix)
 bool dk_compact(const Shape& s);
+// with compact records: dQ on the tensor cores too, its dS tiles built in
+// shared memory from the records (else the SIMT dQ of ds_dq_kernel)
+bool dq_rec_wanted(const Shape& s);
 size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch);
 BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws);
 
