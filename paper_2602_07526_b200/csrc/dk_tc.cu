@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* a = sA + s * MT * 2 * kAtom;
         const uint32_t abase = smem_u32(a) + (uint32_t)ql * 128;
+#ifdef MSN_DK_ROWCLEAR
         // this query's row: MT * 2 atoms x 128 B, 4 threads x (MT * 2 * 8 / 4) x 16 B
 #pragma unroll
         for (int i = 0; i < MT * 2 * 8 / 4; ++i) {
@@ -226,6 +227,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           *reinterpret_cast<uint4*>(a + (c16 >> 3) * kAtom + ql * 128 + (c16 & 7) * 16) = make_uint4(0, 0, 0, 0);
         }
         __syncwarp();
+#else
+        // the stage's A tiles zeroed by the 8 builder warps with contiguous
+        // 16-byte stores (no bank conflicts; per-row clears by the row's own
+        // 4 lanes hit 8-way conflicts), then a named barrier before the records
+#pragma unroll
+        for (int i = 0; i < MT * 2 * kAtom / 16 / 256; ++i)
+          reinterpret_cast<uint4*>(a)[i * 256 + u] = make_uint4(0, 0, 0, 0);
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+#endif
         auto put = [&](uint32_t r) {
           const uint32_t il = (r & 0xffffu) - (uint32_t)i0;  // (the sentinel's 0xffff is past every tile)
           if (il < (uint32_t)(kBM * MT)) {
