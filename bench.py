@@ -704,53 +704,72 @@ def run_sharded(args, rank, world, local_rank):
         sp_e = ShardedPKM(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, B_l, qk_dtype=cfg.qk_dtype,
                           value_dtype=cfg.value_dtype, device=dev, transport=args.transport, dq_in_qk_dtype=True)
         qh, dh = q_l.cpu().pin_memory(), d_l.cpu().pin_memory()
-        out_h = torch.empty((B_l, cfg.d_value), dtype=torch.float32).pin_memory()
-        dq_h = torch.empty((B_l, cfg.heads, 2, cfg.d_half), dtype=sp_e.ph.dq_dtype).pin_memory()
-        qd, dd = torch.empty_like(q_l), torch.empty_like(d_l)
-
-        # copies overlapped with compute on side streams: d_out's H2D under the
-        # forward, out's D2H under the backward (the queries' H2D and d_query's
-        # D2H bracket the step)
+        # two sets of device inputs and host results: step i+1's H2D (copy
+        # engine) runs under step i's compute, step i's D2H under step i+1's
+        out_h = [torch.empty((B_l, cfg.d_value), dtype=torch.float32).pin_memory() for _ in range(2)]
+        dq_h = [torch.empty((B_l, cfg.heads, 2, cfg.d_half), dtype=sp_e.ph.dq_dtype).pin_memory() for _ in range(2)]
+        qd = [torch.empty_like(q_l) for _ in range(2)]
+        dd = [torch.empty_like(d_l) for _ in range(2)]
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        main = torch.cuda.current_stream(dev)
+        done = [torch.cuda.Event() for _ in range(2)]    # step using input set j finished
+        landed = [torch.cuda.Event() for _ in range(2)]  # input set j copied in
 
-        def e2e_step():
-            main = torch.cuda.current_stream(dev)
-            qd.copy_(qh, non_blocking=True)
-            s_in.wait_stream(main)
+        def h2d(i):
+            j = i % 2
+            s_in.wait_event(done[j])  # (the set's previous step is over)
             with torch.cuda.stream(s_in):
-                dd.copy_(dh, non_blocking=True)
-            o, tape = sp_e.forward(qd, K, Vs)
-            s_out.wait_stream(main)
-            with torch.cuda.stream(s_out):
-                out_h.copy_(o, non_blocking=True)
-            main.wait_stream(s_in)
-            dq_e, _, _, _ = sp_e.backward(dd, qd, K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
-            dq_h.copy_(dq_e, non_blocking=True)
+                qd[j].copy_(qh, non_blocking=True)
+                dd[j].copy_(dh, non_blocking=True)
+                landed[j].record(s_in)
+
+        def e2e_steps(n):
+            """n pipelined steps through the public API; returns when every
+            result is on the host."""
+            h2d(0)
+            for i in range(n):
+                j = i % 2
+                main.wait_event(landed[j])
+                if i + 1 < n:
+                    h2d(i + 1)
+                o, tape = sp_e.forward(qd[j], K, Vs)
+                s_out.wait_stream(main)
+                with torch.cuda.stream(s_out):
+                    out_h[j].copy_(o, non_blocking=True)
+                o.record_stream(s_out)
+                dq_e, _, _, _ = sp_e.backward(dd[j], qd[j], K, Vs, tape, d_subkeys=dK, d_value_shard=dVs)
+                done[j].record(main)
+                s_out.wait_stream(main)
+                with torch.cuda.stream(s_out):
+                    dq_h[j].copy_(dq_e, non_blocking=True)
+                dq_e.record_stream(s_out)
             main.wait_stream(s_out)
 
-        for _ in range(3):
-            e2e_step()
+        e2e_steps(3)
         torch.cuda.synchronize()
         n_e2e = max(3, min(args.steps, 20))
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
-        for i in range(n_e2e):
-            flush.zero_()
-            ev[i][0].record(stream)
-            e2e_step()
-            ev[i][1].record(stream)
-            torch.cuda.current_stream(dev).synchronize()  # the result is on the host
-        e2e_ms = sum(a.elapsed_time(b) for a, b in ev) / n_e2e
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(main)
+        e2e_steps(n_e2e)
+        e1.record(main)
+        torch.cuda.synchronize()  # the results are on the host
+        e2e_ms = e0.elapsed_time(e1) / n_e2e
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = qh.numel() * qh.element_size() + dh.numel() * dh.element_size()
-        d2h = out_h.numel() * out_h.element_size() + dq_h.numel() * dq_h.element_size()
+        h2d_b = qh.numel() * qh.element_size() + dh.numel() * dh.element_size()
+        d2h_b = out_h[0].numel() * out_h[0].element_size() + dq_h[0].numel() * dq_h[0].element_size()
         e2e = {"value": cfg.batch * cfg.heads / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": float(te.item()),
+               "h2d_bytes_per_step": int(h2d_b), "d2h_bytes_per_step": int(d2h_b), "ms_per_step": float(te.item()),
+               "steps": n_e2e,
                "note": "ShardedPKM forward+backward (msn_pkm_forward_sharded / msn_pkm_backward_sharded) fed from "
-                       "pinned host memory: H2D of the rank's queries and d_out, D2H of out (fp32) and d_query "
-                       "(bf16), one synchronisation per step; d_out's H2D overlaps the forward and out's D2H the "
-                       "backward (side streams); per-rank bytes"}
+                       "pinned host memory, n pipelined steps between two CUDA events, divided by n: every step "
+                       "copies its queries and d_out in (H2D) and its out (fp32) and d_query (bf16) back (D2H); "
+                       "step i+1's H2D and step i's D2H run on side streams (copy engines) under the compute; "
+                       "the region ends when the last result is on the host; per-rank bytes"}
         del sp_e
 
     # slot-hit statistics (the workload describes itself) from this rank's tape
