@@ -87,7 +87,7 @@ inline int64_t grp_huge_max(int64_t n) { return n / (GRP_WARP_SORT + 1) + 1; }
 // short and long runs and long-run pieces; one atomic per counter per block
 // reserves its output ranges; pass 2 writes the offsets, the run records
 // {offset, length, row, first piece} and the piece records {long run, j}
-// (block-ordered: block scans over 256-row rounds).
+// (block-ordered: block scans over 1024-row rounds, 4 rows per thread).
 __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restrict__ cnt,
                                                        uint32_t nrows, uint32_t* __restrict__ off,
                                                        uint4* __restrict__ runs_short,
@@ -127,13 +127,22 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
   __syncthreads();
   uint32_t base = s_base[0], sb = s_base[1], lb = s_base[2], pb = s_base[3];
   __syncthreads();
-  // pass 2: ordered rounds of 256 rows
-  for (int64_t rr = r0; rr < r1; rr += 256) {
-    const int64_t r = rr + tid;
-    const uint32_t c = r < r1 ? cnt[r] : 0u;
-    const uint32_t is = (c > 0 && c <= GRP_SHORT), il = (c > GRP_SHORT), np = grp_npieces(c);
-    // block exclusive scans of c, (is | il << 16) and np
-    uint32_t x[3] = {c, is | (il << 16), np};
+  // pass 2: ordered rounds of 1024 rows, four consecutive rows per thread
+  for (int64_t rr = r0; rr < r1; rr += 1024) {
+    const int64_t rb = rr + (int64_t)tid * 4;
+    uint32_t c[4], isl[4], np[4];
+    uint32_t x[3] = {0u, 0u, 0u};  // this thread's totals: entries, (short | long << 16), pieces
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      c[i] = rb + i < r1 ? cnt[rb + i] : 0u;
+      isl[i] = (c[i] > 0 && c[i] <= GRP_SHORT) | ((uint32_t)(c[i] > GRP_SHORT) << 16);
+      np[i] = grp_npieces(c[i]);
+      x[0] += c[i];
+      x[1] += isl[i];
+      x[2] += np[i];
+    }
+    const uint32_t own[3] = {x[0], x[1], x[2]};
+    // block exclusive scans of the thread totals
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
 #pragma unroll
@@ -155,21 +164,28 @@ __global__ void __launch_bounds__(256) grp_runs_kernel(const uint32_t* __restric
       }
     }
     __syncthreads();
-    const uint32_t ec = base + pre[0] + x[0] - c;
-    const uint32_t es = pre[1] + x[1] - (is | (il << 16));
-    const uint32_t ep = pb + pre[2] + x[2] - np;
-    if (c > 0) {
-      off[r] = ec;
-      if (is) {
-        runs_short[sb + (es & 0xffffu)] = make_uint4(ec, c, (uint32_t)r, 0u);
-      } else {
-        const uint32_t li = lb + (es >> 16);
-        runs_long[li] = make_uint4(ec, c, (uint32_t)r, ep);
-        // slice j: {first entry, entries (<= GRP_SLICE), row, long run}
-        for (uint32_t j = 0; j < np; ++j)
-          pieces[ep + j] = make_uint4(ec + j * GRP_SLICE, min((uint32_t)GRP_SLICE, c - j * GRP_SLICE), (uint32_t)r, li);
-        if (c > (uint32_t)GRP_WARP_SORT) huge[atomicAdd(&ctl[CTL_NHUGE], 1u)] = li;  // (any order)
+    uint32_t ec = base + pre[0] + x[0] - own[0];
+    uint32_t es = pre[1] + x[1] - own[1];
+    uint32_t ep = pb + pre[2] + x[2] - own[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (c[i] > 0) {
+        const int64_t r = rb + i;
+        off[r] = ec;
+        if (isl[i] & 0xffffu) {
+          runs_short[sb + (es & 0xffffu)] = make_uint4(ec, c[i], (uint32_t)r, 0u);
+        } else {
+          const uint32_t li = lb + (es >> 16);
+          runs_long[li] = make_uint4(ec, c[i], (uint32_t)r, ep);
+          // slice j: {first entry, entries (<= GRP_SLICE), row, long run}
+          for (uint32_t j = 0; j < np[i]; ++j)
+            pieces[ep + j] = make_uint4(ec + j * GRP_SLICE, min((uint32_t)GRP_SLICE, c[i] - j * GRP_SLICE), (uint32_t)r, li);
+          if (c[i] > (uint32_t)GRP_WARP_SORT) huge[atomicAdd(&ctl[CTL_NHUGE], 1u)] = li;  // (any order)
+        }
       }
+      ec += c[i];
+      es += isl[i];
+      ep += np[i];
     }
     base += tot[0];
     sb += tot[1] & 0xffffu;
@@ -1072,7 +1088,15 @@ __global__ void __launch_bounds__(256) ds_dq_kernel(const QT* __restrict__ K,
   for (int half = 0; half < 2; ++half) {
     int r[KPL];
 #pragma unroll
-    for (int u = 0; u < KPL; ++u) r[u] = half == 0 ? f[u] / n_sub : f[u] % n_sub;
+    for (int u = 0; u < KPL; ++u) {
+      // (power-of-two codebooks -- every BASELINE config -- by shift and mask)
+      if ((n_sub & (n_sub - 1)) == 0) {
+        const int sh = __ffs(n_sub) - 1;
+        r[u] = half == 0 ? f[u] >> sh : f[u] & (n_sub - 1);
+      } else {
+        r[u] = half == 0 ? f[u] / n_sub : f[u] % n_sub;
+      }
+    }
     float dS[KPL];
     bool first[KPL];
 #pragma unroll
