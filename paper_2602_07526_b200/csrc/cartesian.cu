@@ -90,7 +90,9 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
         const uint2 c = in ? rc[e] : make_uint2(0u, 0u);
         key[r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
       }
-      warp_sort_u64<R>(key);
+      // (k <= 32: only the top 32 are used -- two 32-sorts and a merge)
+      if constexpr (KMAX == 32 && R == 2) warp_top32_of_64(key);
+      else warp_sort_u64<R>(key);
       if constexpr (KMAX == 32 && SEG == 2) {
         // the row's second column segment (its own list, see select_tc.cu):
         // sorted likewise, then the best 32 of both lists by the half-cleaner
@@ -105,7 +107,7 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
           const uint2 c = in ? rc[CAP + e] : make_uint2(0u, 0u);
           k1[r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
         }
-        warp_sort_u64<2>(k1);
+        warp_top32_of_64(k1);
         const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)k1[0], 31 - lane);
         const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(k1[0] >> 32), 31 - lane);
         const uint64_t bk = ((uint64_t)bhi << 32) | blo;
@@ -249,7 +251,13 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
   // exact rank by composite key; keys are distinct (flat ids are distinct).
   // Up to 64 candidates (the common case): each lane ranks its two in one
   // pass over the list (one shared load per two comparisons).
-  if (m <= 64) {
+  if (KMAX == 32 && m <= 64) {
+    // k <= 32: the top 32 of the (distinct, nonzero) keys by two 32-sorts and
+    // a merge; lane t holds the t-th
+    uint64_t c[2] = {lane < m ? sm.cand[lane] : 0ull, lane + 32 < m ? sm.cand[lane + 32] : 0ull};
+    warp_top32_of_64(c);
+    if (lane < k) sm.res[lane] = c[0];
+  } else if (m <= 64) {
     const uint64_t k0 = lane < m ? sm.cand[lane] : ~0ull;
     const uint64_t k1 = lane + 32 < m ? sm.cand[lane + 32] : ~0ull;
     int r0 = 0, r1 = 0;
