@@ -257,6 +257,12 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
     uint64_t c[2] = {lane < m ? sm.cand[lane] : 0ull, lane + 32 < m ? sm.cand[lane + 32] : 0ull};
     warp_top32_of_64(c);
     if (lane < k) sm.res[lane] = c[0];
+  } else if (KMAX == 32 && MAXC <= 128) {  // (m <= MAXC)
+    uint64_t c[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c[r] = lane + 32 * r < m ? sm.cand[lane + 32 * r] : 0ull;
+    warp_top32_of_128(c);
+    if (lane < k) sm.res[lane] = c[0];
   } else if (m <= 64) {
     const uint64_t k0 = lane < m ? sm.cand[lane] : ~0ull;
     const uint64_t k1 = lane + 32 < m ? sm.cand[lane + 32] : ~0ull;

@@ -137,6 +137,26 @@ __device__ __forceinline__ void warp_top32_of_64(uint64_t (&x)[2]) {
   x[1] = 0ull;
 }
 
+// The 32 largest of 128 u64 keys (four registers), sorted descending in x[0]:
+// the top 32 of each pair, then the half-cleaner of the two and a merge.
+__device__ __forceinline__ void warp_top32_of_128(uint64_t (&x)[4]) {
+  const int lane = threadIdx.x % 32;
+  uint64_t a[2] = {x[0], x[1]}, b[2] = {x[2], x[3]};
+  warp_top32_of_64(a);
+  warp_top32_of_64(b);
+  const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)b[0], 31 - lane);
+  const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(b[0] >> 32), 31 - lane);
+  const uint64_t br = ((uint64_t)bhi << 32) | blo;
+  uint64_t c = a[0] > br ? a[0] : br;
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const uint64_t o = shfl_xor_u64(c, stride);
+    c = ((lane & stride) == 0) == (o > c) ? o : c;
+  }
+  x[0] = c;
+  x[1] = x[2] = x[3] = 0ull;
+}
+
 // Exact per-half top list of lookup l when the scorer's candidate list
 // overflowed (its two ends met): rescore all n_sub sub-keys of this
 // (head, half) and keep the best 64 under (score desc, index asc).  32
