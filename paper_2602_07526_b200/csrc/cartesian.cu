@@ -38,6 +38,9 @@ constexpr int kWarpsPerBlock = 8;
 #ifndef MSN_CART_TAU_STEPS
 #define MSN_CART_TAU_STEPS 3  // counted interpolation steps on tau (see the header)
 #endif
+#ifndef MSN_FUSED_TAU_STEPS
+#define MSN_FUSED_TAU_STEPS 0  // ... and in the fused kernels (see below)
+#endif
 // ... in the standalone Cartesian kernel only: in the fused Cartesian +
 // gather kernel the steps lengthen every query warp's serial prologue before
 // its row stream (measured: C3 +88 us, C4 +57 us per step), so it keeps tau0
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
   const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (b >= B) return;
   for (int h = 0; h < H; ++h)
-    cartesian_lookup<KMAX, MAXC, 0, 1>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
+    cartesian_lookup<KMAX, MAXC, MSN_FUSED_TAU_STEPS, 1>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w,
                                  &s_idx[wid][h * k], &s_w[wid][h * k],
                                  (int32_t)(h / (H / og)) * tab_stride, SC);
   const int HK = H * k;
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_lookup_kernel(
   const int64_t l = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   const int64_t L = B * H;
   if (l < L) {
-    cartesian_lookup<32, MAXC, 0, SEG>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, s_idx[wid], s_w[wid], 0, SC);
+    cartesian_lookup<32, MAXC, MSN_FUSED_TAU_STEPS, SEG>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, s_idx[wid], s_w[wid], 0, SC);
     float p[VPL][PER];
     gather_rows<VT, VPL, G, U>(s_idx[wid], s_w[wid], 0, k, V, d_v, p);
     const int g = lane / LG, gl = lane % LG;
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(256) cartesian_route_kernel(
   const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
   if (b >= B) return;
   for (int h = 0; h < H; ++h)
-    cartesian_lookup<KMAX, MAXC, 0, SEG>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w, &s_idx[wid][h * k],
+    cartesian_lookup<KMAX, MAXC, MSN_FUSED_TAU_STEPS, SEG>(sm[wid], b * H + h, cand, cand_n, n_sub, k, idx, w, &s_idx[wid][h * k],
                                          &s_w[wid][h * k], 0, SC);
   const int HK = H * k;
   const int P = ra.P;
