@@ -33,3 +33,9 @@ ncu -i $O/c2_full.ncu-rep --page raw --csv > $O/c2_full_raw.csv 2>/dev/null
 python tools/traffic_json.py $T c4_large_sharded_bf16_xchg=$O/c4_full_raw.csv c2_mid_bf16=$O/c2_full_raw.csv > $O/traffic.log 2>&1
 cp profiles/traffic.json $O/traffic.json
 rm -f $O/*.ncu-rep
+# the scorer's phase timelines (MSN_SELECT_TS build)
+if [ -f paper_2602_07526_b200/libmsn_pkm_ts.so ]; then
+  for c in c4_large_sharded_bf16 c2_mid_bf16 c5_latency_bf16 c3_train_fp32_zipf; do
+    MSN_LIB=paper_2602_07526_b200/libmsn_pkm_ts.so timeout 200 python tools/select_ts.py $c >> $O/select_ts.txt 2>&1
+  done
+fi
