@@ -50,7 +50,7 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 //   2. grp_runs_kernel: every row with cnt > 0 gets a contiguous segment
 //      [off, off + cnt) (warp-aggregated atomic allocation) and a run record
 //      {off, cnt, row} in the short (cnt <= 32) or the long list;
-//   3. grp_place_kernel: ent[off[key] + rank[p]] = p, went[...] = wts[p].
+//   3. grp_place_kernel: ent[off[key] + rank[p]] = (p, wts[p]) (one 8-byte store).
 // The order inside a segment, and of the runs in their lists, is arbitrary;
 // the reducers sort each run's record ids before summing, so every gradient
 // row is summed in a fixed order (ascending record id inside a warp's slice)
@@ -198,16 +198,14 @@ __global__ void __launch_bounds__(256) grp_place_kernel(const uint32_t* __restri
                                                         const uint32_t* __restrict__ rank,
                                                         const uint32_t* __restrict__ off,
                                                         const float* __restrict__ wts, int64_t n,
-                                                        uint32_t nrows, uint32_t* __restrict__ ent,
-                                                        float* __restrict__ went) {
+                                                        uint32_t nrows, uint2* __restrict__ ent) {
   pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t k = keys[p];
   if (k >= nrows) return;
   const uint32_t pos = off[k] + rank[p];
-  ent[pos] = (uint32_t)p;
-  went[pos] = wts[p];
+  ent[pos] = make_uint2((uint32_t)p, __float_as_uint(wts[p]));  // (one 8-byte scattered store)
 }
 
 // ------------------------------------------------------------- reducers ----
@@ -217,8 +215,7 @@ __global__ void __launch_bounds__(256) grp_place_kernel(const uint32_t* __restri
 enum { MODE_DV = 0, MODE_DK = 1 };
 
 struct GrpArgs {
-  const uint32_t* ent;    // record ids, grouped by row
-  const float* went;      // their weights, same order
+  const uint2* ent;       // (record id, weight bits), grouped by row
   const float* wts;       // weight by record id
   const uint4* runs_short;
   const uint4* runs_long;
@@ -229,7 +226,7 @@ struct GrpArgs {
   const void* Y;          // V (MODE_DV dot)
   float* dots;            // dw (MODE_DV)
   float* G;               // gradient rows (+=)
-  uint32_t* ent_rw;       // = ent (in-place sort of very long runs)
+  uint2* ent_rw;          // = ent (long runs: sorted in place)
   FastDiv div_hk, div_k;  // record -> query: / (H k), / k
   // head groups: the x row of record cid is (b, group of h)
   int og = 1, H = 1;
@@ -250,7 +247,7 @@ struct GrpArgs {
   FastDiv div_xl, div_dl;
   const uint32_t* huge = nullptr;  // long runs > GRP_WARP_SORT entries (indices into runs_long)
   uint32_t* ctl_rw = nullptr;      // = ctl (the sort's work queue counter)
-  float* went_rw = nullptr;        // = went (long runs: rewritten in sorted order by the sort)
+  uint32_t* keys_rw = nullptr;     // scratch for the ids of runs too long for shared memory
   uint32_t id_shift = 0;           // record id >> id_shift < 256 (the huge runs' bucket)
 };
 
@@ -506,8 +503,9 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
   uint32_t me = 0xffffffffu;
   float mw = 0.f;
   if (lane < (int)cur.y) {
-    me = a.ent[cur.x + lane];
-    mw = a.went[cur.x + lane];
+    const uint2 e0 = a.ent[cur.x + lane];
+    me = e0.x;
+    mw = __uint_as_float(e0.y);
   }
   for (; c < nruns; c += nw) {
     const uint32_t key = cur.z;
@@ -537,8 +535,9 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
     me = 0xffffffffu;
     mw = 0.f;
     if (lane < (int)nxt.y) {
-      me = a.ent[nxt.x + lane];
-      mw = a.went[nxt.x + lane];
+      const uint2 e1 = a.ent[nxt.x + lane];
+      me = e1.x;
+      mw = __uint_as_float(e1.y);
     }
     // rank of this lane's record id among the run's
     uint32_t rk = 0;
@@ -638,7 +637,7 @@ __device__ __forceinline__ void warp_sort_run(uint32_t* g, int L) {
 
 // Long runs (> 32 entries), step 1: every run's record ids are sorted
 // ascending in place, fixing its summation order, and its weights are
-// rewritten in that order (went[e] = wts[ent[e]]).  Runs of more than
+// rewritten in that order (ent[e] = (id, wts[id])).  Runs of more than
 // GRP_WARP_SORT entries (the `huge` list, few) go first, one CTA each: a
 // two-level sort in shared memory -- bucket by the id's top 8 bits (a
 // counting pass), then every bucket sorted by a warp in registers (a bucket
@@ -647,29 +646,28 @@ __device__ __forceinline__ void warp_sort_run(uint32_t* g, int L) {
 // (one atomic per run), sorting each in registers -- so a CTA held up by a
 // huge run does not hold up a static share of the short ones.
 template <int R>
-__device__ __forceinline__ void warp_sort_run_w(const GrpArgs& a, uint32_t* g, float* gw, int L) {
+__device__ __forceinline__ void warp_sort_run_w(const GrpArgs& a, uint2* g, int L) {
   const int lane = threadIdx.x % 32;
   uint32_t x[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) x[r] = r * 32 + lane < L ? g[r * 32 + lane] : 0xffffffffu;
+  for (int r = 0; r < R; ++r) x[r] = r * 32 + lane < L ? g[r * 32 + lane].x : 0xffffffffu;
   warp_sort_asc<R>(x);
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (r * 32 + lane < L) {
-      g[r * 32 + lane] = x[r];
-      gw[r * 32 + lane] = a.wts[x[r]];
-    }
+    if (r * 32 + lane < L) g[r * 32 + lane] = make_uint2(x[r], __float_as_uint(a.wts[x[r]]));
 }
-// a warp sorts g[0, L) (L <= GRP_WARP_SORT; gw: the weights in that order, or nullptr)
-__device__ __forceinline__ void warp_sort_any(const GrpArgs& a, uint32_t* g, float* gw, int L) {
-  if (gw) {
-    if (L <= 32) warp_sort_run_w<1>(a, g, gw, L);
-    else if (L <= 64) warp_sort_run_w<2>(a, g, gw, L);
-    else if (L <= 128) warp_sort_run_w<4>(a, g, gw, L);
-    else if (L <= 256) warp_sort_run_w<8>(a, g, gw, L);
-    else if (L <= 512) warp_sort_run_w<16>(a, g, gw, L);
-    else warp_sort_run_w<32>(a, g, gw, L);
-  } else {
+// a warp sorts the (id, weight) pairs g[0, L) by id (L <= GRP_WARP_SORT)
+__device__ __forceinline__ void warp_sort_pairs(const GrpArgs& a, uint2* g, int L) {
+  if (L <= 32) warp_sort_run_w<1>(a, g, L);
+  else if (L <= 64) warp_sort_run_w<2>(a, g, L);
+  else if (L <= 128) warp_sort_run_w<4>(a, g, L);
+  else if (L <= 256) warp_sort_run_w<8>(a, g, L);
+  else if (L <= 512) warp_sort_run_w<16>(a, g, L);
+  else warp_sort_run_w<32>(a, g, L);
+}
+// a warp sorts the ids g[0, L) (L <= GRP_WARP_SORT)
+__device__ __forceinline__ void warp_sort_any(uint32_t* g, int L) {
+  {
     if (L <= 1) return;
     if (L <= 32) warp_sort_run<1>(g, L);
     else if (L <= 64) warp_sort_run<2>(g, L);
@@ -691,13 +689,15 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
   for (int64_t h = blockIdx.x; h < nhuge; h += gridDim.x) {
     const uint4 run = a.runs_long[a.huge[h]];
     const int L = (int)run.y;
-    uint32_t* g = a.ent_rw + run.x;
-    float* gw = a.went_rw + run.x;
-    if (L > GRP_BUCKET_SMEM) {  // (very long: in place in global memory)
+    uint2* g = a.ent_rw + run.x;
+    if (L > GRP_BUCKET_SMEM) {  // (very long: the ids sorted in global scratch)
+      uint32_t* gk = a.keys_rw + run.x;  // (the keys are dead once the records are placed)
+      for (int i = tid; i < L; i += blockDim.x) gk[i] = g[i].x;
+      __syncthreads();
       int P = 1;
       while (P < L) P <<= 1;
-      block_bitonic(g, L, P);
-      for (int i = tid; i < L; i += blockDim.x) gw[i] = a.wts[g[i]];
+      block_bitonic(gk, L, P);
+      for (int i = tid; i < L; i += blockDim.x) g[i] = make_uint2(gk[i], __float_as_uint(a.wts[gk[i]]));
       __syncthreads();
       continue;
     }
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
     cnt[tid] = 0u;
     __syncthreads();
     for (int i = tid; i < L; i += blockDim.x) {
-      const uint32_t v = g[i];
+      const uint32_t v = g[i].x;
       sa[i] = v;
       atomicAdd(&cnt[v >> a.id_shift], 1u);
     }
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
     // cnt[b] is now the end of bucket b
     for (int b = wid; b < 256; b += 8) {
       const int o = (int)off[b], n = (int)cnt[b] - o;
-      if (n <= GRP_WARP_SORT) warp_sort_any(a, sb + o, nullptr, n);
+      if (n <= GRP_WARP_SORT) warp_sort_any(sb + o, n);
     }
     __syncthreads();
     for (int b = 0; b < 256; ++b) {  // (a bucket of more than GRP_WARP_SORT entries: the CTA)
@@ -750,8 +750,7 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
     }
     for (int i = tid; i < L; i += blockDim.x) {
       const uint32_t v = sb[i];
-      g[i] = v;
-      gw[i] = a.wts[v];
+      g[i] = make_uint2(v, __float_as_uint(a.wts[v]));
     }
     __syncthreads();
   }
@@ -762,7 +761,7 @@ __global__ void __launch_bounds__(256) grp_sort_long_kernel(GrpArgs a) {
     if ((int64_t)r >= nruns) break;
     const uint4 run = a.runs_long[r];
     const int L = (int)run.y;
-    if (L <= GRP_WARP_SORT) warp_sort_any(a, a.ent_rw + run.x, a.went_rw + run.x, L);
+    if (L <= GRP_WARP_SORT) warp_sort_pairs(a, a.ent_rw + run.x, L);
   }
 }
 
@@ -788,8 +787,9 @@ __global__ void __launch_bounds__(256, 4) grp_reduce_slice_kernel(GrpArgs a) {
   for (; pc < np; pc += nw) {
     const uint4 nxt = pc + nw < np ? a.pieces[pc + nw] : make_uint4(0, 0, 0, 0);
     const int n = (int)cur.y;
-    const uint32_t myid = lane < n ? a.ent[cur.x + lane] : 0u;
-    const float myw = lane < n ? a.went[cur.x + lane] : 0.f;
+    const uint2 me = lane < n ? a.ent[cur.x + lane] : make_uint2(0u, 0u);
+    const uint32_t myid = me.x;
+    const float myw = __uint_as_float(me.y);
     float y[MODE == MODE_DV ? EPL : 1], acc[EPL];
     if constexpr (MODE == MODE_DV) {
 #pragma unroll
@@ -869,8 +869,7 @@ struct GrpScratch {
   uint32_t* off;    // [rows]
   uint32_t* rank;   // [n]
   uint32_t* keys;   // [n]
-  uint32_t* ent;    // [n]
-  float* went;      // [n]
+  uint2* ent;       // [n] (record id, weight bits)
   uint4* runs_short;  // [min(n, rows)]
   uint4* runs_long;   // [n / 33 + 1]
   uint4* pieces;    // [grp_pieces_max(n)]
@@ -963,15 +962,15 @@ cudaError_t grp_finish(const GrpScratch& g, int64_t n, uint32_t nrows, const flo
   launch_pdl(grp_runs_kernel, (unsigned)rb, 256, 0, st, g.cnt, nrows, g.off, g.runs_short, g.runs_long,
                                                 g.pieces, g.huge, g.ctl);
   launch_pdl(grp_place_kernel, (unsigned)((n + 255) / 256), 256, 0, st, g.keys, g.rank, g.off, wts, n, nrows,
-                                                                g.ent, g.went);
+                                                                g.ent);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 2;
-  GrpArgs a{g.ent, g.went, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
+  GrpArgs a{g.ent, wts, g.runs_short, g.runs_long, g.pieces, g.part, g.ctl, X, Y, dots, G, g.ent,
             FastDiv((uint32_t)(H * k)), FastDiv((uint32_t)k)};
   a.huge = g.huge;
   a.ctl_rw = g.ctl;
-  a.went_rw = g.went;
+  a.keys_rw = g.keys;
   {
     uint32_t bits = 0;
     while (bits < 32 && (uint64_t(1) << bits) < (uint64_t)n) ++bits;
@@ -1343,7 +1342,7 @@ size_t bwd_workspace_bytes(const Shape& s, int64_t gather_batch) {
   const int64_t nshort = pl.n < pl.rows ? pl.n : pl.rows;
   size_t b = 0;
   b += 2 * align256(sizeof(uint32_t) * pl.rows);            // cnt, off
-  b += 4 * align256(sizeof(uint32_t) * pl.n);               // rank, keys, ent, went
+  b += 4 * align256(sizeof(uint32_t) * pl.n);               // rank, keys, ent (8-byte pairs)
   b += align256(sizeof(uint4) * nshort);                    // runs_short
   b += align256(sizeof(uint4) * (pl.n / (GRP_SHORT + 1) + 1));  // runs_long
   b += align256(sizeof(uint4) * grp_pieces_max(pl.n));             // slices
@@ -1367,8 +1366,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
   w.off = (uint32_t*)p; p += align256(sizeof(uint32_t) * pl.rows);
   w.rank = (uint32_t*)p; p += align256(sizeof(uint32_t) * pl.n);
   w.keys = (uint32_t*)p; p += align256(sizeof(uint32_t) * pl.n);
-  w.ent = (uint32_t*)p; p += align256(sizeof(uint32_t) * pl.n);
-  w.went = (float*)p; p += align256(sizeof(uint32_t) * pl.n);
+  w.ent = (uint2*)p; p += 2 * align256(sizeof(uint32_t) * pl.n);
   w.runs_short = (uint4*)p; p += align256(sizeof(uint4) * nshort);
   w.runs_long = (uint4*)p; p += align256(sizeof(uint4) * (pl.n / (GRP_SHORT + 1) + 1));
   w.pieces = (uint4*)p; p += align256(sizeof(uint4) * grp_pieces_max(pl.n));
@@ -1383,7 +1381,7 @@ BwdWorkspace carve_bwd_workspace(const Shape& s, int64_t gather_batch, void* ws)
 
 // ------------------------------------------------------------ launchers ---
 static GrpScratch grp_scratch(const BwdWorkspace& ws) {
-  return GrpScratch{ws.cnt, ws.off, ws.rank, ws.keys, ws.ent, ws.went, ws.runs_short, ws.runs_long,
+  return GrpScratch{ws.cnt, ws.off, ws.rank, ws.keys, ws.ent, ws.runs_short, ws.runs_long,
                     ws.pieces, ws.part, ws.ctl, ws.huge};
 }
 

@@ -115,8 +115,8 @@ cudaError_t launch_gate_backward(int64_t B, int d_v, int kind, const float* x, c
 // ---- backward ----
 struct BwdWorkspace {
   uint32_t *cnt, *off;            // per-row counts / segment offsets (grouping)
-  uint32_t *rank, *keys, *ent;    // per-contribution rank, row key, grouped record ids
-  float* went;                    // grouped weights
+  uint32_t *rank, *keys;          // per-contribution rank, row key
+  uint2* ent;                     // grouped (record id, weight bits) pairs
   uint4 *runs_short, *runs_long;  // run records {offset, length, row, first piece}
   uint4* pieces;                  // long-run slices {first entry, entries, row, long run}
   float* part;                    // piece partial rows
