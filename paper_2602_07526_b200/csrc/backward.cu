@@ -66,6 +66,12 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
                           // red.add is fire-and-forget; a prefetched line evicted before it is read
                           // twice -- C4 DRAM reads 4.77 -> 4.54 GB, reducer 1252 -> 1225 us)
 #endif
+#ifndef MSN_SHORT_U4
+#define MSN_SHORT_U4 4  // ... (<= 4 values/lane: fp32 rows of <= 128)
+#endif
+#ifndef MSN_SHORT_BPS4
+#define MSN_SHORT_BPS4 4  // ... (<= 4 values/lane)
+#endif
 #ifndef MSN_SHORT_BPS
 #define MSN_SHORT_BPS 4  // resident blocks per SM of the short-run reducer (8 values/lane)
 #endif
@@ -485,12 +491,12 @@ __device__ __forceinline__ void grp_accumulate(const GrpArgs& a, int j0, int j1,
 // row sum is added to G by one vector reduction per lane (red.global.add,
 // performed in L2): the row's only update, so G = G + sum bitwise.
 template <int MODE, typename XT, typename YT, int EPL, bool UPD, bool P2P>
-__global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4)))) grp_reduce_short_kernel(GrpArgs a) {
+__global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : MSN_SHORT_BPS4)))) grp_reduce_short_kernel(GrpArgs a) {
   pdl_enter();
   constexpr int VW = EPL < 4 ? EPL : 4;
   constexpr int NVEC = EPL / VW;
   constexpr int D = 32 * EPL;
-  constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_U : 4);
+  constexpr int U = EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_U : MSN_SHORT_U4);
   const int lane = threadIdx.x % 32;
   const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
   int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
@@ -901,7 +907,7 @@ template <int MODE, typename XT, typename YT, int EPL>
 cudaError_t grp_reduce_t(const GrpArgs& a, int64_t n, uint32_t nrows, cudaStream_t st,
                          int* launches, const TraceEvents& tr) {
   const int sms = num_sms();
-  int64_t sb = (int64_t)sms * (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : 4)));
+  int64_t sb = (int64_t)sms * (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >= 8 ? MSN_SHORT_BPS : MSN_SHORT_BPS4)));
   const int64_t sneed = ((n < (int64_t)nrows ? n : (int64_t)nrows) + 7) / 8;
   if (sb > sneed) sb = sneed;
   if (sb < 1) sb = 1;
