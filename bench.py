@@ -929,7 +929,11 @@ def run_reference(args, rank, world):
     value = args.steps * per_step * cfg.heads / t
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True,
+            # (the same scaling as this workload's own arm: the sharded C4 step is strong)
+            "scaling": "strong" if (cfg.name == "c4_large_sharded_bf16" and not getattr(args, "unsharded", False))
+                       else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded)",
             "config": {"workload": cfg.name, "batch_per_step": per_step, "heads": cfg.heads,
                        "n_sub": cfg.n_sub, "d_half": cfg.d_half, "d_value": cfg.d_value, "k": cfg.k},
