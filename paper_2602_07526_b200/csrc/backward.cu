@@ -59,7 +59,7 @@ __device__ __forceinline__ void load_slice(const T* p, float* f) {
 #define MSN_SHORT_U 2  // x rows in flight per warp in the short-run reducer (8 values/lane)
 #endif
 #ifndef MSN_V_PREFETCH
-#define MSN_V_PREFETCH 1  // L2 prefetch of the value row two runs ahead of its load
+#define MSN_V_PREFETCH 2  // L2 prefetch of the value row this many runs ahead of its load (0: off)
 #endif
 #ifndef MSN_G_PREFETCH
 #define MSN_G_PREFETCH 0  // L2 prefetch of the gradient row two runs ahead of its reduction (off: the
@@ -528,9 +528,10 @@ __global__ void __launch_bounds__(256, (EPL >= 32 ? 1 : (EPL >= 16 ? 2 : (EPL >=
     const uint4 nn = c + 2 * nw < nruns ? a.runs_short[c + 2 * nw] : make_uint4(0, 0, 0, 0);
     if constexpr (MODE == MODE_DV) {
       constexpr int LINES = (D * (int)sizeof(YT) + 127) / 128;
-      if (MSN_V_PREFETCH && lane < LINES && c + 2 * nw < nruns)
+      const uint4& pv = MSN_V_PREFETCH == 1 ? nxt : nn;  // (1: one run ahead, 2: two)
+      if (MSN_V_PREFETCH && lane < LINES && c + MSN_V_PREFETCH * nw < nruns)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.Y) +
-                                                       (int64_t)nn.z * D * (int)sizeof(YT) + lane * 128));
+                                                       (int64_t)pv.z * D * (int)sizeof(YT) + lane * 128));
     }
     {  // ... and its gradient row, which the row's single reduction updates in L2
       constexpr int GLINES = (D * 4 + 127) / 128;
