@@ -11,8 +11,10 @@ namespace msn {
 
 // acc = sum over r in [r0, r1) with s_idx[r] >= 0 of s_w[r] * V[s_idx[r]],
 // for the lane's VPL 16-byte vectors (vec = gl * VPL + v) of the row.  Every
-// lane of the warp holds the full sum on return.
-template <typename VT, int VPL, int G, int U>
+// lane of the warp holds the full sum on return.  MASK = false: every index
+// is a valid row (no per-row test, no zero fill: the same sum when none is
+// masked).
+template <typename VT, int VPL, int G, int U, bool MASK = true>
 __device__ __forceinline__ void gather_rows(const int32_t* s_idx, const float* s_w, int r0, int r1,
                                             const VT* __restrict__ V, int d_v,
                                             float (&acc)[VPL][elem<VT>::per16]) {
@@ -31,14 +33,28 @@ __device__ __forceinline__ void gather_rows(const int32_t* s_idx, const float* s
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int r = base + u * G;
-      const int f = r < r1 ? s_idx[r] : -1;
-      wt[u] = f >= 0 ? s_w[r] : 0.f;
-      const VT* row = V + (int64_t)(f >= 0 ? f : 0) * d_v;
+      if constexpr (MASK) {
+        const int f = r < r1 ? s_idx[r] : -1;
+        wt[u] = f >= 0 ? s_w[r] : 0.f;
+        const VT* row = V + (int64_t)(f >= 0 ? f : 0) * d_v;
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const int vec = gl * VPL + v;
-        if (f >= 0 && vec < row_vecs) x[u][v] = ldg_nc_v4(row + vec * PER);
-        else x[u][v] = make_uint4(0, 0, 0, 0);
+        for (int v = 0; v < VPL; ++v) {
+          const int vec = gl * VPL + v;
+          if (f >= 0 && vec < row_vecs) x[u][v] = ldg_nc_v4(row + vec * PER);
+          else x[u][v] = make_uint4(0, 0, 0, 0);
+        }
+      } else {
+        // (past r1: row 0 with weight 0 -- only in a ragged last group)
+        const bool in = r < r1;
+        const int f = in ? s_idx[r] : 0;
+        wt[u] = in ? s_w[r] : 0.f;
+        const VT* row = V + (int64_t)f * d_v;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int vec = gl * VPL + v;
+          if (vec < row_vecs) x[u][v] = ldg_nc_v4(row + vec * PER);
+          else x[u][v] = make_uint4(0, 0, 0, 0);
+        }
       }
     }
 #pragma unroll
@@ -64,7 +80,7 @@ __device__ __forceinline__ void gather_rows(const int32_t* s_idx, const float* s
 // gather of the unsharded path uses this order -- per query (gather_kernel,
 // gather_wide_kernel, cartesian_gather_kernel) or per lookup and then per
 // query (cartesian_gather_lookup_kernel) -- so they agree bitwise.
-template <typename VT, int VPL, int G, int U>
+template <typename VT, int VPL, int G, int U, bool MASK = true>
 __device__ __forceinline__ void gather_rows_heads(const int32_t* s_idx, const float* s_w, int h0, int h1, int k,
                                                   const VT* __restrict__ V, int d_v,
                                                   float (&acc)[VPL][elem<VT>::per16]) {
@@ -75,7 +91,7 @@ __device__ __forceinline__ void gather_rows_heads(const int32_t* s_idx, const fl
     for (int e = 0; e < PER; ++e) acc[v][e] = 0.f;
   for (int h = h0; h < h1; ++h) {
     float p[VPL][PER];
-    gather_rows<VT, VPL, G, U>(s_idx, s_w, h * k, (h + 1) * k, V, d_v, p);
+    gather_rows<VT, VPL, G, U, MASK>(s_idx, s_w, h * k, (h + 1) * k, V, d_v, p);
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
 #pragma unroll
