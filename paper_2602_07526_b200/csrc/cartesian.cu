@@ -72,62 +72,108 @@ __device__ __forceinline__ void cartesian_lookup(CartSmem<KMAX, MAXC>& sm, int64
 
   float va[APL];
   int32_t ia[APL];
+  // the list: [0, n0) u [CAP - n1, CAP) (the scorer's two appending ends);
+  // both halves are loaded, then sorted together (two interleaved networks)
+  constexpr int CAP = cand_cap(KMAX);
+  constexpr int R = CAP / 32;
+  uint64_t key[2][R];  // composite keys (score desc, index asc) as one u64
+  bool joined[2] = {false, false};
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int64_t row = l * 2 + half;
-    float v[2];
-    int32_t ix[2];
-    // the list: [0, n0) u [CAP - n1, CAP) (the scorer's two appending ends)
-    constexpr int CAP = cand_cap(KMAX);
-    constexpr int R = CAP / 32;
-    uint64_t key[R];
-    {
-      // sort by the composite key (score desc, index asc) as one u64
+    const uint2* rc = cand + row * SC * CAP;
+    if constexpr (KMAX == 32 && SEG == 2) {
+      // column segments (select_tc.cu): every list holds its columns >= the
+      // WHOLE row's bound, so together they are a superset of the row's
+      // top-k; when they are compact and total <= 64 (the common case,
+      // ~1.2k) they are read as one list: entry e of the concatenation
+      // lies in segment g = #{segments whose inclusive prefix <= e}
+      const int ng = lane < SC ? cand_n[row * SC + lane] : 0;
+      int incl = ng & 0xffff;
+#pragma unroll
+      for (int d = 1; d < kMaxSeg; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += o;
+      }
+      int pre[kMaxSeg];
+#pragma unroll
+      for (int g = 0; g < kMaxSeg; ++g) pre[g] = __shfl_sync(0xffffffffu, incl, g < SC ? g : SC - 1);
+      const int total = pre[kMaxSeg - 1];
+      if (__all_sync(0xffffffffu, (ng >> 16) == 0) && total <= 64) {
+        joined[half] = true;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int e = r * 32 + lane;
+          int g = 0, base = 0;
+#pragma unroll
+          for (int t = 0; t < kMaxSeg - 1; ++t)
+            if (e >= pre[t]) {
+              g = t + 1;
+              base = pre[t];
+            }
+          const uint2 c = e < total ? rc[g * CAP + (e - base)] : make_uint2(0u, 0u);
+          key[half][r] = e < total ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
+        }
+      }
+    }
+    if (!joined[half]) {
       const uint32_t nn = (uint32_t)cand_n[row * SC];
       const int n0 = (int)(nn & 0xffffu), n1 = (int)(nn >> 16);
-      const uint2* rc = cand + row * SC * CAP;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int e = r * 32 + lane;
         const bool in = e < n0 || e >= CAP - n1;
         const uint2 c = in ? rc[e] : make_uint2(0u, 0u);
-        key[r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
+        key[half][r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
       }
-      // (k <= 32: only the top 32 are used -- two 32-sorts and a merge)
-      if constexpr (KMAX == 32 && R == 2) warp_top32_of_64(key);
-      else warp_sort_u64<R>(key);
-      if constexpr (KMAX == 32 && SEG == 2) {
-        // the row's second column segment (its own list, see select_tc.cu):
-        // sorted likewise, then the best 32 of both lists by the half-cleaner
-        // max(A_i, B_31-i) and a 5-step bitonic merge (k <= 32 here)
-        const uint32_t nb = (uint32_t)cand_n[row * SC + 1];
+    }
+  }
+  // (k <= 32: only the top 32 are used -- two 32-sorts and a merge)
+  if constexpr (KMAX == 32 && R == 2) {
+    warp_top32_of_64_n<2>(*reinterpret_cast<uint64_t (*)[2][2]>(&key));
+  } else {
+    warp_sort_u64<R>(key[0]);
+    warp_sort_u64<R>(key[1]);
+  }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int64_t row = l * 2 + half;
+    const uint2* rc = cand + row * SC * CAP;
+    float v[2];
+    int32_t ix[2];
+    if constexpr (KMAX == 32 && SEG == 2) if (!joined[half]) {
+      // the row's other column segments (SC == S lists, see select_tc.cu):
+      // each sorted likewise, then the best 32 of the running list and it by
+      // the half-cleaner max(A_i, B_31-i) and a 5-step bitonic merge (k <= 32)
+      for (int sg = 1; sg < SC; ++sg) {
+        const uint32_t nb = (uint32_t)cand_n[row * SC + sg];
         const int m0 = (int)(nb & 0xffffu), m1 = (int)(nb >> 16);
         uint64_t k1[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int e = r * 32 + lane;
           const bool in = e < m0 || e >= CAP - m1;
-          const uint2 c = in ? rc[CAP + e] : make_uint2(0u, 0u);
+          const uint2 c = in ? rc[sg * CAP + e] : make_uint2(0u, 0u);
           k1[r] = in ? sel_key(__uint_as_float(c.x), c.y) : 0ull;
         }
         warp_top32_of_64(k1);
         const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)k1[0], 31 - lane);
         const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(k1[0] >> 32), 31 - lane);
         const uint64_t bk = ((uint64_t)bhi << 32) | blo;
-        uint64_t c = key[0] > bk ? key[0] : bk;
+        uint64_t c = key[half][0] > bk ? key[half][0] : bk;
 #pragma unroll
         for (int stride = 16; stride > 0; stride >>= 1) {
           const uint64_t o = shfl_xor_u64(c, stride);
           c = ((lane & stride) == 0) == (o > c) ? o : c;
         }
-        key[0] = c;
-        key[1] = 0ull;
+        key[half][0] = c;
+        key[half][1] = 0ull;
       }
+    }
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        v[r] = key[r] ? sel_key_score(key[r]) : -INFINITY;
-        ix[r] = key[r] ? (int32_t)sel_key_index(key[r]) : 0x7fffffff;
-      }
+    for (int r = 0; r < 2; ++r) {
+      v[r] = key[half][r] ? sel_key_score(key[half][r]) : -INFINITY;
+      ix[r] = key[half][r] ? (int32_t)sel_key_index(key[half][r]) : 0x7fffffff;
     }
     if (half == 0) {
 #pragma unroll
@@ -406,7 +452,15 @@ __global__ void __launch_bounds__(256) cartesian_gather_lookup_kernel(
   if (l < L) {
     cartesian_lookup<32, MAXC, MSN_FUSED_TAU_STEPS, SEG>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, s_idx[wid], s_w[wid], 0, SC);
     float p[VPL][PER];
+#ifndef MSN_LK_NOGATHER
     gather_rows<VT, VPL, G, U, true>(s_idx[wid], s_w[wid], 0, k, V, d_v, p);  // (MASK = false measured slower here: C5 +4 us)
+#else
+    // (experiment builds only: the Cartesian stage alone)
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int e = 0; e < PER; ++e) p[v][e] = s_w[wid][0];
+#endif
     const int g = lane / LG, gl = lane % LG;
     const int row_vecs = d_v / PER;
     if (g == 0) {
@@ -602,11 +656,11 @@ bool cartesian_gather_lookup_ok(const Shape& s) {
 
 cudaError_t launch_cartesian_gather_lookup(const Shape& s, const Cands& cd, int32_t* idx, float* w, const void* V,
                                           float* out, cudaStream_t st, int* launches) {
-  if (!cartesian_gather_lookup_ok(s) || cd.S > 2) return cudaErrorNotSupported;
+  if (!cartesian_gather_lookup_ok(s) || cd.S != cd.SC) return cudaErrorNotSupported;
   if (s.B == 0) return cudaSuccess;
   const bool bf = s.v_dt != F32;
   cudaError_t e;
-  if (cd.S == 2)
+  if (cd.S > 1)
     e = bf ? dispatch_lookup<2, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, out, st)
            : dispatch_lookup<2, float>(s, cd, idx, w, (const float*)V, out, st);
   else
@@ -622,7 +676,7 @@ cudaError_t launch_cartesian_route(const Shape& s, const Cands& cd, int32_t* idx
   if (s.B == 0) return cudaSuccess;
   const bool bf = s.v_dt != F32;
   cudaError_t e;
-  if (s.k <= 32 && cd.S == 2)
+  if (s.k <= 32 && cd.S > 1 && cd.S == cd.SC)
     e = bf ? dispatch_route<32, 119, 2, __nv_bfloat16>(s, cd, idx, w, (const __nv_bfloat16*)V, ra, st)
            : dispatch_route<32, 119, 2, float>(s, cd, idx, w, (const float*)V, ra, st);
   else if (cd.S != 1)
@@ -641,7 +695,7 @@ cudaError_t launch_cartesian(const Shape& s, const Cands& cd, int32_t* idx, floa
                              cudaStream_t st, int* launches) {
   const int64_t L = s.B * s.H;
   const unsigned blocks = (unsigned)((L + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  if (s.k <= 32 && cd.S == 2)
+  if (s.k <= 32 && cd.S > 1 && cd.S == cd.SC)
     launch_pdl(cartesian_kernel<32, 119, 2>, blocks, 256, 0, st, cd.vc, cd.n, L, s.n_sub, s.k, idx, w,
                s.H, s.H / s.og, (int32_t)s.tab_stride, cd.SC);
   else if (cd.S != 1)

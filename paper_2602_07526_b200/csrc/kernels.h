@@ -56,10 +56,12 @@ struct Cands {
 // scorer).  Returns cudaErrorNotSupported when the shape is not handled.
 // fp32 inputs run 3xTF32 (kind::tf32); ws holds the split sub-keys
 // (select_tc_workspace_bytes).
-// Column segments of a scorer row: 2 when a bf16 row of 512 < n_sub <= 1024
-// would otherwise need two MMA sweeps and the grid is small (<= 74 CTAs:
-// latency regime, e.g. C5), else 1.  for_workspace: the layout's SC, which
-// does not depend on B.
+// Column segments of a scorer row (bf16, k <= 32, n_sub <= 1024): the largest
+// S in {4, 2} with n_sub / S >= 256 columns (a multiple of the N tile) whose
+// S x (the unsplit grid) still fits one wave of CTAs (the latency regime,
+// e.g. C5: 32 CTAs -> S = 4), else 1.  MSN_SELECT_SPLIT=S forces it (A/B,
+// tests).  The workspace layout uses the same S (SC == S).
+constexpr int kMaxSeg = 4;
 int select_segments(const Shape& s, bool for_workspace);
 int select_cap(const Shape& s);  // candidate list capacity (64, or 128 for k > 32)
 // qhat (f2, may be null): LayerNorm each query half-vector on load (no affine,

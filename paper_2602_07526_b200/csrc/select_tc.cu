@@ -35,10 +35,11 @@
 // is rescored exactly by its write-out warp (warp_sort.cuh, exact_half_topk)
 // -- correctness never depends on the bound being tight.
 //
-// Small grids of bf16 rows with 512 < n_sub <= 1024 (C5: 32 CTAs) split every
-// row over S = 2 CTAs (blockIdx.z = column segment of n_sub / 2 columns, each
-// resident and scored once); each CTA writes the list of its own columns
-// (a superset of that segment's top-KT), the Cartesian stage merges the two.
+// Small grids of bf16 rows with n_sub <= 1024 split every row over S = 2 or 4
+// CTAs (select_segments; C5: 32 -> 128 CTAs, S = 4; blockIdx.z = column
+// segment of n_sub / S >= 256 columns, each resident and scored once): each
+// CTA writes the list of its own columns (a superset of that segment's
+// top-KT), the Cartesian stage merges the S lists.
 // Rows that fit TMEM (n_sub <= 512, two buffers) are scored once; longer rows
 // are scored twice (the MMA pass is cheap next to the epilogue): the first
 // pass feeds pass A, the second pass B, so tau is the whole row's bound.
@@ -96,6 +97,46 @@ __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
 }
 
+// Thread-block cluster (the column segments of one row tile): a full cluster
+// barrier (every thread of every CTA; release / acquire orders the shared
+// stores before the peers' DSMEM loads), the rank, and a peer's copy of a
+// shared address.
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ float ld_peer_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// Sorts a bitonic sequence of N values descending (the merge half of a
+// bitonic sort).
+template <int N>
+__device__ __forceinline__ void bitonic_merge_desc(float (&v)[N]) {
+#pragma unroll
+  for (int stride = N >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int j = i ^ stride;
+      if (j > i) {
+        const float hi = fmaxf(v[i], v[j]), lo = fminf(v[i], v[j]);
+        v[i] = hi;
+        v[j] = lo;
+      }
+    }
+}
+
 // MSN_SELECT_TS builds (profiling only): globaltimer stamps per CTA at the
 // epilogue's phase boundaries (warp 4, lane 0), summarised by tools/select_ts.py.
 #ifdef MSN_SELECT_TS
@@ -104,7 +145,7 @@ __device__ unsigned long long g_sel_ts[65536 * 16];
   do {                                                                              \
     unsigned long long t_;                                                          \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
-    const int c_ = blockIdx.y * gridDim.x + blockIdx.x;                             \
+    const int c_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;                             \
     if (c_ < 65536) g_sel_ts[c_ * 16 + (i)] = t_;                                   \
   } while (0)
 #define SEL_TS(i)                                                                   \
@@ -280,6 +321,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit(&tfull[buf]);
       }
     }
+  }
+  if (SEG && warp < kEpiWarp0) {
+    // (the epilogue's tau exchange rounds: every thread of the cluster arrives)
+    for (int bit = 1; bit < (int)gridDim.z; bit <<= 1) cluster_sync();
   } else if (warp >= kEpiWarp0) {
     // ---------------------------------------------------------- epilogue
     const int ew = warp - kEpiWarp0;   // 0..7
@@ -491,8 +536,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < KT; ++i) xch[(i * 2 + sh) * 128 + row] = gm[i];
     epi_bar();
     float tau = INFINITY;
+    if constexpr (SEG) {
+      // column segments (a cluster of S = gridDim.z CTAs along z): tau of the
+      // WHOLE row, so that each segment lists only its columns >= the row's
+      // bound (~1.2 KT candidates per row over all S lists, not per list).
+      // c = this CTA's top-KT group maxima (half-cleaner, then sorted); a
+      // butterfly over the cluster: round r meets peer rank ^ 2^r, whose
+      // sorted top-KT c' gives max(c_i, c'_{KT-1-i}) = the top-KT of both
+      // (bitonic, re-sorted).  After log2 S rounds every CTA of the row
+      // holds the same top-KT of all 2S G group maxima (disjoint column
+      // groups): its minimum is a lower bound on the row's KT-th score.
+      // The exchange buffers live in the B ring (every MMA has completed:
+      // the chunks were waited on above); both threads of a row compute the
+      // same lists, thread 0 publishes them.
+      float c[KT];
 #pragma unroll
-    for (int i = 0; i < KT; ++i) tau = fminf(tau, fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]));
+      for (int i = 0; i < KT; ++i) c[i] = fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]);
+      bitonic_merge_desc<KT>(c);
+      float* xg = reinterpret_cast<float*>(sB);  // [rounds][KT][128]
+      const uint32_t rank = cluster_rank();
+      for (int bit = 1, r = 0; bit < (int)gridDim.z; bit <<= 1, ++r) {
+        float* buf = xg + r * KT * 128;
+        if (sh == 0) {
+#pragma unroll
+          for (int i = 0; i < KT; ++i) buf[i * 128 + row] = c[i];
+        }
+        cluster_sync();
+        const uint32_t pa = peer_addr(smem_u32(buf + row), rank ^ (uint32_t)bit);
+        float pv[KT];
+#pragma unroll
+        for (int i = 0; i < KT; ++i) pv[i] = ld_peer_f32(pa + (uint32_t)(i * 128 * 4));
+#pragma unroll
+        for (int i = 0; i < KT; ++i) c[i] = fmaxf(c[i], pv[KT - 1 - i]);
+        bitonic_merge_desc<KT>(c);
+      }
+      tau = c[KT - 1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < KT; ++i) tau = fminf(tau, fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]));
+    }
     if constexpr (TF32 && WIDE) {
       // ||q||^2 summed in fp32 (relative error < 2^-17 for d_h <= 128): x 1.001
       // makes sqrt an upper bound; the margin itself has 2x slack (2^-8 vs 2^-9)
@@ -644,6 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   SEL_TS(6);
+  if constexpr (SEG) cluster_sync();  // no CTA leaves while a peer may read its shared memory
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -713,8 +796,58 @@ cudaError_t launch_ktws(const Shape& s, const CUtensorMap& mq, const CUtensorMap
   // x = head/half (fastest): concurrently resident CTAs spread over all 2H
   // sub-key codebooks instead of hammering one codebook's lines in L2
   dim3 grid(s.H * 2, (unsigned)((s.B + 127) / 128), (unsigned)(s.n_sub / p.seg_cols));
+  if constexpr (SEG) {
+    // the S column segments of a row tile form one cluster (the tau exchange)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = grid.z;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    static const bool no_pdl = getenv("MSN_NO_PDL") != nullptr;
+    cfg.numAttrs = no_pdl ? 1 : 2;
+    return cudaLaunchKernelEx(&cfg, select_tc_kernel<KT, TF32, WIDE, SEG>, mq, mk, mklo, p);
+  }
   launch_pdl(select_tc_kernel<KT, TF32, WIDE, SEG>, grid, kThreads, sm, st, mq, mk, mklo, p);
   return cudaGetLastError();
+}
+
+// How many clusters of S segment CTAs (smem bytes each) the device holds at
+// once (cached per device and S; 0 when cluster launches are unavailable).
+template <int KT>
+int seg_clusters(int S, size_t smem) {
+  static std::atomic<int> cache[64][3];  // [device][log2 S - 1], value + 1
+  const int d = current_device();
+  const int li = S == 2 ? 0 : S == 4 ? 1 : 2;
+  if (d >= 0 && d < 64 && cache[d][li].load() > 0) return cache[d][li].load() - 1;
+  static std::atomic<uint64_t> attr_done{0};
+  int n = 0;
+  if (smem_attr_once(attr_done, select_tc_kernel<KT, false, false, true>, 227 * 1024) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 1, S);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = S;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, select_tc_kernel<KT, false, false, true>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+  }
+  if (d >= 0 && d < 64) cache[d][li].store(n + 1);
+  return n;
 }
 template <int KT, bool TF32, bool WIDE>
 cudaError_t launch_ktw(const Shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
@@ -745,14 +878,27 @@ extern "C" int msn_select_ts_dump(unsigned long long* host, int n) {
 int select_cap(const Shape& s) { return cand_cap(kt_of(s.k)); }
 
 int select_segments(const Shape& s, bool for_workspace) {
-  if (is_tf32(s) || !select_tc_supported(s) || s.k > 32) return 1;
+  (void)for_workspace;  // (the layout uses the same S: every call checks its own workspace size)
+  if (is_tf32(s) || !select_tc_supported(s) || s.k > 32 || s.n_sub > 1024) return 1;
   const int nt = n_tile_for(s);
-  if (s.n_sub <= 512 || s.n_sub > 1024 || (s.n_sub / 2) % nt != 0) return 1;
-  if (for_workspace) return 2;
+  // S segments of >= 256 columns (one full N chunk at least), each resident in TMEM
+  auto ok = [&](int S) {
+    return s.n_sub % S == 0 && s.n_sub / S >= 256 && (s.n_sub / S) % nt == 0 &&
+           kStages * nt * kRowBytes >= (S == 4 ? 2 : 1) * kt_of(s.k) * 128 * 4;  // tau exchange in the B ring
+  };
   static const int mode = getenv("MSN_SELECT_SPLIT") ? atoi(getenv("MSN_SELECT_SPLIT")) : -1;
-  if (mode >= 0) return mode ? 2 : 1;
+  if (mode >= 0) return mode > 1 && ok(mode) ? mode : 1;  // (A/B and tests: force S)
+  // the latency regime: as many segments as keep the grid within one wave
+  // (and as many clusters of S CTAs as row tiles must be resident together)
   const int64_t ctas = (s.B + 127) / 128 * s.H * 2;
-  return ctas <= 74 ? 2 : 1;
+  const int kt = kt_of(s.k);
+  for (int S = kMaxSeg; S >= 2; S /= 2) {
+    if (!ok(S) || ctas * S > device_sms()) continue;
+    const size_t sm = smem_bytes(s);
+    const int fit = kt == 8 ? seg_clusters<8>(S, sm) : kt == 16 ? seg_clusters<16>(S, sm) : seg_clusters<32>(S, sm);
+    if (ctas <= fit) return S;
+  }
+  return 1;
 }
 
 size_t select_tc_workspace_bytes(const Shape& s) {

@@ -109,45 +109,62 @@ __device__ __forceinline__ void warp_sort_u64(uint64_t (&x)[R]) {
 // 32-sequence, the half-cleaner max(A_i, B_{31-i}) keeps the top 32 of A u B
 // as a bitonic sequence, and a 5-step bitonic merge sorts it -- 36 shuffle
 // compare-exchange steps instead of the 41 of a full 64-sort.
-__device__ __forceinline__ void warp_top32_of_64(uint64_t (&x)[2]) {
+template <int N>
+__device__ __forceinline__ void warp_top32_of_64_n(uint64_t (&x)[N][2]) {
+  // N independent sets, their steps interleaved (N shuffle chains in flight)
   const int lane = threadIdx.x % 32;
 #pragma unroll
   for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint64_t o = shfl_xor_u64(x[r], stride);
-        const bool lower = (lane & stride) == 0;
-        const bool desc = size == 32 || (lane & size) == 0;  // (a 32-sequence ends descending)
-        x[r] = (lower == desc) == (o > x[r]) ? o : x[r];
-      }
+      for (int n = 0; n < N; ++n)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const uint64_t o = shfl_xor_u64(x[n][r], stride);
+          const bool lower = (lane & stride) == 0;
+          const bool desc = size == 32 || (lane & size) == 0;  // (a 32-sequence ends descending)
+          x[n][r] = (lower == desc) == (o > x[n][r]) ? o : x[n][r];
+        }
     }
   }
-  const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)x[1], 31 - lane);
-  const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(x[1] >> 32), 31 - lane);
-  const uint64_t b = ((uint64_t)bhi << 32) | blo;
-  uint64_t c = x[0] > b ? x[0] : b;
+  uint64_t c[N];
 #pragma unroll
-  for (int stride = 16; stride > 0; stride >>= 1) {
-    const uint64_t o = shfl_xor_u64(c, stride);
-    c = ((lane & stride) == 0) == (o > c) ? o : c;
+  for (int n = 0; n < N; ++n) {
+    const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)x[n][1], 31 - lane);
+    const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(x[n][1] >> 32), 31 - lane);
+    const uint64_t b = ((uint64_t)bhi << 32) | blo;
+    c[n] = x[n][0] > b ? x[n][0] : b;
   }
-  x[0] = c;
-  x[1] = 0ull;
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1)
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const uint64_t o = shfl_xor_u64(c[n], stride);
+      c[n] = ((lane & stride) == 0) == (o > c[n]) ? o : c[n];
+    }
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    x[n][0] = c[n];
+    x[n][1] = 0ull;
+  }
+}
+__device__ __forceinline__ void warp_top32_of_64(uint64_t (&x)[2]) {
+  uint64_t (&y)[1][2] = *reinterpret_cast<uint64_t (*)[1][2]>(&x);
+  warp_top32_of_64_n<1>(y);
 }
 
 // The 32 largest of 128 u64 keys (four registers), sorted descending in x[0]:
-// the top 32 of each pair, then the half-cleaner of the two and a merge.
+// the top 32 of each pair (interleaved), then the half-cleaner of the two and
+// a merge.
 __device__ __forceinline__ void warp_top32_of_128(uint64_t (&x)[4]) {
   const int lane = threadIdx.x % 32;
-  uint64_t a[2] = {x[0], x[1]}, b[2] = {x[2], x[3]};
-  warp_top32_of_64(a);
-  warp_top32_of_64(b);
-  const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)b[0], 31 - lane);
-  const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(b[0] >> 32), 31 - lane);
+  uint64_t ab[2][2] = {{x[0], x[1]}, {x[2], x[3]}};
+  warp_top32_of_64_n<2>(ab);
+  const uint32_t blo = __shfl_sync(0xffffffffu, (uint32_t)ab[1][0], 31 - lane);
+  const uint32_t bhi = __shfl_sync(0xffffffffu, (uint32_t)(ab[1][0] >> 32), 31 - lane);
   const uint64_t br = ((uint64_t)bhi << 32) | blo;
-  uint64_t c = a[0] > br ? a[0] : br;
+  uint64_t c = ab[0][0] > br ? ab[0][0] : br;
 #pragma unroll
   for (int stride = 16; stride > 0; stride >>= 1) {
     const uint64_t o = shfl_xor_u64(c, stride);

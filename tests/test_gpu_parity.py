@@ -770,24 +770,30 @@ torch.save({"out": out.cpu(), "idx": idx.cpu(), "w": w.cpu()}, sys.argv[4])
 """
 
 
-@pytest.mark.parametrize("name,B", [("c5_latency_bf16", 512), ("c5_latency_bf16", 130)])
+@pytest.mark.parametrize("name,B", [("c5_latency_bf16", 512), ("c5_latency_bf16", 130),
+                                    ("c5_latency_bf16", 1000), ("c2_mid_bf16", 300)])
 def test_select_column_split_matches_unsplit(name, B, tmp_path):
-    """Scorer rows split over two CTAs (MSN_SELECT_SPLIT=1, the default for
-    small grids) and scored by one CTA in two sweeps (=0) select the same
-    slots: idx, w and out bitwise equal (separate processes: the switch is
-    read once per process)."""
+    """Scorer rows split over S = 2 or 4 CTAs (MSN_SELECT_SPLIT=S; the default
+    for small grids picks the largest S that fits one wave) and scored by one
+    CTA (=0: two sweeps for n_sub > 512) select the same slots: idx, w and
+    out bitwise equal (separate processes: the switch is read once per
+    process)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for mode in ("0", "1"):
+    for mode in ("0", "2", "4", None):
         f = str(tmp_path / f"r{mode}.pt")
-        env = dict(os.environ, MSN_SELECT_SPLIT=mode)
+        env = dict(os.environ)
+        env.pop("MSN_SELECT_SPLIT", None)
+        if mode is not None:
+            env["MSN_SELECT_SPLIT"] = mode
         subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT, root, name, str(B), f], env=env, check=True,
                        timeout=600)
         res[mode] = torch.load(f)
-    for key in ("idx", "w", "out"):
-        assert torch.equal(res["0"][key], res["1"][key]), key
+    for mode in ("2", "4", None):
+        for key in ("idx", "w", "out"):
+            assert torch.equal(res["0"][key], res[mode][key]), (mode, key)
 
 
 @pytest.mark.parametrize("name,B,groups", [("c2_mid_bf16", 8192 + 37, 1), ("c3_train_fp32_zipf", 8192 + 5, 1),

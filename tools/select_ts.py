@@ -23,12 +23,14 @@ lk = PKMLookup(cfg.heads, cfg.n_sub, cfg.d_half, cfg.d_value, cfg.k, cfg.batch, 
 for _ in range(3):
     lk.select(Q, K)
 torch.cuda.synchronize()
-ncta = cfg.heads * 2 * ((cfg.batch + 127) // 128)
+ncta = cfg.heads * 2 * ((cfg.batch + 127) // 128) * 4  # (up to 4 column segments)
 buf = (ctypes.c_ulonglong * (ncta * 16))()
 lib = _lib.load()
 lib.msn_select_ts_dump.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert lib.msn_select_ts_dump(buf, ncta) == ncta
 t = np.frombuffer(buf, dtype=np.uint64).reshape(ncta, 16).astype(np.float64)
+t = t[t[:, 0] > 0]  # the CTAs that ran
+ncta = len(t)
 t0 = t[:, 0]
 names = ["start", "chunks ready", "pass A done", "tau done", "pass B done", "all rows done", "write-out done"]
 print(f"{name}: {ncta} CTAs, kernel span {(t[:, 6].max() - t0.min()) / 1e3:.1f} us")
