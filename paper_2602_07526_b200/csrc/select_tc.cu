@@ -114,10 +114,8 @@ __device__ __forceinline__ uint32_t peer_addr(uint32_t local, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local), "r"(rank));
   return a;
 }
-__device__ __forceinline__ float ld_peer_f32(uint32_t a) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
-  return v;
+__device__ __forceinline__ void st_peer_f32(uint32_t a, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
 
 // Sorts a bitonic sequence of N values descending (the merge half of a
@@ -323,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (SEG && warp < kEpiWarp0) {
-    // (the epilogue's tau exchange rounds: every thread of the cluster arrives)
-    for (int bit = 1; bit < (int)gridDim.z; bit <<= 1) cluster_sync();
+    // (the epilogue's tau exchange: every thread of the cluster arrives)
+    cluster_sync();
   } else if (warp >= kEpiWarp0) {
     // ---------------------------------------------------------- epilogue
     const int ew = warp - kEpiWarp0;   // 0..7
@@ -537,40 +535,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     epi_bar();
     float tau = INFINITY;
     if constexpr (SEG) {
-      // column segments (a cluster of S = gridDim.z CTAs along z): tau of the
-      // WHOLE row, so that each segment lists only its columns >= the row's
-      // bound (~1.2 KT candidates per row over all S lists, not per list).
-      // c = this CTA's top-KT group maxima (half-cleaner, then sorted); a
-      // butterfly over the cluster: round r meets peer rank ^ 2^r, whose
-      // sorted top-KT c' gives max(c_i, c'_{KT-1-i}) = the top-KT of both
-      // (bitonic, re-sorted).  After log2 S rounds every CTA of the row
-      // holds the same top-KT of all 2S G group maxima (disjoint column
-      // groups): its minimum is a lower bound on the row's KT-th score.
-      // The exchange buffers live in the B ring (every MMA has completed:
-      // the chunks were waited on above); both threads of a row compute the
-      // same lists, thread 0 publishes them.
-      float c[KT];
+      // column segments (a cluster of S = gridDim.z CTAs along z): a bound on
+      // the WHOLE row, so that each segment lists only its columns >= it
+      // (~1.2 KT candidates per row over all S lists, not per list).  Each
+      // CTA takes the sorted top-Q of its 2G group maxima (half-cleaner of
+      // the two threads' sorted lists + merge) and publishes NP = 16 / S of
+      // them, every T-th (T = KT / 8, Q = T NP): its j-th published value
+      // has >= T (j+1) of the CTA's maxima >= it.  So with the 16 published
+      // values of the cluster sorted, the 8th largest x has >= 8 T = KT
+      // group maxima >= x over the row, from disjoint column groups: x is a
+      // lower bound on the row's KT-th score.  One DSMEM round (one cluster
+      // barrier); both threads of a row compute the same list.
+      constexpr int T = KT / 8;
+      const int S = (int)gridDim.z;
+      float d[KT];  // the sorted top-Q, Q = KT (S = 2) or KT / 2 (S = 4)
+      if (S == 2) {
 #pragma unroll
-      for (int i = 0; i < KT; ++i) c[i] = fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]);
-      bitonic_merge_desc<KT>(c);
-      float* xg = reinterpret_cast<float*>(sB);  // [rounds][KT][128]
-      const uint32_t rank = cluster_rank();
-      for (int bit = 1, r = 0; bit < (int)gridDim.z; bit <<= 1, ++r) {
-        float* buf = xg + r * KT * 128;
-        if (sh == 0) {
+        for (int i = 0; i < KT; ++i) d[i] = fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]);
+        bitonic_merge_desc<KT>(d);
+      } else {
+        float e[KT / 2];
 #pragma unroll
-          for (int i = 0; i < KT; ++i) buf[i * 128 + row] = c[i];
-        }
-        cluster_sync();
-        const uint32_t pa = peer_addr(smem_u32(buf + row), rank ^ (uint32_t)bit);
-        float pv[KT];
+        for (int i = 0; i < KT / 2; ++i) e[i] = fmaxf(gm[i], xch[((KT / 2 - 1 - i) * 2 + (sh ^ 1)) * 128 + row]);
+        bitonic_merge_desc<KT / 2>(e);
 #pragma unroll
-        for (int i = 0; i < KT; ++i) pv[i] = ld_peer_f32(pa + (uint32_t)(i * 128 * 4));
-#pragma unroll
-        for (int i = 0; i < KT; ++i) c[i] = fmaxf(c[i], pv[KT - 1 - i]);
-        bitonic_merge_desc<KT>(c);
+        for (int i = 0; i < KT; ++i) d[i] = i < KT / 2 ? e[i] : -INFINITY;
       }
-      tau = c[KT - 1];
+      // pushed, not pulled: thread 0 of the row stores its NP values into
+      // slots [g NP, g NP + NP) of every cluster CTA's table (remote stores
+      // are fire-and-forget; the barrier's release makes them visible), and
+      // after the barrier every thread reads the 16 values locally.  The
+      // table sits in the candidate area past the local exchange (KT x 2 x
+      // 128 floats): peers write it only before the barrier, pass B
+      // overwrites it only after.
+      float* pub = xch + KT * 2 * 128;  // [16][128]
+      if (sh == 0) {
+        const int np = 16 / S, g = (int)blockIdx.z;
+        for (int r = 0; r < S; ++r) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < np) st_peer_f32(peer_addr(smem_u32(pub + (g * np + j) * 128 + row), (uint32_t)r), d[T * (j + 1) - 1]);
+        }
+      }
+      SEL_TS(7);
+      cluster_sync();
+      SEL_TS(8);
+      float pv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pv[i] = pub[i * 128 + row];
+      bitonic_sort_vals<16>(pv);
+      tau = pv[7];
+      SEL_TS(9);
     } else {
 #pragma unroll
       for (int i = 0; i < KT; ++i) tau = fminf(tau, fmaxf(gm[i], xch[((KT - 1 - i) * 2 + (sh ^ 1)) * 128 + row]));
@@ -687,6 +702,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r0 = ew * 16;
     const int cn_l = cnts[(lane >> 4) * 128 + r0 + (lane & 15)];
     bool any_ovf = false;
+    if constexpr (SEG) {
+      // column segments: a few entries per row (the whole row's bound), so
+      // each thread copies its own ones (thread 1's after thread 0's)
+      const int n0 = cnts[row], n1 = cnts[128 + row];
+      const int64_t b = m0 + row;
+      const int n = n0 + n1;
+      if (b < p.B && n <= CAP) {
+        const int64_t grow = b * p.H * 2 + hh;
+        uint2* dst = p.vc + (grow * p.SC + seg) * CAP + (sh ? n0 : 0);
+        if (sh == 0) p.cn[grow * p.SC + seg] = n;
+        const int mine = sh ? n1 : n0;
+        for (int i = 0; i < mine; ++i) dst[i] = cand[(sh ? CAP - 1 - i : i) * kCStride + row];
+      }
+      const int nr = __shfl_sync(0xffffffffu, cn_l, lane & 15) + __shfl_sync(0xffffffffu, cn_l, 16 + (lane & 15));
+      any_ovf = __any_sync(0xffffffffu, m0 + r0 + (lane & 15) < p.B && nr > CAP);
+    } else {
 #pragma unroll 4
     for (int rr = 0; rr < 16; ++rr) {
       const int trow = r0 + rr;
@@ -707,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    }
     if (any_ovf) {
       // more than CAP columns passed tau (massive exact ties): exact
       // rescoring of those rows by the warp, their best min(64, n_sub) sub-keys
@@ -726,7 +758,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   SEL_TS(6);
-  if constexpr (SEG) cluster_sync();  // no CTA leaves while a peer may read its shared memory
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -883,8 +914,7 @@ int select_segments(const Shape& s, bool for_workspace) {
   const int nt = n_tile_for(s);
   // S segments of >= 256 columns (one full N chunk at least), each resident in TMEM
   auto ok = [&](int S) {
-    return s.n_sub % S == 0 && s.n_sub / S >= 256 && (s.n_sub / S) % nt == 0 &&
-           kStages * nt * kRowBytes >= (S == 4 ? 2 : 1) * kt_of(s.k) * 128 * 4;  // tau exchange in the B ring
+    return s.n_sub % S == 0 && s.n_sub / S >= 256 && (s.n_sub / S) % nt == 0;
   };
   static const int mode = getenv("MSN_SELECT_SPLIT") ? atoi(getenv("MSN_SELECT_SPLIT")) : -1;
   if (mode >= 0) return mode > 1 && ok(mode) ? mode : 1;  // (A/B and tests: force S)

@@ -39,3 +39,6 @@ if [ -f paper_2602_07526_b200/libmsn_pkm_ts.so ]; then
     MSN_LIB=paper_2602_07526_b200/libmsn_pkm_ts.so timeout 200 python tools/select_ts.py $c >> $O/select_ts.txt 2>&1
   done
 fi
+# C5 warm phase times (20 calls per graph) and the column-segment A/B
+for m in 1 2 4; do MSN_SELECT_SPLIT=$m timeout 120 python tools/c5_phases.py >> $O/c5_phases.txt 2>&1; done
+timeout 120 python tools/c5_phases.py >> $O/c5_phases.txt 2>&1

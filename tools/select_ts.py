@@ -37,7 +37,10 @@ print(f"{name}: {ncta} CTAs, kernel span {(t[:, 6].max() - t0.min()) / 1e3:.1f} 
 for i in range(1, 7):
     d = t[:, i] - t0
     print(f"  {names[i]:16s} mean {d.mean() / 1e3:7.2f} us  p90 {np.percentile(d, 90) / 1e3:7.2f}")
-if (t[:, 7] > 0).all():
+if (t[:, 7] > 0).all() and not (t[:, 10] > 0).any():
+    print("  column segments: published at %.2f, cluster barrier passed %.2f, tau %.2f us" %
+          tuple((t[:, c] - t0).mean() / 1e3 for c in (7, 8, 9)))
+elif (t[:, 7] > 0).all():
     print("  two-sweep rows, first sweep: chunk ready at " +
           " ".join(f"{(t[:, 7 + c] - t0).mean() / 1e3:.2f}" for c in range(7)) + " us")
 print(f"  A tile loaded {(t[:, 14] - t0).mean() / 1e3:.2f} us, MMA start {(t[:, 15] - t0).mean() / 1e3:.2f} us")
