@@ -796,13 +796,18 @@ def test_select_column_split_matches_unsplit(name, B, tmp_path):
             assert torch.equal(res["0"][key], res[mode][key]), (mode, key)
 
 
-@pytest.mark.parametrize("name,B,groups", [("c2_mid_bf16", 8192 + 37, 1), ("c3_train_fp32_zipf", 8192 + 5, 1),
-                                           ("f4_tokens_bf16", 40, 16), ("c5_latency_bf16", 8192 + 3, 1)])
-def test_fused_forward_matches_phases(name, B, groups):
-    """msn_pkm_forward (fused Cartesian + gather for B >= 8192) and the phase
-    calls select + gather add in the same order (gather_rows.cuh): bitwise
-    equal idx, weights and outputs."""
-    cfg = wl.CONFIGS[name].scaled(batch=B)
+@pytest.mark.parametrize("name,B,groups,kw", [("c2_mid_bf16", 8192 + 37, 1, {}),
+                                              ("c3_train_fp32_zipf", 8192 + 5, 1, {}),
+                                              ("f4_tokens_bf16", 40, 16, {}), ("c5_latency_bf16", 8192 + 3, 1, {}),
+                                              ("c5_latency_bf16", 512, 1, {}), ("c5_latency_bf16", 130, 1, {}),
+                                              ("c5_latency_bf16", 61, 1, {"heads": 8}),
+                                              ("c3_train_fp32_zipf", 77, 1, {"d_value": 256})])
+def test_fused_forward_matches_phases(name, B, groups, kw):
+    """msn_pkm_forward (fused Cartesian + gather: per query for B >= 8192,
+    per lookup below -- the warp-specialised kernel for rows of 64 vectors)
+    and the phase calls select + gather add in the same order
+    (gather_rows.cuh): bitwise equal idx, weights and outputs."""
+    cfg = wl.CONFIGS[name].scaled(batch=B, **kw)
     Q, K, V, _ = wl.make_all(cfg, DEV)
     lk = lookup_for(cfg, head_groups=groups)
     out, idx, w = lk.forward(Q, K, V)
