@@ -434,6 +434,9 @@ __global__ void __launch_bounds__(256) cartesian_gather_kernel(
 // instead of 512), so a small batch fills the GPU.  k <= 32, d_v <= 512,
 // H | 8, one output group, no gate.
 constexpr int kLkMaxDv = 512;
+#ifndef MSN_LK_MASK
+#define MSN_LK_MASK true  // per-row index test in the per-lookup gather (A/B: false)
+#endif
 template <int MAXC, int SEG, typename VT, int VPL, int G, int U>
 __global__ void __launch_bounds__(256) cartesian_gather_lookup_kernel(
     const uint2* __restrict__ cand, const int32_t* __restrict__ cand_n, int64_t B, int H, int n_sub, int k,
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(256) cartesian_gather_lookup_kernel(
     cartesian_lookup<32, MAXC, MSN_FUSED_TAU_STEPS, SEG>(sm[wid], l, cand, cand_n, n_sub, k, idx, w, s_idx[wid], s_w[wid], 0, SC);
     float p[VPL][PER];
 #ifndef MSN_LK_NOGATHER
-    gather_rows<VT, VPL, G, U, true>(s_idx[wid], s_w[wid], 0, k, V, d_v, p);  // (MASK = false measured slower here: C5 +4 us)
+    gather_rows<VT, VPL, G, U, MSN_LK_MASK>(s_idx[wid], s_w[wid], 0, k, V, d_v, p);  // (MASK = false measured slower here in round 2 r02c: C5 +4 us)
 #else
     // (experiment builds only: the Cartesian stage alone)
 #pragma unroll
