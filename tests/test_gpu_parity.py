@@ -63,6 +63,9 @@ SWEEP = [
     (40, 1, 1024, 32, 64, 5, torch.float32, torch.float32),
     # value rows of 1024 (the paper's inferred width), bf16
     (70, 2, 128, 64, 1024, 16, torch.bfloat16, torch.bfloat16),
+    # small grids: scorer rows split over clusters of 4 (KT = 16, T = 2) and 2 CTAs (n_sub 512)
+    (45, 3, 1024, 128, 128, 16, torch.bfloat16, torch.bfloat16),
+    (129, 2, 512, 64, 64, 32, torch.bfloat16, torch.float32),
 ]
 
 
