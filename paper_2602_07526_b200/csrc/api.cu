@@ -98,7 +98,7 @@ msn_status check_select_shape(const Shape& s) {
 msn_status check_bwd_shape(msn_pkm_t h, bool values, bool keys) {
   if (backward_supported(shape_of(h->cfg, 0), values, keys)) return MSN_OK;
   return fail(MSN_ERR_UNSUPPORTED,
-              "backward needs d_value (%d) and d_half (%d) in 32 * {1, 2, 4, 8, 16} and k <= 64; "
+              "backward needs d_value (%d) in 32 * {1, 2, 4, 8, 16, 32}, d_half (%d) in 32 * {1, 2, 4, 8, 16} and k <= 64; "
               "nothing was launched", h->cfg.d_value, h->cfg.d_half);
 }
 
